@@ -1,0 +1,182 @@
+// HBM-bound best-effort / high-priority kernels, each in Original, Sliced and
+// PTB shape (tally_device.cuh):
+//
+//   vecadd_i64  out[i] = wrap64(a[i] + b[i]) over a flat int64 word image with
+//               the reference IR's three-region layout [a | b | out] and word
+//               offsets as arguments (ref ir/interp.py:195-196, tests/test_ir.py:165-172)
+//   vecadd_f32  c = a + b, 16 B vector loads/stores, streaming cache hints;
+//               one logical block = elems_per_block contiguous floats
+//   rowsum_f32  out[r] = sum_c in[r, c], one warp per row, fixed reduction
+//               order (bit-identical across shapes)
+#include <cstdio>
+
+#include "registry.h"
+
+namespace tally {
+
+// ---------------------------------------------------------------- vecadd_i64
+struct VecAddI64 {
+  static constexpr int kThreads = 256;
+  struct Params {
+    long long* mem;
+    long long a, b, out;   // word offsets into mem
+    long long n;           // elements
+    long long epb;         // elements per logical block
+  };
+  static __device__ __forceinline__ void run(const Params& p, uint3 bidx, uint3, char*) {
+    const long long base = (long long)bidx.x * p.epb;
+    for (long long i = threadIdx.x; i < p.epb; i += kThreads) {
+      const long long k = base + i;
+      if (k < p.n) {
+        const unsigned long long x = (unsigned long long)p.mem[p.a + k];
+        const unsigned long long y = (unsigned long long)p.mem[p.b + k];
+        p.mem[p.out + k] = (long long)(x + y);   // two's-complement wrap
+      }
+    }
+  }
+};
+
+static int bind_vecadd_i64(const tally_kernel_args* a, Instance* inst) {
+  VecAddI64::Params p{};
+  p.mem = static_cast<long long*>(a->ptr[0]);
+  p.a = a->i[0]; p.b = a->i[1]; p.out = a->i[2]; p.n = a->i[3];
+  p.epb = a->i[4] > 0 ? a->i[4] : 1;
+  if (!p.mem || p.n < 1) { set_error("vecadd_i64: need mem and n >= 1"); return TALLY_EINVAL; }
+  const long long blocks = (p.n + p.epb - 1) / p.epb;
+  if (blocks > 0x7fffffffLL) { set_error("vecadd_i64: grid too large"); return TALLY_EINVAL; }
+  memcpy(inst->params, &p, sizeof(p));
+  inst->grid = make_uint3((unsigned)blocks, 1, 1);
+  inst->threads = VecAddI64::kThreads;
+  inst->smem = 0;
+  inst->alg_bytes = 24.0 * (double)p.n;
+  return TALLY_OK;
+}
+
+// ---------------------------------------------------------------- vecadd_f32
+struct VecAddF32 {
+  static constexpr int kThreads = 256;
+  static constexpr int kVecPerThread = 4;            // 4 x float4 = 16 floats / thread
+  static constexpr int kElemsPerBlock = kThreads * kVecPerThread * 4;   // 4096
+  struct Params {
+    const float4* a;
+    const float4* b;
+    float4* c;
+    long long n4;          // number of float4
+  };
+  static __device__ __forceinline__ void run(const Params& p, uint3 bidx, uint3, char*) {
+    const long long base = (long long)bidx.x * (kThreads * kVecPerThread) + threadIdx.x;
+    float4 x[kVecPerThread], y[kVecPerThread];
+#pragma unroll
+    for (int j = 0; j < kVecPerThread; ++j) {
+      const long long k = base + (long long)j * kThreads;
+      if (k < p.n4) { x[j] = __ldcs(p.a + k); y[j] = __ldcs(p.b + k); }
+    }
+#pragma unroll
+    for (int j = 0; j < kVecPerThread; ++j) {
+      const long long k = base + (long long)j * kThreads;
+      if (k < p.n4)
+        __stcs(p.c + k, make_float4(x[j].x + y[j].x, x[j].y + y[j].y, x[j].z + y[j].z,
+                                    x[j].w + y[j].w));
+    }
+  }
+};
+
+static int bind_vecadd_f32(const tally_kernel_args* a, Instance* inst) {
+  VecAddF32::Params p{};
+  p.a = static_cast<const float4*>(a->ptr[0]);
+  p.b = static_cast<const float4*>(a->ptr[1]);
+  p.c = static_cast<float4*>(a->ptr[2]);
+  const long long n = a->i[0];
+  if (!p.a || !p.b || !p.c || n < 4 || n % 4) {
+    set_error("vecadd_f32: need a, b, c and n >= 4 with n %% 4 == 0");
+    return TALLY_EINVAL;
+  }
+  for (int k = 0; k < 3; ++k)
+    if (reinterpret_cast<uintptr_t>(a->ptr[k]) % 16) {
+      set_error("vecadd_f32: pointers must be 16-byte aligned");
+      return TALLY_EINVAL;
+    }
+  p.n4 = n / 4;
+  const long long blocks = (n + VecAddF32::kElemsPerBlock - 1) / VecAddF32::kElemsPerBlock;
+  memcpy(inst->params, &p, sizeof(p));
+  inst->grid = make_uint3((unsigned)blocks, 1, 1);
+  inst->threads = VecAddF32::kThreads;
+  inst->smem = 0;
+  inst->alg_bytes = 12.0 * (double)n;
+  inst->alg_flops = (double)n;
+  return TALLY_OK;
+}
+
+// ---------------------------------------------------------------- rowsum_f32
+struct RowSumF32 {
+  static constexpr int kThreads = 256;
+  static constexpr int kRowsPerBlock = kThreads / 32;
+  struct Params {
+    const float* in;
+    float* out;
+    long long rows;
+    long long cols;
+  };
+  static __device__ __forceinline__ void run(const Params& p, uint3 bidx, uint3, char*) {
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const long long r = (long long)bidx.x * kRowsPerBlock + warp;
+    if (r >= p.rows) return;   // no barrier in this body: warp-level exit is safe
+    const float* row = p.in + r * p.cols;
+    float acc = 0.f;
+    if ((p.cols & 3) == 0 && (reinterpret_cast<uintptr_t>(row) & 15) == 0) {
+      const float4* row4 = reinterpret_cast<const float4*>(row);
+      const long long c4 = p.cols >> 2;
+      for (long long c = lane; c < c4; c += 32) {
+        const float4 v = __ldcs(row4 + c);
+        acc += (v.x + v.y) + (v.z + v.w);
+      }
+    } else {
+      for (long long c = lane; c < p.cols; c += 32) acc += __ldcs(row + c);
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
+    if (lane == 0) p.out[r] = acc;
+  }
+};
+
+static int bind_rowsum_f32(const tally_kernel_args* a, Instance* inst) {
+  RowSumF32::Params p{};
+  p.in = static_cast<const float*>(a->ptr[0]);
+  p.out = static_cast<float*>(a->ptr[1]);
+  p.rows = a->i[0];
+  p.cols = a->i[1];
+  if (!p.in || !p.out || p.rows < 1 || p.cols < 1) {
+    set_error("rowsum_f32: need in, out, rows >= 1, cols >= 1");
+    return TALLY_EINVAL;
+  }
+  const long long blocks = (p.rows + RowSumF32::kRowsPerBlock - 1) / RowSumF32::kRowsPerBlock;
+  memcpy(inst->params, &p, sizeof(p));
+  inst->grid = make_uint3((unsigned)blocks, 1, 1);
+  inst->threads = RowSumF32::kThreads;
+  inst->smem = 0;
+  inst->alg_bytes = 4.0 * (double)p.rows * (double)p.cols + 4.0 * (double)p.rows;
+  inst->alg_flops = (double)p.rows * (double)p.cols;
+  return TALLY_OK;
+}
+
+template <class B>
+static KernelKind make_kind(const char* name, int (*bind)(const tally_kernel_args*, Instance*)) {
+  KernelKind k{};
+  k.name = name;
+  k.fn_original = reinterpret_cast<const void*>(&k_original<B>);
+  k.fn_sliced = reinterpret_cast<const void*>(&k_sliced<B>);
+  k.fn_ptb = reinterpret_cast<const void*>(&k_ptb<B>);
+  k.bind = bind;
+  k.setup = nullptr;
+  return k;
+}
+
+int register_basic_kernels(KernelKind* out, int cap) {
+  if (cap < 3) return 0;
+  out[0] = make_kind<VecAddI64>("vecadd_i64", bind_vecadd_i64);
+  out[1] = make_kind<VecAddF32>("vecadd_f32", bind_vecadd_f32);
+  out[2] = make_kind<RowSumF32>("rowsum_f32", bind_rowsum_f32);
+  return 3;
+}
+
+}  // namespace tally

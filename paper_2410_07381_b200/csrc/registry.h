@@ -1,0 +1,49 @@
+// Kernel-kind registry shared by the runtime and the kernel translation units.
+#pragma once
+#include <cuda_runtime.h>
+
+#include <cstddef>
+#include <cstdint>
+
+#include "../../include/tally_b200.h"
+#include "tally_device.cuh"
+
+namespace tally {
+
+constexpr int kMaxParamBytes = 512;
+
+// A bound kernel: the body's Params blob plus its logical geometry.
+struct Instance {
+  int kind = -1;
+  alignas(16) unsigned char params[kMaxParamBytes];
+  uint3 grid{1, 1, 1};         // logical grid
+  int threads = 0;             // CTA size
+  size_t smem = 0;             // dynamic shared memory per CTA
+  double alg_bytes = 0;        // algorithmic HBM bytes of the whole logical grid
+  double alg_flops = 0;        // algorithmic flops of the whole logical grid
+  unsigned long long total() const {
+    return (unsigned long long)grid.x * grid.y * grid.z;
+  }
+};
+
+// One hand-written kernel, three launch shapes (see tally_device.cuh).
+struct KernelKind {
+  const char* name;
+  const void* fn_original;
+  const void* fn_sliced;
+  const void* fn_ptb;
+  // Validate the generic argument block and fill inst (params, grid, threads,
+  // smem).  Returns TALLY_OK or a negative code with tally::set_error().
+  int (*bind)(const tally_kernel_args* a, Instance* inst);
+  // Optional one-time setup (e.g. smem attribute) -- may be null.
+  int (*setup)();
+};
+
+void set_error(const char* fmt, ...);
+int cuda_fail(cudaError_t e, const char* what);
+
+// Registration hooks implemented by each kernel translation unit.
+int register_basic_kernels(KernelKind* out, int cap);
+int register_gemm_kernels(KernelKind* out, int cap);
+
+}  // namespace tally

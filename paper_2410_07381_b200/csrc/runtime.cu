@@ -1,0 +1,607 @@
+// libtally_b200 runtime: device binding, kernel registry, per-priority
+// streams, launch shapes (Original / Sliced / PTB), preemption flags and
+// completion tracking.  Implements the first half of include/tally_b200.h;
+// the policy runner lives in runner.cpp / cuda_device.cpp.
+#include <cuda.h>
+#include <cuda_runtime.h>
+#include <time.h>
+
+#include <atomic>
+#include <cstdarg>
+#include <cstdio>
+#include <cstring>
+#include <memory>
+#include <mutex>
+#include <vector>
+
+#include "registry.h"
+#include "runtime.h"
+
+namespace tally {
+
+static thread_local char g_err[1024] = "";
+
+void set_error(const char* fmt, ...) {
+  va_list ap;
+  va_start(ap, fmt);
+  vsnprintf(g_err, sizeof(g_err), fmt, ap);
+  va_end(ap);
+}
+
+int cuda_fail(cudaError_t e, const char* what) {
+  set_error("%s: %s", what, cudaGetErrorString(e));
+  return TALLY_ECUDA;
+}
+
+long long host_now_ns() {
+  timespec ts;
+  clock_gettime(CLOCK_MONOTONIC, &ts);
+  return (long long)ts.tv_sec * 1000000000LL + ts.tv_nsec;
+}
+
+Runtime& rt() {
+  static Runtime r;
+  return r;
+}
+
+#define CK(call, what)                                  \
+  do {                                                  \
+    cudaError_t _e = (call);                            \
+    if (_e != cudaSuccess) return cuda_fail(_e, what);  \
+  } while (0)
+
+__global__ void k_stamp(unsigned long long* slot) {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  *reinterpret_cast<volatile unsigned long long*>(slot) = t;
+  __threadfence_system();
+}
+
+int Runtime::init(int dev, tally_gpu_info* out) {
+  std::lock_guard<std::mutex> g(mu);
+  if (inited) {
+    if (dev != device) { set_error("tally already bound to device %d", device); return TALLY_EINVAL; }
+    if (out) *out = info;
+    return TALLY_OK;
+  }
+  int n = 0;
+  cudaError_t e = cudaGetDeviceCount(&n);
+  if (e != cudaSuccess || n == 0) {
+    set_error("no CUDA device available (%s)", cudaGetErrorString(e));
+    return TALLY_ENODEV;
+  }
+  if (dev < 0 || dev >= n) { set_error("device %d out of range (%d devices)", dev, n); return TALLY_EINVAL; }
+  CK(cudaSetDevice(dev), "cudaSetDevice");
+  cudaDeviceProp p;
+  CK(cudaGetDeviceProperties(&p, dev), "cudaGetDeviceProperties");
+  if (p.major != 10) {
+    set_error("libtally_b200 is built for sm_100a; device %d is sm_%d%d", dev, p.major, p.minor);
+    return TALLY_ENODEV;
+  }
+  memset(&info, 0, sizeof(info));
+  info.device = dev;
+  info.num_sms = p.multiProcessorCount;
+  info.max_threads_per_sm = p.maxThreadsPerMultiProcessor;
+  info.max_blocks_per_sm = p.maxBlocksPerMultiProcessor;
+  info.cc_major = p.major;
+  info.cc_minor = p.minor;
+  info.smem_per_sm = (long long)p.sharedMemPerMultiprocessor;
+  info.hbm_bytes = (long long)p.totalGlobalMem;
+  snprintf(info.name, sizeof(info.name), "%s", p.name);
+  device = dev;
+
+  nkinds = register_basic_kernels(kinds, kMaxKinds);
+  nkinds += register_gemm_kernels(kinds + nkinds, kMaxKinds - nkinds);
+  for (int k = 0; k < nkinds; ++k)
+    if (kinds[k].setup) {
+      int rc = kinds[k].setup();
+      if (rc != TALLY_OK) return rc;
+    }
+
+  CK(cudaMalloc(&d_recs, sizeof(LaunchRec) * kMaxRecs), "cudaMalloc(launch records)");
+  CK(cudaMemset(d_recs, 0, sizeof(LaunchRec) * kMaxRecs), "cudaMemset(launch records)");
+  CK(cudaHostAlloc(&h_mirrors, sizeof(LaunchMirror) * kMaxRecs, cudaHostAllocMapped),
+     "cudaHostAlloc(mirrors)");
+  memset(h_mirrors, 0, sizeof(LaunchMirror) * kMaxRecs);
+  CK(cudaHostGetDevicePointer(&d_mirrors, h_mirrors, 0), "mirror device pointer");
+  CK(cudaHostAlloc(&h_flags, sizeof(unsigned) * kMaxRecs, cudaHostAllocMapped),
+     "cudaHostAlloc(flags)");
+  memset((void*)h_flags, 0, sizeof(unsigned) * kMaxRecs);
+  CK(cudaHostGetDevicePointer(&d_hflags, (void*)h_flags, 0), "flag device pointer");
+  CK(cudaHostAlloc(&h_stamp, 64, cudaHostAllocMapped), "cudaHostAlloc(stamp)");
+  CK(cudaHostGetDevicePointer(&d_stamp, (void*)h_stamp, 0), "stamp device pointer");
+  free_recs.clear();
+  for (int i = kMaxRecs - 1; i >= 0; --i) free_recs.push_back(i);
+
+  int lo = 0, hi = 0;
+  CK(cudaDeviceGetStreamPriorityRange(&lo, &hi), "stream priority range");
+  prio_low = lo;
+  prio_high = hi;
+  CK(cudaStreamCreateWithPriority(&sig_stream, cudaStreamNonBlocking, hi), "signal stream");
+
+  // driver stream memory operations: the flag write that preempts a PTB launch
+  cudaDriverEntryPointQueryResult q;
+  void* fn = nullptr;
+  if (cudaGetDriverEntryPoint("cuStreamWriteValue32", &fn, cudaEnableDefault, &q) == cudaSuccess &&
+      q == cudaDriverEntryPointSuccess && fn)
+    write32 = reinterpret_cast<WriteValue32Fn>(fn);
+  fn = nullptr;
+  if (cudaGetDriverEntryPoint("cuStreamWriteValue64", &fn, cudaEnableDefault, &q) == cudaSuccess &&
+      q == cudaDriverEntryPointSuccess && fn)
+    write64 = reinterpret_cast<WriteValue64Fn>(fn);
+  info.stream_mem_ops = 0;
+  if (write32) {
+    // probe on record 0's flag
+    CUresult r = write32((CUstream)sig_stream, (CUdeviceptr)&d_recs[0].flag, 0u, 0u);
+    if (r == CUDA_SUCCESS && cudaStreamSynchronize(sig_stream) == cudaSuccess) info.stream_mem_ops = 1;
+    cudaGetLastError();
+  }
+  flag_host = info.stream_mem_ops ? 0 : 1;
+  inited = true;
+  if (out) *out = info;
+  return TALLY_OK;
+}
+
+int Runtime::clock_offset(long long* off, long long* unc) {
+  if (!inited) { set_error("tally_init first"); return TALLY_EINVAL; }
+  long long best = 0, worst = 0;
+  bool have = false;
+  for (int i = 0; i < 24; ++i) {
+    *h_stamp = 0ull;
+    std::atomic_thread_fence(std::memory_order_seq_cst);
+    k_stamp<<<1, 1, 0, sig_stream>>>(d_stamp);
+    CK(cudaGetLastError(), "k_stamp launch");
+    long long seen = 0;
+    const long long deadline = host_now_ns() + 2000000000LL;
+    while (*h_stamp == 0ull) {
+      if (host_now_ns() > deadline) { set_error("clock calibration timed out"); return TALLY_ECUDA; }
+    }
+    seen = host_now_ns();
+    const long long s = seen - (long long)*h_stamp;
+    CK(cudaStreamSynchronize(sig_stream), "k_stamp sync");
+    if (i < 4) continue;   // warm-up
+    if (!have || s < best) best = s;
+    if (!have || s > worst) worst = s;
+    have = true;
+  }
+  if (off) *off = best;
+  if (unc) *unc = worst - best;
+  return TALLY_OK;
+}
+
+int Runtime::alloc_rec(int* out) {
+  if (free_recs.empty()) {
+    // reclaim records of launches whose kernel has fully exited
+    for (auto it = zombies.begin(); it != zombies.end();) {
+      if (cudaEventQuery(it->second) == cudaSuccess) {
+        free_recs.push_back(it->first);
+        release_event(it->second);
+        it = zombies.erase(it);
+      } else {
+        ++it;
+      }
+    }
+    cudaGetLastError();
+  }
+  if (free_recs.empty()) { set_error("out of PTB launch records"); return TALLY_EBUSY; }
+  *out = free_recs.back();
+  free_recs.pop_back();
+  return TALLY_OK;
+}
+
+cudaEvent_t Runtime::get_event(bool timed) {
+  auto& pool = timed ? timed_events : plain_events;
+  if (!pool.empty()) {
+    cudaEvent_t e = pool.back();
+    pool.pop_back();
+    return e;
+  }
+  cudaEvent_t e = nullptr;
+  cudaEventCreateWithFlags(&e, timed ? cudaEventDefault : cudaEventDisableTiming);
+  event_timed[e] = timed;
+  return e;
+}
+
+void Runtime::release_event(cudaEvent_t e) {
+  if (!e) return;
+  (event_timed[e] ? timed_events : plain_events).push_back(e);
+}
+
+int Runtime::launch(int kernel, int stream, const tally_launch_desc* d, int* out) {
+  if (!inited) { set_error("tally_init first"); return TALLY_EINVAL; }
+  if (!d || !out) { set_error("null descriptor"); return TALLY_EINVAL; }
+  if (kernel < 0 || kernel >= (int)instances.size() || !instances[kernel]) {
+    set_error("unknown kernel instance %d", kernel);
+    return TALLY_EINVAL;
+  }
+  if (stream < 0 || stream >= (int)streams.size() || !streams[stream]) {
+    set_error("unknown stream %d", stream);
+    return TALLY_EINVAL;
+  }
+  const Instance& in = *instances[kernel];
+  const KernelKind& kk = kinds[in.kind];
+  cudaStream_t st = streams[stream];
+  const unsigned long long total = in.total();
+
+  auto L = std::make_unique<Launch>();
+  L->kernel = kernel;
+  L->stream = stream;
+  L->shape = d->shape;
+  L->timed = d->timed != 0;
+  L->host_submit = host_now_ns();
+
+  SliceArgs s{};
+  s.grid = in.grid;
+  s.exec_count = d->exec_count;
+  PtbArgs pa{};
+  const void* fn = nullptr;
+  dim3 grid;
+  void* args[2] = {const_cast<unsigned char*>(in.params), nullptr};
+
+  switch (d->shape) {
+    case TALLY_SHAPE_ORIGINAL:
+      fn = kk.fn_original;
+      grid = dim3(in.grid.x, in.grid.y, in.grid.z);
+      args[1] = &s;
+      L->count = (long long)total;
+      break;
+    case TALLY_SHAPE_SLICED:
+      fn = kk.fn_sliced;
+      if (d->linear) {
+        if (d->linear_offset < 0 || d->count < 1 ||
+            (unsigned long long)(d->linear_offset + d->count) > total || d->count > 0x7fffffffLL) {
+          set_error("slice [%lld, +%lld) outside %llu logical blocks", d->linear_offset, d->count, total);
+          return TALLY_EINVAL;
+        }
+        s.linear = 1;
+        s.linear_offset = (unsigned long long)d->linear_offset;
+        grid = dim3((unsigned)d->count, 1, 1);
+        L->count = d->count;
+      } else {
+        if (d->sub_x < 1 || d->sub_y < 1 || d->sub_z < 1 || d->off_x + d->sub_x > in.grid.x ||
+            d->off_y + d->sub_y > in.grid.y || d->off_z + d->sub_z > in.grid.z) {
+          set_error("sub-grid outside the logical grid");
+          return TALLY_EINVAL;
+        }
+        s.offset = make_uint3(d->off_x, d->off_y, d->off_z);
+        grid = dim3(d->sub_x, d->sub_y, d->sub_z);
+        L->count = (long long)d->sub_x * d->sub_y * d->sub_z;
+      }
+      args[1] = &s;
+      break;
+    case TALLY_SHAPE_PTB: {
+      if (d->workers < 1) { set_error("worker count must be >= 1"); return TALLY_EINVAL; }
+      if (d->start_count < 0) { set_error("persisted counter must be >= 0"); return TALLY_EINVAL; }
+      int rec = -1;
+      int rc = alloc_rec(&rec);
+      if (rc != TALLY_OK) return rc;
+      unsigned ser = next_serial.fetch_add(1) + 1;
+      if (ser == 0) ser = next_serial.fetch_add(1) + 1;
+      L->rec = rec;
+      L->serial = ser;
+      L->start_count = d->start_count;
+      L->workers = d->workers;
+      h_mirrors[rec].serial = 0;
+      h_flags[rec] = 0;
+      std::atomic_thread_fence(std::memory_order_seq_cst);
+      pa.rec = d_recs + rec;
+      pa.flag_is_host = flag_host;
+      pa.flag = flag_host ? (d_hflags + rec) : &d_recs[rec].flag;
+      L->flag_host = flag_host;
+      pa.mirror = d_mirrors + rec;
+      pa.serial = ser;
+      pa.start = (unsigned long long)d->start_count;
+      pa.total = total;
+      pa.preempt_at = d->preempt_at;
+      pa.grid = in.grid;
+      pa.exec_count = d->exec_count;
+      fn = kk.fn_ptb;
+      grid = dim3((unsigned)d->workers, 1, 1);
+      args[1] = &pa;
+      L->count = (long long)total;
+      break;
+    }
+    default:
+      set_error("unknown launch shape %d", d->shape);
+      return TALLY_EINVAL;
+  }
+
+  if (L->timed) {
+    L->ev_start = get_event(true);
+    cudaEventRecord(L->ev_start, st);
+  }
+  cudaError_t e = cudaLaunchKernel(fn, grid, dim3(in.threads), args, in.smem, st);
+  if (e != cudaSuccess) {
+    if (L->rec >= 0) free_recs.push_back(L->rec);
+    release_event(L->ev_start);
+    return cuda_fail(e, kk.name);
+  }
+  L->ev_end = get_event(L->timed);
+  cudaEventRecord(L->ev_end, st);
+  L->active = true;
+
+  std::lock_guard<std::mutex> g(mu);
+  int id;
+  if (!free_launch_ids.empty()) {
+    id = free_launch_ids.back();
+    free_launch_ids.pop_back();
+    launches[id] = std::move(L);
+  } else {
+    id = (int)launches.size();
+    launches.push_back(std::move(L));
+  }
+  *out = id;
+  return TALLY_OK;
+}
+
+Launch* Runtime::get_launch(int id) {
+  if (id < 0 || id >= (int)launches.size() || !launches[id]) {
+    set_error("unknown launch %d", id);
+    return nullptr;
+  }
+  return launches[id].get();
+}
+
+// Update the cached state; returns true when the launch has finished.
+bool Runtime::poll(Launch* L) {
+  if (L->finished) return true;
+  if (L->shape == TALLY_SHAPE_PTB) {
+    volatile LaunchMirror* m = &h_mirrors[L->rec];
+    if (m->serial != L->serial) return false;
+    std::atomic_thread_fence(std::memory_order_acquire);
+    L->claims = (long long)m->claims;
+    L->gt_first_stop = (long long)m->t_first_stop;
+    L->gt_last_exit = (long long)m->t_last_exit;
+    L->gt_first_start = (long long)m->t_first_start;
+    L->parked = (m->status == kMirrorParked);
+    L->finished = true;
+    return true;
+  }
+  cudaError_t e = cudaEventQuery(L->ev_end);
+  if (e == cudaSuccess) {
+    L->finished = true;
+    return true;
+  }
+  if (e != cudaErrorNotReady) L->error = e;
+  return false;
+}
+
+void Runtime::fill_state(const Launch* L, tally_launch_state* o) {
+  memset(o, 0, sizeof(*o));
+  o->done = L->finished && !L->parked;
+  o->parked = L->parked;
+  o->preempted = L->preempted.load();
+  o->claims = L->claims;
+  o->task_counter = L->shape == TALLY_SHAPE_PTB ? L->start_count + L->claims : 0;
+  o->gt_first_start = L->gt_first_start;
+  o->gt_first_stop = L->gt_first_stop;
+  o->gt_last_exit = L->gt_last_exit;
+  o->host_submit_ns = L->host_submit;
+  o->host_preempt_ns = L->host_preempt;
+}
+
+int Runtime::preempt(int id) {
+  std::lock_guard<std::mutex> g(mu);
+  Launch* L = get_launch(id);
+  if (!L) return TALLY_EINVAL;
+  if (L->shape != TALLY_SHAPE_PTB) { set_error("launch %d: not a Ptb launch", id); return TALLY_EINVAL; }
+  if (L->finished) { set_error("launch %d: not in flight", id); return TALLY_EINVAL; }
+  bool expected = false;
+  if (!L->preempted.compare_exchange_strong(expected, true)) return TALLY_OK;
+  L->host_preempt = host_now_ns();
+  if (L->flag_host) {
+    reinterpret_cast<volatile unsigned*>(h_flags)[L->rec] = L->serial;
+    std::atomic_thread_fence(std::memory_order_seq_cst);
+    return TALLY_OK;
+  }
+  CUresult r = write32((CUstream)sig_stream, (CUdeviceptr)&d_recs[L->rec].flag, L->serial, 0u);
+  if (r != CUDA_SUCCESS) { set_error("cuStreamWriteValue32 failed (%d)", (int)r); return TALLY_ECUDA; }
+  return TALLY_OK;
+}
+
+int Runtime::release(int id) {
+  std::lock_guard<std::mutex> g(mu);
+  Launch* L = get_launch(id);
+  if (!L) return TALLY_EINVAL;
+  if (!L->finished && !poll(L)) { set_error("launch %d still in flight", id); return TALLY_EBUSY; }
+  if (L->rec >= 0) {
+    zombies.emplace_back(L->rec, L->ev_end);   // record reusable once the kernel fully exited
+    L->ev_end = nullptr;
+  }
+  release_event(L->ev_start);
+  release_event(L->ev_end);
+  launches[id].reset();
+  free_launch_ids.push_back(id);
+  return TALLY_OK;
+}
+
+}  // namespace tally
+
+using namespace tally;
+
+extern "C" {
+
+int tally_abi_version(void) { return TALLY_ABI_VERSION; }
+const char* tally_last_error(void) { return g_err; }
+long long tally_now_ns(void) { return host_now_ns(); }
+
+int tally_init(int device, tally_gpu_info* out) { return rt().init(device, out); }
+
+int tally_shutdown(void) {
+  Runtime& r = rt();
+  if (!r.inited) return TALLY_OK;
+  cudaDeviceSynchronize();
+  r.instances.clear();
+  for (auto s : r.streams)
+    if (s) cudaStreamDestroy(s);
+  r.streams.clear();
+  r.launches.clear();
+  r.free_launch_ids.clear();
+  r.zombies.clear();
+  return TALLY_OK;
+}
+
+int tally_clock_offset(long long* off, long long* unc) { return rt().clock_offset(off, unc); }
+
+int tally_set_flag_mode(int host_mapped) {
+  Runtime& r = rt();
+  if (!r.inited) { set_error("tally_init first"); return TALLY_EINVAL; }
+  if (!host_mapped && !r.info.stream_mem_ops) {
+    set_error("stream memory operations unavailable; only host-mapped flags");
+    return TALLY_EINVAL;
+  }
+  r.flag_host = host_mapped ? 1 : 0;
+  return TALLY_OK;
+}
+
+int tally_kernel_kind_count(void) {
+  Runtime& r = rt();
+  if (!r.inited) {
+    // registry is static; allow listing without a device
+    KernelKind tmp[Runtime::kMaxKinds];
+    int n = register_basic_kernels(tmp, Runtime::kMaxKinds);
+    return n + register_gemm_kernels(tmp + n, Runtime::kMaxKinds - n);
+  }
+  return r.nkinds;
+}
+
+const char* tally_kernel_kind_name(int kind) {
+  static KernelKind tmp[Runtime::kMaxKinds];
+  static int n = -1;
+  if (n < 0) {
+    n = register_basic_kernels(tmp, Runtime::kMaxKinds);
+    n += register_gemm_kernels(tmp + n, Runtime::kMaxKinds - n);
+  }
+  if (kind < 0 || kind >= n) return nullptr;
+  return tmp[kind].name;
+}
+
+int tally_kernel_create(const char* kind, const tally_kernel_args* args, int* out) {
+  Runtime& r = rt();
+  if (!r.inited) { set_error("tally_init first"); return TALLY_EINVAL; }
+  if (!kind || !args || !out) { set_error("null argument"); return TALLY_EINVAL; }
+  for (int k = 0; k < r.nkinds; ++k) {
+    if (strcmp(r.kinds[k].name, kind) != 0) continue;
+    auto in = std::make_unique<Instance>();
+    in->kind = k;
+    int rc = r.kinds[k].bind(args, in.get());
+    if (rc != TALLY_OK) return rc;
+    *out = (int)r.instances.size();
+    r.instances.push_back(std::move(in));
+    return TALLY_OK;
+  }
+  set_error("unknown kernel kind '%s'", kind);
+  return TALLY_EINVAL;
+}
+
+int tally_kernel_info_get(int kernel, tally_kernel_info* o) {
+  Runtime& r = rt();
+  if (kernel < 0 || kernel >= (int)r.instances.size() || !r.instances[kernel]) {
+    set_error("unknown kernel instance %d", kernel);
+    return TALLY_EINVAL;
+  }
+  const Instance& in = *r.instances[kernel];
+  const KernelKind& kk = r.kinds[in.kind];
+  memset(o, 0, sizeof(*o));
+  o->grid_x = in.grid.x;
+  o->grid_y = in.grid.y;
+  o->grid_z = in.grid.z;
+  o->total_blocks = (long long)in.total();
+  o->threads_per_block = in.threads;
+  o->smem_bytes = (long long)in.smem;
+  o->alg_bytes = in.alg_bytes;
+  o->alg_flops = in.alg_flops;
+  int occ = 0;
+  CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kk.fn_ptb, in.threads, in.smem), "occupancy");
+  o->occupancy_ptb = occ;
+  CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kk.fn_original, in.threads, in.smem), "occupancy");
+  o->occupancy_original = occ;
+  return TALLY_OK;
+}
+
+int tally_kernel_destroy(int kernel) {
+  Runtime& r = rt();
+  if (kernel < 0 || kernel >= (int)r.instances.size() || !r.instances[kernel]) {
+    set_error("unknown kernel instance %d", kernel);
+    return TALLY_EINVAL;
+  }
+  r.instances[kernel].reset();
+  return TALLY_OK;
+}
+
+int tally_stream_create(int prio, int* out) {
+  Runtime& r = rt();
+  if (!r.inited) { set_error("tally_init first"); return TALLY_EINVAL; }
+  if (prio != TALLY_HIGH && prio != TALLY_BEST_EFFORT) { set_error("unknown priority class %d", prio); return TALLY_EINVAL; }
+  cudaStream_t s;
+  CK(cudaStreamCreateWithPriority(&s, cudaStreamNonBlocking, prio == TALLY_HIGH ? r.prio_high : r.prio_low),
+     "cudaStreamCreateWithPriority");
+  *out = (int)r.streams.size();
+  r.streams.push_back(s);
+  return TALLY_OK;
+}
+
+int tally_stream_sync(int stream) {
+  Runtime& r = rt();
+  if (stream < 0 || stream >= (int)r.streams.size() || !r.streams[stream]) { set_error("unknown stream %d", stream); return TALLY_EINVAL; }
+  CK(cudaStreamSynchronize(r.streams[stream]), "cudaStreamSynchronize");
+  return TALLY_OK;
+}
+
+int tally_stream_destroy(int stream) {
+  Runtime& r = rt();
+  if (stream < 0 || stream >= (int)r.streams.size() || !r.streams[stream]) { set_error("unknown stream %d", stream); return TALLY_EINVAL; }
+  cudaStreamDestroy(r.streams[stream]);
+  r.streams[stream] = nullptr;
+  return TALLY_OK;
+}
+
+int tally_launch(int kernel, int stream, const tally_launch_desc* d, int* out) {
+  return rt().launch(kernel, stream, d, out);
+}
+
+int tally_launch_query(int id, tally_launch_state* o) {
+  Runtime& r = rt();
+  std::lock_guard<std::mutex> g(r.mu);
+  Launch* L = r.get_launch(id);
+  if (!L) return TALLY_EINVAL;
+  r.poll(L);
+  if (L->error != cudaSuccess) return cuda_fail(L->error, "launch");
+  if (o) r.fill_state(L, o);
+  return TALLY_OK;
+}
+
+int tally_launch_wait(int id, tally_launch_state* o) {
+  Runtime& r = rt();
+  Launch* L;
+  {
+    std::lock_guard<std::mutex> g(r.mu);
+    L = r.get_launch(id);
+    if (!L) return TALLY_EINVAL;
+  }
+  CK(cudaEventSynchronize(L->ev_end), "launch");
+  std::lock_guard<std::mutex> g(r.mu);
+  if (!r.poll(L)) {
+    set_error("launch %d: kernel exited without publishing its outcome", id);
+    return TALLY_ECUDA;
+  }
+  if (o) r.fill_state(L, o);
+  return TALLY_OK;
+}
+
+int tally_launch_elapsed_ns(int id, long long* out) {
+  Runtime& r = rt();
+  std::lock_guard<std::mutex> g(r.mu);
+  Launch* L = r.get_launch(id);
+  if (!L) return TALLY_EINVAL;
+  if (!L->timed) { set_error("launch %d was not timed", id); return TALLY_EINVAL; }
+  float ms = 0;
+  CK(cudaEventElapsedTime(&ms, L->ev_start, L->ev_end), "cudaEventElapsedTime");
+  *out = (long long)(ms * 1e6);
+  return TALLY_OK;
+}
+
+int tally_preempt(int id) { return rt().preempt(id); }
+int tally_launch_release(int id) { return rt().release(id); }
+
+}  // extern "C"

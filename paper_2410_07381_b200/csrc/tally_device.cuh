@@ -1,0 +1,209 @@
+// Device-side launch shapes for Tally's block-level scheduler on sm_100a.
+//
+// Every best-effort kernel is written once as a *body* -- a struct with
+//   static constexpr int kThreads;                 // CTA size (1-D)
+//   struct Params;                                 // POD launch arguments
+//   static __device__ void run(const Params&, uint3 bidx, uint3 grid, char* smem);
+// and instantiated in three launch shapes:
+//
+//   k_original<Body>  grid = logical grid, blockIdx used as is   (untransformed)
+//   k_sliced<Body>    grid = sub-grid, logical blockIdx = blockIdx + offset,
+//                     gridDim pinned to the logical grid        (ref transforms.py:92-133)
+//   k_ptb<Body>       grid = workers; each worker loops: leader checks the
+//                     preemption flag, and only if clear claims the next task
+//                     index with an L2 atomic, broadcasts it through shared
+//                     memory, barrier, delinearize(task, logical grid), body,
+//                     barrier                                    (ref transforms.py:291-401)
+//
+// Bodies must be "unified-synchronisation shaped" (ref transforms.py:200-288):
+// no thread leaves run() early past a __syncthreads -- the PTB loop's barriers
+// are then the only ones a finished logical block can meet.
+#pragma once
+#include <cstdint>
+#include <cuda_runtime.h>
+
+namespace tally {
+
+// --- per-launch device record (pool in device memory, zeroed at init) ------
+// A PTB launch owns one record for its lifetime; the last worker to exit
+// publishes the outcome to the host mirror and re-zeroes the record so it can
+// be reused without a host-side memset.
+struct alignas(64) LaunchRec {
+  unsigned long long claims;        // atomicAdd target: tasks claimed by this launch
+  unsigned int exited;              // workers that have left the loop
+  unsigned int flag;                // device-resident preemption flag (holds a serial)
+  unsigned long long t_first_stop;  // %globaltimer when the first worker saw the flag (0 = none)
+  unsigned long long t_last_exit;   // %globaltimer of the last worker exit
+  unsigned long long stops;         // workers that stopped because of the flag
+  unsigned long long pad[3];
+};
+
+// Host-visible outcome of a launch (pinned, mapped; written once by the last worker).
+struct alignas(64) LaunchMirror {
+  unsigned long long claims;
+  unsigned long long t_first_stop;
+  unsigned long long t_last_exit;
+  unsigned long long stops;
+  unsigned long long t_first_start;  // %globaltimer at first worker entry
+  unsigned int serial;               // written last: == launch serial when valid
+  unsigned int status;               // 1 = exhausted (done), 2 = parked
+  unsigned long long pad[2];
+};
+
+enum : unsigned { kMirrorDone = 1, kMirrorParked = 2 };
+
+// Shape arguments ------------------------------------------------------------
+struct SliceArgs {
+  uint3 offset;        // rectangular mode: logical block offset of this sub-launch
+  uint3 grid;          // logical (original) grid -- gridDim as the body sees it
+  unsigned long long linear_offset;  // linear mode: first task index of the slice
+  unsigned int linear;               // 1: 1-D sub-grid over task indices
+  unsigned long long* exec_count;  // optional exactly-once counters [total]
+};
+
+struct PtbArgs {
+  LaunchRec* rec;
+  const unsigned int* flag;        // where the preemption flag lives (device or mapped host)
+  LaunchMirror* mirror;            // mapped host outcome slot
+  unsigned int serial;             // this launch's identity; flag == serial means "park"
+  unsigned int flag_is_host;       // 1: flag is in mapped host memory (sys-scope loads)
+  unsigned long long start;        // persisted task counter to resume from
+  unsigned long long total;        // total logical blocks
+  long long preempt_at;            // test trigger: raise flag when counter reaches this (-1 off)
+  uint3 grid;                      // logical grid
+  unsigned long long* exec_count;  // optional exactly-once counters [total]
+};
+
+__device__ __forceinline__ unsigned long long globaltimer() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
+}
+
+__device__ __forceinline__ unsigned ld_acquire_gpu(const unsigned* p) {
+  unsigned v;
+  asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+__device__ __forceinline__ unsigned ld_acquire_sys(const unsigned* p) {
+  unsigned v;
+  asm volatile("ld.acquire.sys.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+__device__ __forceinline__ void st_release_sys(unsigned* p, unsigned v) {
+  asm volatile("st.release.sys.global.u32 [%0], %1;" :: "l"(p), "r"(v) : "memory");
+}
+
+__device__ __forceinline__ uint3 delinearize(unsigned long long t, uint3 g) {
+  // ref ir/core.py:59-65: x fastest
+  uint3 b;
+  b.x = (unsigned)(t % g.x);
+  unsigned long long q = t / g.x;
+  b.y = (unsigned)(q % g.y);
+  b.z = (unsigned)(q / g.y);
+  return b;
+}
+
+__device__ __forceinline__ unsigned long long linear_index(uint3 b, uint3 g) {
+  return (unsigned long long)b.x + (unsigned long long)g.x * (b.y + (unsigned long long)g.y * b.z);
+}
+
+// --- Original: the untransformed kernel --------------------------------------
+template <class Body>
+__global__ void __launch_bounds__(Body::kThreads)
+k_original(const typename Body::Params p, const SliceArgs s) {
+  extern __shared__ __align__(1024) char smem[];
+  const uint3 g = make_uint3(gridDim.x, gridDim.y, gridDim.z);
+  if (s.exec_count != nullptr && threadIdx.x == 0)
+    atomicAdd(&s.exec_count[linear_index(blockIdx, g)], 1ull);
+  Body::run(p, blockIdx, g, smem);
+}
+
+// --- Sliced: block offset + pinned gridDim ------------------------------------
+template <class Body>
+__global__ void __launch_bounds__(Body::kThreads)
+k_sliced(const typename Body::Params p, const SliceArgs s) {
+  extern __shared__ __align__(1024) char smem[];
+  const uint3 b = s.linear ? delinearize(s.linear_offset + blockIdx.x, s.grid)
+                           : make_uint3(blockIdx.x + s.offset.x, blockIdx.y + s.offset.y,
+                                        blockIdx.z + s.offset.z);
+  if (s.exec_count != nullptr && threadIdx.x == 0)
+    atomicAdd(&s.exec_count[linear_index(b, s.grid)], 1ull);
+  Body::run(p, b, s.grid, smem);
+}
+
+// --- PTB: persistent, preemptible workers -------------------------------------
+// Worker exit bookkeeping, run by thread 0 of every worker.
+__device__ __forceinline__ void ptb_worker_exit(const PtbArgs& a, bool stopped,
+                                                unsigned long long t_entry) {
+  const unsigned long long now = globaltimer();
+  LaunchRec* r = a.rec;
+  if (stopped) {
+    atomicAdd(&r->stops, 1ull);
+    // first observation of the flag: min over workers
+    unsigned long long prev = atomicCAS(&r->t_first_stop, 0ull, now);
+    if (prev != 0ull && now < prev) atomicMin(&r->t_first_stop, now);
+  }
+  atomicMax(&r->t_last_exit, now);
+  __threadfence();
+  const unsigned nworkers = gridDim.x * gridDim.y * gridDim.z;
+  if (atomicAdd(&r->exited, 1u) + 1u == nworkers) {
+    // last worker: publish and recycle the record
+    __threadfence();
+    const unsigned long long claims = atomicAdd(&r->claims, 0ull);
+    const unsigned long long progress = a.start + claims;
+    volatile LaunchMirror* m = a.mirror;
+    m->claims = claims;
+    m->t_first_stop = atomicAdd(&r->t_first_stop, 0ull);
+    m->t_last_exit = atomicAdd(&r->t_last_exit, 0ull);
+    m->stops = atomicAdd(&r->stops, 0ull);
+    m->t_first_start = t_entry;
+    // work can only remain if some worker stopped on the flag
+    m->status = (progress < a.total) ? kMirrorParked : kMirrorDone;
+    __threadfence_system();
+    m->serial = a.serial;
+    __threadfence_system();
+    r->claims = 0ull;
+    r->exited = 0u;
+    r->t_first_stop = 0ull;
+    r->t_last_exit = 0ull;
+    r->stops = 0ull;
+    __threadfence();
+  }
+}
+
+template <class Body>
+__global__ void __launch_bounds__(Body::kThreads)
+k_ptb(const typename Body::Params p, const PtbArgs a) {
+  extern __shared__ __align__(1024) char smem[];
+  __shared__ long long s_task;
+  const bool leader = (threadIdx.x == 0);
+  const unsigned long long t_entry = leader ? globaltimer() : 0ull;
+  bool stopped = false;
+  for (;;) {
+    if (leader) {
+      long long task = -1;
+      const unsigned f = a.flag_is_host ? ld_acquire_sys(a.flag) : ld_acquire_gpu(a.flag);
+      if (f != a.serial) {  // flag gates the claim: a parked launch never over-claims
+        const unsigned long long c = atomicAdd(&a.rec->claims, 1ull);
+        task = (long long)(a.start + c);
+        if (a.preempt_at >= 0 && task + 1 == a.preempt_at)
+          st_release_sys(const_cast<unsigned*>(a.flag), a.serial);   // test trigger
+        if (a.exec_count != nullptr && (unsigned long long)task < a.total)
+          atomicAdd(&a.exec_count[task], 1ull);
+      }
+      s_task = task;
+    }
+    __syncthreads();
+    const long long task = s_task;
+    if (task < 0 || (unsigned long long)task >= a.total) {
+      stopped = task < 0;
+      break;
+    }
+    Body::run(p, delinearize((unsigned long long)task, a.grid), a.grid, smem);
+    __syncthreads();
+  }
+  if (leader) ptb_worker_exit(a, stopped, t_entry);
+}
+
+}  // namespace tally

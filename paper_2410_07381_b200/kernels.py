@@ -1,0 +1,232 @@
+"""Registered device kernels and their three launch shapes.
+
+A :class:`DeviceKernel` is a built-in sm_100a kernel bound to device buffers
+(``tally_kernel_create``): it has a *logical grid* -- the untransformed launch
+-- and can be launched as
+
+* ``original()``                       the untransformed kernel,
+* ``sliced(offset, count)``            a contiguous range of logical blocks
+                                       (ref transforms.py:155-197),
+* ``ptb(workers, start_count, ...)``   persistent preemptible workers resuming
+                                       from a persisted task counter
+                                       (ref transforms.py:291-448).
+
+Buffers are torch tensors owned by the caller; the kernel keeps a reference
+for its lifetime.
+"""
+
+from __future__ import annotations
+
+import ctypes as C
+from dataclasses import dataclass
+
+from . import _lib
+from .device import B200Device, KernelCostModel, DEFAULT_LAUNCH_OVERHEAD_NS
+
+
+def _ptr(t):
+    if t is None:
+        return None
+    if hasattr(t, "data_ptr"):
+        if not t.is_cuda:
+            raise ValueError("device kernels need CUDA tensors")
+        if not t.is_contiguous():
+            raise ValueError("device kernels need contiguous tensors")
+        return t.data_ptr()
+    return int(t)
+
+
+class Stream:
+    """A CUDA stream at the greatest (HIGH) or least (BEST_EFFORT) priority."""
+
+    def __init__(self, high_priority: bool):
+        B200Device.get()
+        sid = C.c_int()
+        _lib.check(_lib.lib.tally_stream_create(_lib.HIGH_CLASS if high_priority
+                                                else _lib.BEST_EFFORT_CLASS, C.byref(sid)),
+                   "stream")
+        self.id = sid.value
+
+    def synchronize(self):
+        _lib.check(_lib.lib.tally_stream_sync(self.id), "stream sync")
+
+    def close(self):
+        if self.id >= 0:
+            _lib.lib.tally_stream_destroy(self.id)
+            self.id = -1
+
+
+@dataclass
+class LaunchState:
+    done: bool
+    parked: bool
+    preempted: bool
+    task_counter: int
+    claims: int
+    gt_first_start: int
+    gt_first_stop: int
+    gt_last_exit: int
+    host_submit_ns: int
+    host_preempt_ns: int
+
+
+def _state(s: _lib.c_launch_state) -> LaunchState:
+    return LaunchState(bool(s.done), bool(s.parked), bool(s.preempted), s.task_counter, s.claims,
+                       s.gt_first_start, s.gt_first_stop, s.gt_last_exit, s.host_submit_ns,
+                       s.host_preempt_ns)
+
+
+class Launch:
+    """One in-flight launch (a KernelHandle on the real device)."""
+
+    def __init__(self, lid: int, shape: int):
+        self.id = lid
+        self.shape = shape
+        self._final = None
+
+    def query(self) -> LaunchState:
+        if self._final is not None:
+            return self._final
+        s = _lib.c_launch_state()
+        _lib.check(_lib.lib.tally_launch_query(self.id, C.byref(s)), "launch query")
+        st = _state(s)
+        if st.done or st.parked:
+            self._finish(st)
+        return st
+
+    def wait(self) -> LaunchState:
+        if self._final is not None:
+            return self._final
+        s = _lib.c_launch_state()
+        _lib.check(_lib.lib.tally_launch_wait(self.id, C.byref(s)), "launch wait")
+        st = _state(s)
+        self._finish(st)
+        return st
+
+    def _finish(self, st):
+        self._final = st
+        self._elapsed = None
+        v = C.c_longlong()
+        if _lib.lib.tally_launch_elapsed_ns(self.id, C.byref(v)) == 0:
+            self._elapsed = v.value
+        _lib.lib.tally_launch_release(self.id)
+
+    @property
+    def elapsed_ns(self):
+        """Device time between the launch's bracketing events (timed launches)."""
+        if self._final is None:
+            self.wait()
+        return self._elapsed
+
+    def preempt(self):
+        _lib.check(_lib.lib.tally_preempt(self.id), "preempt")
+
+
+@dataclass(frozen=True)
+class KernelInfo:
+    grid: tuple
+    total_blocks: int
+    threads_per_block: int
+    smem_bytes: int
+    occupancy_ptb: int
+    occupancy_original: int
+    alg_bytes: float
+    alg_flops: float
+
+
+class DeviceKernel:
+    """A built-in kernel kind bound to arguments (``tally_kernel_create``)."""
+
+    def __init__(self, kind: str, ptrs=(), ints=(), floats=(), keep=()):
+        B200Device.get()
+        a = _lib.c_kernel_args()
+        for i, p in enumerate(ptrs):
+            a.ptr[i] = _ptr(p)
+        for i, v in enumerate(ints):
+            a.i[i] = int(v)
+        for i, v in enumerate(floats):
+            a.f[i] = float(v)
+        kid = C.c_int()
+        _lib.check(_lib.lib.tally_kernel_create(kind.encode(), C.byref(a), C.byref(kid)), kind)
+        self.kind = kind
+        self.id = kid.value
+        self._keep = tuple(keep) + tuple(p for p in ptrs if hasattr(p, "data_ptr"))
+        ki = _lib.c_kernel_info()
+        _lib.check(_lib.lib.tally_kernel_info_get(self.id, C.byref(ki)), "kernel info")
+        self.info = KernelInfo((ki.grid_x, ki.grid_y, ki.grid_z), ki.total_blocks,
+                               ki.threads_per_block, ki.smem_bytes, ki.occupancy_ptb,
+                               ki.occupancy_original, ki.alg_bytes, ki.alg_flops)
+
+    @property
+    def total_blocks(self) -> int:
+        return self.info.total_blocks
+
+    def _launch(self, stream: Stream, desc: _lib.c_launch_desc) -> Launch:
+        lid = C.c_int()
+        _lib.check(_lib.lib.tally_launch(self.id, stream.id, C.byref(desc), C.byref(lid)),
+                   f"{self.kind} launch")
+        return Launch(lid.value, desc.shape)
+
+    def original(self, stream: Stream, exec_count=None, timed=False) -> Launch:
+        d = _lib.c_launch_desc(shape=_lib.SHAPE_ORIGINAL, preempt_at=-1,
+                               exec_count=_ptr(exec_count), timed=int(timed))
+        return self._launch(stream, d)
+
+    def sliced(self, stream: Stream, offset: int, count: int, exec_count=None,
+               timed=False) -> Launch:
+        """Logical blocks [offset, offset + count) of the x-fastest order."""
+        d = _lib.c_launch_desc(shape=_lib.SHAPE_SLICED, linear=1, linear_offset=offset,
+                               count=count, preempt_at=-1, exec_count=_ptr(exec_count),
+                               timed=int(timed))
+        return self._launch(stream, d)
+
+    def sliced_rect(self, stream: Stream, offset, sub_grid, exec_count=None) -> Launch:
+        """Rectangular sub-grid at a 3-D block offset (ref transforms.py:92-133)."""
+        d = _lib.c_launch_desc(shape=_lib.SHAPE_SLICED, linear=0, off_x=offset[0],
+                               off_y=offset[1], off_z=offset[2], sub_x=sub_grid[0],
+                               sub_y=sub_grid[1], sub_z=sub_grid[2], preempt_at=-1,
+                               exec_count=_ptr(exec_count))
+        return self._launch(stream, d)
+
+    def ptb(self, stream: Stream, workers: int, start_count: int = 0, preempt_at=None,
+            exec_count=None, timed=False) -> Launch:
+        d = _lib.c_launch_desc(shape=_lib.SHAPE_PTB, workers=workers, start_count=start_count,
+                               preempt_at=-1 if preempt_at is None else preempt_at,
+                               exec_count=_ptr(exec_count), timed=int(timed))
+        return self._launch(stream, d)
+
+    def cost(self, block_duration_ns: int = 0, launch_overhead_ns: int = DEFAULT_LAUNCH_OVERHEAD_NS,
+             ptb_iteration_overhead_ns: int = 0) -> KernelCostModel:
+        """The KernelCostModel this kernel registers with (durations are
+        informational on the B200; the profiler measures the real ones)."""
+        return KernelCostModel(block_duration_ns, launch_overhead_ns, ptb_iteration_overhead_ns,
+                               self.info.threads_per_block, self.info.total_blocks)
+
+    def close(self):
+        if self.id >= 0:
+            _lib.lib.tally_kernel_destroy(self.id)
+            self.id = -1
+            self._keep = ()
+
+
+# -- constructors for the built-in kinds ------------------------------------
+def vecadd_i64(mem, a_base: int, b_base: int, out_base: int, n: int,
+               elems_per_block: int = 1) -> DeviceKernel:
+    """IR vecadd over an int64 word image ``[a | b | out]`` (ref tests/test_ir.py:165-172)."""
+    return DeviceKernel("vecadd_i64", (mem,), (a_base, b_base, out_base, n, elems_per_block))
+
+
+def vecadd_f32(a, b, c) -> DeviceKernel:
+    """c = a + b; 4096 elements per logical block."""
+    return DeviceKernel("vecadd_f32", (a, b, c), (a.numel(),))
+
+
+def rowsum_f32(x, out) -> DeviceKernel:
+    """out[r] = sum(x[r, :]); 8 rows per logical block."""
+    rows, cols = x.shape
+    return DeviceKernel("rowsum_f32", (x, out), (rows, cols))
+
+
+def kind_names():
+    n = _lib.lib.tally_kernel_kind_count()
+    return [_lib.lib.tally_kernel_kind_name(i).decode() for i in range(n)]
