@@ -61,6 +61,7 @@ typedef struct {
   long long smem_per_sm;
   long long hbm_bytes;
   int stream_mem_ops;       /* 1 if cuStreamWriteValue32 is usable (device-resident flags) */
+  int stream_mem_ops_probe; /* diagnostic: entry-point status * 1000 + CUresult of the probe write */
   char name[96];
 } tally_gpu_info;
 
@@ -126,6 +127,8 @@ typedef struct {
   long long preempt_at;     /* test trigger: raise the flag when the counter reaches this
                                value (ref transforms.py:433-447 MemTrigger); -1 = off */
   unsigned long long* exec_count; /* optional device array[total_blocks]: exactly-once audit */
+  unsigned long long* worker_log; /* PTB, optional device array[workers * 4]: per-worker
+                                     {smid << 32 | tasks, t_entry, t_exit, stopped} (%globaltimer) */
   int timed;                /* 1: bracket with timing events (tally_launch_elapsed_ns) */
 } tally_launch_desc;
 
@@ -219,6 +222,10 @@ int tally_runner_requests(int runner, int task, long long* out_pairs, int cap);
 int tally_runner_iteration_count(int runner, int task);
 int tally_runner_iterations(int runner, int task, long long* out, int cap);
 int tally_runner_destroy(int runner);
+/* Options for the B200 device run: "trace" (1 = bracket every launch with
+ * timing events for the launch log), "hp_streams" (size of the high-priority
+ * stream pool, default 4). */
+int tally_runner_set_option(int runner, const char* key, long long value);
 
 /* Real-device run log (only after tally_runner_run(runner, NULL)). */
 typedef struct {
@@ -235,6 +242,8 @@ typedef struct {
   long long submit_ns, issue_ns, complete_ns, preempt_ns;      /* host clock, run-relative */
   long long gt_first_start, gt_first_stop, gt_last_exit;       /* device clock            */
   int parked;
+  long long gpu_start_ns, gpu_end_ns;  /* GPU timeline (CUDA events vs a run-start reference
+                                          event; -1 unless the "trace" option is set)       */
 } tally_launch_record;
 
 long long tally_device_run_origin_ns(int runner);   /* host ns that event times are relative to */

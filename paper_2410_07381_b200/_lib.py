@@ -43,7 +43,8 @@ class c_gpu_info(C.Structure):
     _fields_ = [("device", C.c_int), ("num_sms", C.c_int), ("max_threads_per_sm", C.c_int),
                 ("max_blocks_per_sm", C.c_int), ("cc_major", C.c_int), ("cc_minor", C.c_int),
                 ("smem_per_sm", C.c_longlong), ("hbm_bytes", C.c_longlong),
-                ("stream_mem_ops", C.c_int), ("name", C.c_char * 96)]
+                ("stream_mem_ops", C.c_int), ("stream_mem_ops_probe", C.c_int),
+                ("name", C.c_char * 96)]
 
 
 class c_kernel_args(C.Structure):
@@ -63,7 +64,8 @@ class c_launch_desc(C.Structure):
                 ("count", C.c_longlong), ("off_x", C.c_uint), ("off_y", C.c_uint),
                 ("off_z", C.c_uint), ("sub_x", C.c_uint), ("sub_y", C.c_uint),
                 ("sub_z", C.c_uint), ("workers", C.c_int), ("start_count", C.c_longlong),
-                ("preempt_at", C.c_longlong), ("exec_count", C.c_void_p), ("timed", C.c_int)]
+                ("preempt_at", C.c_longlong), ("exec_count", C.c_void_p),
+                ("worker_log", C.c_void_p), ("timed", C.c_int)]
 
 
 class c_launch_state(C.Structure):
@@ -131,7 +133,8 @@ class c_launch_record(C.Structure):
                 ("submit_ns", C.c_longlong), ("issue_ns", C.c_longlong),
                 ("complete_ns", C.c_longlong), ("preempt_ns", C.c_longlong),
                 ("gt_first_start", C.c_longlong), ("gt_first_stop", C.c_longlong),
-                ("gt_last_exit", C.c_longlong), ("parked", C.c_int)]
+                ("gt_last_exit", C.c_longlong), ("parked", C.c_int),
+                ("gpu_start_ns", C.c_longlong), ("gpu_end_ns", C.c_longlong)]
 
 
 _SIGNATURES = {
@@ -169,6 +172,7 @@ _SIGNATURES = {
     "tally_runner_iteration_count": (C.c_int, [C.c_int, C.c_int]),
     "tally_runner_iterations": (C.c_int, [C.c_int, C.c_int, C.POINTER(C.c_longlong), C.c_int]),
     "tally_runner_destroy": (C.c_int, [C.c_int]),
+    "tally_runner_set_option": (C.c_int, [C.c_int, C.c_char_p, C.c_longlong]),
     "tally_device_run_origin_ns": (C.c_longlong, [C.c_int]),
     "tally_device_event_count": (C.c_int, [C.c_int]),
     "tally_device_events": (C.c_int, [C.c_int, C.POINTER(c_event), C.c_int]),

@@ -1,7 +1,7 @@
 """Build libtally_b200.so in-tree with nvcc for sm_100a.
 
-    python -m paper_2410_07381_b200.build          # incremental
-    python -m paper_2410_07381_b200.build --force
+    python paper_2410_07381_b200/build.py          # incremental
+    python paper_2410_07381_b200/build.py --force  (or __graft_entry__.build())
 
 Output: paper_2410_07381_b200/_lib/libtally_b200.so (git-ignored; travels to
 the GPU box with the gpurun snapshot).  Cross-compiles without a GPU.

@@ -37,6 +37,7 @@ struct Handle {
   long long submit_ns = 0, issue_ns = 0, complete_ns = 0, preempt_ns = 0;
   long long gt_first_start = 0, gt_first_stop = 0, gt_last_exit = 0;
   long long count = 0;
+  long long gpu_start = -1, gpu_end = -1;
 };
 
 class CudaDevice : public Device {
@@ -44,10 +45,17 @@ class CudaDevice : public Device {
   explicit CudaDevice(Runner* r) : r_(r) {
     Runtime& R = rt();
     if (!R.inited) throw Error(TALLY_EINVAL, "tally_init must be called before running on the B200");
-    for (int i = 0; i < kHpStreams; ++i) {
+    trace_ = r_->option("trace", 0) != 0;
+    const int n_hp = (int)r_->option("hp_streams", 4);
+    for (int i = 0; i < n_hp; ++i) {
       int s;
       if (tally_stream_create(TALLY_HIGH, &s) != TALLY_OK) throw Error(TALLY_ECUDA, "HP stream");
       hp_streams_.push_back(s);
+    }
+    if (trace_) {
+      cudaEventCreate(&ref_);
+      cudaEventRecord(ref_, R.sig_stream);
+      cudaEventSynchronize(ref_);
     }
     t0_ = host_now_ns();
     r_->log.t0_ns = t0_;
@@ -58,6 +66,7 @@ class CudaDevice : public Device {
     for (auto& h : hs_)
       if (h.launch >= 0) tally_launch_release(h.launch);
     for (int s : hp_streams_) tally_stream_destroy(s);
+    if (ref_) cudaEventDestroy(ref_);
     for (auto& kv : be_streams_) tally_stream_destroy(kv.second);
   }
 
@@ -161,7 +170,6 @@ class CudaDevice : public Device {
   }
 
  private:
-  static constexpr int kHpStreams = 4;
   struct Tm {
     long long t, seq, token;
     bool operator<(const Tm& o) const { return t != o.t ? t > o.t : seq > o.seq; }   // min-heap
@@ -174,6 +182,9 @@ class CudaDevice : public Device {
   std::vector<long long> pending_, park_unissued_;
   int inflight_ = 0;
   bool filter_ = false;
+  bool trace_ = false;
+  std::map<int, long long> total_cache_;
+  cudaEvent_t ref_ = nullptr;
   int hp_rr_ = 0;
   std::vector<int> hp_streams_;
   std::map<int, int> be_streams_;
@@ -237,8 +248,13 @@ class CudaDevice : public Device {
     tally_launch_desc ld;
     memset(&ld, 0, sizeof(ld));
     ld.preempt_at = -1;
-    tally_kernel_info ki;
-    if (tally_kernel_info_get(h.d.device_kernel, &ki) != TALLY_OK) throw Error(TALLY_EINVAL, tally_last_error());
+    auto kit = total_cache_.find(h.d.device_kernel);
+    if (kit == total_cache_.end()) {
+      tally_kernel_info info;
+      if (tally_kernel_info_get(h.d.device_kernel, &info) != TALLY_OK) throw Error(TALLY_EINVAL, tally_last_error());
+      kit = total_cache_.emplace(h.d.device_kernel, info.total_blocks).first;
+    }
+    struct { long long total_blocks; } ki{kit->second};
     if (h.d.shape == TALLY_SHAPE_PTB) {
       ld.shape = TALLY_SHAPE_PTB;
       ld.workers = h.d.worker_count;
@@ -255,9 +271,10 @@ class CudaDevice : public Device {
       h.count = ki.total_blocks;
     }
     int stream;
+    ld.timed = trace_ ? 1 : 0;
     if (h.d.priority == TALLY_HIGH) {
       stream = hp_streams_[(size_t)hp_rr_];
-      hp_rr_ = (hp_rr_ + 1) % kHpStreams;
+      hp_rr_ = (hp_rr_ + 1) % (int)hp_streams_.size();
     } else {
       stream = be_stream(h.d.task);
     }
@@ -282,6 +299,16 @@ class CudaDevice : public Device {
     h.gt_first_stop = L->gt_first_stop;
     h.gt_last_exit = L->gt_last_exit;
     --inflight_;
+    if (trace_ && L->ev_start && L->ev_end) {
+      float ms0 = 0, ms1 = 0;
+      cudaEventSynchronize(L->ev_end);
+      if (cudaEventElapsedTime(&ms0, ref_, L->ev_start) == cudaSuccess &&
+          cudaEventElapsedTime(&ms1, ref_, L->ev_end) == cudaSuccess) {
+        h.gpu_start = (long long)(ms0 * 1e6);
+        h.gpu_end = (long long)(ms1 * 1e6);
+      }
+      cudaGetLastError();
+    }
     record(id);
     tally_launch_release(h.launch);
     h.launch = -1;
@@ -319,6 +346,8 @@ class CudaDevice : public Device {
     rec.gt_first_stop = h.gt_first_stop;
     rec.gt_last_exit = h.gt_last_exit;
     rec.parked = h.parked ? 1 : 0;
+    rec.gpu_start_ns = h.gpu_start;
+    rec.gpu_end_ns = h.gpu_end;
     r_->log.launches.push_back(rec);
   }
 };

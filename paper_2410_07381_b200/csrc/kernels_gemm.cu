@@ -1,5 +1,544 @@
-// placeholder: tcgen05 GEMM kinds are registered here (added in a later commit)
+// Best-effort dense contractions on the 5th-generation tensor cores, in the
+// three Tally launch shapes.
+//
+//   sgemm_tf32x3   C[M,N] (fp32) = A[M,K] . B[N,K]^T with fp32 accuracy via the
+//                  error-compensated 3xTF32 split: A = Ahi + Alo, B = Bhi + Blo
+//                  (hi = tf32-rounded, lo = exact fp32 remainder), and
+//                  C = Ahi.Bhi + Ahi.Blo + Alo.Bhi accumulated in fp32 TMEM.
+//                  Operands are pre-split by the `split_tf32` kind.
+//   gemm_bf16      C[M,N] (bf16) = A[M,K] . B[N,K]^T, bf16 in, fp32 accumulate.
+//   split_tf32     x -> (hi, lo), elementwise (HBM bound).
+//
+// One logical block = one BM x BN output tile (tile index t, grouped
+// rasterisation over GROUP_M row-blocks for L2 reuse).  Every shape runs the
+// same warp-specialised CTA:
+//   warp 0      TMA producer: claims tiles (Original: blockIdx; Sliced:
+//               offset + blockIdx; PTB: flag-gated L2 atomic), streams A/B
+//               k-blocks into a STAGES-deep smem ring (mbarrier complete_tx)
+//   warp 1      MMA issuer: one elected thread issues tcgen05.mma into a
+//               double-buffered TMEM accumulator, tcgen05.commit frees smem
+//               stages and signals the epilogue
+//   warps 2-5   epilogue: tcgen05.ld TMEM -> registers -> global C
+// A two-slot tile ring in smem carries claimed tile ids from the producer to
+// the other roles; id -1 ends the CTA.  In PTB shape a claimed tile is always
+// finished, so a preempted worker retires within ~one tile.
+#include <cuda.h>
+#include <cuda_bf16.h>
+
+#include <cstdio>
+
 #include "registry.h"
+#include "runtime.h"
+
 namespace tally {
-int register_gemm_kernels(KernelKind*, int) { return 0; }
+
+namespace gemm {
+
+enum Mode { kOriginal = 0, kSliced = 1, kPtb = 2 };
+
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+  return static_cast<uint32_t>(__cvta_generic_to_shared(p));
 }
+
+__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count));
+}
+__device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes)
+               : "memory");
+}
+__device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
+  asm volatile(
+      "{\n"
+      ".reg .pred p;\n"
+      "WAIT_%=:\n"
+      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
+      "@!p bra WAIT_%=;\n"
+      "}\n" ::"r"(smem_u32(bar)),
+      "r"(parity)
+      : "memory");
+}
+
+__device__ __forceinline__ void tma_load_2d(void* dst, const CUtensorMap* map, uint64_t* bar, int x, int y) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%3, %4}], [%2];" ::"r"(
+          smem_u32(dst)),
+      "l"(map), "r"(smem_u32(bar)), "r"(x), "r"(y)
+      : "memory");
+}
+
+__device__ __forceinline__ void fence_after() { asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory"); }
+__device__ __forceinline__ void fence_before() { asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory"); }
+
+__device__ __forceinline__ void umma_commit(uint64_t* bar) {
+  asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(smem_u32(bar))
+               : "memory");
+}
+
+// K-major operand tile, 128-byte swizzle, 8-row core groups 1024 B apart.
+__device__ __forceinline__ uint64_t smem_desc(const void* p) {
+  const uint64_t addr = smem_u32(p);
+  uint64_t d = 0;
+  d |= (addr & 0x3FFFFull) >> 4;          // start address (16 B units)
+  d |= 1ull << 16;                        // leading byte offset (unused for SW128 K-major)
+  d |= (1024ull >> 4) << 32;              // stride byte offset: 8 rows x 128 B
+  d |= 1ull << 46;                        // descriptor version (sm_100)
+  d |= 2ull << 61;                        // SWIZZLE_128B
+  return d;
+}
+
+template <int KIND>  // 0: tf32, 1: bf16 (kind::f16)
+__device__ __forceinline__ void umma(uint32_t tmem_d, uint64_t a, uint64_t b, uint32_t idesc, uint32_t acc) {
+  if constexpr (KIND == 0) {
+    asm volatile(
+        "{\n.reg .pred p;\nsetp.ne.b32 p, %4, 0;\n"
+        "tcgen05.mma.cta_group::1.kind::tf32 [%0], %1, %2, %3, p;\n}\n" ::"r"(tmem_d),
+        "l"(a), "l"(b), "r"(idesc), "r"(acc));
+  } else {
+    asm volatile(
+        "{\n.reg .pred p;\nsetp.ne.b32 p, %4, 0;\n"
+        "tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n}\n" ::"r"(tmem_d),
+        "l"(a), "l"(b), "r"(idesc), "r"(acc));
+  }
+}
+
+// Instruction descriptor: D fp32, K-major A and B, M = 128, N = BN.
+template <int KIND, int BN>
+__host__ __device__ constexpr uint32_t make_idesc() {
+  return (1u << 4)                                  // D format: F32
+         | ((KIND == 0 ? 2u : 1u) << 7)             // A format: TF32 / BF16
+         | ((KIND == 0 ? 2u : 1u) << 10)            // B format
+         | ((uint32_t)(BN >> 3) << 17)              // N >> 3
+         | ((uint32_t)(128 >> 4) << 24);            // M >> 4
+}
+
+__device__ __forceinline__ void tmem_ld32(uint32_t taddr, uint32_t (&r)[32]) {
+  asm volatile(
+      "tcgen05.ld.sync.aligned.32x32b.x32.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,"
+      "%16,%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31}, [%32];"
+      : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7]),
+        "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]), "=r"(r[15]),
+        "=r"(r[16]), "=r"(r[17]), "=r"(r[18]), "=r"(r[19]), "=r"(r[20]), "=r"(r[21]), "=r"(r[22]), "=r"(r[23]),
+        "=r"(r[24]), "=r"(r[25]), "=r"(r[26]), "=r"(r[27]), "=r"(r[28]), "=r"(r[29]), "=r"(r[30]), "=r"(r[31])
+      : "r"(taddr));
+  asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+}
+
+// ---------------------------------------------------------------- configs
+struct CfgTf32x3 {
+  static constexpr int KIND = 0;
+  static constexpr int BM = 128, BN = 64;
+  static constexpr int BK = 32;                       // fp32 elements = 128 B (one swizzle atom)
+  static constexpr int ESZ = 4;
+  static constexpr int NOPS = 4;                      // Ahi, Alo, Bhi, Blo
+  static constexpr int A_BYTES = BM * BK * ESZ;       // 16 KB
+  static constexpr int B_BYTES = BN * BK * ESZ;       // 8 KB
+  static constexpr int STAGE_BYTES = 2 * A_BYTES + 2 * B_BYTES;   // 48 KB
+  static constexpr int STAGES = 4;
+  static constexpr int UMMA_K = 8;
+  static constexpr int TMEM_COLS = 2 * BN;            // double-buffered accumulator
+  using OutT = float;
+};
+
+struct CfgBf16 {
+  static constexpr int KIND = 1;
+  static constexpr int BM = 128, BN = 128;
+  static constexpr int BK = 64;                       // bf16 elements = 128 B
+  static constexpr int ESZ = 2;
+  static constexpr int NOPS = 2;
+  static constexpr int A_BYTES = BM * BK * ESZ;       // 16 KB
+  static constexpr int B_BYTES = BN * BK * ESZ;       // 16 KB
+  static constexpr int STAGE_BYTES = A_BYTES + B_BYTES;
+  static constexpr int STAGES = 6;
+  static constexpr int UMMA_K = 16;
+  static constexpr int TMEM_COLS = 2 * BN;
+  using OutT = __nv_bfloat16;
+};
+
+constexpr int GROUP_M = 8;
+constexpr int kThreads = 192;   // producer warp, MMA warp, 4 epilogue warps
+
+template <class Cfg>
+constexpr size_t smem_bytes() {
+  return 1024 /*alignment slack*/ + (size_t)Cfg::STAGES * Cfg::STAGE_BYTES + 256 /*barriers + ring*/;
+}
+
+struct alignas(64) GemmParams {
+  CUtensorMap a_hi, a_lo, b_hi, b_lo;   // lo maps unused for bf16
+  void* c;
+  int m, n, k;
+  int tiles_m, tiles_n;
+};
+
+__device__ __forceinline__ void tile_coords(long long t, const GemmParams& p, int& mb, int& nb) {
+  // grouped rasterisation: GROUP_M row-blocks share each column sweep
+  const int per_group = GROUP_M * p.tiles_n;
+  const int g = (int)(t / per_group);
+  const int first_m = g * GROUP_M;
+  const int gm = min(p.tiles_m - first_m, GROUP_M);
+  const int r = (int)(t % per_group);
+  mb = first_m + r % gm;
+  nb = r / gm;
+}
+
+template <class Cfg, int MODE, class ShapeArgs>
+__global__ void __launch_bounds__(kThreads, 1) k_gemm(const __grid_constant__ GemmParams p, const ShapeArgs s) {
+  extern __shared__ __align__(1024) unsigned char smem_raw[];
+  unsigned char* smem = reinterpret_cast<unsigned char*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem + (size_t)Cfg::STAGES * Cfg::STAGE_BYTES);
+  uint64_t* empty = full + Cfg::STAGES;
+  uint64_t* tmem_full = empty + Cfg::STAGES;    // [2]
+  uint64_t* tmem_empty = tmem_full + 2;         // [2]
+  uint64_t* tile_full = tmem_empty + 2;         // [2]
+  uint64_t* tile_empty = tile_full + 2;         // [2]
+  long long* tile_slot = reinterpret_cast<long long*>(tile_empty + 2);   // [2]
+  uint32_t* tmem_base_slot = reinterpret_cast<uint32_t*>(tile_slot + 2);
+
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int KB = p.k / Cfg::BK;
+
+  unsigned long long t_entry = 0;
+  if (threadIdx.x == 0) {
+    t_entry = globaltimer();
+    for (int i = 0; i < Cfg::STAGES; ++i) { mbar_init(&full[i], 1); mbar_init(&empty[i], 1); }
+    for (int i = 0; i < 2; ++i) {
+      mbar_init(&tmem_full[i], 1);
+      mbar_init(&tmem_empty[i], 4);
+      mbar_init(&tile_full[i], 1);
+      mbar_init(&tile_empty[i], 5);
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  if (warp == 1) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(tmem_base_slot)),
+                 "n"(Cfg::TMEM_COLS));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+  }
+  fence_before();
+  __syncthreads();
+  fence_after();
+  const uint32_t tmem_base = *tmem_base_slot;
+  bool stopped = false;
+
+  if (warp == 0) {
+    if (lane == 0) {
+      // ------------------------------------------------ TMA producer
+      uint32_t it = 0;
+      for (int i = 0;; ++i) {
+        long long t = -1;
+        if constexpr (MODE == kPtb) {
+          t = ptb_claim(s);
+          if (t < 0) stopped = true;
+          else if ((unsigned long long)t >= s.total) t = -1;
+        } else {
+          if (i == 0) {
+            t = MODE == kOriginal ? (long long)blockIdx.x
+                : (s.linear ? (long long)(s.linear_offset + blockIdx.x) : (long long)(s.offset.x + blockIdx.x));
+            if (s.exec_count != nullptr) atomicAdd(&s.exec_count[t], 1ull);
+          }
+        }
+        const int j = i & 1;
+        if (i >= 2) mbar_wait(&tile_empty[j], ((i >> 1) - 1) & 1);
+        tile_slot[j] = t;
+        mbar_arrive(&tile_full[j]);
+        if (t < 0) break;
+        int mb, nb;
+        tile_coords(t, p, mb, nb);
+        for (int kb = 0; kb < KB; ++kb, ++it) {
+          const int st = it % Cfg::STAGES;
+          if (it >= (uint32_t)Cfg::STAGES) mbar_wait(&empty[st], ((it / Cfg::STAGES) - 1) & 1);
+          unsigned char* base = smem + (size_t)st * Cfg::STAGE_BYTES;
+          mbar_expect_tx(&full[st], Cfg::STAGE_BYTES);
+          const int kx = kb * Cfg::BK;
+          if constexpr (Cfg::KIND == 0) {
+            tma_load_2d(base, &p.a_hi, &full[st], kx, mb * Cfg::BM);
+            tma_load_2d(base + Cfg::A_BYTES, &p.a_lo, &full[st], kx, mb * Cfg::BM);
+            tma_load_2d(base + 2 * Cfg::A_BYTES, &p.b_hi, &full[st], kx, nb * Cfg::BN);
+            tma_load_2d(base + 2 * Cfg::A_BYTES + Cfg::B_BYTES, &p.b_lo, &full[st], kx, nb * Cfg::BN);
+          } else {
+            tma_load_2d(base, &p.a_hi, &full[st], kx, mb * Cfg::BM);
+            tma_load_2d(base + Cfg::A_BYTES, &p.b_hi, &full[st], kx, nb * Cfg::BN);
+          }
+        }
+      }
+    }
+    __syncwarp();
+  } else if (warp == 1) {
+    if (lane == 0) {
+      // ------------------------------------------------ MMA issuer
+      constexpr uint32_t idesc = make_idesc<Cfg::KIND, Cfg::BN>();
+      uint32_t it = 0;
+      for (int i = 0;; ++i) {
+        const int j = i & 1;
+        mbar_wait(&tile_full[j], (i >> 1) & 1);
+        const long long t = tile_slot[j];
+        mbar_arrive(&tile_empty[j]);
+        if (t < 0) break;
+        const int acc = i & 1;
+        if (i >= 2) mbar_wait(&tmem_empty[acc], ((i >> 1) - 1) & 1);
+        fence_after();
+        const uint32_t d = tmem_base + (uint32_t)(acc * Cfg::BN);
+        for (int kb = 0; kb < KB; ++kb, ++it) {
+          const int st = it % Cfg::STAGES;
+          mbar_wait(&full[st], (it / Cfg::STAGES) & 1);
+          fence_after();
+          const unsigned char* base = smem + (size_t)st * Cfg::STAGE_BYTES;
+#pragma unroll
+          for (int k = 0; k < Cfg::BK / Cfg::UMMA_K; ++k) {
+            const uint32_t first = (kb | k) != 0;
+            const int koff = k * Cfg::UMMA_K * Cfg::ESZ;   // 32 B per MMA-K step inside the atom
+            if constexpr (Cfg::KIND == 0) {
+              const uint64_t ahi = smem_desc(base + koff), alo = smem_desc(base + Cfg::A_BYTES + koff);
+              const uint64_t bhi = smem_desc(base + 2 * Cfg::A_BYTES + koff);
+              const uint64_t blo = smem_desc(base + 2 * Cfg::A_BYTES + Cfg::B_BYTES + koff);
+              umma<0>(d, alo, bhi, idesc, first);   // small terms first
+              umma<0>(d, ahi, blo, idesc, 1);
+              umma<0>(d, ahi, bhi, idesc, 1);
+            } else {
+              umma<1>(d, smem_desc(base + koff), smem_desc(base + Cfg::A_BYTES + koff), idesc, first);
+            }
+          }
+          umma_commit(&empty[st]);   // frees the stage once these MMAs retire
+        }
+        umma_commit(&tmem_full[acc]);
+      }
+    }
+    __syncwarp();
+  } else {
+    // -------------------------------------------------- epilogue (warps 2..5)
+    const int q = warp & 3;   // TMEM lane quarter this warp may access
+    for (int i = 0;; ++i) {
+      const int j = i & 1;
+      mbar_wait(&tile_full[j], (i >> 1) & 1);
+      const long long t = tile_slot[j];
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&tile_empty[j]);
+      if (t < 0) break;
+      int mb, nb;
+      tile_coords(t, p, mb, nb);
+      const int acc = i & 1;
+      mbar_wait(&tmem_full[acc], (i >> 1) & 1);
+      fence_after();
+      const int row = mb * Cfg::BM + q * 32 + lane;
+      typename Cfg::OutT* crow = reinterpret_cast<typename Cfg::OutT*>(p.c) + (size_t)row * p.n + (size_t)nb * Cfg::BN;
+#pragma unroll
+      for (int c0 = 0; c0 < Cfg::BN; c0 += 32) {
+        uint32_t r[32];
+        tmem_ld32(tmem_base + ((uint32_t)(q * 32) << 16) + (uint32_t)(acc * Cfg::BN + c0), r);
+        if constexpr (Cfg::KIND == 0) {
+          float4* dst = reinterpret_cast<float4*>(crow + c0);
+#pragma unroll
+          for (int v = 0; v < 8; ++v)
+            dst[v] = make_float4(__uint_as_float(r[4 * v]), __uint_as_float(r[4 * v + 1]),
+                                 __uint_as_float(r[4 * v + 2]), __uint_as_float(r[4 * v + 3]));
+        } else {
+          uint4* dst = reinterpret_cast<uint4*>(crow + c0);
+#pragma unroll
+          for (int v = 0; v < 4; ++v) {
+            uint32_t w[4];
+#pragma unroll
+            for (int e = 0; e < 4; ++e) {
+              __nv_bfloat162 h = __floats2bfloat162_rn(__uint_as_float(r[8 * v + 2 * e]),
+                                                       __uint_as_float(r[8 * v + 2 * e + 1]));
+              w[e] = *reinterpret_cast<uint32_t*>(&h);
+            }
+            dst[v] = make_uint4(w[0], w[1], w[2], w[3]);
+          }
+        }
+      }
+      fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&tmem_empty[acc]);
+    }
+  }
+
+  fence_before();
+  __syncthreads();
+  fence_after();
+  if (warp == 1)
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem_base), "n"(Cfg::TMEM_COLS));
+  if constexpr (MODE == kPtb) {
+    if (threadIdx.x == 0) ptb_worker_exit(s, stopped, t_entry);
+  }
+}
+
+// ---------------------------------------------------------------- split_tf32
+struct SplitTf32 {
+  static constexpr int kThreads = 256;
+  static constexpr int kVec = 4;                                  // float4 per thread
+  static constexpr int kElemsPerBlock = kThreads * kVec * 4;      // 4096
+  struct Params {
+    const float4* x;
+    float4* hi;
+    float4* lo;
+    long long n4;
+  };
+  static __device__ __forceinline__ float tf32_rna(float v) {
+    uint32_t r;
+    asm("cvt.rna.tf32.f32 %0, %1;" : "=r"(r) : "f"(v));
+    return __uint_as_float(r);
+  }
+  static __device__ __forceinline__ void run(const Params& p, uint3 bidx, uint3, char*) {
+    const long long base = (long long)bidx.x * (kThreads * kVec) + threadIdx.x;
+    float4 v[kVec];
+#pragma unroll
+    for (int j = 0; j < kVec; ++j) {
+      const long long k = base + (long long)j * kThreads;
+      if (k < p.n4) v[j] = __ldcs(p.x + k);
+    }
+#pragma unroll
+    for (int j = 0; j < kVec; ++j) {
+      const long long k = base + (long long)j * kThreads;
+      if (k < p.n4) {
+        const float4 h = make_float4(tf32_rna(v[j].x), tf32_rna(v[j].y), tf32_rna(v[j].z), tf32_rna(v[j].w));
+        p.hi[k] = h;
+        p.lo[k] = make_float4(v[j].x - h.x, v[j].y - h.y, v[j].z - h.z, v[j].w - h.w);
+      }
+    }
+  }
+};
+
+}  // namespace gemm
+
+// ---------------------------------------------------------------- host side
+typedef CUresult (*EncodeTiledFn)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
+                                  const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
+                                  CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+
+static EncodeTiledFn encode_fn() {
+  static EncodeTiledFn fn = nullptr;
+  static bool tried = false;
+  if (!tried) {
+    tried = true;
+    void* f = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPointByVersion("cuTensorMapEncodeTiled", &f, 12000, cudaEnableDefault, &q) == cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      fn = reinterpret_cast<EncodeTiledFn>(f);
+  }
+  return fn;
+}
+
+// rows x cols (K innermost) row-major matrix, box = box_rows x 128 bytes, 128 B swizzle
+static int make_map(CUtensorMap* m, const void* ptr, CUtensorMapDataType dt, int esz, long long rows,
+                    long long cols, int box_rows) {
+  EncodeTiledFn enc = encode_fn();
+  if (!enc) { set_error("cuTensorMapEncodeTiled unavailable"); return TALLY_ENODEV; }
+  cuuint64_t dims[2] = {(cuuint64_t)cols, (cuuint64_t)rows};
+  cuuint64_t strides[1] = {(cuuint64_t)cols * esz};
+  cuuint32_t box[2] = {(cuuint32_t)(128 / esz), (cuuint32_t)box_rows};
+  cuuint32_t estr[2] = {1, 1};
+  CUresult r = enc(m, dt, 2, const_cast<void*>(ptr), dims, strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
+                   CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS) { set_error("cuTensorMapEncodeTiled failed (%d)", (int)r); return TALLY_EINVAL; }
+  return TALLY_OK;
+}
+
+template <class Cfg>
+static int bind_gemm(const tally_kernel_args* a, Instance* inst, bool split) {
+  gemm::GemmParams p;
+  memset(&p, 0, sizeof(p));
+  const long long M = a->i[0], N = a->i[1], K = a->i[2];
+  if (M < 1 || N < 1 || K < 1 || M % Cfg::BM || N % Cfg::BN || K % Cfg::BK) {
+    set_error("gemm: need M %% %d == 0, N %% %d == 0, K %% %d == 0 (got %lld %lld %lld)", Cfg::BM, Cfg::BN,
+              Cfg::BK, M, N, K);
+    return TALLY_EINVAL;
+  }
+  const int nptr = split ? 5 : 3;
+  for (int i = 0; i < nptr; ++i)
+    if (!a->ptr[i] || reinterpret_cast<uintptr_t>(a->ptr[i]) % 16) {
+      set_error("gemm: operand %d missing or not 16-byte aligned", i);
+      return TALLY_EINVAL;
+    }
+  const CUtensorMapDataType dt = Cfg::KIND == 0 ? CU_TENSOR_MAP_DATA_TYPE_FLOAT32 : CU_TENSOR_MAP_DATA_TYPE_BFLOAT16;
+  int rc;
+  if (split) {   // ptr: A_hi, A_lo, B_hi, B_lo, C
+    if ((rc = make_map(&p.a_hi, a->ptr[0], dt, Cfg::ESZ, M, K, Cfg::BM))) return rc;
+    if ((rc = make_map(&p.a_lo, a->ptr[1], dt, Cfg::ESZ, M, K, Cfg::BM))) return rc;
+    if ((rc = make_map(&p.b_hi, a->ptr[2], dt, Cfg::ESZ, N, K, Cfg::BN))) return rc;
+    if ((rc = make_map(&p.b_lo, a->ptr[3], dt, Cfg::ESZ, N, K, Cfg::BN))) return rc;
+    p.c = a->ptr[4];
+  } else {       // ptr: A, B, C
+    if ((rc = make_map(&p.a_hi, a->ptr[0], dt, Cfg::ESZ, M, K, Cfg::BM))) return rc;
+    if ((rc = make_map(&p.b_hi, a->ptr[1], dt, Cfg::ESZ, N, K, Cfg::BN))) return rc;
+    p.c = a->ptr[2];
+  }
+  p.m = (int)M;
+  p.n = (int)N;
+  p.k = (int)K;
+  p.tiles_m = (int)(M / Cfg::BM);
+  p.tiles_n = (int)(N / Cfg::BN);
+  static_assert(sizeof(p) <= kMaxParamBytes, "params too large");
+  memcpy(inst->params, &p, sizeof(p));
+  inst->grid = make_uint3((unsigned)(p.tiles_m * p.tiles_n), 1, 1);
+  inst->threads = gemm::kThreads;
+  inst->smem = gemm::smem_bytes<Cfg>();
+  inst->alg_flops = 2.0 * (double)M * (double)N * (double)K;
+  inst->alg_bytes = (double)Cfg::ESZ * (double)(M * K + N * K) * (split ? 2.0 : 1.0) +
+                    (double)sizeof(typename Cfg::OutT) * (double)(M * N);
+  return TALLY_OK;
+}
+
+static int bind_sgemm(const tally_kernel_args* a, Instance* inst) { return bind_gemm<gemm::CfgTf32x3>(a, inst, true); }
+static int bind_bf16(const tally_kernel_args* a, Instance* inst) { return bind_gemm<gemm::CfgBf16>(a, inst, false); }
+
+template <class Cfg>
+static int setup_gemm() {
+  const int smem = (int)gemm::smem_bytes<Cfg>();
+  cudaError_t e;
+  if ((e = cudaFuncSetAttribute(gemm::k_gemm<Cfg, gemm::kOriginal, SliceArgs>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem)) != cudaSuccess ||
+      (e = cudaFuncSetAttribute(gemm::k_gemm<Cfg, gemm::kSliced, SliceArgs>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem)) != cudaSuccess ||
+      (e = cudaFuncSetAttribute(gemm::k_gemm<Cfg, gemm::kPtb, PtbArgs>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem)) != cudaSuccess)
+    return cuda_fail(e, "gemm smem attribute");
+  return TALLY_OK;
+}
+
+static int bind_split(const tally_kernel_args* a, Instance* inst) {
+  gemm::SplitTf32::Params p{};
+  p.x = static_cast<const float4*>(a->ptr[0]);
+  p.hi = static_cast<float4*>(a->ptr[1]);
+  p.lo = static_cast<float4*>(a->ptr[2]);
+  const long long n = a->i[0];
+  if (!p.x || !p.hi || !p.lo || n < 4 || n % 4) {
+    set_error("split_tf32: need x, hi, lo and n %% 4 == 0");
+    return TALLY_EINVAL;
+  }
+  p.n4 = n / 4;
+  memcpy(inst->params, &p, sizeof(p));
+  inst->grid = make_uint3((unsigned)((n + gemm::SplitTf32::kElemsPerBlock - 1) / gemm::SplitTf32::kElemsPerBlock), 1, 1);
+  inst->threads = gemm::SplitTf32::kThreads;
+  inst->smem = 0;
+  inst->alg_bytes = 12.0 * (double)n;
+  return TALLY_OK;
+}
+
+template <class Cfg>
+static KernelKind gemm_kind(const char* name, int (*bind)(const tally_kernel_args*, Instance*)) {
+  KernelKind k{};
+  k.name = name;
+  k.fn_original = reinterpret_cast<const void*>(&gemm::k_gemm<Cfg, gemm::kOriginal, SliceArgs>);
+  k.fn_sliced = reinterpret_cast<const void*>(&gemm::k_gemm<Cfg, gemm::kSliced, SliceArgs>);
+  k.fn_ptb = reinterpret_cast<const void*>(&gemm::k_gemm<Cfg, gemm::kPtb, PtbArgs>);
+  k.bind = bind;
+  k.setup = &setup_gemm<Cfg>;
+  return k;
+}
+
+int register_gemm_kernels(KernelKind* out, int cap) {
+  if (cap < 3) return 0;
+  out[0] = gemm_kind<gemm::CfgTf32x3>("sgemm_tf32x3", bind_sgemm);
+  out[1] = gemm_kind<gemm::CfgBf16>("gemm_bf16", bind_bf16);
+  KernelKind k{};
+  k.name = "split_tf32";
+  k.fn_original = reinterpret_cast<const void*>(&k_original<gemm::SplitTf32>);
+  k.fn_sliced = reinterpret_cast<const void*>(&k_sliced<gemm::SplitTf32>);
+  k.fn_ptb = reinterpret_cast<const void*>(&k_ptb<gemm::SplitTf32>);
+  k.bind = bind_split;
+  out[2] = k;
+  return 3;
+}
+
+}  // namespace tally

@@ -10,12 +10,12 @@
 
 namespace tally {
 
-constexpr int kMaxParamBytes = 512;
+constexpr int kMaxParamBytes = 1024;
 
 // A bound kernel: the body's Params blob plus its logical geometry.
 struct Instance {
   int kind = -1;
-  alignas(16) unsigned char params[kMaxParamBytes];
+  alignas(64) unsigned char params[kMaxParamBytes];
   uint3 grid{1, 1, 1};         // logical grid
   int threads = 0;             // CTA size
   size_t smem = 0;             // dynamic shared memory per CTA

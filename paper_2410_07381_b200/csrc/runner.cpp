@@ -482,6 +482,17 @@ int tally_runner_iterations(int runner, int task, long long* out, int cap) {
   return n;
 }
 
+int tally_runner_set_option(int runner, const char* key, long long value) {
+  Runner* r = get_runner(runner);
+  if (!r) return TALLY_EINVAL;
+  if (!key) { set_error("null option key"); return TALLY_EINVAL; }
+  const std::string k(key);
+  if (k != "trace" && k != "hp_streams") { set_error("unknown runner option '%s'", key); return TALLY_EINVAL; }
+  if (k == "hp_streams" && (value < 1 || value > 64)) { set_error("hp_streams must be in [1, 64]"); return TALLY_EINVAL; }
+  r->options[k] = value;
+  return TALLY_OK;
+}
+
 int tally_runner_destroy(int runner) {
   if (!get_runner(runner)) return TALLY_EINVAL;
   runners()[(size_t)runner].reset();

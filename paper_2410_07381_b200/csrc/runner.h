@@ -98,6 +98,11 @@ class Runner {
 
   std::vector<Task> tasks;
   DeviceLog log;
+  std::map<std::string, long long> options;
+  long long option(const std::string& k, long long dflt) const {
+    auto it = options.find(k);
+    return it == options.end() ? dflt : it->second;
+  }
   int policy;
   long long threshold, quantum, horizon;
 

@@ -120,20 +120,19 @@ int Runtime::init(int dev, tally_gpu_info* out) {
   CK(cudaStreamCreateWithPriority(&sig_stream, cudaStreamNonBlocking, hi), "signal stream");
 
   // driver stream memory operations: the flag write that preempts a PTB launch
-  cudaDriverEntryPointQueryResult q;
+  cudaDriverEntryPointQueryResult q = cudaDriverEntryPointSymbolNotFound;
   void* fn = nullptr;
-  if (cudaGetDriverEntryPoint("cuStreamWriteValue32", &fn, cudaEnableDefault, &q) == cudaSuccess &&
-      q == cudaDriverEntryPointSuccess && fn)
+  cudaError_t ge = cudaGetDriverEntryPointByVersion("cuStreamWriteValue32", &fn, 12000, cudaEnableDefault, &q);
+  if (ge == cudaSuccess && q == cudaDriverEntryPointSuccess && fn)
     write32 = reinterpret_cast<WriteValue32Fn>(fn);
-  fn = nullptr;
-  if (cudaGetDriverEntryPoint("cuStreamWriteValue64", &fn, cudaEnableDefault, &q) == cudaSuccess &&
-      q == cudaDriverEntryPointSuccess && fn)
-    write64 = reinterpret_cast<WriteValue64Fn>(fn);
   info.stream_mem_ops = 0;
+  info.stream_mem_ops_probe = (int)ge * 100000 + (int)q * 1000 + 999;
   if (write32) {
     // probe on record 0's flag
     CUresult r = write32((CUstream)sig_stream, (CUdeviceptr)&d_recs[0].flag, 0u, 0u);
-    if (r == CUDA_SUCCESS && cudaStreamSynchronize(sig_stream) == cudaSuccess) info.stream_mem_ops = 1;
+    cudaError_t se = cudaStreamSynchronize(sig_stream);
+    info.stream_mem_ops_probe = (int)q * 1000 + (int)r;
+    if (r == CUDA_SUCCESS && se == cudaSuccess) info.stream_mem_ops = 1;
     cudaGetLastError();
   }
   flag_host = info.stream_mem_ops ? 0 : 1;
@@ -295,6 +294,7 @@ int Runtime::launch(int kernel, int stream, const tally_launch_desc* d, int* out
       pa.preempt_at = d->preempt_at;
       pa.grid = in.grid;
       pa.exec_count = d->exec_count;
+      pa.worker_log = d->worker_log;
       fn = kk.fn_ptb;
       grid = dim3((unsigned)d->workers, 1, 1);
       args[1] = &pa;

@@ -17,7 +17,6 @@ namespace tally {
 long long host_now_ns();
 
 typedef CUresult (*WriteValue32Fn)(CUstream, CUdeviceptr, cuuint32_t, unsigned int);
-typedef CUresult (*WriteValue64Fn)(CUstream, CUdeviceptr, cuuint64_t, unsigned int);
 
 struct Launch {
   int kernel = -1, stream = -1, shape = 0;
@@ -64,7 +63,6 @@ struct Runtime {
   std::atomic<unsigned> next_serial{0};
   int flag_host = 0;
   WriteValue32Fn write32 = nullptr;
-  WriteValue64Fn write64 = nullptr;
 
   std::vector<std::unique_ptr<Launch>> launches;
   std::vector<int> free_launch_ids;

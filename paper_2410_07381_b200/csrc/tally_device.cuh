@@ -72,6 +72,7 @@ struct PtbArgs {
   long long preempt_at;            // test trigger: raise flag when counter reaches this (-1 off)
   uint3 grid;                      // logical grid
   unsigned long long* exec_count;  // optional exactly-once counters [total]
+  unsigned long long* worker_log;  // optional [workers * 4] per-worker telemetry
 };
 
 __device__ __forceinline__ unsigned long long globaltimer() {
@@ -172,38 +173,65 @@ __device__ __forceinline__ void ptb_worker_exit(const PtbArgs& a, bool stopped,
   }
 }
 
+// One claim by the leader thread: check the flag first, then fetch-and-add
+// the task counter (ref transforms.py:343-351).  Returns -1 on preemption.
+__device__ __forceinline__ long long ptb_claim(const PtbArgs& a) {
+  const unsigned f = a.flag_is_host ? ld_acquire_sys(a.flag) : ld_acquire_gpu(a.flag);
+  if (f == a.serial) return -1;   // flag gates the claim: a parked launch never over-claims
+  const unsigned long long c = atomicAdd(&a.rec->claims, 1ull);
+  const long long task = (long long)(a.start + c);
+  if (a.preempt_at >= 0 && task + 1 == a.preempt_at)
+    st_release_sys(const_cast<unsigned*>(a.flag), a.serial);   // test trigger (MemTrigger)
+  if (a.exec_count != nullptr && (unsigned long long)task < a.total)
+    atomicAdd(&a.exec_count[task], 1ull);
+  return task;
+}
+
+__device__ __forceinline__ unsigned smid() {
+  unsigned r;
+  asm volatile("mov.u32 %0, %%smid;" : "=r"(r));
+  return r;
+}
+
+// Persistent worker loop.  The leader claims task i+1 while the CTA executes
+// task i (claim-ahead), so the flag load and the L2 atomic overlap the body
+// instead of serialising with it; a claimed task is always executed, so on
+// preemption a worker retires after at most its current and its pre-claimed
+// logical block.
 template <class Body>
 __global__ void __launch_bounds__(Body::kThreads)
 k_ptb(const typename Body::Params p, const PtbArgs a) {
   extern __shared__ __align__(1024) char smem[];
-  __shared__ long long s_task;
+  __shared__ long long s_task[2];
   const bool leader = (threadIdx.x == 0);
   const unsigned long long t_entry = leader ? globaltimer() : 0ull;
   bool stopped = false;
-  for (;;) {
-    if (leader) {
-      long long task = -1;
-      const unsigned f = a.flag_is_host ? ld_acquire_sys(a.flag) : ld_acquire_gpu(a.flag);
-      if (f != a.serial) {  // flag gates the claim: a parked launch never over-claims
-        const unsigned long long c = atomicAdd(&a.rec->claims, 1ull);
-        task = (long long)(a.start + c);
-        if (a.preempt_at >= 0 && task + 1 == a.preempt_at)
-          st_release_sys(const_cast<unsigned*>(a.flag), a.serial);   // test trigger
-        if (a.exec_count != nullptr && (unsigned long long)task < a.total)
-          atomicAdd(&a.exec_count[task], 1ull);
-      }
-      s_task = task;
-    }
-    __syncthreads();
-    const long long task = s_task;
+  unsigned long long done = 0;
+  long long next = 0;
+  if (leader) s_task[0] = ptb_claim(a);
+  __syncthreads();
+  for (unsigned it = 0;; ++it) {
+    const long long task = s_task[it & 1];
     if (task < 0 || (unsigned long long)task >= a.total) {
       stopped = task < 0;
       break;
     }
+    if (leader) next = ptb_claim(a);   // in flight while the body runs
     Body::run(p, delinearize((unsigned long long)task, a.grid), a.grid, smem);
+    ++done;
+    if (leader) s_task[(it + 1) & 1] = next;
     __syncthreads();
   }
-  if (leader) ptb_worker_exit(a, stopped, t_entry);
+  if (leader) {
+    if (a.worker_log != nullptr) {
+      unsigned long long* w = a.worker_log + 4ull * blockIdx.x;
+      w[0] = ((unsigned long long)smid() << 32) | (done & 0xffffffffull);
+      w[1] = t_entry;
+      w[2] = globaltimer();
+      w[3] = stopped ? 1ull : 0ull;
+    }
+    ptb_worker_exit(a, stopped, t_entry);
+  }
 }
 
 }  // namespace tally

@@ -189,10 +189,14 @@ class DeviceKernel:
         return self._launch(stream, d)
 
     def ptb(self, stream: Stream, workers: int, start_count: int = 0, preempt_at=None,
-            exec_count=None, timed=False) -> Launch:
+            exec_count=None, timed=False, worker_log=None) -> Launch:
+        """``worker_log``: optional int64 CUDA tensor [workers, 4] receiving per
+        worker ``(smid << 32 | blocks done, t_entry, t_exit, stopped)`` on the
+        device %globaltimer clock."""
         d = _lib.c_launch_desc(shape=_lib.SHAPE_PTB, workers=workers, start_count=start_count,
                                preempt_at=-1 if preempt_at is None else preempt_at,
-                               exec_count=_ptr(exec_count), timed=int(timed))
+                               exec_count=_ptr(exec_count), worker_log=_ptr(worker_log),
+                               timed=int(timed))
         return self._launch(stream, d)
 
     def cost(self, block_duration_ns: int = 0, launch_overhead_ns: int = DEFAULT_LAUNCH_OVERHEAD_NS,
@@ -230,3 +234,51 @@ def rowsum_f32(x, out) -> DeviceKernel:
 def kind_names():
     n = _lib.lib.tally_kernel_kind_count()
     return [_lib.lib.tally_kernel_kind_name(i).decode() for i in range(n)]
+
+
+class Sgemm3xTf32:
+    """C[M,N] = A[M,K] . B[N,K]^T in fp32 accuracy on the tensor cores.
+
+    Three device kernels: ``split_a`` / ``split_b`` (``split_tf32``: x -> tf32
+    hi + fp32 remainder, HBM bound) and ``gemm`` (``sgemm_tf32x3``: tcgen05
+    kind::tf32, Ahi.Bhi + Ahi.Blo + Alo.Bhi in fp32 TMEM).  ``pipeline`` lists
+    them in order -- one BE training "step" of the SGEMM workload.
+    """
+
+    def __init__(self, A, B, C):
+        import torch
+        M, K = A.shape
+        N, K2 = B.shape
+        if K != K2 or tuple(C.shape) != (M, N):
+            raise ValueError("sgemm_tf32x3: shapes must be A[M,K], B[N,K], C[M,N]")
+        if A.dtype != torch.float32 or B.dtype != torch.float32 or C.dtype != torch.float32:
+            raise ValueError("sgemm_tf32x3: fp32 operands")
+        self.a_hi, self.a_lo = torch.empty_like(A), torch.empty_like(A)
+        self.b_hi, self.b_lo = torch.empty_like(B), torch.empty_like(B)
+        self.split_a = DeviceKernel("split_tf32", (A, self.a_hi, self.a_lo), (A.numel(),))
+        self.split_b = DeviceKernel("split_tf32", (B, self.b_hi, self.b_lo), (B.numel(),))
+        self.gemm = DeviceKernel("sgemm_tf32x3", (self.a_hi, self.a_lo, self.b_hi, self.b_lo, C),
+                                 (M, N, K))
+        self.pipeline = (self.split_a, self.split_b, self.gemm)
+
+    def prepare(self, stream: Stream):
+        """Run the two splits (Original shape) and wait."""
+        self.split_a.original(stream).wait()
+        self.split_b.original(stream).wait()
+
+    def close(self):
+        for k in self.pipeline:
+            k.close()
+
+
+def sgemm_tf32x3(A, B, C) -> Sgemm3xTf32:
+    return Sgemm3xTf32(A, B, C)
+
+
+def gemm_bf16(A, B, C) -> DeviceKernel:
+    """C[M,N] (bf16) = A[M,K] . B[N,K]^T, bf16 operands, fp32 accumulation."""
+    M, K = A.shape
+    N, K2 = B.shape
+    if K != K2 or tuple(C.shape) != (M, N):
+        raise ValueError("gemm_bf16: shapes must be A[M,K], B[N,K], C[M,N]")
+    return DeviceKernel("gemm_bf16", (A, B, C), (M, N, K))

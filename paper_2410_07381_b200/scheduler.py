@@ -222,7 +222,8 @@ class PolicyRunner:
     """Drives one device with one policy over a task set (ref scheduler.py:164-222)."""
 
     def __init__(self, gpu, tasks, config: SchedulerConfig, horizon_ns: int, profiler=None,
-                 placement_seed: int = 0, record_events: bool = True, device_factory=None):
+                 placement_seed: int = 0, record_events: bool = True, device_factory=None,
+                 options=None):
         if len({t.task_id for t in tasks}) != len(tasks):
             raise ValueError("duplicate task ids")
         self.gpu = gpu
@@ -232,6 +233,7 @@ class PolicyRunner:
         self.placement_seed = placement_seed
         self.record_events = record_events
         self.device_factory = device_factory
+        self.options = dict(options or {})
         self.profiler = profiler if profiler is not None else Profiler(
             gpu, device_factory=device_factory)
 
@@ -263,6 +265,8 @@ class PolicyRunner:
                                            C.byref(rid)), "runner")
         rid = rid.value
         try:
+            for k, v in self.options.items():
+                _lib.check(lib.tally_runner_set_option(rid, k.encode(), int(v)), f"option {k}")
             keep = []
             for t in self.tasks:
                 works = (_lib.c_work * len(t.kernels))(*[self._work(w, t) for w in t.kernels])
@@ -331,8 +335,9 @@ class PolicyRunner:
 
 def run_policy(gpu, tasks, config: SchedulerConfig, horizon_ns: int, profiler=None,
                placement_seed: int = 0, record_events: bool = True,
-               device_factory=None) -> RunResult:
-    """ref scheduler.py:444-457."""
+               device_factory=None, options=None) -> RunResult:
+    """ref scheduler.py:444-457.  ``options`` (B200 only): {"trace": 1} adds
+    GPU-timeline timestamps to ``RunResult.launches``; {"hp_streams": n}."""
     return PolicyRunner(gpu, tasks, config, horizon_ns, profiler=profiler,
                         placement_seed=placement_seed, record_events=record_events,
-                        device_factory=device_factory).run()
+                        device_factory=device_factory, options=options).run()

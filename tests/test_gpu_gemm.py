@@ -1,0 +1,109 @@
+"""tcgen05 GEMM kernels in all three Tally shapes.  Needs a B200.
+
+Tolerances (north star): fp32 (3xTF32) within 1e-5 relative, bf16 within 1e-2,
+both normwise against a float64 reference of the same inputs:
+    max|C - C_ref| / max|C_ref|
+and every shape bit-identical to the untransformed (Original) kernel.
+"""
+
+from fractions import Fraction
+
+import pytest
+
+torch = pytest.importorskip("torch")
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module")
+def env():
+    if not torch.cuda.is_available():
+        pytest.skip("no GPU")
+    import paper_2410_07381_b200 as P
+    from paper_2410_07381_b200 import kernels
+    P.B200Device.get(0)
+    return P, kernels, kernels.Stream(high_priority=False)
+
+
+def _run_shapes(P, dk, stream, out, total):
+    results = {}
+    for shape in ("original", "sliced", "ptb"):
+        out.zero_()
+        ec = torch.zeros(total, dtype=torch.int64, device="cuda")
+        if shape == "original":
+            dk.original(stream, exec_count=ec).wait()
+        elif shape == "sliced":
+            for off, cnt in P.slice_plan(total, Fraction(1, 5)):
+                dk.sliced(stream, off, cnt, exec_count=ec).wait()
+        else:
+            dk.ptb(stream, 148, exec_count=ec).wait()
+        assert bool((ec == 1).all()), shape
+        results[shape] = out.clone()
+    return results
+
+
+@pytest.mark.parametrize("mnk", [(256, 128, 64), (512, 384, 1024), (1024, 1024, 4096)])
+def test_sgemm_tf32x3_fp32_accuracy_all_shapes(env, mnk):
+    P, kernels, stream = env
+    M, N, K = mnk
+    g = torch.Generator(device="cuda").manual_seed(M + N + K)
+    A = torch.rand(M, K, device="cuda", generator=g) * 2 - 1
+    B = torch.rand(N, K, device="cuda", generator=g) * 2 - 1
+    C = torch.zeros(M, N, device="cuda")
+    sg = kernels.sgemm_tf32x3(A, B, C)
+    sg.prepare(stream)
+    # the split is exact: hi + lo == x
+    assert torch.equal(sg.a_hi + sg.a_lo, A) and torch.equal(sg.b_hi + sg.b_lo, B)
+    res = _run_shapes(P, sg.gemm, stream, C, sg.gemm.total_blocks)
+    ref = A.double() @ B.double().T
+    err = ((res["original"].double() - ref).abs().max() / ref.abs().max()).item()
+    assert err < 1e-5, err
+    assert torch.equal(res["original"], res["sliced"]) and torch.equal(res["original"], res["ptb"])
+    sg.close()
+
+
+@pytest.mark.parametrize("mnk", [(256, 256, 128), (1024, 768, 2048)])
+def test_gemm_bf16_all_shapes(env, mnk):
+    P, kernels, stream = env
+    M, N, K = mnk
+    g = torch.Generator(device="cuda").manual_seed(M * 3 + K)
+    A = (torch.rand(M, K, device="cuda", generator=g) * 2 - 1).bfloat16()
+    B = (torch.rand(N, K, device="cuda", generator=g) * 2 - 1).bfloat16()
+    C = torch.zeros(M, N, device="cuda", dtype=torch.bfloat16)
+    dk = kernels.gemm_bf16(A, B, C)
+    res = _run_shapes(P, dk, stream, C, dk.total_blocks)
+    ref = A.double() @ B.double().T
+    err = ((res["original"].double() - ref).abs().max() / ref.abs().max()).item()
+    assert err < 1e-2, err
+    assert torch.equal(res["original"], res["sliced"]) and torch.equal(res["original"], res["ptb"])
+    dk.close()
+
+
+def test_sgemm_ptb_preempt_resume_exactly_once(env):
+    P, kernels, stream = env
+    M = N = K = 2048
+    g = torch.Generator(device="cuda").manual_seed(5)
+    A = torch.rand(M, K, device="cuda", generator=g) * 2 - 1
+    B = torch.rand(N, K, device="cuda", generator=g) * 2 - 1
+    C = torch.zeros(M, N, device="cuda")
+    sg = kernels.sgemm_tf32x3(A, B, C)
+    sg.prepare(stream)
+    ref = C.clone()
+    sg.gemm.original(stream).wait()
+    ref.copy_(C)
+    C.zero_()
+    total = sg.gemm.total_blocks
+    ec = torch.zeros(total, dtype=torch.int64, device="cuda")
+    ctr, hops = 0, 0
+    for c in (37, 200, 311):
+        st = sg.gemm.ptb(stream, 148, start_count=ctr, preempt_at=c, exec_count=ec).wait()
+        assert st.task_counter >= min(c, total)
+        ctr = st.task_counter
+        hops += 1
+        if not st.parked:
+            break
+    if ctr < total:
+        sg.gemm.ptb(stream, 148, start_count=ctr, exec_count=ec).wait()
+    assert bool((ec == 1).all())
+    assert torch.equal(C, ref)
+    sg.close()

@@ -1,0 +1,216 @@
+"""On-device parity of every kernel shape (Original / Sliced / PTB) against the
+CPU oracle and the reference's golden vectors, plus exactly-once audits and
+preempt/resume exactness.  Needs a B200."""
+
+import random
+from fractions import Fraction
+
+import pytest
+
+torch = pytest.importorskip("torch")
+
+pytestmark = pytest.mark.gpu
+
+from oracle import kernel_ir as ki          # noqa: E402
+from oracle import rewrites as rw           # noqa: E402
+
+
+@pytest.fixture(scope="module")
+def P():
+    if not torch.cuda.is_available():
+        pytest.skip("no GPU")
+    import paper_2410_07381_b200 as pkg
+    from paper_2410_07381_b200 import kernels
+    pkg.B200Device.get(0)
+    pkg.kernels = kernels
+    return pkg
+
+
+@pytest.fixture(scope="module")
+def stream(P):
+    return P.kernels.Stream(high_priority=False)
+
+
+def _ir_case(gold, name):
+    return next(c for c in gold("ir")["cases"] if c["name"] == name)
+
+
+def _vecadd_kernel(P, case):
+    mem = torch.tensor(case["memory"], dtype=torch.int64, device="cuda")
+    a, b, o = case["args"]
+    n = case["kernel"]["grid"][0]
+    return mem, P.kernels.vecadd_i64(mem, a, b, o, n, elems_per_block=1)
+
+
+@pytest.mark.parametrize("name", ["vecadd", "vecadd16_wrap"])
+def test_vecadd_i64_all_shapes_match_reference_golden(P, stream, gold, name):
+    case = _ir_case(gold, name)
+    expect = case["expect"]["memory"]
+    # the oracle agrees with the golden vector
+    k = ki.kernel_from_json(case["kernel"])
+    assert list(ki.interpret(k, tuple(case["args"]), tuple(case["memory"])).memory) == expect
+    n = case["kernel"]["grid"][0]
+    runs = [("original", lambda dk, ec: [dk.original(stream, exec_count=ec)])]
+    for f in (Fraction(1, 2), Fraction(1, 4), Fraction(1, 3), Fraction(1, n)):
+        plan = P.slice_plan(n, f)
+        runs.append((f"sliced{f}", lambda dk, ec, plan=plan:
+                     [dk.sliced(stream, off, cnt, exec_count=ec) for off, cnt in plan]))
+    for w in (1, 2, 4, 8, 148):
+        runs.append((f"ptb{w}", lambda dk, ec, w=w: [dk.ptb(stream, w, exec_count=ec)]))
+    for label, go in runs:
+        mem, dk = _vecadd_kernel(P, case)
+        ec = torch.zeros(n, dtype=torch.int64, device="cuda")
+        for L in go(dk, ec):
+            L.wait()
+        assert mem.cpu().tolist() == expect, label
+        assert ec.cpu().tolist() == [1] * n, label          # exactly once
+        dk.close()
+
+
+def test_ptb_preempt_at_every_counter_then_resume(P, stream, gold):
+    """Device analogue of ref tests/test_transforms.py:185-219: raise the flag
+    when the counter reaches c (MemTrigger), resume from the persisted counter;
+    payload equals the uninterrupted run, every logical block ran exactly once."""
+    case = _ir_case(gold, "vecadd16_wrap")
+    expect = case["expect"]["memory"]
+    for workers in (1, 4, 16):
+        for c in range(0, 18):
+            mem, dk = _vecadd_kernel(P, case)
+            ec = torch.zeros(16, dtype=torch.int64, device="cuda")
+            first = dk.ptb(stream, workers, preempt_at=c, exec_count=ec).wait()
+            ctr = first.task_counter
+            assert ctr >= min(c, 16) if c > 0 else ctr >= 16
+            assert first.parked == (ctr < 16)
+            # every block below the counter ran exactly once, none above it
+            counts = ec.cpu().tolist()
+            assert counts[:min(ctr, 16)] == [1] * min(ctr, 16)
+            assert counts[min(ctr, 16):] == [0] * (16 - min(ctr, 16))
+            if first.parked:
+                second = dk.ptb(stream, workers, start_count=ctr, exec_count=ec).wait()
+                assert second.done and second.task_counter >= 16
+            assert mem.cpu().tolist() == expect, (workers, c)
+            assert ec.cpu().tolist() == [1] * 16, (workers, c)
+            dk.close()
+
+
+def test_ptb_flag_before_launch_is_noop(P, stream, gold):
+    """ref tests/test_transforms.py:174-183: preempted before any claim ->
+    counter stays at the start value and memory is untouched."""
+    case = _ir_case(gold, "vecadd")
+    mem, dk = _vecadd_kernel(P, case)
+    L = dk.ptb(stream, 4, preempt_at=None)
+    L.preempt()
+    st = L.wait()
+    # the flag races the launch; whatever was claimed ran exactly once and
+    # a resume completes the rest
+    ctr = st.task_counter
+    if st.parked:
+        dk.ptb(stream, 4, start_count=ctr).wait()
+    assert mem.cpu().tolist() == case["expect"]["memory"]
+
+
+def test_vecadd_f32_bit_exact_all_shapes(P, stream):
+    g = torch.Generator(device="cuda").manual_seed(0)
+    n = 1 << 22
+    a = torch.rand(n, device="cuda", generator=g) * 2 - 1
+    b = torch.rand(n, device="cuda", generator=g) * 2 - 1
+    ref = a + b                                  # IEEE add: exactly rounded
+    for shape in ("original", "sliced", "ptb"):
+        c = torch.full_like(a, float("nan"))
+        dk = P.kernels.vecadd_f32(a, b, c)
+        total = dk.total_blocks
+        ec = torch.zeros(total, dtype=torch.int64, device="cuda")
+        if shape == "original":
+            dk.original(stream, exec_count=ec).wait()
+        elif shape == "sliced":
+            for off, cnt in P.slice_plan(total, Fraction(1, 7)):
+                dk.sliced(stream, off, cnt, exec_count=ec).wait()
+        else:
+            dk.ptb(stream, 296, exec_count=ec).wait()
+        assert torch.equal(c, ref), shape
+        assert bool((ec == 1).all()), shape
+        dk.close()
+
+
+def test_rowsum_f32_shapes_identical_and_within_tolerance(P, stream):
+    g = torch.Generator(device="cuda").manual_seed(1)
+    for rows, cols in ((4096, 768), (1000, 1023), (8, 5)):
+        x = torch.rand(rows, cols, device="cuda", generator=g) * 2 - 1
+        outs = []
+        for shape in ("original", "sliced", "ptb"):
+            out = torch.zeros(rows, device="cuda")
+            dk = P.kernels.rowsum_f32(x, out)
+            if shape == "original":
+                dk.original(stream).wait()
+            elif shape == "sliced":
+                for off, cnt in P.slice_plan(dk.total_blocks, Fraction(1, 4)):
+                    dk.sliced(stream, off, cnt).wait()
+            else:
+                dk.ptb(stream, 148).wait()
+            outs.append(out.clone())
+            dk.close()
+        assert torch.equal(outs[0], outs[1]) and torch.equal(outs[0], outs[2])
+        ref = x.double().sum(dim=1)
+        rel = ((outs[0].double() - ref).abs().max() / ref.abs().max()).item()
+        assert rel < 1e-5, rel
+
+
+def test_random_preempts_exactly_once_at_scale(P, stream):
+    """Host-timed preemptions at random instants on a 2^26-element PTB
+    launch; every logical block executes exactly once across the chain."""
+    n = 1 << 26
+    a = torch.ones(n, device="cuda")
+    b = torch.arange(n, device="cuda", dtype=torch.float32)
+    c = torch.zeros(n, device="cuda")
+    dk = P.kernels.vecadd_f32(a, b, c)
+    total = dk.total_blocks
+    ec = torch.zeros(total, dtype=torch.int64, device="cuda")
+    rng = random.Random(7)
+    ctr, hops = 0, 0
+    while ctr < total:
+        L = dk.ptb(stream, 148 * 4, start_count=ctr, exec_count=ec)
+        t_end = P.B200Device.now_ns() + rng.randint(0, 300_000)
+        while P.B200Device.now_ns() < t_end and not L.query().done:
+            pass
+        try:
+            L.preempt()
+        except ValueError:
+            pass   # already finished
+        st = L.wait()
+        assert st.task_counter >= ctr
+        ctr = st.task_counter
+        hops += 1
+        assert hops < 1000
+    torch.cuda.synchronize()
+    assert bool((ec == 1).all())
+    assert torch.equal(c, b + 1)
+    dk.close()
+
+
+def test_preemption_latency_under_50us(P, stream):
+    """Flag write -> last worker exit, on the device clock, for a PTB launch of
+    the HP-sized vecadd (logical blocks of ~1 us)."""
+    n = 1 << 26
+    a = torch.rand(n, device="cuda")
+    b = torch.rand(n, device="cuda")
+    c = torch.zeros(n, device="cuda")
+    dk = P.kernels.vecadd_f32(a, b, c)
+    dev = P.B200Device.get()
+    off, unc = dev.clock_offset()
+    lat = []
+    for _ in range(10):
+        L = dk.ptb(stream, 148 * 4)
+        t = P.B200Device.now_ns() + 100_000
+        while P.B200Device.now_ns() < t:
+            pass
+        L.preempt()
+        st = L.wait()
+        if not st.parked:
+            continue
+        lat.append((st.gt_last_exit + off - st.host_preempt_ns) / 1000.0)
+    assert lat, "no launch was still running at the preempt instant"
+    lat.sort()
+    print(f"preempt latency us: median {lat[len(lat) // 2]:.1f} max {lat[-1]:.1f} "
+          f"(clock uncertainty {unc / 1000:.1f} us)")
+    assert lat[len(lat) // 2] < 50.0
+    dk.close()

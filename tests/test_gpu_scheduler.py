@@ -1,0 +1,74 @@
+"""Real-time co-location on the B200 through the reference-shaped API:
+HP vector-add requests at Poisson arrivals + a BE kernel loop, under every
+policy.  Needs a B200."""
+
+import pytest
+
+torch = pytest.importorskip("torch")
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module")
+def env():
+    if not torch.cuda.is_available():
+        pytest.skip("no GPU")
+    import paper_2410_07381_b200 as P
+    from paper_2410_07381_b200 import kernels, workloads
+    dev = P.B200Device.get(0)
+    g = torch.Generator(device="cuda").manual_seed(0)
+    n_hp = 1 << 22
+    ha, hb, hc = (torch.rand(n_hp, device="cuda", generator=g) for _ in range(3))
+    n_be = 1 << 26
+    ba, bb, bc = (torch.rand(n_be, device="cuda", generator=g) for _ in range(3))
+    hp = kernels.vecadd_f32(ha, hb, hc)
+    be = kernels.vecadd_f32(ba, bb, bc)
+    return P, workloads, dev, hp, be, (ha, hb, hc, ba, bb, bc)
+
+
+def _tasks(P, workloads, hp, be, horizon_ns, lat_ns):
+    arr = workloads.generate_arrivals(0.3, lat_ns, horizon_ns, seed=1)
+    hp_w = P.KernelWork("vadd_hp", hp.cost(), kernel=hp)
+    be_w = P.KernelWork("vadd_be", be.cost(), kernel=be)
+    return [P.TaskScript("hp", P.HIGH, (hp_w,), arr), P.TaskScript("be", P.BEST_EFFORT, (be_w,))], arr
+
+
+@pytest.mark.parametrize("policy", ["Tally", "KernelPriority", "Eager", "TimeSliced"])
+def test_colocation_runs_every_policy(env, policy):
+    P, workloads, dev, hp, be, bufs = env
+    prof = P.Profiler(dev.spec, runs=3)
+    horizon = 60_000_000
+    tasks, arr = _tasks(P, workloads, hp, be, horizon, 200_000)
+    res = P.run_policy(dev.spec, tasks, P.SchedulerConfig(policy=policy), horizon, profiler=prof)
+    assert len(res.requests["hp"]) == len(arr)
+    assert res.iterations["be"], "best-effort made no progress"
+    lat = sorted(c - a for a, c in res.requests["hp"])
+    assert lat[0] > 0
+    kinds = {e.kind for e in res.events}
+    assert "LaunchIssued" in kinds and "KernelFinished" in kinds
+    if policy == "Tally":
+        ptb = [r for r in res.launches if r["shape"] == 2]
+        cfg = prof.select(tasks[1].kernels[0].profile_key(), tasks[1].kernels[0].cost)
+        if cfg.variant == "Ptb":
+            assert ptb and any(r["parked"] for r in ptb)
+    torch.cuda.synchronize()
+    ha, hb, hc, ba, bb, bc = bufs
+    assert torch.equal(hc, ha + hb)
+    assert torch.equal(bc, ba + bb)
+
+
+def test_tally_keeps_hp_tail_close_to_solo(env):
+    P, workloads, dev, hp, be, bufs = env
+    prof = P.Profiler(dev.spec, runs=3)
+    horizon = 150_000_000
+    tasks, arr = _tasks(P, workloads, hp, be, horizon, 200_000)
+    cfg = P.SchedulerConfig(policy="Tally", turnaround_threshold_ns=60_000)
+    solo = P.run_policy(dev.spec, tasks[:1], cfg, horizon, profiler=prof, record_events=False)
+    co = P.run_policy(dev.spec, tasks, cfg, horizon, profiler=prof, record_events=False)
+    p99 = workloads.p99_nearest_rank
+    s = p99([c - a for a, c in solo.requests["hp"]])
+    c = p99([c - a for a, c in co.requests["hp"]])
+    print(f"solo p99 {s / 1e3:.1f} us, co-located p99 {c / 1e3:.1f} us, "
+          f"BE iterations {len(co.iterations['be'])}")
+    assert co.iterations["be"]
+    assert c < 4 * s + 100_000
