@@ -15,6 +15,7 @@
 
 #include <algorithm>
 #include <cstring>
+#include <deque>
 #include <map>
 #include <queue>
 #include <vector>
@@ -38,6 +39,7 @@ struct Handle {
   long long gt_first_start = 0, gt_first_stop = 0, gt_last_exit = 0;
   long long count = 0;
   long long gpu_start = -1, gpu_end = -1;
+  int hp_slot = -1;
 };
 
 class CudaDevice : public Device {
@@ -51,6 +53,7 @@ class CudaDevice : public Device {
       int s;
       if (tally_stream_create(TALLY_HIGH, &s) != TALLY_OK) throw Error(TALLY_ECUDA, "HP stream");
       hp_streams_.push_back(s);
+      hp_load_.push_back(0);
     }
     if (trace_) {
       cudaEventCreate(&ref_);
@@ -151,18 +154,24 @@ class CudaDevice : public Device {
       }
       park_unissued_.clear();
       if (inflight_ > 0) {
-        for (size_t i = 0; i < hs_.size(); ++i) {
-          Handle& h = hs_[i];
-          if (!h.issued || h.finished) continue;
+        // poll in submission order; complete() may submit (appending to live_)
+        const size_t n = live_.size();
+        for (size_t k = 0; k < n; ++k) {
+          const long long id = live_[k];
+          Handle& h = hs_[(size_t)id];
+          if (h.finished) continue;
           Launch* L = rt().get_launch(h.launch);
           if (!L) throw Error(TALLY_ECUDA, "lost launch");
           if (!rt().poll(L)) {
             if (L->error != cudaSuccess) throw Error(TALLY_ECUDA, cudaGetErrorString(L->error));
             continue;
           }
-          complete((long long)i, L);
+          complete(id, L);
           progress = true;
         }
+        live_.erase(std::remove_if(live_.begin(), live_.end(),
+                                   [this](long long id) { return hs_[(size_t)id].finished; }),
+                    live_.end());
       }
       if (!pending_.empty()) { dispatch(); }
       if (!progress) spin_pause();
@@ -178,7 +187,8 @@ class CudaDevice : public Device {
   Runner* r_;
   long long t0_ = 0, seq_ = 0, last_fired_ = 0;
   std::priority_queue<Tm> timers_;
-  std::vector<Handle> hs_;
+  std::deque<Handle> hs_;          // deque: references stay valid across submit()
+  std::vector<long long> live_;    // issued, not yet observed finished
   std::vector<long long> pending_, park_unissued_;
   int inflight_ = 0;
   bool filter_ = false;
@@ -187,6 +197,7 @@ class CudaDevice : public Device {
   cudaEvent_t ref_ = nullptr;
   int hp_rr_ = 0;
   std::vector<int> hp_streams_;
+  std::vector<int> hp_load_;   // in-flight launches per HP stream
   std::map<int, int> be_streams_;
 
   static void spin_pause() {
@@ -273,8 +284,18 @@ class CudaDevice : public Device {
     int stream;
     ld.timed = trace_ ? 1 : 0;
     if (h.d.priority == TALLY_HIGH) {
-      stream = hp_streams_[(size_t)hp_rr_];
-      hp_rr_ = (hp_rr_ + 1) % (int)hp_streams_.size();
+      // an idle high-priority stream if there is one (no head-of-line blocking
+      // behind another request), else the least loaded
+      size_t best = 0;
+      for (size_t k = 0; k < hp_streams_.size(); ++k) {
+        const size_t c = (hp_rr_ + k) % hp_streams_.size();
+        if (hp_load_[c] < hp_load_[best] || (k == 0)) best = c;
+        if (hp_load_[c] == 0) { best = c; break; }
+      }
+      hp_rr_ = (int)((best + 1) % hp_streams_.size());
+      h.hp_slot = (int)best;
+      ++hp_load_[best];
+      stream = hp_streams_[best];
     } else {
       stream = be_stream(h.d.task);
     }
@@ -285,12 +306,14 @@ class CudaDevice : public Device {
     h.issued = true;
     h.issue_ns = now();
     ++inflight_;
+    live_.push_back(id);
     if (h.preempted) tally_preempt(lid);
   }
 
   void complete(long long id, Launch* L) {
     Handle& h = hs_[(size_t)id];
     h.finished = true;
+    if (h.hp_slot >= 0) --hp_load_[(size_t)h.hp_slot];
     h.parked = L->parked;
     h.complete_ns = now();
     h.finish_time = h.complete_ns;

@@ -171,6 +171,7 @@ struct alignas(64) GemmParams {
   void* c;
   int m, n, k;
   int tiles_m, tiles_n;
+  int kchunk;   // k-blocks per TMEM accumulation chunk (promotion to fp32 registers)
 };
 
 __device__ __forceinline__ void tile_coords(long long t, const GemmParams& p, int& mb, int& nb) {
@@ -269,47 +270,54 @@ __global__ void __launch_bounds__(kThreads, 1) k_gemm(const __grid_constant__ Ge
   } else if (warp == 1) {
     if (lane == 0) {
       // ------------------------------------------------ MMA issuer
+      // The tile's K range is cut into chunks of p.kchunk k-blocks; each chunk
+      // accumulates into one of two TMEM buffers and is promoted to fp32
+      // registers by the epilogue (bounded tensor-core accumulation chains).
       constexpr uint32_t idesc = make_idesc<Cfg::KIND, Cfg::BN>();
-      uint32_t it = 0;
+      uint32_t it = 0, ci = 0;
       for (int i = 0;; ++i) {
         const int j = i & 1;
         mbar_wait(&tile_full[j], (i >> 1) & 1);
         const long long t = tile_slot[j];
         mbar_arrive(&tile_empty[j]);
         if (t < 0) break;
-        const int acc = i & 1;
-        if (i >= 2) mbar_wait(&tmem_empty[acc], ((i >> 1) - 1) & 1);
-        fence_after();
-        const uint32_t d = tmem_base + (uint32_t)(acc * Cfg::BN);
-        for (int kb = 0; kb < KB; ++kb, ++it) {
-          const int st = it % Cfg::STAGES;
-          mbar_wait(&full[st], (it / Cfg::STAGES) & 1);
+        for (int kb0 = 0; kb0 < KB; kb0 += p.kchunk, ++ci) {
+          const int acc = ci & 1;
+          if (ci >= 2) mbar_wait(&tmem_empty[acc], ((ci >> 1) - 1) & 1);
           fence_after();
-          const unsigned char* base = smem + (size_t)st * Cfg::STAGE_BYTES;
+          const uint32_t d = tmem_base + (uint32_t)(acc * Cfg::BN);
+          const int kb1 = min(KB, kb0 + p.kchunk);
+          for (int kb = kb0; kb < kb1; ++kb, ++it) {
+            const int st = it % Cfg::STAGES;
+            mbar_wait(&full[st], (it / Cfg::STAGES) & 1);
+            fence_after();
+            const unsigned char* base = smem + (size_t)st * Cfg::STAGE_BYTES;
 #pragma unroll
-          for (int k = 0; k < Cfg::BK / Cfg::UMMA_K; ++k) {
-            const uint32_t first = (kb | k) != 0;
-            const int koff = k * Cfg::UMMA_K * Cfg::ESZ;   // 32 B per MMA-K step inside the atom
-            if constexpr (Cfg::KIND == 0) {
-              const uint64_t ahi = smem_desc(base + koff), alo = smem_desc(base + Cfg::A_BYTES + koff);
-              const uint64_t bhi = smem_desc(base + 2 * Cfg::A_BYTES + koff);
-              const uint64_t blo = smem_desc(base + 2 * Cfg::A_BYTES + Cfg::B_BYTES + koff);
-              umma<0>(d, alo, bhi, idesc, first);   // small terms first
-              umma<0>(d, ahi, blo, idesc, 1);
-              umma<0>(d, ahi, bhi, idesc, 1);
-            } else {
-              umma<1>(d, smem_desc(base + koff), smem_desc(base + Cfg::A_BYTES + koff), idesc, first);
+            for (int k = 0; k < Cfg::BK / Cfg::UMMA_K; ++k) {
+              const uint32_t first = (kb != kb0 || k != 0);
+              const int koff = k * Cfg::UMMA_K * Cfg::ESZ;   // 32 B per MMA-K step inside the atom
+              if constexpr (Cfg::KIND == 0) {
+                const uint64_t ahi = smem_desc(base + koff), alo = smem_desc(base + Cfg::A_BYTES + koff);
+                const uint64_t bhi = smem_desc(base + 2 * Cfg::A_BYTES + koff);
+                const uint64_t blo = smem_desc(base + 2 * Cfg::A_BYTES + Cfg::B_BYTES + koff);
+                umma<0>(d, alo, bhi, idesc, first);   // small terms first
+                umma<0>(d, ahi, blo, idesc, 1);
+                umma<0>(d, ahi, bhi, idesc, 1);
+              } else {
+                umma<1>(d, smem_desc(base + koff), smem_desc(base + Cfg::A_BYTES + koff), idesc, first);
+              }
             }
+            umma_commit(&empty[st]);   // frees the stage once these MMAs retire
           }
-          umma_commit(&empty[st]);   // frees the stage once these MMAs retire
+          umma_commit(&tmem_full[acc]);
         }
-        umma_commit(&tmem_full[acc]);
       }
     }
     __syncwarp();
   } else {
     // -------------------------------------------------- epilogue (warps 2..5)
     const int q = warp & 3;   // TMEM lane quarter this warp may access
+    uint32_t ci = 0;
     for (int i = 0;; ++i) {
       const int j = i & 1;
       mbar_wait(&tile_full[j], (i >> 1) & 1);
@@ -319,39 +327,44 @@ __global__ void __launch_bounds__(kThreads, 1) k_gemm(const __grid_constant__ Ge
       if (t < 0) break;
       int mb, nb;
       tile_coords(t, p, mb, nb);
-      const int acc = i & 1;
-      mbar_wait(&tmem_full[acc], (i >> 1) & 1);
-      fence_after();
+      float sum[Cfg::BN];
+#pragma unroll
+      for (int c = 0; c < Cfg::BN; ++c) sum[c] = 0.f;
+      for (int kb0 = 0; kb0 < KB; kb0 += p.kchunk, ++ci) {
+        const int acc = ci & 1;
+        mbar_wait(&tmem_full[acc], (ci >> 1) & 1);
+        fence_after();
+#pragma unroll
+        for (int c0 = 0; c0 < Cfg::BN; c0 += 32) {
+          uint32_t r[32];
+          tmem_ld32(tmem_base + ((uint32_t)(q * 32) << 16) + (uint32_t)(acc * Cfg::BN + c0), r);
+#pragma unroll
+          for (int e = 0; e < 32; ++e) sum[c0 + e] += __uint_as_float(r[e]);
+        }
+        fence_before();
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&tmem_empty[acc]);
+      }
       const int row = mb * Cfg::BM + q * 32 + lane;
       typename Cfg::OutT* crow = reinterpret_cast<typename Cfg::OutT*>(p.c) + (size_t)row * p.n + (size_t)nb * Cfg::BN;
+      if constexpr (Cfg::KIND == 0) {
+        float4* dst = reinterpret_cast<float4*>(crow);
 #pragma unroll
-      for (int c0 = 0; c0 < Cfg::BN; c0 += 32) {
-        uint32_t r[32];
-        tmem_ld32(tmem_base + ((uint32_t)(q * 32) << 16) + (uint32_t)(acc * Cfg::BN + c0), r);
-        if constexpr (Cfg::KIND == 0) {
-          float4* dst = reinterpret_cast<float4*>(crow + c0);
+        for (int v = 0; v < Cfg::BN / 4; ++v)
+          dst[v] = make_float4(sum[4 * v], sum[4 * v + 1], sum[4 * v + 2], sum[4 * v + 3]);
+      } else {
+        uint4* dst = reinterpret_cast<uint4*>(crow);
 #pragma unroll
-          for (int v = 0; v < 8; ++v)
-            dst[v] = make_float4(__uint_as_float(r[4 * v]), __uint_as_float(r[4 * v + 1]),
-                                 __uint_as_float(r[4 * v + 2]), __uint_as_float(r[4 * v + 3]));
-        } else {
-          uint4* dst = reinterpret_cast<uint4*>(crow + c0);
+        for (int v = 0; v < Cfg::BN / 8; ++v) {
+          uint32_t w[4];
 #pragma unroll
-          for (int v = 0; v < 4; ++v) {
-            uint32_t w[4];
-#pragma unroll
-            for (int e = 0; e < 4; ++e) {
-              __nv_bfloat162 h = __floats2bfloat162_rn(__uint_as_float(r[8 * v + 2 * e]),
-                                                       __uint_as_float(r[8 * v + 2 * e + 1]));
-              w[e] = *reinterpret_cast<uint32_t*>(&h);
-            }
-            dst[v] = make_uint4(w[0], w[1], w[2], w[3]);
+          for (int e = 0; e < 4; ++e) {
+            __nv_bfloat162 h = __floats2bfloat162_rn(sum[8 * v + 2 * e], sum[8 * v + 2 * e + 1]);
+            w[e] = *reinterpret_cast<uint32_t*>(&h);
           }
+          dst[v] = make_uint4(w[0], w[1], w[2], w[3]);
         }
       }
-      fence_before();
-      __syncwarp();
-      if (lane == 0) mbar_arrive(&tmem_empty[acc]);
     }
   }
 
@@ -471,6 +484,9 @@ static int bind_gemm(const tally_kernel_args* a, Instance* inst, bool split) {
   p.k = (int)K;
   p.tiles_m = (int)(M / Cfg::BM);
   p.tiles_n = (int)(N / Cfg::BN);
+  // promote the tensor-core accumulator to fp32 registers every 512 of K for
+  // the fp32-accuracy kernel; bf16 (1e-2 budget) accumulates the whole K in TMEM
+  p.kchunk = Cfg::KIND == 0 ? 512 / Cfg::BK : (int)(K / Cfg::BK);
   static_assert(sizeof(p) <= kMaxParamBytes, "params too large");
   memcpy(inst->params, &p, sizeof(p));
   inst->grid = make_uint3((unsigned)(p.tiles_m * p.tiles_n), 1, 1);

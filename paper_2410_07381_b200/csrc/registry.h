@@ -37,6 +37,16 @@ struct KernelKind {
   int (*bind)(const tally_kernel_args* a, Instance* inst);
   // Optional one-time setup (e.g. smem attribute) -- may be null.
   int (*setup)();
+  // 1: not a kernel but a host<->device copy (cudaMemcpyAsync on the launch
+  // stream) -- the data-movement steps of an end-to-end request pipeline.
+  // Copies are exempt from transformation: Original shape only.
+  int copy;
+};
+
+struct CopyParams {
+  void* dst;
+  const void* src;
+  long long bytes;
 };
 
 void set_error(const char* fmt, ...);
@@ -45,5 +55,6 @@ int cuda_fail(cudaError_t e, const char* what);
 // Registration hooks implemented by each kernel translation unit.
 int register_basic_kernels(KernelKind* out, int cap);
 int register_gemm_kernels(KernelKind* out, int cap);
+int register_copy_kernels(KernelKind* out, int cap);
 
 }  // namespace tally

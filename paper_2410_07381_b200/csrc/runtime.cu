@@ -92,6 +92,7 @@ int Runtime::init(int dev, tally_gpu_info* out) {
 
   nkinds = register_basic_kernels(kinds, kMaxKinds);
   nkinds += register_gemm_kernels(kinds + nkinds, kMaxKinds - nkinds);
+  nkinds += register_copy_kernels(kinds + nkinds, kMaxKinds - nkinds);
   for (int k = 0; k < nkinds; ++k)
     if (kinds[k].setup) {
       int rc = kinds[k].setup();
@@ -169,19 +170,15 @@ int Runtime::clock_offset(long long* off, long long* unc) {
 }
 
 int Runtime::alloc_rec(int* out) {
-  if (free_recs.empty()) {
-    // reclaim records of launches whose kernel has fully exited
-    for (auto it = zombies.begin(); it != zombies.end();) {
-      if (cudaEventQuery(it->second) == cudaSuccess) {
-        free_recs.push_back(it->first);
-        release_event(it->second);
-        it = zombies.erase(it);
-      } else {
-        ++it;
-      }
-    }
-    cudaGetLastError();
+  // Reclaim records of launches whose kernel has fully exited, oldest first
+  // and only while they are done: O(1) amortised, no scan stalls the daemon.
+  while (!zombies.empty() && (free_recs.empty() || zombies.size() > 64)) {
+    if (cudaEventQuery(zombies.front().second) != cudaSuccess) break;
+    free_recs.push_back(zombies.front().first);
+    release_event(zombies.front().second);
+    zombies.pop_front();
   }
+  cudaGetLastError();
   if (free_recs.empty()) { set_error("out of PTB launch records"); return TALLY_EBUSY; }
   *out = free_recs.back();
   free_recs.pop_back();
@@ -236,6 +233,40 @@ int Runtime::launch(int kernel, int stream, const tally_launch_desc* d, int* out
   const void* fn = nullptr;
   dim3 grid;
   void* args[2] = {const_cast<unsigned char*>(in.params), nullptr};
+
+  if (kk.copy) {
+    if (d->shape != TALLY_SHAPE_ORIGINAL) {
+      set_error("%s: copies are exempt from slicing / preemption (Original shape only)", kk.name);
+      return TALLY_ETRANSFORM;
+    }
+    CopyParams cp;
+    memcpy(&cp, in.params, sizeof(cp));
+    L->count = 1;
+    if (L->timed) {
+      L->ev_start = get_event(true);
+      cudaEventRecord(L->ev_start, st);
+    }
+    cudaError_t e = cudaMemcpyAsync(cp.dst, cp.src, (size_t)cp.bytes, cudaMemcpyDefault, st);
+    if (e != cudaSuccess) {
+      release_event(L->ev_start);
+      return cuda_fail(e, kk.name);
+    }
+    L->ev_end = get_event(L->timed);
+    cudaEventRecord(L->ev_end, st);
+    L->active = true;
+    std::lock_guard<std::mutex> g(mu);
+    int id;
+    if (!free_launch_ids.empty()) {
+      id = free_launch_ids.back();
+      free_launch_ids.pop_back();
+      launches[id] = std::move(L);
+    } else {
+      id = (int)launches.size();
+      launches.push_back(std::move(L));
+    }
+    *out = id;
+    return TALLY_OK;
+  }
 
   switch (d->shape) {
     case TALLY_SHAPE_ORIGINAL:
@@ -415,6 +446,32 @@ int Runtime::release(int id) {
   return TALLY_OK;
 }
 
+static int bind_memcpy(const tally_kernel_args* a, Instance* inst) {
+  CopyParams p;
+  p.dst = a->ptr[0];
+  p.src = a->ptr[1];
+  p.bytes = a->i[0];
+  if (!p.dst || !p.src || p.bytes < 1) {
+    set_error("memcpy: need dst, src and bytes >= 1");
+    return TALLY_EINVAL;
+  }
+  memcpy(inst->params, &p, sizeof(p));
+  inst->grid = make_uint3(1, 1, 1);
+  inst->threads = 1;
+  inst->alg_bytes = (double)p.bytes;
+  return TALLY_OK;
+}
+
+int register_copy_kernels(KernelKind* out, int cap) {
+  if (cap < 1) return 0;
+  KernelKind k{};
+  k.name = "memcpy";
+  k.bind = bind_memcpy;
+  k.copy = 1;
+  out[0] = k;
+  return 1;
+}
+
 }  // namespace tally
 
 using namespace tally;
@@ -460,7 +517,8 @@ int tally_kernel_kind_count(void) {
     // registry is static; allow listing without a device
     KernelKind tmp[Runtime::kMaxKinds];
     int n = register_basic_kernels(tmp, Runtime::kMaxKinds);
-    return n + register_gemm_kernels(tmp + n, Runtime::kMaxKinds - n);
+    n += register_gemm_kernels(tmp + n, Runtime::kMaxKinds - n);
+    return n + register_copy_kernels(tmp + n, Runtime::kMaxKinds - n);
   }
   return r.nkinds;
 }
@@ -471,6 +529,7 @@ const char* tally_kernel_kind_name(int kind) {
   if (n < 0) {
     n = register_basic_kernels(tmp, Runtime::kMaxKinds);
     n += register_gemm_kernels(tmp + n, Runtime::kMaxKinds - n);
+    n += register_copy_kernels(tmp + n, Runtime::kMaxKinds - n);
   }
   if (kind < 0 || kind >= n) return nullptr;
   return tmp[kind].name;
@@ -512,6 +571,7 @@ int tally_kernel_info_get(int kernel, tally_kernel_info* o) {
   o->alg_bytes = in.alg_bytes;
   o->alg_flops = in.alg_flops;
   int occ = 0;
+  if (kk.copy) return TALLY_OK;
   CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kk.fn_ptb, in.threads, in.smem), "occupancy");
   o->occupancy_ptb = occ;
   CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kk.fn_original, in.threads, in.smem), "occupancy");

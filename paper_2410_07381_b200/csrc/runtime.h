@@ -4,6 +4,7 @@
 #include <cuda_runtime.h>
 
 #include <atomic>
+#include <deque>
 #include <memory>
 #include <mutex>
 #include <unordered_map>
@@ -59,7 +60,7 @@ struct Runtime {
   volatile unsigned long long* h_stamp = nullptr;
   unsigned long long* d_stamp = nullptr;
   std::vector<int> free_recs;
-  std::vector<std::pair<int, cudaEvent_t>> zombies;
+  std::deque<std::pair<int, cudaEvent_t>> zombies;
   std::atomic<unsigned> next_serial{0};
   int flag_host = 0;
   WriteValue32Fn write32 = nullptr;

@@ -282,3 +282,13 @@ def gemm_bf16(A, B, C) -> DeviceKernel:
     if K != K2 or tuple(C.shape) != (M, N):
         raise ValueError("gemm_bf16: shapes must be A[M,K], B[N,K], C[M,N]")
     return DeviceKernel("gemm_bf16", (A, B, C), (M, N, K))
+
+
+def memcpy(dst, src, nbytes: int | None = None) -> DeviceKernel:
+    """A host<->device copy step of a request pipeline (``cudaMemcpyAsync`` on
+    the launch stream).  Copies are exempt from transformation -- register
+    them with ``KernelWork(..., exempt=True)``; only ``original()`` launches."""
+    nb = nbytes if nbytes is not None else src.numel() * src.element_size()
+    if dst.numel() * dst.element_size() < nb:
+        raise ValueError("memcpy: destination too small")
+    return DeviceKernel("memcpy", (dst.data_ptr(), src.data_ptr()), (nb,), keep=(dst, src))
