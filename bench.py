@@ -187,6 +187,19 @@ def run_reference_arm(args):
 
 
 # ----------------------------------------------------------------- GPU arm
+def gather_pairs(local_out, dist=None):
+    """Every rank runs an independent HP/BE pair; rank 0 reports the worst
+    pair (largest p99 overhead).  The only cross-rank traffic is this metric
+    gather -- no collective touches the data path."""
+    if dist is not None and dist.is_initialized() and dist.get_world_size() > 1:
+        gathered = [None] * dist.get_world_size()
+        dist.all_gather_object(gathered, local_out)
+    else:
+        gathered = [local_out]
+    worst = max(gathered, key=lambda d: d["overhead"])
+    return gathered, worst
+
+
 def main_ours(args):
     import torch
     world = int(os.environ.get("WORLD_SIZE", "1"))
@@ -400,15 +413,10 @@ def main_ours(args):
         "p99_solo_us": p99(solo_lat) / 1e3, "p99_co_us": p99(co_lat) / 1e3,
         "preempt_us": [pct(pl_us, 0.5), pct(pl_us, 0.99), max(pl_us)] if pl_us else None,
     }
-    if dist is not None:
-        gathered = [None] * world
-        dist.all_gather_object(gathered, local_out)
-    else:
-        gathered = [local_out]
+    gathered, worst = gather_pairs(local_out, dist)
     if rank != 0:
         dist.destroy_process_group()
         return
-    worst = max(gathered, key=lambda d: d["overhead"])
     out = {
         "metric": METRIC,
         "value": worst["overhead"],

@@ -78,6 +78,10 @@ int tally_clock_offset(long long* out_offset_ns, long long* out_uncertainty_ns);
 /* 0 = device-resident flags written with cuStreamWriteValue32 (default when
  * available), 1 = flags in mapped pinned host memory. */
 int tally_set_flag_mode(int host_mapped);
+/* Diagnostic: median / max ns from a host-side flag write to a spinning device
+ * reader observing it (mode 0 = device flag via cuStreamWriteValue32,
+ * 1 = mapped host flag). */
+int tally_probe_flag_latency(int mode, int iters, long long* out_median_ns, long long* out_max_ns);
 
 /* ==== kernel registration (ref scheduler.py:73-86 KernelWork; ir/core.py:153-214) */
 typedef struct {

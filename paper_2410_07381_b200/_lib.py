@@ -145,6 +145,8 @@ _SIGNATURES = {
     "tally_shutdown": (C.c_int, []),
     "tally_clock_offset": (C.c_int, [C.POINTER(C.c_longlong), C.POINTER(C.c_longlong)]),
     "tally_set_flag_mode": (C.c_int, [C.c_int]),
+    "tally_probe_flag_latency": (C.c_int, [C.c_int, C.c_int, C.POINTER(C.c_longlong),
+                                           C.POINTER(C.c_longlong)]),
     "tally_kernel_kind_count": (C.c_int, []),
     "tally_kernel_kind_name": (C.c_char_p, [C.c_int]),
     "tally_kernel_create": (C.c_int, [C.c_char_p, C.POINTER(c_kernel_args), C.POINTER(C.c_int)]),

@@ -115,6 +115,18 @@ __host__ __device__ constexpr uint32_t make_idesc() {
          | ((uint32_t)(128 >> 4) << 24);            // M >> 4
 }
 
+__device__ __forceinline__ void tmem_st32(uint32_t taddr, const uint32_t (&r)[32]) {
+  asm volatile(
+      "tcgen05.st.sync.aligned.32x32b.x32.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,%16,"
+      "%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31,%32};" ::"r"(taddr),
+      "r"(r[0]), "r"(r[1]), "r"(r[2]), "r"(r[3]), "r"(r[4]), "r"(r[5]), "r"(r[6]), "r"(r[7]), "r"(r[8]),
+      "r"(r[9]), "r"(r[10]), "r"(r[11]), "r"(r[12]), "r"(r[13]), "r"(r[14]), "r"(r[15]), "r"(r[16]),
+      "r"(r[17]), "r"(r[18]), "r"(r[19]), "r"(r[20]), "r"(r[21]), "r"(r[22]), "r"(r[23]), "r"(r[24]),
+      "r"(r[25]), "r"(r[26]), "r"(r[27]), "r"(r[28]), "r"(r[29]), "r"(r[30]), "r"(r[31])
+      : "memory");
+  asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
+}
+
 __device__ __forceinline__ void tmem_ld32(uint32_t taddr, uint32_t (&r)[32]) {
   asm volatile(
       "tcgen05.ld.sync.aligned.32x32b.x32.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,"
@@ -139,7 +151,7 @@ struct CfgTf32x3 {
   static constexpr int STAGE_BYTES = 2 * A_BYTES + 2 * B_BYTES;   // 48 KB
   static constexpr int STAGES = 4;
   static constexpr int UMMA_K = 8;
-  static constexpr int TMEM_COLS = 2 * BN;            // double-buffered accumulator
+  static constexpr int TMEM_COLS = 256;               // 2 x BN accumulators + BN running total
   using OutT = float;
 };
 
@@ -154,7 +166,7 @@ struct CfgBf16 {
   static constexpr int STAGE_BYTES = A_BYTES + B_BYTES;
   static constexpr int STAGES = 6;
   static constexpr int UMMA_K = 16;
-  static constexpr int TMEM_COLS = 2 * BN;
+  static constexpr int TMEM_COLS = 512;               // 2 x BN accumulators + BN running total
   using OutT = __nv_bfloat16;
 };
 
@@ -327,43 +339,52 @@ __global__ void __launch_bounds__(kThreads, 1) k_gemm(const __grid_constant__ Ge
       if (t < 0) break;
       int mb, nb;
       tile_coords(t, p, mb, nb);
-      float sum[Cfg::BN];
-#pragma unroll
-      for (int c = 0; c < Cfg::BN; ++c) sum[c] = 0.f;
-      for (int kb0 = 0; kb0 < KB; kb0 += p.kchunk, ++ci) {
+      const int row = mb * Cfg::BM + q * 32 + lane;
+      typename Cfg::OutT* crow = reinterpret_cast<typename Cfg::OutT*>(p.c) + (size_t)row * p.n + (size_t)nb * Cfg::BN;
+      const uint32_t lane_base = tmem_base + ((uint32_t)(q * 32) << 16);
+      const int nchunks = (KB + p.kchunk - 1) / p.kchunk;
+      for (int c = 0; c < nchunks; ++c, ++ci) {
         const int acc = ci & 1;
         mbar_wait(&tmem_full[acc], (ci >> 1) & 1);
         fence_after();
-#pragma unroll
+        const bool last = (c == nchunks - 1);
+#pragma unroll 1
         for (int c0 = 0; c0 < Cfg::BN; c0 += 32) {
+          // chunk partial + running fp32 total (kept in TMEM columns [2BN, 3BN))
           uint32_t r[32];
-          tmem_ld32(tmem_base + ((uint32_t)(q * 32) << 16) + (uint32_t)(acc * Cfg::BN + c0), r);
+          tmem_ld32(lane_base + (uint32_t)(acc * Cfg::BN + c0), r);
+          if (c > 0) {
+            uint32_t s[32];
+            tmem_ld32(lane_base + (uint32_t)(2 * Cfg::BN + c0), s);
 #pragma unroll
-          for (int e = 0; e < 32; ++e) sum[c0 + e] += __uint_as_float(r[e]);
+            for (int e = 0; e < 32; ++e) r[e] = __float_as_uint(__uint_as_float(r[e]) + __uint_as_float(s[e]));
+          }
+          if (!last) {
+            tmem_st32(lane_base + (uint32_t)(2 * Cfg::BN + c0), r);
+          } else if constexpr (Cfg::KIND == 0) {
+            float4* dst = reinterpret_cast<float4*>(crow + c0);
+#pragma unroll
+            for (int v = 0; v < 8; ++v)
+              dst[v] = make_float4(__uint_as_float(r[4 * v]), __uint_as_float(r[4 * v + 1]),
+                                   __uint_as_float(r[4 * v + 2]), __uint_as_float(r[4 * v + 3]));
+          } else {
+            uint4* dst = reinterpret_cast<uint4*>(crow + c0);
+#pragma unroll
+            for (int v = 0; v < 4; ++v) {
+              uint32_t w[4];
+#pragma unroll
+              for (int e = 0; e < 4; ++e) {
+                __nv_bfloat162 h = __floats2bfloat162_rn(__uint_as_float(r[8 * v + 2 * e]),
+                                                         __uint_as_float(r[8 * v + 2 * e + 1]));
+                w[e] = *reinterpret_cast<uint32_t*>(&h);
+              }
+              dst[v] = make_uint4(w[0], w[1], w[2], w[3]);
+            }
+          }
         }
         fence_before();
         __syncwarp();
         if (lane == 0) mbar_arrive(&tmem_empty[acc]);
-      }
-      const int row = mb * Cfg::BM + q * 32 + lane;
-      typename Cfg::OutT* crow = reinterpret_cast<typename Cfg::OutT*>(p.c) + (size_t)row * p.n + (size_t)nb * Cfg::BN;
-      if constexpr (Cfg::KIND == 0) {
-        float4* dst = reinterpret_cast<float4*>(crow);
-#pragma unroll
-        for (int v = 0; v < Cfg::BN / 4; ++v)
-          dst[v] = make_float4(sum[4 * v], sum[4 * v + 1], sum[4 * v + 2], sum[4 * v + 3]);
-      } else {
-        uint4* dst = reinterpret_cast<uint4*>(crow);
-#pragma unroll
-        for (int v = 0; v < Cfg::BN / 8; ++v) {
-          uint32_t w[4];
-#pragma unroll
-          for (int e = 0; e < 4; ++e) {
-            __nv_bfloat162 h = __floats2bfloat162_rn(sum[8 * v + 2 * e], sum[8 * v + 2 * e + 1]);
-            w[e] = *reinterpret_cast<uint32_t*>(&h);
-          }
-          dst[v] = make_uint4(w[0], w[1], w[2], w[3]);
-        }
       }
     }
   }

@@ -6,6 +6,7 @@
 #include <cuda_runtime.h>
 #include <time.h>
 
+#include <algorithm>
 #include <atomic>
 #include <cstdarg>
 #include <cstdio>
@@ -54,6 +55,19 @@ __global__ void k_stamp(unsigned long long* slot) {
   unsigned long long t;
   asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
   *reinterpret_cast<volatile unsigned long long*>(slot) = t;
+  __threadfence_system();
+}
+
+__global__ void k_flag_watch(const unsigned* flag, unsigned want, int host, unsigned long long* stamp) {
+  if (threadIdx.x != 0) return;
+  unsigned v;
+  do {
+    if (host) asm volatile("ld.acquire.sys.global.u32 %0, [%1];" : "=r"(v) : "l"(flag) : "memory");
+    else asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(flag) : "memory");
+  } while (v != want);
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  *reinterpret_cast<volatile unsigned long long*>(stamp) = t;
   __threadfence_system();
 }
 
@@ -508,6 +522,54 @@ int tally_set_flag_mode(int host_mapped) {
     return TALLY_EINVAL;
   }
   r.flag_host = host_mapped ? 1 : 0;
+  return TALLY_OK;
+}
+
+// Diagnostic: flag propagation latency, host signal -> a spinning device
+// reader observes it.  mode 0: device-resident flag written with
+// cuStreamWriteValue32 on the signal stream; mode 1: mapped host flag written
+// by a host store.
+int tally_probe_flag_latency(int mode, int iters, long long* out_median_ns, long long* out_max_ns) {
+  Runtime& r = rt();
+  if (!r.inited) { set_error("tally_init first"); return TALLY_EINVAL; }
+  if (mode == 0 && !r.write32) { set_error("no stream memory operations"); return TALLY_EINVAL; }
+  long long off = 0, unc = 0;
+  int rc = r.clock_offset(&off, &unc);
+  if (rc != TALLY_OK) return rc;
+  cudaStream_t ws;
+  CK(cudaStreamCreateWithFlags(&ws, cudaStreamNonBlocking), "probe stream");
+  unsigned* dflag = nullptr;
+  CK(cudaMalloc(&dflag, 64), "probe flag");
+  CK(cudaMemset(dflag, 0, 64), "probe flag");
+  std::vector<long long> lat;
+  for (int i = 0; i < iters; ++i) {
+    const unsigned want = (unsigned)(i + 1);
+    *r.h_stamp = 0ull;
+    const unsigned* f = mode == 0 ? dflag : r.d_hflags + (Runtime::kMaxRecs - 1);
+    r.h_flags[Runtime::kMaxRecs - 1] = 0;
+    std::atomic_thread_fence(std::memory_order_seq_cst);
+    k_flag_watch<<<1, 32, 0, ws>>>(f, want, mode, r.d_stamp);
+    CK(cudaGetLastError(), "probe launch");
+    const long long t_arm = host_now_ns() + 200000;   // let the watcher start spinning
+    while (host_now_ns() < t_arm) {}
+    const long long t0 = host_now_ns();
+    if (mode == 0) {
+      if (r.write32((CUstream)r.sig_stream, (CUdeviceptr)dflag, want, 0u) != CUDA_SUCCESS) {
+        set_error("cuStreamWriteValue32 failed");
+        return TALLY_ECUDA;
+      }
+    } else {
+      r.h_flags[Runtime::kMaxRecs - 1] = want;
+      std::atomic_thread_fence(std::memory_order_seq_cst);
+    }
+    CK(cudaStreamSynchronize(ws), "probe sync");
+    lat.push_back((long long)*r.h_stamp + off - t0);
+  }
+  cudaFree(dflag);
+  cudaStreamDestroy(ws);
+  std::sort(lat.begin(), lat.end());
+  if (out_median_ns) *out_median_ns = lat[lat.size() / 2];
+  if (out_max_ns) *out_max_ns = lat.back();
   return TALLY_OK;
 }
 

@@ -23,6 +23,23 @@ def arg(name, default):
     return type(default)(sys.argv[sys.argv.index(name) + 1]) if name in sys.argv else default
 
 
+def _pick(recs, f, q):
+    xs = sorted(f(r) for r in recs if r["priority"] == 0 and r["gpu_start_ns"] >= 0)
+    return xs[min(len(xs) - 1, int(q * (len(xs) - 1)))] / 1e3 if xs else None
+
+
+def _q(recs, q):   # issue -> GPU start (queueing for SM resources / stream)
+    return _pick(recs, lambda r: r["gpu_start_ns"] - r["issue_ns"], q)
+
+
+def _r(recs, q):   # GPU start -> end
+    return _pick(recs, lambda r: r["gpu_end_ns"] - r["gpu_start_ns"], q)
+
+
+def _h(recs, q):   # host submit -> issue
+    return _pick(recs, lambda r: r["issue_ns"] - r["submit_ns"], q)
+
+
 def main():
     dev = P.B200Device.get(0)
     be_kind = arg("--be", "vecadd_f32")
@@ -41,6 +58,11 @@ def main():
     elif be_kind == "rowsum_f32":
         x = torch.rand(1 << 16, 1024, device="cuda", generator=g)
         be = kernels.rowsum_f32(x, torch.zeros(1 << 16, device="cuda"))
+    elif be_kind == "sgemm_pipeline":
+        A = torch.rand(4096, 4096, device="cuda", generator=g) * 2 - 1
+        B = torch.rand(4096, 4096, device="cuda", generator=g) * 2 - 1
+        sg = kernels.sgemm_tf32x3(A, B, torch.zeros(4096, 4096, device="cuda"))
+        be = sg.gemm
     else:
         from tools.microbench import make
         be = make(be_kind)
@@ -49,6 +71,12 @@ def main():
     be_w = P.KernelWork(be_kind, be.cost(), kernel=be)
     prof.bind("vadd_hp", hp)
     prof.bind(be_kind, be)
+    be_ws = (be_w,)
+    if be_kind == "sgemm_pipeline":
+        be_ws = (P.KernelWork("split_a", sg.split_a.cost(), kernel=sg.split_a),
+                 P.KernelWork("split_b", sg.split_b.cost(), kernel=sg.split_b), be_w)
+        for w in be_ws:
+            prof.bind(w.kernel_id, w.kernel)
     hp_lat = workloads.isolated_request_latency_ns(prof, (hp_w,))
     arr = workloads.generate_arrivals(load, hp_lat, horizon, seed=0)
     recs = prof.profile(be_w.profile_key(), be_w.cost)
@@ -61,8 +89,9 @@ def main():
     for pol in ("Tally", "KernelPriority", "Eager"):
         cfg = P.SchedulerConfig(policy=pol, turnaround_threshold_ns=threshold)
         hp_t = P.TaskScript("hp", P.HIGH, (hp_w,), arr)
-        be_t = P.TaskScript("be", P.BEST_EFFORT, (be_w,))
-        solo_hp = P.run_policy(dev.spec, [hp_t], cfg, horizon, profiler=prof, record_events=False)
+        be_t = P.TaskScript("be", P.BEST_EFFORT, be_ws)
+        solo_hp = P.run_policy(dev.spec, [hp_t], cfg, horizon, profiler=prof, record_events=False,
+                               options={"trace": 1})
         solo_be = P.run_policy(dev.spec, [be_t], cfg, horizon, profiler=prof, record_events=False)
         co = P.run_policy(dev.spec, [hp_t, be_t], cfg, horizon, profiler=prof, record_events=False,
                           options={"trace": 1})
@@ -96,6 +125,12 @@ def main():
             "preempts": len(pre),
             "preempt_us_p50_p99_max": [pl[len(pl) // 2], pl[int(0.99 * (len(pl) - 1))], pl[-1]] if pl else None,
             "worst_hp": worst,
+            "hp_queue_us_p50_p99_solo_co": [
+                _q(solo_hp.launches, 0.5), _q(solo_hp.launches, 0.99), _q(co.launches, 0.5), _q(co.launches, 0.99)],
+            "hp_run_us_p50_p99_solo_co": [
+                _r(solo_hp.launches, 0.5), _r(solo_hp.launches, 0.99), _r(co.launches, 0.5), _r(co.launches, 0.99)],
+            "hp_host_issue_us_p50_p99_solo_co": [
+                _h(solo_hp.launches, 0.5), _h(solo_hp.launches, 0.99), _h(co.launches, 0.5), _h(co.launches, 0.99)],
         }
     print(json.dumps(out, indent=1))
 

@@ -83,6 +83,14 @@ def main():
         if info.alg_flops:
             rec["TFLOPs"] = info.alg_flops / t / 1e3
         out["shapes"][name] = rec
+    # flag propagation: host signal -> a spinning device reader sees it
+    import ctypes as C
+    from paper_2410_07381_b200 import _lib
+    out["flag_propagation_us"] = {}
+    for mode, name in ((0, "device_streamwrite"), (1, "host_mapped")):
+        med, mx = C.c_longlong(), C.c_longlong()
+        if _lib.lib.tally_probe_flag_latency(mode, 20, C.byref(med), C.byref(mx)) == 0:
+            out["flag_propagation_us"][name] = {"median": med.value / 1e3, "max": mx.value / 1e3}
     # preemption latency, both flag placements
     off, unc = dev.clock_offset()
     out["clock_uncertainty_ns"] = unc
