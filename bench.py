@@ -61,6 +61,8 @@ def parse():
     ap.add_argument("--load", type=float, default=0.5)
     ap.add_argument("--threshold-us", type=float, default=31.6)
     ap.add_argument("--no-baselines", action="store_true")
+    ap.add_argument("--suspend", type=int, default=1,
+                    help="Tally with cooperative suspension of pausable BE kernels (B200 extension)")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-sample-ms", type=float, default=1.0)
@@ -244,6 +246,10 @@ def main_ours(args):
     choices = {w.kernel_id: prof.select(w.profile_key(), w.cost, threshold).describe() for w in be_ws}
     sg_recs = {r.candidate.describe(): r for r in prof.profile(be_ws[2].profile_key(), be_ws[2].cost)}
 
+    def run_(tasks, cfg, horizon, **kw):
+        opts = {"suspend": 1} if (args.suspend and cfg.policy == "Tally") else None
+        return P.run_policy(gpu, tasks, cfg, horizon, options=opts, **kw)
+
     def arrivals(seed):
         return workloads.generate_arrivals(args.load, hp_lat, window, seed)
 
@@ -264,15 +270,15 @@ def main_ours(args):
     # --- calibration (untimed) -------------------------------------------------
     solo_lat = []
     for k in range(args.steps):
-        solo_lat += lat_after_warm(P.run_policy(gpu, [hp_task(k)], tally, window, profiler=prof,
+        solo_lat += lat_after_warm(run_([hp_task(k)], tally, window, profiler=prof,
                                                 record_events=False))
     eager = P.SchedulerConfig(policy="Eager")
-    be_untransformed = be_rate(P.run_policy(gpu, [be_task], eager, window, profiler=prof,
+    be_untransformed = be_rate(run_([be_task], eager, window, profiler=prof,
                                             record_events=False))
-    be_same_policy = be_rate(P.run_policy(gpu, [be_task], tally, window, profiler=prof,
+    be_same_policy = be_rate(run_([be_task], tally, window, profiler=prof,
                                           record_events=False))
     for w in range(args.warmup):
-        P.run_policy(gpu, [hp_task(100 + w), be_task], tally, window, profiler=prof,
+        run_([hp_task(100 + w), be_task], tally, window, profiler=prof,
                      record_events=False)
     off, _unc = dev.clock_offset()
 
@@ -287,7 +293,7 @@ def main_ours(args):
     t_host0 = time.perf_counter()
     results = []
     for k in range(args.steps):
-        results.append(P.run_policy(gpu, [hp_task(k), be_task], tally, window, profiler=prof,
+        results.append(run_([hp_task(k), be_task], tally, window, profiler=prof,
                                     record_events=False))
     ev1.record()
     torch.cuda.synchronize()
@@ -367,9 +373,9 @@ def main_ours(args):
                                 workloads.generate_arrivals(args.load, e2e_lat, window, seed))
         e_solo, e_co, reqs = [], [], 0
         for k in range(args.steps):
-            e_solo += lat_after_warm(P.run_policy(gpu, [e2e_task(k)], tally, window, profiler=prof,
+            e_solo += lat_after_warm(run_([e2e_task(k)], tally, window, profiler=prof,
                                                   record_events=False))
-            r = P.run_policy(gpu, [e2e_task(k), be_task], tally, window, profiler=prof,
+            r = run_([e2e_task(k), be_task], tally, window, profiler=prof,
                              record_events=False)
             reqs += len(r.requests["hp"])
             e_co += lat_after_warm(r)
@@ -388,12 +394,12 @@ def main_ours(args):
             cfg = P.SchedulerConfig(policy=pol)
             lat, rate = [], []
             for k in range(min(2, args.steps)):
-                r = P.run_policy(gpu, [hp_task(k), be_task], cfg, window, profiler=prof,
+                r = run_([hp_task(k), be_task], cfg, window, profiler=prof,
                                  record_events=False)
                 lat += lat_after_warm(r)
                 rate.append(be_rate(r))
             sl = [x for k in range(min(2, args.steps)) for x in lat_after_warm(
-                P.run_policy(gpu, [hp_task(k)], cfg, window, profiler=prof, record_events=False))]
+                run_([hp_task(k)], cfg, window, profiler=prof, record_events=False))]
             baselines[pol] = {"p99_overhead_pct": 100.0 * (p99(lat) / p99(sl) - 1.0),
                               "be_throughput_pct": 100.0 * (sum(rate) / len(rate)) / be_untransformed}
 
@@ -433,6 +439,7 @@ def main_ours(args):
         "config": {"workload": WORKLOAD, "hp_elements": n, "be_gemm": [m, m, m],
                    "load": args.load, "window_ms": args.window_ms,
                    "turnaround_threshold_us": args.threshold_us,
+                   "policy": "Tally + cooperative suspension" if args.suspend else "Tally (reference semantics)",
                    "tuner_choice": choices, "l2": "inputs larger than L2 (201 MB HP, 256 MB BE)",
                    "parallelism": f"{world} independent HP/BE pair(s), one per GPU"},
         "components": {

@@ -131,6 +131,7 @@ typedef struct {
   long long preempt_at;     /* test trigger: raise the flag when the counter reaches this
                                value (ref transforms.py:433-447 MemTrigger); -1 = off */
   unsigned long long* exec_count; /* optional device array[total_blocks]: exactly-once audit */
+  int pausable;             /* PTB: honour the global suspension word (tally_set_pause) */
   unsigned long long* worker_log; /* PTB, optional device array[workers * 4]: per-worker
                                      {smid << 32 | tasks, t_entry, t_exit, stopped} (%globaltimer) */
   int timed;                /* 1: bracket with timing events (tally_launch_elapsed_ns) */
@@ -152,6 +153,10 @@ int tally_launch_query(int launch, tally_launch_state* out);    /* non-blocking 
 int tally_launch_wait(int launch, tally_launch_state* out);     /* blocking            */
 int tally_launch_elapsed_ns(int launch, long long* out);        /* needs desc.timed=1  */
 int tally_preempt(int launch);                                  /* flag write; thread-safe */
+/* Cooperative suspension (B200 extension): while on, pausable PTB launches
+ * hold their place at the next suspension point (GEMM: every 4 k-blocks) and
+ * resume in place when it clears -- no park, no relaunch. */
+int tally_set_pause(int on);
 int tally_launch_release(int launch);
 
 /* ==== policy runner (ref scheduler.py:164-457) =============================== */
@@ -228,7 +233,10 @@ int tally_runner_iterations(int runner, int task, long long* out, int cap);
 int tally_runner_destroy(int runner);
 /* Options for the B200 device run: "trace" (1 = bracket every launch with
  * timing events for the launch log), "hp_streams" (size of the high-priority
- * stream pool, default 4). */
+ * stream pool, default 4), "suspend" (1 = Tally with cooperative suspension:
+ * on HP arrival pausable BE launches are suspended in place instead of
+ * parked, and resumed when HP goes inactive; other BE launches are preempted
+ * as usual). */
 int tally_runner_set_option(int runner, const char* key, long long value);
 
 /* Real-device run log (only after tally_runner_run(runner, NULL)). */

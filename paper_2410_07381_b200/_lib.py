@@ -65,7 +65,7 @@ class c_launch_desc(C.Structure):
                 ("off_z", C.c_uint), ("sub_x", C.c_uint), ("sub_y", C.c_uint),
                 ("sub_z", C.c_uint), ("workers", C.c_int), ("start_count", C.c_longlong),
                 ("preempt_at", C.c_longlong), ("exec_count", C.c_void_p),
-                ("worker_log", C.c_void_p), ("timed", C.c_int)]
+                ("pausable", C.c_int), ("worker_log", C.c_void_p), ("timed", C.c_int)]
 
 
 class c_launch_state(C.Structure):
@@ -160,6 +160,7 @@ _SIGNATURES = {
     "tally_launch_wait": (C.c_int, [C.c_int, C.POINTER(c_launch_state)]),
     "tally_launch_elapsed_ns": (C.c_int, [C.c_int, C.POINTER(C.c_longlong)]),
     "tally_preempt": (C.c_int, [C.c_int]),
+    "tally_set_pause": (C.c_int, [C.c_int]),
     "tally_launch_release": (C.c_int, [C.c_int]),
     "tally_runner_create": (C.c_int, [C.c_int, C.c_longlong, C.c_longlong, C.c_longlong,
                                       C.POINTER(C.c_int)]),

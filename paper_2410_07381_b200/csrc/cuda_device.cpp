@@ -64,6 +64,7 @@ class CudaDevice : public Device {
     r_->log.t0_ns = t0_;
   }
   ~CudaDevice() override {
+    if (held_) tally_set_pause(0);
     for (auto& h : hs_)
       if (h.launch >= 0 && !h.finished) tally_launch_wait(h.launch, nullptr);
     for (auto& h : hs_)
@@ -122,6 +123,25 @@ class CudaDevice : public Device {
 
   void call_at(long long t, long long token) override {
     timers_.push(Tm{t, seq_++, token});
+  }
+
+  bool hold(long long id) override {
+    Handle& h = get(id);
+    if (h.d.shape != TALLY_SHAPE_PTB || h.finished || !pausable(h.d.device_kernel)) return false;
+    if (!held_) {
+      int rc = tally_set_pause(1);
+      if (rc != TALLY_OK) throw Error(rc, tally_last_error());
+      held_ = true;
+      log_event(TALLY_EV_PREEMPT_SIGNALED, id, -2);   // block -2 marks a suspension
+    }
+    return true;
+  }
+
+  void release_holds() override {
+    if (!held_) return;
+    int rc = tally_set_pause(0);
+    if (rc != TALLY_OK) throw Error(rc, tally_last_error());
+    held_ = false;
   }
 
   void set_dispatch_filter(bool e) override { filter_ = e; }
@@ -193,6 +213,18 @@ class CudaDevice : public Device {
   int inflight_ = 0;
   bool filter_ = false;
   bool trace_ = false;
+  bool held_ = false;
+  std::map<int, bool> pausable_cache_;
+
+  bool pausable(int kernel) {
+    auto it = pausable_cache_.find(kernel);
+    if (it != pausable_cache_.end()) return it->second;
+    Runtime& R = rt();
+    bool p = kernel >= 0 && kernel < (int)R.instances.size() && R.instances[(size_t)kernel] &&
+             R.kinds[R.instances[(size_t)kernel]->kind].pausable;
+    pausable_cache_[kernel] = p;
+    return p;
+  }
   std::map<int, long long> total_cache_;
   cudaEvent_t ref_ = nullptr;
   int hp_rr_ = 0;
@@ -268,6 +300,7 @@ class CudaDevice : public Device {
     struct { long long total_blocks; } ki{kit->second};
     if (h.d.shape == TALLY_SHAPE_PTB) {
       ld.shape = TALLY_SHAPE_PTB;
+      ld.pausable = r_->option("suspend", 0) ? 1 : 0;
       ld.workers = h.d.worker_count;
       ld.start_count = h.d.start_count;
       h.count = ki.total_blocks;

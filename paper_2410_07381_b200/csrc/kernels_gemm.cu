@@ -262,6 +262,11 @@ __global__ void __launch_bounds__(kThreads, 1) k_gemm(const __grid_constant__ Ge
         tile_coords(t, p, mb, nb);
         for (int kb = 0; kb < KB; ++kb, ++it) {
           const int st = it % Cfg::STAGES;
+          if constexpr (MODE == kPtb) {
+            // suspension point between k-blocks: the tile stays claimed and
+            // resumes in place; a park request lets the tile run to completion
+            if ((kb & 3) == 0 && ptb_hold_while_paused(s)) {}
+          }
           if (it >= (uint32_t)Cfg::STAGES) mbar_wait(&empty[st], ((it / Cfg::STAGES) - 1) & 1);
           unsigned char* base = smem + (size_t)st * Cfg::STAGE_BYTES;
           mbar_expect_tx(&full[st], Cfg::STAGE_BYTES);
@@ -561,6 +566,7 @@ static KernelKind gemm_kind(const char* name, int (*bind)(const tally_kernel_arg
   k.fn_ptb = reinterpret_cast<const void*>(&gemm::k_gemm<Cfg, gemm::kPtb, PtbArgs>);
   k.bind = bind;
   k.setup = &setup_gemm<Cfg>;
+  k.pausable = 1;
   return k;
 }
 

@@ -41,6 +41,9 @@ struct KernelKind {
   // stream) -- the data-movement steps of an end-to-end request pipeline.
   // Copies are exempt from transformation: Original shape only.
   int copy;
+  // 1: the PTB shape has fine-grained suspension points and a footprint that
+  // leaves room for high-priority CTAs (GEMM: 1 CTA/SM, ~90 regs/thread)
+  int pausable;
 };
 
 struct CopyParams {

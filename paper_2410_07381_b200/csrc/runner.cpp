@@ -54,6 +54,7 @@ long long Runner::token(int kind, int task, long long t) {
 
 void Runner::run(Device* dev) {
   dev_ = dev;
+  suspend_ = policy == TALLY_POLICY_TALLY && option("suspend", 0) != 0;
   hp_.clear();
   be_.clear();
   for (size_t i = 0; i < tasks.size(); ++i) {
@@ -101,6 +102,7 @@ void Runner::tick() {
     absorb();
     if (policy == TALLY_POLICY_TALLY || policy == TALLY_POLICY_KERNEL_PRIORITY) {
       for (int i : hp_) advance(i, TALLY_HIGH);
+      if (suspend_ && !hp_active()) dev_->release_holds();
       if (!hp_active()) {
         const int n = (int)be_.size();
         std::vector<int> order;
@@ -245,7 +247,10 @@ void Runner::preempt_be() {
     const long long h = tasks[(size_t)i].h;
     if (h < 0) continue;
     const tally_handle_state s = dev_->query(h);
-    if (s.is_ptb && !s.done && !s.preempted) dev_->signal_preempt(h);
+    if (s.is_ptb && !s.done && !s.preempted) {
+      if (suspend_ && dev_->hold(h)) continue;   // suspended in place, resumes when HP is idle
+      dev_->signal_preempt(h);
+    }
   }
 }
 
@@ -487,7 +492,7 @@ int tally_runner_set_option(int runner, const char* key, long long value) {
   if (!r) return TALLY_EINVAL;
   if (!key) { set_error("null option key"); return TALLY_EINVAL; }
   const std::string k(key);
-  if (k != "trace" && k != "hp_streams") { set_error("unknown runner option '%s'", key); return TALLY_EINVAL; }
+  if (k != "trace" && k != "hp_streams" && k != "suspend") { set_error("unknown runner option '%s'", key); return TALLY_EINVAL; }
   if (k == "hp_streams" && (value < 1 || value > 64)) { set_error("hp_streams must be in [1, 64]"); return TALLY_EINVAL; }
   r->options[k] = value;
   return TALLY_OK;

@@ -32,6 +32,10 @@ struct Device {
   virtual void set_dispatch_filter(bool enabled) = 0;
   virtual void kick() = 0;
   virtual void run_to_completion() = 0;
+  // Cooperative suspension (B200 extension; no-op for foreign devices):
+  // hold() suspends launch h in place and returns true if it can.
+  virtual bool hold(long long) { return false; }
+  virtual void release_holds() {}
 };
 
 struct Work {
@@ -122,6 +126,7 @@ class Runner {
   std::vector<int> hp_, be_;
   int rr_ = 0;
   bool ticking_ = false;
+  bool suspend_ = false;
   int ts_active_ = 0;
   bool ts_armed_ = false;
 

@@ -123,6 +123,8 @@ int Runtime::init(int dev, tally_gpu_info* out) {
      "cudaHostAlloc(flags)");
   memset((void*)h_flags, 0, sizeof(unsigned) * kMaxRecs);
   CK(cudaHostGetDevicePointer(&d_hflags, (void*)h_flags, 0), "flag device pointer");
+  CK(cudaMalloc(&d_pause, 64), "cudaMalloc(pause)");
+  CK(cudaMemset(d_pause, 0, 64), "cudaMemset(pause)");
   CK(cudaHostAlloc(&h_stamp, 64, cudaHostAllocMapped), "cudaHostAlloc(stamp)");
   CK(cudaHostGetDevicePointer(&d_stamp, (void*)h_stamp, 0), "stamp device pointer");
   free_recs.clear();
@@ -340,6 +342,7 @@ int Runtime::launch(int kernel, int stream, const tally_launch_desc* d, int* out
       pa.grid = in.grid;
       pa.exec_count = d->exec_count;
       pa.worker_log = d->worker_log;
+      pa.pause = (d->pausable && kk.pausable) ? d_pause : nullptr;
       fn = kk.fn_ptb;
       grid = dim3((unsigned)d->workers, 1, 1);
       args[1] = &pa;
@@ -441,6 +444,22 @@ int Runtime::preempt(int id) {
   }
   CUresult r = write32((CUstream)sig_stream, (CUdeviceptr)&d_recs[L->rec].flag, L->serial, 0u);
   if (r != CUDA_SUCCESS) { set_error("cuStreamWriteValue32 failed (%d)", (int)r); return TALLY_ECUDA; }
+  return TALLY_OK;
+}
+
+int Runtime::set_pause(int on) {
+  if (!inited) { set_error("tally_init first"); return TALLY_EINVAL; }
+  on = on ? 1 : 0;
+  if (on == pause_on) return TALLY_OK;
+  pause_on = on;
+  if (write32) {
+    CUresult r = write32((CUstream)sig_stream, (CUdeviceptr)d_pause, (cuuint32_t)on, 0u);
+    if (r != CUDA_SUCCESS) { set_error("cuStreamWriteValue32(pause) failed (%d)", (int)r); return TALLY_ECUDA; }
+    return TALLY_OK;
+  }
+  const unsigned v = (unsigned)on;
+  CK(cudaMemcpyAsync(d_pause, &v, sizeof(v), cudaMemcpyHostToDevice, sig_stream), "pause write");
+  CK(cudaStreamSynchronize(sig_stream), "pause write");
   return TALLY_OK;
 }
 
@@ -724,6 +743,7 @@ int tally_launch_elapsed_ns(int id, long long* out) {
 }
 
 int tally_preempt(int id) { return rt().preempt(id); }
+int tally_set_pause(int on) { return rt().set_pause(on); }
 int tally_launch_release(int id) { return rt().release(id); }
 
 }  // extern "C"

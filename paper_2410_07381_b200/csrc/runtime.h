@@ -57,6 +57,8 @@ struct Runtime {
   LaunchMirror* d_mirrors = nullptr;
   volatile unsigned* h_flags = nullptr;
   unsigned* d_hflags = nullptr;
+  unsigned* d_pause = nullptr;        // global suspension word (device memory)
+  int pause_on = 0;
   volatile unsigned long long* h_stamp = nullptr;
   unsigned long long* d_stamp = nullptr;
   std::vector<int> free_recs;
@@ -80,6 +82,7 @@ struct Runtime {
   bool poll(Launch* L);
   void fill_state(const Launch* L, tally_launch_state* o);
   int preempt(int id);
+  int set_pause(int on);
   int release(int id);
 };
 

@@ -73,6 +73,7 @@ struct PtbArgs {
   uint3 grid;                      // logical grid
   unsigned long long* exec_count;  // optional exactly-once counters [total]
   unsigned long long* worker_log;  // optional [workers * 4] per-worker telemetry
+  const unsigned int* pause;       // optional suspension word (device memory); non-zero = hold
 };
 
 __device__ __forceinline__ unsigned long long globaltimer() {
@@ -175,7 +176,22 @@ __device__ __forceinline__ void ptb_worker_exit(const PtbArgs& a, bool stopped,
 
 // One claim by the leader thread: check the flag first, then fetch-and-add
 // the task counter (ref transforms.py:343-351).  Returns -1 on preemption.
+// Cooperative suspension (B200 extension): while the pause
+// word is set the worker holds its place -- no claims, no memory traffic --
+// and resumes in place when it clears; a park request (flag == serial) ends
+// the wait.  Returns true if a park was requested while waiting.
+__device__ __forceinline__ bool ptb_hold_while_paused(const PtbArgs& a) {
+  if (a.pause == nullptr || ld_acquire_gpu(a.pause) == 0u) return false;
+  for (;;) {
+    __nanosleep(256);
+    const unsigned f = a.flag_is_host ? ld_acquire_sys(a.flag) : ld_acquire_gpu(a.flag);
+    if (f == a.serial) return true;
+    if (ld_acquire_gpu(a.pause) == 0u) return false;
+  }
+}
+
 __device__ __forceinline__ long long ptb_claim(const PtbArgs& a) {
+  ptb_hold_while_paused(a);
   const unsigned f = a.flag_is_host ? ld_acquire_sys(a.flag) : ld_acquire_gpu(a.flag);
   if (f == a.serial) return -1;   // flag gates the claim: a parked launch never over-claims
   const unsigned long long c = atomicAdd(&a.rec->claims, 1ull);

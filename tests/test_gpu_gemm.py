@@ -107,3 +107,37 @@ def test_sgemm_ptb_preempt_resume_exactly_once(env):
     assert bool((ec == 1).all())
     assert torch.equal(C, ref)
     sg.close()
+
+
+def test_gemm_cooperative_suspension_resumes_in_place(env):
+    """Pausable PTB GEMM: suspend mid-run (global pause word), verify it stops
+    making progress, resume, and the result equals the Original kernel's."""
+    P, kernels, stream = env
+    from paper_2410_07381_b200 import _lib
+    import ctypes as C
+    M = N = K = 4096
+    g = torch.Generator(device="cuda").manual_seed(9)
+    A = (torch.rand(M, K, device="cuda", generator=g) * 2 - 1).bfloat16()
+    B = (torch.rand(N, K, device="cuda", generator=g) * 2 - 1).bfloat16()
+    C_ = torch.zeros(M, N, device="cuda", dtype=torch.bfloat16)
+    dk = kernels.gemm_bf16(A, B, C_)
+    dk.original(stream).wait()
+    ref = C_.clone()
+    C_.zero_()
+    ec = torch.zeros(dk.total_blocks, dtype=torch.int64, device="cuda")
+    d = _lib.c_launch_desc(shape=_lib.SHAPE_PTB, workers=148, start_count=0, preempt_at=-1,
+                           exec_count=ec.data_ptr(), pausable=1)
+    lid = C.c_int()
+    _lib.check(_lib.lib.tally_set_pause(1), "pause")      # start suspended
+    _lib.check(_lib.lib.tally_launch(dk.id, stream.id, C.byref(d), C.byref(lid)), "launch")
+    L = kernels.Launch(lid.value, _lib.SHAPE_PTB)
+    t_end = P.B200Device.now_ns() + 20_000_000
+    while P.B200Device.now_ns() < t_end:
+        pass
+    assert not L.query().done                              # held in place
+    _lib.check(_lib.lib.tally_set_pause(0), "resume")
+    st = L.wait()
+    assert st.done and not st.parked
+    assert bool((ec == 1).all())
+    assert torch.equal(C_, ref)
+    dk.close()
