@@ -108,6 +108,15 @@ const char* tally_kernel_kind_name(int kind);
 int tally_kernel_create(const char* kind, const tally_kernel_args* args, int* out_kernel);
 int tally_kernel_info_get(int kernel, tally_kernel_info* out);
 int tally_kernel_destroy(int kernel);
+/* IR-JIT: register a kernel kind from an NVRTC-compiled cubin holding the
+ * three shape instantiations of one IR kernel body (irjit.py generates them
+ * from a reference KernelDef; ref ir/core.py:153-214, transforms.py).
+ * Arguments of tally_kernel_create for such a kind: ptr[0] = int64 word
+ * image, ptr[1] = fault word, i[0] = words, i[1..7] = IR kernel arguments. */
+int tally_jit_register(const char* name, const void* cubin, const char* sym_original,
+                       const char* sym_sliced, const char* sym_ptb, unsigned grid_x,
+                       unsigned grid_y, unsigned grid_z, int threads, long long smem_bytes,
+                       int* out_kind);
 
 /* ==== streams (per-priority CUDA streams) ================================== */
 int tally_stream_create(int priority_class, int* out_stream);   /* TALLY_HIGH / TALLY_BEST_EFFORT */

@@ -152,6 +152,9 @@ _SIGNATURES = {
     "tally_kernel_create": (C.c_int, [C.c_char_p, C.POINTER(c_kernel_args), C.POINTER(C.c_int)]),
     "tally_kernel_info_get": (C.c_int, [C.c_int, C.POINTER(c_kernel_info)]),
     "tally_kernel_destroy": (C.c_int, [C.c_int]),
+    "tally_jit_register": (C.c_int, [C.c_char_p, C.c_void_p, C.c_char_p, C.c_char_p, C.c_char_p,
+                                     C.c_uint, C.c_uint, C.c_uint, C.c_int, C.c_longlong,
+                                     C.POINTER(C.c_int)]),
     "tally_stream_create": (C.c_int, [C.c_int, C.POINTER(C.c_int)]),
     "tally_stream_sync": (C.c_int, [C.c_int]),
     "tally_stream_destroy": (C.c_int, [C.c_int]),

@@ -567,6 +567,7 @@ static KernelKind gemm_kind(const char* name, int (*bind)(const tally_kernel_arg
   k.bind = bind;
   k.setup = &setup_gemm<Cfg>;
   k.pausable = 1;
+  k.host_flag = 1;
   return k;
 }
 

@@ -44,7 +44,18 @@ struct KernelKind {
   // 1: the PTB shape has fine-grained suspension points and a footprint that
   // leaves room for high-priority CTAs (GEMM: 1 CTA/SM, ~90 regs/thread)
   int pausable;
+  // 1: PTB launches read their preemption flag from mapped host memory
+  // (few readers, one read per long logical block)
+  int host_flag;
+  // IR-JIT kinds (irjit.py): NVRTC-compiled module, launched with the driver API
+  int jit;
+  void* cu_fn[3];             // CUfunction for Original / Sliced / PTB
+  unsigned jit_grid[3];       // logical grid of the IR kernel
+  int jit_threads;
+  long long jit_smem;
+  char jit_name[64];
 };
+
 
 struct CopyParams {
   void* dst;

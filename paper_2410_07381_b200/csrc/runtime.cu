@@ -10,6 +10,7 @@
 #include <atomic>
 #include <cstdarg>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <memory>
 #include <mutex>
@@ -112,6 +113,20 @@ int Runtime::init(int dev, tally_gpu_info* out) {
       int rc = kinds[k].setup();
       if (rc != TALLY_OK) return rc;
     }
+  // Optional: one L1/shared carveout for every kernel (TALLY_CARVEOUT=max).
+  // Off by default -- measured on B200 (profiles/r01_summary.md): a max-shared
+  // carveout costs the streaming HP kernel ~25 % (fewer L1 lines for loads
+  // in flight), more than co-residency gains.
+  const char* cv = getenv("TALLY_CARVEOUT");
+  if (cv && strcmp(cv, "max") == 0) {
+    for (int k = 0; k < nkinds; ++k) {
+      if (kinds[k].copy) continue;
+      for (const void* f : {kinds[k].fn_original, kinds[k].fn_sliced, kinds[k].fn_ptb})
+        if (f) cudaFuncSetAttribute(f, cudaFuncAttributePreferredSharedMemoryCarveout,
+                                    cudaSharedmemCarveoutMaxShared);
+    }
+    cudaGetLastError();
+  }
 
   CK(cudaMalloc(&d_recs, sizeof(LaunchRec) * kMaxRecs), "cudaMalloc(launch records)");
   CK(cudaMemset(d_recs, 0, sizeof(LaunchRec) * kMaxRecs), "cudaMemset(launch records)");
@@ -153,6 +168,19 @@ int Runtime::init(int dev, tally_gpu_info* out) {
     cudaGetLastError();
   }
   flag_host = info.stream_mem_ops ? 0 : 1;
+  auto entry = [](const char* sym) -> void* {
+    void* f = nullptr;
+    cudaDriverEntryPointQueryResult qq;
+    if (cudaGetDriverEntryPointByVersion(sym, &f, 12000, cudaEnableDefault, &qq) != cudaSuccess ||
+        qq != cudaDriverEntryPointSuccess)
+      return nullptr;
+    return f;
+  };
+  cu_module_load = reinterpret_cast<ModuleLoadDataFn>(entry("cuModuleLoadData"));
+  cu_get_function = reinterpret_cast<ModuleGetFunctionFn>(entry("cuModuleGetFunction"));
+  cu_launch = reinterpret_cast<LaunchKernelFn>(entry("cuLaunchKernel"));
+  cu_occupancy = reinterpret_cast<OccupancyFn>(entry("cuOccupancyMaxActiveBlocksPerMultiprocessor"));
+  cudaGetLastError();
   inited = true;
   if (out) *out = info;
   return TALLY_OK;
@@ -331,9 +359,12 @@ int Runtime::launch(int kernel, int stream, const tally_launch_desc* d, int* out
       h_flags[rec] = 0;
       std::atomic_thread_fence(std::memory_order_seq_cst);
       pa.rec = d_recs + rec;
-      pa.flag_is_host = flag_host;
-      pa.flag = flag_host ? (d_hflags + rec) : &d_recs[rec].flag;
-      L->flag_host = flag_host;
+      // few, rare readers (a GEMM producer per SM, once per tile) -> the flag
+      // can live in mapped host memory: ~2 us propagation instead of ~6 us
+      const int use_host = flag_host || kk.host_flag;
+      pa.flag_is_host = use_host;
+      pa.flag = use_host ? (d_hflags + rec) : &d_recs[rec].flag;
+      L->flag_host = use_host;
       pa.mirror = d_mirrors + rec;
       pa.serial = ser;
       pa.start = (unsigned long long)d->start_count;
@@ -358,7 +389,15 @@ int Runtime::launch(int kernel, int stream, const tally_launch_desc* d, int* out
     L->ev_start = get_event(true);
     cudaEventRecord(L->ev_start, st);
   }
-  cudaError_t e = cudaLaunchKernel(fn, grid, dim3(in.threads), args, in.smem, st);
+  cudaError_t e = cudaSuccess;
+  if (kk.jit) {
+    const int idx = d->shape == TALLY_SHAPE_ORIGINAL ? 0 : (d->shape == TALLY_SHAPE_SLICED ? 1 : 2);
+    CUresult cr = cu_launch((CUfunction)kk.cu_fn[idx], grid.x, grid.y, grid.z, (unsigned)in.threads, 1, 1,
+                            (unsigned)in.smem, (CUstream)st, args, nullptr);
+    if (cr != CUDA_SUCCESS) e = cudaErrorLaunchFailure;
+  } else {
+    e = cudaLaunchKernel(fn, grid, dim3(in.threads), args, in.smem, st);
+  }
   if (e != cudaSuccess) {
     if (L->rec >= 0) free_recs.push_back(L->rec);
     release_event(L->ev_start);
@@ -444,6 +483,56 @@ int Runtime::preempt(int id) {
   }
   CUresult r = write32((CUstream)sig_stream, (CUdeviceptr)&d_recs[L->rec].flag, L->serial, 0u);
   if (r != CUDA_SUCCESS) { set_error("cuStreamWriteValue32 failed (%d)", (int)r); return TALLY_ECUDA; }
+  return TALLY_OK;
+}
+
+static int bind_jit(const tally_kernel_args* a, Instance* inst) {
+  const KernelKind& kk = rt().kinds[inst->kind];
+  JitParams p;
+  memset(&p, 0, sizeof(p));
+  p.mem = static_cast<long long*>(a->ptr[0]);
+  p.fault = static_cast<unsigned long long*>(a->ptr[1]);
+  p.nwords = a->i[0];
+  for (int k = 0; k < 7; ++k) p.args[k] = a->i[k + 1];
+  if (!p.mem || p.nwords < 0 || !p.fault) {
+    set_error("%s: need mem, fault word and nwords", kk.name);
+    return TALLY_EINVAL;
+  }
+  memcpy(inst->params, &p, sizeof(p));
+  inst->grid = make_uint3(kk.jit_grid[0], kk.jit_grid[1], kk.jit_grid[2]);
+  inst->threads = kk.jit_threads;
+  inst->smem = (size_t)kk.jit_smem;
+  return TALLY_OK;
+}
+
+int Runtime::jit_register(const char* name, const void* image, const char* syms[3], const unsigned grid[3],
+                          int threads, long long smem, int* out_kind) {
+  if (!inited) { set_error("tally_init first"); return TALLY_EINVAL; }
+  if (!cu_module_load || !cu_get_function || !cu_launch) { set_error("driver module API unavailable"); return TALLY_ENODEV; }
+  if (nkinds >= kMaxKinds) { set_error("too many kernel kinds"); return TALLY_ENOMEM; }
+  if (threads < 1 || threads > 1024 || smem < 0 || smem > 48 * 1024 || !grid[0] || !grid[1] || !grid[2]) {
+    set_error("jit kernel geometry out of range");
+    return TALLY_EINVAL;
+  }
+  CUmodule mod;
+  CUresult r = cu_module_load(&mod, image);
+  if (r != CUDA_SUCCESS) { set_error("cuModuleLoadData failed (%d)", (int)r); return TALLY_ECUDA; }
+  KernelKind& k = kinds[nkinds];
+  memset(&k, 0, sizeof(k));
+  snprintf(k.jit_name, sizeof(k.jit_name), "%s", name);
+  k.name = k.jit_name;
+  k.jit = 1;
+  for (int i = 0; i < 3; ++i) {
+    CUfunction f;
+    r = cu_get_function(&f, mod, syms[i]);
+    if (r != CUDA_SUCCESS) { set_error("cuModuleGetFunction(%s) failed (%d)", syms[i], (int)r); return TALLY_ECUDA; }
+    k.cu_fn[i] = (void*)f;
+    k.jit_grid[i] = grid[i];
+  }
+  k.jit_threads = threads;
+  k.jit_smem = smem;
+  k.bind = bind_jit;
+  *out_kind = nkinds++;
   return TALLY_OK;
 }
 
@@ -596,21 +685,21 @@ int tally_kernel_kind_count(void) {
   Runtime& r = rt();
   if (!r.inited) {
     // registry is static; allow listing without a device
-    KernelKind tmp[Runtime::kMaxKinds];
-    int n = register_basic_kernels(tmp, Runtime::kMaxKinds);
-    n += register_gemm_kernels(tmp + n, Runtime::kMaxKinds - n);
-    return n + register_copy_kernels(tmp + n, Runtime::kMaxKinds - n);
+    static KernelKind tmp[32];
+    int n = register_basic_kernels(tmp, 32);
+    n += register_gemm_kernels(tmp + n, 32 - n);
+    return n + register_copy_kernels(tmp + n, 32 - n);
   }
   return r.nkinds;
 }
 
 const char* tally_kernel_kind_name(int kind) {
-  static KernelKind tmp[Runtime::kMaxKinds];
+  static KernelKind tmp[32];
   static int n = -1;
   if (n < 0) {
-    n = register_basic_kernels(tmp, Runtime::kMaxKinds);
-    n += register_gemm_kernels(tmp + n, Runtime::kMaxKinds - n);
-    n += register_copy_kernels(tmp + n, Runtime::kMaxKinds - n);
+    n = register_basic_kernels(tmp, 32);
+    n += register_gemm_kernels(tmp + n, 32 - n);
+    n += register_copy_kernels(tmp + n, 32 - n);
   }
   if (kind < 0 || kind >= n) return nullptr;
   return tmp[kind].name;
@@ -653,6 +742,15 @@ int tally_kernel_info_get(int kernel, tally_kernel_info* o) {
   o->alg_flops = in.alg_flops;
   int occ = 0;
   if (kk.copy) return TALLY_OK;
+  if (kk.jit) {
+    if (r.cu_occupancy) {
+      r.cu_occupancy(&occ, (CUfunction)kk.cu_fn[2], in.threads, in.smem);
+      o->occupancy_ptb = occ;
+      r.cu_occupancy(&occ, (CUfunction)kk.cu_fn[0], in.threads, in.smem);
+      o->occupancy_original = occ;
+    }
+    return TALLY_OK;
+  }
   CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kk.fn_ptb, in.threads, in.smem), "occupancy");
   o->occupancy_ptb = occ;
   CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kk.fn_original, in.threads, in.smem), "occupancy");
@@ -675,7 +773,9 @@ int tally_stream_create(int prio, int* out) {
   if (!r.inited) { set_error("tally_init first"); return TALLY_EINVAL; }
   if (prio != TALLY_HIGH && prio != TALLY_BEST_EFFORT) { set_error("unknown priority class %d", prio); return TALLY_EINVAL; }
   cudaStream_t s;
-  CK(cudaStreamCreateWithPriority(&s, cudaStreamNonBlocking, prio == TALLY_HIGH ? r.prio_high : r.prio_low),
+  // Blocking streams: ordered after work on the legacy default stream (where
+  // PyTorch initialises the buffers we are handed), concurrent with each other.
+  CK(cudaStreamCreateWithPriority(&s, cudaStreamDefault, prio == TALLY_HIGH ? r.prio_high : r.prio_low),
      "cudaStreamCreateWithPriority");
   *out = (int)r.streams.size();
   r.streams.push_back(s);
@@ -744,6 +844,18 @@ int tally_launch_elapsed_ns(int id, long long* out) {
 
 int tally_preempt(int id) { return rt().preempt(id); }
 int tally_set_pause(int on) { return rt().set_pause(on); }
+
+int tally_jit_register(const char* name, const void* image, const char* sym_original, const char* sym_sliced,
+                       const char* sym_ptb, unsigned gx, unsigned gy, unsigned gz, int threads, long long smem,
+                       int* out_kind) {
+  if (!name || !image || !sym_original || !sym_sliced || !sym_ptb || !out_kind) {
+    set_error("null argument");
+    return TALLY_EINVAL;
+  }
+  const char* syms[3] = {sym_original, sym_sliced, sym_ptb};
+  const unsigned grid[3] = {gx, gy, gz};
+  return rt().jit_register(name, image, syms, grid, threads, smem, out_kind);
+}
 int tally_launch_release(int id) { return rt().release(id); }
 
 }  // extern "C"

@@ -18,6 +18,11 @@ namespace tally {
 long long host_now_ns();
 
 typedef CUresult (*WriteValue32Fn)(CUstream, CUdeviceptr, cuuint32_t, unsigned int);
+typedef CUresult (*ModuleLoadDataFn)(CUmodule*, const void*);
+typedef CUresult (*ModuleGetFunctionFn)(CUfunction*, CUmodule, const char*);
+typedef CUresult (*LaunchKernelFn)(CUfunction, unsigned, unsigned, unsigned, unsigned, unsigned, unsigned,
+                                   unsigned, CUstream, void**, void**);
+typedef CUresult (*OccupancyFn)(int*, CUfunction, int, size_t);
 
 struct Launch {
   int kernel = -1, stream = -1, shape = 0;
@@ -38,7 +43,7 @@ struct Launch {
 };
 
 struct Runtime {
-  static constexpr int kMaxKinds = 16;
+  static constexpr int kMaxKinds = 1024;   // built-ins + IR-JIT kinds
   static constexpr int kMaxRecs = 1024;
 
   std::mutex mu;
@@ -66,6 +71,12 @@ struct Runtime {
   std::atomic<unsigned> next_serial{0};
   int flag_host = 0;
   WriteValue32Fn write32 = nullptr;
+  ModuleLoadDataFn cu_module_load = nullptr;
+  ModuleGetFunctionFn cu_get_function = nullptr;
+  LaunchKernelFn cu_launch = nullptr;
+  OccupancyFn cu_occupancy = nullptr;
+  int jit_register(const char* name, const void* image, const char* syms[3], const unsigned grid[3],
+                   int threads, long long smem, int* out_kind);
 
   std::vector<std::unique_ptr<Launch>> launches;
   std::vector<int> free_launch_ids;

@@ -19,8 +19,10 @@
 // no thread leaves run() early past a __syncthreads -- the PTB loop's barriers
 // are then the only ones a finished logical block can meet.
 #pragma once
+#ifndef __CUDACC_RTC__   // also compiled by NVRTC for IR-JIT kernels (irjit.py)
 #include <cstdint>
 #include <cuda_runtime.h>
+#endif
 
 namespace tally {
 
@@ -51,6 +53,14 @@ struct alignas(64) LaunchMirror {
 };
 
 enum : unsigned { kMirrorDone = 1, kMirrorParked = 2 };
+
+// Params of an IR-JIT body (irjit.py; the runtime's generic bind fills it)
+struct JitParams {
+  long long* mem;                 // flat int64 word image
+  long long nwords;
+  unsigned long long* fault;      // set non-zero on an out-of-range access / step limit
+  long long args[8];              // IR kernel arguments (low registers)
+};
 
 // Shape arguments ------------------------------------------------------------
 struct SliceArgs {
