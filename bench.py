@@ -59,9 +59,14 @@ def parse():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--window-ms", type=float, default=100.0)
     ap.add_argument("--load", type=float, default=0.5)
-    ap.add_argument("--threshold-us", type=float, default=31.6)
+    # The paper's 0.0316 ms default was tuned on A100 kernels.  On the B200 no
+    # configuration of C1's SGEMM (one 128x64 3xTF32 tile ~ 70 us) meets
+    # 31.6 us, and the reference's fallback -- least turnaround -- then picks
+    # a one-tile-per-launch slicing (2048 launches per GEMM).  0.1 ms admits
+    # PTB(148) (Eq. 1 ~ 74 us).  The library default stays 31.6 us.
+    ap.add_argument("--threshold-us", type=float, default=100.0)
     ap.add_argument("--no-baselines", action="store_true")
-    ap.add_argument("--suspend", type=int, default=1,
+    ap.add_argument("--suspend", type=int, default=0,
                     help="Tally with cooperative suspension of pausable BE kernels (B200 extension)")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
@@ -343,9 +348,16 @@ def main_ours(args):
     bf16_peak = peaks.get("bf16_tflops", 1590.0)
     peak_3xtf32 = bf16_peak / 6.0     # tf32 dense = bf16/2; three tf32 MMAs per fp32 MAC
     achieved = sg.gemm.info.alg_flops / chosen_ns / 1e3
+    traffic = None   # dram__bytes_read.sum + dram__bytes_write.sum per launch, one ncu capture
+    try:
+        traffic = json.load(open(os.path.join(ROOT, "profiles", "ncu_traffic.json"))).get(
+            f"sgemm_tf32x3_4096_{cand.describe()}")
+    except (OSError, ValueError):
+        pass
     roofline = {"bound": "tensor", "kernel": f"sgemm_tf32x3 4096^3 ({cand.describe()})",
                 "achieved": achieved, "peak": peak_3xtf32, "unit": "TFLOP/s",
-                "frac": achieved / peak_3xtf32, "traffic": None,
+                "frac": achieved / peak_3xtf32, "traffic": traffic,
+                "traffic_note": "bytes per launch from profiles/ncu_traffic.json (ncu --set full)",
                 "peak_note": f"MEASURED_PEAKS bf16_tflops {bf16_peak} / 6 (tf32 = bf16/2, 3 MMAs per MAC)",
                 "vs_untransformed": dur["Original"] / chosen_ns,
                 "untransformed_ns": dur["Original"], "chosen_ns": chosen_ns}

@@ -69,7 +69,7 @@ struct VecAddF32 {
 #pragma unroll
     for (int j = 0; j < kVecPerThread; ++j) {
       const long long k = base + (long long)j * kThreads;
-      if (k < p.n4) { x[j] = __ldcs(p.a + k); y[j] = __ldcs(p.b + k); }
+      if (k < p.n4) { x[j] = ld_stream(p.a + k); y[j] = ld_stream(p.b + k); }
     }
 #pragma unroll
     for (int j = 0; j < kVecPerThread; ++j) {
@@ -127,7 +127,7 @@ struct RowSumF32 {
       const float4* row4 = reinterpret_cast<const float4*>(row);
       const long long c4 = p.cols >> 2;
       for (long long c = lane; c < c4; c += 32) {
-        const float4 v = __ldcs(row4 + c);
+        const float4 v = ld_stream(row4 + c);
         acc += (v.x + v.y) + (v.z + v.w);
       }
     } else {

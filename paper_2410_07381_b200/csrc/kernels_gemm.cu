@@ -426,7 +426,7 @@ struct SplitTf32 {
 #pragma unroll
     for (int j = 0; j < kVec; ++j) {
       const long long k = base + (long long)j * kThreads;
-      if (k < p.n4) v[j] = __ldcs(p.x + k);
+      if (k < p.n4) v[j] = ld_stream(p.x + k);
     }
 #pragma unroll
     for (int j = 0; j < kVec; ++j) {

@@ -37,9 +37,10 @@ struct KernelKind {
   int (*bind)(const tally_kernel_args* a, Instance* inst);
   // Optional one-time setup (e.g. smem attribute) -- may be null.
   int (*setup)();
-  // 1: not a kernel but a host<->device copy (cudaMemcpyAsync on the launch
-  // stream) -- the data-movement steps of an end-to-end request pipeline.
-  // Copies are exempt from transformation: Original shape only.
+  // Not a kernel: 1 = host<->device copy (cudaMemcpyAsync on the launch
+  // stream), 2 = captured CUDA graph (cudaGraphLaunch) -- data movement and
+  // unmodified framework programs in a request pipeline.  Exempt from
+  // transformation: Original shape only.
   int copy;
   // 1: the PTB shape has fine-grained suspension points and a footprint that
   // leaves room for high-priority CTAs (GEMM: 1 CTA/SM, ~90 regs/thread)

@@ -106,6 +106,16 @@ __device__ __forceinline__ void st_release_sys(unsigned* p, unsigned v) {
   asm volatile("st.release.sys.global.u32 [%0], %1;" :: "l"(p), "r"(v) : "memory");
 }
 
+// Streaming 16 B load that does not allocate in L1: the HBM kernels read
+// every byte once, and must not depend on how much L1 a co-resident CTA
+// (e.g. a GEMM worker holding ~198 KB of shared memory) leaves them.
+__device__ __forceinline__ float4 ld_stream(const float4* p) {
+  float4 v;
+  asm volatile("ld.global.nc.L1::no_allocate.v4.f32 {%0, %1, %2, %3}, [%4];"
+               : "=f"(v.x), "=f"(v.y), "=f"(v.z), "=f"(v.w) : "l"(p));
+  return v;
+}
+
 __device__ __forceinline__ uint3 delinearize(unsigned long long t, uint3 g) {
   // ref ir/core.py:59-65: x fastest
   uint3 b;

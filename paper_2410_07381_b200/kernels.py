@@ -292,3 +292,11 @@ def memcpy(dst, src, nbytes: int | None = None) -> DeviceKernel:
     if dst.numel() * dst.element_size() < nb:
         raise ValueError("memcpy: destination too small")
     return DeviceKernel("memcpy", (dst.data_ptr(), src.data_ptr()), (nb,), keep=(dst, src))
+
+
+def cuda_graph(graph) -> DeviceKernel:
+    """An unmodified program -- a captured ``torch.cuda.CUDAGraph`` (e.g. a
+    model's inference forward) -- as one exempt pipeline step, launched with
+    ``cudaGraphLaunch`` on the scheduler's stream of its priority."""
+    exec_handle = graph.raw_cuda_graph_exec() if hasattr(graph, "raw_cuda_graph_exec") else int(graph)
+    return DeviceKernel("cuda_graph", (int(exec_handle),), (), keep=(graph,))
