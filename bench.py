@@ -71,6 +71,8 @@ def parse():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-sample-ms", type=float, default=1.0)
+    ap.add_argument("--profile-cache", default=None,
+                    help="tuner cache JSON: loaded if present, else written after profiling")
     return ap.parse_args()
 
 
@@ -246,10 +248,15 @@ def main_ours(args):
              P.KernelWork("sgemm_tf32x3_4096", sg.gemm.cost(), kernel=sg.gemm))
     for w in (hp_w,) + be_ws:
         prof.bind(w.kernel_id, w.kernel)
+    if args.profile_cache and os.path.exists(args.profile_cache):
+        prof.load_cache(open(args.profile_cache).read())    # ref profiler.py:252-291
     threshold = int(args.threshold_us * 1000)
     hp_lat = workloads.isolated_request_latency_ns(prof, (hp_w,))
     choices = {w.kernel_id: prof.select(w.profile_key(), w.cost, threshold).describe() for w in be_ws}
     sg_recs = {r.candidate.describe(): r for r in prof.profile(be_ws[2].profile_key(), be_ws[2].cost)}
+    if args.profile_cache and not os.path.exists(args.profile_cache) and rank == 0:
+        with open(args.profile_cache, "w") as fh:
+            fh.write(prof.dump_cache())
 
     def run_(tasks, cfg, horizon, **kw):
         opts = {"suspend": 1} if (args.suspend and cfg.policy == "Tally") else None

@@ -184,6 +184,7 @@ struct alignas(64) GemmParams {
   int m, n, k;
   int tiles_m, tiles_n;
   int kchunk;   // k-blocks per TMEM accumulation chunk (promotion to fp32 registers)
+  unsigned long long* resume;   // chunk-preemption resume ring (sgemm_tf32x3), see tally_device.cuh
 };
 
 __device__ __forceinline__ void tile_coords(long long t, const GemmParams& p, int& mb, int& nb) {
@@ -207,8 +208,10 @@ __global__ void __launch_bounds__(kThreads, 1) k_gemm(const __grid_constant__ Ge
   uint64_t* tmem_empty = tmem_full + 2;         // [2]
   uint64_t* tile_full = tmem_empty + 2;         // [2]
   uint64_t* tile_empty = tile_full + 2;         // [2]
-  long long* tile_slot = reinterpret_cast<long long*>(tile_empty + 2);   // [2]
-  uint32_t* tmem_base_slot = reinterpret_cast<uint32_t*>(tile_slot + 2);
+  long long* tile_slot = reinterpret_cast<long long*>(tile_empty + 2);   // [2] claimed tile id
+  int* tile_c0 = reinterpret_cast<int*>(tile_slot + 2);                  // [2] first chunk (resumed tiles)
+  int* tile_cut = tile_c0 + 2;                                           // [2] chunk the tile stops before
+  uint32_t* tmem_base_slot = reinterpret_cast<uint32_t*>(tile_cut + 2);
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int KB = p.k / Cfg::BK;
@@ -235,17 +238,48 @@ __global__ void __launch_bounds__(kThreads, 1) k_gemm(const __grid_constant__ Ge
   fence_after();
   const uint32_t tmem_base = *tmem_base_slot;
   bool stopped = false;
+  const int NCH = (KB + p.kchunk - 1) / p.kchunk;   // accumulation chunks per tile
+  // chunk-granular preemption (fp32-output kernels in PTB shape with a resume
+  // ring): a preempted worker stops its tile at the next chunk boundary,
+  // saves the fp32 running total into its C tile and queues (tile, chunk)
+  constexpr bool kChunkPreempt = (MODE == kPtb) && (Cfg::KIND == 0);
 
   if (warp == 0) {
     if (lane == 0) {
       // ------------------------------------------------ TMA producer
       uint32_t it = 0;
+      unsigned flag_seen = 0;
       for (int i = 0;; ++i) {
         long long t = -1;
+        int c0 = 0;
         if constexpr (MODE == kPtb) {
-          t = ptb_claim(s);
-          if (t < 0) stopped = true;
-          else if ((unsigned long long)t >= s.total) t = -1;
+          bool popped = false;
+          if (kChunkPreempt && p.resume != nullptr) {
+            // resume a tile a preempted worker left half-done
+            ptb_hold_while_paused(s);
+            const unsigned f = s.flag_is_host ? ld_acquire_sys(s.flag) : ld_acquire_gpu(s.flag);
+            if (f != s.serial) {
+              unsigned long long* ring = p.resume;
+              for (;;) {
+                const unsigned long long h = atomicAdd(ring + 1, 0ull), tl = atomicAdd(ring, 0ull);
+                if (h >= tl) break;
+                if (atomicCAS(ring + 1, h, h + 1) != h) continue;
+                volatile unsigned long long* e = ring + 2 + (h % kResumeCap);
+                unsigned long long v;
+                while ((v = *e) == 0ull) __nanosleep(64);
+                *e = 0ull;
+                t = (long long)(v & 0xFFFFFFFFFFull) - 1;
+                c0 = (int)(v >> 40);
+                popped = true;
+                break;
+              }
+            }
+          }
+          if (!popped) {
+            t = ptb_claim(s);
+            if (t < 0) stopped = true;
+            else if ((unsigned long long)t >= s.total) t = -1;
+          }
         } else {
           if (i == 0) {
             t = MODE == kOriginal ? (long long)blockIdx.x
@@ -256,29 +290,50 @@ __global__ void __launch_bounds__(kThreads, 1) k_gemm(const __grid_constant__ Ge
         const int j = i & 1;
         if (i >= 2) mbar_wait(&tile_empty[j], ((i >> 1) - 1) & 1);
         tile_slot[j] = t;
+        tile_c0[j] = c0;
+        tile_cut[j] = NCH;
         mbar_arrive(&tile_full[j]);
         if (t < 0) break;
         int mb, nb;
         tile_coords(t, p, mb, nb);
-        for (int kb = 0; kb < KB; ++kb, ++it) {
-          const int st = it % Cfg::STAGES;
-          if constexpr (MODE == kPtb) {
-            // suspension point between k-blocks: the tile stays claimed and
-            // resumes in place; a park request lets the tile run to completion
-            if ((kb & 3) == 0 && ptb_hold_while_paused(s)) {}
+        for (int c = c0; c < NCH; ++c) {
+          if constexpr (kChunkPreempt) {
+            // flag_seen was loaded half a chunk ago; the load has long completed
+            if (p.resume != nullptr && c > c0) {
+              if (flag_seen == s.serial) {
+                // cut the tile before chunk c: publish the cut, then wake the
+                // MMA issuer with an empty ("poisoned") stage
+                *reinterpret_cast<volatile int*>(&tile_cut[j]) = c;
+                const int st = it % Cfg::STAGES;
+                if (it >= (uint32_t)Cfg::STAGES) mbar_wait(&empty[st], ((it / Cfg::STAGES) - 1) & 1);
+                mbar_arrive(&full[st]);
+                ++it;
+                break;
+              }
+            }
           }
-          if (it >= (uint32_t)Cfg::STAGES) mbar_wait(&empty[st], ((it / Cfg::STAGES) - 1) & 1);
-          unsigned char* base = smem + (size_t)st * Cfg::STAGE_BYTES;
-          mbar_expect_tx(&full[st], Cfg::STAGE_BYTES);
-          const int kx = kb * Cfg::BK;
-          if constexpr (Cfg::KIND == 0) {
-            tma_load_2d(base, &p.a_hi, &full[st], kx, mb * Cfg::BM);
-            tma_load_2d(base + Cfg::A_BYTES, &p.a_lo, &full[st], kx, mb * Cfg::BM);
-            tma_load_2d(base + 2 * Cfg::A_BYTES, &p.b_hi, &full[st], kx, nb * Cfg::BN);
-            tma_load_2d(base + 2 * Cfg::A_BYTES + Cfg::B_BYTES, &p.b_lo, &full[st], kx, nb * Cfg::BN);
-          } else {
-            tma_load_2d(base, &p.a_hi, &full[st], kx, mb * Cfg::BM);
-            tma_load_2d(base + Cfg::A_BYTES, &p.b_hi, &full[st], kx, nb * Cfg::BN);
+          const int kb1 = min(KB, (c + 1) * p.kchunk);
+          for (int kb = c * p.kchunk; kb < kb1; ++kb, ++it) {
+            const int st = it % Cfg::STAGES;
+            if constexpr (MODE == kPtb) {
+              // suspension point between k-blocks (cooperative suspension option)
+              if ((kb & 3) == 0 && ptb_hold_while_paused(s)) {}
+              if (kChunkPreempt && p.resume != nullptr && kb == c * p.kchunk + p.kchunk / 2)
+                flag_seen = s.flag_is_host ? ld_relaxed_sys(s.flag) : ld_acquire_gpu(s.flag);
+            }
+            if (it >= (uint32_t)Cfg::STAGES) mbar_wait(&empty[st], ((it / Cfg::STAGES) - 1) & 1);
+            unsigned char* base = smem + (size_t)st * Cfg::STAGE_BYTES;
+            mbar_expect_tx(&full[st], Cfg::STAGE_BYTES);
+            const int kx = kb * Cfg::BK;
+            if constexpr (Cfg::KIND == 0) {
+              tma_load_2d(base, &p.a_hi, &full[st], kx, mb * Cfg::BM);
+              tma_load_2d(base + Cfg::A_BYTES, &p.a_lo, &full[st], kx, mb * Cfg::BM);
+              tma_load_2d(base + 2 * Cfg::A_BYTES, &p.b_hi, &full[st], kx, nb * Cfg::BN);
+              tma_load_2d(base + 2 * Cfg::A_BYTES + Cfg::B_BYTES, &p.b_lo, &full[st], kx, nb * Cfg::BN);
+            } else {
+              tma_load_2d(base, &p.a_hi, &full[st], kx, mb * Cfg::BM);
+              tma_load_2d(base + Cfg::A_BYTES, &p.b_hi, &full[st], kx, nb * Cfg::BN);
+            }
           }
         }
       }
@@ -288,25 +343,36 @@ __global__ void __launch_bounds__(kThreads, 1) k_gemm(const __grid_constant__ Ge
     if (lane == 0) {
       // ------------------------------------------------ MMA issuer
       // The tile's K range is cut into chunks of p.kchunk k-blocks; each chunk
-      // accumulates into one of two TMEM buffers and is promoted to fp32
-      // registers by the epilogue (bounded tensor-core accumulation chains).
+      // accumulates into one of two TMEM buffers and is promoted to an fp32
+      // running total by the epilogue (bounded tensor-core accumulation chains).
       constexpr uint32_t idesc = make_idesc<Cfg::KIND, Cfg::BN>();
       uint32_t it = 0, ci = 0;
       for (int i = 0;; ++i) {
         const int j = i & 1;
         mbar_wait(&tile_full[j], (i >> 1) & 1);
         const long long t = tile_slot[j];
-        mbar_arrive(&tile_empty[j]);
-        if (t < 0) break;
-        for (int kb0 = 0; kb0 < KB; kb0 += p.kchunk, ++ci) {
+        const int c0 = tile_c0[j];
+        if (t < 0) {
+          mbar_arrive(&tile_empty[j]);
+          break;
+        }
+        for (int c = c0; c < NCH; ++c, ++ci) {
           const int acc = ci & 1;
           if (ci >= 2) mbar_wait(&tmem_empty[acc], ((ci >> 1) - 1) & 1);
           fence_after();
           const uint32_t d = tmem_base + (uint32_t)(acc * Cfg::BN);
-          const int kb1 = min(KB, kb0 + p.kchunk);
+          const int kb0 = c * p.kchunk, kb1 = min(KB, kb0 + p.kchunk);
+          bool cut = false;
           for (int kb = kb0; kb < kb1; ++kb, ++it) {
             const int st = it % Cfg::STAGES;
             mbar_wait(&full[st], (it / Cfg::STAGES) & 1);
+            if (kChunkPreempt && kb == kb0 && *reinterpret_cast<volatile int*>(&tile_cut[j]) <= c) {
+              mbar_arrive(&empty[st]);        // poisoned stage: no data, hand it back
+              mbar_arrive(&tmem_full[acc]);   // and tell the epilogue this chunk is the cut
+              ++it;
+              cut = true;
+              break;
+            }
             fence_after();
             const unsigned char* base = smem + (size_t)st * Cfg::STAGE_BYTES;
 #pragma unroll
@@ -326,8 +392,13 @@ __global__ void __launch_bounds__(kThreads, 1) k_gemm(const __grid_constant__ Ge
             }
             umma_commit(&empty[st]);   // frees the stage once these MMAs retire
           }
+          if (cut) {
+            ++ci;
+            break;
+          }
           umma_commit(&tmem_full[acc]);
         }
+        mbar_arrive(&tile_empty[j]);
       }
     }
     __syncwarp();
@@ -339,41 +410,85 @@ __global__ void __launch_bounds__(kThreads, 1) k_gemm(const __grid_constant__ Ge
       const int j = i & 1;
       mbar_wait(&tile_full[j], (i >> 1) & 1);
       const long long t = tile_slot[j];
-      __syncwarp();
-      if (lane == 0) mbar_arrive(&tile_empty[j]);
-      if (t < 0) break;
+      const int c0 = tile_c0[j];
+      if (t < 0) {
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&tile_empty[j]);
+        break;
+      }
       int mb, nb;
       tile_coords(t, p, mb, nb);
       const int row = mb * Cfg::BM + q * 32 + lane;
       typename Cfg::OutT* crow = reinterpret_cast<typename Cfg::OutT*>(p.c) + (size_t)row * p.n + (size_t)nb * Cfg::BN;
       const uint32_t lane_base = tmem_base + ((uint32_t)(q * 32) << 16);
-      const int nchunks = (KB + p.kchunk - 1) / p.kchunk;
-      for (int c = 0; c < nchunks; ++c, ++ci) {
+      for (int c = c0; c < NCH; ++c, ++ci) {
         const int acc = ci & 1;
         mbar_wait(&tmem_full[acc], (ci >> 1) & 1);
         fence_after();
-        const bool last = (c == nchunks - 1);
+        if (kChunkPreempt && *reinterpret_cast<volatile int*>(&tile_cut[j]) <= c) {
+          // preempted before chunk c: park the fp32 running total in C
+          if (c > c0) {
 #pragma unroll 1
-        for (int c0 = 0; c0 < Cfg::BN; c0 += 32) {
+            for (int c1 = 0; c1 < Cfg::BN; c1 += 32) {
+              uint32_t r[32];
+              tmem_ld32(lane_base + (uint32_t)(2 * Cfg::BN + c1), r);
+              float4* dst = reinterpret_cast<float4*>(crow + c1);
+#pragma unroll
+              for (int v = 0; v < 8; ++v)
+                dst[v] = make_float4(__uint_as_float(r[4 * v]), __uint_as_float(r[4 * v + 1]),
+                                     __uint_as_float(r[4 * v + 2]), __uint_as_float(r[4 * v + 3]));
+            }
+          }
+          __threadfence();
+          asm volatile("bar.sync 1, 128;" ::: "memory");   // all four epilogue warps saved
+          if (warp == 2 && lane == 0) {
+            unsigned long long* ring = p.resume;
+            const unsigned long long slot = atomicAdd(ring, 1ull);
+            __threadfence();
+            *reinterpret_cast<volatile unsigned long long*>(ring + 2 + (slot % kResumeCap)) =
+                (unsigned long long)(t + 1) | ((unsigned long long)c << 40);
+          }
+          fence_before();
+          __syncwarp();
+          if (lane == 0) mbar_arrive(&tmem_empty[acc]);
+          ++ci;
+          break;
+        }
+        const bool last = (c == NCH - 1);
+#pragma unroll 1
+        for (int c1 = 0; c1 < Cfg::BN; c1 += 32) {
           // chunk partial + running fp32 total (kept in TMEM columns [2BN, 3BN))
           uint32_t r[32];
-          tmem_ld32(lane_base + (uint32_t)(acc * Cfg::BN + c0), r);
-          if (c > 0) {
-            uint32_t s[32];
-            tmem_ld32(lane_base + (uint32_t)(2 * Cfg::BN + c0), s);
+          tmem_ld32(lane_base + (uint32_t)(acc * Cfg::BN + c1), r);
+          if (c > c0) {
+            uint32_t sv[32];
+            tmem_ld32(lane_base + (uint32_t)(2 * Cfg::BN + c1), sv);
 #pragma unroll
-            for (int e = 0; e < 32; ++e) r[e] = __float_as_uint(__uint_as_float(r[e]) + __uint_as_float(s[e]));
+            for (int e = 0; e < 32; ++e) r[e] = __float_as_uint(__uint_as_float(r[e]) + __uint_as_float(sv[e]));
+          } else if (c0 > 0) {
+            // resumed tile: the partial total a preempted worker saved in C
+            if constexpr (Cfg::KIND == 0) {
+              const float4* src = reinterpret_cast<const float4*>(crow + c1);
+#pragma unroll
+              for (int v = 0; v < 8; ++v) {
+                const float4 x = src[v];
+                r[4 * v] = __float_as_uint(__uint_as_float(r[4 * v]) + x.x);
+                r[4 * v + 1] = __float_as_uint(__uint_as_float(r[4 * v + 1]) + x.y);
+                r[4 * v + 2] = __float_as_uint(__uint_as_float(r[4 * v + 2]) + x.z);
+                r[4 * v + 3] = __float_as_uint(__uint_as_float(r[4 * v + 3]) + x.w);
+              }
+            }
           }
           if (!last) {
-            tmem_st32(lane_base + (uint32_t)(2 * Cfg::BN + c0), r);
+            tmem_st32(lane_base + (uint32_t)(2 * Cfg::BN + c1), r);
           } else if constexpr (Cfg::KIND == 0) {
-            float4* dst = reinterpret_cast<float4*>(crow + c0);
+            float4* dst = reinterpret_cast<float4*>(crow + c1);
 #pragma unroll
             for (int v = 0; v < 8; ++v)
               dst[v] = make_float4(__uint_as_float(r[4 * v]), __uint_as_float(r[4 * v + 1]),
                                    __uint_as_float(r[4 * v + 2]), __uint_as_float(r[4 * v + 3]));
           } else {
-            uint4* dst = reinterpret_cast<uint4*>(crow + c0);
+            uint4* dst = reinterpret_cast<uint4*>(crow + c1);
 #pragma unroll
             for (int v = 0; v < 4; ++v) {
               uint32_t w[4];
@@ -391,6 +506,8 @@ __global__ void __launch_bounds__(kThreads, 1) k_gemm(const __grid_constant__ Ge
         __syncwarp();
         if (lane == 0) mbar_arrive(&tmem_empty[acc]);
       }
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&tile_empty[j]);
     }
   }
 
@@ -400,7 +517,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_gemm(const __grid_constant__ Ge
   if (warp == 1)
     asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem_base), "n"(Cfg::TMEM_COLS));
   if constexpr (MODE == kPtb) {
-    if (threadIdx.x == 0) ptb_worker_exit(s, stopped, t_entry);
+    if (threadIdx.x == 0) ptb_worker_exit(s, stopped, t_entry, kChunkPreempt ? p.resume : nullptr);
   }
 }
 
@@ -513,6 +630,15 @@ static int bind_gemm(const tally_kernel_args* a, Instance* inst, bool split) {
   // promote the tensor-core accumulator to fp32 registers every 512 of K for
   // the fp32-accuracy kernel; bf16 (1e-2 budget) accumulates the whole K in TMEM
   p.kchunk = Cfg::KIND == 0 ? 512 / Cfg::BK : (int)(K / Cfg::BK);
+  p.resume = nullptr;
+  if (Cfg::KIND == 0) {
+    const size_t bytes = (2 + kResumeCap) * sizeof(unsigned long long);
+    cudaError_t e = cudaMalloc(&p.resume, bytes);
+    if (e == cudaSuccess) e = cudaMemset(p.resume, 0, bytes);
+    if (e != cudaSuccess) return cuda_fail(e, "gemm resume ring");
+    inst->resume_ring = p.resume;
+    inst->resume_bytes = bytes;
+  }
   static_assert(sizeof(p) <= kMaxParamBytes, "params too large");
   memcpy(inst->params, &p, sizeof(p));
   inst->grid = make_uint3((unsigned)(p.tiles_m * p.tiles_n), 1, 1);

@@ -359,6 +359,11 @@ int Runtime::launch(int kernel, int stream, const tally_launch_desc* d, int* out
       L->workers = d->workers;
       h_mirrors[rec].serial = 0;
       h_flags[rec] = 0;
+      if (in.resume_ring != nullptr && d->start_count == 0) {
+        // a new chain: no half-done tiles carried over from an earlier one
+        cudaError_t me = cudaMemsetAsync(in.resume_ring, 0, in.resume_bytes, st);
+        if (me != cudaSuccess) { free_recs.push_back(rec); return cuda_fail(me, "resume ring reset"); }
+      }
       std::atomic_thread_fence(std::memory_order_seq_cst);
       pa.rec = d_recs + rec;
       // few, rare readers (a GEMM producer per SM, once per tile) -> the flag

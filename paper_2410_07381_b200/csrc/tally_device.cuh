@@ -102,6 +102,11 @@ __device__ __forceinline__ unsigned ld_acquire_sys(const unsigned* p) {
   asm volatile("ld.acquire.sys.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
   return v;
 }
+__device__ __forceinline__ unsigned ld_relaxed_sys(const unsigned* p) {
+  unsigned v;
+  asm volatile("ld.relaxed.sys.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
 __device__ __forceinline__ void st_release_sys(unsigned* p, unsigned v) {
   asm volatile("st.release.sys.global.u32 [%0], %1;" :: "l"(p), "r"(v) : "memory");
 }
@@ -156,8 +161,24 @@ k_sliced(const typename Body::Params p, const SliceArgs s) {
 
 // --- PTB: persistent, preemptible workers -------------------------------------
 // Worker exit bookkeeping, run by thread 0 of every worker.
+// Resume ring of a chunk-preemptible kernel (one per kernel instance, device
+// memory): [0] = pushes (tail), [1] = pops (head), [2 + i % kResumeCap] =
+// entries (tile + 1) | (next_chunk << 40); 0 = empty.  A worker preempted
+// mid-tile saves its partial state and pushes (tile, chunk); the next launch
+// of the chain pops before claiming fresh tiles.  Outstanding entries <=
+// resident workers, so the ring never overflows.
+constexpr unsigned kResumeCap = 1024;
+
+__device__ __forceinline__ unsigned long long resume_pending(const unsigned long long* ring) {
+  if (ring == nullptr) return 0ull;
+  const unsigned long long tail = atomicAdd(const_cast<unsigned long long*>(ring), 0ull);
+  const unsigned long long head = atomicAdd(const_cast<unsigned long long*>(ring + 1), 0ull);
+  return tail > head ? tail - head : 0ull;
+}
+
 __device__ __forceinline__ void ptb_worker_exit(const PtbArgs& a, bool stopped,
-                                                unsigned long long t_entry) {
+                                                unsigned long long t_entry,
+                                                const unsigned long long* resume_ring = nullptr) {
   const unsigned long long now = globaltimer();
   LaunchRec* r = a.rec;
   if (stopped) {
@@ -181,7 +202,7 @@ __device__ __forceinline__ void ptb_worker_exit(const PtbArgs& a, bool stopped,
     m->stops = atomicAdd(&r->stops, 0ull);
     m->t_first_start = t_entry;
     // work can only remain if some worker stopped on the flag
-    m->status = (progress < a.total) ? kMirrorParked : kMirrorDone;
+    m->status = (progress < a.total || resume_pending(resume_ring) > 0) ? kMirrorParked : kMirrorDone;
     __threadfence_system();
     m->serial = a.serial;
     __threadfence_system();

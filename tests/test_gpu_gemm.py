@@ -80,6 +80,10 @@ def test_gemm_bf16_all_shapes(env, mnk):
 
 
 def test_sgemm_ptb_preempt_resume_exactly_once(env):
+    """Preempt the PTB SGEMM at claim counts 37, 200, 311 (device MemTrigger)
+    and resume until done.  Preempted workers stop at a K-chunk boundary and
+    park their fp32 running total in C; the chain's result is bit-identical
+    to the untransformed kernel and every tile is claimed exactly once."""
     P, kernels, stream = env
     M = N = K = 2048
     g = torch.Generator(device="cuda").manual_seed(5)
@@ -88,24 +92,78 @@ def test_sgemm_ptb_preempt_resume_exactly_once(env):
     C = torch.zeros(M, N, device="cuda")
     sg = kernels.sgemm_tf32x3(A, B, C)
     sg.prepare(stream)
-    ref = C.clone()
     sg.gemm.original(stream).wait()
-    ref.copy_(C)
+    ref = C.clone()
     C.zero_()
+    torch.cuda.synchronize()
     total = sg.gemm.total_blocks
     ec = torch.zeros(total, dtype=torch.int64, device="cuda")
-    ctr, hops = 0, 0
-    for c in (37, 200, 311):
+    ctr, hops, parked = 0, 0, 0
+    triggers = [37, 200, 311]
+    while True:
+        c = triggers[hops] if hops < len(triggers) else None
         st = sg.gemm.ptb(stream, 148, start_count=ctr, preempt_at=c, exec_count=ec).wait()
-        assert st.task_counter >= min(c, total)
+        assert st.task_counter >= ctr
         ctr = st.task_counter
         hops += 1
+        parked += st.parked
         if not st.parked:
             break
-    if ctr < total:
-        sg.gemm.ptb(stream, 148, start_count=ctr, exec_count=ec).wait()
+        assert hops < 50
+    assert parked >= 3
+    torch.cuda.synchronize()
     assert bool((ec == 1).all())
     assert torch.equal(C, ref)
+    sg.close()
+
+
+def test_sgemm_chunk_preemption_latency_and_exactness(env):
+    """Host-timed preemptions of a 4096^3 PTB SGEMM at random instants: the
+    chain stays bit-exact and the flag->last-exit latency is a fraction of a
+    tile (chunk granularity, ~1/8 of a 128x64 3xTF32 tile)."""
+    import random
+    P, kernels, stream = env
+    M = N = K = 4096
+    g = torch.Generator(device="cuda").manual_seed(6)
+    A = torch.rand(M, K, device="cuda", generator=g) * 2 - 1
+    B = torch.rand(N, K, device="cuda", generator=g) * 2 - 1
+    C = torch.zeros(M, N, device="cuda")
+    sg = kernels.sgemm_tf32x3(A, B, C)
+    sg.prepare(stream)
+    sg.gemm.original(stream).wait()
+    ref = C.clone()
+    C.zero_()
+    torch.cuda.synchronize()
+    dev = P.B200Device.get()
+    off, _ = dev.clock_offset()
+    total = sg.gemm.total_blocks
+    ec = torch.zeros(total, dtype=torch.int64, device="cuda")
+    rng = random.Random(3)
+    ctr, lat, hops = 0, [], 0
+    while True:
+        L = sg.gemm.ptb(stream, 148, start_count=ctr, exec_count=ec)
+        t_end = P.B200Device.now_ns() + rng.randint(20_000, 120_000)
+        while P.B200Device.now_ns() < t_end and not L.query().done:
+            pass
+        if hops < 12:
+            try:
+                L.preempt()
+            except ValueError:
+                pass
+        st = L.wait()
+        ctr = st.task_counter
+        hops += 1
+        if st.parked:
+            lat.append((st.gt_last_exit + off - st.host_preempt_ns) / 1e3)
+        else:
+            break
+        assert hops < 100
+    torch.cuda.synchronize()
+    assert bool((ec == 1).all())
+    assert torch.equal(C, ref)
+    lat.sort()
+    print(f"sgemm chunk-preemption latency us: median {lat[len(lat) // 2]:.1f} max {lat[-1]:.1f}")
+    assert lat[len(lat) // 2] < 30.0
     sg.close()
 
 
