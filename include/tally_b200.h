@@ -99,6 +99,8 @@ typedef struct {
   int occupancy_original;
   double alg_bytes;         /* algorithmic HBM bytes of one full launch          */
   double alg_flops;         /* algorithmic flops of one full launch              */
+  int preempt_units;        /* PTB preemption points per logical block (>1: chunk-granular
+                               preemption with saved partial state, e.g. sgemm_tf32x3) */
 } tally_kernel_info;
 
 int tally_kernel_kind_count(void);

@@ -298,7 +298,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_gemm(const __grid_constant__ Ge
         tile_coords(t, p, mb, nb);
         for (int c = c0; c < NCH; ++c) {
           if constexpr (kChunkPreempt) {
-            // flag_seen was loaded half a chunk ago; the load has long completed
+            // flag_seen was loaded three k-blocks ago; the L2 load has completed
             if (p.resume != nullptr && c > c0) {
               if (flag_seen == s.serial) {
                 // cut the tile before chunk c: publish the cut, then wake the
@@ -318,8 +318,8 @@ __global__ void __launch_bounds__(kThreads, 1) k_gemm(const __grid_constant__ Ge
             if constexpr (MODE == kPtb) {
               // suspension point between k-blocks (cooperative suspension option)
               if ((kb & 3) == 0 && ptb_hold_while_paused(s)) {}
-              if (kChunkPreempt && p.resume != nullptr && kb == c * p.kchunk + p.kchunk / 2)
-                flag_seen = s.flag_is_host ? ld_relaxed_sys(s.flag) : ld_acquire_gpu(s.flag);
+              if (kChunkPreempt && p.resume != nullptr && kb == max(c * p.kchunk, kb1 - 3))
+                flag_seen = s.flag_is_host ? ld_relaxed_sys(s.flag) : ld_relaxed_gpu(s.flag);
             }
             if (it >= (uint32_t)Cfg::STAGES) mbar_wait(&empty[st], ((it / Cfg::STAGES) - 1) & 1);
             unsigned char* base = smem + (size_t)st * Cfg::STAGE_BYTES;
@@ -627,9 +627,10 @@ static int bind_gemm(const tally_kernel_args* a, Instance* inst, bool split) {
   p.k = (int)K;
   p.tiles_m = (int)(M / Cfg::BM);
   p.tiles_n = (int)(N / Cfg::BN);
-  // promote the tensor-core accumulator to fp32 registers every 512 of K for
-  // the fp32-accuracy kernel; bf16 (1e-2 budget) accumulates the whole K in TMEM
-  p.kchunk = Cfg::KIND == 0 ? 512 / Cfg::BK : (int)(K / Cfg::BK);
+  // fp32 promotion + preemption point every 256 of K for the fp32-accuracy
+  // kernel (16 chunks of ~4.5 us per 4096-deep tile); bf16 (1e-2 budget)
+  // accumulates the whole K in TMEM
+  p.kchunk = Cfg::KIND == 0 ? 256 / Cfg::BK : (int)(K / Cfg::BK);
   p.resume = nullptr;
   if (Cfg::KIND == 0) {
     const size_t bytes = (2 + kResumeCap) * sizeof(unsigned long long);
@@ -638,6 +639,7 @@ static int bind_gemm(const tally_kernel_args* a, Instance* inst, bool split) {
     if (e != cudaSuccess) return cuda_fail(e, "gemm resume ring");
     inst->resume_ring = p.resume;
     inst->resume_bytes = bytes;
+    inst->preempt_units = (int)((K / Cfg::BK + p.kchunk - 1) / p.kchunk);
   }
   static_assert(sizeof(p) <= kMaxParamBytes, "params too large");
   memcpy(inst->params, &p, sizeof(p));
@@ -693,7 +695,9 @@ static KernelKind gemm_kind(const char* name, int (*bind)(const tally_kernel_arg
   k.bind = bind;
   k.setup = &setup_gemm<Cfg>;
   k.pausable = 1;
-  k.host_flag = 1;
+  // device-resident flag: producers poll it every K-chunk (~9 us) -- 148
+  // readers x 110 k reads/s would saturate PCIe reads of a mapped host word
+  k.host_flag = 0;
   return k;
 }
 

@@ -21,6 +21,7 @@ struct Instance {
   size_t smem = 0;             // dynamic shared memory per CTA
   double alg_bytes = 0;        // algorithmic HBM bytes of the whole logical grid
   double alg_flops = 0;        // algorithmic flops of the whole logical grid
+  int preempt_units = 1;       // PTB preemption points per logical block (K-chunks for sgemm_tf32x3)
   void* resume_ring = nullptr; // chunk-preemption resume ring (reset when a PTB chain starts)
   size_t resume_bytes = 0;
   unsigned long long total() const {

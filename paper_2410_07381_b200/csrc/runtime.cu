@@ -767,6 +767,7 @@ int tally_kernel_info_get(int kernel, tally_kernel_info* o) {
   o->smem_bytes = (long long)in.smem;
   o->alg_bytes = in.alg_bytes;
   o->alg_flops = in.alg_flops;
+  o->preempt_units = in.preempt_units;
   int occ = 0;
   if (kk.copy) return TALLY_OK;
   if (kk.jit) {

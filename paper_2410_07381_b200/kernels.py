@@ -132,6 +132,7 @@ class KernelInfo:
     occupancy_original: int
     alg_bytes: float
     alg_flops: float
+    preempt_units: int = 1
 
 
 class DeviceKernel:
@@ -155,7 +156,8 @@ class DeviceKernel:
         _lib.check(_lib.lib.tally_kernel_info_get(self.id, C.byref(ki)), "kernel info")
         self.info = KernelInfo((ki.grid_x, ki.grid_y, ki.grid_z), ki.total_blocks,
                                ki.threads_per_block, ki.smem_bytes, ki.occupancy_ptb,
-                               ki.occupancy_original, ki.alg_bytes, ki.alg_flops)
+                               ki.occupancy_original, ki.alg_bytes, ki.alg_flops,
+                               max(1, ki.preempt_units))
 
     @property
     def total_blocks(self) -> int:
