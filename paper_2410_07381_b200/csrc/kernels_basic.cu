@@ -159,6 +159,41 @@ static int bind_rowsum_f32(const tally_kernel_args* a, Instance* inst) {
   return TALLY_OK;
 }
 
+// ---------------------------------------------------------------- spin
+// A cost-model kernel: every logical block occupies its CTA slot for exactly
+// block_ns of device time.  It runs the reference's abstract workloads
+// (KernelCostModel: blocks x threads x block duration, ref sim.py:77-111) on
+// the real GPU, in all three shapes, so configs written for the simulator
+// execute on the B200 through the same scheduler (cli.py).
+struct SpinKernel {
+  static constexpr int kThreads = 1024;   // upper bound; launched with the model's tpb
+  struct Params {
+    long long block_ns;
+  };
+  static __device__ __forceinline__ void run(const Params& p, uint3, uint3, char*) {
+    if (threadIdx.x == 0) {
+      const unsigned long long t0 = globaltimer();
+      while (globaltimer() - t0 < (unsigned long long)p.block_ns) __nanosleep(128);
+    }
+    __syncthreads();
+  }
+};
+
+static int bind_spin(const tally_kernel_args* a, Instance* inst) {
+  SpinKernel::Params p{};
+  const long long blocks = a->i[0], tpb = a->i[1];
+  p.block_ns = a->i[2];
+  if (blocks < 1 || blocks > 0x7fffffffLL || tpb < 1 || tpb > 1024 || p.block_ns < 0) {
+    set_error("spin: need 1 <= blocks, 1 <= threads_per_block <= 1024, block_ns >= 0");
+    return TALLY_EINVAL;
+  }
+  memcpy(inst->params, &p, sizeof(p));
+  inst->grid = make_uint3((unsigned)blocks, 1, 1);
+  inst->threads = (int)tpb;
+  inst->smem = 0;
+  return TALLY_OK;
+}
+
 template <class B>
 static KernelKind make_kind(const char* name, int (*bind)(const tally_kernel_args*, Instance*)) {
   KernelKind k{};
@@ -172,11 +207,12 @@ static KernelKind make_kind(const char* name, int (*bind)(const tally_kernel_arg
 }
 
 int register_basic_kernels(KernelKind* out, int cap) {
-  if (cap < 3) return 0;
+  if (cap < 4) return 0;
   out[0] = make_kind<VecAddI64>("vecadd_i64", bind_vecadd_i64);
   out[1] = make_kind<VecAddF32>("vecadd_f32", bind_vecadd_f32);
   out[2] = make_kind<RowSumF32>("rowsum_f32", bind_rowsum_f32);
-  return 3;
+  out[3] = make_kind<SpinKernel>("spin", bind_spin);
+  return 4;
 }
 
 }  // namespace tally

@@ -302,3 +302,10 @@ def cuda_graph(graph) -> DeviceKernel:
     ``cudaGraphLaunch`` on the scheduler's stream of its priority."""
     exec_handle = graph.raw_cuda_graph_exec() if hasattr(graph, "raw_cuda_graph_exec") else int(graph)
     return DeviceKernel("cuda_graph", (int(exec_handle),), (), keep=(graph,))
+
+
+def spin(total_blocks: int, threads_per_block: int, block_duration_ns: int) -> DeviceKernel:
+    """A cost-model kernel (ref ``KernelCostModel``): ``total_blocks`` logical
+    blocks of ``threads_per_block`` threads, each holding its slot for
+    ``block_duration_ns`` -- the reference's abstract workloads on the GPU."""
+    return DeviceKernel("spin", (), (total_blocks, threads_per_block, block_duration_ns))
