@@ -320,9 +320,20 @@ def main_ours(args):
     co_lat = [x for r in results for x in lat_after_warm(r)]
     be_co = sum(be_rate(r) for r in results) / len(results)
     overhead = 100.0 * (p99(co_lat) / p99(solo_lat) - 1.0)
-    pre = [r for res in results for r in res.launches if r["preempt_ns"] >= 0 and r["parked"]]
-    origin = {id(r): res.origin_ns for res in results for r in res.launches}
-    pl_us = [(r["gt_last_exit"] + off - (r["preempt_ns"] + origin[id(r)])) / 1e3 for r in pre]
+    def preempt_latencies(res_list):
+        """Host signal -> last worker exit, for PTB launches already running
+        on the device when the flag was raised (queued launches that see the
+        flag at start are not preemptions)."""
+        out = []
+        for res in res_list:
+            for r in res.launches:
+                if r["preempt_ns"] < 0 or not r["parked"]:
+                    continue
+                sig = r["preempt_ns"] + res.origin_ns
+                if r["gt_first_start"] and r["gt_first_start"] + off < sig:
+                    out.append((r["gt_last_exit"] + off - sig) / 1e3)
+        return out
+    pl_us = preempt_latencies(results)
     launches = sum(len(r.launches) for r in results)
     n_be = sum(1 for r in results for x in r.launches if x["priority"] == 1)
 
@@ -426,6 +437,25 @@ def main_ours(args):
                 run_([hp_task(k)], cfg, window, profiler=prof, record_events=False))]
             baselines[pol] = {"p99_overhead_pct": 100.0 * (p99(lat) / p99(sl) - 1.0),
                               "be_throughput_pct": 100.0 * (sum(rate) / len(rate)) / be_untransformed}
+        # the same Tally policy with tile-granular (block-level, as in the
+        # paper) PTB preemption of the SGEMM instead of chunk-granular
+        sg_blk = kernels.sgemm_tf32x3(A, B, C, chunk_preempt=False)
+        blk_ws = be_ws[:2] + (P.KernelWork("sgemm_tf32x3_4096_tile_preempt", sg_blk.gemm.cost(),
+                                           kernel=sg_blk.gemm),)
+        prof.bind(blk_ws[2].kernel_id, sg_blk.gemm)
+        blk_task = P.TaskScript("be", P.BEST_EFFORT, blk_ws)
+        lat, rate, res_b = [], [], []
+        for k in range(args.steps):
+            r = run_([hp_task(k), blk_task], tally, window, profiler=prof, record_events=False)
+            res_b.append(r)
+            lat += lat_after_warm(r)
+            rate.append(be_rate(r))
+        pb = preempt_latencies(res_b)
+        baselines["Tally_tile_granular_PTB"] = {
+            "p99_overhead_pct": 100.0 * (p99(lat) / p99(solo_lat) - 1.0),
+            "be_throughput_pct": 100.0 * (sum(rate) / len(rate)) / be_untransformed,
+            "preempt_latency_us_p50_p99": [pct(pb, 0.5), pct(pb, 0.99)] if pb else None,
+            "tuner_choice": prof.select(blk_ws[2].profile_key(), blk_ws[2].cost, threshold).describe()}
 
     # --- CPU baseline: the reference algorithm on the host -------------------------
     cpu = None

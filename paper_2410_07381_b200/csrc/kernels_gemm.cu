@@ -632,7 +632,8 @@ static int bind_gemm(const tally_kernel_args* a, Instance* inst, bool split) {
   // accumulates the whole K in TMEM
   p.kchunk = Cfg::KIND == 0 ? 256 / Cfg::BK : (int)(K / Cfg::BK);
   p.resume = nullptr;
-  if (Cfg::KIND == 0) {
+  // i[3] = 1: block-granular preemption only (no resume ring)
+  if (Cfg::KIND == 0 && a->i[3] == 0) {
     const size_t bytes = (2 + kResumeCap) * sizeof(unsigned long long);
     cudaError_t e = cudaMalloc(&p.resume, bytes);
     if (e == cudaSuccess) e = cudaMemset(p.resume, 0, bytes);
