@@ -439,6 +439,7 @@ def main_ours(args):
                               "be_throughput_pct": 100.0 * (sum(rate) / len(rate)) / be_untransformed}
         # the same Tally policy with tile-granular (block-level, as in the
         # paper) PTB preemption of the SGEMM instead of chunk-granular
+        off, _unc = dev.clock_offset()      # re-anchor: globaltimer drifts vs CLOCK_MONOTONIC
         sg_blk = kernels.sgemm_tf32x3(A, B, C, chunk_preempt=False)
         blk_ws = be_ws[:2] + (P.KernelWork("sgemm_tf32x3_4096_tile_preempt", sg_blk.gemm.cost(),
                                            kernel=sg_blk.gemm),)

@@ -140,20 +140,25 @@ __device__ __forceinline__ void tmem_ld32(uint32_t taddr, uint32_t (&r)[32]) {
 }
 
 // ---------------------------------------------------------------- configs
-struct CfgTf32x3 {
+template <int BN_, int STAGES_>
+struct CfgTf32x3T {
   static constexpr int KIND = 0;
-  static constexpr int BM = 128, BN = 64;
+  static constexpr int BM = 128, BN = BN_;
   static constexpr int BK = 32;                       // fp32 elements = 128 B (one swizzle atom)
   static constexpr int ESZ = 4;
   static constexpr int NOPS = 4;                      // Ahi, Alo, Bhi, Blo
   static constexpr int A_BYTES = BM * BK * ESZ;       // 16 KB
-  static constexpr int B_BYTES = BN * BK * ESZ;       // 8 KB
-  static constexpr int STAGE_BYTES = 2 * A_BYTES + 2 * B_BYTES;   // 48 KB
-  static constexpr int STAGES = 4;
+  static constexpr int B_BYTES = BN * BK * ESZ;       // 8 / 16 KB
+  static constexpr int STAGE_BYTES = 2 * A_BYTES + 2 * B_BYTES;   // 48 / 64 KB
+  static constexpr int STAGES = STAGES_;
   static constexpr int UMMA_K = 8;
-  static constexpr int TMEM_COLS = 256;               // 2 x BN accumulators + BN running total
+  static constexpr int TMEM_COLS = BN == 64 ? 256 : 512;   // 2 x BN accumulators + BN running total
   using OutT = float;
 };
+// 128x128 tiles halve L2->SM operand bytes per flop (the kernel is L2-bound);
+// chunk-granular preemption keeps the preemption latency independent of the tile
+using CfgTf32x3 = CfgTf32x3T<128, 3>;
+using CfgTf32x3N64 = CfgTf32x3T<64, 4>;
 
 struct CfgBf16 {
   static constexpr int KIND = 1;
@@ -654,6 +659,9 @@ static int bind_gemm(const tally_kernel_args* a, Instance* inst, bool split) {
 }
 
 static int bind_sgemm(const tally_kernel_args* a, Instance* inst) { return bind_gemm<gemm::CfgTf32x3>(a, inst, true); }
+static int bind_sgemm_n64(const tally_kernel_args* a, Instance* inst) {
+  return bind_gemm<gemm::CfgTf32x3N64>(a, inst, true);
+}
 static int bind_bf16(const tally_kernel_args* a, Instance* inst) { return bind_gemm<gemm::CfgBf16>(a, inst, false); }
 
 template <class Cfg>
@@ -703,9 +711,10 @@ static KernelKind gemm_kind(const char* name, int (*bind)(const tally_kernel_arg
 }
 
 int register_gemm_kernels(KernelKind* out, int cap) {
-  if (cap < 3) return 0;
+  if (cap < 4) return 0;
   out[0] = gemm_kind<gemm::CfgTf32x3>("sgemm_tf32x3", bind_sgemm);
   out[1] = gemm_kind<gemm::CfgBf16>("gemm_bf16", bind_bf16);
+  out[3] = gemm_kind<gemm::CfgTf32x3N64>("sgemm_tf32x3_n64", bind_sgemm_n64);
   KernelKind k{};
   k.name = "split_tf32";
   k.fn_original = reinterpret_cast<const void*>(&k_original<gemm::SplitTf32>);
@@ -713,7 +722,7 @@ int register_gemm_kernels(KernelKind* out, int cap) {
   k.fn_ptb = reinterpret_cast<const void*>(&k_ptb<gemm::SplitTf32>);
   k.bind = bind_split;
   out[2] = k;
-  return 3;
+  return 4;
 }
 
 }  // namespace tally

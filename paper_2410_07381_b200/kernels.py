@@ -247,7 +247,7 @@ class Sgemm3xTf32:
     them in order -- one BE training "step" of the SGEMM workload.
     """
 
-    def __init__(self, A, B, C, chunk_preempt: bool = True):
+    def __init__(self, A, B, C, chunk_preempt: bool = True, tile_n: int = 128):
         import torch
         M, K = A.shape
         N, K2 = B.shape
@@ -259,7 +259,8 @@ class Sgemm3xTf32:
         self.b_hi, self.b_lo = torch.empty_like(B), torch.empty_like(B)
         self.split_a = DeviceKernel("split_tf32", (A, self.a_hi, self.a_lo), (A.numel(),))
         self.split_b = DeviceKernel("split_tf32", (B, self.b_hi, self.b_lo), (B.numel(),))
-        self.gemm = DeviceKernel("sgemm_tf32x3", (self.a_hi, self.a_lo, self.b_hi, self.b_lo, C),
+        kind = {128: "sgemm_tf32x3", 64: "sgemm_tf32x3_n64"}[tile_n]
+        self.gemm = DeviceKernel(kind, (self.a_hi, self.a_lo, self.b_hi, self.b_lo, C),
                                  (M, N, K, 0 if chunk_preempt else 1))
         self.pipeline = (self.split_a, self.split_b, self.gemm)
 
@@ -273,10 +274,10 @@ class Sgemm3xTf32:
             k.close()
 
 
-def sgemm_tf32x3(A, B, C, chunk_preempt: bool = True) -> Sgemm3xTf32:
+def sgemm_tf32x3(A, B, C, chunk_preempt: bool = True, tile_n: int = 128) -> Sgemm3xTf32:
     """``chunk_preempt``: PTB workers yield at every 256-deep K chunk, saving
     the fp32 partial tile (default); False = block (tile) granularity only."""
-    return Sgemm3xTf32(A, B, C, chunk_preempt)
+    return Sgemm3xTf32(A, B, C, chunk_preempt, tile_n)
 
 
 def gemm_bf16(A, B, C) -> DeviceKernel:

@@ -30,11 +30,12 @@ def make(kind):
     if kind == "rowsum_f32":
         x = torch.rand(1 << 16, 1024, device="cuda", generator=g)
         return kernels.rowsum_f32(x, torch.zeros(1 << 16, device="cuda"))
-    if kind == "sgemm_tf32x3":
+    if kind.startswith("sgemm_tf32x3"):
         m = 4096
         A = torch.rand(m, m, device="cuda", generator=g) * 2 - 1
         B = torch.rand(m, m, device="cuda", generator=g) * 2 - 1
-        sg = kernels.sgemm_tf32x3(A, B, torch.zeros(m, m, device="cuda"))
+        sg = kernels.sgemm_tf32x3(A, B, torch.zeros(m, m, device="cuda"),
+                                  tile_n=64 if kind.endswith("n64") else 128)
         sg.prepare(kernels.Stream(high_priority=False))
         sg.gemm._owner = sg
         return sg.gemm
