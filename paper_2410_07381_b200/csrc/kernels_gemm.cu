@@ -160,20 +160,32 @@ struct CfgTf32x3T {
 using CfgTf32x3 = CfgTf32x3T<128, 3>;
 using CfgTf32x3N64 = CfgTf32x3T<64, 4>;
 
-struct CfgBf16 {
+// bf16 operands, fp32 TMEM accumulation; BN = 128 or 64 (N % 128 != 0, e.g.
+// 64-channel convolutions), output bf16 (activations) or fp32 (split-K
+// weight-gradient partials, logits)
+template <int BN_, class OutT_>
+struct CfgBf16T {
   static constexpr int KIND = 1;
-  static constexpr int BM = 128, BN = 128;
+  static constexpr int BM = 128, BN = BN_;
   static constexpr int BK = 64;                       // bf16 elements = 128 B
   static constexpr int ESZ = 2;
   static constexpr int NOPS = 2;
   static constexpr int A_BYTES = BM * BK * ESZ;       // 16 KB
-  static constexpr int B_BYTES = BN * BK * ESZ;       // 16 KB
+  static constexpr int B_BYTES = BN * BK * ESZ;       // 16 / 8 KB
   static constexpr int STAGE_BYTES = A_BYTES + B_BYTES;
-  static constexpr int STAGES = 6;
+  // 128 KB / 120 KB of operand ring: room for co-resident high-priority CTAs
+  static constexpr int STAGES = BN == 128 ? 4 : 5;
   static constexpr int UMMA_K = 16;
-  static constexpr int TMEM_COLS = 512;               // 2 x BN accumulators + BN running total
-  using OutT = __nv_bfloat16;
+  // the whole (split) K range accumulates in one TMEM buffer (no fp32
+  // promotion chunks at the 1e-2 bf16 budget): 2 x BN columns, leaving TMEM
+  // for co-resident high-priority tensor-core kernels
+  static constexpr int TMEM_COLS = 2 * BN;
+  using OutT = OutT_;
 };
+using CfgBf16 = CfgBf16T<128, __nv_bfloat16>;
+using CfgBf16N64 = CfgBf16T<64, __nv_bfloat16>;
+using CfgBf16F32 = CfgBf16T<128, float>;
+using CfgBf16F32N64 = CfgBf16T<64, float>;
 
 constexpr int GROUP_M = 8;
 constexpr int kThreads = 192;   // producer warp, MMA warp, 4 epilogue warps
@@ -190,6 +202,10 @@ struct alignas(64) GemmParams {
   int tiles_m, tiles_n;
   int kchunk;   // k-blocks per TMEM accumulation chunk (promotion to fp32 registers)
   unsigned long long* resume;   // chunk-preemption resume ring (sgemm_tf32x3), see tally_device.cuh
+  long long ldc;                // row stride of C (elements)
+  long long split_stride;       // elements between split-K partial outputs
+  int splits;                   // split-K factor: logical block = (split, tile)
+  int kb_per_split;             // k-blocks per split
 };
 
 __device__ __forceinline__ void tile_coords(long long t, const GemmParams& p, int& mb, int& nb) {
@@ -201,6 +217,23 @@ __device__ __forceinline__ void tile_coords(long long t, const GemmParams& p, in
   const int r = (int)(t % per_group);
   mb = first_m + r % gm;
   nb = r / gm;
+}
+
+// Logical block t -> (output tile, K range).  With split-K the block index is
+// split-major: t = split * tiles + tile; split s covers k-blocks
+// [s * kb_per_split, min(KB, (s + 1) * kb_per_split)).
+struct TileWork {
+  int mb, nb, split, kbeg, kend, nch;
+};
+__device__ __forceinline__ TileWork tile_work(long long t, const GemmParams& p, int KB) {
+  TileWork w;
+  const long long tiles = (long long)p.tiles_m * p.tiles_n;
+  w.split = (int)(t / tiles);
+  tile_coords(t - (long long)w.split * tiles, p, w.mb, w.nb);
+  w.kbeg = w.split * p.kb_per_split;
+  w.kend = min(KB, w.kbeg + p.kb_per_split);
+  w.nch = (w.kend - w.kbeg + p.kchunk - 1) / p.kchunk;
+  return w;
 }
 
 template <class Cfg, int MODE, class ShapeArgs>
@@ -219,7 +252,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_gemm(const __grid_constant__ Ge
   uint32_t* tmem_base_slot = reinterpret_cast<uint32_t*>(tile_cut + 2);
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int KB = p.k / Cfg::BK;
+  const int KB = (p.k + Cfg::BK - 1) / Cfg::BK;
 
   unsigned long long t_entry = 0;
   if (threadIdx.x == 0) {
@@ -243,7 +276,6 @@ __global__ void __launch_bounds__(kThreads, 1) k_gemm(const __grid_constant__ Ge
   fence_after();
   const uint32_t tmem_base = *tmem_base_slot;
   bool stopped = false;
-  const int NCH = (KB + p.kchunk - 1) / p.kchunk;   // accumulation chunks per tile
   // chunk-granular preemption (fp32-output kernels in PTB shape with a resume
   // ring): a preempted worker stops its tile at the next chunk boundary,
   // saves the fp32 running total into its C tile and queues (tile, chunk)
@@ -296,12 +328,12 @@ __global__ void __launch_bounds__(kThreads, 1) k_gemm(const __grid_constant__ Ge
         if (i >= 2) mbar_wait(&tile_empty[j], ((i >> 1) - 1) & 1);
         tile_slot[j] = t;
         tile_c0[j] = c0;
-        tile_cut[j] = NCH;
+        const TileWork w = tile_work(t < 0 ? 0 : t, p, KB);
+        tile_cut[j] = w.nch;
         mbar_arrive(&tile_full[j]);
         if (t < 0) break;
-        int mb, nb;
-        tile_coords(t, p, mb, nb);
-        for (int c = c0; c < NCH; ++c) {
+        const int mb = w.mb, nb = w.nb;
+        for (int c = c0; c < w.nch; ++c) {
           if constexpr (kChunkPreempt) {
             // flag_seen was loaded three k-blocks ago; the L2 load has completed
             if (p.resume != nullptr && c > c0) {
@@ -317,13 +349,13 @@ __global__ void __launch_bounds__(kThreads, 1) k_gemm(const __grid_constant__ Ge
               }
             }
           }
-          const int kb1 = min(KB, (c + 1) * p.kchunk);
-          for (int kb = c * p.kchunk; kb < kb1; ++kb, ++it) {
+          const int kb1 = min(w.kend, w.kbeg + (c + 1) * p.kchunk);
+          for (int kb = w.kbeg + c * p.kchunk; kb < kb1; ++kb, ++it) {
             const int st = it % Cfg::STAGES;
             if constexpr (MODE == kPtb) {
               // suspension point between k-blocks (cooperative suspension option)
               if ((kb & 3) == 0 && ptb_hold_while_paused(s)) {}
-              if (kChunkPreempt && p.resume != nullptr && kb == max(c * p.kchunk, kb1 - 3))
+              if (kChunkPreempt && p.resume != nullptr && kb == max(w.kbeg + c * p.kchunk, kb1 - 3))
                 flag_seen = s.flag_is_host ? ld_relaxed_sys(s.flag) : ld_relaxed_gpu(s.flag);
             }
             if (it >= (uint32_t)Cfg::STAGES) mbar_wait(&empty[st], ((it / Cfg::STAGES) - 1) & 1);
@@ -361,12 +393,13 @@ __global__ void __launch_bounds__(kThreads, 1) k_gemm(const __grid_constant__ Ge
           mbar_arrive(&tile_empty[j]);
           break;
         }
-        for (int c = c0; c < NCH; ++c, ++ci) {
+        const TileWork w = tile_work(t, p, KB);
+        for (int c = c0; c < w.nch; ++c, ++ci) {
           const int acc = ci & 1;
           if (ci >= 2) mbar_wait(&tmem_empty[acc], ((ci >> 1) - 1) & 1);
           fence_after();
           const uint32_t d = tmem_base + (uint32_t)(acc * Cfg::BN);
-          const int kb0 = c * p.kchunk, kb1 = min(KB, kb0 + p.kchunk);
+          const int kb0 = w.kbeg + c * p.kchunk, kb1 = min(w.kend, kb0 + p.kchunk);
           bool cut = false;
           for (int kb = kb0; kb < kb1; ++kb, ++it) {
             const int st = it % Cfg::STAGES;
@@ -421,12 +454,13 @@ __global__ void __launch_bounds__(kThreads, 1) k_gemm(const __grid_constant__ Ge
         if (lane == 0) mbar_arrive(&tile_empty[j]);
         break;
       }
-      int mb, nb;
-      tile_coords(t, p, mb, nb);
-      const int row = mb * Cfg::BM + q * 32 + lane;
-      typename Cfg::OutT* crow = reinterpret_cast<typename Cfg::OutT*>(p.c) + (size_t)row * p.n + (size_t)nb * Cfg::BN;
+      const TileWork w = tile_work(t, p, KB);
+      const int row = w.mb * Cfg::BM + q * 32 + lane;
+      const bool row_ok = row < p.m;   // M tail: TMA zero-fills the rows past M, stores skip them
+      typename Cfg::OutT* crow = reinterpret_cast<typename Cfg::OutT*>(p.c) + (size_t)w.split * p.split_stride +
+                                 (size_t)(row_ok ? row : 0) * p.ldc + (size_t)w.nb * Cfg::BN;
       const uint32_t lane_base = tmem_base + ((uint32_t)(q * 32) << 16);
-      for (int c = c0; c < NCH; ++c, ++ci) {
+      for (int c = c0; c < w.nch; ++c, ++ci) {
         const int acc = ci & 1;
         mbar_wait(&tmem_full[acc], (ci >> 1) & 1);
         fence_after();
@@ -459,7 +493,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_gemm(const __grid_constant__ Ge
           ++ci;
           break;
         }
-        const bool last = (c == NCH - 1);
+        const bool last = (c == w.nch - 1);
 #pragma unroll 1
         for (int c1 = 0; c1 < Cfg::BN; c1 += 32) {
           // chunk partial + running fp32 total (kept in TMEM columns [2BN, 3BN))
@@ -486,7 +520,8 @@ __global__ void __launch_bounds__(kThreads, 1) k_gemm(const __grid_constant__ Ge
           }
           if (!last) {
             tmem_st32(lane_base + (uint32_t)(2 * Cfg::BN + c1), r);
-          } else if constexpr (Cfg::KIND == 0) {
+          } else if (!row_ok) {
+          } else if constexpr (sizeof(typename Cfg::OutT) == 4) {
             float4* dst = reinterpret_cast<float4*>(crow + c1);
 #pragma unroll
             for (int v = 0; v < 8; ++v)
@@ -603,9 +638,20 @@ static int bind_gemm(const tally_kernel_args* a, Instance* inst, bool split) {
   gemm::GemmParams p;
   memset(&p, 0, sizeof(p));
   const long long M = a->i[0], N = a->i[1], K = a->i[2];
-  if (M < 1 || N < 1 || K < 1 || M % Cfg::BM || N % Cfg::BN || K % Cfg::BK) {
-    set_error("gemm: need M %% %d == 0, N %% %d == 0, K %% %d == 0 (got %lld %lld %lld)", Cfg::BM, Cfg::BN,
-              Cfg::BK, M, N, K);
+  const long long splits = a->i[4] > 0 ? a->i[4] : 1;
+  // bf16 kinds take any M (row tail); the 3xTF32 kind keeps whole tiles
+  // (K tail: TMA zero-fills the k-block past K in both operands; rows must
+  // stay 16-byte aligned for the tensor map)
+  const bool m_ok = Cfg::KIND == 1 ? true : (M % Cfg::BM == 0);
+  const bool k_ok = Cfg::KIND == 1 ? (K % 8 == 0) : (K % Cfg::BK == 0);
+  if (M < 1 || N < 1 || K < 1 || !m_ok || N % Cfg::BN || !k_ok) {
+    set_error("gemm: need M %s, N %% %d == 0, K %s (got %lld %lld %lld)",
+              Cfg::KIND == 1 ? ">= 1" : "% 128 == 0", Cfg::BN, Cfg::KIND == 1 ? "% 8 == 0" : "% 32 == 0", M, N, K);
+    return TALLY_EINVAL;
+  }
+  const long long KBlocks = (K + Cfg::BK - 1) / Cfg::BK;
+  if (splits > KBlocks || (Cfg::KIND == 0 && splits != 1) || (splits > 1 && sizeof(typename Cfg::OutT) != 4)) {
+    set_error("gemm: split-K needs fp32 output, 1 <= splits <= K / %d (got %lld)", Cfg::BK, splits);
     return TALLY_EINVAL;
   }
   const int nptr = split ? 5 : 3;
@@ -630,12 +676,21 @@ static int bind_gemm(const tally_kernel_args* a, Instance* inst, bool split) {
   p.m = (int)M;
   p.n = (int)N;
   p.k = (int)K;
-  p.tiles_m = (int)(M / Cfg::BM);
+  p.tiles_m = (int)((M + Cfg::BM - 1) / Cfg::BM);
   p.tiles_n = (int)(N / Cfg::BN);
+  p.ldc = N;
+  p.split_stride = M * N;
+  p.splits = (int)splits;
+  p.kb_per_split = (int)((KBlocks + splits - 1) / splits);
+  if ((KBlocks + p.kb_per_split - 1) / p.kb_per_split != splits) {
+    set_error("gemm: %lld splits of %lld k-blocks leave an empty split (use ceil(KB / ceil(KB / splits)))",
+              splits, KBlocks);
+    return TALLY_EINVAL;
+  }
   // fp32 promotion + preemption point every 256 of K for the fp32-accuracy
   // kernel (16 chunks of ~4.5 us per 4096-deep tile); bf16 (1e-2 budget)
   // accumulates the whole K in TMEM
-  p.kchunk = Cfg::KIND == 0 ? 256 / Cfg::BK : (int)(K / Cfg::BK);
+  p.kchunk = Cfg::KIND == 0 ? 256 / Cfg::BK : p.kb_per_split;
   p.resume = nullptr;
   // i[3] = 1: block-granular preemption only (no resume ring)
   if (Cfg::KIND == 0 && a->i[3] == 0) {
@@ -649,12 +704,12 @@ static int bind_gemm(const tally_kernel_args* a, Instance* inst, bool split) {
   }
   static_assert(sizeof(p) <= kMaxParamBytes, "params too large");
   memcpy(inst->params, &p, sizeof(p));
-  inst->grid = make_uint3((unsigned)(p.tiles_m * p.tiles_n), 1, 1);
+  inst->grid = make_uint3((unsigned)(p.tiles_m * p.tiles_n * p.splits), 1, 1);
   inst->threads = gemm::kThreads;
   inst->smem = gemm::smem_bytes<Cfg>();
   inst->alg_flops = 2.0 * (double)M * (double)N * (double)K;
   inst->alg_bytes = (double)Cfg::ESZ * (double)(M * K + N * K) * (split ? 2.0 : 1.0) +
-                    (double)sizeof(typename Cfg::OutT) * (double)(M * N);
+                    (double)sizeof(typename Cfg::OutT) * (double)(M * N) * (double)splits;
   return TALLY_OK;
 }
 
@@ -662,7 +717,8 @@ static int bind_sgemm(const tally_kernel_args* a, Instance* inst) { return bind_
 static int bind_sgemm_n64(const tally_kernel_args* a, Instance* inst) {
   return bind_gemm<gemm::CfgTf32x3N64>(a, inst, true);
 }
-static int bind_bf16(const tally_kernel_args* a, Instance* inst) { return bind_gemm<gemm::CfgBf16>(a, inst, false); }
+template <class Cfg>
+static int bind_bf16(const tally_kernel_args* a, Instance* inst) { return bind_gemm<Cfg>(a, inst, false); }
 
 template <class Cfg>
 static int setup_gemm() {
@@ -711,10 +767,13 @@ static KernelKind gemm_kind(const char* name, int (*bind)(const tally_kernel_arg
 }
 
 int register_gemm_kernels(KernelKind* out, int cap) {
-  if (cap < 4) return 0;
+  if (cap < 7) return 0;
   out[0] = gemm_kind<gemm::CfgTf32x3>("sgemm_tf32x3", bind_sgemm);
-  out[1] = gemm_kind<gemm::CfgBf16>("gemm_bf16", bind_bf16);
+  out[1] = gemm_kind<gemm::CfgBf16>("gemm_bf16", bind_bf16<gemm::CfgBf16>);
   out[3] = gemm_kind<gemm::CfgTf32x3N64>("sgemm_tf32x3_n64", bind_sgemm_n64);
+  out[4] = gemm_kind<gemm::CfgBf16N64>("gemm_bf16_n64", bind_bf16<gemm::CfgBf16N64>);
+  out[5] = gemm_kind<gemm::CfgBf16F32>("gemm_bf16f32", bind_bf16<gemm::CfgBf16F32>);
+  out[6] = gemm_kind<gemm::CfgBf16F32N64>("gemm_bf16f32_n64", bind_bf16<gemm::CfgBf16F32N64>);
   KernelKind k{};
   k.name = "split_tf32";
   k.fn_original = reinterpret_cast<const void*>(&k_original<gemm::SplitTf32>);
@@ -722,7 +781,7 @@ int register_gemm_kernels(KernelKind* out, int cap) {
   k.fn_ptb = reinterpret_cast<const void*>(&k_ptb<gemm::SplitTf32>);
   k.bind = bind_split;
   out[2] = k;
-  return 4;
+  return 7;
 }
 
 }  // namespace tally

@@ -1,0 +1,959 @@
+// Best-effort training kernels (config C2: ResNet-50 training, BASELINE.json
+// configs[1]) in the three Tally launch shapes -- the "coalesced/vectorised
+// elementwise and reduction kernels" of the north star.  The dense
+// contractions (convolutions as GEMMs, the classifier) run on the tcgen05
+// GEMM kinds in kernels_gemm.cu.
+//
+// Layout: activations are NHWC bf16, i.e. a [P = N*H*W, C] row-major matrix;
+// every kernel moves 16 B (8 x bf16) vectors and needs C % 8 == 0 (the input
+// image is stored with 8 channels, 3 real + 5 zero).  Reductions are
+// deterministic (fixed per-block partials, fixed-order finalisation), so every
+// launch shape produces bit-identical results.
+//
+//   im2col_bf16     x[N,H,W,C] -> col[N*OH*OW, Kp], k = (kh*KW + kw)*C + c, zero pad
+//   col2im_bf16     dcol -> dx (gather form: each input vector sums the col
+//                   entries it fed), fp32 accumulation
+//   transpose_bf16  [R, C] -> [C, R], 64x64 tiles through shared memory
+//   bn_stats        per-(row block, channel) partial sums: mode 0 (x, x^2),
+//                   mode 1 (dz, dz*xhat) with dz = (g [+ g2]) * (y > 0)
+//   bn_finalize     partials -> mean/invstd/scale/shift (mode 0) or
+//                   dgamma/dbeta and the backward coefficients (mode 1)
+//   bn_act          y = act(x*scale + shift [+ residual])
+//   bn_bwd          dx = gamma*invstd*(dz - k1 - xhat*k2), optional dz output
+//   maxpool_fwd/bwd 3x3 stride 2 pad 1 with an argmax byte per output element
+//   avgpool_fwd/bwd global average pool [N, HW, C] <-> [N, C]
+//   softmax_xent    logits(+bias) -> per-row loss, dlogits (bf16 and fp32)
+//   sgd_update      momentum SGD over a table of parameter segments; sums
+//                   split-K gradient partials; refreshes the bf16 weight
+//                   copies (row-major and transposed) the GEMMs read
+#include <cuda_bf16.h>
+
+#include <cstdio>
+
+#include "registry.h"
+
+namespace tally {
+
+namespace nn {
+
+__device__ __forceinline__ void unpack8(const uint4 v, float (&f)[8]) {
+  const __nv_bfloat162* h = reinterpret_cast<const __nv_bfloat162*>(&v);
+#pragma unroll
+  for (int i = 0; i < 4; ++i) {
+    const float2 t = __bfloat1622float2(h[i]);
+    f[2 * i] = t.x;
+    f[2 * i + 1] = t.y;
+  }
+}
+
+__device__ __forceinline__ uint4 pack8(const float (&f)[8]) {
+  uint4 v;
+  uint32_t* w = reinterpret_cast<uint32_t*>(&v);
+#pragma unroll
+  for (int i = 0; i < 4; ++i) {
+    __nv_bfloat162 h = __floats2bfloat162_rn(f[2 * i], f[2 * i + 1]);
+    w[i] = *reinterpret_cast<uint32_t*>(&h);
+  }
+  return v;
+}
+
+__device__ __forceinline__ uint4 ld16(const uint4* p) {
+  uint4 v;
+  asm volatile("ld.global.nc.L1::no_allocate.v4.u32 {%0, %1, %2, %3}, [%4];"
+               : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w) : "l"(p));
+  return v;
+}
+
+constexpr int kVecPerBlock = 2048;   // 32 KB of bf16 per logical block for the elementwise kinds
+
+// ---------------------------------------------------------------- im2col
+struct Geometry {
+  int N, H, W, C;        // input
+  int KH, KW, stride, pad;
+  int OH, OW;            // output spatial
+  int K, Kp;             // K = KH*KW*C, Kp = K rounded up to 64
+};
+
+struct Im2Col {
+  static constexpr int kThreads = 256;
+  struct Params {
+    const uint4* x;
+    uint4* col;
+    Geometry g;
+    long long rows;   // N*OH*OW
+    int rpb;          // output rows per logical block
+  };
+  static __device__ __forceinline__ void run(const Params& p, uint3 bidx, uint3, char*) {
+    const Geometry& g = p.g;
+    const int kv = g.Kp >> 3, cv = g.C >> 3;
+    const long long r0 = (long long)bidx.x * p.rpb;
+    const int total = p.rpb * kv;
+    for (int i = threadIdx.x; i < total; i += kThreads) {
+      const int rr = i / kv, j = i - rr * kv;
+      const long long r = r0 + rr;
+      if (r >= p.rows) break;
+      uint4 v = make_uint4(0u, 0u, 0u, 0u);
+      const int k = j << 3;
+      if (k < g.K) {
+        const int ow = (int)(r % g.OW);
+        const long long t = r / g.OW;
+        const int oh = (int)(t % g.OH);
+        const int n = (int)(t / g.OH);
+        const int kwc = g.KW * g.C;
+        const int kh = k / kwc, rem = k - kh * kwc;
+        const int kw = rem / g.C, c = rem - kw * g.C;
+        const int ih = oh * g.stride - g.pad + kh, iw = ow * g.stride - g.pad + kw;
+        if (ih >= 0 && ih < g.H && iw >= 0 && iw < g.W)
+          v = ld16(p.x + (((long long)n * g.H + ih) * g.W + iw) * cv + (c >> 3));
+      }
+      p.col[r * kv + j] = v;
+    }
+  }
+};
+
+// ---------------------------------------------------------------- col2im (gather)
+struct Col2Im {
+  static constexpr int kThreads = 256;
+  struct Params {
+    const uint4* col;
+    uint4* dx;
+    Geometry g;
+    long long nvec;   // N*H*W*C/8
+  };
+  static __device__ __forceinline__ void run(const Params& p, uint3 bidx, uint3, char*) {
+    const Geometry& g = p.g;
+    const int cv = g.C >> 3, kv = g.Kp >> 3;
+    const long long v0 = (long long)bidx.x * kVecPerBlock;
+    for (int i = threadIdx.x; i < kVecPerBlock; i += kThreads) {
+      const long long v = v0 + i;
+      if (v >= p.nvec) break;
+      const int c8 = (int)(v % cv);
+      const long long pix = v / cv;
+      const int iw = (int)(pix % g.W);
+      const long long t = pix / g.W;
+      const int ih = (int)(t % g.H);
+      const int n = (int)(t / g.H);
+      float acc[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
+      for (int kh = 0; kh < g.KH; ++kh) {
+        const int ohn = ih + g.pad - kh;
+        if (ohn < 0 || ohn % g.stride) continue;
+        const int oh = ohn / g.stride;
+        if (oh >= g.OH) continue;
+        for (int kw = 0; kw < g.KW; ++kw) {
+          const int own = iw + g.pad - kw;
+          if (own < 0 || own % g.stride) continue;
+          const int ow = own / g.stride;
+          if (ow >= g.OW) continue;
+          const long long r = ((long long)n * g.OH + oh) * g.OW + ow;
+          float f[8];
+          unpack8(ld16(p.col + r * kv + ((kh * g.KW + kw) * cv + c8)), f);
+#pragma unroll
+          for (int e = 0; e < 8; ++e) acc[e] += f[e];
+        }
+      }
+      p.dx[v] = pack8(acc);
+    }
+  }
+};
+
+// ---------------------------------------------------------------- transpose
+struct Transpose {
+  static constexpr int kThreads = 256;
+  static constexpr int T = 64;
+  struct Params {
+    const unsigned short* src;
+    unsigned short* dst;
+    long long R, C;
+  };
+  static __device__ __forceinline__ void run(const Params& p, uint3 bidx, uint3, char* smem) {
+    unsigned short* tile = reinterpret_cast<unsigned short*>(smem);   // [T][T + 2]
+    const long long c0 = (long long)bidx.x * T, r0 = (long long)bidx.y * T;
+    // rows of the source tile: 4 threads x 16 elements per 64-wide row
+    for (int i = threadIdx.x; i < T * T; i += kThreads) {
+      const int rr = i / T, cc = i % T;
+      const long long r = r0 + rr, c = c0 + cc;
+      tile[rr * (T + 2) + cc] = (r < p.R && c < p.C) ? p.src[r * p.C + c] : (unsigned short)0;
+    }
+    __syncthreads();
+    for (int i = threadIdx.x; i < T * T; i += kThreads) {
+      const int cc = i / T, rr = i % T;
+      const long long r = r0 + rr, c = c0 + cc;
+      if (r < p.R && c < p.C) p.dst[c * p.R + r] = tile[rr * (T + 2) + cc];
+    }
+    __syncthreads();   // the tile is reused by the next logical block of a PTB worker
+  }
+};
+
+// ---------------------------------------------------------------- batch-norm statistics
+struct BnStats {
+  static constexpr int kThreads = 256;
+  struct Params {
+    const uint4* x;        // pre-BN activations [P, C]
+    const uint4* g;        // mode 1: upstream gradient
+    const uint4* g2;       // mode 1: optional second gradient term (residual)
+    const uint4* y;        // mode 1: optional ReLU output (mask y > 0)
+    const float* mean;     // mode 1
+    const float* invstd;   // mode 1
+    float* part;           // [2][nrb][C]
+    long long P;
+    int C, RB, nrb, mode;
+  };
+  static __device__ __forceinline__ void run(const Params& p, uint3 bidx, uint3, char* smem) {
+    const int CB = min(p.C, 256);
+    const int cv = CB >> 3, rl = kThreads / cv;
+    const int lane_c = threadIdx.x % cv, lane_r = threadIdx.x / cv;
+    const int c = bidx.x * 256 + lane_c * 8;
+    const long long rbeg = (long long)bidx.y * p.RB;
+    const long long rend = min(p.P, rbeg + p.RB);
+    const int cvec = p.C >> 3;
+    float s1[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f}, s2[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
+    float mu[8], is[8];
+    if (p.mode == 1) {
+#pragma unroll
+      for (int e = 0; e < 8; ++e) { mu[e] = p.mean[c + e]; is[e] = p.invstd[c + e]; }
+    }
+    for (long long r = rbeg + lane_r; r < rend; r += rl) {
+      const long long off = r * cvec + (c >> 3);
+      float x[8];
+      unpack8(ld16(p.x + off), x);
+      if (p.mode == 0) {
+#pragma unroll
+        for (int e = 0; e < 8; ++e) { s1[e] += x[e]; s2[e] += x[e] * x[e]; }
+      } else {
+        float dz[8];
+        unpack8(ld16(p.g + off), dz);
+        if (p.g2) {
+          float t[8];
+          unpack8(ld16(p.g2 + off), t);
+#pragma unroll
+          for (int e = 0; e < 8; ++e) dz[e] += t[e];
+        }
+        if (p.y) {
+          float t[8];
+          unpack8(ld16(p.y + off), t);
+#pragma unroll
+          for (int e = 0; e < 8; ++e) dz[e] = t[e] > 0.f ? dz[e] : 0.f;
+        }
+#pragma unroll
+        for (int e = 0; e < 8; ++e) { s1[e] += dz[e]; s2[e] += dz[e] * ((x[e] - mu[e]) * is[e]); }
+      }
+    }
+    float* red = reinterpret_cast<float*>(smem);   // [2][rl][CB]
+#pragma unroll
+    for (int e = 0; e < 8; ++e) {
+      red[lane_r * CB + lane_c * 8 + e] = s1[e];
+      red[rl * CB + lane_r * CB + lane_c * 8 + e] = s2[e];
+    }
+    __syncthreads();
+    if (threadIdx.x < CB) {
+      float a = 0.f, b = 0.f;
+      for (int k = 0; k < rl; ++k) { a += red[k * CB + threadIdx.x]; b += red[rl * CB + k * CB + threadIdx.x]; }
+      const int ch = bidx.x * 256 + threadIdx.x;
+      p.part[(long long)bidx.y * p.C + ch] = a;
+      p.part[((long long)p.nrb + bidx.y) * p.C + ch] = b;
+    }
+    __syncthreads();
+  }
+};
+
+struct BnFinalize {
+  static constexpr int kThreads = 256;   // 8 warps = 8 channels per logical block
+  struct Params {
+    const float* part;   // [2][nrb][C]
+    int nrb, C, mode;
+    float inv_count, eps;
+    const float* gamma;
+    const float* beta;
+    float* mean;     // mode 0 outputs
+    float* invstd;
+    float* scale;
+    float* shift;
+    float* dgamma;   // mode 1 outputs (gradient slots)
+    float* dbeta;
+    float* k1;
+    float* k2;
+  };
+  static __device__ __forceinline__ void run(const Params& p, uint3 bidx, uint3, char*) {
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int c = bidx.x * 8 + warp;
+    if (c >= p.C) return;   // warp-uniform, no barrier in this body
+    float a = 0.f, b = 0.f;
+    for (int k = lane; k < p.nrb; k += 32) {
+      a += p.part[(long long)k * p.C + c];
+      b += p.part[((long long)p.nrb + k) * p.C + c];
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+      a += __shfl_xor_sync(0xffffffffu, a, o);
+      b += __shfl_xor_sync(0xffffffffu, b, o);
+    }
+    if (lane != 0) return;
+    if (p.mode == 0) {
+      const float m = a * p.inv_count;
+      const float var = fmaxf(b * p.inv_count - m * m, 0.f);
+      const float is = rsqrtf(var + p.eps);
+      p.mean[c] = m;
+      p.invstd[c] = is;
+      const float sc = p.gamma[c] * is;
+      p.scale[c] = sc;
+      p.shift[c] = p.beta[c] - m * sc;
+    } else {
+      p.dbeta[c] = a;
+      p.dgamma[c] = b;
+      p.k1[c] = a * p.inv_count;
+      p.k2[c] = b * p.inv_count;
+    }
+  }
+};
+
+// ---------------------------------------------------------------- batch-norm apply
+struct BnAct {
+  static constexpr int kThreads = 256;
+  struct Params {
+    const uint4* x;
+    const uint4* res;   // optional residual added before the activation
+    uint4* y;
+    const float* scale;
+    const float* shift;
+    long long nvec;
+    int C, relu;
+  };
+  static __device__ __forceinline__ void run(const Params& p, uint3 bidx, uint3, char*) {
+    const int cv = p.C >> 3;
+    const long long v0 = (long long)bidx.x * kVecPerBlock;
+    for (int i = threadIdx.x; i < kVecPerBlock; i += kThreads) {
+      const long long v = v0 + i;
+      if (v >= p.nvec) break;
+      const int c = (int)(v % cv) << 3;
+      float x[8];
+      unpack8(ld16(p.x + v), x);
+      const float4 s0 = *reinterpret_cast<const float4*>(p.scale + c), s1 = *reinterpret_cast<const float4*>(p.scale + c + 4);
+      const float4 h0 = *reinterpret_cast<const float4*>(p.shift + c), h1 = *reinterpret_cast<const float4*>(p.shift + c + 4);
+      const float sc[8] = {s0.x, s0.y, s0.z, s0.w, s1.x, s1.y, s1.z, s1.w};
+      const float sh[8] = {h0.x, h0.y, h0.z, h0.w, h1.x, h1.y, h1.z, h1.w};
+#pragma unroll
+      for (int e = 0; e < 8; ++e) x[e] = x[e] * sc[e] + sh[e];
+      if (p.res) {
+        float r[8];
+        unpack8(ld16(p.res + v), r);
+#pragma unroll
+        for (int e = 0; e < 8; ++e) x[e] += r[e];
+      }
+      if (p.relu) {
+#pragma unroll
+        for (int e = 0; e < 8; ++e) x[e] = fmaxf(x[e], 0.f);
+      }
+      p.y[v] = pack8(x);
+    }
+  }
+};
+
+struct BnBwd {
+  static constexpr int kThreads = 256;
+  struct Params {
+    const uint4* g;
+    const uint4* g2;    // optional
+    const uint4* y;     // optional ReLU mask source
+    const uint4* x;
+    const float* mean;
+    const float* invstd;
+    const float* gamma;
+    const float* k1;
+    const float* k2;
+    uint4* dx;
+    uint4* dz_out;      // optional: the masked upstream gradient (for the shortcut)
+    long long nvec;
+    int C;
+  };
+  static __device__ __forceinline__ void run(const Params& p, uint3 bidx, uint3, char*) {
+    const int cv = p.C >> 3;
+    const long long v0 = (long long)bidx.x * kVecPerBlock;
+    for (int i = threadIdx.x; i < kVecPerBlock; i += kThreads) {
+      const long long v = v0 + i;
+      if (v >= p.nvec) break;
+      const int c = (int)(v % cv) << 3;
+      float dz[8], x[8];
+      unpack8(ld16(p.g + v), dz);
+      if (p.g2) {
+        float t[8];
+        unpack8(ld16(p.g2 + v), t);
+#pragma unroll
+        for (int e = 0; e < 8; ++e) dz[e] += t[e];
+      }
+      if (p.y) {
+        float t[8];
+        unpack8(ld16(p.y + v), t);
+#pragma unroll
+        for (int e = 0; e < 8; ++e) dz[e] = t[e] > 0.f ? dz[e] : 0.f;
+      }
+      if (p.dz_out) p.dz_out[v] = pack8(dz);
+      unpack8(ld16(p.x + v), x);
+      float o[8];
+#pragma unroll
+      for (int e = 0; e < 8; ++e) {
+        const float is = p.invstd[c + e];
+        const float xh = (x[e] - p.mean[c + e]) * is;
+        o[e] = p.gamma[c + e] * is * (dz[e] - p.k1[c + e] - xh * p.k2[c + e]);
+      }
+      p.dx[v] = pack8(o);
+    }
+  }
+};
+
+// ---------------------------------------------------------------- pooling
+struct MaxPoolFwd {   // 3x3, stride 2, pad 1
+  static constexpr int kThreads = 256;
+  struct Params {
+    const uint4* x;
+    uint4* y;
+    uint2* arg;       // argmax (0..8) per output element, 8 bytes per vector
+    int N, H, W, C, OH, OW;
+    long long nvec;   // N*OH*OW*C/8
+  };
+  static __device__ __forceinline__ void run(const Params& p, uint3 bidx, uint3, char*) {
+    const int cv = p.C >> 3;
+    const long long v0 = (long long)bidx.x * kVecPerBlock;
+    for (int i = threadIdx.x; i < kVecPerBlock; i += kThreads) {
+      const long long v = v0 + i;
+      if (v >= p.nvec) break;
+      const int c8 = (int)(v % cv);
+      const long long pix = v / cv;
+      const int ow = (int)(pix % p.OW);
+      const long long t = pix / p.OW;
+      const int oh = (int)(t % p.OH), n = (int)(t / p.OH);
+      float m[8];
+      unsigned char a[8];
+#pragma unroll
+      for (int e = 0; e < 8; ++e) { m[e] = -INFINITY; a[e] = 0; }
+      for (int kh = 0; kh < 3; ++kh) {
+        const int ih = oh * 2 - 1 + kh;
+        if (ih < 0 || ih >= p.H) continue;
+        for (int kw = 0; kw < 3; ++kw) {
+          const int iw = ow * 2 - 1 + kw;
+          if (iw < 0 || iw >= p.W) continue;
+          float f[8];
+          unpack8(ld16(p.x + (((long long)n * p.H + ih) * p.W + iw) * cv + c8), f);
+#pragma unroll
+          for (int e = 0; e < 8; ++e)
+            if (f[e] > m[e]) { m[e] = f[e]; a[e] = (unsigned char)(kh * 3 + kw); }
+        }
+      }
+      p.y[v] = pack8(m);
+      uint2 w;
+      w.x = a[0] | (a[1] << 8) | (a[2] << 16) | ((unsigned)a[3] << 24);
+      w.y = a[4] | (a[5] << 8) | (a[6] << 16) | ((unsigned)a[7] << 24);
+      p.arg[v] = w;
+    }
+  }
+};
+
+struct MaxPoolBwd {
+  static constexpr int kThreads = 256;
+  struct Params {
+    const uint4* dy;
+    const uint4* dy2;   // optional second gradient term
+    const uint2* arg;
+    uint4* dx;
+    int N, H, W, C, OH, OW;
+    long long nvec;     // N*H*W*C/8
+  };
+  static __device__ __forceinline__ void run(const Params& p, uint3 bidx, uint3, char*) {
+    const int cv = p.C >> 3;
+    const long long v0 = (long long)bidx.x * kVecPerBlock;
+    for (int i = threadIdx.x; i < kVecPerBlock; i += kThreads) {
+      const long long v = v0 + i;
+      if (v >= p.nvec) break;
+      const int c8 = (int)(v % cv);
+      const long long pix = v / cv;
+      const int iw = (int)(pix % p.W);
+      const long long t = pix / p.W;
+      const int ih = (int)(t % p.H), n = (int)(t / p.H);
+      float acc[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
+      // output rows whose window [2*oh - 1, 2*oh + 1] contains ih
+      const int oh_lo = max(0, ih / 2), oh_hi = min(p.OH - 1, (ih + 1) / 2);
+      const int ow_lo = max(0, iw / 2), ow_hi = min(p.OW - 1, (iw + 1) / 2);
+      for (int oh = oh_lo; oh <= oh_hi; ++oh) {
+        const int kh = ih - (oh * 2 - 1);
+        if (kh < 0 || kh > 2) continue;
+        for (int ow = ow_lo; ow <= ow_hi; ++ow) {
+          const int kw = iw - (ow * 2 - 1);
+          if (kw < 0 || kw > 2) continue;
+          const long long o = (((long long)n * p.OH + oh) * p.OW + ow) * cv + c8;
+          const uint2 w = p.arg[o];
+          const unsigned char* a = reinterpret_cast<const unsigned char*>(&w);
+          float d[8];
+          unpack8(ld16(p.dy + o), d);
+          if (p.dy2) {
+            float d2[8];
+            unpack8(ld16(p.dy2 + o), d2);
+#pragma unroll
+            for (int e = 0; e < 8; ++e) d[e] += d2[e];
+          }
+          const unsigned char me = (unsigned char)(kh * 3 + kw);
+#pragma unroll
+          for (int e = 0; e < 8; ++e)
+            if (a[e] == me) acc[e] += d[e];
+        }
+      }
+      p.dx[v] = pack8(acc);
+    }
+  }
+};
+
+struct AvgPoolFwd {   // [N, HW, C] -> [N, C]
+  static constexpr int kThreads = 256;
+  struct Params {
+    const uint4* x;
+    uint4* y;
+    int N, HW, C;
+  };
+  static __device__ __forceinline__ void run(const Params& p, uint3 bidx, uint3, char*) {
+    const int cv = p.C >> 3;
+    const long long v = (long long)bidx.x * kThreads + threadIdx.x;
+    if (v >= (long long)p.N * cv) return;
+    const int n = (int)(v / cv), c8 = (int)(v % cv);
+    float acc[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
+    for (int q = 0; q < p.HW; ++q) {
+      float f[8];
+      unpack8(ld16(p.x + ((long long)n * p.HW + q) * cv + c8), f);
+#pragma unroll
+      for (int e = 0; e < 8; ++e) acc[e] += f[e];
+    }
+    const float s = 1.f / (float)p.HW;
+#pragma unroll
+    for (int e = 0; e < 8; ++e) acc[e] *= s;
+    p.y[v] = pack8(acc);
+  }
+};
+
+struct AvgPoolBwd {
+  static constexpr int kThreads = 256;
+  struct Params {
+    const uint4* dy;   // [N, C]
+    uint4* dx;         // [N, HW, C]
+    int N, HW, C;
+    long long nvec;
+  };
+  static __device__ __forceinline__ void run(const Params& p, uint3 bidx, uint3, char*) {
+    const int cv = p.C >> 3;
+    const long long v0 = (long long)bidx.x * kVecPerBlock;
+    const float s = 1.f / (float)p.HW;
+    for (int i = threadIdx.x; i < kVecPerBlock; i += kThreads) {
+      const long long v = v0 + i;
+      if (v >= p.nvec) break;
+      const int c8 = (int)(v % cv);
+      const long long n = v / cv / p.HW;
+      float d[8];
+      unpack8(p.dy[n * cv + c8], d);
+#pragma unroll
+      for (int e = 0; e < 8; ++e) d[e] *= s;
+      p.dx[v] = pack8(d);
+    }
+  }
+};
+
+// ---------------------------------------------------------------- loss
+struct SoftmaxXent {   // one row per logical block
+  static constexpr int kThreads = 256;
+  struct Params {
+    const float* logits;   // [B, Npad] fp32 (GEMM output)
+    const float* bias;     // [Npad]
+    const int* labels;     // [B]
+    float* loss;           // [B]
+    __nv_bfloat16* dl;     // [B, Npad], zero in the pad columns
+    float* dl32;           // [B, Npad]: the bias-gradient partials (summed over B by sgd_update)
+    int B, Npad, ncls;
+  };
+  static __device__ __forceinline__ void run(const Params& p, uint3 bidx, uint3, char* smem) {
+    float* red = reinterpret_cast<float*>(smem);   // [kThreads / 32]
+    const int b = bidx.x;
+    const float* z = p.logits + (long long)b * p.Npad;
+    float m = -INFINITY;
+    for (int j = threadIdx.x; j < p.ncls; j += kThreads) m = fmaxf(m, z[j] + p.bias[j]);
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) m = fmaxf(m, __shfl_xor_sync(0xffffffffu, m, o));
+    if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = m;
+    __syncthreads();
+    m = red[0];
+    for (int w = 1; w < kThreads / 32; ++w) m = fmaxf(m, red[w]);
+    __syncthreads();
+    float s = 0.f;
+    for (int j = threadIdx.x; j < p.ncls; j += kThreads) s += __expf(z[j] + p.bias[j] - m);
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+    if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = s;
+    __syncthreads();
+    s = 0.f;
+    for (int w = 0; w < kThreads / 32; ++w) s += red[w];
+    const int lab = p.labels[b];
+    const float inv_b = 1.f / (float)p.B;
+    for (int j = threadIdx.x; j < p.Npad; j += kThreads) {
+      float d = 0.f;
+      if (j < p.ncls) d = (__expf(z[j] + p.bias[j] - m) / s - (j == lab ? 1.f : 0.f)) * inv_b;
+      p.dl[(long long)b * p.Npad + j] = __float2bfloat16_rn(d);
+      p.dl32[(long long)b * p.Npad + j] = d;
+    }
+    if (threadIdx.x == 0) p.loss[b] = logf(s) + m - (z[lab] + p.bias[lab]);
+    __syncthreads();
+  }
+};
+
+// ---------------------------------------------------------------- optimizer
+struct SgdSeg {
+  float* w;               // fp32 master weights [rows, cols]
+  float* v;               // momentum
+  const float* grad;      // [S][gstride] partials (split-K slices / batch rows)
+  long long n;
+  long long gstride;
+  int S;
+  float wd;
+  __nv_bfloat16* wb;      // optional bf16 copy, same layout
+  __nv_bfloat16* wt;      // optional bf16 transposed copy [cols, rows]
+  int rows, cols;
+};
+
+struct SgdUpdate {
+  static constexpr int kThreads = 256;
+  static constexpr int kChunk = 4096;   // elements per logical block
+  struct Params {
+    const SgdSeg* segs;
+    const int2* map;      // logical block -> (segment, chunk)
+    float lr, momentum;
+  };
+  static __device__ __forceinline__ void run(const Params& p, uint3 bidx, uint3, char*) {
+    const int2 m = p.map[bidx.x];
+    const SgdSeg& s = p.segs[m.x];
+    const long long i0 = (long long)m.y * kChunk;
+    for (int k = threadIdx.x; k < kChunk; k += kThreads) {
+      const long long i = i0 + k;
+      if (i >= s.n) break;
+      float g = 0.f;
+      for (int j = 0; j < s.S; ++j) g += s.grad[(long long)j * s.gstride + i];
+      const float w = s.w[i];
+      g += s.wd * w;
+      const float v = p.momentum * s.v[i] + g;
+      const float w2 = w - p.lr * v;
+      s.v[i] = v;
+      s.w[i] = w2;
+      const __nv_bfloat16 h = __float2bfloat16_rn(w2);
+      if (s.wb) s.wb[i] = h;
+      if (s.wt) {
+        const long long r = i / s.cols, c = i - r * s.cols;
+        s.wt[c * s.rows + r] = h;
+      }
+    }
+  }
+};
+
+}  // namespace nn
+
+// ---------------------------------------------------------------- host binding
+static bool aligned16(const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15) == 0; }
+
+static int geometry(const tally_kernel_args* a, int base, nn::Geometry& g) {
+  g.N = (int)a->i[base + 0];
+  g.H = (int)a->i[base + 1];
+  g.W = (int)a->i[base + 2];
+  g.C = (int)a->i[base + 3];
+  const long long kh_kw_s_p = a->i[base + 4];   // packed: kh | kw << 8 | stride << 16 | pad << 24
+  g.KH = (int)(kh_kw_s_p & 0xff);
+  g.KW = (int)((kh_kw_s_p >> 8) & 0xff);
+  g.stride = (int)((kh_kw_s_p >> 16) & 0xff);
+  g.pad = (int)((kh_kw_s_p >> 24) & 0xff);
+  if (g.N < 1 || g.H < 1 || g.W < 1 || g.C < 8 || g.C % 8 || g.KH < 1 || g.KW < 1 || g.stride < 1) {
+    set_error("conv geometry: need N,H,W >= 1, C %% 8 == 0, kernel >= 1, stride >= 1");
+    return TALLY_EINVAL;
+  }
+  g.OH = (g.H + 2 * g.pad - g.KH) / g.stride + 1;
+  g.OW = (g.W + 2 * g.pad - g.KW) / g.stride + 1;
+  g.K = g.KH * g.KW * g.C;
+  g.Kp = (g.K + 63) / 64 * 64;
+  if (g.OH < 1 || g.OW < 1) { set_error("conv geometry: empty output"); return TALLY_EINVAL; }
+  return TALLY_OK;
+}
+
+template <class P>
+static void finish(Instance* inst, const P& p, long long blocks, int threads, size_t smem, double bytes) {
+  memcpy(inst->params, &p, sizeof(p));
+  inst->grid = make_uint3((unsigned)blocks, 1, 1);
+  inst->threads = threads;
+  inst->smem = smem;
+  inst->alg_bytes = bytes;
+}
+
+// ptr: x, col.  i: N, H, W, C, packed(kh,kw,stride,pad)
+static int bind_im2col(const tally_kernel_args* a, Instance* inst) {
+  nn::Im2Col::Params p{};
+  int rc = geometry(a, 0, p.g);
+  if (rc) return rc;
+  p.x = static_cast<const uint4*>(a->ptr[0]);
+  p.col = static_cast<uint4*>(a->ptr[1]);
+  if (!p.x || !p.col || !aligned16(p.x) || !aligned16(p.col)) { set_error("im2col: 16-byte aligned x, col"); return TALLY_EINVAL; }
+  p.rows = (long long)p.g.N * p.g.OH * p.g.OW;
+  p.rpb = max(1, nn::kVecPerBlock / (p.g.Kp / 8));
+  finish(inst, p, (p.rows + p.rpb - 1) / p.rpb, nn::Im2Col::kThreads, 0,
+         2.0 * ((double)p.rows * p.g.Kp + (double)p.g.N * p.g.H * p.g.W * p.g.C));
+  return TALLY_OK;
+}
+
+// ptr: col, dx.  i: geometry as im2col
+static int bind_col2im(const tally_kernel_args* a, Instance* inst) {
+  nn::Col2Im::Params p{};
+  int rc = geometry(a, 0, p.g);
+  if (rc) return rc;
+  p.col = static_cast<const uint4*>(a->ptr[0]);
+  p.dx = static_cast<uint4*>(a->ptr[1]);
+  if (!p.col || !p.dx || !aligned16(p.col) || !aligned16(p.dx)) { set_error("col2im: 16-byte aligned col, dx"); return TALLY_EINVAL; }
+  p.nvec = (long long)p.g.N * p.g.H * p.g.W * (p.g.C / 8);
+  finish(inst, p, (p.nvec + nn::kVecPerBlock - 1) / nn::kVecPerBlock, nn::Col2Im::kThreads, 0,
+         2.0 * ((double)p.g.N * p.g.OH * p.g.OW * p.g.Kp + 8.0 * p.nvec));
+  return TALLY_OK;
+}
+
+// ptr: src, dst.  i: R, C
+static int bind_transpose(const tally_kernel_args* a, Instance* inst) {
+  nn::Transpose::Params p{};
+  p.src = static_cast<const unsigned short*>(a->ptr[0]);
+  p.dst = static_cast<unsigned short*>(a->ptr[1]);
+  p.R = a->i[0];
+  p.C = a->i[1];
+  if (!p.src || !p.dst || p.R < 1 || p.C < 1) { set_error("transpose: need src, dst, R, C >= 1"); return TALLY_EINVAL; }
+  memcpy(inst->params, &p, sizeof(p));
+  const int T = nn::Transpose::T;
+  inst->grid = make_uint3((unsigned)((p.C + T - 1) / T), (unsigned)((p.R + T - 1) / T), 1);
+  inst->threads = nn::Transpose::kThreads;
+  inst->smem = (size_t)T * (T + 2) * 2;
+  inst->alg_bytes = 4.0 * (double)p.R * (double)p.C;
+  return TALLY_OK;
+}
+
+// ptr: x, g, g2, y, mean, invstd, part.  i: P, C, mode, RB
+static int bind_bn_stats(const tally_kernel_args* a, Instance* inst) {
+  nn::BnStats::Params p{};
+  p.x = static_cast<const uint4*>(a->ptr[0]);
+  p.g = static_cast<const uint4*>(a->ptr[1]);
+  p.g2 = static_cast<const uint4*>(a->ptr[2]);
+  p.y = static_cast<const uint4*>(a->ptr[3]);
+  p.mean = static_cast<const float*>(a->ptr[4]);
+  p.invstd = static_cast<const float*>(a->ptr[5]);
+  p.part = static_cast<float*>(a->ptr[6]);
+  p.P = a->i[0];
+  p.C = (int)a->i[1];
+  p.mode = (int)a->i[2];
+  p.RB = (int)a->i[3];
+  const bool c_ok = p.C >= 64 && (p.C < 256 ? (256 % p.C == 0) : (p.C % 256 == 0));
+  if (!p.x || !p.part || p.P < 1 || !c_ok || p.RB < 1 ||
+      (p.mode == 1 && (!p.g || !p.mean || !p.invstd)) || (p.mode != 0 && p.mode != 1)) {
+    set_error("bn_stats: need x, part, C in {64, 128} or a multiple of 256, mode 0/1 operands");
+    return TALLY_EINVAL;
+  }
+  p.nrb = (int)((p.P + p.RB - 1) / p.RB);
+  memcpy(inst->params, &p, sizeof(p));
+  inst->grid = make_uint3((unsigned)((p.C + 255) / 256), (unsigned)p.nrb, 1);
+  inst->threads = nn::BnStats::kThreads;
+  inst->smem = 2 * 256 * 8 * sizeof(float);   // [2][rl][CB] with rl * CB = 256 * 8
+  const int streams = p.mode == 0 ? 1 : 2 + (p.g2 ? 1 : 0) + (p.y ? 1 : 0);
+  inst->alg_bytes = 2.0 * streams * (double)p.P * p.C + 8.0 * p.nrb * p.C;
+  return TALLY_OK;
+}
+
+// ptr: part, gamma, beta, mean, invstd, scale, shift.  (mode 1: ptr[3..6] = dgamma, dbeta, k1, k2)
+// i: nrb, C, mode, count.  f: eps
+static int bind_bn_finalize(const tally_kernel_args* a, Instance* inst) {
+  nn::BnFinalize::Params p{};
+  p.part = static_cast<const float*>(a->ptr[0]);
+  p.nrb = (int)a->i[0];
+  p.C = (int)a->i[1];
+  p.mode = (int)a->i[2];
+  const long long count = a->i[3];
+  p.eps = (float)a->f[0];
+  if (!p.part || p.nrb < 1 || p.C < 1 || count < 1 || (p.mode != 0 && p.mode != 1)) {
+    set_error("bn_finalize: need part, nrb, C, count >= 1, mode 0/1");
+    return TALLY_EINVAL;
+  }
+  p.inv_count = (float)(1.0 / (double)count);
+  if (p.mode == 0) {
+    p.gamma = static_cast<const float*>(a->ptr[1]);
+    p.beta = static_cast<const float*>(a->ptr[2]);
+    p.mean = static_cast<float*>(a->ptr[3]);
+    p.invstd = static_cast<float*>(a->ptr[4]);
+    p.scale = static_cast<float*>(a->ptr[5]);
+    p.shift = static_cast<float*>(a->ptr[6]);
+    if (!p.gamma || !p.beta || !p.mean || !p.invstd || !p.scale || !p.shift) { set_error("bn_finalize: mode 0 outputs"); return TALLY_EINVAL; }
+  } else {
+    p.dgamma = static_cast<float*>(a->ptr[3]);
+    p.dbeta = static_cast<float*>(a->ptr[4]);
+    p.k1 = static_cast<float*>(a->ptr[5]);
+    p.k2 = static_cast<float*>(a->ptr[6]);
+    if (!p.dgamma || !p.dbeta || !p.k1 || !p.k2) { set_error("bn_finalize: mode 1 outputs"); return TALLY_EINVAL; }
+  }
+  finish(inst, p, (p.C + 7) / 8, nn::BnFinalize::kThreads, 0, 8.0 * p.nrb * p.C + 16.0 * p.C);
+  return TALLY_OK;
+}
+
+// ptr: x, res, y, scale, shift.  i: P, C, relu
+static int bind_bn_act(const tally_kernel_args* a, Instance* inst) {
+  nn::BnAct::Params p{};
+  p.x = static_cast<const uint4*>(a->ptr[0]);
+  p.res = static_cast<const uint4*>(a->ptr[1]);
+  p.y = static_cast<uint4*>(a->ptr[2]);
+  p.scale = static_cast<const float*>(a->ptr[3]);
+  p.shift = static_cast<const float*>(a->ptr[4]);
+  const long long P = a->i[0];
+  p.C = (int)a->i[1];
+  p.relu = (int)a->i[2];
+  if (!p.x || !p.y || !p.scale || !p.shift || P < 1 || p.C < 8 || p.C % 8) { set_error("bn_act: need x, y, scale, shift, C %% 8 == 0"); return TALLY_EINVAL; }
+  p.nvec = P * (p.C / 8);
+  finish(inst, p, (p.nvec + nn::kVecPerBlock - 1) / nn::kVecPerBlock, nn::BnAct::kThreads, 0,
+         16.0 * p.nvec * (p.res ? 3 : 2));
+  return TALLY_OK;
+}
+
+// ptr[0..7] = g, g2, y, x, mean, invstd, gamma, dx;  i: P, C, then the k1, k2 and
+// optional dz_out device addresses (the argument block has eight pointer slots)
+static int bind_bn_bwd(const tally_kernel_args* a, Instance* inst) {
+  nn::BnBwd::Params p{};
+  p.g = static_cast<const uint4*>(a->ptr[0]);
+  p.g2 = static_cast<const uint4*>(a->ptr[1]);
+  p.y = static_cast<const uint4*>(a->ptr[2]);
+  p.x = static_cast<const uint4*>(a->ptr[3]);
+  p.mean = static_cast<const float*>(a->ptr[4]);
+  p.invstd = static_cast<const float*>(a->ptr[5]);
+  p.gamma = static_cast<const float*>(a->ptr[6]);
+  p.dx = static_cast<uint4*>(a->ptr[7]);
+  const long long P = a->i[0];
+  p.C = (int)a->i[1];
+  p.k1 = reinterpret_cast<const float*>(a->i[2]);
+  p.k2 = reinterpret_cast<const float*>(a->i[3]);
+  p.dz_out = reinterpret_cast<uint4*>(a->i[4]);
+  if (!p.g || !p.x || !p.mean || !p.invstd || !p.gamma || !p.dx || !p.k1 || !p.k2 || P < 1 || p.C < 8 || p.C % 8) {
+    set_error("bn_bwd: need g, x, mean, invstd, gamma, dx, k1, k2 and C %% 8 == 0");
+    return TALLY_EINVAL;
+  }
+  p.nvec = P * (p.C / 8);
+  const int streams = 3 + (p.g2 ? 1 : 0) + (p.y ? 1 : 0) + (p.dz_out ? 1 : 0);
+  finish(inst, p, (p.nvec + nn::kVecPerBlock - 1) / nn::kVecPerBlock, nn::BnBwd::kThreads, 0, 16.0 * p.nvec * streams);
+  return TALLY_OK;
+}
+
+// ptr: x, y, arg.  i: N, H, W, C
+static int bind_maxpool_fwd(const tally_kernel_args* a, Instance* inst) {
+  nn::MaxPoolFwd::Params p{};
+  p.x = static_cast<const uint4*>(a->ptr[0]);
+  p.y = static_cast<uint4*>(a->ptr[1]);
+  p.arg = static_cast<uint2*>(a->ptr[2]);
+  p.N = (int)a->i[0]; p.H = (int)a->i[1]; p.W = (int)a->i[2]; p.C = (int)a->i[3];
+  if (!p.x || !p.y || !p.arg || p.N < 1 || p.H < 1 || p.W < 1 || p.C < 8 || p.C % 8) { set_error("maxpool: bad arguments"); return TALLY_EINVAL; }
+  p.OH = (p.H + 2 - 3) / 2 + 1;
+  p.OW = (p.W + 2 - 3) / 2 + 1;
+  p.nvec = (long long)p.N * p.OH * p.OW * (p.C / 8);
+  finish(inst, p, (p.nvec + nn::kVecPerBlock - 1) / nn::kVecPerBlock, nn::MaxPoolFwd::kThreads, 0,
+         2.0 * p.N * p.H * p.W * p.C + 24.0 * p.nvec);
+  return TALLY_OK;
+}
+
+// ptr: dy, dy2, arg, dx.  i: N, H, W, C (input geometry)
+static int bind_maxpool_bwd(const tally_kernel_args* a, Instance* inst) {
+  nn::MaxPoolBwd::Params p{};
+  p.dy = static_cast<const uint4*>(a->ptr[0]);
+  p.dy2 = static_cast<const uint4*>(a->ptr[1]);
+  p.arg = static_cast<const uint2*>(a->ptr[2]);
+  p.dx = static_cast<uint4*>(a->ptr[3]);
+  p.N = (int)a->i[0]; p.H = (int)a->i[1]; p.W = (int)a->i[2]; p.C = (int)a->i[3];
+  if (!p.dy || !p.arg || !p.dx || p.N < 1 || p.H < 1 || p.W < 1 || p.C < 8 || p.C % 8) { set_error("maxpool_bwd: bad arguments"); return TALLY_EINVAL; }
+  p.OH = (p.H + 2 - 3) / 2 + 1;
+  p.OW = (p.W + 2 - 3) / 2 + 1;
+  p.nvec = (long long)p.N * p.H * p.W * (p.C / 8);
+  const double out_vec = (double)p.N * p.OH * p.OW * (p.C / 8);
+  finish(inst, p, (p.nvec + nn::kVecPerBlock - 1) / nn::kVecPerBlock, nn::MaxPoolBwd::kThreads, 0,
+         16.0 * p.nvec + out_vec * (p.dy2 ? 40.0 : 24.0));
+  return TALLY_OK;
+}
+
+// ptr: x, y.  i: N, HW, C
+static int bind_avgpool_fwd(const tally_kernel_args* a, Instance* inst) {
+  nn::AvgPoolFwd::Params p{};
+  p.x = static_cast<const uint4*>(a->ptr[0]);
+  p.y = static_cast<uint4*>(a->ptr[1]);
+  p.N = (int)a->i[0]; p.HW = (int)a->i[1]; p.C = (int)a->i[2];
+  if (!p.x || !p.y || p.N < 1 || p.HW < 1 || p.C < 8 || p.C % 8) { set_error("avgpool: bad arguments"); return TALLY_EINVAL; }
+  const long long nv = (long long)p.N * (p.C / 8);
+  finish(inst, p, (nv + 255) / 256, nn::AvgPoolFwd::kThreads, 0, 2.0 * p.N * p.C * (p.HW + 1.0));
+  return TALLY_OK;
+}
+
+// ptr: dy, dx.  i: N, HW, C
+static int bind_avgpool_bwd(const tally_kernel_args* a, Instance* inst) {
+  nn::AvgPoolBwd::Params p{};
+  p.dy = static_cast<const uint4*>(a->ptr[0]);
+  p.dx = static_cast<uint4*>(a->ptr[1]);
+  p.N = (int)a->i[0]; p.HW = (int)a->i[1]; p.C = (int)a->i[2];
+  if (!p.dy || !p.dx || p.N < 1 || p.HW < 1 || p.C < 8 || p.C % 8) { set_error("avgpool_bwd: bad arguments"); return TALLY_EINVAL; }
+  p.nvec = (long long)p.N * p.HW * (p.C / 8);
+  finish(inst, p, (p.nvec + nn::kVecPerBlock - 1) / nn::kVecPerBlock, nn::AvgPoolBwd::kThreads, 0,
+         16.0 * p.nvec + 2.0 * p.N * p.C);
+  return TALLY_OK;
+}
+
+// ptr: logits, bias, labels, loss, dl, dl32.  i: B, Npad, ncls
+static int bind_softmax_xent(const tally_kernel_args* a, Instance* inst) {
+  nn::SoftmaxXent::Params p{};
+  p.logits = static_cast<const float*>(a->ptr[0]);
+  p.bias = static_cast<const float*>(a->ptr[1]);
+  p.labels = static_cast<const int*>(a->ptr[2]);
+  p.loss = static_cast<float*>(a->ptr[3]);
+  p.dl = static_cast<__nv_bfloat16*>(a->ptr[4]);
+  p.dl32 = static_cast<float*>(a->ptr[5]);
+  p.B = (int)a->i[0]; p.Npad = (int)a->i[1]; p.ncls = (int)a->i[2];
+  if (!p.logits || !p.bias || !p.labels || !p.loss || !p.dl || !p.dl32 || p.B < 1 || p.ncls < 1 || p.Npad < p.ncls) {
+    set_error("softmax_xent: bad arguments");
+    return TALLY_EINVAL;
+  }
+  finish(inst, p, p.B, nn::SoftmaxXent::kThreads, 64, (double)p.B * p.Npad * 10.0);
+  return TALLY_OK;
+}
+
+// ptr: segs (device SgdSeg[]), map (device int2[]).  i: blocks.  f: lr, momentum
+static int bind_sgd(const tally_kernel_args* a, Instance* inst) {
+  nn::SgdUpdate::Params p{};
+  p.segs = static_cast<const nn::SgdSeg*>(a->ptr[0]);
+  p.map = static_cast<const int2*>(a->ptr[1]);
+  const long long blocks = a->i[0];
+  p.lr = (float)a->f[0];
+  p.momentum = (float)a->f[1];
+  if (!p.segs || !p.map || blocks < 1) { set_error("sgd_update: need segs, map, blocks >= 1"); return TALLY_EINVAL; }
+  finish(inst, p, blocks, nn::SgdUpdate::kThreads, 0, (double)a->i[1]);   // i[1]: bytes (host computed)
+  return TALLY_OK;
+}
+
+template <class B>
+static KernelKind nn_kind(const char* name, int (*bind)(const tally_kernel_args*, Instance*)) {
+  KernelKind k{};
+  k.name = name;
+  k.fn_original = reinterpret_cast<const void*>(&k_original<B>);
+  k.fn_sliced = reinterpret_cast<const void*>(&k_sliced<B>);
+  k.fn_ptb = reinterpret_cast<const void*>(&k_ptb<B>);
+  k.bind = bind;
+  return k;
+}
+
+int register_nn_kernels(KernelKind* out, int cap) {
+  if (cap < 13) return 0;
+  int n = 0;
+  out[n++] = nn_kind<nn::Im2Col>("im2col_bf16", bind_im2col);
+  out[n++] = nn_kind<nn::Col2Im>("col2im_bf16", bind_col2im);
+  out[n++] = nn_kind<nn::Transpose>("transpose_bf16", bind_transpose);
+  out[n++] = nn_kind<nn::BnStats>("bn_stats", bind_bn_stats);
+  out[n++] = nn_kind<nn::BnFinalize>("bn_finalize", bind_bn_finalize);
+  out[n++] = nn_kind<nn::BnAct>("bn_act", bind_bn_act);
+  out[n++] = nn_kind<nn::BnBwd>("bn_bwd", bind_bn_bwd);
+  out[n++] = nn_kind<nn::MaxPoolFwd>("maxpool_fwd", bind_maxpool_fwd);
+  out[n++] = nn_kind<nn::MaxPoolBwd>("maxpool_bwd", bind_maxpool_bwd);
+  out[n++] = nn_kind<nn::AvgPoolFwd>("avgpool_fwd", bind_avgpool_fwd);
+  out[n++] = nn_kind<nn::AvgPoolBwd>("avgpool_bwd", bind_avgpool_bwd);
+  out[n++] = nn_kind<nn::SoftmaxXent>("softmax_xent", bind_softmax_xent);
+  out[n++] = nn_kind<nn::SgdUpdate>("sgd_update", bind_sgd);
+  return n;
+}
+
+}  // namespace tally

@@ -74,5 +74,6 @@ int cuda_fail(cudaError_t e, const char* what);
 int register_basic_kernels(KernelKind* out, int cap);
 int register_gemm_kernels(KernelKind* out, int cap);
 int register_copy_kernels(KernelKind* out, int cap);
+int register_nn_kernels(KernelKind* out, int cap);
 
 }  // namespace tally

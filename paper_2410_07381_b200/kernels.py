@@ -312,3 +312,91 @@ def spin(total_blocks: int, threads_per_block: int, block_duration_ns: int) -> D
     blocks of ``threads_per_block`` threads, each holding its slot for
     ``block_duration_ns`` -- the reference's abstract workloads on the GPU."""
     return DeviceKernel("spin", (), (total_blocks, threads_per_block, block_duration_ns))
+
+
+# -- best-effort training kinds (config C2, kernels_nn.cu) ---------------------
+def _pack_conv(kh, kw, stride, pad):
+    return kh | (kw << 8) | (stride << 16) | (pad << 24)
+
+
+def gemm(A, B, C, splits: int = 1) -> DeviceKernel:
+    """C[M,N] = A[M,K] . B[N,K]^T on tcgen05 (bf16 operands, fp32 accumulation).
+
+    The kind follows the operands: N % 128 == 0 -> 128-wide tiles, else
+    64-wide; C bf16 or fp32.  ``splits`` > 1 (fp32 C of shape [splits, M, N])
+    is split-K: logical block = (split, tile), each split writing its own
+    fp32 partial (summed later by ``sgd_update``)."""
+    import torch
+    M, K = A.shape
+    N, K2 = B.shape
+    if K != K2:
+        raise ValueError("gemm: A[M,K], B[N,K] need the same K")
+    out_f32 = C.dtype == torch.float32
+    if tuple(C.shape[-2:]) != (M, N) or (splits > 1 and (not out_f32 or C.numel() != splits * M * N)):
+        raise ValueError("gemm: C must be [M,N] (or [splits,M,N] fp32 for split-K)")
+    kind = "gemm_bf16" + ("f32" if out_f32 else "") + ("" if N % 128 == 0 else "_n64")
+    return DeviceKernel(kind, (A, B, C), (M, N, K, 0, splits))
+
+
+def im2col(x, col, n, h, w, c, kh, kw, stride, pad) -> DeviceKernel:
+    return DeviceKernel("im2col_bf16", (x, col), (n, h, w, c, _pack_conv(kh, kw, stride, pad)))
+
+
+def col2im(col, dx, n, h, w, c, kh, kw, stride, pad) -> DeviceKernel:
+    return DeviceKernel("col2im_bf16", (col, dx), (n, h, w, c, _pack_conv(kh, kw, stride, pad)))
+
+
+def transpose(src, dst) -> DeviceKernel:
+    R, Cc = src.shape
+    return DeviceKernel("transpose_bf16", (src, dst), (R, Cc))
+
+
+def bn_stats(x, part, P, C, rb, mode=0, g=None, g2=None, y=None, mean=None, invstd=None) -> DeviceKernel:
+    return DeviceKernel("bn_stats", (x, g, g2, y, mean, invstd, part), (P, C, mode, rb))
+
+
+def bn_finalize_fwd(part, nrb, C, count, gamma, beta, mean, invstd, scale, shift,
+                    eps=1e-5) -> DeviceKernel:
+    return DeviceKernel("bn_finalize", (part, gamma, beta, mean, invstd, scale, shift),
+                        (nrb, C, 0, count), (eps,))
+
+
+def bn_finalize_bwd(part, nrb, C, count, dgamma, dbeta, k1, k2) -> DeviceKernel:
+    return DeviceKernel("bn_finalize", (part, None, None, dgamma, dbeta, k1, k2), (nrb, C, 1, count))
+
+
+def bn_act(x, y, scale, shift, P, C, relu=True, res=None) -> DeviceKernel:
+    return DeviceKernel("bn_act", (x, res, y, scale, shift), (P, C, int(relu)))
+
+
+def bn_bwd(g, x, mean, invstd, gamma, k1, k2, dx, P, C, g2=None, y=None, dz_out=None) -> DeviceKernel:
+    return DeviceKernel("bn_bwd", (g, g2, y, x, mean, invstd, gamma, dx),
+                        (P, C, _ptr(k1), _ptr(k2), _ptr(dz_out) or 0),
+                        keep=tuple(t for t in (k1, k2, dz_out) if t is not None))
+
+
+def maxpool_fwd(x, y, arg, n, h, w, c) -> DeviceKernel:
+    return DeviceKernel("maxpool_fwd", (x, y, arg), (n, h, w, c))
+
+
+def maxpool_bwd(dy, arg, dx, n, h, w, c, dy2=None) -> DeviceKernel:
+    return DeviceKernel("maxpool_bwd", (dy, dy2, arg, dx), (n, h, w, c))
+
+
+def avgpool_fwd(x, y, n, hw, c) -> DeviceKernel:
+    return DeviceKernel("avgpool_fwd", (x, y), (n, hw, c))
+
+
+def avgpool_bwd(dy, dx, n, hw, c) -> DeviceKernel:
+    return DeviceKernel("avgpool_bwd", (dy, dx), (n, hw, c))
+
+
+def softmax_xent(logits, bias, labels, loss, dl, dl32, ncls) -> DeviceKernel:
+    B, Npad = logits.shape
+    return DeviceKernel("softmax_xent", (logits, bias, labels, loss, dl, dl32), (B, Npad, ncls))
+
+
+def sgd_update(segs, blockmap, blocks, nbytes, lr, momentum) -> DeviceKernel:
+    """``segs``: device tensor of packed SgdSeg records; ``blockmap``: int32
+    [blocks, 2] (segment, chunk) pairs -- see resnet.SgdTable."""
+    return DeviceKernel("sgd_update", (segs, blockmap), (blocks, int(nbytes)), (lr, momentum))

@@ -1,0 +1,419 @@
+"""Config C2 best-effort training kernels (kernels_nn.cu + the bf16 GEMM
+kinds) and the ResNet-50 training step, on a B200.
+
+Every kernel is checked (a) against a PyTorch fp32 reference of the same op
+on the same bf16 inputs and (b) in all three Tally shapes -- Original,
+Sliced(1/5), PTB -- which must be bit-identical to each other and execute
+every logical block exactly once.
+
+Tolerances (north star: bf16 within 1e-2), normwise max|x - ref| / max|ref|:
+  data movement (im2col, transpose, maxpool fwd)      exact
+  bf16-output kernels                                  1e-2
+  fp32-output GEMM (fp32 accumulation order only)      1e-4
+"""
+
+from fractions import Fraction
+
+import pytest
+
+torch = pytest.importorskip("torch")
+F = pytest.importorskip("torch.nn.functional")
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module")
+def env():
+    if not torch.cuda.is_available():
+        pytest.skip("no GPU")
+    import paper_2410_07381_b200 as P
+    from paper_2410_07381_b200 import kernels
+    P.B200Device.get(0)
+    return P, kernels, kernels.Stream(high_priority=False)
+
+
+def nerr(x, ref):
+    ref = ref.double()
+    return ((x.double() - ref).abs().max() / ref.abs().max().clamp_min(1e-30)).item()
+
+
+def shapes(P, dk, stream, outs):
+    """Run dk in the three shapes; returns {shape: [clones of outs]}."""
+    res = {}
+    total = dk.total_blocks
+    workers = 148 * min(2, max(1, dk.info.occupancy_ptb))
+    for shape in ("original", "sliced", "ptb"):
+        for o in outs:
+            o.zero_()
+        ec = torch.zeros(total, dtype=torch.int64, device="cuda")
+        if shape == "original":
+            dk.original(stream, exec_count=ec).wait()
+        elif shape == "sliced":
+            for off, cnt in P.slice_plan(total, Fraction(1, 5)):
+                dk.sliced(stream, off, cnt, exec_count=ec).wait()
+        else:
+            dk.ptb(stream, min(workers, total), exec_count=ec).wait()
+        assert bool((ec == 1).all()), shape
+        res[shape] = [o.clone() for o in outs]
+    for a, b, c in zip(res["original"], res["sliced"], res["ptb"]):
+        assert torch.equal(a, b) and torch.equal(a, c)
+    return res["original"]
+
+
+def rnd(*shape, seed=0, dtype=torch.bfloat16):
+    g = torch.Generator(device="cuda").manual_seed(seed)
+    return (torch.randn(*shape, device="cuda", generator=g)).to(dtype)
+
+
+# ------------------------------------------------------------------ GEMM kinds
+@pytest.mark.parametrize("M,N,K,out,splits", [
+    (200, 64, 64, torch.bfloat16, 1),         # M tail, 64-wide tiles
+    (384, 192, 136, torch.bfloat16, 1),       # K tail (136 = 2 k-blocks + 8)
+    (256, 256, 576, torch.float32, 1),
+    (64, 576, 2048, torch.float32, 8),        # split-K weight-gradient shape
+    (1000, 128, 4096, torch.float32, 4),
+    (8, 2048, 1024, torch.bfloat16, 1),       # M = 8 (fc dgrad at batch 8)
+    (1024, 2048, 8, torch.float32, 1),        # K = 8 (fc wgrad at batch 8)
+    (512, 576, 32, torch.float32, 1),         # K = 32 (layer4 wgrad at 64 px)
+])
+def test_gemm_variants(env, M, N, K, out, splits):
+    P, kernels, stream = env
+    A, B = rnd(M, K, seed=1), rnd(N, K, seed=2)
+    C = torch.zeros(*((splits, M, N) if splits > 1 else (M, N)), device="cuda", dtype=out)
+    dk = kernels.gemm(A, B, C, splits=splits)
+    (got,) = shapes(P, dk, stream, [C])
+    if splits > 1:
+        got = got.sum(0)
+    ref = A.double() @ B.double().T
+    assert nerr(got, ref) < (1e-2 if out == torch.bfloat16 else 1e-4)
+
+
+# ------------------------------------------------------------------ im2col / col2im
+def _unfold_nhwc(x_nhwc, k, stride, pad):
+    """Reference im2col in the kernel's (kh, kw, c) column order."""
+    N, H, W, C = x_nhwc.shape
+    u = F.unfold(x_nhwc.permute(0, 3, 1, 2).float(), k, padding=pad, stride=stride)   # [N, C*k*k, L]
+    L = u.shape[-1]
+    u = u.view(N, C, k * k, L).permute(0, 3, 2, 1).reshape(N * L, k * k * C)
+    return u
+
+
+@pytest.mark.parametrize("geo", [(2, 9, 9, 16, 3, 1, 1), (2, 10, 10, 8, 7, 2, 3), (3, 8, 8, 24, 1, 2, 0),
+                                 (1, 7, 7, 64, 3, 2, 1)])
+def test_im2col_col2im(env, geo):
+    P, kernels, stream = env
+    n, h, w, c, k, s, p = geo
+    x = rnd(n, h, w, c, seed=3)
+    oh = (h + 2 * p - k) // s + 1
+    kdim = k * k * c
+    kp = (kdim + 63) // 64 * 64
+    col = torch.zeros(n * oh * oh, kp, dtype=torch.bfloat16, device="cuda")
+    dk = kernels.im2col(x, col, n, h, w, c, k, k, s, p)
+    (got,) = shapes(P, dk, stream, [col])
+    ref = _unfold_nhwc(x, k, s, p)
+    assert torch.equal(got[:, :kdim].float(), ref)
+    assert not got[:, kdim:].any()
+    # col2im = adjoint of im2col (F.fold)
+    dcol = rnd(n * oh * oh, kp, seed=4)
+    dx = torch.zeros(n, h, w, c, dtype=torch.bfloat16, device="cuda")
+    dk2 = kernels.col2im(dcol, dx, n, h, w, c, k, k, s, p)
+    (got2,) = shapes(P, dk2, stream, [dx])
+    L = oh * oh
+    u = dcol[:, :kdim].float().view(n, L, k * k, c).permute(0, 3, 2, 1).reshape(n, c * k * k, L)
+    ref2 = F.fold(u, (h, w), k, padding=p, stride=s).permute(0, 2, 3, 1)
+    assert nerr(got2, ref2) < 1e-2
+
+
+def test_transpose(env):
+    P, kernels, stream = env
+    src = rnd(300, 136, seed=5)
+    dst = torch.zeros(136, 300, dtype=torch.bfloat16, device="cuda")
+    (got,) = shapes(P, kernels.transpose(src, dst), stream, [dst])
+    assert torch.equal(got, src.t())
+
+
+# ------------------------------------------------------------------ batch norm
+@pytest.mark.parametrize("P_,C,relu,res", [(1000, 64, True, False), (777, 256, True, True), (300, 512, False, False)])
+def test_bn_forward(env, P_, C, relu, res):
+    P, kernels, stream = env
+    x = (rnd(P_, C, seed=6).float() * 3 + 1).bfloat16()
+    r = rnd(P_, C, seed=7) if res else None
+    gamma = torch.rand(C, device="cuda") + 0.5
+    beta = torch.randn(C, device="cuda")
+    rb = 128 if C < 256 else 64
+    nrb = (P_ + rb - 1) // rb
+    part = torch.zeros(2 * nrb * C, device="cuda")
+    mean, invstd, scale, shift = (torch.zeros(C, device="cuda") for _ in range(4))
+    (pt,) = shapes(P, kernels.bn_stats(x, part, P_, C, rb), stream, [part])
+    part.copy_(pt)
+    fin = kernels.bn_finalize_fwd(part, nrb, C, P_, gamma, beta, mean, invstd, scale, shift)
+    shapes(P, fin, stream, [])
+    fin.original(stream).wait()
+    xf = x.float()
+    assert nerr(mean, xf.mean(0)) < 1e-5
+    assert nerr(invstd, 1 / torch.sqrt(xf.var(0, unbiased=False) + 1e-5)) < 1e-4
+    y = torch.zeros_like(x)
+    (got,) = shapes(P, kernels.bn_act(x, y, scale, shift, P_, C, relu, r), stream, [y])
+    ref = F.batch_norm(xf, None, None, gamma, beta, training=True, eps=1e-5)
+    if res:
+        ref = ref + r.float()
+    if relu:
+        ref = ref.relu()
+    assert nerr(got, ref) < 1e-2
+
+
+@pytest.mark.parametrize("P_,C,with_g2", [(1000, 64, True), (500, 256, False)])
+def test_bn_backward(env, P_, C, with_g2):
+    """dz = (g [+ g2]) * (y > 0); dx = BN-backward(dz) -- vs autograd."""
+    P, kernels, stream = env
+    x = (rnd(P_, C, seed=8).float() * 2 + 0.5).bfloat16()
+    g = rnd(P_, C, seed=9)
+    g2 = rnd(P_, C, seed=10) if with_g2 else None
+    gamma = torch.rand(C, device="cuda") + 0.5
+    beta = torch.randn(C, device="cuda")
+    xf = x.float().requires_grad_(True)
+    gm = gamma.clone().requires_grad_(True)
+    bt = beta.clone().requires_grad_(True)
+    z = F.batch_norm(xf, None, None, gm, bt, training=True, eps=1e-5)
+    yv = z.relu()
+    up = g.float() + (g2.float() if with_g2 else 0)
+    yv.backward(up)
+    # our forward statistics
+    rb = 128 if C < 256 else 64
+    nrb = (P_ + rb - 1) // rb
+    part = torch.zeros(2 * nrb * C, device="cuda")
+    mean, invstd, scale, shift, dgam, dbet, k1, k2 = (torch.zeros(C, device="cuda") for _ in range(8))
+    kernels.bn_stats(x, part, P_, C, rb).original(stream).wait()
+    kernels.bn_finalize_fwd(part, nrb, C, P_, gamma, beta, mean, invstd, scale, shift).original(stream).wait()
+    y = torch.zeros_like(x)
+    kernels.bn_act(x, y, scale, shift, P_, C, True).original(stream).wait()
+    (pt,) = shapes(P, kernels.bn_stats(x, part, P_, C, rb, 1, g, g2, y, mean, invstd), stream, [part])
+    part.copy_(pt)
+    kernels.bn_finalize_bwd(part, nrb, C, P_, dgam, dbet, k1, k2).original(stream).wait()
+    assert nerr(dbet, bt.grad) < 1e-2 and nerr(dgam, gm.grad) < 1e-2
+    dx = torch.zeros_like(x)
+    dz = torch.zeros_like(x)
+    (gdx, gdz) = shapes(P, kernels.bn_bwd(g, x, mean, invstd, gamma, k1, k2, dx, P_, C, g2=g2, y=y, dz_out=dz),
+                        stream, [dx, dz])
+    assert nerr(gdx, xf.grad) < 1e-2
+    assert nerr(gdz, up * (y.float() > 0)) < 1e-2
+
+
+# ------------------------------------------------------------------ pooling, loss, optimizer
+def test_maxpool(env):
+    P, kernels, stream = env
+    n, h, w, c = 2, 15, 15, 64
+    x = rnd(n, h, w, c, seed=11)
+    oh = (h + 2 - 3) // 2 + 1
+    y = torch.zeros(n, oh, oh, c, dtype=torch.bfloat16, device="cuda")
+    arg = torch.zeros(n * oh * oh * c, dtype=torch.uint8, device="cuda")
+    got, _ = shapes(P, kernels.maxpool_fwd(x, y, arg, n, h, w, c), stream, [y, arg])
+    xf = x.float().permute(0, 3, 1, 2).requires_grad_(True)
+    ref = F.max_pool2d(xf, 3, 2, 1)
+    assert torch.equal(got.float(), ref.permute(0, 2, 3, 1))
+    kernels.maxpool_fwd(x, y, arg, n, h, w, c).original(stream).wait()
+    dy, dy2 = rnd(n, oh, oh, c, seed=12), rnd(n, oh, oh, c, seed=13)
+    ref.backward((dy.float() + dy2.float()).permute(0, 3, 1, 2))
+    dx = torch.zeros_like(x)
+    (gdx,) = shapes(P, kernels.maxpool_bwd(dy, arg, dx, n, h, w, c, dy2=dy2), stream, [dx])
+    assert nerr(gdx, xf.grad.permute(0, 2, 3, 1)) < 1e-2
+
+
+def test_avgpool(env):
+    P, kernels, stream = env
+    n, hw, c = 4, 49, 2048
+    x = rnd(n, hw, c, seed=14)
+    y = torch.zeros(n, c, dtype=torch.bfloat16, device="cuda")
+    (got,) = shapes(P, kernels.avgpool_fwd(x, y, n, hw, c), stream, [y])
+    assert nerr(got, x.float().mean(1)) < 1e-2
+    dy = rnd(n, c, seed=15)
+    dx = torch.zeros_like(x)
+    (gdx,) = shapes(P, kernels.avgpool_bwd(dy, dx, n, hw, c), stream, [dx])
+    assert nerr(gdx, (dy.float() / hw).unsqueeze(1).expand(n, hw, c)) < 1e-2
+
+
+def test_softmax_xent(env):
+    P, kernels, stream = env
+    B, npad, ncls = 16, 1024, 1000
+    logits = torch.randn(B, npad, device="cuda") * 3
+    bias = torch.randn(npad, device="cuda")
+    labels = torch.randint(0, ncls, (B,), device="cuda", dtype=torch.int32)
+    loss = torch.zeros(B, device="cuda")
+    dl = torch.zeros(B, npad, dtype=torch.bfloat16, device="cuda")
+    dl32 = torch.zeros(B, npad, device="cuda")
+    gl, gdl, gdl32 = shapes(P, kernels.softmax_xent(logits, bias, labels, loss, dl, dl32, ncls), stream,
+                            [loss, dl, dl32])
+    z = (logits + bias)[:, :ncls].clone().requires_grad_(True)
+    ref = F.cross_entropy(z, labels.long(), reduction="none")
+    ref.mean().backward()
+    assert nerr(gl, ref) < 1e-5
+    assert nerr(gdl32[:, :ncls], z.grad) < 1e-4 and not gdl32[:, ncls:].any()
+    assert nerr(gdl[:, :ncls], z.grad) < 1e-2
+
+
+def test_sgd_update(env):
+    P, kernels, stream = env
+    from paper_2410_07381_b200.resnet import SgdTable
+    w = torch.randn(96, 200, device="cuda")
+    v = torch.randn_like(w)
+    parts = torch.randn(3, 96, 200, device="cuda")
+    w2 = torch.randn(5000, device="cuda")
+    v2 = torch.zeros_like(w2)
+    g2 = torch.randn(1, 5000, device="cuda")
+    wb = torch.zeros(96, 200, dtype=torch.bfloat16, device="cuda")
+    wt = torch.zeros(200, 96, dtype=torch.bfloat16, device="cuda")
+    ref_v = 0.9 * v + parts.sum(0) + 1e-4 * w
+    ref_w = w - 0.1 * ref_v
+    ref_v2 = g2[0].clone()
+    ref_w2 = w2 - 0.1 * ref_v2
+    t = SgdTable()
+    t.add(w, v, parts, 3, 96 * 200, 1e-4, wb, wt, 96, 200)
+    t.add(w2, v2, g2, 1, 5000, 0.0)
+    t.build("cuda")
+    kernels.sgd_update(t.dev_segs, t.dev_map, t.blocks, t.nbytes, 0.1, 0.9).original(stream).wait()
+    assert nerr(w, ref_w) < 1e-6 and nerr(v, ref_v) < 1e-6
+    assert nerr(w2, ref_w2) < 1e-6
+    assert torch.equal(wb, w.bfloat16()) and torch.equal(wt, w.t().bfloat16())
+
+
+# ------------------------------------------------------------------ the training step
+def _nchw(t, B, h):
+    return t.float().view(B, h, h, -1).permute(0, 3, 1, 2)
+
+
+def _bn_grad(y, gamma, beta, dz):
+    """fp32 autograd of training-mode BN at our pre-BN activation y."""
+    y = y.detach().requires_grad_(True)
+    gm = gamma.clone().requires_grad_(True)
+    bt = beta.clone().requires_grad_(True)
+    F.batch_norm(y, None, None, gm, bt, training=True, eps=1e-5).backward(dz)
+    return y.grad, gm.grad, bt.grad
+
+
+def _conv_grad(x, w, stride, pad, dy):
+    x = x.detach().requires_grad_(True)
+    w = w.detach().requires_grad_(True)
+    F.conv2d(x, w, stride=stride, padding=pad).backward(dy)
+    return x.grad, w.grad
+
+
+def test_resnet50_train_step_vs_pytorch(env):
+    """One training step of the B200 program against PyTorch fp32.
+
+    Forward, per bottleneck: the torchvision block (fp32 weights, training-mode
+    BN) on OUR bf16 input activation vs our block output.
+    Backward, per bottleneck: fp32 autograd of every op of the block, each
+    evaluated at OUR saved forward tensors (so ReLU masks and BN statistics are
+    the same ones the program used), chained from our upstream gradient; vs
+    our parameter gradients and input gradient.
+    (An end-to-end fp32 run is not a parity test at this depth: PyTorch's own
+    bf16 ResNet-50 drifts 0.46 normwise from fp32 by layer4 on this batch --
+    tools/debug_resnet.py -- because bf16 rounding flips ReLU masks; ours
+    tracks that drift.)
+
+    Tolerance: the north star's bf16 1e-2, normwise max|x - ref| / max|ref|,
+    for every block output, input gradient and parameter gradient (measured
+    worst case on the B200: 8.2e-3, a block output)."""
+    P, kernels, stream = env
+    import torchvision
+    from paper_2410_07381_b200 import resnet
+    torch.manual_seed(0)
+    model = torchvision.models.resnet50(weights=None)
+    B, img, lr = 8, 64, 0.05
+    tr = resnet.ResNet50Train(batch=B, image=img, lr=lr, model=model)
+    g = torch.Generator(device="cuda").manual_seed(7)
+    images = torch.randn(B, 3, img, img, device="cuda", generator=g).bfloat16()
+    labels = torch.randint(0, 1000, (B,), device="cuda", generator=g)
+    tr.set_batch(images, labels)
+    w0 = {id(c): c.w.clone() for c in tr._all_convs()}
+    bn0 = {}
+    for blk in tr.blocks:
+        for k in ("b1", "b2", "b3", "bd"):
+            if k in blk:
+                bn0[id(blk[k])] = (blk[k].gamma.clone(), blk[k].beta.clone())
+    tr.step_original(stream)
+    m = model.cuda().float().train()
+
+    def W(c):   # the bf16 weights our GEMMs used, OIHW fp32
+        sp = c.spec
+        w = w0[id(c)][:, :sp.kdim].bfloat16().float().reshape(sp.cout, sp.k, sp.k, sp.cin)
+        return w.permute(0, 3, 1, 2).contiguous()
+
+    def ours_w(c):
+        sp = c.spec
+        return c.gpart.sum(0)[:, :sp.kdim].reshape(sp.cout, sp.k, sp.k, sp.cin).permute(0, 3, 1, 2)
+
+    errs = {}
+    prev = "maxpool"
+    for blk, sv in zip(tr.blocks, tr.saved):
+        pre = blk["pre"]
+        li, bi = int(pre[5]), int(pre.split(".")[1])
+        hh, ho = blk["h"], blk["ho"]
+        # forward: the torchvision block on our input
+        with torch.no_grad():
+            out = getattr(m, f"layer{li}")[bi](_nchw(tr.acts[prev], B, hh))
+        errs[pre + ".out"] = nerr(_nchw(tr.acts[pre], B, ho), out)
+        prev = pre
+        # backward, op by op at our forward tensors
+        bg = tr.block_grads[pre]
+        up = _nchw(bg["g"], B, ho) + (_nchw(bg["g2"], B, ho) if bg["g2"] is not None else 0)
+        dz3 = up * (_nchw(sv["out"], B, ho) > 0)
+        dy3, g3, b3 = _bn_grad(_nchw(sv["y3"], B, ho), *bn0[id(blk["b3"])], dz3)
+        do2, dw3 = _conv_grad(_nchw(sv["o2"], B, ho), W(blk["c3"]), 1, 0, dy3)
+        dy2, g2_, b2_ = _bn_grad(_nchw(sv["y2"], B, ho), *bn0[id(blk["b2"])], do2 * (_nchw(sv["o2"], B, ho) > 0))
+        do1, dw2 = _conv_grad(_nchw(sv["o1"], B, hh), W(blk["c2"]), blk["stride"], 1, dy2)
+        dy1, g1_, b1_ = _bn_grad(_nchw(sv["y1"], B, hh), *bn0[id(blk["b1"])], do1 * (_nchw(sv["o1"], B, hh) > 0))
+        dx1, dw1 = _conv_grad(_nchw(sv["x"], B, hh), W(blk["c1"]), 1, 0, dy1)
+        refs = {"conv1": (blk["c1"], dw1), "conv2": (blk["c2"], dw2), "conv3": (blk["c3"], dw3)}
+        bns = {"bn1": (blk["b1"], g1_, b1_), "bn2": (blk["b2"], g2_, b2_), "bn3": (blk["b3"], g3, b3)}
+        if "cd" in blk:
+            dyd, gd, bd = _bn_grad(_nchw(sv["yd"], B, ho), *bn0[id(blk["bd"])], dz3)
+            dxd, dwd = _conv_grad(_nchw(sv["x"], B, hh), W(blk["cd"]), blk["stride"], 0, dyd)
+            refs["downsample.0"] = (blk["cd"], dwd)
+            bns["downsample.1"] = (blk["bd"], gd, bd)
+            dx_ref = dx1 + dxd
+        else:
+            dx_ref = dx1 + dz3
+        errs[pre + ".dx"] = nerr(_nchw(bg["dx"], B, hh) + _nchw(bg["dsc"], B, hh), dx_ref)
+        for name, (c, ref) in refs.items():
+            errs[f"{pre}.{name}.wgrad"] = nerr(ours_w(c), ref)
+        for name, (bn, gr, br) in bns.items():
+            errs[f"{pre}.{name}.dgamma"] = nerr(bn.dgamma, gr)
+            errs[f"{pre}.{name}.dbeta"] = nerr(bn.dbeta, br)
+    for k, v in errs.items():
+        print(f"parity {k} {v:.3e}")
+    bad = {k: v for k, v in errs.items() if v > 1e-2}
+    assert not bad, bad
+
+
+def test_resnet50_train_step_shapes_bit_identical(env):
+    """The whole step with every kernel in PTB shape (and in Sliced(1/4))
+    produces bit-identical parameters to the untransformed step."""
+    P, kernels, stream = env
+    from paper_2410_07381_b200 import resnet
+    outs = {}
+    for shape in ("original", "ptb", "sliced"):
+        tr = resnet.ResNet50Train(batch=8, image=64, seed=3)
+        g = torch.Generator(device="cuda").manual_seed(11)
+        tr.set_batch(torch.randn(8, 3, 64, 64, device="cuda", generator=g), torch.arange(8, device="cuda"))
+        for name, dk in tr.program:
+            if shape == "original":
+                dk.original(stream).wait()
+            elif shape == "ptb":
+                dk.ptb(stream, min(dk.total_blocks, 148 * max(1, dk.info.occupancy_ptb))).wait()
+            else:
+                for off, cnt in P.slice_plan(dk.total_blocks, Fraction(1, 4)):
+                    dk.sliced(stream, off, cnt).wait()
+        outs[shape] = [t.clone() for _, t in tr.params] + [tr.loss.clone()]
+    for a, b, c in zip(outs["original"], outs["ptb"], outs["sliced"]):
+        assert torch.equal(a, b) and torch.equal(a, c)
+
+
+def test_resnet50_infer_graph(env):
+    P, kernels, stream = env
+    from paper_2410_07381_b200 import resnet
+    hp = resnet.ResNet50Infer(batch=1, image=224)
+    hs = kernels.Stream(high_priority=True)
+    hp.kernel.original(hs).wait()
+    ref = hp.reference()
+    assert nerr(hp.out, ref) < 1e-2
