@@ -105,12 +105,28 @@ __device__ __forceinline__ void umma(uint32_t tmem_d, uint64_t a, uint64_t b, ui
   }
 }
 
-// Instruction descriptor: D fp32, K-major A and B, M = 128, N = BN.
-template <int KIND, int BN>
+// MN-major operand tile (MN contiguous), 128-byte swizzle: 64-element-wide
+// atoms of 8 K-rows x 128 B; K-row groups 1024 B apart (SBO), MN atoms
+// 8192 B apart (LBO: one 64-wide TMA box of BK = 64 rows each).
+__device__ __forceinline__ uint64_t smem_desc_mn(const void* p) {
+  const uint64_t addr = smem_u32(p);
+  uint64_t d = 0;
+  d |= (addr & 0x3FFFFull) >> 4;          // start address (16 B units)
+  d |= (8192ull >> 4) << 16;              // leading byte offset: next 64-wide MN atom
+  d |= (1024ull >> 4) << 32;              // stride byte offset: next 8 K-rows
+  d |= 1ull << 46;                        // descriptor version (sm_100)
+  d |= 2ull << 61;                        // SWIZZLE_128B
+  return d;
+}
+
+// Instruction descriptor: D fp32, A and B K-major (or both MN-major), M = 128, N = BN.
+template <int KIND, int BN, bool MN = false>
 __host__ __device__ constexpr uint32_t make_idesc() {
   return (1u << 4)                                  // D format: F32
          | ((KIND == 0 ? 2u : 1u) << 7)             // A format: TF32 / BF16
          | ((KIND == 0 ? 2u : 1u) << 10)            // B format
+         | ((MN ? 1u : 0u) << 15)                   // A major: MN
+         | ((MN ? 1u : 0u) << 16)                   // B major: MN
          | ((uint32_t)(BN >> 3) << 17)              // N >> 3
          | ((uint32_t)(128 >> 4) << 24);            // M >> 4
 }
@@ -153,6 +169,7 @@ struct CfgTf32x3T {
   static constexpr int STAGES = STAGES_;
   static constexpr int UMMA_K = 8;
   static constexpr int TMEM_COLS = BN == 64 ? 256 : 512;   // 2 x BN accumulators + BN running total
+  static constexpr bool MN = false;
   using OutT = float;
 };
 // 128x128 tiles halve L2->SM operand bytes per flop (the kernel is L2-bound);
@@ -163,7 +180,7 @@ using CfgTf32x3N64 = CfgTf32x3T<64, 4>;
 // bf16 operands, fp32 TMEM accumulation; BN = 128 or 64 (N % 128 != 0, e.g.
 // 64-channel convolutions), output bf16 (activations) or fp32 (split-K
 // weight-gradient partials, logits)
-template <int BN_, class OutT_>
+template <int BN_, class OutT_, bool MN_ = false>
 struct CfgBf16T {
   static constexpr int KIND = 1;
   static constexpr int BM = 128, BN = BN_;
@@ -180,12 +197,18 @@ struct CfgBf16T {
   // promotion chunks at the 1e-2 bf16 budget): 2 x BN columns, leaving TMEM
   // for co-resident high-priority tensor-core kernels
   static constexpr int TMEM_COLS = 2 * BN;
+  // MN-major operands: A given as A^T [K, M] and B as B^T [K, N] (M / N
+  // contiguous) -- the weight gradient dW = dY^T . X reads both activations
+  // as stored, no transposes
+  static constexpr bool MN = MN_;
   using OutT = OutT_;
 };
 using CfgBf16 = CfgBf16T<128, __nv_bfloat16>;
 using CfgBf16N64 = CfgBf16T<64, __nv_bfloat16>;
 using CfgBf16F32 = CfgBf16T<128, float>;
 using CfgBf16F32N64 = CfgBf16T<64, float>;
+using CfgBf16MN = CfgBf16T<128, float, true>;
+using CfgBf16MNN64 = CfgBf16T<64, float, true>;
 
 constexpr int GROUP_M = 8;
 constexpr int kThreads = 192;   // producer warp, MMA warp, 4 epilogue warps
@@ -367,6 +390,14 @@ __global__ void __launch_bounds__(kThreads, 1) k_gemm(const __grid_constant__ Ge
               tma_load_2d(base + Cfg::A_BYTES, &p.a_lo, &full[st], kx, mb * Cfg::BM);
               tma_load_2d(base + 2 * Cfg::A_BYTES, &p.b_hi, &full[st], kx, nb * Cfg::BN);
               tma_load_2d(base + 2 * Cfg::A_BYTES + Cfg::B_BYTES, &p.b_lo, &full[st], kx, nb * Cfg::BN);
+            } else if constexpr (Cfg::MN) {
+              // boxes of 64 MN-elements x BK K-rows, 8 KB each
+#pragma unroll
+              for (int h = 0; h < Cfg::BM / 64; ++h)
+                tma_load_2d(base + h * 8192, &p.a_hi, &full[st], mb * Cfg::BM + h * 64, kb * Cfg::BK);
+#pragma unroll
+              for (int h = 0; h < Cfg::BN / 64; ++h)
+                tma_load_2d(base + Cfg::A_BYTES + h * 8192, &p.b_hi, &full[st], nb * Cfg::BN + h * 64, kb * Cfg::BK);
             } else {
               tma_load_2d(base, &p.a_hi, &full[st], kx, mb * Cfg::BM);
               tma_load_2d(base + Cfg::A_BYTES, &p.b_hi, &full[st], kx, nb * Cfg::BN);
@@ -382,7 +413,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_gemm(const __grid_constant__ Ge
       // The tile's K range is cut into chunks of p.kchunk k-blocks; each chunk
       // accumulates into one of two TMEM buffers and is promoted to an fp32
       // running total by the epilogue (bounded tensor-core accumulation chains).
-      constexpr uint32_t idesc = make_idesc<Cfg::KIND, Cfg::BN>();
+      constexpr uint32_t idesc = make_idesc<Cfg::KIND, Cfg::BN, Cfg::MN>();
       uint32_t it = 0, ci = 0;
       for (int i = 0;; ++i) {
         const int j = i & 1;
@@ -424,6 +455,9 @@ __global__ void __launch_bounds__(kThreads, 1) k_gemm(const __grid_constant__ Ge
                 umma<0>(d, alo, bhi, idesc, first);   // small terms first
                 umma<0>(d, ahi, blo, idesc, 1);
                 umma<0>(d, ahi, bhi, idesc, 1);
+              } else if constexpr (Cfg::MN) {
+                // UMMA_K = 16 K-rows = two 8-row groups = 2048 B per step
+                umma<1>(d, smem_desc_mn(base + k * 2048), smem_desc_mn(base + Cfg::A_BYTES + k * 2048), idesc, first);
               } else {
                 umma<1>(d, smem_desc(base + koff), smem_desc(base + Cfg::A_BYTES + koff), idesc, first);
               }
@@ -643,7 +677,8 @@ static int bind_gemm(const tally_kernel_args* a, Instance* inst, bool split) {
   // (K tail: TMA zero-fills the k-block past K in both operands; rows must
   // stay 16-byte aligned for the tensor map)
   const bool m_ok = Cfg::KIND == 1 ? true : (M % Cfg::BM == 0);
-  const bool k_ok = Cfg::KIND == 1 ? (K % 8 == 0) : (K % Cfg::BK == 0);
+  // (MN-major: the tensor-map rows are K, the contiguous dims M and N)
+  const bool k_ok = Cfg::MN ? (M % 8 == 0) : Cfg::KIND == 1 ? (K % 8 == 0) : (K % Cfg::BK == 0);
   if (M < 1 || N < 1 || K < 1 || !m_ok || N % Cfg::BN || !k_ok) {
     set_error("gemm: need M %s, N %% %d == 0, K %s (got %lld %lld %lld)",
               Cfg::KIND == 1 ? ">= 1" : "% 128 == 0", Cfg::BN, Cfg::KIND == 1 ? "% 8 == 0" : "% 32 == 0", M, N, K);
@@ -668,6 +703,10 @@ static int bind_gemm(const tally_kernel_args* a, Instance* inst, bool split) {
     if ((rc = make_map(&p.b_hi, a->ptr[2], dt, Cfg::ESZ, N, K, Cfg::BN))) return rc;
     if ((rc = make_map(&p.b_lo, a->ptr[3], dt, Cfg::ESZ, N, K, Cfg::BN))) return rc;
     p.c = a->ptr[4];
+  } else if (Cfg::MN) {   // ptr: A^T [K, M], B^T [K, N], C; boxes of 64 MN x BK K-rows
+    if ((rc = make_map(&p.a_hi, a->ptr[0], dt, Cfg::ESZ, K, M, Cfg::BK))) return rc;
+    if ((rc = make_map(&p.b_hi, a->ptr[1], dt, Cfg::ESZ, K, N, Cfg::BK))) return rc;
+    p.c = a->ptr[2];
   } else {       // ptr: A, B, C
     if ((rc = make_map(&p.a_hi, a->ptr[0], dt, Cfg::ESZ, M, K, Cfg::BM))) return rc;
     if ((rc = make_map(&p.b_hi, a->ptr[1], dt, Cfg::ESZ, N, K, Cfg::BN))) return rc;
@@ -767,13 +806,15 @@ static KernelKind gemm_kind(const char* name, int (*bind)(const tally_kernel_arg
 }
 
 int register_gemm_kernels(KernelKind* out, int cap) {
-  if (cap < 7) return 0;
+  if (cap < 9) return 0;
   out[0] = gemm_kind<gemm::CfgTf32x3>("sgemm_tf32x3", bind_sgemm);
   out[1] = gemm_kind<gemm::CfgBf16>("gemm_bf16", bind_bf16<gemm::CfgBf16>);
   out[3] = gemm_kind<gemm::CfgTf32x3N64>("sgemm_tf32x3_n64", bind_sgemm_n64);
   out[4] = gemm_kind<gemm::CfgBf16N64>("gemm_bf16_n64", bind_bf16<gemm::CfgBf16N64>);
   out[5] = gemm_kind<gemm::CfgBf16F32>("gemm_bf16f32", bind_bf16<gemm::CfgBf16F32>);
   out[6] = gemm_kind<gemm::CfgBf16F32N64>("gemm_bf16f32_n64", bind_bf16<gemm::CfgBf16F32N64>);
+  out[7] = gemm_kind<gemm::CfgBf16MN>("gemm_bf16f32_mn", bind_bf16<gemm::CfgBf16MN>);
+  out[8] = gemm_kind<gemm::CfgBf16MNN64>("gemm_bf16f32_mn_n64", bind_bf16<gemm::CfgBf16MNN64>);
   KernelKind k{};
   k.name = "split_tf32";
   k.fn_original = reinterpret_cast<const void*>(&k_original<gemm::SplitTf32>);
@@ -781,7 +822,7 @@ int register_gemm_kernels(KernelKind* out, int cap) {
   k.fn_ptb = reinterpret_cast<const void*>(&k_ptb<gemm::SplitTf32>);
   k.bind = bind_split;
   out[2] = k;
-  return 7;
+  return 9;
 }
 
 }  // namespace tally

@@ -64,7 +64,12 @@ __device__ __forceinline__ uint4 ld16(const uint4* p) {
   return v;
 }
 
-constexpr int kVecPerBlock = 2048;   // 32 KB of bf16 per logical block for the elementwise kinds
+// Logical blocks are small (16 KB of bf16 for the elementwise kinds) so that a
+// kernel has many more of them than PTB workers: Eq. 1's turnaround estimate
+// (latency x workers / blocks) stays under the threshold with full-occupancy
+// worker counts.  Each thread keeps kIlp 16-byte loads in flight.
+constexpr int kIlp = 4;
+constexpr int kVecPerBlock = 256 * kIlp;
 
 // ---------------------------------------------------------------- im2col
 struct Geometry {
@@ -88,25 +93,33 @@ struct Im2Col {
     const int kv = g.Kp >> 3, cv = g.C >> 3;
     const long long r0 = (long long)bidx.x * p.rpb;
     const int total = p.rpb * kv;
-    for (int i = threadIdx.x; i < total; i += kThreads) {
-      const int rr = i / kv, j = i - rr * kv;
-      const long long r = r0 + rr;
-      if (r >= p.rows) break;
-      uint4 v = make_uint4(0u, 0u, 0u, 0u);
-      const int k = j << 3;
-      if (k < g.K) {
-        const int ow = (int)(r % g.OW);
-        const long long t = r / g.OW;
-        const int oh = (int)(t % g.OH);
-        const int n = (int)(t / g.OH);
-        const int kwc = g.KW * g.C;
-        const int kh = k / kwc, rem = k - kh * kwc;
-        const int kw = rem / g.C, c = rem - kw * g.C;
-        const int ih = oh * g.stride - g.pad + kh, iw = ow * g.stride - g.pad + kw;
-        if (ih >= 0 && ih < g.H && iw >= 0 && iw < g.W)
-          v = ld16(p.x + (((long long)n * g.H + ih) * g.W + iw) * cv + (c >> 3));
+    const int kwc = g.KW * g.C;
+    for (int i0 = 0; i0 < total; i0 += kThreads * kIlp) {
+      uint4 v[kIlp];
+      long long dst[kIlp];
+#pragma unroll
+      for (int u = 0; u < kIlp; ++u) {
+        const int i = i0 + u * kThreads + threadIdx.x;
+        const int rr = i / kv, j = i - rr * kv;
+        const long long r = r0 + rr;
+        dst[u] = (i < total && r < p.rows) ? r * kv + j : -1;
+        v[u] = make_uint4(0u, 0u, 0u, 0u);
+        const int k = j << 3;
+        if (dst[u] >= 0 && k < g.K) {
+          const int ow = (int)(r % g.OW);
+          const long long t = r / g.OW;
+          const int oh = (int)(t % g.OH);
+          const int n = (int)(t / g.OH);
+          const int kh = k / kwc, rem = k - kh * kwc;
+          const int kw = rem / g.C, c = rem - kw * g.C;
+          const int ih = oh * g.stride - g.pad + kh, iw = ow * g.stride - g.pad + kw;
+          if (ih >= 0 && ih < g.H && iw >= 0 && iw < g.W)
+            v[u] = ld16(p.x + (((long long)n * g.H + ih) * g.W + iw) * cv + (c >> 3));
+        }
       }
-      p.col[r * kv + j] = v;
+#pragma unroll
+      for (int u = 0; u < kIlp; ++u)
+        if (dst[u] >= 0) p.col[dst[u]] = v[u];
     }
   }
 };
@@ -124,6 +137,7 @@ struct Col2Im {
     const Geometry& g = p.g;
     const int cv = g.C >> 3, kv = g.Kp >> 3;
     const long long v0 = (long long)bidx.x * kVecPerBlock;
+#pragma unroll 2
     for (int i = threadIdx.x; i < kVecPerBlock; i += kThreads) {
       const long long v = v0 + i;
       if (v >= p.nvec) break;
@@ -212,30 +226,49 @@ struct BnStats {
 #pragma unroll
       for (int e = 0; e < 8; ++e) { mu[e] = p.mean[c + e]; is[e] = p.invstd[c + e]; }
     }
-    for (long long r = rbeg + lane_r; r < rend; r += rl) {
-      const long long off = r * cvec + (c >> 3);
-      float x[8];
-      unpack8(ld16(p.x + off), x);
-      if (p.mode == 0) {
+    for (long long r0 = rbeg + lane_r; r0 < rend; r0 += (long long)rl * kIlp) {
+      uint4 xv[kIlp], gv[kIlp], g2v[kIlp], yv[kIlp];
+      bool ok[kIlp];
 #pragma unroll
-        for (int e = 0; e < 8; ++e) { s1[e] += x[e]; s2[e] += x[e] * x[e]; }
-      } else {
-        float dz[8];
-        unpack8(ld16(p.g + off), dz);
-        if (p.g2) {
-          float t[8];
-          unpack8(ld16(p.g2 + off), t);
-#pragma unroll
-          for (int e = 0; e < 8; ++e) dz[e] += t[e];
+      for (int u = 0; u < kIlp; ++u) {
+        const long long r = r0 + (long long)u * rl;
+        ok[u] = r < rend;
+        const long long off = r * cvec + (c >> 3);
+        if (ok[u]) {
+          xv[u] = ld16(p.x + off);
+          if (p.mode == 1) {
+            gv[u] = ld16(p.g + off);
+            if (p.g2) g2v[u] = ld16(p.g2 + off);
+            if (p.y) yv[u] = ld16(p.y + off);
+          }
         }
-        if (p.y) {
-          float t[8];
-          unpack8(ld16(p.y + off), t);
+      }
 #pragma unroll
-          for (int e = 0; e < 8; ++e) dz[e] = t[e] > 0.f ? dz[e] : 0.f;
+      for (int u = 0; u < kIlp; ++u) {
+        if (!ok[u]) continue;
+        float x[8];
+        unpack8(xv[u], x);
+        if (p.mode == 0) {
+#pragma unroll
+          for (int e = 0; e < 8; ++e) { s1[e] += x[e]; s2[e] += x[e] * x[e]; }
+        } else {
+          float dz[8];
+          unpack8(gv[u], dz);
+          if (p.g2) {
+            float t[8];
+            unpack8(g2v[u], t);
+#pragma unroll
+            for (int e = 0; e < 8; ++e) dz[e] += t[e];
+          }
+          if (p.y) {
+            float t[8];
+            unpack8(yv[u], t);
+#pragma unroll
+            for (int e = 0; e < 8; ++e) dz[e] = t[e] > 0.f ? dz[e] : 0.f;
+          }
+#pragma unroll
+          for (int e = 0; e < 8; ++e) { s1[e] += dz[e]; s2[e] += dz[e] * ((x[e] - mu[e]) * is[e]); }
         }
-#pragma unroll
-        for (int e = 0; e < 8; ++e) { s1[e] += dz[e]; s2[e] += dz[e] * ((x[e] - mu[e]) * is[e]); }
       }
     }
     float* red = reinterpret_cast<float*>(smem);   // [2][rl][CB]
@@ -257,52 +290,76 @@ struct BnStats {
 };
 
 struct BnFinalize {
-  static constexpr int kThreads = 256;   // 8 warps = 8 channels per logical block
+  // 32 channels x 8 row lanes per logical block; each lane sums every 8th
+  // partial row, then a fixed-order combine in shared memory (deterministic)
+  static constexpr int kThreads = 256;
   struct Params {
     const float* part;   // [2][nrb][C]
     int nrb, C, mode;
     float inv_count, eps;
     const float* gamma;
-    const float* beta;
-    float* mean;     // mode 0 outputs
-    float* invstd;
+    const float* beta;     // mode 0
+    const float* mean;     // mode 1 inputs
+    const float* invstd;
+    float* o_mean;         // mode 0 outputs
+    float* o_invstd;
     float* scale;
     float* shift;
-    float* dgamma;   // mode 1 outputs (gradient slots)
-    float* dbeta;
-    float* k1;
-    float* k2;
+    float* dgamma;         // mode 1 outputs: gradient slots and the
+    float* dbeta;          //   bn_bwd coefficients dx = ca*dz + cb*x + cc
+    float* ca;
+    float* cb;
+    float* cc;
   };
-  static __device__ __forceinline__ void run(const Params& p, uint3 bidx, uint3, char*) {
-    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    const int c = bidx.x * 8 + warp;
-    if (c >= p.C) return;   // warp-uniform, no barrier in this body
+  static __device__ __forceinline__ void run(const Params& p, uint3 bidx, uint3, char* smem) {
+    const int lane_c = threadIdx.x & 31, lane_r = threadIdx.x >> 5;
+    const int c = bidx.x * 32 + lane_c;
     float a = 0.f, b = 0.f;
-    for (int k = lane; k < p.nrb; k += 32) {
-      a += p.part[(long long)k * p.C + c];
-      b += p.part[((long long)p.nrb + k) * p.C + c];
+    if (c < p.C) {
+      int k = lane_r;
+      for (; k + 24 < p.nrb; k += 32) {
+        float x0 = p.part[(long long)k * p.C + c], x1 = p.part[(long long)(k + 8) * p.C + c];
+        float x2 = p.part[(long long)(k + 16) * p.C + c], x3 = p.part[(long long)(k + 24) * p.C + c];
+        float y0 = p.part[((long long)p.nrb + k) * p.C + c], y1 = p.part[((long long)p.nrb + k + 8) * p.C + c];
+        float y2 = p.part[((long long)p.nrb + k + 16) * p.C + c], y3 = p.part[((long long)p.nrb + k + 24) * p.C + c];
+        a += ((x0 + x1) + (x2 + x3));
+        b += ((y0 + y1) + (y2 + y3));
+      }
+      for (; k < p.nrb; k += 8) {
+        a += p.part[(long long)k * p.C + c];
+        b += p.part[((long long)p.nrb + k) * p.C + c];
+      }
     }
+    float* red = reinterpret_cast<float*>(smem);   // [2][8][32]
+    red[lane_r * 32 + lane_c] = a;
+    red[256 + lane_r * 32 + lane_c] = b;
+    __syncthreads();
+    if (lane_r == 0 && c < p.C) {
+      a = 0.f;
+      b = 0.f;
 #pragma unroll
-    for (int o = 16; o > 0; o >>= 1) {
-      a += __shfl_xor_sync(0xffffffffu, a, o);
-      b += __shfl_xor_sync(0xffffffffu, b, o);
+      for (int r = 0; r < 8; ++r) { a += red[r * 32 + lane_c]; b += red[256 + r * 32 + lane_c]; }
+      if (p.mode == 0) {
+        const float m = a * p.inv_count;
+        const float var = fmaxf(b * p.inv_count - m * m, 0.f);
+        const float is = rsqrtf(var + p.eps);
+        p.o_mean[c] = m;
+        p.o_invstd[c] = is;
+        const float sc = p.gamma[c] * is;
+        p.scale[c] = sc;
+        p.shift[c] = p.beta[c] - m * sc;
+      } else {
+        p.dbeta[c] = a;
+        p.dgamma[c] = b;
+        const float is = p.invstd[c];
+        const float k1 = a * p.inv_count, k2 = b * p.inv_count;
+        const float al = p.gamma[c] * is;
+        p.ca[c] = al;
+        p.cb[c] = -al * k2 * is;
+        p.cc[c] = al * (k2 * is * p.mean[c] - k1);
+      }
     }
-    if (lane != 0) return;
-    if (p.mode == 0) {
-      const float m = a * p.inv_count;
-      const float var = fmaxf(b * p.inv_count - m * m, 0.f);
-      const float is = rsqrtf(var + p.eps);
-      p.mean[c] = m;
-      p.invstd[c] = is;
-      const float sc = p.gamma[c] * is;
-      p.scale[c] = sc;
-      p.shift[c] = p.beta[c] - m * sc;
-    } else {
-      p.dbeta[c] = a;
-      p.dgamma[c] = b;
-      p.k1[c] = a * p.inv_count;
-      p.k2[c] = b * p.inv_count;
-    }
+    __syncthreads();
   }
 };
 
@@ -320,22 +377,34 @@ struct BnAct {
   };
   static __device__ __forceinline__ void run(const Params& p, uint3 bidx, uint3, char*) {
     const int cv = p.C >> 3;
-    const long long v0 = (long long)bidx.x * kVecPerBlock;
-    for (int i = threadIdx.x; i < kVecPerBlock; i += kThreads) {
-      const long long v = v0 + i;
-      if (v >= p.nvec) break;
+    const long long v0 = (long long)bidx.x * kVecPerBlock + threadIdx.x;
+    uint4 xv[kIlp], rv[kIlp];
+#pragma unroll
+    for (int u = 0; u < kIlp; ++u) {
+      const long long v = v0 + u * kThreads;
+      if (v < p.nvec) {
+        xv[u] = ld16(p.x + v);
+        if (p.res) rv[u] = ld16(p.res + v);
+      }
+    }
+#pragma unroll
+    for (int u = 0; u < kIlp; ++u) {
+      const long long v = v0 + u * kThreads;
+      if (v >= p.nvec) continue;
       const int c = (int)(v % cv) << 3;
       float x[8];
-      unpack8(ld16(p.x + v), x);
-      const float4 s0 = *reinterpret_cast<const float4*>(p.scale + c), s1 = *reinterpret_cast<const float4*>(p.scale + c + 4);
-      const float4 h0 = *reinterpret_cast<const float4*>(p.shift + c), h1 = *reinterpret_cast<const float4*>(p.shift + c + 4);
+      unpack8(xv[u], x);
+      const float4 s0 = __ldg(reinterpret_cast<const float4*>(p.scale + c));
+      const float4 s1 = __ldg(reinterpret_cast<const float4*>(p.scale + c + 4));
+      const float4 h0 = __ldg(reinterpret_cast<const float4*>(p.shift + c));
+      const float4 h1 = __ldg(reinterpret_cast<const float4*>(p.shift + c + 4));
       const float sc[8] = {s0.x, s0.y, s0.z, s0.w, s1.x, s1.y, s1.z, s1.w};
       const float sh[8] = {h0.x, h0.y, h0.z, h0.w, h1.x, h1.y, h1.z, h1.w};
 #pragma unroll
       for (int e = 0; e < 8; ++e) x[e] = x[e] * sc[e] + sh[e];
       if (p.res) {
         float r[8];
-        unpack8(ld16(p.res + v), r);
+        unpack8(rv[u], r);
 #pragma unroll
         for (int e = 0; e < 8; ++e) x[e] += r[e];
       }
@@ -348,6 +417,11 @@ struct BnAct {
   }
 };
 
+__device__ __forceinline__ void ld8f(const float* p, float (&f)[8]) {
+  const float4 a = __ldg(reinterpret_cast<const float4*>(p)), b = __ldg(reinterpret_cast<const float4*>(p + 4));
+  f[0] = a.x; f[1] = a.y; f[2] = a.z; f[3] = a.w; f[4] = b.x; f[5] = b.y; f[6] = b.z; f[7] = b.w;
+}
+
 struct BnBwd {
   static constexpr int kThreads = 256;
   struct Params {
@@ -355,11 +429,9 @@ struct BnBwd {
     const uint4* g2;    // optional
     const uint4* y;     // optional ReLU mask source
     const uint4* x;
-    const float* mean;
-    const float* invstd;
-    const float* gamma;
-    const float* k1;
-    const float* k2;
+    const float* ca;    // dx = ca*dz + cb*x + cc (bn_finalize mode 1)
+    const float* cb;
+    const float* cc;
     uint4* dx;
     uint4* dz_out;      // optional: the masked upstream gradient (for the shortcut)
     long long nvec;
@@ -367,34 +439,46 @@ struct BnBwd {
   };
   static __device__ __forceinline__ void run(const Params& p, uint3 bidx, uint3, char*) {
     const int cv = p.C >> 3;
-    const long long v0 = (long long)bidx.x * kVecPerBlock;
-    for (int i = threadIdx.x; i < kVecPerBlock; i += kThreads) {
-      const long long v = v0 + i;
-      if (v >= p.nvec) break;
+    const long long v0 = (long long)bidx.x * kVecPerBlock + threadIdx.x;
+    uint4 gv[kIlp], g2v[kIlp], yv[kIlp], xv[kIlp];
+#pragma unroll
+    for (int u = 0; u < kIlp; ++u) {
+      const long long v = v0 + u * kThreads;
+      if (v < p.nvec) {
+        gv[u] = ld16(p.g + v);
+        xv[u] = ld16(p.x + v);
+        if (p.g2) g2v[u] = ld16(p.g2 + v);
+        if (p.y) yv[u] = ld16(p.y + v);
+      }
+    }
+#pragma unroll
+    for (int u = 0; u < kIlp; ++u) {
+      const long long v = v0 + u * kThreads;
+      if (v >= p.nvec) continue;
       const int c = (int)(v % cv) << 3;
       float dz[8], x[8];
-      unpack8(ld16(p.g + v), dz);
+      unpack8(gv[u], dz);
       if (p.g2) {
         float t[8];
-        unpack8(ld16(p.g2 + v), t);
+        unpack8(g2v[u], t);
 #pragma unroll
         for (int e = 0; e < 8; ++e) dz[e] += t[e];
       }
       if (p.y) {
         float t[8];
-        unpack8(ld16(p.y + v), t);
+        unpack8(yv[u], t);
 #pragma unroll
         for (int e = 0; e < 8; ++e) dz[e] = t[e] > 0.f ? dz[e] : 0.f;
       }
       if (p.dz_out) p.dz_out[v] = pack8(dz);
-      unpack8(ld16(p.x + v), x);
+      unpack8(xv[u], x);
+      float a[8], b[8], k[8];
+      ld8f(p.ca + c, a);
+      ld8f(p.cb + c, b);
+      ld8f(p.cc + c, k);
       float o[8];
 #pragma unroll
-      for (int e = 0; e < 8; ++e) {
-        const float is = p.invstd[c + e];
-        const float xh = (x[e] - p.mean[c + e]) * is;
-        o[e] = p.gamma[c + e] * is * (dz[e] - p.k1[c + e] - xh * p.k2[c + e]);
-      }
+      for (int e = 0; e < 8; ++e) o[e] = a[e] * dz[e] + (b[e] * x[e] + k[e]);
       p.dx[v] = pack8(o);
     }
   }
@@ -614,32 +698,60 @@ struct SgdSeg {
 
 struct SgdUpdate {
   static constexpr int kThreads = 256;
-  static constexpr int kChunk = 4096;   // elements per logical block
+  static constexpr int kChunk = kThreads * 4;   // elements per logical block (float4 per thread)
   struct Params {
     const SgdSeg* segs;
     const int2* map;      // logical block -> (segment, chunk)
     float lr, momentum;
   };
+  static __device__ __forceinline__ float4 ld4(const float* p) { return __ldg(reinterpret_cast<const float4*>(p)); }
   static __device__ __forceinline__ void run(const Params& p, uint3 bidx, uint3, char*) {
     const int2 m = p.map[bidx.x];
     const SgdSeg& s = p.segs[m.x];
-    const long long i0 = (long long)m.y * kChunk;
-    for (int k = threadIdx.x; k < kChunk; k += kThreads) {
-      const long long i = i0 + k;
-      if (i >= s.n) break;
-      float g = 0.f;
-      for (int j = 0; j < s.S; ++j) g += s.grad[(long long)j * s.gstride + i];
-      const float w = s.w[i];
-      g += s.wd * w;
-      const float v = p.momentum * s.v[i] + g;
-      const float w2 = w - p.lr * v;
-      s.v[i] = v;
-      s.w[i] = w2;
-      const __nv_bfloat16 h = __float2bfloat16_rn(w2);
-      if (s.wb) s.wb[i] = h;
-      if (s.wt) {
-        const long long r = i / s.cols, c = i - r * s.cols;
-        s.wt[c * s.rows + r] = h;
+    const long long i = (long long)m.y * kChunk + threadIdx.x * 4;
+    if (i >= s.n) return;   // no barrier in this body; segment sizes are multiples of 4
+    // split-K / per-row gradient partials, summed in a fixed order
+    float4 g = make_float4(0.f, 0.f, 0.f, 0.f);
+    int j = 0;
+    for (; j + 4 <= s.S; j += 4) {
+      const float4 a0 = ld4(s.grad + (long long)j * s.gstride + i);
+      const float4 a1 = ld4(s.grad + (long long)(j + 1) * s.gstride + i);
+      const float4 a2 = ld4(s.grad + (long long)(j + 2) * s.gstride + i);
+      const float4 a3 = ld4(s.grad + (long long)(j + 3) * s.gstride + i);
+      g.x = (((g.x + a0.x) + a1.x) + a2.x) + a3.x;
+      g.y = (((g.y + a0.y) + a1.y) + a2.y) + a3.y;
+      g.z = (((g.z + a0.z) + a1.z) + a2.z) + a3.z;
+      g.w = (((g.w + a0.w) + a1.w) + a2.w) + a3.w;
+    }
+    for (; j < s.S; ++j) {
+      const float4 a = ld4(s.grad + (long long)j * s.gstride + i);
+      g.x += a.x; g.y += a.y; g.z += a.z; g.w += a.w;
+    }
+    const float4 w = *reinterpret_cast<const float4*>(s.w + i);
+    const float4 v = *reinterpret_cast<const float4*>(s.v + i);
+    const float gw[4] = {g.x + s.wd * w.x, g.y + s.wd * w.y, g.z + s.wd * w.z, g.w + s.wd * w.w};
+    const float wv[4] = {w.x, w.y, w.z, w.w};
+    const float vv[4] = {v.x, v.y, v.z, v.w};
+    float nw[4], nv[4];
+#pragma unroll
+    for (int e = 0; e < 4; ++e) {
+      nv[e] = p.momentum * vv[e] + gw[e];
+      nw[e] = wv[e] - p.lr * nv[e];
+    }
+    *reinterpret_cast<float4*>(s.v + i) = make_float4(nv[0], nv[1], nv[2], nv[3]);
+    *reinterpret_cast<float4*>(s.w + i) = make_float4(nw[0], nw[1], nw[2], nw[3]);
+    if (s.wb) {
+      __nv_bfloat162 h0 = __floats2bfloat162_rn(nw[0], nw[1]), h1 = __floats2bfloat162_rn(nw[2], nw[3]);
+      uint2 u;
+      u.x = *reinterpret_cast<uint32_t*>(&h0);
+      u.y = *reinterpret_cast<uint32_t*>(&h1);
+      *reinterpret_cast<uint2*>(s.wb + i) = u;
+    }
+    if (s.wt) {
+#pragma unroll
+      for (int e = 0; e < 4; ++e) {
+        const long long r = (i + e) / s.cols, c = (i + e) - r * s.cols;
+        s.wt[c * s.rows + r] = __float2bfloat16_rn(nw[e]);
       }
     }
   }
@@ -757,37 +869,41 @@ static int bind_bn_stats(const tally_kernel_args* a, Instance* inst) {
   return TALLY_OK;
 }
 
-// ptr: part, gamma, beta, mean, invstd, scale, shift.  (mode 1: ptr[3..6] = dgamma, dbeta, k1, k2)
+// mode 0 -- ptr: part, gamma, beta, mean, invstd, scale, shift
+// mode 1 -- ptr: part, gamma, mean, invstd, dgamma, dbeta, ca, cb; i[4]: cc address
 // i: nrb, C, mode, count.  f: eps
 static int bind_bn_finalize(const tally_kernel_args* a, Instance* inst) {
   nn::BnFinalize::Params p{};
   p.part = static_cast<const float*>(a->ptr[0]);
+  p.gamma = static_cast<const float*>(a->ptr[1]);
   p.nrb = (int)a->i[0];
   p.C = (int)a->i[1];
   p.mode = (int)a->i[2];
   const long long count = a->i[3];
   p.eps = (float)a->f[0];
-  if (!p.part || p.nrb < 1 || p.C < 1 || count < 1 || (p.mode != 0 && p.mode != 1)) {
-    set_error("bn_finalize: need part, nrb, C, count >= 1, mode 0/1");
+  if (!p.part || !p.gamma || p.nrb < 1 || p.C < 1 || count < 1 || (p.mode != 0 && p.mode != 1)) {
+    set_error("bn_finalize: need part, gamma, nrb, C, count >= 1, mode 0/1");
     return TALLY_EINVAL;
   }
   p.inv_count = (float)(1.0 / (double)count);
   if (p.mode == 0) {
-    p.gamma = static_cast<const float*>(a->ptr[1]);
     p.beta = static_cast<const float*>(a->ptr[2]);
-    p.mean = static_cast<float*>(a->ptr[3]);
-    p.invstd = static_cast<float*>(a->ptr[4]);
+    p.o_mean = static_cast<float*>(a->ptr[3]);
+    p.o_invstd = static_cast<float*>(a->ptr[4]);
     p.scale = static_cast<float*>(a->ptr[5]);
     p.shift = static_cast<float*>(a->ptr[6]);
-    if (!p.gamma || !p.beta || !p.mean || !p.invstd || !p.scale || !p.shift) { set_error("bn_finalize: mode 0 outputs"); return TALLY_EINVAL; }
+    if (!p.beta || !p.o_mean || !p.o_invstd || !p.scale || !p.shift) { set_error("bn_finalize: mode 0 operands"); return TALLY_EINVAL; }
   } else {
-    p.dgamma = static_cast<float*>(a->ptr[3]);
-    p.dbeta = static_cast<float*>(a->ptr[4]);
-    p.k1 = static_cast<float*>(a->ptr[5]);
-    p.k2 = static_cast<float*>(a->ptr[6]);
-    if (!p.dgamma || !p.dbeta || !p.k1 || !p.k2) { set_error("bn_finalize: mode 1 outputs"); return TALLY_EINVAL; }
+    p.mean = static_cast<const float*>(a->ptr[2]);
+    p.invstd = static_cast<const float*>(a->ptr[3]);
+    p.dgamma = static_cast<float*>(a->ptr[4]);
+    p.dbeta = static_cast<float*>(a->ptr[5]);
+    p.ca = static_cast<float*>(a->ptr[6]);
+    p.cb = static_cast<float*>(a->ptr[7]);
+    p.cc = reinterpret_cast<float*>(a->i[4]);
+    if (!p.mean || !p.invstd || !p.dgamma || !p.dbeta || !p.ca || !p.cb || !p.cc) { set_error("bn_finalize: mode 1 operands"); return TALLY_EINVAL; }
   }
-  finish(inst, p, (p.C + 7) / 8, nn::BnFinalize::kThreads, 0, 8.0 * p.nrb * p.C + 16.0 * p.C);
+  finish(inst, p, (p.C + 31) / 32, nn::BnFinalize::kThreads, 2 * 8 * 32 * sizeof(float), 8.0 * p.nrb * p.C + 24.0 * p.C);
   return TALLY_OK;
 }
 
@@ -809,25 +925,22 @@ static int bind_bn_act(const tally_kernel_args* a, Instance* inst) {
   return TALLY_OK;
 }
 
-// ptr[0..7] = g, g2, y, x, mean, invstd, gamma, dx;  i: P, C, then the k1, k2 and
-// optional dz_out device addresses (the argument block has eight pointer slots)
+// ptr[0..7] = g, g2, y, x, ca, cb, cc, dx;  i: P, C, optional dz_out address
 static int bind_bn_bwd(const tally_kernel_args* a, Instance* inst) {
   nn::BnBwd::Params p{};
   p.g = static_cast<const uint4*>(a->ptr[0]);
   p.g2 = static_cast<const uint4*>(a->ptr[1]);
   p.y = static_cast<const uint4*>(a->ptr[2]);
   p.x = static_cast<const uint4*>(a->ptr[3]);
-  p.mean = static_cast<const float*>(a->ptr[4]);
-  p.invstd = static_cast<const float*>(a->ptr[5]);
-  p.gamma = static_cast<const float*>(a->ptr[6]);
+  p.ca = static_cast<const float*>(a->ptr[4]);
+  p.cb = static_cast<const float*>(a->ptr[5]);
+  p.cc = static_cast<const float*>(a->ptr[6]);
   p.dx = static_cast<uint4*>(a->ptr[7]);
   const long long P = a->i[0];
   p.C = (int)a->i[1];
-  p.k1 = reinterpret_cast<const float*>(a->i[2]);
-  p.k2 = reinterpret_cast<const float*>(a->i[3]);
-  p.dz_out = reinterpret_cast<uint4*>(a->i[4]);
-  if (!p.g || !p.x || !p.mean || !p.invstd || !p.gamma || !p.dx || !p.k1 || !p.k2 || P < 1 || p.C < 8 || p.C % 8) {
-    set_error("bn_bwd: need g, x, mean, invstd, gamma, dx, k1, k2 and C %% 8 == 0");
+  p.dz_out = reinterpret_cast<uint4*>(a->i[2]);
+  if (!p.g || !p.x || !p.ca || !p.cb || !p.cc || !p.dx || P < 1 || p.C < 8 || p.C % 8) {
+    set_error("bn_bwd: need g, x, ca, cb, cc, dx and C %% 8 == 0");
     return TALLY_EINVAL;
   }
   p.nvec = P * (p.C / 8);

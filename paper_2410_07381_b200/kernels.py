@@ -338,6 +338,21 @@ def gemm(A, B, C, splits: int = 1) -> DeviceKernel:
     return DeviceKernel(kind, (A, B, C), (M, N, K, 0, splits))
 
 
+def gemm_mn(At, Bt, C, splits: int = 1) -> DeviceKernel:
+    """C[M,N] (fp32) = At[K,M]^T . Bt[K,N] with both operands MN-major (as
+    stored: M / N contiguous) -- the weight gradient dW = dY^T . X of a
+    convolution straight from the NHWC activations.  Split-K as ``gemm``."""
+    import torch
+    K, M = At.shape
+    K2, N = Bt.shape
+    if K != K2:
+        raise ValueError("gemm_mn: At[K,M], Bt[K,N] need the same K")
+    if C.dtype != torch.float32 or tuple(C.shape[-2:]) != (M, N) or C.numel() != splits * M * N:
+        raise ValueError("gemm_mn: C must be fp32 [M,N] (or [splits,M,N])")
+    kind = "gemm_bf16f32_mn" + ("" if N % 128 == 0 else "_n64")
+    return DeviceKernel(kind, (At, Bt, C), (M, N, K, 0, splits))
+
+
 def im2col(x, col, n, h, w, c, kh, kw, stride, pad) -> DeviceKernel:
     return DeviceKernel("im2col_bf16", (x, col), (n, h, w, c, _pack_conv(kh, kw, stride, pad)))
 
@@ -361,18 +376,21 @@ def bn_finalize_fwd(part, nrb, C, count, gamma, beta, mean, invstd, scale, shift
                         (nrb, C, 0, count), (eps,))
 
 
-def bn_finalize_bwd(part, nrb, C, count, dgamma, dbeta, k1, k2) -> DeviceKernel:
-    return DeviceKernel("bn_finalize", (part, None, None, dgamma, dbeta, k1, k2), (nrb, C, 1, count))
+def bn_finalize_bwd(part, nrb, C, count, gamma, mean, invstd, dgamma, dbeta, ca, cb, cc) -> DeviceKernel:
+    """Backward statistics -> dgamma, dbeta and bn_bwd's per-channel
+    coefficients (dx = ca*dz + cb*x + cc)."""
+    return DeviceKernel("bn_finalize", (part, gamma, mean, invstd, dgamma, dbeta, ca, cb),
+                        (nrb, C, 1, count, _ptr(cc)), keep=(cc,))
 
 
 def bn_act(x, y, scale, shift, P, C, relu=True, res=None) -> DeviceKernel:
     return DeviceKernel("bn_act", (x, res, y, scale, shift), (P, C, int(relu)))
 
 
-def bn_bwd(g, x, mean, invstd, gamma, k1, k2, dx, P, C, g2=None, y=None, dz_out=None) -> DeviceKernel:
-    return DeviceKernel("bn_bwd", (g, g2, y, x, mean, invstd, gamma, dx),
-                        (P, C, _ptr(k1), _ptr(k2), _ptr(dz_out) or 0),
-                        keep=tuple(t for t in (k1, k2, dz_out) if t is not None))
+def bn_bwd(g, x, ca, cb, cc, dx, P, C, g2=None, y=None, dz_out=None) -> DeviceKernel:
+    """dz = (g [+ g2]) * (y > 0);  dx = ca*dz + cb*x + cc;  optional dz output."""
+    return DeviceKernel("bn_bwd", (g, g2, y, x, ca, cb, cc, dx), (P, C, _ptr(dz_out) or 0),
+                        keep=tuple(t for t in (dz_out,) if t is not None))
 
 
 def maxpool_fwd(x, y, arg, n, h, w, c) -> DeviceKernel:

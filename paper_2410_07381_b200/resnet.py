@@ -12,7 +12,8 @@ matrices); BN statistics and the optimizer run in fp32.
   conv (1 x 1, stride 1)   gemm directly on the activation
   batch-norm (training)    bn_stats -> bn_finalize -> bn_act (+ residual, ReLU)
   backward                 bn_stats(mode 1) -> bn_finalize -> bn_bwd;
-                           dgrad gemm (+ col2im); wgrad = transposes + split-K gemm
+                           dgrad gemm (+ col2im); wgrad = split-K gemm_mn reading
+                           dY and the forward operand MN-major (no transposes)
   head                     avgpool -> gemm (fp32 logits) -> softmax_xent
   optimizer                sgd_update (momentum 0.9, weight decay 1e-4) over all
                            parameters, one launch
@@ -43,9 +44,10 @@ WEIGHT_DECAY = 1e-4
 BN_EPS = 1e-5
 
 
-def _rb(C):
-    """Rows per bn_stats logical block (~16-32 KB of activations)."""
-    return 128 if C < 256 else 64
+def _rb(P, C):
+    """Rows per bn_stats logical block: at most 256 partial rows per channel
+    (bn_finalize stays a few microseconds), at least 32 rows per block."""
+    return max(32, (P + 255) // 256 + 7) // 8 * 8
 
 
 @dataclass
@@ -84,7 +86,7 @@ class ConvSpec:
 class SgdTable:
     """Packed ``nn::SgdSeg`` records + the logical-block map of sgd_update."""
 
-    CHUNK = 4096
+    CHUNK = 1024     # elements per sgd_update logical block
 
     def __init__(self):
         self.segs = []
@@ -103,6 +105,8 @@ class SgdTable:
         nbytes = 0
         for i, (w, v, g, S, gs, wd, wb, wt, rows, cols) in enumerate(self.segs):
             n = w.numel()
+            if n % 4 or gs % 4:
+                raise ValueError("sgd_update segments need sizes and gradient strides divisible by 4")
             rec[i] = (w.data_ptr(), v.data_ptr(), g.data_ptr(), n, gs, S, wd,
                       wb.data_ptr() if wb is not None else 0, wt.data_ptr() if wt is not None else 0,
                       rows, cols)
@@ -226,7 +230,7 @@ class ResNet50Train:
         b.vg, b.vb = torch.zeros_like(b.gamma), torch.zeros_like(b.beta)
         z = lambda: torch.zeros(C, device=dev)  # noqa: E731
         b.mean, b.invstd, b.scale, b.shift = z(), z(), z(), z()
-        b.dgamma, b.dbeta, b.k1, b.k2 = z(), z(), z(), z()
+        b.dgamma, b.dbeta, b.ca, b.cb, b.cc = z(), z(), z(), z(), z()
         self.params += [(name + ".weight", b.gamma), (name + ".bias", b.beta)]
         self.sgd.add(b.gamma, b.vg, b.dgamma, 1, C, WEIGHT_DECAY)
         self.sgd.add(b.beta, b.vb, b.dbeta, 1, C, WEIGHT_DECAY)
@@ -272,7 +276,7 @@ class ResNet50Train:
 
     def _bn_fwd(self, bn, y, P, relu, res=None):
         torch = self.torch
-        rb = _rb(bn.C)
+        rb = _rb(P, bn.C)
         nrb = (P + rb - 1) // rb
         part = self._scr("part", 2 * nrb * bn.C, torch.float32)
         out = self._buf(P, bn.C)
@@ -284,22 +288,25 @@ class ResNet50Train:
 
     def _bn_bwd(self, bn, g, x, P, g2=None, mask=None, dz_out=None):
         torch = self.torch
-        rb = _rb(bn.C)
+        rb = _rb(P, bn.C)
         nrb = (P + rb - 1) // rb
         part = self._scr("part", 2 * nrb * bn.C, torch.float32)
         dx = self._buf(P, bn.C)
         self._add(bn.name + ".bwd_stats", K.bn_stats(x, part, P, bn.C, rb, 1, g, g2, mask, bn.mean, bn.invstd))
-        self._add(bn.name + ".bwd_finalize", K.bn_finalize_bwd(part, nrb, bn.C, P, bn.dgamma, bn.dbeta,
-                                                               bn.k1, bn.k2))
-        self._add(bn.name + ".bwd", K.bn_bwd(g, x, bn.mean, bn.invstd, bn.gamma, bn.k1, bn.k2, dx, P, bn.C,
-                                             g2=g2, y=mask, dz_out=dz_out))
+        self._add(bn.name + ".bwd_finalize", K.bn_finalize_bwd(part, nrb, bn.C, P, bn.gamma, bn.mean, bn.invstd,
+                                                               bn.dgamma, bn.dbeta, bn.ca, bn.cb, bn.cc))
+        self._add(bn.name + ".bwd", K.bn_bwd(g, x, bn.ca, bn.cb, bn.cc, dx, P, bn.C, g2=g2, y=mask,
+                                             dz_out=dz_out))
         return dx
 
     @staticmethod
     def _splits(M, N, Kdim):
+        """Split-K factor of a weight-gradient GEMM: K ranges of ~4096 so a
+        logical block (one output tile over one K range) stays ~10 us -- a
+        preemption-friendly granularity -- and at least ~2 waves of blocks."""
         tiles = math.ceil(M / 128) * (N // (128 if N % 128 == 0 else 64))
         kb = math.ceil(Kdim / 64)
-        s = max(1, min(kb // 4, math.ceil(2 * 148 / tiles)))
+        s = max(1, min(kb // 2, max(math.ceil(kb / 64), math.ceil(2 * 148 / tiles))))
         return math.ceil(kb / math.ceil(kb / s))     # no empty split
 
     def _conv_bwd(self, conv, dy, A, need_dx=True):
@@ -309,14 +316,10 @@ class ResNet50Train:
         torch = self.torch
         s = conv.spec
         P = self.B * s.oh * s.ow
-        # weight gradient: dW[Cout, Kp] = dy^T . A
-        dyt = self._scr("dyt", s.cout * P).view(s.cout, P)
-        at = self._scr("at", s.kp * P).view(s.kp, P)
-        self._add(s.name + ".wgrad_tdy", K.transpose(dy, dyt))
-        self._add(s.name + ".wgrad_ta", K.transpose(A, at))
+        # weight gradient: dW[Cout, Kp] = dy^T . A, both read MN-major as stored
         S = self._splits(s.cout, s.kp, P)
         conv.gpart = torch.empty(S, s.cout, s.kp, dtype=torch.float32, device=self.device)
-        self._add(s.name + ".wgrad", K.gemm(dyt, at, conv.gpart, splits=S))
+        self._add(s.name + ".wgrad", K.gemm_mn(dy, A, conv.gpart, splits=S))
         self.sgd.add(conv.w, conv.v, conv.gpart, S, s.cout * s.kp, WEIGHT_DECAY, conv.wb, conv.wt,
                      s.cout, s.kp)
         if not need_dx:
@@ -338,20 +341,14 @@ class ResNet50Train:
     def _reserve_all(self):
         torch = self.torch
         convs = self._all_convs()
-        part = dyt = at = dcol = 0
+        part = dcol = 0
         for c in convs:
             s = c.spec
             P = self.B * s.oh * s.ow
-            part = max(part, 2 * ((P + _rb(s.cout) - 1) // _rb(s.cout)) * s.cout)
-            dyt = max(dyt, s.cout * P)
-            at = max(at, s.kp * P)
+            part = max(part, 2 * ((P + _rb(P, s.cout) - 1) // _rb(P, s.cout)) * s.cout)
             if not s.direct:
                 dcol = max(dcol, P * s.kp)
-        at = max(at, 2048 * self.B)
-        dyt = max(dyt, CLS_PAD * self.B)
         self._reserve("part", part, torch.float32)
-        self._reserve("dyt", dyt, torch.bfloat16)
-        self._reserve("at", at, torch.bfloat16)
         self._reserve("dcol", dcol, torch.bfloat16)
 
     # ---- the step ----------------------------------------------------------------
@@ -406,12 +403,8 @@ class ResNet50Train:
         # backward: head
         dfeat = self._buf(B, 2048)
         self._add("fc.dgrad", K.gemm(dl, self.fc_wt, dfeat))
-        dlt = self._scr("dyt", CLS_PAD * B).view(CLS_PAD, B)
-        ft = self._scr("at", 2048 * B).view(2048, B)
-        self._add("fc.wgrad_tdl", K.transpose(dl, dlt))
-        self._add("fc.wgrad_tfeat", K.transpose(feat, ft))
         self.fc_g = torch.empty(1, CLS_PAD, 2048, dtype=torch.float32, device=self.device)
-        self._add("fc.wgrad", K.gemm(dlt, ft, self.fc_g[0]))
+        self._add("fc.wgrad", K.gemm_mn(dl, feat, self.fc_g[0]))
         self.sgd.add(self.fc_w, self.fc_v, self.fc_g, 1, CLS_PAD * 2048, WEIGHT_DECAY, self.fc_wb, self.fc_wt,
                      CLS_PAD, 2048)
         self.sgd.add(self.fc_b, self.fc_bv, dl32, B, CLS_PAD, WEIGHT_DECAY)

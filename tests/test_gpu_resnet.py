@@ -88,6 +88,19 @@ def test_gemm_variants(env, M, N, K, out, splits):
     assert nerr(got, ref) < (1e-2 if out == torch.bfloat16 else 1e-4)
 
 
+@pytest.mark.parametrize("M,N,K,splits", [(64, 576, 2048, 8), (256, 128, 1000, 1), (200, 64, 136, 2),
+                                           (1024, 2048, 8, 1)])
+def test_gemm_mn_major(env, M, N, K, splits):
+    """Weight-gradient GEMM with both operands MN-major (At[K,M], Bt[K,N])."""
+    P, kernels, stream = env
+    At, Bt = rnd(K, M, seed=21), rnd(K, N, seed=22)
+    C = torch.zeros(*((splits, M, N) if splits > 1 else (M, N)), device="cuda")
+    (got,) = shapes(P, kernels.gemm_mn(At, Bt, C, splits=splits), stream, [C])
+    if splits > 1:
+        got = got.sum(0)
+    assert nerr(got, At.double().T @ Bt.double()) < 1e-4
+
+
 # ------------------------------------------------------------------ im2col / col2im
 def _unfold_nhwc(x_nhwc, k, stride, pad):
     """Reference im2col in the kernel's (kh, kw, c) column order."""
@@ -182,19 +195,19 @@ def test_bn_backward(env, P_, C, with_g2):
     rb = 128 if C < 256 else 64
     nrb = (P_ + rb - 1) // rb
     part = torch.zeros(2 * nrb * C, device="cuda")
-    mean, invstd, scale, shift, dgam, dbet, k1, k2 = (torch.zeros(C, device="cuda") for _ in range(8))
+    mean, invstd, scale, shift, dgam, dbet, ca, cb, cc = (torch.zeros(C, device="cuda") for _ in range(9))
     kernels.bn_stats(x, part, P_, C, rb).original(stream).wait()
     kernels.bn_finalize_fwd(part, nrb, C, P_, gamma, beta, mean, invstd, scale, shift).original(stream).wait()
     y = torch.zeros_like(x)
     kernels.bn_act(x, y, scale, shift, P_, C, True).original(stream).wait()
     (pt,) = shapes(P, kernels.bn_stats(x, part, P_, C, rb, 1, g, g2, y, mean, invstd), stream, [part])
     part.copy_(pt)
-    kernels.bn_finalize_bwd(part, nrb, C, P_, dgam, dbet, k1, k2).original(stream).wait()
+    shapes(P, kernels.bn_finalize_bwd(part, nrb, C, P_, gamma, mean, invstd, dgam, dbet, ca, cb, cc), stream, [])
+    kernels.bn_finalize_bwd(part, nrb, C, P_, gamma, mean, invstd, dgam, dbet, ca, cb, cc).original(stream).wait()
     assert nerr(dbet, bt.grad) < 1e-2 and nerr(dgam, gm.grad) < 1e-2
     dx = torch.zeros_like(x)
     dz = torch.zeros_like(x)
-    (gdx, gdz) = shapes(P, kernels.bn_bwd(g, x, mean, invstd, gamma, k1, k2, dx, P_, C, g2=g2, y=y, dz_out=dz),
-                        stream, [dx, dz])
+    (gdx, gdz) = shapes(P, kernels.bn_bwd(g, x, ca, cb, cc, dx, P_, C, g2=g2, y=y, dz_out=dz), stream, [dx, dz])
     assert nerr(gdx, xf.grad) < 1e-2
     assert nerr(gdz, up * (y.float() > 0)) < 1e-2
 

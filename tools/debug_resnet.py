@@ -75,5 +75,39 @@ def main():
         print(f"torch-bf16 vs fp32 {n:10s} err {nerr(refb[n], ref[n]):.3e}")
 
 
-if __name__ == "__main__":
+if __name__ == "__main__" and "--train" not in sys.argv:
     main()
+
+
+def train_trajectory(steps=12, lr=0.01, B=32, img=112):
+    """Loss over repeated SGD steps on one fixed batch: our program vs the
+    PyTorch fp32 model from the same initial weights (memorisation: both
+    should fall)."""
+    P.B200Device.get(0)
+    s = kernels.Stream(high_priority=False)
+    torch.manual_seed(0)
+    model = torchvision.models.resnet50(weights=None)
+    tr = resnet.ResNet50Train(batch=B, image=img, lr=lr, model=model)
+    g = torch.Generator(device="cuda").manual_seed(7)
+    images = torch.randn(B, 3, img, img, device="cuda", generator=g).bfloat16()
+    labels = torch.randint(0, 1000, (B,), device="cuda", generator=g)
+    tr.set_batch(images, labels)
+    ours = []
+    for _ in range(steps):
+        tr.step_original(s)
+        ours.append(round(tr.loss.mean().item(), 4))
+    m = model.cuda().float().train()
+    opt = torch.optim.SGD(m.parameters(), lr=lr, momentum=0.9, weight_decay=1e-4)
+    ref = []
+    for _ in range(steps):
+        opt.zero_grad()
+        loss = F.cross_entropy(m(images.float()), labels)
+        ref.append(round(loss.item(), 4))
+        loss.backward()
+        opt.step()
+    print("loss ours ", ours)
+    print("loss torch", ref)
+
+
+if __name__ == "__main__" and "--train" in sys.argv:
+    train_trajectory()
