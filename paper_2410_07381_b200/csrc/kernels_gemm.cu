@@ -170,6 +170,7 @@ struct CfgTf32x3T {
   static constexpr int UMMA_K = 8;
   static constexpr int TMEM_COLS = BN == 64 ? 256 : 512;   // 2 x BN accumulators + BN running total
   static constexpr bool MN = false;
+  static constexpr int EPI_BYTES = 0;   // fp32 rows are stored straight from registers
   using OutT = float;
 };
 // 128x128 tiles halve L2->SM operand bytes per flop (the kernel is L2-bound);
@@ -190,8 +191,11 @@ struct CfgBf16T {
   static constexpr int A_BYTES = BM * BK * ESZ;       // 16 KB
   static constexpr int B_BYTES = BN * BK * ESZ;       // 16 / 8 KB
   static constexpr int STAGE_BYTES = A_BYTES + B_BYTES;
-  // 128 KB / 120 KB of operand ring: room for co-resident high-priority CTAs
-  static constexpr int STAGES = BN == 128 ? 4 : 5;
+  // 64-96 KB of operand ring (+ bf16 staging): two CTAs per SM, so an
+  // untransformed launch (one output tile per CTA) overlaps one CTA's
+  // prologue / pipeline fill with the other's tile, and high-priority CTAs
+  // find room next to a best-effort one
+  static constexpr int STAGES = BN == 128 ? (sizeof(OutT_) == 2 ? 2 : 3) : (sizeof(OutT_) == 2 ? 3 : 4);
   static constexpr int UMMA_K = 16;
   // the whole (split) K range accumulates in one TMEM buffer (no fp32
   // promotion chunks at the 1e-2 bf16 budget): 2 x BN columns, leaving TMEM
@@ -202,6 +206,9 @@ struct CfgBf16T {
   // as stored, no transposes
   static constexpr bool MN = MN_;
   using OutT = OutT_;
+  // bf16 output: each epilogue warp stages its 32 x BN tile rows in shared
+  // memory (XOR-swizzled 16 B chunks) and writes whole rows, coalesced
+  static constexpr int EPI_BYTES = sizeof(OutT_) == 2 ? 4 * 32 * BN * 2 : 0;
 };
 using CfgBf16 = CfgBf16T<128, __nv_bfloat16>;
 using CfgBf16N64 = CfgBf16T<64, __nv_bfloat16>;
@@ -212,10 +219,14 @@ using CfgBf16MNN64 = CfgBf16T<64, float, true>;
 
 constexpr int GROUP_M = 8;
 constexpr int kThreads = 192;   // producer warp, MMA warp, 4 epilogue warps
+// claimed-tile ring depth: the producer runs up to kSlots tiles ahead of the
+// epilogue (short-K tiles are load-latency bound otherwise)
+constexpr int kSlots = 4;
 
 template <class Cfg>
 constexpr size_t smem_bytes() {
-  return 1024 /*alignment slack*/ + (size_t)Cfg::STAGES * Cfg::STAGE_BYTES + 256 /*barriers + ring*/;
+  return 1024 /*alignment slack*/ + (size_t)Cfg::STAGES * Cfg::STAGE_BYTES + Cfg::EPI_BYTES +
+         512 /*barriers + ring*/;
 }
 
 struct alignas(64) GemmParams {
@@ -263,16 +274,17 @@ template <class Cfg, int MODE, class ShapeArgs>
 __global__ void __launch_bounds__(kThreads, 1) k_gemm(const __grid_constant__ GemmParams p, const ShapeArgs s) {
   extern __shared__ __align__(1024) unsigned char smem_raw[];
   unsigned char* smem = reinterpret_cast<unsigned char*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
-  uint64_t* full = reinterpret_cast<uint64_t*>(smem + (size_t)Cfg::STAGES * Cfg::STAGE_BYTES);
+  unsigned char* epi_smem = smem + (size_t)Cfg::STAGES * Cfg::STAGE_BYTES;
+  uint64_t* full = reinterpret_cast<uint64_t*>(epi_smem + Cfg::EPI_BYTES);
   uint64_t* empty = full + Cfg::STAGES;
   uint64_t* tmem_full = empty + Cfg::STAGES;    // [2]
   uint64_t* tmem_empty = tmem_full + 2;         // [2]
-  uint64_t* tile_full = tmem_empty + 2;         // [2]
-  uint64_t* tile_empty = tile_full + 2;         // [2]
-  long long* tile_slot = reinterpret_cast<long long*>(tile_empty + 2);   // [2] claimed tile id
-  int* tile_c0 = reinterpret_cast<int*>(tile_slot + 2);                  // [2] first chunk (resumed tiles)
-  int* tile_cut = tile_c0 + 2;                                           // [2] chunk the tile stops before
-  uint32_t* tmem_base_slot = reinterpret_cast<uint32_t*>(tile_cut + 2);
+  uint64_t* tile_full = tmem_empty + 2;         // [kSlots]
+  uint64_t* tile_empty = tile_full + kSlots;    // [kSlots]
+  long long* tile_slot = reinterpret_cast<long long*>(tile_empty + kSlots);   // claimed tile id
+  int* tile_c0 = reinterpret_cast<int*>(tile_slot + kSlots);                  // first chunk (resumed tiles)
+  int* tile_cut = tile_c0 + kSlots;                                           // chunk the tile stops before
+  uint32_t* tmem_base_slot = reinterpret_cast<uint32_t*>(tile_cut + kSlots);
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int KB = (p.k + Cfg::BK - 1) / Cfg::BK;
@@ -284,6 +296,8 @@ __global__ void __launch_bounds__(kThreads, 1) k_gemm(const __grid_constant__ Ge
     for (int i = 0; i < 2; ++i) {
       mbar_init(&tmem_full[i], 1);
       mbar_init(&tmem_empty[i], 4);
+    }
+    for (int i = 0; i < kSlots; ++i) {
       mbar_init(&tile_full[i], 1);
       mbar_init(&tile_empty[i], 5);
     }
@@ -347,8 +361,8 @@ __global__ void __launch_bounds__(kThreads, 1) k_gemm(const __grid_constant__ Ge
             if (s.exec_count != nullptr) atomicAdd(&s.exec_count[t], 1ull);
           }
         }
-        const int j = i & 1;
-        if (i >= 2) mbar_wait(&tile_empty[j], ((i >> 1) - 1) & 1);
+        const int j = i % kSlots;
+        if (i >= kSlots) mbar_wait(&tile_empty[j], ((i / kSlots) - 1) & 1);
         tile_slot[j] = t;
         tile_c0[j] = c0;
         const TileWork w = tile_work(t < 0 ? 0 : t, p, KB);
@@ -416,8 +430,8 @@ __global__ void __launch_bounds__(kThreads, 1) k_gemm(const __grid_constant__ Ge
       constexpr uint32_t idesc = make_idesc<Cfg::KIND, Cfg::BN, Cfg::MN>();
       uint32_t it = 0, ci = 0;
       for (int i = 0;; ++i) {
-        const int j = i & 1;
-        mbar_wait(&tile_full[j], (i >> 1) & 1);
+        const int j = i % kSlots;
+        mbar_wait(&tile_full[j], (i / kSlots) & 1);
         const long long t = tile_slot[j];
         const int c0 = tile_c0[j];
         if (t < 0) {
@@ -479,8 +493,8 @@ __global__ void __launch_bounds__(kThreads, 1) k_gemm(const __grid_constant__ Ge
     const int q = warp & 3;   // TMEM lane quarter this warp may access
     uint32_t ci = 0;
     for (int i = 0;; ++i) {
-      const int j = i & 1;
-      mbar_wait(&tile_full[j], (i >> 1) & 1);
+      const int j = i % kSlots;
+      mbar_wait(&tile_full[j], (i / kSlots) & 1);
       const long long t = tile_slot[j];
       const int c0 = tile_c0[j];
       if (t < 0) {
@@ -562,7 +576,9 @@ __global__ void __launch_bounds__(kThreads, 1) k_gemm(const __grid_constant__ Ge
               dst[v] = make_float4(__uint_as_float(r[4 * v]), __uint_as_float(r[4 * v + 1]),
                                    __uint_as_float(r[4 * v + 2]), __uint_as_float(r[4 * v + 3]));
           } else {
-            uint4* dst = reinterpret_cast<uint4*>(crow + c1);
+            // stage this lane's row (16 B chunks, chunk index XOR row % 8:
+            // conflict-free) -- written out coalesced below
+            unsigned char* srow = epi_smem + (size_t)q * (32 * Cfg::BN * 2) + (size_t)lane * (Cfg::BN * 2);
 #pragma unroll
             for (int v = 0; v < 4; ++v) {
               uint32_t w[4];
@@ -572,13 +588,32 @@ __global__ void __launch_bounds__(kThreads, 1) k_gemm(const __grid_constant__ Ge
                                                          __uint_as_float(r[8 * v + 2 * e + 1]));
                 w[e] = *reinterpret_cast<uint32_t*>(&h);
               }
-              dst[v] = make_uint4(w[0], w[1], w[2], w[3]);
+              const int chunk = (c1 >> 3) + v;
+              *reinterpret_cast<uint4*>(srow + ((chunk ^ (lane & 7)) << 4)) = make_uint4(w[0], w[1], w[2], w[3]);
             }
           }
         }
         fence_before();
         __syncwarp();
         if (lane == 0) mbar_arrive(&tmem_empty[acc]);
+        if constexpr (sizeof(typename Cfg::OutT) == 2) {
+          if (last) {
+            // coalesced write-out of the warp's 32 staged rows: one warp
+            // instruction covers 512 contiguous bytes (2 rows of BN = 128)
+            constexpr int CPR = Cfg::BN / 8;   // 16 B chunks per row
+            const unsigned char* sbase = epi_smem + (size_t)q * (32 * Cfg::BN * 2);
+            const long long row0 = (long long)w.mb * Cfg::BM + q * 32;
+            __nv_bfloat16* cbase = reinterpret_cast<__nv_bfloat16*>(p.c) + (size_t)w.nb * Cfg::BN;
+#pragma unroll 4
+            for (int i2 = lane; i2 < 32 * CPR; i2 += 32) {
+              const int rr = i2 / CPR, ch = i2 % CPR;
+              const uint4 v = *reinterpret_cast<const uint4*>(sbase + (size_t)rr * (Cfg::BN * 2) + ((ch ^ (rr & 7)) << 4));
+              if (row0 + rr < p.m)
+                *reinterpret_cast<uint4*>(cbase + (size_t)(row0 + rr) * p.ldc + ch * 8) = v;
+            }
+            __syncwarp();
+          }
+        }
       }
       __syncwarp();
       if (lane == 0) mbar_arrive(&tile_empty[j]);

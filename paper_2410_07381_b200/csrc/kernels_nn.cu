@@ -70,6 +70,7 @@ __device__ __forceinline__ uint4 ld16(const uint4* p) {
 // worker counts.  Each thread keeps kIlp 16-byte loads in flight.
 constexpr int kIlp = 4;
 constexpr int kVecPerBlock = 256 * kIlp;
+constexpr int kCol2ImVec = 256;   // col2im gathers up to KH*KW vectors per output vector
 
 // ---------------------------------------------------------------- im2col
 struct Geometry {
@@ -81,6 +82,7 @@ struct Geometry {
 
 struct Im2Col {
   static constexpr int kThreads = 256;
+  static constexpr int kMinBlocks = 4;   // register cap: 4+ resident CTAs per SM
   struct Params {
     const uint4* x;
     uint4* col;
@@ -127,6 +129,7 @@ struct Im2Col {
 // ---------------------------------------------------------------- col2im (gather)
 struct Col2Im {
   static constexpr int kThreads = 256;
+  static constexpr int kMinBlocks = 4;   // register cap: 4+ resident CTAs per SM
   struct Params {
     const uint4* col;
     uint4* dx;
@@ -136,9 +139,8 @@ struct Col2Im {
   static __device__ __forceinline__ void run(const Params& p, uint3 bidx, uint3, char*) {
     const Geometry& g = p.g;
     const int cv = g.C >> 3, kv = g.Kp >> 3;
-    const long long v0 = (long long)bidx.x * kVecPerBlock;
-#pragma unroll 2
-    for (int i = threadIdx.x; i < kVecPerBlock; i += kThreads) {
+    const long long v0 = (long long)bidx.x * kCol2ImVec;
+    for (int i = threadIdx.x; i < kCol2ImVec; i += kThreads) {
       const long long v = v0 + i;
       if (v >= p.nvec) break;
       const int c8 = (int)(v % cv);
@@ -199,44 +201,92 @@ struct Transpose {
 };
 
 // ---------------------------------------------------------------- batch-norm statistics
+// One kernel computes the per-channel statistics AND finalises them: each
+// logical block (channel block cb, row block rb) writes its partial sums;
+// the last block of every group of kGroup row blocks folds the group
+// (fixed order) into a second-level partial; the last group of a channel
+// block folds those and writes the channel outputs.  Deterministic (every sum
+// has a fixed order), exactly-once under every launch shape (the counters
+// count logical blocks, and survive a PTB park / resume), and no separate
+// finalisation launch.
+template <int MODE>   // 0: forward statistics, 1: backward statistics
 struct BnStats {
   static constexpr int kThreads = 256;
+  static constexpr int kMinBlocks = MODE == 0 ? 4 : 2;   // register cap: enough bytes in flight per SM
+  static constexpr int kRows = MODE == 0 ? kIlp : 2;   // rows in flight per thread (1 or 4 streams each)
+  static constexpr int kGroup = 32;
   struct Params {
     const uint4* x;        // pre-BN activations [P, C]
     const uint4* g;        // mode 1: upstream gradient
     const uint4* g2;       // mode 1: optional second gradient term (residual)
     const uint4* y;        // mode 1: optional ReLU output (mask y > 0)
-    const float* mean;     // mode 1
-    const float* invstd;   // mode 1
-    float* part;           // [2][nrb][C]
+    float* mean;           // mode 0: output; mode 1: input
+    float* invstd;         // mode 0: output; mode 1: input
+    float* part;           // [2][nrb][C] level-1 partials
+    float* part2;          // [2][ngroups][C] level-2 partials
+    unsigned* cnt1;        // [cblocks][ngroups] finished row blocks per group
+    unsigned* cnt2;        // [cblocks] finished groups
+    const float* gamma;
+    const float* beta;     // mode 0
+    float* scale_shift;    // mode 0 output [2][C]: y = x*scale + shift
+    float* dgamma;         // mode 1 outputs
+    float* dbeta;
+    float* coef;           // mode 1 output [3][C]: dx = ca*dz + cb*x + cc
     long long P;
-    int C, RB, nrb, mode;
+    int C, RB, nrb, ngroups, mode;
+    float inv_count, eps;
   };
+
+  // sum rows [r0, r1) of a [2][rows][C] partial array for this block's
+  // channels into red (first 2*CB floats), using every thread
+  static __device__ __forceinline__ void fold(const float* src, long long rows_total, int r0, int r1, int C,
+                                              int c0, int CB, float* red, float* out_a, float* out_b) {
+    const int lanes_r = kThreads / CB;
+    const int lc = threadIdx.x % CB, lr = threadIdx.x / CB;
+    float a = 0.f, b = 0.f;
+    for (int r = r0 + lr; r < r1; r += lanes_r) {
+      a += __ldcg(src + (long long)r * C + c0 + lc);
+      b += __ldcg(src + (rows_total + r) * C + c0 + lc);
+    }
+    red[lr * CB + lc] = a;
+    red[kThreads + lr * CB + lc] = b;
+    __syncthreads();
+    if (threadIdx.x < CB) {
+      a = 0.f;
+      b = 0.f;
+      for (int k = 0; k < lanes_r; ++k) { a += red[k * CB + threadIdx.x]; b += red[kThreads + k * CB + threadIdx.x]; }
+      *out_a = a;
+      *out_b = b;
+    }
+    __syncthreads();
+  }
+
   static __device__ __forceinline__ void run(const Params& p, uint3 bidx, uint3, char* smem) {
     const int CB = min(p.C, 256);
     const int cv = CB >> 3, rl = kThreads / cv;
     const int lane_c = threadIdx.x % cv, lane_r = threadIdx.x / cv;
-    const int c = bidx.x * 256 + lane_c * 8;
+    const int c0 = bidx.x * 256;
+    const int c = c0 + lane_c * 8;
     const long long rbeg = (long long)bidx.y * p.RB;
     const long long rend = min(p.P, rbeg + p.RB);
     const int cvec = p.C >> 3;
     float s1[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f}, s2[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
     float mu[8], is[8];
-    if (p.mode == 1) {
+    if constexpr (MODE == 1) {
 #pragma unroll
       for (int e = 0; e < 8; ++e) { mu[e] = p.mean[c + e]; is[e] = p.invstd[c + e]; }
     }
-    for (long long r0 = rbeg + lane_r; r0 < rend; r0 += (long long)rl * kIlp) {
-      uint4 xv[kIlp], gv[kIlp], g2v[kIlp], yv[kIlp];
-      bool ok[kIlp];
+    for (long long r0 = rbeg + lane_r; r0 < rend; r0 += (long long)rl * kRows) {
+      uint4 xv[kRows], gv[kRows], g2v[kRows], yv[kRows];
+      bool ok[kRows];
 #pragma unroll
-      for (int u = 0; u < kIlp; ++u) {
+      for (int u = 0; u < kRows; ++u) {
         const long long r = r0 + (long long)u * rl;
         ok[u] = r < rend;
         const long long off = r * cvec + (c >> 3);
         if (ok[u]) {
           xv[u] = ld16(p.x + off);
-          if (p.mode == 1) {
+          if constexpr (MODE == 1) {
             gv[u] = ld16(p.g + off);
             if (p.g2) g2v[u] = ld16(p.g2 + off);
             if (p.y) yv[u] = ld16(p.y + off);
@@ -244,11 +294,11 @@ struct BnStats {
         }
       }
 #pragma unroll
-      for (int u = 0; u < kIlp; ++u) {
+      for (int u = 0; u < kRows; ++u) {
         if (!ok[u]) continue;
         float x[8];
         unpack8(xv[u], x);
-        if (p.mode == 0) {
+        if constexpr (MODE == 0) {
 #pragma unroll
           for (int e = 0; e < 8; ++e) { s1[e] += x[e]; s2[e] += x[e] * x[e]; }
         } else {
@@ -271,7 +321,8 @@ struct BnStats {
         }
       }
     }
-    float* red = reinterpret_cast<float*>(smem);   // [2][rl][CB]
+    float* red = reinterpret_cast<float*>(smem);   // [2][rl][CB] = 2 x 2048 floats
+    unsigned* flag = reinterpret_cast<unsigned*>(smem + 2 * 2048 * sizeof(float));
 #pragma unroll
     for (int e = 0; e < 8; ++e) {
       red[lane_r * CB + lane_c * 8 + e] = s1[e];
@@ -281,9 +332,60 @@ struct BnStats {
     if (threadIdx.x < CB) {
       float a = 0.f, b = 0.f;
       for (int k = 0; k < rl; ++k) { a += red[k * CB + threadIdx.x]; b += red[rl * CB + k * CB + threadIdx.x]; }
-      const int ch = bidx.x * 256 + threadIdx.x;
+      const int ch = c0 + threadIdx.x;
       p.part[(long long)bidx.y * p.C + ch] = a;
       p.part[((long long)p.nrb + bidx.y) * p.C + ch] = b;
+    }
+    // ---- level 1: the last row block of the group folds the group
+    __threadfence();
+    __syncthreads();
+    const int gi = bidx.y / kGroup;
+    if (threadIdx.x == 0) {
+      const unsigned in_group = (unsigned)min(kGroup, p.nrb - gi * kGroup);
+      flag[0] = atomicAdd(&p.cnt1[bidx.x * p.ngroups + gi], 1u) + 1u == in_group;
+    }
+    __syncthreads();
+    if (flag[0]) {
+      __threadfence();
+      float a = 0.f, b = 0.f;
+      fold(p.part, p.nrb, gi * kGroup, min(p.nrb, (gi + 1) * kGroup), p.C, c0, CB, red, &a, &b);
+      if (threadIdx.x < CB) {
+        p.part2[(long long)gi * p.C + c0 + threadIdx.x] = a;
+        p.part2[((long long)p.ngroups + gi) * p.C + c0 + threadIdx.x] = b;
+      }
+      if (threadIdx.x == 0) p.cnt1[bidx.x * p.ngroups + gi] = 0u;   // ready for the next launch
+      __threadfence();
+      __syncthreads();
+      if (threadIdx.x == 0) flag[1] = atomicAdd(&p.cnt2[bidx.x], 1u) + 1u == (unsigned)p.ngroups;
+      __syncthreads();
+      if (flag[1]) {
+        // ---- level 2: the last group finalises this channel block
+        __threadfence();
+        fold(p.part2, p.ngroups, 0, p.ngroups, p.C, c0, CB, red, &a, &b);
+        if (threadIdx.x < CB) {
+          const int ch = c0 + threadIdx.x;
+          if constexpr (MODE == 0) {
+            const float m = a * p.inv_count;
+            const float var = fmaxf(b * p.inv_count - m * m, 0.f);
+            const float isd = rsqrtf(var + p.eps);
+            p.mean[ch] = m;
+            p.invstd[ch] = isd;
+            const float sc = p.gamma[ch] * isd;
+            p.scale_shift[ch] = sc;
+            p.scale_shift[p.C + ch] = p.beta[ch] - m * sc;
+          } else {
+            p.dbeta[ch] = a;
+            p.dgamma[ch] = b;
+            const float isd = p.invstd[ch];
+            const float k1 = a * p.inv_count, k2 = b * p.inv_count;
+            const float al = p.gamma[ch] * isd;
+            p.coef[ch] = al;
+            p.coef[p.C + ch] = -al * k2 * isd;
+            p.coef[2 * p.C + ch] = al * (k2 * isd * p.mean[ch] - k1);
+          }
+        }
+        if (threadIdx.x == 0) p.cnt2[bidx.x] = 0u;
+      }
     }
     __syncthreads();
   }
@@ -366,6 +468,7 @@ struct BnFinalize {
 // ---------------------------------------------------------------- batch-norm apply
 struct BnAct {
   static constexpr int kThreads = 256;
+  static constexpr int kMinBlocks = 4;   // register cap: 4+ resident CTAs per SM
   struct Params {
     const uint4* x;
     const uint4* res;   // optional residual added before the activation
@@ -424,6 +527,9 @@ __device__ __forceinline__ void ld8f(const float* p, float (&f)[8]) {
 
 struct BnBwd {
   static constexpr int kThreads = 256;
+  static constexpr int kMinBlocks = 3;
+  static constexpr int kV = 2;                 // vectors per thread (4 input streams each)
+  static constexpr int kBlockVec = kThreads * kV;
   struct Params {
     const uint4* g;
     const uint4* g2;    // optional
@@ -439,10 +545,10 @@ struct BnBwd {
   };
   static __device__ __forceinline__ void run(const Params& p, uint3 bidx, uint3, char*) {
     const int cv = p.C >> 3;
-    const long long v0 = (long long)bidx.x * kVecPerBlock + threadIdx.x;
-    uint4 gv[kIlp], g2v[kIlp], yv[kIlp], xv[kIlp];
+    const long long v0 = (long long)bidx.x * kBlockVec + threadIdx.x;
+    uint4 gv[kV], g2v[kV], yv[kV], xv[kV];
 #pragma unroll
-    for (int u = 0; u < kIlp; ++u) {
+    for (int u = 0; u < kV; ++u) {
       const long long v = v0 + u * kThreads;
       if (v < p.nvec) {
         gv[u] = ld16(p.g + v);
@@ -452,7 +558,7 @@ struct BnBwd {
       }
     }
 #pragma unroll
-    for (int u = 0; u < kIlp; ++u) {
+    for (int u = 0; u < kV; ++u) {
       const long long v = v0 + u * kThreads;
       if (v >= p.nvec) continue;
       const int c = (int)(v % cv) << 3;
@@ -487,6 +593,7 @@ struct BnBwd {
 // ---------------------------------------------------------------- pooling
 struct MaxPoolFwd {   // 3x3, stride 2, pad 1
   static constexpr int kThreads = 256;
+  static constexpr int kMinBlocks = 4;   // register cap: 4+ resident CTAs per SM
   struct Params {
     const uint4* x;
     uint4* y;
@@ -533,6 +640,7 @@ struct MaxPoolFwd {   // 3x3, stride 2, pad 1
 
 struct MaxPoolBwd {
   static constexpr int kThreads = 256;
+  static constexpr int kMinBlocks = 4;   // register cap: 4+ resident CTAs per SM
   struct Params {
     const uint4* dy;
     const uint4* dy2;   // optional second gradient term
@@ -586,6 +694,7 @@ struct MaxPoolBwd {
 
 struct AvgPoolFwd {   // [N, HW, C] -> [N, C]
   static constexpr int kThreads = 256;
+  static constexpr int kMinBlocks = 4;   // register cap: 4+ resident CTAs per SM
   struct Params {
     const uint4* x;
     uint4* y;
@@ -679,6 +788,52 @@ struct SoftmaxXent {   // one row per logical block
     }
     if (threadIdx.x == 0) p.loss[b] = logf(s) + m - (z[lab] + p.bias[lab]);
     __syncthreads();
+  }
+};
+
+// ---------------------------------------------------------------- split-K reduction
+// out (bf16) = sum over S fp32 partials [S][n], fixed order: the epilogue of a
+// split-K activation GEMM (few output tiles, long K -> more, shorter logical
+// blocks for the scheduler)
+struct SplitKReduce {
+  static constexpr int kThreads = 256;
+  static constexpr int kMinBlocks = 3;
+  static constexpr int kVec = 2;   // output vectors (8 x bf16) per thread
+  struct Params {
+    const float4* in;    // [S][n / 4]
+    uint4* out;          // [n / 8]
+    long long n8;
+    long long stride4;   // n / 4
+    int S;
+  };
+  static __device__ __forceinline__ void run(const Params& p, uint3 bidx, uint3, char*) {
+    const long long v0 = (long long)bidx.x * (kThreads * kVec) + threadIdx.x;
+    float acc[kVec][8];
+#pragma unroll
+    for (int u = 0; u < kVec; ++u)
+#pragma unroll
+      for (int e = 0; e < 8; ++e) acc[u][e] = 0.f;
+    for (int sp = 0; sp < p.S; ++sp) {
+      float4 t[kVec][2];
+#pragma unroll
+      for (int u = 0; u < kVec; ++u) {
+        const long long v = v0 + u * kThreads;
+        if (v < p.n8) {
+          t[u][0] = __ldcs(p.in + sp * p.stride4 + 2 * v);
+          t[u][1] = __ldcs(p.in + sp * p.stride4 + 2 * v + 1);
+        }
+      }
+#pragma unroll
+      for (int u = 0; u < kVec; ++u) {
+        acc[u][0] += t[u][0].x; acc[u][1] += t[u][0].y; acc[u][2] += t[u][0].z; acc[u][3] += t[u][0].w;
+        acc[u][4] += t[u][1].x; acc[u][5] += t[u][1].y; acc[u][6] += t[u][1].z; acc[u][7] += t[u][1].w;
+      }
+    }
+#pragma unroll
+    for (int u = 0; u < kVec; ++u) {
+      const long long v = v0 + u * kThreads;
+      if (v < p.n8) p.out[v] = pack8(acc[u]);
+    }
   }
 };
 
@@ -817,7 +972,7 @@ static int bind_col2im(const tally_kernel_args* a, Instance* inst) {
   p.dx = static_cast<uint4*>(a->ptr[1]);
   if (!p.col || !p.dx || !aligned16(p.col) || !aligned16(p.dx)) { set_error("col2im: 16-byte aligned col, dx"); return TALLY_EINVAL; }
   p.nvec = (long long)p.g.N * p.g.H * p.g.W * (p.g.C / 8);
-  finish(inst, p, (p.nvec + nn::kVecPerBlock - 1) / nn::kVecPerBlock, nn::Col2Im::kThreads, 0,
+  finish(inst, p, (p.nvec + nn::kCol2ImVec - 1) / nn::kCol2ImVec, nn::Col2Im::kThreads, 0,
          2.0 * ((double)p.g.N * p.g.OH * p.g.OW * p.g.Kp + 8.0 * p.nvec));
   return TALLY_OK;
 }
@@ -839,31 +994,63 @@ static int bind_transpose(const tally_kernel_args* a, Instance* inst) {
   return TALLY_OK;
 }
 
-// ptr: x, g, g2, y, mean, invstd, part.  i: P, C, mode, RB
+// ptr: x, g, g2, y, mean, invstd, part, gamma.  i: P, C, mode, RB, then
+//   mode 0: beta, scale_shift ([2][C]) addresses
+//   mode 1: dgamma, dbeta, coef ([3][C]) addresses.   f: eps
+template <int MODE>
 static int bind_bn_stats(const tally_kernel_args* a, Instance* inst) {
-  nn::BnStats::Params p{};
+  using Body = nn::BnStats<MODE>;
+  typename Body::Params p{};
   p.x = static_cast<const uint4*>(a->ptr[0]);
   p.g = static_cast<const uint4*>(a->ptr[1]);
   p.g2 = static_cast<const uint4*>(a->ptr[2]);
   p.y = static_cast<const uint4*>(a->ptr[3]);
-  p.mean = static_cast<const float*>(a->ptr[4]);
-  p.invstd = static_cast<const float*>(a->ptr[5]);
+  p.mean = static_cast<float*>(a->ptr[4]);
+  p.invstd = static_cast<float*>(a->ptr[5]);
   p.part = static_cast<float*>(a->ptr[6]);
+  p.gamma = static_cast<const float*>(a->ptr[7]);
   p.P = a->i[0];
   p.C = (int)a->i[1];
   p.mode = (int)a->i[2];
   p.RB = (int)a->i[3];
+  p.eps = (float)a->f[0];
+  if (p.mode != MODE) { set_error("bn_stats: mode %d given to the mode-%d kind", p.mode, MODE); return TALLY_EINVAL; }
+  if (p.mode == 0) {
+    p.beta = reinterpret_cast<const float*>(a->i[4]);
+    p.scale_shift = reinterpret_cast<float*>(a->i[5]);
+  } else {
+    p.dgamma = reinterpret_cast<float*>(a->i[4]);
+    p.dbeta = reinterpret_cast<float*>(a->i[5]);
+    p.coef = reinterpret_cast<float*>(a->i[6]);
+  }
   const bool c_ok = p.C >= 64 && (p.C < 256 ? (256 % p.C == 0) : (p.C % 256 == 0));
-  if (!p.x || !p.part || p.P < 1 || !c_ok || p.RB < 1 ||
-      (p.mode == 1 && (!p.g || !p.mean || !p.invstd)) || (p.mode != 0 && p.mode != 1)) {
-    set_error("bn_stats: need x, part, C in {64, 128} or a multiple of 256, mode 0/1 operands");
+  const bool ops0 = p.mode == 0 && p.beta && p.scale_shift;
+  const bool ops1 = p.mode == 1 && p.g && p.dgamma && p.dbeta && p.coef;
+  if (!p.x || !p.part || !p.mean || !p.invstd || !p.gamma || p.P < 1 || !c_ok || p.RB < 1 || !(ops0 || ops1)) {
+    set_error("bn_stats: need x, part, mean, invstd, gamma, C in {64, 128} or a multiple of 256, and the "
+              "mode 0 (beta, scale_shift) / mode 1 (g, dgamma, dbeta, coef) operands");
     return TALLY_EINVAL;
   }
   p.nrb = (int)((p.P + p.RB - 1) / p.RB);
+  p.ngroups = (p.nrb + Body::kGroup - 1) / Body::kGroup;
+  p.inv_count = (float)(1.0 / (double)p.P);
+  const int cblocks = (p.C + 255) / 256;
+  // chain state: counters + level-2 partials (zeroed at bind and per new PTB chain)
+  const size_t cnt_bytes = ((size_t)cblocks * (p.ngroups + 1) * sizeof(unsigned) + 255) / 256 * 256;
+  const size_t bytes = cnt_bytes + (size_t)2 * p.ngroups * p.C * sizeof(float);
+  void* st = nullptr;
+  cudaError_t e = cudaMalloc(&st, bytes);
+  if (e == cudaSuccess) e = cudaMemset(st, 0, cnt_bytes);
+  if (e != cudaSuccess) return cuda_fail(e, "bn_stats state");
+  inst->resume_ring = st;
+  inst->resume_bytes = cnt_bytes;   // only the counters need zeroing
+  p.cnt1 = static_cast<unsigned*>(st);
+  p.cnt2 = p.cnt1 + (size_t)cblocks * p.ngroups;
+  p.part2 = reinterpret_cast<float*>(static_cast<char*>(st) + cnt_bytes);
   memcpy(inst->params, &p, sizeof(p));
-  inst->grid = make_uint3((unsigned)((p.C + 255) / 256), (unsigned)p.nrb, 1);
-  inst->threads = nn::BnStats::kThreads;
-  inst->smem = 2 * 256 * 8 * sizeof(float);   // [2][rl][CB] with rl * CB = 256 * 8
+  inst->grid = make_uint3((unsigned)cblocks, (unsigned)p.nrb, 1);
+  inst->threads = Body::kThreads;
+  inst->smem = 2 * 2048 * sizeof(float) + 16;
   const int streams = p.mode == 0 ? 1 : 2 + (p.g2 ? 1 : 0) + (p.y ? 1 : 0);
   inst->alg_bytes = 2.0 * streams * (double)p.P * p.C + 8.0 * p.nrb * p.C;
   return TALLY_OK;
@@ -945,7 +1132,8 @@ static int bind_bn_bwd(const tally_kernel_args* a, Instance* inst) {
   }
   p.nvec = P * (p.C / 8);
   const int streams = 3 + (p.g2 ? 1 : 0) + (p.y ? 1 : 0) + (p.dz_out ? 1 : 0);
-  finish(inst, p, (p.nvec + nn::kVecPerBlock - 1) / nn::kVecPerBlock, nn::BnBwd::kThreads, 0, 16.0 * p.nvec * streams);
+  finish(inst, p, (p.nvec + nn::BnBwd::kBlockVec - 1) / nn::BnBwd::kBlockVec, nn::BnBwd::kThreads, 0,
+         16.0 * p.nvec * streams);
   return TALLY_OK;
 }
 
@@ -1039,6 +1227,24 @@ static int bind_sgd(const tally_kernel_args* a, Instance* inst) {
   return TALLY_OK;
 }
 
+// ptr: in (fp32 [S][n]), out (bf16 [n]).  i: n, S
+static int bind_splitk_reduce(const tally_kernel_args* a, Instance* inst) {
+  nn::SplitKReduce::Params p{};
+  p.in = static_cast<const float4*>(a->ptr[0]);
+  p.out = static_cast<uint4*>(a->ptr[1]);
+  const long long n = a->i[0];
+  p.S = (int)a->i[1];
+  if (!p.in || !p.out || n < 8 || n % 8 || p.S < 1 || !aligned16(p.in) || !aligned16(p.out)) {
+    set_error("splitk_reduce: need 16-byte aligned in, out, n %% 8 == 0, S >= 1");
+    return TALLY_EINVAL;
+  }
+  p.n8 = n / 8;
+  p.stride4 = n / 4;
+  const long long per = nn::SplitKReduce::kThreads * nn::SplitKReduce::kVec;
+  finish(inst, p, (p.n8 + per - 1) / per, nn::SplitKReduce::kThreads, 0, (4.0 * p.S + 2.0) * (double)n);
+  return TALLY_OK;
+}
+
 template <class B>
 static KernelKind nn_kind(const char* name, int (*bind)(const tally_kernel_args*, Instance*)) {
   KernelKind k{};
@@ -1051,12 +1257,13 @@ static KernelKind nn_kind(const char* name, int (*bind)(const tally_kernel_args*
 }
 
 int register_nn_kernels(KernelKind* out, int cap) {
-  if (cap < 13) return 0;
+  if (cap < 15) return 0;
   int n = 0;
   out[n++] = nn_kind<nn::Im2Col>("im2col_bf16", bind_im2col);
   out[n++] = nn_kind<nn::Col2Im>("col2im_bf16", bind_col2im);
   out[n++] = nn_kind<nn::Transpose>("transpose_bf16", bind_transpose);
-  out[n++] = nn_kind<nn::BnStats>("bn_stats", bind_bn_stats);
+  out[n++] = nn_kind<nn::BnStats<0>>("bn_stats", bind_bn_stats<0>);
+  out[n++] = nn_kind<nn::BnStats<1>>("bn_stats_bwd", bind_bn_stats<1>);
   out[n++] = nn_kind<nn::BnFinalize>("bn_finalize", bind_bn_finalize);
   out[n++] = nn_kind<nn::BnAct>("bn_act", bind_bn_act);
   out[n++] = nn_kind<nn::BnBwd>("bn_bwd", bind_bn_bwd);
@@ -1066,6 +1273,7 @@ int register_nn_kernels(KernelKind* out, int cap) {
   out[n++] = nn_kind<nn::AvgPoolBwd>("avgpool_bwd", bind_avgpool_bwd);
   out[n++] = nn_kind<nn::SoftmaxXent>("softmax_xent", bind_softmax_xent);
   out[n++] = nn_kind<nn::SgdUpdate>("sgd_update", bind_sgd);
+  out[n++] = nn_kind<nn::SplitKReduce>("splitk_reduce", bind_splitk_reduce);
   return n;
 }
 

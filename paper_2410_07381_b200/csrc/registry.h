@@ -22,8 +22,18 @@ struct Instance {
   double alg_bytes = 0;        // algorithmic HBM bytes of the whole logical grid
   double alg_flops = 0;        // algorithmic flops of the whole logical grid
   int preempt_units = 1;       // PTB preemption points per logical block (K-chunks for sgemm_tf32x3)
-  void* resume_ring = nullptr; // chunk-preemption resume ring (reset when a PTB chain starts)
+  // Per-instance device state that lives across the launches of one PTB
+  // chain: the chunk-preemption resume ring (sgemm_tf32x3) or bn_stats'
+  // reduction counters + second-level partials.  Zeroed at bind and when a
+  // new PTB chain starts (start_count == 0); freed with the instance.
+  void* resume_ring = nullptr;
   size_t resume_bytes = 0;
+  Instance() = default;
+  Instance(const Instance&) = delete;
+  Instance& operator=(const Instance&) = delete;
+  ~Instance() {
+    if (resume_ring) cudaFree(resume_ring);
+  }
   unsigned long long total() const {
     return (unsigned long long)grid.x * grid.y * grid.z;
   }

@@ -140,9 +140,23 @@ __device__ __forceinline__ unsigned long long linear_index(uint3 b, uint3 g) {
   return (unsigned long long)b.x + (unsigned long long)g.x * (b.y + (unsigned long long)g.y * b.z);
 }
 
+// Optional per-body occupancy hint: a body may declare
+//   static constexpr int kMinBlocks = n;   // resident CTAs per SM to compile for
+// (register cap for HBM-streaming bodies); default 1.
+template <class...>
+using void_t_ = void;
+template <class B, class = void>
+struct MinBlocks {
+  static constexpr int value = 1;
+};
+template <class B>
+struct MinBlocks<B, void_t_<decltype(B::kMinBlocks)>> {
+  static constexpr int value = B::kMinBlocks;
+};
+
 // --- Original: the untransformed kernel --------------------------------------
 template <class Body>
-__global__ void __launch_bounds__(Body::kThreads)
+__global__ void __launch_bounds__(Body::kThreads, MinBlocks<Body>::value)
 k_original(const typename Body::Params p, const SliceArgs s) {
   extern __shared__ __align__(1024) char smem[];
   const uint3 g = make_uint3(gridDim.x, gridDim.y, gridDim.z);
@@ -153,7 +167,7 @@ k_original(const typename Body::Params p, const SliceArgs s) {
 
 // --- Sliced: block offset + pinned gridDim ------------------------------------
 template <class Body>
-__global__ void __launch_bounds__(Body::kThreads)
+__global__ void __launch_bounds__(Body::kThreads, MinBlocks<Body>::value)
 k_sliced(const typename Body::Params p, const SliceArgs s) {
   extern __shared__ __align__(1024) char smem[];
   const uint3 b = s.linear ? delinearize(s.linear_offset + blockIdx.x, s.grid)
@@ -261,7 +275,7 @@ __device__ __forceinline__ unsigned smid() {
 // preemption a worker retires after at most its current and its pre-claimed
 // logical block.
 template <class Body>
-__global__ void __launch_bounds__(Body::kThreads)
+__global__ void __launch_bounds__(Body::kThreads, MinBlocks<Body>::value)
 k_ptb(const typename Body::Params p, const PtbArgs a) {
   extern __shared__ __align__(1024) char smem[];
   __shared__ long long s_task[2];

@@ -366,8 +366,23 @@ def transpose(src, dst) -> DeviceKernel:
     return DeviceKernel("transpose_bf16", (src, dst), (R, Cc))
 
 
-def bn_stats(x, part, P, C, rb, mode=0, g=None, g2=None, y=None, mean=None, invstd=None) -> DeviceKernel:
-    return DeviceKernel("bn_stats", (x, g, g2, y, mean, invstd, part), (P, C, mode, rb))
+def bn_stats(x, part, P, C, rb, mean, invstd, gamma, beta=None, scale_shift=None, eps=1e-5) -> DeviceKernel:
+    """Forward BN statistics, finalised in the same kernel: mean, invstd and
+    scale_shift [2, C] (y = x*scale + shift)."""
+    return DeviceKernel("bn_stats", (x, None, None, None, mean, invstd, part, gamma),
+                        (P, C, 0, rb, _ptr(beta), _ptr(scale_shift)), (eps,), keep=(beta, scale_shift))
+
+
+def bn_stats_bwd(x, g, part, P, C, rb, mean, invstd, gamma, dgamma, dbeta, coef, g2=None, y=None) -> DeviceKernel:
+    """Backward BN statistics, finalised in the same kernel: dgamma, dbeta and
+    coef [3, C] with dx = coef[0]*dz + coef[1]*x + coef[2], dz = (g [+ g2]) * (y > 0)."""
+    return DeviceKernel("bn_stats_bwd", (x, g, g2, y, mean, invstd, part, gamma),
+                        (P, C, 1, rb, _ptr(dgamma), _ptr(dbeta), _ptr(coef)), keep=(dgamma, dbeta, coef))
+
+
+def splitk_reduce(parts, out) -> DeviceKernel:
+    """out (bf16) = parts.sum(0) for fp32 split-K partials [S, ...]."""
+    return DeviceKernel("splitk_reduce", (parts, out), (out.numel(), parts.shape[0]))
 
 
 def bn_finalize_fwd(part, nrb, C, count, gamma, beta, mean, invstd, scale, shift,

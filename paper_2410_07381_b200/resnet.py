@@ -45,9 +45,22 @@ BN_EPS = 1e-5
 
 
 def _rb(P, C):
-    """Rows per bn_stats logical block: at most 256 partial rows per channel
-    (bn_finalize stays a few microseconds), at least 32 rows per block."""
-    return max(32, (P + 255) // 256 + 7) // 8 * 8
+    """Rows per bn_stats logical block: ~128 KB of activations per block (the
+    per-block fixed cost -- partial write, fence, counter -- stays small) while
+    a block still streams in a few microseconds."""
+    return 1024 if C < 128 else (512 if C < 256 else 256)
+
+
+def _gemm_splits(M, N, Kdim):
+    """Split-K factor for a GEMM: enough logical blocks of <= ~40 MFLOP each
+    (~10 us on one SM) that the tuner finds a preemptible configuration under
+    the turnaround threshold, without empty splits."""
+    tiles = math.ceil(M / 128) * (N // (128 if N % 128 == 0 else 64))
+    kb = math.ceil(Kdim / 64)
+    flops = 2.0 * tiles * 128 * (128 if N % 128 == 0 else 64) * Kdim
+    want = max(tiles, math.ceil(flops / 40e6))
+    s = max(1, min(kb // 2, math.ceil(want / tiles)))
+    return math.ceil(kb / math.ceil(kb / s))
 
 
 @dataclass
@@ -229,8 +242,9 @@ class ResNet50Train:
         b.beta = sd[name + ".bias"].to(dev).clone()
         b.vg, b.vb = torch.zeros_like(b.gamma), torch.zeros_like(b.beta)
         z = lambda: torch.zeros(C, device=dev)  # noqa: E731
-        b.mean, b.invstd, b.scale, b.shift = z(), z(), z(), z()
-        b.dgamma, b.dbeta, b.ca, b.cb, b.cc = z(), z(), z(), z(), z()
+        b.mean, b.invstd, b.dgamma, b.dbeta = z(), z(), z(), z()
+        b.scale_shift = torch.zeros(2, C, device=dev)
+        b.coef = torch.zeros(3, C, device=dev)
         self.params += [(name + ".weight", b.gamma), (name + ".bias", b.beta)]
         self.sgd.add(b.gamma, b.vg, b.dgamma, 1, C, WEIGHT_DECAY)
         self.sgd.add(b.beta, b.vb, b.dbeta, 1, C, WEIGHT_DECAY)
@@ -271,8 +285,22 @@ class ResNet50Train:
             A = self._buf(P, s.kp)
             self._add(s.name + ".im2col", K.im2col(x, A, self.B, s.h, s.w, s.cin, s.k, s.k, s.stride, s.pad))
         y = self._buf(P, s.cout)
-        self._add(s.name + ".gemm", K.gemm(A, conv.wb, y))
+        self._gemm(s.name + ".gemm", A, conv.wb, y)
         return y, A
+
+    def _gemm(self, name, A, B, out):
+        """out[M,N] (bf16) = A . B^T, split-K through an fp32 workspace when the
+        GEMM has few, long output tiles (see _gemm_splits)."""
+        torch = self.torch
+        M, Kd = A.shape
+        N = B.shape[0]
+        S = _gemm_splits(M, N, Kd)
+        if S == 1:
+            self._add(name, K.gemm(A, B, out))
+            return
+        ws = self._scr("splitk", S * M * N, torch.float32).view(S, M, N)
+        self._add(name, K.gemm(A, B, ws, splits=S))
+        self._add(name + ".reduce", K.splitk_reduce(ws, out))
 
     def _bn_fwd(self, bn, y, P, relu, res=None):
         torch = self.torch
@@ -280,10 +308,9 @@ class ResNet50Train:
         nrb = (P + rb - 1) // rb
         part = self._scr("part", 2 * nrb * bn.C, torch.float32)
         out = self._buf(P, bn.C)
-        self._add(bn.name + ".stats", K.bn_stats(y, part, P, bn.C, rb))
-        self._add(bn.name + ".finalize", K.bn_finalize_fwd(part, nrb, bn.C, P, bn.gamma, bn.beta, bn.mean,
-                                                          bn.invstd, bn.scale, bn.shift, BN_EPS))
-        self._add(bn.name + ".act", K.bn_act(y, out, bn.scale, bn.shift, P, bn.C, relu, res))
+        self._add(bn.name + ".stats", K.bn_stats(y, part, P, bn.C, rb, bn.mean, bn.invstd, bn.gamma, bn.beta,
+                                                 bn.scale_shift, BN_EPS))
+        self._add(bn.name + ".act", K.bn_act(y, out, bn.scale_shift[0], bn.scale_shift[1], P, bn.C, relu, res))
         return out
 
     def _bn_bwd(self, bn, g, x, P, g2=None, mask=None, dz_out=None):
@@ -292,22 +319,11 @@ class ResNet50Train:
         nrb = (P + rb - 1) // rb
         part = self._scr("part", 2 * nrb * bn.C, torch.float32)
         dx = self._buf(P, bn.C)
-        self._add(bn.name + ".bwd_stats", K.bn_stats(x, part, P, bn.C, rb, 1, g, g2, mask, bn.mean, bn.invstd))
-        self._add(bn.name + ".bwd_finalize", K.bn_finalize_bwd(part, nrb, bn.C, P, bn.gamma, bn.mean, bn.invstd,
-                                                               bn.dgamma, bn.dbeta, bn.ca, bn.cb, bn.cc))
-        self._add(bn.name + ".bwd", K.bn_bwd(g, x, bn.ca, bn.cb, bn.cc, dx, P, bn.C, g2=g2, y=mask,
+        self._add(bn.name + ".bwd_stats", K.bn_stats_bwd(x, g, part, P, bn.C, rb, bn.mean, bn.invstd, bn.gamma,
+                                                         bn.dgamma, bn.dbeta, bn.coef, g2=g2, y=mask))
+        self._add(bn.name + ".bwd", K.bn_bwd(g, x, bn.coef[0], bn.coef[1], bn.coef[2], dx, P, bn.C, g2=g2, y=mask,
                                              dz_out=dz_out))
         return dx
-
-    @staticmethod
-    def _splits(M, N, Kdim):
-        """Split-K factor of a weight-gradient GEMM: K ranges of ~4096 so a
-        logical block (one output tile over one K range) stays ~10 us -- a
-        preemption-friendly granularity -- and at least ~2 waves of blocks."""
-        tiles = math.ceil(M / 128) * (N // (128 if N % 128 == 0 else 64))
-        kb = math.ceil(Kdim / 64)
-        s = max(1, min(kb // 2, max(math.ceil(kb / 64), math.ceil(2 * 148 / tiles))))
-        return math.ceil(kb / math.ceil(kb / s))     # no empty split
 
     def _conv_bwd(self, conv, dy, A, need_dx=True):
         """dy [P_out, Cout]; A = the forward GEMM operand [P_out, Kp].
@@ -317,7 +333,7 @@ class ResNet50Train:
         s = conv.spec
         P = self.B * s.oh * s.ow
         # weight gradient: dW[Cout, Kp] = dy^T . A, both read MN-major as stored
-        S = self._splits(s.cout, s.kp, P)
+        S = _gemm_splits(s.cout, s.kp, P)
         conv.gpart = torch.empty(S, s.cout, s.kp, dtype=torch.float32, device=self.device)
         self._add(s.name + ".wgrad", K.gemm_mn(dy, A, conv.gpart, splits=S))
         self.sgd.add(conv.w, conv.v, conv.gpart, S, s.cout * s.kp, WEIGHT_DECAY, conv.wb, conv.wt,
@@ -327,10 +343,10 @@ class ResNet50Train:
         # data gradient: dcol[P_out, Kp] = dy . W  (B operand = W^T [Kp, Cout])
         if s.direct:
             dx = self._buf(P, s.cin)
-            self._add(s.name + ".dgrad", K.gemm(dy, conv.wt, dx))
+            self._gemm(s.name + ".dgrad", dy, conv.wt, dx)
             return dx
         dcol = self._scr("dcol", P * s.kp).view(P, s.kp)
-        self._add(s.name + ".dgrad", K.gemm(dy, conv.wt, dcol))
+        self._gemm(s.name + ".dgrad", dy, conv.wt, dcol)
         dx = self._buf(self.B * s.h * s.w, s.cin)
         self._add(s.name + ".col2im", K.col2im(dcol, dx, self.B, s.h, s.w, s.cin, s.k, s.k, s.stride, s.pad))
         return dx
@@ -341,13 +357,18 @@ class ResNet50Train:
     def _reserve_all(self):
         torch = self.torch
         convs = self._all_convs()
-        part = dcol = 0
+        part = dcol = splitk = 0
         for c in convs:
             s = c.spec
             P = self.B * s.oh * s.ow
             part = max(part, 2 * ((P + _rb(P, s.cout) - 1) // _rb(P, s.cout)) * s.cout)
             if not s.direct:
                 dcol = max(dcol, P * s.kp)
+            for (M, N, Kd) in ((P, s.cout, s.kp), (P, s.kp, s.cout)):     # forward, dgrad
+                S = _gemm_splits(M, N, Kd)
+                if S > 1:
+                    splitk = max(splitk, S * M * N)
+        self._reserve("splitk", max(splitk, 8), torch.float32)
         self._reserve("part", part, torch.float32)
         self._reserve("dcol", dcol, torch.bfloat16)
 

@@ -146,27 +146,27 @@ def test_transpose(env):
 
 
 # ------------------------------------------------------------------ batch norm
-@pytest.mark.parametrize("P_,C,relu,res", [(1000, 64, True, False), (777, 256, True, True), (300, 512, False, False)])
-def test_bn_forward(env, P_, C, relu, res):
+@pytest.mark.parametrize("P_,C,relu,res,rb", [(1000, 64, True, False, 16), (777, 256, True, True, 8),
+                                              (300, 512, False, False, 8), (40000, 64, True, False, 32)])
+def test_bn_forward(env, P_, C, relu, res, rb):
+    """bn_stats (statistics + fused two-level finalisation) and bn_act."""
     P, kernels, stream = env
     x = (rnd(P_, C, seed=6).float() * 3 + 1).bfloat16()
     r = rnd(P_, C, seed=7) if res else None
     gamma = torch.rand(C, device="cuda") + 0.5
     beta = torch.randn(C, device="cuda")
-    rb = 128 if C < 256 else 64
     nrb = (P_ + rb - 1) // rb
     part = torch.zeros(2 * nrb * C, device="cuda")
-    mean, invstd, scale, shift = (torch.zeros(C, device="cuda") for _ in range(4))
-    (pt,) = shapes(P, kernels.bn_stats(x, part, P_, C, rb), stream, [part])
-    part.copy_(pt)
-    fin = kernels.bn_finalize_fwd(part, nrb, C, P_, gamma, beta, mean, invstd, scale, shift)
-    shapes(P, fin, stream, [])
-    fin.original(stream).wait()
+    mean, invstd = torch.zeros(C, device="cuda"), torch.zeros(C, device="cuda")
+    ss = torch.zeros(2, C, device="cuda")
+    gm, gi, gss = shapes(P, kernels.bn_stats(x, part, P_, C, rb, mean, invstd, gamma, beta, ss), stream,
+                         [mean, invstd, ss])
     xf = x.float()
-    assert nerr(mean, xf.mean(0)) < 1e-5
-    assert nerr(invstd, 1 / torch.sqrt(xf.var(0, unbiased=False) + 1e-5)) < 1e-4
+    assert nerr(gm, xf.mean(0)) < 1e-5
+    assert nerr(gi, 1 / torch.sqrt(xf.var(0, unbiased=False) + 1e-5)) < 1e-4
+    ss.copy_(gss)
     y = torch.zeros_like(x)
-    (got,) = shapes(P, kernels.bn_act(x, y, scale, shift, P_, C, relu, r), stream, [y])
+    (got,) = shapes(P, kernels.bn_act(x, y, ss[0], ss[1], P_, C, relu, r), stream, [y])
     ref = F.batch_norm(xf, None, None, gamma, beta, training=True, eps=1e-5)
     if res:
         ref = ref + r.float()
@@ -175,7 +175,7 @@ def test_bn_forward(env, P_, C, relu, res):
     assert nerr(got, ref) < 1e-2
 
 
-@pytest.mark.parametrize("P_,C,with_g2", [(1000, 64, True), (500, 256, False)])
+@pytest.mark.parametrize("P_,C,with_g2", [(1000, 64, True), (500, 256, False), (30000, 128, True)])
 def test_bn_backward(env, P_, C, with_g2):
     """dz = (g [+ g2]) * (y > 0); dx = BN-backward(dz) -- vs autograd."""
     P, kernels, stream = env
@@ -191,25 +191,33 @@ def test_bn_backward(env, P_, C, with_g2):
     yv = z.relu()
     up = g.float() + (g2.float() if with_g2 else 0)
     yv.backward(up)
-    # our forward statistics
-    rb = 128 if C < 256 else 64
+    rb = 64
     nrb = (P_ + rb - 1) // rb
     part = torch.zeros(2 * nrb * C, device="cuda")
-    mean, invstd, scale, shift, dgam, dbet, ca, cb, cc = (torch.zeros(C, device="cuda") for _ in range(9))
-    kernels.bn_stats(x, part, P_, C, rb).original(stream).wait()
-    kernels.bn_finalize_fwd(part, nrb, C, P_, gamma, beta, mean, invstd, scale, shift).original(stream).wait()
+    mean, invstd, dgam, dbet = (torch.zeros(C, device="cuda") for _ in range(4))
+    ss = torch.zeros(2, C, device="cuda")
+    coef = torch.zeros(3, C, device="cuda")
+    kernels.bn_stats(x, part, P_, C, rb, mean, invstd, gamma, beta, ss).original(stream).wait()
     y = torch.zeros_like(x)
-    kernels.bn_act(x, y, scale, shift, P_, C, True).original(stream).wait()
-    (pt,) = shapes(P, kernels.bn_stats(x, part, P_, C, rb, 1, g, g2, y, mean, invstd), stream, [part])
-    part.copy_(pt)
-    shapes(P, kernels.bn_finalize_bwd(part, nrb, C, P_, gamma, mean, invstd, dgam, dbet, ca, cb, cc), stream, [])
-    kernels.bn_finalize_bwd(part, nrb, C, P_, gamma, mean, invstd, dgam, dbet, ca, cb, cc).original(stream).wait()
-    assert nerr(dbet, bt.grad) < 1e-2 and nerr(dgam, gm.grad) < 1e-2
+    kernels.bn_act(x, y, ss[0], ss[1], P_, C, True).original(stream).wait()
+    gdg, gdb, gco = shapes(P, kernels.bn_stats_bwd(x, g, part, P_, C, rb, mean, invstd, gamma, dgam, dbet, coef,
+                                                   g2=g2, y=y), stream, [dgam, dbet, coef])
+    assert nerr(gdb, bt.grad) < 1e-2 and nerr(gdg, gm.grad) < 1e-2
+    coef.copy_(gco)
     dx = torch.zeros_like(x)
     dz = torch.zeros_like(x)
-    (gdx, gdz) = shapes(P, kernels.bn_bwd(g, x, ca, cb, cc, dx, P_, C, g2=g2, y=y, dz_out=dz), stream, [dx, dz])
+    (gdx, gdz) = shapes(P, kernels.bn_bwd(g, x, coef[0], coef[1], coef[2], dx, P_, C, g2=g2, y=y, dz_out=dz),
+                        stream, [dx, dz])
     assert nerr(gdx, xf.grad) < 1e-2
     assert nerr(gdz, up * (y.float() > 0)) < 1e-2
+
+
+def test_splitk_reduce(env):
+    P, kernels, stream = env
+    parts = torch.randn(5, 300, 64, device="cuda")
+    out = torch.zeros(300, 64, dtype=torch.bfloat16, device="cuda")
+    (got,) = shapes(P, kernels.splitk_reduce(parts, out), stream, [out])
+    assert torch.equal(got, parts.sum(0).bfloat16()) or nerr(got, parts.sum(0)) < 1e-2
 
 
 # ------------------------------------------------------------------ pooling, loss, optimizer
