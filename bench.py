@@ -77,7 +77,7 @@ def parse():
                     help="Tally with cooperative suspension of pausable BE kernels (B200 extension)")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
-    ap.add_argument("--cpu-sample-ms", type=float, default=1.0)
+    ap.add_argument("--cpu-sample-ms", type=float, default=None, help="default 1 (c1) / 4 (c2)")
     ap.add_argument("--profile-cache", default=None,
                     help="tuner cache JSON: loaded if present, else written after profiling")
     return ap.parse_args()
@@ -827,13 +827,14 @@ def main_c2(args):
     baselines = {}
     if not args.no_baselines:
         for pol in ("KernelPriority", "Eager"):
+            # the same K windows (arrival seeds) as the Tally measurement
             cfg = P.SchedulerConfig(policy=pol)
             lat, rate = [], []
-            for k in range(min(2, args.steps)):
+            for k in range(args.steps):
                 r = run_([hp_task(k), be_task], cfg, window)
                 lat += lat_after_warm(r)
                 rate.append(be_rate(r))
-            sl = [x for k in range(min(2, args.steps)) for x in lat_after_warm(run_([hp_task(k)], cfg, window))]
+            sl = [x for k in range(args.steps) for x in lat_after_warm(run_([hp_task(k)], cfg, window))]
             baselines[pol] = {"p99_overhead_pct": 100.0 * (p99(lat) / p99(sl) - 1.0),
                               "be_throughput_pct": 100.0 * (sum(rate) / len(rate)) / be_untransformed}
 
@@ -910,6 +911,8 @@ def main():
         args.window_ms = 100.0 if args.config == "c1" else 500.0
     if args.load is None:
         args.load = 0.5 if args.config == "c1" else 0.25
+    if args.cpu_sample_ms is None:
+        args.cpu_sample_ms = 1.0 if args.config == "c1" else 4.0
     if args.impl == "reference":
         (run_reference_arm if args.config == "c1" else run_reference_arm_c2)(args)
     else:

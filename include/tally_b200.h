@@ -82,6 +82,19 @@ int tally_set_flag_mode(int host_mapped);
  * reader observing it (mode 0 = device flag via cuStreamWriteValue32,
  * 1 = mapped host flag). */
 int tally_probe_flag_latency(int mode, int iters, long long* out_median_ns, long long* out_max_ns);
+/* Co-location cache policy (B200 extension; no reference counterpart): make
+ * [base, base + bytes) L2-persisting for kernels launched on (or captured
+ * from) the CUDA stream `cuda_stream` -- a high-priority request's weights
+ * stay L2-resident while best-effort kernels stream gigabytes through L2.
+ * Sets the device's persisting-L2 limit to min(bytes, device maximum).
+ * out_window_bytes: the window actually applied (clamped to the device max). */
+int tally_l2_persist(void* cuda_stream, const void* base, long long bytes, float hit_ratio,
+                     long long* out_window_bytes);
+/* The same window applied to every kernel node of a captured (not yet
+ * instantiated, or to be re-instantiated) cudaGraph_t.  out_nodes: kernel
+ * nodes updated. */
+int tally_graph_l2_persist(void* cuda_graph, const void* base, long long bytes, float hit_ratio,
+                           int* out_nodes);
 
 /* ==== kernel registration (ref scheduler.py:73-86 KernelWork; ir/core.py:153-214) */
 typedef struct {

@@ -70,6 +70,15 @@ __device__ __forceinline__ void tma_load_2d(void* dst, const CUtensorMap* map, u
       : "memory");
 }
 
+// Output tiles are written L2 evict-first (best-effort traffic must not push
+// a co-located high-priority request's working set out of L2; see kernels_nn.cu)
+__device__ __forceinline__ void st_out16(void* p, uint4 v) {
+  uint64_t pol;
+  asm("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(pol));
+  asm volatile("st.global.L2::cache_hint.v4.u32 [%0], {%1, %2, %3, %4}, %5;"
+               :: "l"(p), "r"(v.x), "r"(v.y), "r"(v.z), "r"(v.w), "l"(pol) : "memory");
+}
+
 __device__ __forceinline__ void fence_after() { asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory"); }
 __device__ __forceinline__ void fence_before() { asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory"); }
 
@@ -570,11 +579,9 @@ __global__ void __launch_bounds__(kThreads, 1) k_gemm(const __grid_constant__ Ge
             tmem_st32(lane_base + (uint32_t)(2 * Cfg::BN + c1), r);
           } else if (!row_ok) {
           } else if constexpr (sizeof(typename Cfg::OutT) == 4) {
-            float4* dst = reinterpret_cast<float4*>(crow + c1);
 #pragma unroll
             for (int v = 0; v < 8; ++v)
-              dst[v] = make_float4(__uint_as_float(r[4 * v]), __uint_as_float(r[4 * v + 1]),
-                                   __uint_as_float(r[4 * v + 2]), __uint_as_float(r[4 * v + 3]));
+              st_out16(crow + c1 + 4 * v, make_uint4(r[4 * v], r[4 * v + 1], r[4 * v + 2], r[4 * v + 3]));
           } else {
             // stage this lane's row (16 B chunks, chunk index XOR row % 8:
             // conflict-free) -- written out coalesced below
@@ -608,8 +615,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_gemm(const __grid_constant__ Ge
             for (int i2 = lane; i2 < 32 * CPR; i2 += 32) {
               const int rr = i2 / CPR, ch = i2 % CPR;
               const uint4 v = *reinterpret_cast<const uint4*>(sbase + (size_t)rr * (Cfg::BN * 2) + ((ch ^ (rr & 7)) << 4));
-              if (row0 + rr < p.m)
-                *reinterpret_cast<uint4*>(cbase + (size_t)(row0 + rr) * p.ldc + ch * 8) = v;
+              if (row0 + rr < p.m) st_out16(cbase + (size_t)(row0 + rr) * p.ldc + ch * 8, v);
             }
             __syncwarp();
           }

@@ -57,11 +57,26 @@ __device__ __forceinline__ uint4 pack8(const float (&f)[8]) {
   return v;
 }
 
+// Best-effort traffic is L2 evict-first: the training job streams gigabytes
+// per step, and evict-first lines are replaced before the evict-normal lines
+// of a co-located high-priority request (its weights and activations), which
+// otherwise come back cold after every best-effort burst.
+__device__ __forceinline__ uint64_t l2_evict_first() {
+  uint64_t pol;
+  asm("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(pol));
+  return pol;
+}
+
 __device__ __forceinline__ uint4 ld16(const uint4* p) {
   uint4 v;
-  asm volatile("ld.global.nc.L1::no_allocate.v4.u32 {%0, %1, %2, %3}, [%4];"
-               : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w) : "l"(p));
+  asm volatile("ld.global.nc.L1::no_allocate.L2::cache_hint.v4.u32 {%0, %1, %2, %3}, [%4], %5;"
+               : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w) : "l"(p), "l"(l2_evict_first()));
   return v;
+}
+
+__device__ __forceinline__ void st16(uint4* p, uint4 v) {
+  asm volatile("st.global.L1::no_allocate.L2::cache_hint.v4.u32 [%0], {%1, %2, %3, %4}, %5;"
+               :: "l"(p), "r"(v.x), "r"(v.y), "r"(v.z), "r"(v.w), "l"(l2_evict_first()) : "memory");
 }
 
 // Logical blocks are small (16 KB of bf16 for the elementwise kinds) so that a
@@ -121,7 +136,7 @@ struct Im2Col {
       }
 #pragma unroll
       for (int u = 0; u < kIlp; ++u)
-        if (dst[u] >= 0) p.col[dst[u]] = v[u];
+        if (dst[u] >= 0) st16(p.col + dst[u], v[u]);
     }
   }
 };
@@ -167,7 +182,7 @@ struct Col2Im {
           for (int e = 0; e < 8; ++e) acc[e] += f[e];
         }
       }
-      p.dx[v] = pack8(acc);
+      st16(p.dx + v, pack8(acc));
     }
   }
 };
@@ -515,7 +530,7 @@ struct BnAct {
 #pragma unroll
         for (int e = 0; e < 8; ++e) x[e] = fmaxf(x[e], 0.f);
       }
-      p.y[v] = pack8(x);
+      st16(p.y + v, pack8(x));
     }
   }
 };
@@ -576,7 +591,7 @@ struct BnBwd {
 #pragma unroll
         for (int e = 0; e < 8; ++e) dz[e] = t[e] > 0.f ? dz[e] : 0.f;
       }
-      if (p.dz_out) p.dz_out[v] = pack8(dz);
+      if (p.dz_out) st16(p.dz_out + v, pack8(dz));
       unpack8(xv[u], x);
       float a[8], b[8], k[8];
       ld8f(p.ca + c, a);
@@ -585,7 +600,7 @@ struct BnBwd {
       float o[8];
 #pragma unroll
       for (int e = 0; e < 8; ++e) o[e] = a[e] * dz[e] + (b[e] * x[e] + k[e]);
-      p.dx[v] = pack8(o);
+      st16(p.dx + v, pack8(o));
     }
   }
 };
@@ -629,7 +644,7 @@ struct MaxPoolFwd {   // 3x3, stride 2, pad 1
             if (f[e] > m[e]) { m[e] = f[e]; a[e] = (unsigned char)(kh * 3 + kw); }
         }
       }
-      p.y[v] = pack8(m);
+      st16(p.y + v, pack8(m));
       uint2 w;
       w.x = a[0] | (a[1] << 8) | (a[2] << 16) | ((unsigned)a[3] << 24);
       w.y = a[4] | (a[5] << 8) | (a[6] << 16) | ((unsigned)a[7] << 24);
@@ -687,7 +702,7 @@ struct MaxPoolBwd {
             if (a[e] == me) acc[e] += d[e];
         }
       }
-      p.dx[v] = pack8(acc);
+      st16(p.dx + v, pack8(acc));
     }
   }
 };
@@ -715,7 +730,7 @@ struct AvgPoolFwd {   // [N, HW, C] -> [N, C]
     const float s = 1.f / (float)p.HW;
 #pragma unroll
     for (int e = 0; e < 8; ++e) acc[e] *= s;
-    p.y[v] = pack8(acc);
+    st16(p.y + v, pack8(acc));
   }
 };
 
@@ -740,7 +755,7 @@ struct AvgPoolBwd {
       unpack8(p.dy[n * cv + c8], d);
 #pragma unroll
       for (int e = 0; e < 8; ++e) d[e] *= s;
-      p.dx[v] = pack8(d);
+      st16(p.dx + v, pack8(d));
     }
   }
 };
@@ -832,7 +847,7 @@ struct SplitKReduce {
 #pragma unroll
     for (int u = 0; u < kVec; ++u) {
       const long long v = v0 + u * kThreads;
-      if (v < p.n8) p.out[v] = pack8(acc[u]);
+      if (v < p.n8) st16(p.out + v, pack8(acc[u]));
     }
   }
 };

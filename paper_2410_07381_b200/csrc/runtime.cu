@@ -665,6 +665,66 @@ int tally_set_flag_mode(int host_mapped) {
 // reader observes it.  mode 0: device-resident flag written with
 // cuStreamWriteValue32 on the signal stream; mode 1: mapped host flag written
 // by a host store.
+int tally_l2_persist(void* cuda_stream, const void* base, long long bytes, float hit_ratio,
+                     long long* out_window_bytes) {
+  if (!base || bytes <= 0 || hit_ratio < 0.f || hit_ratio > 1.f) {
+    set_error("l2_persist: need base, bytes > 0, 0 <= hit_ratio <= 1");
+    return TALLY_EINVAL;
+  }
+  int dev = 0, max_win = 0, max_persist = 0;
+  CK(cudaGetDevice(&dev), "cudaGetDevice");
+  CK(cudaDeviceGetAttribute(&max_win, cudaDevAttrMaxAccessPolicyWindowSize, dev), "max window");
+  CK(cudaDeviceGetAttribute(&max_persist, cudaDevAttrMaxPersistingL2CacheSize, dev), "max persisting L2");
+  const size_t win = (size_t)std::min<long long>(bytes, max_win);
+  CK(cudaDeviceSetLimit(cudaLimitPersistingL2CacheSize, std::min<size_t>(win, (size_t)max_persist)),
+     "persisting L2 limit");
+  cudaStreamAttrValue v{};
+  v.accessPolicyWindow.base_ptr = const_cast<void*>(base);
+  v.accessPolicyWindow.num_bytes = win;
+  v.accessPolicyWindow.hitRatio = hit_ratio;
+  v.accessPolicyWindow.hitProp = cudaAccessPropertyPersisting;
+  v.accessPolicyWindow.missProp = cudaAccessPropertyStreaming;
+  CK(cudaStreamSetAttribute(static_cast<cudaStream_t>(cuda_stream), cudaStreamAttributeAccessPolicyWindow, &v),
+     "access policy window");
+  if (out_window_bytes) *out_window_bytes = (long long)win;
+  return TALLY_OK;
+}
+
+int tally_graph_l2_persist(void* cuda_graph, const void* base, long long bytes, float hit_ratio, int* out_nodes) {
+  if (!cuda_graph || !base || bytes <= 0 || hit_ratio < 0.f || hit_ratio > 1.f) {
+    set_error("graph_l2_persist: need graph, base, bytes > 0, 0 <= hit_ratio <= 1");
+    return TALLY_EINVAL;
+  }
+  int dev = 0, max_win = 0, max_persist = 0;
+  CK(cudaGetDevice(&dev), "cudaGetDevice");
+  CK(cudaDeviceGetAttribute(&max_win, cudaDevAttrMaxAccessPolicyWindowSize, dev), "max window");
+  CK(cudaDeviceGetAttribute(&max_persist, cudaDevAttrMaxPersistingL2CacheSize, dev), "max persisting L2");
+  const size_t win = (size_t)std::min<long long>(bytes, max_win);
+  CK(cudaDeviceSetLimit(cudaLimitPersistingL2CacheSize, std::min<size_t>(win, (size_t)max_persist)),
+     "persisting L2 limit");
+  cudaGraph_t g = static_cast<cudaGraph_t>(cuda_graph);
+  size_t n = 0;
+  CK(cudaGraphGetNodes(g, nullptr, &n), "graph nodes");
+  std::vector<cudaGraphNode_t> nodes(n);
+  CK(cudaGraphGetNodes(g, nodes.data(), &n), "graph nodes");
+  cudaKernelNodeAttrValue v{};
+  v.accessPolicyWindow.base_ptr = const_cast<void*>(base);
+  v.accessPolicyWindow.num_bytes = win;
+  v.accessPolicyWindow.hitRatio = hit_ratio;
+  v.accessPolicyWindow.hitProp = cudaAccessPropertyPersisting;
+  v.accessPolicyWindow.missProp = cudaAccessPropertyStreaming;
+  int k = 0;
+  for (auto nd : nodes) {
+    cudaGraphNodeType t;
+    CK(cudaGraphNodeGetType(nd, &t), "node type");
+    if (t != cudaGraphNodeTypeKernel) continue;
+    CK(cudaGraphKernelNodeSetAttribute(nd, cudaKernelNodeAttributeAccessPolicyWindow, &v), "node window");
+    ++k;
+  }
+  if (out_nodes) *out_nodes = k;
+  return TALLY_OK;
+}
+
 int tally_probe_flag_latency(int mode, int iters, long long* out_median_ns, long long* out_max_ns) {
   Runtime& r = rt();
   if (!r.inited) { set_error("tally_init first"); return TALLY_EINVAL; }
