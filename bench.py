@@ -1,27 +1,34 @@
 #!/usr/bin/env python
-"""Headline benchmark: Tally block-level scheduling on the B200 (config C1).
+"""Headline benchmark: Tally block-level scheduling on the B200.
 
     python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
-                    [--window-ms 100] [--load 0.5] [--threshold-us 31.6]
+                    [--config c2|c1] [--window-ms T] [--load L] [--threshold-us 31.6]
 
-Workload (BASELINE.json configs[0] -- the metric's configuration; configs[1..3]
-need the PyTorch BE routing that is not built yet):
-  HP  vector-add, N = 2^24 fp32 (4096 logical blocks), Poisson arrivals at
-      load 0.5 of its isolated latency, launched unmodified at top stream
-      priority;
-  BE  SGEMM 4096^2 fp32 training loop (split_tf32 x2 + sgemm_tf32x3 on
-      tcgen05), shaped by the profile-guided tuner (Original / Sliced / PTB).
+Default workload -- config C2, BASELINE.json configs[1] (the metric's
+single-GPU configuration; configs[0] is the reference's CPU-runnable case):
+  HP  ResNet-50 inference, batch 1, 3x224x224 (torchvision, random init, bf16,
+      channels-last, cuDNN) captured into one CUDA graph and launched
+      unmodified at top stream priority, on a bursty 2-state MMPP trace
+      (bursts 4x the calm rate, 10% of the time) at mean load 0.25 of its
+      isolated latency;
+  BE  ResNet-50 training, batch 64, bf16: forward, backward and momentum SGD
+      as a program of ~430 of this package's transformable sm_100a kernels
+      (resnet.ResNet50Train), each shaped by the profile-guided tuner
+      (Original / Sliced / PTB) under the 31.6 us turnaround threshold.
+  --config c1 runs the synthetic pair (HP vecadd_f32 2^24 at Poisson load 0.5
+  + BE SGEMM 4096^2 3xTF32) instead.
 
-A *step* is one co-location window (default 100 ms) of that traffic through
-the public API (``run_policy`` on the native runner, real time).  Calibration
-(solo HP over the same arrival traces, solo BE untransformed and same-policy)
-and W warm-up windows run before the timed region; the K timed windows are
-bracketed by a barrier + cuda synchronize, timed with CUDA events, max over
-ranks.  Inputs (201 MB HP, 256 MB BE operands) exceed the 126 MB L2.
+A *step* is one co-location window (default 1000 ms for C2, 100 ms for C1)
+of that traffic through the public API (``run_policy`` on the native runner,
+real time).  Calibration (solo HP over the same arrival traces, solo BE
+untransformed and under the same policy) and W warm-up windows run before the
+timed region; the K timed windows are bracketed by a barrier + cuda
+synchronize, timed with CUDA events, max over ranks.  BE activations (~10 GB
+per step) exceed the 126 MB L2.
 
 value  = p99 HP-latency overhead % = 100 * (p99_co / p99_solo - 1)   (lower is better)
 e2e    = the same metric with HP requests carrying their data over PCIe
-         (pipeline: H2D a, H2D b, vecadd, D2H c from/to pinned host memory)
+         (C2: H2D image + graph + D2H logits, pinned host memory)
 
 Multi-GPU (torchrun): one independent HP/BE pair per GPU, no collective on the
 data path; rank 0 reports the worst pair (max overhead, min BE fraction).
@@ -60,7 +67,7 @@ def parse():
     ap.add_argument("--config", default="c2", choices=["c1", "c2"],
                     help="c2 = BASELINE configs[1] (ResNet-50 HP bs=1 + ResNet-50 training bs=64); "
                          "c1 = the synthetic vecadd + SGEMM pair")
-    ap.add_argument("--window-ms", type=float, default=None, help="default 100 (c1) / 500 (c2)")
+    ap.add_argument("--window-ms", type=float, default=None, help="default 100 (c1) / 1000 (c2)")
     ap.add_argument("--load", type=float, default=None, help="mean HP load; default 0.5 (c1) / 0.25 (c2)")
     ap.add_argument("--burst", type=float, default=4.0, help="c2: MMPP burst-rate factor")
     ap.add_argument("--batch", type=int, default=64, help="c2: BE training batch")
@@ -299,7 +306,7 @@ def main_c1(args):
     for w in range(args.warmup):
         run_([hp_task(100 + w), be_task], tally, window, profiler=prof,
                      record_events=False)
-    off, _unc = dev.clock_offset()
+    clkmap = ClockMap(dev)
 
     # --- timed region: K co-located windows --------------------------------------
     clocks = Clocks(local)
@@ -327,20 +334,8 @@ def main_c1(args):
     co_lat = [x for r in results for x in lat_after_warm(r)]
     be_co = sum(be_rate(r) for r in results) / len(results)
     overhead = 100.0 * (p99(co_lat) / p99(solo_lat) - 1.0)
-    def preempt_latencies(res_list):
-        """Host signal -> last worker exit, for PTB launches already running
-        on the device when the flag was raised (queued launches that see the
-        flag at start are not preemptions)."""
-        out = []
-        for res in res_list:
-            for r in res.launches:
-                if r["preempt_ns"] < 0 or not r["parked"]:
-                    continue
-                sig = r["preempt_ns"] + res.origin_ns
-                if r["gt_first_start"] and r["gt_first_start"] + off < sig:
-                    out.append((r["gt_last_exit"] + off - sig) / 1e3)
-        return out
-    pl_us = preempt_latencies(results)
+    clkmap.close()
+    pl_us = preempt_latencies_us(results, clkmap)
     launches = sum(len(r.launches) for r in results)
     n_be = sum(1 for r in results for x in r.launches if x["priority"] == 1)
 
@@ -446,7 +441,7 @@ def main_c1(args):
                               "be_throughput_pct": 100.0 * (sum(rate) / len(rate)) / be_untransformed}
         # the same Tally policy with tile-granular (block-level, as in the
         # paper) PTB preemption of the SGEMM instead of chunk-granular
-        off, _unc = dev.clock_offset()      # re-anchor: globaltimer drifts vs CLOCK_MONOTONIC
+        clkmap_b = ClockMap(dev)      # re-anchor: globaltimer drifts vs CLOCK_MONOTONIC
         sg_blk = kernels.sgemm_tf32x3(A, B, C, chunk_preempt=False)
         blk_ws = be_ws[:2] + (P.KernelWork("sgemm_tf32x3_4096_tile_preempt", sg_blk.gemm.cost(),
                                            kernel=sg_blk.gemm),)
@@ -458,7 +453,8 @@ def main_c1(args):
             res_b.append(r)
             lat += lat_after_warm(r)
             rate.append(be_rate(r))
-        pb = preempt_latencies(res_b)
+        clkmap_b.close()
+        pb = preempt_latencies_us(res_b, clkmap_b)
         baselines["Tally_tile_granular_PTB"] = {
             "p99_overhead_pct": 100.0 * (p99(lat) / p99(solo_lat) - 1.0),
             "be_throughput_pct": 100.0 * (sum(rate) / len(rate)) / be_untransformed,
@@ -544,20 +540,24 @@ def c2_trace(load, hp_lat_ns, window_ns, seed, burst):
     return tuple(t for t in arr if t < window_ns)
 
 
-def cpu_c2_sample(costs, sample_ms, load, burst, seed):
+def cpu_c2_sample(costs, sample_ms, load, burst, seed, be_kernels=24, profiler=None):
     """Bounded C2 sample through the reference algorithm (oracle port of
     tallysim) on GpuSpec(148, 2048, 32): the HP request as one kernel of its
-    measured latency; the BE step as its kernel program, each kernel's cost
-    model from its measured B200 duration (blocks x per-block time)."""
+    measured latency, arriving every hp_latency / load; the BE task as the
+    first ``be_kernels`` kernels of the training step (stem + layer1 forward),
+    each kernel's cost model from its measured B200 duration (blocks x
+    per-block time).  The reference profiles every BE kernel's candidate
+    configurations by simulation first (ref profiler.py:176-248), which is
+    most of the CPU time.  ``burst`` is unused: a sample this short holds a
+    handful of requests, so they are spaced evenly at the mean load."""
     from oracle import gpu_model as gm
     from oracle import policy as pol
     from oracle import tuner as tu
-    from paper_2410_07381_b200 import workloads
     gpu = gm.GpuSpec(148, 2048, 32)
     hp_lat = int(costs["hp_latency_ns"])
     hp_cost = gm.KernelCostModel(max(1, hp_lat - 5_000), 5_000, gm.default_ptb_iteration_overhead_ns(hp_lat), 256, 1)
     works = []
-    for k in costs["be"]:
+    for k in costs["be"][:be_kernels]:
         tpb, total, ns = k["threads"], k["blocks"], k["ns"]
         slots = 148 * max(1, min(gpu.occupancy_limit(tpb), k.get("occupancy", 8)))
         waves = max(1, math.ceil(total / slots))
@@ -565,13 +565,13 @@ def cpu_c2_sample(costs, sample_ms, load, burst, seed):
         works.append(pol.KernelWork(k["sig"], gm.KernelCostModel(bd, 5_000, gm.default_ptb_iteration_overhead_ns(bd),
                                                                  tpb, total)))
     horizon = int(sample_ms * 1e6)
-    path = tempfile.mktemp(suffix=".csv")
-    workloads.bursty_trace(path, hp_lat / 1e6 / load, sample_ms, seed=seed, burst_factor=burst)
-    arr = tuple(t for t in workloads.load_trace(path) if t < horizon)
-    os.unlink(path)
+    gap = int(hp_lat / load)
+    arr = tuple(range(200_000 + seed * 1000, horizon, gap))
     hp = pol.TaskScript("hp", gm.HIGH, (pol.KernelWork("resnet50_infer", hp_cost),), arr)
     be = pol.TaskScript("be", gm.BEST_EFFORT, tuple(works))
-    prof = tu.Profiler(gpu, runs=1)
+    # one tuner per process, as the reference shares it across runs (its
+    # profiles are cached for the process lifetime, ref profiler.py:176-248)
+    prof = profiler if profiler is not None else tu.Profiler(gpu, runs=1)
     cfg = pol.SchedulerConfig()
     t0 = time.perf_counter()
     solo = pol.run_policy(gpu, [hp], cfg, horizon, profiler=prof, record_events=False)
@@ -588,13 +588,16 @@ def run_reference_arm_c2(args):
     rank = int(os.environ.get("RANK", "0"))
     if rank != 0:
         return
+    from oracle import gpu_model as gm
+    from oracle import tuner as tu
     costs = json.load(open(C2_COSTS))
+    prof = tu.Profiler(gm.GpuSpec(148, 2048, 32), runs=1)
     vals, walls, sim_ns, evs = [], [], 0, 0
-    for w in range(args.warmup):
-        cpu_c2_sample(costs, args.cpu_sample_ms, args.load, args.burst, 500 + w)
+    for w in range(args.warmup):     # the first sample also profiles the BE kernels (cached after)
+        cpu_c2_sample(costs, args.cpu_sample_ms, args.load, args.burst, 500 + w, profiler=prof)
     t0 = time.perf_counter()
     for k in range(args.steps):
-        v, wall, hz, ne = cpu_c2_sample(costs, args.cpu_sample_ms, args.load, args.burst, k)
+        v, wall, hz, ne = cpu_c2_sample(costs, args.cpu_sample_ms, args.load, args.burst, k, profiler=prof)
         walls.append(wall)
         sim_ns += hz
         evs += ne
@@ -602,9 +605,9 @@ def run_reference_arm_c2(args):
             vals.append(v)
     total = time.perf_counter() - t0
     value = sum(vals) / len(vals) if vals else None
-    sample = (f"{args.cpu_sample_ms} ms simulated C2 window per step (solo HP + co-located Tally; "
-              f"{len(costs['be'])}-kernel BE step with B200-measured costs from profiles/c2_costs.json) "
-              f"on GpuSpec(148,2048,32), oracle port of tallysim, 1 thread")
+    sample = (f"{args.cpu_sample_ms} ms simulated C2 window per step (solo HP + co-located Tally; HP every "
+              f"latency/load, BE = first 24 of the {len(costs['be'])} training-step kernels with B200-measured "
+              f"costs from profiles/c2_costs.json) on GpuSpec(148,2048,32), oracle port of tallysim, 1 thread")
     print(json.dumps({
         "impl": "reference", "metric": METRIC, "value": value, "unit": "%",
         "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
@@ -618,18 +621,44 @@ def run_reference_arm_c2(args):
     }))
 
 
-def preempt_latencies_us(res_list, off):
-    """Host signal -> last worker exit, for PTB launches already running on
-    the device when the flag was raised."""
+class ClockMap:
+    """Device %globaltimer -> host CLOCK_MONOTONIC, linear between two
+    calibrations bracketing the measured run: the two clocks drift apart by
+    tens of microseconds per second, more than the latencies measured."""
+
+    def __init__(self, dev):
+        self.dev = dev
+        self.a = (self.dev.now_ns(), self.dev.clock_offset()[0])
+        self.b = None
+
+    def close(self):
+        self.b = (self.dev.now_ns(), self.dev.clock_offset()[0])
+
+    def off(self, host_ns):
+        (t0, o0), (t1, o1) = self.a, self.b or self.a
+        if t1 == t0:
+            return o0
+        return o0 + (o1 - o0) * (host_ns - t0) / (t1 - t0)
+
+
+def preempt_latencies_us(res_list, clk):
+    """Host signal -> last worker exit (ref sim.py:509-517 measured_turnaround),
+    for PTB launches that parked (were running when the flag was raised);
+    device times mapped to the host clock by ``clk`` (a ClockMap)."""
     out = []
     for res in res_list:
         for r in res.launches:
-            if r["preempt_ns"] < 0 or not r["parked"]:
+            if r["preempt_ns"] < 0 or not r["parked"] or not r["gt_last_exit"]:
                 continue
             sig = r["preempt_ns"] + res.origin_ns
-            if r["gt_first_start"] and r["gt_first_start"] + off < sig:
-                out.append((r["gt_last_exit"] + off - sig) / 1e3)
+            out.append((r["gt_last_exit"] + clk.off(sig) - sig) / 1e3)
     return out
+
+
+def drain_us(res_list):
+    """First worker stop -> last worker exit (device clock only)."""
+    return [(r["gt_last_exit"] - r["gt_first_stop"]) / 1e3 for res in res_list for r in res.launches
+            if r["parked"] and r["gt_first_stop"] and r["gt_last_exit"]]
 
 
 def main_c2(args):
@@ -702,7 +731,7 @@ def main_c2(args):
     be_same_policy = be_rate(run_([be_task], tally, window))
     for w in range(args.warmup):
         run_([hp_task(100 + w), be_task], tally, window)
-    off, _unc = dev.clock_offset()
+    clkmap = ClockMap(dev)
 
     # --- timed region: K co-located windows ----------------------------------------
     clocks = Clocks(local)
@@ -727,7 +756,9 @@ def main_c2(args):
     co_lat = [x for r in results for x in lat_after_warm(r)]
     be_co = sum(be_rate(r) for r in results) / len(results)
     overhead = 100.0 * (p99(co_lat) / p99(solo_lat) - 1.0)
-    pl_us = preempt_latencies_us(results, off)
+    clkmap.close()
+    pl_us = preempt_latencies_us(results, clkmap)
+    dr_us = drain_us(results)
     launches = sum(len(r.launches) for r in results)
 
     # --- BE step composition and the dominant kernel's roofline --------------------
@@ -742,7 +773,18 @@ def main_c2(args):
     kind_ns = collections.Counter()
     for ns, _n, dk, _c in per:
         kind_ns[dk.kind] += ns
-    top_ns, top_name, top_dk, top_cand = max(per, key=lambda p: p[0])
+    # the dominant kernel: the largest launch of the kind with the largest share of the step
+    top_kind = kind_ns.most_common(1)[0][0]
+    top_ns, top_name, top_dk, top_cand = max((p for p in per if p[2].kind == top_kind), key=lambda p: p[0])
+    # native standalone step: the untransformed program back to back on one stream, no scheduler
+    for _ in range(2):
+        tr.step_original(s)
+    nat = []
+    for _ in range(3):
+        t0n = time.perf_counter()
+        tr.step_original(s)
+        nat.append(time.perf_counter() - t0n)
+    native_step_s = sorted(nat)[1]
 
     def timed(shape_fn, reps=5):
         ts = []
@@ -776,15 +818,12 @@ def main_c2(args):
         peaks = json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))
     except OSError:
         pass
-    is_gemm = top_dk.kind.startswith("gemm")
-    if is_gemm:
-        peak = peaks.get("bf16_tflops", 1644.3)
-        achieved = top_dk.info.alg_flops / chosen_ns / 1e3
-        unit, bound = "TFLOP/s", "tensor"
+    # roofline bound of this launch: whichever of tensor time and HBM time is larger
+    pk_t, pk_b = peaks.get("bf16_tflops", 1644.3), peaks.get("hbm_gbs", 6547.8)
+    if top_dk.info.alg_flops / (pk_t * 1e3) > top_dk.info.alg_bytes / pk_b:
+        peak, achieved, unit, bound = pk_t, top_dk.info.alg_flops / chosen_ns / 1e3, "TFLOP/s", "tensor"
     else:
-        peak = peaks.get("hbm_gbs", 6547.8)
-        achieved = top_dk.info.alg_bytes / chosen_ns
-        unit, bound = "GB/s", "hbm"
+        peak, achieved, unit, bound = pk_b, top_dk.info.alg_bytes / chosen_ns, "GB/s", "hbm"
     traffic = None
     try:
         traffic = json.load(open(os.path.join(ROOT, "profiles", "ncu_traffic.json"))).get(
@@ -792,6 +831,7 @@ def main_c2(args):
     except (OSError, ValueError):
         pass
     roofline = {"bound": bound, "kernel": f"{top_name} ({top_dk.kind}, {top_cand.describe()})",
+                "algorithmic_work_per_launch": {"bytes": top_dk.info.alg_bytes, "flops": top_dk.info.alg_flops},
                 "achieved": achieved, "peak": peak, "unit": unit, "frac": achieved / peak,
                 "traffic": traffic, "vs_untransformed": orig_ns / chosen_ns,
                 "untransformed_ns": orig_ns, "chosen_ns": chosen_ns,
@@ -852,11 +892,12 @@ def main_c2(args):
     with open(os.path.join(ROOT, "gpurun_out", "c2_costs.json"), "w") as fh:
         json.dump(costs, fh)
     cpu = None
-    if rank == 0 and not args.no_cpu_baseline:
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
         v, wall, hz, ne = cpu_c2_sample(costs, args.cpu_sample_ms, args.load, args.burst, 0)
         cpu = {"value": v, "unit": "%", "cores": 1, "kind": "port",
-               "sample": f"{args.cpu_sample_ms} ms simulated C2 window (solo + Tally co-run), oracle port of "
-                         f"tallysim on GpuSpec(148,2048,32) with the B200-measured kernel costs",
+               "sample": f"{args.cpu_sample_ms} ms simulated C2 window (solo + Tally co-run; HP every latency/load, "
+                         f"BE = first 24 training-step kernels), oracle port of tallysim on GpuSpec(148,2048,32) "
+                         f"with the B200-measured kernel costs",
                "wall_s": wall, "sim_ms_per_wall_s": hz / 1e6 / wall, "events_per_s": ne / wall}
 
     local_out = {
@@ -864,6 +905,7 @@ def main_c2(args):
         "be_frac_same_policy": 100.0 * be_co / be_same_policy,
         "p99_solo_us": p99(solo_lat) / 1e3, "p99_co_us": p99(co_lat) / 1e3,
         "preempt_us": [pct(pl_us, 0.5), pct(pl_us, 0.99), max(pl_us)] if pl_us else None,
+        "drain_us": [pct(dr_us, 0.5), pct(dr_us, 0.99)] if dr_us else None, "preemptions": len(pl_us),
     }
     gathered, worst = gather_pairs(local_out, dist)
     if rank != 0:
@@ -888,8 +930,12 @@ def main_c2(args):
             "be_throughput_pct": min(d["be_frac"] for d in gathered),
             "be_throughput_pct_vs_same_policy_solo": min(d["be_frac_same_policy"] for d in gathered),
             "be_steps_per_s": {"untransformed_solo": be_untransformed, "tally_solo": be_same_policy,
-                               "colocated": be_co},
+                               "colocated": be_co, "native_back_to_back": 1.0 / native_step_s},
+            "be_throughput_pct_vs_native": 100.0 * be_co * native_step_s,
             "preempt_latency_us_p50_p99_max": worst["preempt_us"],
+            "preempt_drain_us_p50_p99": worst["drain_us"], "preemptions": worst["preemptions"],
+            "preempt_note": "host signal -> last worker exit (device clock mapped to host, linear drift "
+                            "correction); drain = first worker stop -> last exit on the device clock",
             "hp_isolated_latency_us": hp_lat / 1e3,
             "hp_requests_timed": len(co_lat),
             "be_step_kernel_ms": step_kernel_ns / 1e6,
@@ -908,7 +954,7 @@ def main_c2(args):
 def main():
     args = parse()
     if args.window_ms is None:
-        args.window_ms = 100.0 if args.config == "c1" else 500.0
+        args.window_ms = 100.0 if args.config == "c1" else 1000.0
     if args.load is None:
         args.load = 0.5 if args.config == "c1" else 0.25
     if args.cpu_sample_ms is None:

@@ -62,12 +62,28 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
       : "memory");
 }
 
+#ifndef TALLY_GEMM_OPERAND_EVICT_FIRST
+#define TALLY_GEMM_OPERAND_EVICT_FIRST 1
+#endif
+// Operand tiles are loaded L2 evict-first too (see st_out16): tiles still
+// reuse L2 within a wave (evict-first lines are only replaced under pressure,
+// among themselves first) but do not displace a co-located request's lines.
 __device__ __forceinline__ void tma_load_2d(void* dst, const CUtensorMap* map, uint64_t* bar, int x, int y) {
+#if TALLY_GEMM_OPERAND_EVICT_FIRST
+  uint64_t pol;
+  asm("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(pol));
+  asm volatile(
+      "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint"
+      " [%0], [%1, {%3, %4}], [%2], %5;" ::"r"(smem_u32(dst)),
+      "l"(map), "r"(smem_u32(bar)), "r"(x), "r"(y), "l"(pol)
+      : "memory");
+#else
   asm volatile(
       "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%3, %4}], [%2];" ::"r"(
           smem_u32(dst)),
       "l"(map), "r"(smem_u32(bar)), "r"(x), "r"(y)
       : "memory");
+#endif
 }
 
 // Output tiles are written L2 evict-first (best-effort traffic must not push
@@ -227,7 +243,10 @@ using CfgBf16MN = CfgBf16T<128, float, true>;
 using CfgBf16MNN64 = CfgBf16T<64, float, true>;
 
 constexpr int GROUP_M = 8;
-constexpr int kThreads = 192;   // producer warp, MMA warp, 4 epilogue warps
+// producer warp, MMA warp, 8 epilogue warps: two per TMEM lane quarter, each
+// draining half of the tile's columns (the epilogue bounds short-K tiles)
+constexpr int kEpiWarps = 8;
+constexpr int kThreads = 64 + 32 * kEpiWarps;
 // claimed-tile ring depth: the producer runs up to kSlots tiles ahead of the
 // epilogue (short-K tiles are load-latency bound otherwise)
 constexpr int kSlots = 4;
@@ -249,6 +268,7 @@ struct alignas(64) GemmParams {
   long long split_stride;       // elements between split-K partial outputs
   int splits;                   // split-K factor: logical block = (split, tile)
   int kb_per_split;             // k-blocks per split
+  int claim_batch;              // PTB: tiles claimed per L2 atomic
 };
 
 __device__ __forceinline__ void tile_coords(long long t, const GemmParams& p, int& mb, int& nb) {
@@ -280,7 +300,7 @@ __device__ __forceinline__ TileWork tile_work(long long t, const GemmParams& p, 
 }
 
 template <class Cfg, int MODE, class ShapeArgs>
-__global__ void __launch_bounds__(kThreads, 1) k_gemm(const __grid_constant__ GemmParams p, const ShapeArgs s) {
+__global__ void __launch_bounds__(kThreads, Cfg::KIND == 1 ? 2 : 1) k_gemm(const __grid_constant__ GemmParams p, const ShapeArgs s) {
   extern __shared__ __align__(1024) unsigned char smem_raw[];
   unsigned char* smem = reinterpret_cast<unsigned char*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   unsigned char* epi_smem = smem + (size_t)Cfg::STAGES * Cfg::STAGE_BYTES;
@@ -304,11 +324,11 @@ __global__ void __launch_bounds__(kThreads, 1) k_gemm(const __grid_constant__ Ge
     for (int i = 0; i < Cfg::STAGES; ++i) { mbar_init(&full[i], 1); mbar_init(&empty[i], 1); }
     for (int i = 0; i < 2; ++i) {
       mbar_init(&tmem_full[i], 1);
-      mbar_init(&tmem_empty[i], 4);
+      mbar_init(&tmem_empty[i], kEpiWarps);
     }
     for (int i = 0; i < kSlots; ++i) {
       mbar_init(&tile_full[i], 1);
-      mbar_init(&tile_empty[i], 5);
+      mbar_init(&tile_empty[i], kEpiWarps + 1);
     }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
@@ -330,8 +350,16 @@ __global__ void __launch_bounds__(kThreads, 1) k_gemm(const __grid_constant__ Ge
   if (warp == 0) {
     if (lane == 0) {
       // ------------------------------------------------ TMA producer
+      // descriptor fetch off the critical path of the first tile
+      asm volatile("prefetch.tensormap [%0];" ::"l"(&p.a_hi) : "memory");
+      asm volatile("prefetch.tensormap [%0];" ::"l"(&p.b_hi) : "memory");
+      if constexpr (Cfg::KIND == 0) {
+        asm volatile("prefetch.tensormap [%0];" ::"l"(&p.a_lo) : "memory");
+        asm volatile("prefetch.tensormap [%0];" ::"l"(&p.b_lo) : "memory");
+      }
       uint32_t it = 0;
       unsigned flag_seen = 0;
+      long long q_next = 0, q_end = 0;   // PTB: tiles claimed in a batch, not yet started
       for (int i = 0;; ++i) {
         long long t = -1;
         int c0 = 0;
@@ -359,7 +387,18 @@ __global__ void __launch_bounds__(kThreads, 1) k_gemm(const __grid_constant__ Ge
             }
           }
           if (!popped) {
-            t = ptb_claim(s);
+            if (q_next < q_end) {
+              t = q_next++;   // claimed earlier in this batch: always executed
+            } else {
+              // short-K tiles are claim-latency bound: claim claim_batch tiles
+              // with one flag-gated L2 atomic (exactly-once is unchanged; a
+              // preempted worker finishes its batch, <= claim_batch tiles)
+              t = ptb_claim_n(s, p.claim_batch);
+              if (t >= 0) {
+                q_next = t + 1;
+                q_end = t + p.claim_batch;
+              }
+            }
             if (t < 0) stopped = true;
             else if ((unsigned long long)t >= s.total) t = -1;
           }
@@ -498,8 +537,10 @@ __global__ void __launch_bounds__(kThreads, 1) k_gemm(const __grid_constant__ Ge
     }
     __syncwarp();
   } else {
-    // -------------------------------------------------- epilogue (warps 2..5)
-    const int q = warp & 3;   // TMEM lane quarter this warp may access
+    // -------------------------------------------------- epilogue (warps 2..9)
+    const int q = warp & 3;                     // TMEM lane quarter this warp may access
+    const int half = (warp - 2) >> 2;           // which half of the tile's columns it drains
+    constexpr int HALF = Cfg::BN / 2;
     uint32_t ci = 0;
     for (int i = 0;; ++i) {
       const int j = i % kSlots;
@@ -525,7 +566,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_gemm(const __grid_constant__ Ge
           // preempted before chunk c: park the fp32 running total in C
           if (c > c0) {
 #pragma unroll 1
-            for (int c1 = 0; c1 < Cfg::BN; c1 += 32) {
+            for (int c1 = half * HALF; c1 < (half + 1) * HALF; c1 += 32) {
               uint32_t r[32];
               tmem_ld32(lane_base + (uint32_t)(2 * Cfg::BN + c1), r);
               float4* dst = reinterpret_cast<float4*>(crow + c1);
@@ -536,7 +577,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_gemm(const __grid_constant__ Ge
             }
           }
           __threadfence();
-          asm volatile("bar.sync 1, 128;" ::: "memory");   // all four epilogue warps saved
+          asm volatile("bar.sync 1, %0;" ::"n"(32 * kEpiWarps) : "memory");   // all epilogue warps saved
           if (warp == 2 && lane == 0) {
             unsigned long long* ring = p.resume;
             const unsigned long long slot = atomicAdd(ring, 1ull);
@@ -552,7 +593,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_gemm(const __grid_constant__ Ge
         }
         const bool last = (c == w.nch - 1);
 #pragma unroll 1
-        for (int c1 = 0; c1 < Cfg::BN; c1 += 32) {
+        for (int c1 = half * HALF; c1 < (half + 1) * HALF; c1 += 32) {
           // chunk partial + running fp32 total (kept in TMEM columns [2BN, 3BN))
           uint32_t r[32];
           tmem_ld32(lane_base + (uint32_t)(acc * Cfg::BN + c1), r);
@@ -605,19 +646,22 @@ __global__ void __launch_bounds__(kThreads, 1) k_gemm(const __grid_constant__ Ge
         if (lane == 0) mbar_arrive(&tmem_empty[acc]);
         if constexpr (sizeof(typename Cfg::OutT) == 2) {
           if (last) {
-            // coalesced write-out of the warp's 32 staged rows: one warp
-            // instruction covers 512 contiguous bytes (2 rows of BN = 128)
+            // the two warps of this lane quarter staged the two column halves
+            // of the same 32 rows; after a pair barrier each writes 16 whole
+            // rows out, coalesced (one warp instruction = 512 contiguous bytes
+            // for BN = 128)
+            asm volatile("bar.sync %0, 64;" ::"r"(2 + q) : "memory");
             constexpr int CPR = Cfg::BN / 8;   // 16 B chunks per row
             const unsigned char* sbase = epi_smem + (size_t)q * (32 * Cfg::BN * 2);
             const long long row0 = (long long)w.mb * Cfg::BM + q * 32;
             __nv_bfloat16* cbase = reinterpret_cast<__nv_bfloat16*>(p.c) + (size_t)w.nb * Cfg::BN;
 #pragma unroll 4
-            for (int i2 = lane; i2 < 32 * CPR; i2 += 32) {
+            for (int i2 = half * 16 * CPR + lane; i2 < (half + 1) * 16 * CPR; i2 += 32) {
               const int rr = i2 / CPR, ch = i2 % CPR;
               const uint4 v = *reinterpret_cast<const uint4*>(sbase + (size_t)rr * (Cfg::BN * 2) + ((ch ^ (rr & 7)) << 4));
               if (row0 + rr < p.m) st_out16(cbase + (size_t)(row0 + rr) * p.ldc + ch * 8, v);
             }
-            __syncwarp();
+            asm volatile("bar.sync %0, 64;" ::"r"(2 + q) : "memory");   // staging free for the next tile
           }
         }
       }
@@ -771,6 +815,9 @@ static int bind_gemm(const tally_kernel_args* a, Instance* inst, bool split) {
   // kernel (16 chunks of ~4.5 us per 4096-deep tile); bf16 (1e-2 budget)
   // accumulates the whole K in TMEM
   p.kchunk = Cfg::KIND == 0 ? 256 / Cfg::BK : p.kb_per_split;
+  // a logical block of <= 2 k-blocks is ~1 us: claim 4 at a time (<= 4 us of
+  // committed work on preemption); longer blocks one at a time
+  p.claim_batch = (Cfg::KIND == 1 && p.kb_per_split <= 2) ? 4 : 1;
   p.resume = nullptr;
   // i[3] = 1: block-granular preemption only (no resume ring)
   if (Cfg::KIND == 0 && a->i[3] == 0) {

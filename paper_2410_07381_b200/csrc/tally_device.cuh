@@ -263,6 +263,23 @@ __device__ __forceinline__ long long ptb_claim(const PtbArgs& a) {
   return task;
 }
 
+// Batched claim: n consecutive task indices with one flag-gated atomic.
+// Returns the first (tasks >= total are skipped by the caller) or -1.
+__device__ __forceinline__ long long ptb_claim_n(const PtbArgs& a, int n) {
+  if (n <= 1) return ptb_claim(a);
+  ptb_hold_while_paused(a);
+  const unsigned f = a.flag_is_host ? ld_acquire_sys(a.flag) : ld_acquire_gpu(a.flag);
+  if (f == a.serial) return -1;
+  const unsigned long long c = atomicAdd(&a.rec->claims, (unsigned long long)n);
+  const long long task = (long long)(a.start + c);
+  if (a.preempt_at >= 0 && task < a.preempt_at && a.preempt_at <= task + n)
+    st_release_sys(const_cast<unsigned*>(a.flag), a.serial);   // test trigger (MemTrigger)
+  if (a.exec_count != nullptr)
+    for (int k = 0; k < n; ++k)
+      if ((unsigned long long)(task + k) < a.total) atomicAdd(&a.exec_count[task + k], 1ull);
+  return task;
+}
+
 __device__ __forceinline__ unsigned smid() {
   unsigned r;
   asm volatile("mov.u32 %0, %%smid;" : "=r"(r));

@@ -69,6 +69,15 @@ def main():
         a[2] += dk.info.alg_bytes
         a[3] += dk.info.alg_flops
         per.append((ns / 1e3, name, dk.kind, dk.info.alg_bytes / max(ns, 1), dk.info.alg_flops / max(ns, 1) / 1e3))
+    # the same, every kernel in PTB shape at full resident occupancy
+    aggp = collections.defaultdict(lambda: [0, 0.0])
+    for name, dk in tr.program:
+        L = dk.ptb(s, min(dk.total_blocks, 148 * max(1, dk.info.occupancy_ptb)), timed=True)
+        L.wait()
+        aggp[dk.kind][0] += 1
+        aggp[dk.kind][1] += L.elapsed_ns / 1e3
+    out["ptb_by_kind_us"] = {k: round(v[1], 1) for k, v in sorted(aggp.items(), key=lambda x: -x[1][1])}
+    out["sum_of_kernel_us_ptb"] = sum(v[1] for v in aggp.values())
     tot = sum(a[1] for a in agg.values())
     out["sum_of_kernel_us"] = tot
     out["by_kind"] = {k: {"n": a[0], "us": round(a[1], 1), "share": round(a[1] / tot, 4),

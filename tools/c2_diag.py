@@ -98,6 +98,19 @@ def main():
                 run.append(L["gpu_end_ns"] - L["gpu_start_ns"])
                 nt.append(L["complete_ns"] - L["gpu_end_ns"])
             tot.append(c - a)
+        pre = []
+        for r in be_l:
+            if r["preempt_ns"] < 0:
+                continue
+            sig = r["preempt_ns"] + res.origin_ns
+            pre.append({"kernel": be_ws[r["kernel_index"]].kernel_id[:40] if 0 <= r["kernel_index"] < len(be_ws) else r["kernel_index"],
+                        "shape": r["shape"], "workers": r["workers"], "parked": r["parked"],
+                        "first_start_minus_sig_us": round((r["gt_first_start"] + off - sig) / 1e3, 1) if r["gt_first_start"] else None,
+                        "first_stop_minus_sig_us": round((r["gt_first_stop"] + off - sig) / 1e3, 1) if r["gt_first_stop"] else None,
+                        "last_exit_minus_sig_us": round((r["gt_last_exit"] + off - sig) / 1e3, 1) if r["gt_last_exit"] else None,
+                        "issue_minus_sig_us": round((r["issue_ns"] - r["preempt_ns"]) / 1e3, 1),
+                        "complete_minus_sig_us": round((r["complete_ns"] - r["preempt_ns"]) / 1e3, 1)})
+        out[label + "_preempts"] = pre[:40]
         out[label] = {"requests": len(reqs), "latency_p50_p90_p99_max_us": pcts(tot),
                       "queue": pcts(q), "issue": pcts(iss), "gpu_start": pcts(st), "gpu_run": pcts(run),
                       "notice": pcts(nt), "be_launches": len(be_l),

@@ -40,11 +40,21 @@ def main():
                  torch.randint(0, 1000, (64,), device="cuda", generator=g))
     big = next(dk for name, dk in tr.program if name == "layer1.0.bn3.bwd")
     flush = torch.empty(512 << 20, dtype=torch.uint8, device="cuda")
-    out = {}
-    for persist in (None, "stream", "nodes"):
+    out = {"l2_MB": torch.cuda.get_device_properties(0).L2_cache_size / 2 ** 20}
+    try:
+        from cuda.bindings import runtime as rt
+        err, v = rt.cudaDeviceGetAttribute(rt.cudaDeviceAttr.cudaDevAttrMaxPersistingL2CacheSize, 0)
+        out["max_persisting_l2_MB"] = v / 2 ** 20
+    except Exception as e:   # noqa: BLE001
+        out["max_persisting_l2_MB"] = repr(e)
+    spin = kernels.spin(148 * 8, 256, 100_000)   # 100 us of pure SM occupancy, no memory traffic
+    sweep = torch.empty(12 << 30, dtype=torch.uint8, device="cuda")   # 12 GB, touched once per 2 MB page
+    gemm = next(dk for name, dk in tr.program if name == "layer3.0.conv2.gemm")
+    for persist in (None, "nodes"):
         hp = resnet.ResNet50Infer(batch=1, image=224, persist_l2=persist)
         res = {"l2_window_MB": hp.l2_window_bytes / 2 ** 20}
-        for label in ("warm", "flush64", "l2flush", "be_kernel", "be_step"):
+        for label in ("warm", "flush64", "tlb_sweep", "be_kernel", "be_kernel_then_hp", "spin100us", "be_gemm",
+                      "be_step"):
             ts = []
             for i in range(12):
                 if label == "l2flush":
@@ -53,6 +63,21 @@ def main():
                     flush[:64 << 20].zero_()
                 elif label == "be_kernel":
                     big.original(be_s).wait()
+                elif label == "be_kernel_sleep2ms":
+                    big.original(be_s).wait()
+                    import time as _t
+                    t_end = _t.perf_counter() + 0.002
+                    while _t.perf_counter() < t_end:
+                        pass
+                elif label == "be_kernel_then_hp":
+                    big.original(be_s).wait()
+                    hp.kernel.original(hp_s).wait()
+                elif label == "tlb_sweep":
+                    sweep[:: 2 << 20].zero_()      # ~6000 pages, 6 KB of data
+                elif label == "spin100us":
+                    spin.original(be_s).wait()
+                elif label == "be_gemm":
+                    gemm.original(be_s).wait()
                 elif label == "be_step":
                     tr.step_original(be_s)
                 torch.cuda.synchronize()
