@@ -95,6 +95,12 @@ int tally_l2_persist(void* cuda_stream, const void* base, long long bytes, float
  * nodes updated. */
 int tally_graph_l2_persist(void* cuda_graph, const void* base, long long bytes, float hit_ratio,
                            int* out_nodes);
+/* Enqueue an L2 warm-up of [base, base + bytes) on `cuda_stream` (capturable
+ * into a CUDA graph): bulk L2 prefetches with the evict-last policy, a few
+ * microseconds for tens of MB.  A request graph forks it next to its first
+ * kernels so weights evicted by best-effort traffic come back ahead of the
+ * layers that read them. */
+int tally_l2_prefetch(void* cuda_stream, const void* base, long long bytes);
 
 /* ==== kernel registration (ref scheduler.py:73-86 KernelWork; ir/core.py:153-214) */
 typedef struct {

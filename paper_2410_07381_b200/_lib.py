@@ -147,6 +147,7 @@ _SIGNATURES = {
     "tally_set_flag_mode": (C.c_int, [C.c_int]),
     "tally_l2_persist": (C.c_int, [C.c_void_p, C.c_void_p, C.c_longlong, C.c_float, C.POINTER(C.c_longlong)]),
     "tally_graph_l2_persist": (C.c_int, [C.c_void_p, C.c_void_p, C.c_longlong, C.c_float, C.POINTER(C.c_int)]),
+    "tally_l2_prefetch": (C.c_int, [C.c_void_p, C.c_void_p, C.c_longlong]),
     "tally_probe_flag_latency": (C.c_int, [C.c_int, C.c_int, C.POINTER(C.c_longlong),
                                            C.POINTER(C.c_longlong)]),
     "tally_kernel_kind_count": (C.c_int, []),

@@ -8,6 +8,7 @@
 //               one logical block = elems_per_block contiguous floats
 //   rowsum_f32  out[r] = sum_c in[r, c], one warp per row, fixed reduction
 //               order (bit-identical across shapes)
+#include <algorithm>
 #include <cstdio>
 
 #include "registry.h"
@@ -192,6 +193,37 @@ static int bind_spin(const tally_kernel_args* a, Instance* inst) {
   inst->threads = (int)tpb;
   inst->smem = 0;
   return TALLY_OK;
+}
+
+// ---------------------------------------------------------------- L2 warm-up
+// Not a Tally kernel kind: launched directly on a caller's stream
+// (tally_l2_prefetch), typically inside a captured request graph.
+__global__ void __launch_bounds__(128) k_l2_prefetch(const char* base, long long bytes) {
+  constexpr long long kChunk = 32 << 10;
+  uint64_t pol;
+  asm("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(pol));
+  const long long nchunks = (bytes + kChunk - 1) / kChunk;
+  for (long long c = blockIdx.x * (long long)blockDim.x + threadIdx.x; c < nchunks;
+       c += (long long)gridDim.x * blockDim.x) {
+    const long long off = c * kChunk;
+    const unsigned sz = (unsigned)(min(kChunk, bytes - off) & ~15LL);
+    if (sz)
+      asm volatile("cp.async.bulk.prefetch.L2.global.L2::cache_hint [%0], %1, %2;" ::"l"(base + off), "r"(sz),
+                   "l"(pol)
+                   : "memory");
+  }
+}
+
+int launch_l2_prefetch(cudaStream_t s, const void* base, long long bytes) {
+  if (!base || bytes < 16 || (reinterpret_cast<uintptr_t>(base) & 15)) {
+    set_error("l2_prefetch: need a 16-byte aligned base and >= 16 bytes");
+    return TALLY_EINVAL;
+  }
+  const long long nchunks = (bytes + (32 << 10) - 1) / (32 << 10);
+  const int blocks = (int)std::min<long long>(16, (nchunks + 127) / 128);
+  k_l2_prefetch<<<blocks, 128, 0, s>>>(static_cast<const char*>(base), bytes);
+  const cudaError_t e = cudaGetLastError();
+  return e == cudaSuccess ? TALLY_OK : cuda_fail(e, "l2 prefetch launch");
 }
 
 template <class B>

@@ -725,6 +725,10 @@ int tally_graph_l2_persist(void* cuda_graph, const void* base, long long bytes, 
   return TALLY_OK;
 }
 
+int tally_l2_prefetch(void* cuda_stream, const void* base, long long bytes) {
+  return launch_l2_prefetch(static_cast<cudaStream_t>(cuda_stream), base, bytes);
+}
+
 int tally_probe_flag_latency(int mode, int iters, long long* out_median_ns, long long* out_max_ns) {
   Runtime& r = rt();
   if (!r.inited) { set_error("tally_init first"); return TALLY_EINVAL; }

@@ -496,7 +496,7 @@ class ResNet50Infer:
     request pipeline is this single exempt step (``kernel``) -- high-priority
     kernels are launched as the application wrote them (§4.1)."""
 
-    def __init__(self, batch=1, image=224, seed=1, device="cuda", persist_l2="nodes"):
+    def __init__(self, batch=1, image=224, seed=1, device="cuda", persist_l2="nodes", warm_l2=True):
         import ctypes as C
 
         import torch
@@ -539,8 +539,20 @@ class ResNet50Infer:
             torch.cuda.current_stream().wait_stream(side)
             torch.cuda.synchronize()
             self.graph = torch.cuda.CUDAGraph(keep_graph=True)
+            warm = torch.cuda.Stream() if warm_l2 else None
             with torch.cuda.graph(self.graph):
+                if warm is not None:
+                    # fork: an L2 warm-up of the weights runs next to the first
+                    # layers, so a request that follows best-effort traffic
+                    # finds the later layers' weights in L2 again
+                    warm.wait_stream(torch.cuda.current_stream())
+                    with torch.cuda.stream(warm):
+                        _lib.check(_lib.lib.tally_l2_prefetch(C.c_void_p(warm.cuda_stream),
+                                                              C.c_void_p(self.weights.data_ptr()),
+                                                              self.weights.numel() * 2), "l2 prefetch")
                 self.out = m(self.inp)
+                if warm is not None:
+                    torch.cuda.current_stream().wait_stream(warm)
         torch.cuda.synchronize()
         if persist_l2 == "nodes":
             # every kernel node of the request graph keeps the weights L2-persisting

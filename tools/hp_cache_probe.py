@@ -50,11 +50,10 @@ def main():
     spin = kernels.spin(148 * 8, 256, 100_000)   # 100 us of pure SM occupancy, no memory traffic
     sweep = torch.empty(12 << 30, dtype=torch.uint8, device="cuda")   # 12 GB, touched once per 2 MB page
     gemm = next(dk for name, dk in tr.program if name == "layer3.0.conv2.gemm")
-    for persist in (None, "nodes"):
-        hp = resnet.ResNet50Infer(batch=1, image=224, persist_l2=persist)
+    for persist, warm in ((None, False), ("nodes", False), (None, True), ("nodes", True)):
+        hp = resnet.ResNet50Infer(batch=1, image=224, persist_l2=persist, warm_l2=warm)
         res = {"l2_window_MB": hp.l2_window_bytes / 2 ** 20}
-        for label in ("warm", "flush64", "tlb_sweep", "be_kernel", "be_kernel_then_hp", "spin100us", "be_gemm",
-                      "be_step"):
+        for label in ("warm", "flush64", "be_kernel", "be_gemm", "be_step"):
             ts = []
             for i in range(12):
                 if label == "l2flush":
@@ -86,7 +85,7 @@ def main():
                 if i >= 2:
                     ts.append(L.elapsed_ns)
             res[label] = med(ts)
-        out[str(persist)] = res
+        out[f"persist={persist} warm={warm}"] = res
         del hp
         torch.cuda.synchronize()
     print(json.dumps(out, indent=1))
