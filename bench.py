@@ -723,9 +723,6 @@ def main_c2(args):
         return done / ((window - warm) / 1e9)
 
     # --- calibration (untimed) ---------------------------------------------------
-    solo_lat = []
-    for k in range(args.steps):
-        solo_lat += lat_after_warm(run_([hp_task(k)], tally, window))
     eager = P.SchedulerConfig(policy="Eager")
     be_untransformed = be_rate(run_([be_task], eager, window))
     be_same_policy = be_rate(run_([be_task], tally, window))
@@ -734,19 +731,29 @@ def main_c2(args):
     clkmap = ClockMap(dev)
 
     # --- timed region: K co-located windows ----------------------------------------
+    # Each step k is preceded by the solo-HP window of the same arrival trace
+    # (paired measurement: the HP graph's speed drifts by a few percent over a
+    # run, so solo and co-located p99 are taken side by side).  Every step is
+    # bracketed by a barrier + synchronize; ms_per_step is the sum of the K
+    # co-located windows' device time / K.
     clocks = Clocks(local)
-    if dist is not None:
-        dist.barrier()
-    torch.cuda.synchronize()
     clocks.start()
     ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    ev0.record()
-    t_host0 = time.perf_counter()
-    results = [run_([hp_task(k), be_task], tally, window) for k in range(args.steps)]
-    ev1.record()
-    torch.cuda.synchronize()
-    host_s = time.perf_counter() - t_host0
-    elapsed_ms = ev0.elapsed_time(ev1)
+    solo_lat, results = [], []
+    elapsed_ms = 0.0
+    host_s = 0.0
+    for k in range(args.steps):
+        solo_lat += lat_after_warm(run_([hp_task(k)], tally, window))
+        if dist is not None:
+            dist.barrier()
+        torch.cuda.synchronize()
+        ev0.record()
+        t_host0 = time.perf_counter()
+        results.append(run_([hp_task(k), be_task], tally, window))
+        ev1.record()
+        torch.cuda.synchronize()
+        host_s += time.perf_counter() - t_host0
+        elapsed_ms += ev0.elapsed_time(ev1)
     clk = clocks.stop()
     if dist is not None:
         t = torch.tensor([elapsed_ms], device="cuda")
@@ -870,11 +877,12 @@ def main_c2(args):
             # the same K windows (arrival seeds) as the Tally measurement
             cfg = P.SchedulerConfig(policy=pol)
             lat, rate = [], []
-            for k in range(args.steps):
+            sl = []
+            for k in range(args.steps):     # paired, as the Tally measurement
+                sl += lat_after_warm(run_([hp_task(k)], cfg, window))
                 r = run_([hp_task(k), be_task], cfg, window)
                 lat += lat_after_warm(r)
                 rate.append(be_rate(r))
-            sl = [x for k in range(args.steps) for x in lat_after_warm(run_([hp_task(k)], cfg, window))]
             baselines[pol] = {"p99_overhead_pct": 100.0 * (p99(lat) / p99(sl) - 1.0),
                               "be_throughput_pct": 100.0 * (sum(rate) / len(rate)) / be_untransformed}
 
