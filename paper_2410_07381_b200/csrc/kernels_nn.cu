@@ -864,6 +864,7 @@ struct SgdSeg {
   __nv_bfloat16* wb;      // optional bf16 copy, same layout
   __nv_bfloat16* wt;      // optional bf16 transposed copy [cols, rows]
   int rows, cols;
+  int chunk;              // elements per logical block (64..1024, power of 2)
 };
 
 struct SgdUpdate {
@@ -878,8 +879,9 @@ struct SgdUpdate {
   static __device__ __forceinline__ void run(const Params& p, uint3 bidx, uint3, char*) {
     const int2 m = p.map[bidx.x];
     const SgdSeg& s = p.segs[m.x];
-    const long long i = (long long)m.y * kChunk + threadIdx.x * 4;
-    if (i >= s.n) return;   // no barrier in this body; segment sizes are multiples of 4
+    if (threadIdx.x * 4 >= s.chunk) return;   // no barrier in this body
+    const long long i = (long long)m.y * s.chunk + threadIdx.x * 4;
+    if (i >= s.n) return;   // segment sizes are multiples of 4
     // split-K / per-row gradient partials, summed in a fixed order
     float4 g = make_float4(0.f, 0.f, 0.f, 0.f);
     int j = 0;

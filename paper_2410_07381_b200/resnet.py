@@ -49,17 +49,18 @@ def _rb(P, C, streams=1):
     per-block fixed cost -- partial write, fence, counter -- stays small) while
     a block still streams in a few microseconds; backward statistics read up
     to four streams."""
-    return (1024 if C < 128 else (512 if C < 256 else 256)) // streams
+    return (512 if C < 128 else (256 if C < 256 else 128)) // streams
 
 
 def _gemm_splits(M, N, Kdim):
-    """Split-K factor for a GEMM: enough logical blocks of <= ~40 MFLOP each
-    (~10 us on one SM) that the tuner finds a preemptible configuration under
-    the turnaround threshold, without empty splits."""
+    """Split-K factor for a GEMM: enough logical blocks of <= ~20 MFLOP each
+    (~10 us on one SM, the preemption granularity) that the tuner finds a
+    preemptible configuration under the turnaround threshold, without empty
+    splits."""
     tiles = math.ceil(M / 128) * (N // (128 if N % 128 == 0 else 64))
     kb = math.ceil(Kdim / 64)
     flops = 2.0 * tiles * 128 * (128 if N % 128 == 0 else 64) * Kdim
-    want = max(tiles, math.ceil(flops / 40e6))
+    want = max(tiles, math.ceil(flops / 20e6))
     s = max(1, min(kb // 2, math.ceil(want / tiles)))
     return math.ceil(kb / math.ceil(kb / s))
 
@@ -100,7 +101,7 @@ class ConvSpec:
 class SgdTable:
     """Packed ``nn::SgdSeg`` records + the logical-block map of sgd_update."""
 
-    CHUNK = 1024     # elements per sgd_update logical block
+    CHUNK = 1024     # max elements per sgd_update logical block
 
     def __init__(self):
         self.segs = []
@@ -111,9 +112,9 @@ class SgdTable:
     def build(self, device):
         import numpy as np
         import torch
-        dt = np.dtype({"names": ["w", "v", "grad", "n", "gstride", "S", "wd", "wb", "wt", "rows", "cols"],
-                       "formats": ["<u8", "<u8", "<u8", "<i8", "<i8", "<i4", "<f4", "<u8", "<u8", "<i4", "<i4"],
-                       "offsets": [0, 8, 16, 24, 32, 40, 44, 48, 56, 64, 68], "itemsize": 72})
+        dt = np.dtype({"names": ["w", "v", "grad", "n", "gstride", "S", "wd", "wb", "wt", "rows", "cols", "chunk"],
+                       "formats": ["<u8", "<u8", "<u8", "<i8", "<i8", "<i4", "<f4", "<u8", "<u8", "<i4", "<i4", "<i4"],
+                       "offsets": [0, 8, 16, 24, 32, 40, 44, 48, 56, 64, 68, 72], "itemsize": 80})
         rec = np.zeros(len(self.segs), dtype=dt)
         bmap = []
         nbytes = 0
@@ -121,10 +122,15 @@ class SgdTable:
             n = w.numel()
             if n % 4 or gs % 4:
                 raise ValueError("sgd_update segments need sizes and gradient strides divisible by 4")
+            # elements per logical block: ~32 KB of gradient partials read per
+            # block (short blocks = short preemption latency), 1024 at most
+            chunk = self.CHUNK
+            while chunk > 64 and chunk * S * 4 > 32 * 1024:
+                chunk //= 2
             rec[i] = (w.data_ptr(), v.data_ptr(), g.data_ptr(), n, gs, S, wd,
                       wb.data_ptr() if wb is not None else 0, wt.data_ptr() if wt is not None else 0,
-                      rows, cols)
-            for c in range((n + self.CHUNK - 1) // self.CHUNK):
+                      rows, cols, chunk)
+            for c in range((n + chunk - 1) // chunk):
                 bmap.append((i, c))
             nbytes += n * (4 * S + 16 + (2 if wb is not None else 0) + (2 if wt is not None else 0))
         self.dev_segs = torch.from_numpy(rec.view(np.uint8).copy()).to(device)

@@ -40,17 +40,18 @@ def test_gemm_splits_never_empty(M, N, K):
     assert math.ceil(kb / per) == S          # every split has work (bind_gemm rejects empty splits)
     tiles = math.ceil(M / 128) * (N // (128 if N % 128 == 0 else 64))
     flops_per_block = 2.0 * 128 * (128 if N % 128 == 0 else 64) * per * 64
-    assert S == 1 or flops_per_block <= 80e6 or S == kb // 2
+    assert S == 1 or flops_per_block <= 40e6 or S == kb // 2
 
 
 def test_bn_rows_per_block():
-    assert resnet._rb(802816, 64) == 1024 and resnet._rb(802816, 64, 4) == 256
-    assert resnet._rb(3136, 2048) == 256 and resnet._rb(3136, 2048, 4) == 64
+    assert resnet._rb(802816, 64) == 512 and resnet._rb(802816, 64, 4) == 128
+    assert resnet._rb(3136, 2048) == 128 and resnet._rb(3136, 2048, 4) == 32
 
 
 def test_sgd_table_layout():
-    """72-byte nn::SgdSeg records and a (segment, chunk) map covering every
-    element (kernels_nn.cu SgdUpdate)."""
+    """80-byte nn::SgdSeg records and a (segment, chunk) map covering every
+    element (kernels_nn.cu SgdUpdate); segments with many gradient partials
+    get smaller logical blocks."""
     import numpy as np
     w = torch.zeros(96, 200)
     v = torch.zeros_like(w)
@@ -61,14 +62,20 @@ def test_sgd_table_layout():
     t.add(w2, torch.zeros_like(w2), torch.zeros(1, 5000), 1, 5000, 0.0)
     t.build("cpu")
     raw = t.dev_segs.numpy().view(np.uint8)
-    assert raw.size == 2 * 72
+    assert raw.size == 2 * 80
     rec = np.frombuffer(raw.tobytes(), dtype=np.dtype({
-        "names": ["w", "n", "gstride", "S", "rows", "cols"], "formats": ["<u8", "<i8", "<i8", "<i4", "<i4", "<i4"],
-        "offsets": [0, 24, 32, 40, 64, 68], "itemsize": 72}))
+        "names": ["w", "n", "gstride", "S", "rows", "cols", "chunk"],
+        "formats": ["<u8", "<i8", "<i8", "<i4", "<i4", "<i4", "<i4"],
+        "offsets": [0, 24, 32, 40, 64, 68, 72], "itemsize": 80}))
     assert rec["w"][0] == w.data_ptr() and rec["n"][0] == 19200 and rec["S"][0] == 3
     assert rec["gstride"][1] == 5000 and rec["rows"][0] == 96 and rec["cols"][0] == 200
     m = t.dev_map.numpy()
+    assert rec["chunk"][0] == 1024 and rec["chunk"][1] == 1024
     assert t.blocks == math.ceil(19200 / 1024) + math.ceil(5000 / 1024) == len(m)
+    many = resnet.SgdTable()
+    many.add(torch.zeros(4096), torch.zeros(4096), torch.zeros(64, 4096), 64, 4096, 0.0)
+    many.build("cpu")
+    assert many.blocks == 4096 // 128
     assert sorted(set(m[:, 0].tolist())) == [0, 1]
     with pytest.raises(ValueError):
         bad = resnet.SgdTable()

@@ -42,7 +42,7 @@ def pcts(xs):
 
 def main():
     sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
-    from bench import c2_trace
+    from bench import ClockMap, c2_trace
     dev = P.B200Device.get(0)
     gpu = dev.spec
     window = int(arg("--ms", 500.0) * 1e6)
@@ -81,11 +81,12 @@ def main():
     arr = c2_trace(load, hp_lat, window, 0, burst)
     hp_task = P.TaskScript("hp", P.HIGH, (hp_w,), arr)
     be_task = P.TaskScript("be", P.BEST_EFFORT, tuple(be_ws))
-    off, _ = dev.clock_offset()
     for label, tasks, pol in (("solo", [hp_task], "Tally"), ("tally", [hp_task, be_task], "Tally"),
                               ("kp", [hp_task, be_task], "KernelPriority")):
         cfg = P.SchedulerConfig(policy=pol, turnaround_threshold_ns=threshold)
+        clk = ClockMap(dev)
         res = P.run_policy(gpu, tasks, cfg, window, profiler=prof, record_events=False, options={"trace": 1})
+        clk.close()
         hp_l = [r for r in res.launches if r["priority"] == 0]
         be_l = [r for r in res.launches if r["priority"] != 0]
         reqs = res.requests["hp"]
@@ -98,19 +99,19 @@ def main():
                 run.append(L["gpu_end_ns"] - L["gpu_start_ns"])
                 nt.append(L["complete_ns"] - L["gpu_end_ns"])
             tot.append(c - a)
-        pre = []
+        bykind = collections.defaultdict(list)
         for r in be_l:
-            if r["preempt_ns"] < 0:
+            if r["preempt_ns"] < 0 or not r["parked"] or not r["gt_last_exit"]:
                 continue
             sig = r["preempt_ns"] + res.origin_ns
-            pre.append({"kernel": be_ws[r["kernel_index"]].kernel_id[:40] if 0 <= r["kernel_index"] < len(be_ws) else r["kernel_index"],
-                        "shape": r["shape"], "workers": r["workers"], "parked": r["parked"],
-                        "first_start_minus_sig_us": round((r["gt_first_start"] + off - sig) / 1e3, 1) if r["gt_first_start"] else None,
-                        "first_stop_minus_sig_us": round((r["gt_first_stop"] + off - sig) / 1e3, 1) if r["gt_first_stop"] else None,
-                        "last_exit_minus_sig_us": round((r["gt_last_exit"] + off - sig) / 1e3, 1) if r["gt_last_exit"] else None,
-                        "issue_minus_sig_us": round((r["issue_ns"] - r["preempt_ns"]) / 1e3, 1),
-                        "complete_minus_sig_us": round((r["complete_ns"] - r["preempt_ns"]) / 1e3, 1)})
-        out[label + "_preempts"] = pre[:40]
+            kind = be_ws[r["kernel_index"]].kernel_id.split(":")[0] if 0 <= r["kernel_index"] < len(be_ws) else "?"
+            lat = (r["gt_last_exit"] + clk.off(sig) - sig) / 1e3
+            drain = (r["gt_last_exit"] - r["gt_first_stop"]) / 1e3 if r["gt_first_stop"] else None
+            bykind[kind].append((lat, drain, be_ws[r["kernel_index"]].kernel_id if 0 <= r["kernel_index"] < len(be_ws) else "?"))
+        out[label + "_preempt_by_kind"] = {
+            k: {"n": len(v), "lat_p50_max": [round(sorted(x[0] for x in v)[len(v) // 2], 1), round(max(x[0] for x in v), 1)],
+                "drain_max": round(max((x[1] or 0) for x in v), 1),
+                "worst": max(v)[2][:60]} for k, v in bykind.items()}
         out[label] = {"requests": len(reqs), "latency_p50_p90_p99_max_us": pcts(tot),
                       "queue": pcts(q), "issue": pcts(iss), "gpu_start": pcts(st), "gpu_run": pcts(run),
                       "notice": pcts(nt), "be_launches": len(be_l),
