@@ -18,7 +18,7 @@ single-GPU configuration; configs[0] is the reference's CPU-runnable case):
   --config c1 runs the synthetic pair (HP vecadd_f32 2^24 at Poisson load 0.5
   + BE SGEMM 4096^2 3xTF32) instead.
 
-A *step* is one co-location window (default 1000 ms for C2, 100 ms for C1)
+A *step* is one co-location window (default 2000 ms for C2, 100 ms for C1)
 of that traffic through the public API (``run_policy`` on the native runner,
 real time).  Calibration (solo HP over the same arrival traces, solo BE
 untransformed and under the same policy) and W warm-up windows run before the
@@ -67,7 +67,7 @@ def parse():
     ap.add_argument("--config", default="c2", choices=["c1", "c2"],
                     help="c2 = BASELINE configs[1] (ResNet-50 HP bs=1 + ResNet-50 training bs=64); "
                          "c1 = the synthetic vecadd + SGEMM pair")
-    ap.add_argument("--window-ms", type=float, default=None, help="default 100 (c1) / 1000 (c2)")
+    ap.add_argument("--window-ms", type=float, default=None, help="default 100 (c1) / 2000 (c2)")
     ap.add_argument("--load", type=float, default=None, help="mean HP load; default 0.5 (c1) / 0.25 (c2)")
     ap.add_argument("--burst", type=float, default=4.0, help="c2: MMPP burst-rate factor")
     ap.add_argument("--batch", type=int, default=64, help="c2: BE training batch")
@@ -739,11 +739,12 @@ def main_c2(args):
     clocks = Clocks(local)
     clocks.start()
     ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    solo_lat, results = [], []
+    solo_lat, results, solo_res = [], [], []
     elapsed_ms = 0.0
     host_s = 0.0
     for k in range(args.steps):
-        solo_lat += lat_after_warm(run_([hp_task(k)], tally, window))
+        solo_res.append(run_([hp_task(k)], tally, window))
+        solo_lat += lat_after_warm(solo_res[-1])
         if dist is not None:
             dist.barrier()
         torch.cuda.synchronize()
@@ -761,6 +762,15 @@ def main_c2(args):
         elapsed_ms = float(t.item())
 
     co_lat = [x for r in results for x in lat_after_warm(r)]
+    # per-request deltas (same arrival, co-located minus solo) and per-window p99s
+    deltas = []
+    win_p99 = []
+    for rs, rc in zip(solo_res, results):
+        ds = dict(rs.requests["hp"])
+        deltas += [(c - a) - (ds[a] - a) for a, c in rc.requests["hp"] if a >= warm and a in ds]
+        ls, lc = lat_after_warm(rs), lat_after_warm(rc)
+        if ls and lc:
+            win_p99.append([round(p99(ls) / 1e3), round(p99(lc) / 1e3)])
     be_co = sum(be_rate(r) for r in results) / len(results)
     overhead = 100.0 * (p99(co_lat) / p99(solo_lat) - 1.0)
     clkmap.close()
@@ -914,6 +924,8 @@ def main_c2(args):
         "p99_solo_us": p99(solo_lat) / 1e3, "p99_co_us": p99(co_lat) / 1e3,
         "preempt_us": [pct(pl_us, 0.5), pct(pl_us, 0.99), max(pl_us)] if pl_us else None,
         "drain_us": [pct(dr_us, 0.5), pct(dr_us, 0.99)] if dr_us else None, "preemptions": len(pl_us),
+        "delta_us": [round(pct(deltas, q) / 1e3, 1) for q in (0.5, 0.9, 0.99, 1.0)] if deltas else None,
+        "window_p99_us_solo_co": win_p99,
     }
     gathered, worst = gather_pairs(local_out, dist)
     if rank != 0:
@@ -942,6 +954,8 @@ def main_c2(args):
             "be_throughput_pct_vs_native": 100.0 * be_co * native_step_s,
             "preempt_latency_us_p50_p99_max": worst["preempt_us"],
             "preempt_drain_us_p50_p99": worst["drain_us"], "preemptions": worst["preemptions"],
+            "request_delta_us_p50_p90_p99_max": worst["delta_us"],
+            "window_p99_us_solo_co": worst["window_p99_us_solo_co"],
             "preempt_note": "host signal -> last worker exit (device clock mapped to host, linear drift "
                             "correction); drain = first worker stop -> last exit on the device clock",
             "hp_isolated_latency_us": hp_lat / 1e3,
@@ -962,7 +976,7 @@ def main_c2(args):
 def main():
     args = parse()
     if args.window_ms is None:
-        args.window_ms = 100.0 if args.config == "c1" else 1000.0
+        args.window_ms = 100.0 if args.config == "c1" else 2000.0
     if args.load is None:
         args.load = 0.5 if args.config == "c1" else 0.25
     if args.cpu_sample_ms is None:

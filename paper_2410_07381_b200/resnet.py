@@ -49,7 +49,7 @@ def _rb(P, C, streams=1):
     per-block fixed cost -- partial write, fence, counter -- stays small) while
     a block still streams in a few microseconds; backward statistics read up
     to four streams."""
-    return (512 if C < 128 else (256 if C < 256 else 128)) // streams
+    return (1024 if C < 128 else (512 if C < 256 else 256)) // streams
 
 
 def _gemm_splits(M, N, Kdim):

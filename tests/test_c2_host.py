@@ -44,8 +44,8 @@ def test_gemm_splits_never_empty(M, N, K):
 
 
 def test_bn_rows_per_block():
-    assert resnet._rb(802816, 64) == 512 and resnet._rb(802816, 64, 4) == 128
-    assert resnet._rb(3136, 2048) == 128 and resnet._rb(3136, 2048, 4) == 32
+    assert resnet._rb(802816, 64) == 1024 and resnet._rb(802816, 64, 4) == 256
+    assert resnet._rb(3136, 2048) == 256 and resnet._rb(3136, 2048, 4) == 64
 
 
 def test_sgd_table_layout():
