@@ -17,6 +17,7 @@
 #include <cstring>
 #include <deque>
 #include <map>
+#include <unordered_map>
 #include <queue>
 #include <vector>
 
@@ -39,6 +40,7 @@ struct Handle {
   long long gt_first_start = 0, gt_first_stop = 0, gt_last_exit = 0;
   long long count = 0;
   long long gpu_start = -1, gpu_end = -1;
+  int kernel_index = -1;   // position of the work in its task's pipeline
   int hp_slot = -1;
 };
 
@@ -81,6 +83,7 @@ class CudaDevice : public Device {
     Handle h;
     h.d = d;
     h.submit_ns = now();
+    h.kernel_index = kernel_index_of(d.task, d.device_kernel);
     hs_.push_back(h);
     const long long id = (long long)hs_.size() - 1;
     log_event(TALLY_EV_LAUNCH_ISSUED, id, -1);
@@ -238,6 +241,20 @@ class CudaDevice : public Device {
 #endif
   }
 
+  // (task, device kernel) -> pipeline position, built once per task: the
+  // daemon's per-event bookkeeping stays O(1) for ~400-kernel pipelines
+  std::vector<std::unordered_map<int, int>> kidx_;
+  int kernel_index_of(int task, int device_kernel) {
+    if ((size_t)task >= kidx_.size()) kidx_.resize((size_t)task + 1);
+    auto& m = kidx_[(size_t)task];
+    if (m.empty()) {
+      const auto& ks = r_->tasks[(size_t)task].kernels;
+      for (size_t k = ks.size(); k-- > 0;) m[ks[k].device_kernel] = (int)k;   // first occurrence wins
+    }
+    auto it = m.find(device_kernel);
+    return it == m.end() ? -1 : it->second;
+  }
+
   Handle& get(long long id) {
     if (id < 0 || id >= (long long)hs_.size()) throw Error(TALLY_EINVAL, "unknown handle");
     return hs_[(size_t)id];
@@ -249,12 +266,7 @@ class CudaDevice : public Device {
     e.time_ns = now();
     e.kind = kind;
     e.task = h.d.task;
-    e.kernel_index = -1;
-    for (size_t k = 0; k < r_->tasks[(size_t)h.d.task].kernels.size(); ++k)
-      if (r_->tasks[(size_t)h.d.task].kernels[k].device_kernel == h.d.device_kernel) {
-        e.kernel_index = (int)k;
-        break;
-      }
+    e.kernel_index = h.kernel_index;
     e.block = block;
     r_->log.events.push_back(e);
   }
@@ -383,10 +395,7 @@ class CudaDevice : public Device {
     tally_launch_record rec;
     memset(&rec, 0, sizeof(rec));
     rec.task = h.d.task;
-    rec.kernel_index = -1;
-    const auto& ks = r_->tasks[(size_t)h.d.task].kernels;
-    for (size_t k = 0; k < ks.size(); ++k)
-      if (ks[k].device_kernel == h.d.device_kernel) { rec.kernel_index = (int)k; break; }
+    rec.kernel_index = h.kernel_index;
     rec.priority = h.d.priority;
     rec.shape = h.d.shape == TALLY_SHAPE_PTB ? TALLY_SHAPE_PTB
                 : (h.d.is_slice ? TALLY_SHAPE_SLICED : TALLY_SHAPE_ORIGINAL);
