@@ -268,7 +268,8 @@ struct alignas(64) GemmParams {
   long long split_stride;       // elements between split-K partial outputs
   int splits;                   // split-K factor: logical block = (split, tile)
   int kb_per_split;             // k-blocks per split
-  int claim_batch;              // PTB: tiles claimed per L2 atomic
+  int tpb;                      // tiles per logical block
+  long long total_tiles;        // tiles * splits
 };
 
 __device__ __forceinline__ void tile_coords(long long t, const GemmParams& p, int& mb, int& nb) {
@@ -359,7 +360,10 @@ __global__ void __launch_bounds__(kThreads, Cfg::KIND == 1 ? 2 : 1) k_gemm(const
       }
       uint32_t it = 0;
       unsigned flag_seen = 0;
-      long long q_next = 0, q_end = 0;   // PTB: tiles claimed in a batch, not yet started
+      // a logical block covers tiles [b * tpb, b * tpb + tpb) of the tile
+      // sequence (tpb > 1 for short-K GEMMs, whose one-tile CTAs are
+      // prologue / pipeline-fill bound)
+      long long q_next = 0, q_end = 0;
       for (int i = 0;; ++i) {
         long long t = -1;
         int c0 = 0;
@@ -388,26 +392,27 @@ __global__ void __launch_bounds__(kThreads, Cfg::KIND == 1 ? 2 : 1) k_gemm(const
           }
           if (!popped) {
             if (q_next < q_end) {
-              t = q_next++;   // claimed earlier in this batch: always executed
+              t = q_next++;   // the rest of a claimed logical block: always executed
             } else {
-              // short-K tiles are claim-latency bound: claim claim_batch tiles
-              // with one flag-gated L2 atomic (exactly-once is unchanged; a
-              // preempted worker finishes its batch, <= claim_batch tiles)
-              t = ptb_claim_n(s, p.claim_batch);
-              if (t >= 0) {
-                q_next = t + 1;
-                q_end = t + p.claim_batch;
+              const long long b = ptb_claim(s);
+              if (b < 0) {
+                stopped = true;
+              } else if ((unsigned long long)b < s.total) {
+                q_next = b * p.tpb;
+                q_end = min((long long)p.total_tiles, q_next + p.tpb);
+                t = q_next++;
               }
             }
-            if (t < 0) stopped = true;
-            else if ((unsigned long long)t >= s.total) t = -1;
           }
         } else {
           if (i == 0) {
-            t = MODE == kOriginal ? (long long)blockIdx.x
+            const long long b = MODE == kOriginal ? (long long)blockIdx.x
                 : (s.linear ? (long long)(s.linear_offset + blockIdx.x) : (long long)(s.offset.x + blockIdx.x));
-            if (s.exec_count != nullptr) atomicAdd(&s.exec_count[t], 1ull);
+            if (s.exec_count != nullptr) atomicAdd(&s.exec_count[b], 1ull);
+            q_next = b * p.tpb;
+            q_end = min((long long)p.total_tiles, q_next + p.tpb);
           }
+          if (q_next < q_end) t = q_next++;
         }
         const int j = i % kSlots;
         if (i >= kSlots) mbar_wait(&tile_empty[j], ((i / kSlots) - 1) & 1);
@@ -815,9 +820,11 @@ static int bind_gemm(const tally_kernel_args* a, Instance* inst, bool split) {
   // kernel (16 chunks of ~4.5 us per 4096-deep tile); bf16 (1e-2 budget)
   // accumulates the whole K in TMEM
   p.kchunk = Cfg::KIND == 0 ? 256 / Cfg::BK : p.kb_per_split;
-  // a logical block of <= 2 k-blocks is ~1 us: claim 4 at a time (<= 4 us of
-  // committed work on preemption); longer blocks one at a time
-  p.claim_batch = (Cfg::KIND == 1 && p.kb_per_split <= 2) ? 4 : 1;
+  // short-K tiles (<= 2 k-blocks, ~1 us each): 4 tiles per logical block, so
+  // an untransformed CTA pipelines 4 tiles behind one prologue and a PTB
+  // claim covers ~4 us of work; longer tiles are one logical block each
+  p.tpb = (Cfg::KIND == 1 && p.kb_per_split <= 2) ? 4 : 1;
+  p.total_tiles = (long long)p.tiles_m * p.tiles_n * p.splits;
   p.resume = nullptr;
   // i[3] = 1: block-granular preemption only (no resume ring)
   if (Cfg::KIND == 0 && a->i[3] == 0) {
@@ -831,7 +838,7 @@ static int bind_gemm(const tally_kernel_args* a, Instance* inst, bool split) {
   }
   static_assert(sizeof(p) <= kMaxParamBytes, "params too large");
   memcpy(inst->params, &p, sizeof(p));
-  inst->grid = make_uint3((unsigned)(p.tiles_m * p.tiles_n * p.splits), 1, 1);
+  inst->grid = make_uint3((unsigned)((p.total_tiles + p.tpb - 1) / p.tpb), 1, 1);
   inst->threads = gemm::kThreads;
   inst->smem = gemm::smem_bytes<Cfg>();
   inst->alg_flops = 2.0 * (double)M * (double)N * (double)K;

@@ -53,14 +53,15 @@ def _rb(P, C, streams=1):
 
 
 def _gemm_splits(M, N, Kdim):
-    """Split-K factor for a GEMM: enough logical blocks of <= ~20 MFLOP each
-    (~10 us on one SM, the preemption granularity) that the tuner finds a
+    """Split-K factor for a GEMM: enough logical blocks of <= ~40 MFLOP each
+    (~10-20 us on one SM, the preemption granularity) that the tuner finds a
     preemptible configuration under the turnaround threshold, without empty
-    splits."""
+    splits.  (20 MFLOP blocks cut the wgrad drain from ~19 to ~12 us but cost
+    ~0.4 ms per step in split-K partial traffic.)"""
     tiles = math.ceil(M / 128) * (N // (128 if N % 128 == 0 else 64))
     kb = math.ceil(Kdim / 64)
     flops = 2.0 * tiles * 128 * (128 if N % 128 == 0 else 64) * Kdim
-    want = max(tiles, math.ceil(flops / 20e6))
+    want = max(tiles, math.ceil(flops / 40e6))
     s = max(1, min(kb // 2, math.ceil(want / tiles)))
     return math.ceil(kb / math.ceil(kb / s))
 
