@@ -842,9 +842,13 @@ def main_c2(args):
     else:
         peak, achieved, unit, bound = pk_b, top_dk.info.alg_bytes / chosen_ns, "GB/s", "hbm"
     traffic = None
-    try:
-        traffic = json.load(open(os.path.join(ROOT, "profiles", "ncu_traffic.json"))).get(
-            f"c2:{top_name}:{top_cand.describe()}")
+    try:   # per-launch DRAM bytes from an ncu --set full capture of this kernel (shape-independent to ~1 %)
+        tr_db = json.load(open(os.path.join(ROOT, "profiles", "ncu_traffic.json")))
+        for key in (f"c2:{top_name}:{top_cand.describe()}", f"c2:{top_name}:Ptb(full occupancy)",
+                    f"c2:{top_name}:Original"):
+            if key in tr_db:
+                traffic = tr_db[key]
+                break
     except (OSError, ValueError):
         pass
     roofline = {"bound": bound, "kernel": f"{top_name} ({top_dk.kind}, {top_cand.describe()})",

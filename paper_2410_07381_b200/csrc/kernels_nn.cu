@@ -259,9 +259,18 @@ struct BnStats {
     const int lanes_r = kThreads / CB;
     const int lc = threadIdx.x % CB, lr = threadIdx.x / CB;
     float a = 0.f, b = 0.f;
-    for (int r = r0 + lr; r < r1; r += lanes_r) {
-      a += __ldcg(src + (long long)r * C + c0 + lc);
-      b += __ldcg(src + (rows_total + r) * C + c0 + lc);
+    // 8 rows' loads in flight per batch, summed in row order (deterministic):
+    // a dependent load per row would put ~32 L2 round trips on the tail
+    for (int r = r0 + lr; r < r1; r += 8 * lanes_r) {
+      float va[8], vb[8];
+#pragma unroll
+      for (int u = 0; u < 8; ++u) {
+        const int rr = r + u * lanes_r;
+        va[u] = rr < r1 ? __ldcg(src + (long long)rr * C + c0 + lc) : 0.f;
+        vb[u] = rr < r1 ? __ldcg(src + (rows_total + rr) * C + c0 + lc) : 0.f;
+      }
+#pragma unroll
+      for (int u = 0; u < 8; ++u) { a += va[u]; b += vb[u]; }
     }
     red[lr * CB + lc] = a;
     red[kThreads + lr * CB + lc] = b;
@@ -351,31 +360,36 @@ struct BnStats {
       p.part[(long long)bidx.y * p.C + ch] = a;
       p.part[((long long)p.nrb + bidx.y) * p.C + ch] = b;
     }
-    // ---- level 1: the last row block of the group folds the group
-    __threadfence();
+    // ---- level 1: the last row block of the group folds the group.
+    // Barrier, then one thread's GPU-scope fence (cumulative over the CTA's
+    // writes ordered before the barrier) + counter; its fence after the
+    // counter orders the folder's reads after every other block's release.
     __syncthreads();
     const int gi = bidx.y / kGroup;
     if (threadIdx.x == 0) {
       const unsigned in_group = (unsigned)min(kGroup, p.nrb - gi * kGroup);
+      __threadfence();
       flag[0] = atomicAdd(&p.cnt1[bidx.x * p.ngroups + gi], 1u) + 1u == in_group;
+      __threadfence();
     }
     __syncthreads();
     if (flag[0]) {
-      __threadfence();
       float a = 0.f, b = 0.f;
       fold(p.part, p.nrb, gi * kGroup, min(p.nrb, (gi + 1) * kGroup), p.C, c0, CB, red, &a, &b);
       if (threadIdx.x < CB) {
         p.part2[(long long)gi * p.C + c0 + threadIdx.x] = a;
         p.part2[((long long)p.ngroups + gi) * p.C + c0 + threadIdx.x] = b;
       }
-      if (threadIdx.x == 0) p.cnt1[bidx.x * p.ngroups + gi] = 0u;   // ready for the next launch
-      __threadfence();
       __syncthreads();
-      if (threadIdx.x == 0) flag[1] = atomicAdd(&p.cnt2[bidx.x], 1u) + 1u == (unsigned)p.ngroups;
+      if (threadIdx.x == 0) {
+        p.cnt1[bidx.x * p.ngroups + gi] = 0u;   // ready for the next launch
+        __threadfence();
+        flag[1] = atomicAdd(&p.cnt2[bidx.x], 1u) + 1u == (unsigned)p.ngroups;
+        __threadfence();
+      }
       __syncthreads();
       if (flag[1]) {
         // ---- level 2: the last group finalises this channel block
-        __threadfence();
         fold(p.part2, p.ngroups, 0, p.ngroups, p.C, c0, CB, red, &a, &b);
         if (threadIdx.x < CB) {
           const int ch = c0 + threadIdx.x;
