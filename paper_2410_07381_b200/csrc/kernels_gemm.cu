@@ -857,11 +857,17 @@ static int bind_bf16(const tally_kernel_args* a, Instance* inst) { return bind_g
 template <class Cfg>
 static int setup_gemm() {
   const int smem = (int)gemm::smem_bytes<Cfg>();
-  cudaError_t e;
-  if ((e = cudaFuncSetAttribute(gemm::k_gemm<Cfg, gemm::kOriginal, SliceArgs>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem)) != cudaSuccess ||
-      (e = cudaFuncSetAttribute(gemm::k_gemm<Cfg, gemm::kSliced, SliceArgs>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem)) != cudaSuccess ||
-      (e = cudaFuncSetAttribute(gemm::k_gemm<Cfg, gemm::kPtb, PtbArgs>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem)) != cudaSuccess)
-    return cuda_fail(e, "gemm smem attribute");
+  const void* fns[3] = {reinterpret_cast<const void*>(&gemm::k_gemm<Cfg, gemm::kOriginal, SliceArgs>),
+                        reinterpret_cast<const void*>(&gemm::k_gemm<Cfg, gemm::kSliced, SliceArgs>),
+                        reinterpret_cast<const void*>(&gemm::k_gemm<Cfg, gemm::kPtb, PtbArgs>)};
+  for (const void* f : fns) {
+    cudaError_t e = cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+    // the whole carveout as shared memory: two bf16 GEMM CTAs (~100 KB each)
+    // share an SM -- the occupancy the tuner's PTB worker menu is built from
+    if (e == cudaSuccess)
+      e = cudaFuncSetAttribute(f, cudaFuncAttributePreferredSharedMemoryCarveout, cudaSharedmemCarveoutMaxShared);
+    if (e != cudaSuccess) return cuda_fail(e, "gemm smem attribute");
+  }
   return TALLY_OK;
 }
 
@@ -894,6 +900,7 @@ static KernelKind gemm_kind(const char* name, int (*bind)(const tally_kernel_arg
   k.bind = bind;
   k.setup = &setup_gemm<Cfg>;
   k.pausable = 1;
+  k.tmem_cols = Cfg::TMEM_COLS;
   // device-resident flag: producers poll it every K-chunk (~9 us) -- 148
   // readers x 110 k reads/s would saturate PCIe reads of a mapped host word
   k.host_flag = 0;

@@ -61,6 +61,11 @@ struct KernelKind {
   // 1: PTB launches read their preemption flag from mapped host memory
   // (few readers, one read per long logical block)
   int host_flag;
+  // tcgen05 kinds: TMEM columns one CTA allocates (0 = none).  The runtime's
+  // occupancy API reports 1 CTA/SM for these kernels even where smem,
+  // registers and TMEM admit 2 (and the hardware co-schedules 2, ncu
+  // r01_ncu_c2_summary); the PTB worker menu uses the resource-derived count.
+  int tmem_cols;
   // IR-JIT kinds (irjit.py): NVRTC-compiled module, launched with the driver API
   int jit;
   void* cu_fn[3];             // CUfunction for Original / Sliced / PTB

@@ -848,6 +848,22 @@ int tally_kernel_info_get(int kernel, tally_kernel_info* o) {
   o->occupancy_ptb = occ;
   CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kk.fn_original, in.threads, in.smem), "occupancy");
   o->occupancy_original = occ;
+  if (kk.tmem_cols > 0) {
+    // resource-derived residency of a tcgen05 kernel: TMEM columns, shared
+    // memory (+1 KB reserved per CTA), registers (256-register warp granules)
+    cudaFuncAttributes fa;
+    CK(cudaFuncGetAttributes(&fa, kk.fn_ptb), "func attributes");
+    int smem_sm = 0;
+    CK(cudaDeviceGetAttribute(&smem_sm, cudaDevAttrMaxSharedMemoryPerMultiprocessor, r.device), "smem per SM");
+    const int warps = (in.threads + 31) / 32;
+    const int regs_warp = (fa.numRegs * 32 + 255) / 256 * 256;
+    int n = 512 / kk.tmem_cols;
+    n = std::min(n, smem_sm / (int)(in.smem + 1024));
+    n = std::min(n, 65536 / std::max(1, regs_warp * warps));
+    n = std::min(n, 64 / warps);
+    o->occupancy_ptb = std::max(o->occupancy_ptb, n);
+    o->occupancy_original = std::max(o->occupancy_original, n);
+  }
   return TALLY_OK;
 }
 
