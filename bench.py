@@ -95,6 +95,12 @@ def p99(xs):
     return s[math.ceil(0.99 * len(s)) - 1]
 
 
+def frac(a, b):
+    """100 * a / b, or None when the denominator is empty (a window too short
+    to finish a best-effort step)."""
+    return 100.0 * a / b if b else None
+
+
 def pct(xs, q):
     s = sorted(xs)
     return s[min(len(s) - 1, int(q * (len(s) - 1)))]
@@ -209,6 +215,25 @@ def run_reference_arm(args):
     }))
 
 
+def init_dist(local, world):
+    """One process per GPU; the only cross-rank traffic is the barrier, the
+    timing max and the metric gather (NCCL by default).
+    TALLY_BENCH_DIST_BACKEND=gloo allows a functional multi-rank run with
+    several ranks on one GPU (ranks map to local % device_count)."""
+    import torch
+    dev_index = local % max(1, torch.cuda.device_count())
+    torch.cuda.set_device(dev_index)
+    if world <= 1:
+        return None, dev_index, "cuda"
+    import torch.distributed as dist
+    backend = os.environ.get("TALLY_BENCH_DIST_BACKEND", "nccl")
+    if backend == "nccl":
+        dist.init_process_group("nccl", device_id=torch.device("cuda", dev_index))
+        return dist, dev_index, "cuda"
+    dist.init_process_group(backend)
+    return dist, dev_index, "cpu"
+
+
 # ----------------------------------------------------------------- GPU arm
 def gather_pairs(local_out, dist=None):
     """Every rank runs an independent HP/BE pair; rank 0 reports the worst
@@ -228,11 +253,7 @@ def main_c1(args):
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
-    torch.cuda.set_device(local)
-    dist = None
-    if world > 1:
-        import torch.distributed as dist
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    dist, local, red_dev = init_dist(local, world)
 
     import paper_2410_07381_b200 as P
     from paper_2410_07381_b200 import kernels, workloads
@@ -294,40 +315,35 @@ def main_c1(args):
         return done / ((window - warm) / 1e9)
 
     # --- calibration (untimed) -------------------------------------------------
-    solo_lat = []
-    for k in range(args.steps):
-        solo_lat += lat_after_warm(run_([hp_task(k)], tally, window, profiler=prof,
-                                                record_events=False))
     eager = P.SchedulerConfig(policy="Eager")
-    be_untransformed = be_rate(run_([be_task], eager, window, profiler=prof,
-                                            record_events=False))
-    be_same_policy = be_rate(run_([be_task], tally, window, profiler=prof,
-                                          record_events=False))
+    be_untransformed = be_rate(run_([be_task], eager, window, profiler=prof, record_events=False))
+    be_same_policy = be_rate(run_([be_task], tally, window, profiler=prof, record_events=False))
     for w in range(args.warmup):
-        run_([hp_task(100 + w), be_task], tally, window, profiler=prof,
-                     record_events=False)
+        run_([hp_task(100 + w), be_task], tally, window, profiler=prof, record_events=False)
     clkmap = ClockMap(dev)
 
-    # --- timed region: K co-located windows --------------------------------------
+    # --- timed region: K co-located windows, each paired with the solo-HP
+    # window of the same arrival trace run just before it (as in C2) -------
     clocks = Clocks(local)
-    if dist is not None:
-        dist.barrier()
-    torch.cuda.synchronize()
     clocks.start()
     ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    ev0.record()
-    t_host0 = time.perf_counter()
-    results = []
+    solo_lat, results = [], []
+    elapsed_ms = host_s = 0.0
     for k in range(args.steps):
-        results.append(run_([hp_task(k), be_task], tally, window, profiler=prof,
-                                    record_events=False))
-    ev1.record()
-    torch.cuda.synchronize()
-    host_s = time.perf_counter() - t_host0
-    elapsed_ms = ev0.elapsed_time(ev1)
+        solo_lat += lat_after_warm(run_([hp_task(k)], tally, window, profiler=prof, record_events=False))
+        if dist is not None:
+            dist.barrier()
+        torch.cuda.synchronize()
+        ev0.record()
+        t_host0 = time.perf_counter()
+        results.append(run_([hp_task(k), be_task], tally, window, profiler=prof, record_events=False))
+        ev1.record()
+        torch.cuda.synchronize()
+        host_s += time.perf_counter() - t_host0
+        elapsed_ms += ev0.elapsed_time(ev1)
     clk = clocks.stop()
     if dist is not None:
-        t = torch.tensor([elapsed_ms], device="cuda")
+        t = torch.tensor([elapsed_ms], device=red_dev)
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         elapsed_ms = float(t.item())
 
@@ -438,7 +454,7 @@ def main_c1(args):
             sl = [x for k in range(min(2, args.steps)) for x in lat_after_warm(
                 run_([hp_task(k)], cfg, window, profiler=prof, record_events=False))]
             baselines[pol] = {"p99_overhead_pct": 100.0 * (p99(lat) / p99(sl) - 1.0),
-                              "be_throughput_pct": 100.0 * (sum(rate) / len(rate)) / be_untransformed}
+                              "be_throughput_pct": frac(sum(rate) / len(rate), be_untransformed)}
         # the same Tally policy with tile-granular (block-level, as in the
         # paper) PTB preemption of the SGEMM instead of chunk-granular
         clkmap_b = ClockMap(dev)      # re-anchor: globaltimer drifts vs CLOCK_MONOTONIC
@@ -457,7 +473,7 @@ def main_c1(args):
         pb = preempt_latencies_us(res_b, clkmap_b)
         baselines["Tally_tile_granular_PTB"] = {
             "p99_overhead_pct": 100.0 * (p99(lat) / p99(solo_lat) - 1.0),
-            "be_throughput_pct": 100.0 * (sum(rate) / len(rate)) / be_untransformed,
+            "be_throughput_pct": frac(sum(rate) / len(rate), be_untransformed),
             "preempt_latency_us_p50_p99": [pct(pb, 0.5), pct(pb, 0.99)] if pb else None,
             "tuner_choice": prof.select(blk_ws[2].profile_key(), blk_ws[2].cost, threshold).describe()}
 
@@ -472,8 +488,8 @@ def main_c1(args):
                "wall_s": wall, "sim_ms_per_wall_s": hz / 1e6 / wall, "events_per_s": ne / wall}
 
     local_out = {
-        "overhead": overhead, "be_frac": 100.0 * be_co / be_untransformed,
-        "be_frac_same_policy": 100.0 * be_co / be_same_policy,
+        "overhead": overhead, "be_frac": frac(be_co, be_untransformed),
+        "be_frac_same_policy": frac(be_co, be_same_policy),
         "p99_solo_us": p99(solo_lat) / 1e3, "p99_co_us": p99(co_lat) / 1e3,
         "preempt_us": [pct(pl_us, 0.5), pct(pl_us, 0.99), max(pl_us)] if pl_us else None,
     }
@@ -503,8 +519,9 @@ def main_c1(args):
         "components": {
             "p99_overhead_pct": worst["overhead"],
             "p99_hp_us": {"solo": worst["p99_solo_us"], "colocated": worst["p99_co_us"]},
-            "be_throughput_pct": min(d["be_frac"] for d in gathered),
-            "be_throughput_pct_vs_same_policy_solo": min(d["be_frac_same_policy"] for d in gathered),
+            "be_throughput_pct": min((d["be_frac"] for d in gathered if d["be_frac"] is not None), default=None),
+            "be_throughput_pct_vs_same_policy_solo": min(
+                (d["be_frac_same_policy"] for d in gathered if d["be_frac_same_policy"] is not None), default=None),
             "preempt_latency_us_p50_p99_max": worst["preempt_us"],
             "hp_isolated_latency_us": hp_lat / 1e3,
             "hp_requests_timed": len(co_lat), "be_launches_timed": n_be,
@@ -667,11 +684,7 @@ def main_c2(args):
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
-    torch.cuda.set_device(local)
-    dist = None
-    if world > 1:
-        import torch.distributed as dist
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    dist, local, red_dev = init_dist(local, world)
 
     import paper_2410_07381_b200 as P
     from paper_2410_07381_b200 import kernels, resnet, workloads
@@ -757,7 +770,7 @@ def main_c2(args):
         elapsed_ms += ev0.elapsed_time(ev1)
     clk = clocks.stop()
     if dist is not None:
-        t = torch.tensor([elapsed_ms], device="cuda")
+        t = torch.tensor([elapsed_ms], device=red_dev)
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         elapsed_ms = float(t.item())
 
@@ -898,7 +911,7 @@ def main_c2(args):
                 lat += lat_after_warm(r)
                 rate.append(be_rate(r))
             baselines[pol] = {"p99_overhead_pct": 100.0 * (p99(lat) / p99(sl) - 1.0),
-                              "be_throughput_pct": 100.0 * (sum(rate) / len(rate)) / be_untransformed}
+                              "be_throughput_pct": frac(sum(rate) / len(rate), be_untransformed)}
 
     # --- the measured costs the CPU reference consumes; CPU baseline ------------------
     recs = {}
@@ -923,8 +936,8 @@ def main_c2(args):
                "wall_s": wall, "sim_ms_per_wall_s": hz / 1e6 / wall, "events_per_s": ne / wall}
 
     local_out = {
-        "overhead": overhead, "be_frac": 100.0 * be_co / be_untransformed,
-        "be_frac_same_policy": 100.0 * be_co / be_same_policy,
+        "overhead": overhead, "be_frac": frac(be_co, be_untransformed),
+        "be_frac_same_policy": frac(be_co, be_same_policy),
         "p99_solo_us": p99(solo_lat) / 1e3, "p99_co_us": p99(co_lat) / 1e3,
         "preempt_us": [pct(pl_us, 0.5), pct(pl_us, 0.99), max(pl_us)] if pl_us else None,
         "drain_us": [pct(dr_us, 0.5), pct(dr_us, 0.99)] if dr_us else None, "preemptions": len(pl_us),
@@ -951,8 +964,9 @@ def main_c2(args):
         "components": {
             "p99_overhead_pct": worst["overhead"],
             "p99_hp_us": {"solo": worst["p99_solo_us"], "colocated": worst["p99_co_us"]},
-            "be_throughput_pct": min(d["be_frac"] for d in gathered),
-            "be_throughput_pct_vs_same_policy_solo": min(d["be_frac_same_policy"] for d in gathered),
+            "be_throughput_pct": min((d["be_frac"] for d in gathered if d["be_frac"] is not None), default=None),
+            "be_throughput_pct_vs_same_policy_solo": min(
+                (d["be_frac_same_policy"] for d in gathered if d["be_frac_same_policy"] is not None), default=None),
             "be_steps_per_s": {"untransformed_solo": be_untransformed, "tally_solo": be_same_policy,
                                "colocated": be_co, "native_back_to_back": 1.0 / native_step_s},
             "be_throughput_pct_vs_native": 100.0 * be_co * native_step_s,
