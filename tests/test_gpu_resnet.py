@@ -438,3 +438,30 @@ def test_resnet50_infer_graph(env):
     hp.kernel.original(hs).wait()
     ref = hp.reference()
     assert nerr(hp.out, ref) < 1e-2
+
+
+def test_l2_persist_and_prefetch_api(env):
+    """B200 co-location cache policy entry points: the persisting window on a
+    stream and on a graph's kernel nodes, and the capturable L2 warm-up --
+    the request graph built with them computes the same logits."""
+    P, kernels, stream = env
+    import ctypes as C
+    from paper_2410_07381_b200 import _lib, resnet
+    buf = torch.zeros(1 << 20, device="cuda")
+    side = torch.cuda.Stream()
+    win = C.c_longlong()
+    _lib.check(_lib.lib.tally_l2_persist(C.c_void_p(side.cuda_stream), C.c_void_p(buf.data_ptr()),
+                                         buf.numel() * 4, 1.0, C.byref(win)), "l2 persist")
+    assert win.value == buf.numel() * 4
+    _lib.check(_lib.lib.tally_l2_prefetch(C.c_void_p(side.cuda_stream), C.c_void_p(buf.data_ptr()),
+                                          buf.numel() * 4), "l2 prefetch")
+    side.synchronize()
+    assert _lib.lib.tally_l2_prefetch(C.c_void_p(side.cuda_stream), C.c_void_p(buf.data_ptr() + 4), 64) != 0
+    plain = resnet.ResNet50Infer(batch=1, image=224, persist_l2=None, warm_l2=False)
+    tuned = resnet.ResNet50Infer(batch=1, image=224, persist_l2="nodes", warm_l2=True)
+    hs = kernels.Stream(high_priority=True)
+    tuned.inp.copy_(plain.inp)
+    plain.kernel.original(hs).wait()
+    tuned.kernel.original(hs).wait()
+    assert tuned.l2_nodes > 50
+    assert torch.equal(plain.out, tuned.out)
