@@ -268,13 +268,12 @@ class ResNet50Train:
 
     def _scr(self, key, numel, dtype=None):
         """Shared scratch: kernels of the step run strictly in order on one
-        stream, so transient operands (BN partials, transposes, dgrad
-        columns) reuse one buffer per role, sized for the largest layer."""
-        torch = self.torch
-        dtype = dtype or torch.bfloat16
+        stream, so transient operands (BN partials, dgrad columns, split-K
+        workspaces) reuse one buffer per role, sized for the largest layer
+        by _reserve_all."""
         cur = self._scratch.get(key)
-        if cur is None or cur.numel() < numel:
-            raise RuntimeError("scratch not reserved")  # sized in _reserve
+        if cur is None or cur.numel() < numel or (dtype is not None and cur.dtype != dtype):
+            raise RuntimeError(f"scratch {key!r} not reserved for {numel} elements")
         return cur[:numel]
 
     def _reserve(self, key, numel, dtype):
