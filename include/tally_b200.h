@@ -109,6 +109,22 @@ typedef struct {
   double f[4];
 } tally_kernel_args;
 
+/* Optional layout of a bf16 GEMM kind (tally_kernel_args.ptr[3], host memory,
+ * read at tally_kernel_create): batched launches over sub-matrices of larger
+ * row-major tensors (attention: per (sequence, head) blocks of a fused QKV
+ * activation).  Logical block = (batch z, output tile, K split); batch z has
+ * zb = z / hdiv, zh = z % hdiv and every operand's (row, col) origin is
+ * off[0] * zb + off[1] * zh, in the tensor's own row / column coordinates. */
+typedef struct {
+  long long a_rows, a_cols, a_ld; /* A extent (row-major, cols contiguous), row pitch */
+  long long b_rows, b_cols, b_ld; /* B extent and row pitch (elements)               */
+  long long ldc;                  /* C row stride (elements)                      */
+  int batches, hdiv;
+  long long a_row_off[2], a_col_off[2];
+  long long b_row_off[2], b_col_off[2];
+  long long c_row_off[2], c_col_off[2];
+} tally_gemm_layout;
+
 typedef struct {
   unsigned grid_x, grid_y, grid_z;  /* logical grid (the untransformed launch)  */
   long long total_blocks;

@@ -51,6 +51,15 @@ class c_kernel_args(C.Structure):
     _fields_ = [("ptr", C.c_void_p * 8), ("i", C.c_longlong * 8), ("f", C.c_double * 4)]
 
 
+class c_gemm_layout(C.Structure):
+    _fields_ = [("a_rows", C.c_longlong), ("a_cols", C.c_longlong), ("a_ld", C.c_longlong),
+                ("b_rows", C.c_longlong), ("b_cols", C.c_longlong), ("b_ld", C.c_longlong),
+                ("ldc", C.c_longlong), ("batches", C.c_int), ("hdiv", C.c_int),
+                ("a_row_off", C.c_longlong * 2), ("a_col_off", C.c_longlong * 2),
+                ("b_row_off", C.c_longlong * 2), ("b_col_off", C.c_longlong * 2),
+                ("c_row_off", C.c_longlong * 2), ("c_col_off", C.c_longlong * 2)]
+
+
 class c_kernel_info(C.Structure):
     _fields_ = [("grid_x", C.c_uint), ("grid_y", C.c_uint), ("grid_z", C.c_uint),
                 ("total_blocks", C.c_longlong), ("threads_per_block", C.c_int),

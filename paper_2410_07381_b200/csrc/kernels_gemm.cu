@@ -145,13 +145,13 @@ __device__ __forceinline__ uint64_t smem_desc_mn(const void* p) {
 }
 
 // Instruction descriptor: D fp32, A and B K-major (or both MN-major), M = 128, N = BN.
-template <int KIND, int BN, bool MN = false>
+template <int KIND, int BN, bool A_MN = false, bool B_MN = false>
 __host__ __device__ constexpr uint32_t make_idesc() {
   return (1u << 4)                                  // D format: F32
          | ((KIND == 0 ? 2u : 1u) << 7)             // A format: TF32 / BF16
          | ((KIND == 0 ? 2u : 1u) << 10)            // B format
-         | ((MN ? 1u : 0u) << 15)                   // A major: MN
-         | ((MN ? 1u : 0u) << 16)                   // B major: MN
+         | ((A_MN ? 1u : 0u) << 15)                 // A major: MN
+         | ((B_MN ? 1u : 0u) << 16)                 // B major: MN
          | ((uint32_t)(BN >> 3) << 17)              // N >> 3
          | ((uint32_t)(128 >> 4) << 24);            // M >> 4
 }
@@ -194,7 +194,7 @@ struct CfgTf32x3T {
   static constexpr int STAGES = STAGES_;
   static constexpr int UMMA_K = 8;
   static constexpr int TMEM_COLS = BN == 64 ? 256 : 512;   // 2 x BN accumulators + BN running total
-  static constexpr bool MN = false;
+  static constexpr bool A_MN = false, B_MN = false;
   static constexpr int EPI_BYTES = 0;   // fp32 rows are stored straight from registers
   using OutT = float;
 };
@@ -206,7 +206,7 @@ using CfgTf32x3N64 = CfgTf32x3T<64, 4>;
 // bf16 operands, fp32 TMEM accumulation; BN = 128 or 64 (N % 128 != 0, e.g.
 // 64-channel convolutions), output bf16 (activations) or fp32 (split-K
 // weight-gradient partials, logits)
-template <int BN_, class OutT_, bool MN_ = false>
+template <int BN_, class OutT_, bool A_MN_ = false, bool B_MN_ = false>
 struct CfgBf16T {
   static constexpr int KIND = 1;
   static constexpr int BM = 128, BN = BN_;
@@ -226,10 +226,10 @@ struct CfgBf16T {
   // promotion chunks at the 1e-2 bf16 budget): 2 x BN columns, leaving TMEM
   // for co-resident high-priority tensor-core kernels
   static constexpr int TMEM_COLS = 2 * BN;
-  // MN-major operands: A given as A^T [K, M] and B as B^T [K, N] (M / N
+  // MN-major operands: A given as A^T [K, M] and/or B as B^T [K, N] (M / N
   // contiguous) -- the weight gradient dW = dY^T . X reads both activations
-  // as stored, no transposes
-  static constexpr bool MN = MN_;
+  // as stored (no transposes); P . V and dY . W read V / W as stored
+  static constexpr bool A_MN = A_MN_, B_MN = B_MN_;
   using OutT = OutT_;
   // bf16 output: each epilogue warp stages its 32 x BN tile rows in shared
   // memory (XOR-swizzled 16 B chunks) and writes whole rows, coalesced
@@ -239,8 +239,14 @@ using CfgBf16 = CfgBf16T<128, __nv_bfloat16>;
 using CfgBf16N64 = CfgBf16T<64, __nv_bfloat16>;
 using CfgBf16F32 = CfgBf16T<128, float>;
 using CfgBf16F32N64 = CfgBf16T<64, float>;
-using CfgBf16MN = CfgBf16T<128, float, true>;
-using CfgBf16MNN64 = CfgBf16T<64, float, true>;
+using CfgBf16MN = CfgBf16T<128, float, true, true>;
+using CfgBf16MNN64 = CfgBf16T<64, float, true, true>;
+using CfgBf16KMN = CfgBf16T<128, __nv_bfloat16, false, true>;
+using CfgBf16KMNN64 = CfgBf16T<64, __nv_bfloat16, false, true>;
+using CfgBf16F32KMN = CfgBf16T<128, float, false, true>;
+using CfgBf16F32KMNN64 = CfgBf16T<64, float, false, true>;
+using CfgBf16MNb = CfgBf16T<128, __nv_bfloat16, true, true>;
+using CfgBf16MNbN64 = CfgBf16T<64, __nv_bfloat16, true, true>;
 
 constexpr int GROUP_M = 8;
 // producer warp, MMA warp, 8 epilogue warps: two per TMEM lane quarter, each
@@ -269,7 +275,9 @@ struct alignas(64) GemmParams {
   int splits;                   // split-K factor: logical block = (split, tile)
   int kb_per_split;             // k-blocks per split
   int tpb;                      // tiles per logical block
-  long long total_tiles;        // tiles * splits
+  long long total_tiles;        // tiles * splits * batches
+  int batches, hdiv;            // batched layout (tally_gemm_layout): z = (zb, zh)
+  long long off[6][2];          // (row, col) origins of A, B, C: [a_row, a_col, b_row, b_col, c_row, c_col]
 };
 
 __device__ __forceinline__ void tile_coords(long long t, const GemmParams& p, int& mb, int& nb) {
@@ -287,17 +295,25 @@ __device__ __forceinline__ void tile_coords(long long t, const GemmParams& p, in
 // split-major: t = split * tiles + tile; split s covers k-blocks
 // [s * kb_per_split, min(KB, (s + 1) * kb_per_split)).
 struct TileWork {
-  int mb, nb, split, kbeg, kend, nch;
+  int mb, nb, split, kbeg, kend, nch, z;
 };
 __device__ __forceinline__ TileWork tile_work(long long t, const GemmParams& p, int KB) {
   TileWork w;
   const long long tiles = (long long)p.tiles_m * p.tiles_n;
+  const long long per_batch = tiles * p.splits;
+  w.z = (int)(t / per_batch);
+  t -= (long long)w.z * per_batch;
   w.split = (int)(t / tiles);
   tile_coords(t - (long long)w.split * tiles, p, w.mb, w.nb);
   w.kbeg = w.split * p.kb_per_split;
   w.kend = min(KB, w.kbeg + p.kb_per_split);
   w.nch = (w.kend - w.kbeg + p.kchunk - 1) / p.kchunk;
   return w;
+}
+
+// origin offset (elements) of operand coordinate `which` for batch z
+__device__ __forceinline__ int goff(const GemmParams& p, int which, int z) {
+  return (int)(p.off[which][0] * (z / p.hdiv) + p.off[which][1] * (z % p.hdiv));
 }
 
 template <class Cfg, int MODE, class ShapeArgs>
@@ -457,17 +473,25 @@ __global__ void __launch_bounds__(kThreads, Cfg::KIND == 1 ? 2 : 1) k_gemm(const
               tma_load_2d(base + Cfg::A_BYTES, &p.a_lo, &full[st], kx, mb * Cfg::BM);
               tma_load_2d(base + 2 * Cfg::A_BYTES, &p.b_hi, &full[st], kx, nb * Cfg::BN);
               tma_load_2d(base + 2 * Cfg::A_BYTES + Cfg::B_BYTES, &p.b_lo, &full[st], kx, nb * Cfg::BN);
-            } else if constexpr (Cfg::MN) {
-              // boxes of 64 MN-elements x BK K-rows, 8 KB each
-#pragma unroll
-              for (int h = 0; h < Cfg::BM / 64; ++h)
-                tma_load_2d(base + h * 8192, &p.a_hi, &full[st], mb * Cfg::BM + h * 64, kb * Cfg::BK);
-#pragma unroll
-              for (int h = 0; h < Cfg::BN / 64; ++h)
-                tma_load_2d(base + Cfg::A_BYTES + h * 8192, &p.b_hi, &full[st], nb * Cfg::BN + h * 64, kb * Cfg::BK);
             } else {
-              tma_load_2d(base, &p.a_hi, &full[st], kx, mb * Cfg::BM);
-              tma_load_2d(base + Cfg::A_BYTES, &p.b_hi, &full[st], kx, nb * Cfg::BN);
+              // (batched layouts: every operand's origin moves with the batch)
+              const int ar = goff(p, 0, w.z), ac = goff(p, 1, w.z), br = goff(p, 2, w.z), bc = goff(p, 3, w.z);
+              if constexpr (Cfg::A_MN) {
+                // boxes of 64 M-elements x BK K-rows, 8 KB each
+#pragma unroll
+                for (int h = 0; h < Cfg::BM / 64; ++h)
+                  tma_load_2d(base + h * 8192, &p.a_hi, &full[st], mb * Cfg::BM + h * 64 + ac, kb * Cfg::BK + ar);
+              } else {
+                tma_load_2d(base, &p.a_hi, &full[st], kx + ac, mb * Cfg::BM + ar);
+              }
+              if constexpr (Cfg::B_MN) {
+#pragma unroll
+                for (int h = 0; h < Cfg::BN / 64; ++h)
+                  tma_load_2d(base + Cfg::A_BYTES + h * 8192, &p.b_hi, &full[st], nb * Cfg::BN + h * 64 + bc,
+                              kb * Cfg::BK + br);
+              } else {
+                tma_load_2d(base + Cfg::A_BYTES, &p.b_hi, &full[st], kx + bc, nb * Cfg::BN + br);
+              }
             }
           }
         }
@@ -480,7 +504,7 @@ __global__ void __launch_bounds__(kThreads, Cfg::KIND == 1 ? 2 : 1) k_gemm(const
       // The tile's K range is cut into chunks of p.kchunk k-blocks; each chunk
       // accumulates into one of two TMEM buffers and is promoted to an fp32
       // running total by the epilogue (bounded tensor-core accumulation chains).
-      constexpr uint32_t idesc = make_idesc<Cfg::KIND, Cfg::BN, Cfg::MN>();
+      constexpr uint32_t idesc = make_idesc<Cfg::KIND, Cfg::BN, Cfg::A_MN, Cfg::B_MN>();
       uint32_t it = 0, ci = 0;
       for (int i = 0;; ++i) {
         const int j = i % kSlots;
@@ -522,11 +546,13 @@ __global__ void __launch_bounds__(kThreads, Cfg::KIND == 1 ? 2 : 1) k_gemm(const
                 umma<0>(d, alo, bhi, idesc, first);   // small terms first
                 umma<0>(d, ahi, blo, idesc, 1);
                 umma<0>(d, ahi, bhi, idesc, 1);
-              } else if constexpr (Cfg::MN) {
-                // UMMA_K = 16 K-rows = two 8-row groups = 2048 B per step
-                umma<1>(d, smem_desc_mn(base + k * 2048), smem_desc_mn(base + Cfg::A_BYTES + k * 2048), idesc, first);
               } else {
-                umma<1>(d, smem_desc(base + koff), smem_desc(base + Cfg::A_BYTES + koff), idesc, first);
+                // MN-major: UMMA_K = 16 K-rows = two 8-row groups = 2048 B per step;
+                // K-major: 32 B per step inside the 128 B swizzle atom
+                const uint64_t da = Cfg::A_MN ? smem_desc_mn(base + k * 2048) : smem_desc(base + koff);
+                const uint64_t db = Cfg::B_MN ? smem_desc_mn(base + Cfg::A_BYTES + k * 2048)
+                                              : smem_desc(base + Cfg::A_BYTES + koff);
+                umma<1>(d, da, db, idesc, first);
               }
             }
             umma_commit(&empty[st]);   // frees the stage once these MMAs retire
@@ -560,8 +586,9 @@ __global__ void __launch_bounds__(kThreads, Cfg::KIND == 1 ? 2 : 1) k_gemm(const
       const TileWork w = tile_work(t, p, KB);
       const int row = w.mb * Cfg::BM + q * 32 + lane;
       const bool row_ok = row < p.m;   // M tail: TMA zero-fills the rows past M, stores skip them
+      const int cr = goff(p, 4, w.z), cc = goff(p, 5, w.z);
       typename Cfg::OutT* crow = reinterpret_cast<typename Cfg::OutT*>(p.c) + (size_t)w.split * p.split_stride +
-                                 (size_t)(row_ok ? row : 0) * p.ldc + (size_t)w.nb * Cfg::BN;
+                                 (size_t)(cr + (row_ok ? row : 0)) * p.ldc + (size_t)(cc + w.nb * Cfg::BN);
       const uint32_t lane_base = tmem_base + ((uint32_t)(q * 32) << 16);
       for (int c = c0; c < w.nch; ++c, ++ci) {
         const int acc = ci & 1;
@@ -659,7 +686,7 @@ __global__ void __launch_bounds__(kThreads, Cfg::KIND == 1 ? 2 : 1) k_gemm(const
             constexpr int CPR = Cfg::BN / 8;   // 16 B chunks per row
             const unsigned char* sbase = epi_smem + (size_t)q * (32 * Cfg::BN * 2);
             const long long row0 = (long long)w.mb * Cfg::BM + q * 32;
-            __nv_bfloat16* cbase = reinterpret_cast<__nv_bfloat16*>(p.c) + (size_t)w.nb * Cfg::BN;
+            __nv_bfloat16* cbase = reinterpret_cast<__nv_bfloat16*>(p.c) + (size_t)cr * p.ldc + (size_t)(cc + w.nb * Cfg::BN);
 #pragma unroll 4
             for (int i2 = half * 16 * CPR + lane; i2 < (half + 1) * 16 * CPR; i2 += 32) {
               const int rr = i2 / CPR, ch = i2 % CPR;
@@ -744,11 +771,11 @@ static EncodeTiledFn encode_fn() {
 
 // rows x cols (K innermost) row-major matrix, box = box_rows x 128 bytes, 128 B swizzle
 static int make_map(CUtensorMap* m, const void* ptr, CUtensorMapDataType dt, int esz, long long rows,
-                    long long cols, int box_rows) {
+                    long long cols, int box_rows, long long ld = 0) {
   EncodeTiledFn enc = encode_fn();
   if (!enc) { set_error("cuTensorMapEncodeTiled unavailable"); return TALLY_ENODEV; }
   cuuint64_t dims[2] = {(cuuint64_t)cols, (cuuint64_t)rows};
-  cuuint64_t strides[1] = {(cuuint64_t)cols * esz};
+  cuuint64_t strides[1] = {(cuuint64_t)(ld > 0 ? ld : cols) * esz};
   cuuint32_t box[2] = {(cuuint32_t)(128 / esz), (cuuint32_t)box_rows};
   cuuint32_t estr[2] = {1, 1};
   CUresult r = enc(m, dt, 2, const_cast<void*>(ptr), dims, strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
@@ -768,7 +795,7 @@ static int bind_gemm(const tally_kernel_args* a, Instance* inst, bool split) {
   // stay 16-byte aligned for the tensor map)
   const bool m_ok = Cfg::KIND == 1 ? true : (M % Cfg::BM == 0);
   // (MN-major: the tensor-map rows are K, the contiguous dims M and N)
-  const bool k_ok = Cfg::MN ? (M % 8 == 0) : Cfg::KIND == 1 ? (K % 8 == 0) : (K % Cfg::BK == 0);
+  const bool k_ok = (Cfg::A_MN || Cfg::B_MN) ? (M % 8 == 0 && K % 8 == 0) : Cfg::KIND == 1 ? (K % 8 == 0) : (K % Cfg::BK == 0);
   if (M < 1 || N < 1 || K < 1 || !m_ok || N % Cfg::BN || !k_ok) {
     set_error("gemm: need M %s, N %% %d == 0, K %s (got %lld %lld %lld)",
               Cfg::KIND == 1 ? ">= 1" : "% 128 == 0", Cfg::BN, Cfg::KIND == 1 ? "% 8 == 0" : "% 32 == 0", M, N, K);
@@ -793,21 +820,28 @@ static int bind_gemm(const tally_kernel_args* a, Instance* inst, bool split) {
     if ((rc = make_map(&p.b_hi, a->ptr[2], dt, Cfg::ESZ, N, K, Cfg::BN))) return rc;
     if ((rc = make_map(&p.b_lo, a->ptr[3], dt, Cfg::ESZ, N, K, Cfg::BN))) return rc;
     p.c = a->ptr[4];
-  } else if (Cfg::MN) {   // ptr: A^T [K, M], B^T [K, N], C; boxes of 64 MN x BK K-rows
-    if ((rc = make_map(&p.a_hi, a->ptr[0], dt, Cfg::ESZ, K, M, Cfg::BK))) return rc;
-    if ((rc = make_map(&p.b_hi, a->ptr[1], dt, Cfg::ESZ, K, N, Cfg::BK))) return rc;
+  } else {       // ptr: A, B, C [, layout]; MN-major operand = its transpose stored row-major
+    const tally_gemm_layout* L = static_cast<const tally_gemm_layout*>(a->ptr[3]);
+    const long long ar = L ? L->a_rows : (Cfg::A_MN ? K : M), acl = L ? L->a_cols : (Cfg::A_MN ? M : K);
+    const long long br = L ? L->b_rows : (Cfg::B_MN ? K : N), bcl = L ? L->b_cols : (Cfg::B_MN ? N : K);
+    if ((rc = make_map(&p.a_hi, a->ptr[0], dt, Cfg::ESZ, ar, acl, Cfg::A_MN ? Cfg::BK : Cfg::BM, L ? L->a_ld : 0))) return rc;
+    if ((rc = make_map(&p.b_hi, a->ptr[1], dt, Cfg::ESZ, br, bcl, Cfg::B_MN ? Cfg::BK : Cfg::BN, L ? L->b_ld : 0))) return rc;
     p.c = a->ptr[2];
-  } else {       // ptr: A, B, C
-    if ((rc = make_map(&p.a_hi, a->ptr[0], dt, Cfg::ESZ, M, K, Cfg::BM))) return rc;
-    if ((rc = make_map(&p.b_hi, a->ptr[1], dt, Cfg::ESZ, N, K, Cfg::BN))) return rc;
-    p.c = a->ptr[2];
+    if (L) {
+      if (L->batches < 1 || L->hdiv < 1 || L->ldc < N) { set_error("gemm layout: batches, hdiv >= 1, ldc >= N"); return TALLY_EINVAL; }
+      const long long* offs[6] = {L->a_row_off, L->a_col_off, L->b_row_off, L->b_col_off, L->c_row_off, L->c_col_off};
+      for (int w = 0; w < 6; ++w) { p.off[w][0] = offs[w][0]; p.off[w][1] = offs[w][1]; }
+    }
   }
   p.m = (int)M;
   p.n = (int)N;
   p.k = (int)K;
   p.tiles_m = (int)((M + Cfg::BM - 1) / Cfg::BM);
   p.tiles_n = (int)(N / Cfg::BN);
-  p.ldc = N;
+  const tally_gemm_layout* lay = split ? nullptr : static_cast<const tally_gemm_layout*>(a->ptr[3]);
+  p.batches = lay ? lay->batches : 1;
+  p.hdiv = lay ? lay->hdiv : 1;
+  p.ldc = lay ? lay->ldc : N;
   p.split_stride = M * N;
   p.splits = (int)splits;
   p.kb_per_split = (int)((KBlocks + splits - 1) / splits);
@@ -824,7 +858,7 @@ static int bind_gemm(const tally_kernel_args* a, Instance* inst, bool split) {
   // an untransformed CTA pipelines 4 tiles behind one prologue and a PTB
   // claim covers ~4 us of work; longer tiles are one logical block each
   p.tpb = (Cfg::KIND == 1 && p.kb_per_split <= 2) ? 4 : 1;
-  p.total_tiles = (long long)p.tiles_m * p.tiles_n * p.splits;
+  p.total_tiles = (long long)p.tiles_m * p.tiles_n * p.splits * p.batches;
   p.resume = nullptr;
   // i[3] = 1: block-granular preemption only (no resume ring)
   if (Cfg::KIND == 0 && a->i[3] == 0) {
@@ -841,9 +875,9 @@ static int bind_gemm(const tally_kernel_args* a, Instance* inst, bool split) {
   inst->grid = make_uint3((unsigned)((p.total_tiles + p.tpb - 1) / p.tpb), 1, 1);
   inst->threads = gemm::kThreads;
   inst->smem = gemm::smem_bytes<Cfg>();
-  inst->alg_flops = 2.0 * (double)M * (double)N * (double)K;
-  inst->alg_bytes = (double)Cfg::ESZ * (double)(M * K + N * K) * (split ? 2.0 : 1.0) +
-                    (double)sizeof(typename Cfg::OutT) * (double)(M * N) * (double)splits;
+  inst->alg_flops = 2.0 * (double)M * (double)N * (double)K * (double)p.batches;
+  inst->alg_bytes = ((double)Cfg::ESZ * (double)(M * K + N * K) * (split ? 2.0 : 1.0) +
+                     (double)sizeof(typename Cfg::OutT) * (double)(M * N) * (double)splits) * (double)p.batches;
   return TALLY_OK;
 }
 
@@ -908,7 +942,7 @@ static KernelKind gemm_kind(const char* name, int (*bind)(const tally_kernel_arg
 }
 
 int register_gemm_kernels(KernelKind* out, int cap) {
-  if (cap < 9) return 0;
+  if (cap < 15) return 0;
   out[0] = gemm_kind<gemm::CfgTf32x3>("sgemm_tf32x3", bind_sgemm);
   out[1] = gemm_kind<gemm::CfgBf16>("gemm_bf16", bind_bf16<gemm::CfgBf16>);
   out[3] = gemm_kind<gemm::CfgTf32x3N64>("sgemm_tf32x3_n64", bind_sgemm_n64);
@@ -917,6 +951,12 @@ int register_gemm_kernels(KernelKind* out, int cap) {
   out[6] = gemm_kind<gemm::CfgBf16F32N64>("gemm_bf16f32_n64", bind_bf16<gemm::CfgBf16F32N64>);
   out[7] = gemm_kind<gemm::CfgBf16MN>("gemm_bf16f32_mn", bind_bf16<gemm::CfgBf16MN>);
   out[8] = gemm_kind<gemm::CfgBf16MNN64>("gemm_bf16f32_mn_n64", bind_bf16<gemm::CfgBf16MNN64>);
+  out[9] = gemm_kind<gemm::CfgBf16KMN>("gemm_bf16_kmn", bind_bf16<gemm::CfgBf16KMN>);
+  out[10] = gemm_kind<gemm::CfgBf16KMNN64>("gemm_bf16_kmn_n64", bind_bf16<gemm::CfgBf16KMNN64>);
+  out[11] = gemm_kind<gemm::CfgBf16F32KMN>("gemm_bf16f32_kmn", bind_bf16<gemm::CfgBf16F32KMN>);
+  out[12] = gemm_kind<gemm::CfgBf16F32KMNN64>("gemm_bf16f32_kmn_n64", bind_bf16<gemm::CfgBf16F32KMNN64>);
+  out[13] = gemm_kind<gemm::CfgBf16MNb>("gemm_bf16_mn", bind_bf16<gemm::CfgBf16MNb>);
+  out[14] = gemm_kind<gemm::CfgBf16MNbN64>("gemm_bf16_mn_n64", bind_bf16<gemm::CfgBf16MNbN64>);
   KernelKind k{};
   k.name = "split_tf32";
   k.fn_original = reinterpret_cast<const void*>(&k_original<gemm::SplitTf32>);
@@ -924,7 +964,7 @@ int register_gemm_kernels(KernelKind* out, int cap) {
   k.fn_ptb = reinterpret_cast<const void*>(&k_ptb<gemm::SplitTf32>);
   k.bind = bind_split;
   out[2] = k;
-  return 9;
+  return 15;
 }
 
 }  // namespace tally

@@ -338,6 +338,37 @@ def gemm(A, B, C, splits: int = 1) -> DeviceKernel:
     return DeviceKernel(kind, (A, B, C), (M, N, K, 0, splits))
 
 
+def gemm_ex(A, B, Cout, M, N, K, a_mn=False, b_mn=False, splits=1, batches=1, hdiv=1,
+            a_off=((0, 0), (0, 0)), b_off=((0, 0), (0, 0)), c_off=((0, 0), (0, 0))) -> DeviceKernel:
+    """General bf16 GEMM on tcgen05: per batch, C[M,N] = A . B^T with A
+    K-major (A[M,K] row-major) or MN-major (stored as A^T [K,M]), likewise B
+    ([N,K] or [K,N]).  ``A``, ``B``, ``Cout`` are 2-D row-major views (any
+    column offset and row pitch, e.g. one head's columns of a fused QKV
+    activation).  Batch z = (zb, zh) = (z // hdiv, z % hdiv) moves each
+    operand's (row, col) origin by off[0] * zb + off[1] * zh, with
+    ``a_off = ((row_per_zb, row_per_zh), (col_per_zb, col_per_zh))``.
+    bf16 or fp32 output; fp32 allows split-K."""
+    import torch
+    kinds = {(False, False): "", (True, True): "_mn", (False, True): "_kmn"}
+    if (a_mn, b_mn) not in kinds:
+        raise ValueError("gemm_ex: an MN-major A needs an MN-major B")
+    for t in (A, B, Cout):
+        if t.dim() != 2 or t.stride(1) != 1:
+            raise ValueError("gemm_ex: operands must be 2-D row-major views (unit column stride)")
+    out = "f32" if Cout.dtype == torch.float32 else ""
+    kind = "gemm_bf16" + out + kinds[(a_mn, b_mn)] + ("" if N % 128 == 0 else "_n64")
+    lay = _lib.c_gemm_layout()
+    lay.a_rows, lay.a_cols, lay.a_ld = A.shape[0], A.shape[1], A.stride(0)
+    lay.b_rows, lay.b_cols, lay.b_ld = B.shape[0], B.shape[1], B.stride(0)
+    lay.ldc = Cout.stride(0)
+    lay.batches, lay.hdiv = batches, hdiv
+    for name, (r, c) in (("a", a_off), ("b", b_off), ("c", c_off)):
+        getattr(lay, name + "_row_off")[0], getattr(lay, name + "_row_off")[1] = r
+        getattr(lay, name + "_col_off")[0], getattr(lay, name + "_col_off")[1] = c
+    return DeviceKernel(kind, (A.data_ptr(), B.data_ptr(), Cout.data_ptr(), C.addressof(lay)),
+                        (M, N, K, 0, splits), keep=(A, B, Cout, lay))
+
+
 def gemm_mn(At, Bt, C, splits: int = 1) -> DeviceKernel:
     """C[M,N] (fp32) = At[K,M]^T . Bt[K,N] with both operands MN-major (as
     stored: M / N contiguous) -- the weight gradient dW = dY^T . X of a

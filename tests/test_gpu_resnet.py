@@ -465,3 +465,50 @@ def test_l2_persist_and_prefetch_api(env):
     tuned.kernel.original(hs).wait()
     assert tuned.l2_nodes > 50
     assert torch.equal(plain.out, tuned.out)
+
+
+# ------------------------------------------------------------------ batched / mixed-major GEMMs (attention)
+def test_gemm_ex_attention_shapes(env):
+    """Batched GEMMs over (sequence, head) blocks of a fused QKV activation,
+    all operands read in place: S = Q K^T (K-major, K-major), O = P V
+    (K-major A, MN-major B), dK = dS^T Q (MN-major, MN-major), in all shapes."""
+    P, kernels, stream = env
+    B_, T, H, D = 2, 256, 4, 64
+    HD = H * D
+    qkv = rnd(B_ * T, 3 * HD, seed=31)
+    q, k, v = qkv[:, :HD], qkv[:, HD:2 * HD], qkv[:, 2 * HD:]
+    qh = q.float().view(B_, T, H, D).permute(0, 2, 1, 3)
+    kh = k.float().view(B_, T, H, D).permute(0, 2, 1, 3)
+    vh = v.float().view(B_, T, H, D).permute(0, 2, 1, 3)
+    # S = Q K^T  -> S[(b, h), T, T]
+    S = torch.zeros(B_ * H * T, T, device="cuda")
+    dk = kernels.gemm_ex(q, k, S, T, T, D, batches=B_ * H, hdiv=H,
+                         a_off=((T, 0), (0, D)), b_off=((T, 0), (0, D)), c_off=((H * T, T), (0, 0)))
+    (got,) = shapes(P, dk, stream, [S])
+    ref = (qh @ kh.transpose(-1, -2)).reshape(B_ * H * T, T)
+    assert nerr(got, ref) < 1e-4
+    # O = P V  -> O[B*T, HD] (head h at columns h*D)
+    Pm = rnd(B_ * H * T, T, seed=32)
+    O = torch.zeros(B_ * T, HD, dtype=torch.bfloat16, device="cuda")
+    dk = kernels.gemm_ex(Pm, v, O, T, D, T, b_mn=True, batches=B_ * H, hdiv=H,
+                         a_off=((H * T, T), (0, 0)), b_off=((T, 0), (0, D)), c_off=((T, 0), (0, D)))
+    (got,) = shapes(P, dk, stream, [O])
+    ref = (Pm.float().view(B_, H, T, T) @ vh).permute(0, 2, 1, 3).reshape(B_ * T, HD)
+    assert nerr(got, ref) < 1e-2
+    # dK = dS^T Q -> dK[B*T, HD]
+    dS = rnd(B_ * H * T, T, seed=33)
+    dK = torch.zeros(B_ * T, HD, dtype=torch.bfloat16, device="cuda")
+    dk = kernels.gemm_ex(dS, q, dK, T, D, T, a_mn=True, b_mn=True, batches=B_ * H, hdiv=H,
+                         a_off=((H * T, T), (0, 0)), b_off=((T, 0), (0, D)), c_off=((T, 0), (0, D)))
+    (got,) = shapes(P, dk, stream, [dK])
+    ref = (dS.float().view(B_, H, T, T).transpose(-1, -2) @ qh).permute(0, 2, 1, 3).reshape(B_ * T, HD)
+    assert nerr(got, ref) < 1e-2
+
+
+def test_gemm_ex_linear_backward_input(env):
+    """dX = dY . W with W [out, in] read as stored (MN-major B)."""
+    P, kernels, stream = env
+    dY, W = rnd(1000, 768, seed=34), rnd(768, 3072, seed=35)
+    dX = torch.zeros(1000, 3072, dtype=torch.bfloat16, device="cuda")
+    (got,) = shapes(P, kernels.gemm_ex(dY, W, dX, 1000, 3072, 768, b_mn=True), stream, [dX])
+    assert nerr(got, dY.float() @ W.float()) < 1e-2
