@@ -27,7 +27,7 @@ COMMON = ["-O3", "-std=c++17", "-lineinfo", "-Xcompiler", "-fPIC,-Wall,-Wno-form
           "-I", os.path.join(ROOT, "include"), "-I", CSRC]
 CU_FLAGS = ARCH + COMMON + ["-Xptxas", "-warn-spills", "--expt-relaxed-constexpr"]
 
-SOURCES = ["runtime.cu", "kernels_basic.cu", "kernels_gemm.cu", "kernels_nn.cu", "runner.cpp", "cuda_device.cpp"]
+SOURCES = ["runtime.cu", "kernels_basic.cu", "kernels_gemm.cu", "kernels_nn.cu", "kernels_tf.cu", "runner.cpp", "cuda_device.cpp"]
 HEADERS = ["tally_device.cuh", "registry.h", "runtime.h", "runner.h", "gemm_sm100.cuh"]
 
 

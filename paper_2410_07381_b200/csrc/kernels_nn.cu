@@ -224,7 +224,11 @@ struct Transpose {
 // has a fixed order), exactly-once under every launch shape (the counters
 // count logical blocks, and survive a PTB park / resume), and no separate
 // finalisation launch.
-template <int MODE>   // 0: forward statistics, 1: backward statistics
+// MODE 0: forward statistics; 1: backward statistics (per-channel mean /
+// invstd); 2: column sums over rows for LayerNorm / bias gradients -- s1 = sum g,
+// s2 = sum g * (x - mean[row]) * rstd[row] (x optional), finalised as
+// dbeta = s1, dgamma = s2.
+template <int MODE>
 struct BnStats {
   static constexpr int kThreads = 256;
   static constexpr int kMinBlocks = MODE == 0 ? 4 : 2;   // register cap: enough bytes in flight per SM
@@ -309,8 +313,8 @@ struct BnStats {
         ok[u] = r < rend;
         const long long off = r * cvec + (c >> 3);
         if (ok[u]) {
-          xv[u] = ld16(p.x + off);
-          if constexpr (MODE == 1) {
+          if (MODE != 2 || p.x) xv[u] = ld16(p.x + off);
+          if constexpr (MODE >= 1) {
             gv[u] = ld16(p.g + off);
             if (p.g2) g2v[u] = ld16(p.g2 + off);
             if (p.y) yv[u] = ld16(p.y + off);
@@ -321,6 +325,26 @@ struct BnStats {
       for (int u = 0; u < kRows; ++u) {
         if (!ok[u]) continue;
         float x[8];
+        if constexpr (MODE == 2) {
+          float g[8];
+          unpack8(gv[u], g);
+          if (p.g2) {
+            float t[8];
+            unpack8(g2v[u], t);
+#pragma unroll
+            for (int e = 0; e < 8; ++e) g[e] += t[e];
+          }
+#pragma unroll
+          for (int e = 0; e < 8; ++e) s1[e] += g[e];
+          if (p.x) {
+            const long long r = r0 + (long long)u * rl;
+            const float mr = p.mean[r], rr = p.invstd[r];
+            unpack8(xv[u], x);
+#pragma unroll
+            for (int e = 0; e < 8; ++e) s2[e] += g[e] * ((x[e] - mr) * rr);
+          }
+          continue;
+        }
         unpack8(xv[u], x);
         if constexpr (MODE == 0) {
 #pragma unroll
@@ -402,6 +426,9 @@ struct BnStats {
             const float sc = p.gamma[ch] * isd;
             p.scale_shift[ch] = sc;
             p.scale_shift[p.C + ch] = p.beta[ch] - m * sc;
+          } else if constexpr (MODE == 2) {
+            p.dbeta[ch] = a;
+            if (p.dgamma) p.dgamma[ch] = b;
           } else {
             p.dbeta[ch] = a;
             p.dgamma[ch] = b;
@@ -502,10 +529,11 @@ struct BnAct {
     const uint4* x;
     const uint4* res;   // optional residual added before the activation
     uint4* y;
-    const float* scale;
+    const float* scale;   // optional (1)
     const float* shift;
+    uint4* pre;           // optional: the pre-activation values (GELU backward input)
     long long nvec;
-    int C, relu;
+    int C, relu;          // activation: 0 none, 1 ReLU, 2 GELU (tanh approximation)
   };
   static __device__ __forceinline__ void run(const Params& p, uint3 bidx, uint3, char*) {
     const int cv = p.C >> 3;
@@ -526,23 +554,35 @@ struct BnAct {
       const int c = (int)(v % cv) << 3;
       float x[8];
       unpack8(xv[u], x);
-      const float4 s0 = __ldg(reinterpret_cast<const float4*>(p.scale + c));
-      const float4 s1 = __ldg(reinterpret_cast<const float4*>(p.scale + c + 4));
       const float4 h0 = __ldg(reinterpret_cast<const float4*>(p.shift + c));
       const float4 h1 = __ldg(reinterpret_cast<const float4*>(p.shift + c + 4));
-      const float sc[8] = {s0.x, s0.y, s0.z, s0.w, s1.x, s1.y, s1.z, s1.w};
       const float sh[8] = {h0.x, h0.y, h0.z, h0.w, h1.x, h1.y, h1.z, h1.w};
+      if (p.scale) {
+        const float4 s0 = __ldg(reinterpret_cast<const float4*>(p.scale + c));
+        const float4 s1 = __ldg(reinterpret_cast<const float4*>(p.scale + c + 4));
+        const float sc[8] = {s0.x, s0.y, s0.z, s0.w, s1.x, s1.y, s1.z, s1.w};
 #pragma unroll
-      for (int e = 0; e < 8; ++e) x[e] = x[e] * sc[e] + sh[e];
+        for (int e = 0; e < 8; ++e) x[e] = x[e] * sc[e] + sh[e];
+      } else {
+#pragma unroll
+        for (int e = 0; e < 8; ++e) x[e] += sh[e];
+      }
       if (p.res) {
         float r[8];
         unpack8(rv[u], r);
 #pragma unroll
         for (int e = 0; e < 8; ++e) x[e] += r[e];
       }
-      if (p.relu) {
+      if (p.pre) st16(p.pre + v, pack8(x));
+      if (p.relu == 1) {
 #pragma unroll
         for (int e = 0; e < 8; ++e) x[e] = fmaxf(x[e], 0.f);
+      } else if (p.relu == 2) {
+#pragma unroll
+        for (int e = 0; e < 8; ++e) {
+          const float u = 0.7978845608028654f * (x[e] + 0.044715f * x[e] * x[e] * x[e]);
+          x[e] = 0.5f * x[e] * (1.f + tanhf(u));
+        }
       }
       st16(p.y + v, pack8(x));
     }
@@ -813,7 +853,7 @@ struct SoftmaxXent {   // one row per logical block
       float d = 0.f;
       if (j < p.ncls) d = (__expf(z[j] + p.bias[j] - m) / s - (j == lab ? 1.f : 0.f)) * inv_b;
       p.dl[(long long)b * p.Npad + j] = __float2bfloat16_rn(d);
-      p.dl32[(long long)b * p.Npad + j] = d;
+      if (p.dl32) p.dl32[(long long)b * p.Npad + j] = d;
     }
     if (threadIdx.x == 0) p.loss[b] = logf(s) + m - (z[lab] + p.bias[lab]);
     __syncthreads();
@@ -879,6 +919,7 @@ struct SgdSeg {
   __nv_bfloat16* wt;      // optional bf16 transposed copy [cols, rows]
   int rows, cols;
   int chunk;              // elements per logical block (64..1024, power of 2)
+  int zero_from;          // >= 0: zero gradient slices [zero_from, S) after reading (atomic accumulators)
 };
 
 struct SgdUpdate {
@@ -913,6 +954,9 @@ struct SgdUpdate {
       const float4 a = ld4(s.grad + (long long)j * s.gstride + i);
       g.x += a.x; g.y += a.y; g.z += a.z; g.w += a.w;
     }
+    if (s.zero_from >= 0)
+      for (int z = s.zero_from; z < s.S; ++z)
+        *reinterpret_cast<float4*>(const_cast<float*>(s.grad) + (long long)z * s.gstride + i) = make_float4(0.f, 0.f, 0.f, 0.f);
     const float4 w = *reinterpret_cast<const float4*>(s.w + i);
     const float4 v = *reinterpret_cast<const float4*>(s.v + i);
     const float gw[4] = {g.x + s.wd * w.x, g.y + s.wd * w.y, g.z + s.wd * w.z, g.w + s.wd * w.w};
@@ -1052,12 +1096,13 @@ static int bind_bn_stats(const tally_kernel_args* a, Instance* inst) {
   } else {
     p.dgamma = reinterpret_cast<float*>(a->i[4]);
     p.dbeta = reinterpret_cast<float*>(a->i[5]);
-    p.coef = reinterpret_cast<float*>(a->i[6]);
+    p.coef = reinterpret_cast<float*>(a->i[6]);   // mode 1 only
   }
   const bool c_ok = p.C >= 64 && (p.C < 256 ? (256 % p.C == 0) : (p.C % 256 == 0));
-  const bool ops0 = p.mode == 0 && p.beta && p.scale_shift;
-  const bool ops1 = p.mode == 1 && p.g && p.dgamma && p.dbeta && p.coef;
-  if (!p.x || !p.part || !p.mean || !p.invstd || !p.gamma || p.P < 1 || !c_ok || p.RB < 1 || !(ops0 || ops1)) {
+  const bool ops0 = p.mode == 0 && p.x && p.mean && p.invstd && p.gamma && p.beta && p.scale_shift;
+  const bool ops1 = p.mode == 1 && p.x && p.mean && p.invstd && p.gamma && p.g && p.dgamma && p.dbeta && p.coef;
+  const bool ops2 = p.mode == 2 && p.g && p.dbeta && (!p.x || (p.mean && p.invstd && p.dgamma));
+  if (!p.part || p.P < 1 || !c_ok || p.RB < 1 || !(ops0 || ops1 || ops2)) {
     set_error("bn_stats: need x, part, mean, invstd, gamma, C in {64, 128} or a multiple of 256, and the "
               "mode 0 (beta, scale_shift) / mode 1 (g, dgamma, dbeta, coef) operands");
     return TALLY_EINVAL;
@@ -1082,7 +1127,7 @@ static int bind_bn_stats(const tally_kernel_args* a, Instance* inst) {
   inst->grid = make_uint3((unsigned)cblocks, (unsigned)p.nrb, 1);
   inst->threads = Body::kThreads;
   inst->smem = 2 * 2048 * sizeof(float) + 16;
-  const int streams = p.mode == 0 ? 1 : 2 + (p.g2 ? 1 : 0) + (p.y ? 1 : 0);
+  const int streams = p.mode == 0 ? 1 : (p.x ? 2 : 1) + (p.g2 ? 1 : 0) + (p.y ? 1 : 0);
   inst->alg_bytes = 2.0 * streams * (double)p.P * p.C + 8.0 * p.nrb * p.C;
   return TALLY_OK;
 }
@@ -1133,10 +1178,14 @@ static int bind_bn_act(const tally_kernel_args* a, Instance* inst) {
   p.y = static_cast<uint4*>(a->ptr[2]);
   p.scale = static_cast<const float*>(a->ptr[3]);
   p.shift = static_cast<const float*>(a->ptr[4]);
+  p.pre = static_cast<uint4*>(a->ptr[5]);
   const long long P = a->i[0];
   p.C = (int)a->i[1];
   p.relu = (int)a->i[2];
-  if (!p.x || !p.y || !p.scale || !p.shift || P < 1 || p.C < 8 || p.C % 8) { set_error("bn_act: need x, y, scale, shift, C %% 8 == 0"); return TALLY_EINVAL; }
+  if (!p.x || !p.y || !p.shift || P < 1 || p.C < 8 || p.C % 8 || p.relu < 0 || p.relu > 2) {
+    set_error("bn_act: need x, y, shift, C %% 8 == 0, act in {0 none, 1 relu, 2 gelu}");
+    return TALLY_EINVAL;
+  }
   p.nvec = P * (p.C / 8);
   finish(inst, p, (p.nvec + nn::kVecPerBlock - 1) / nn::kVecPerBlock, nn::BnAct::kThreads, 0,
          16.0 * p.nvec * (p.res ? 3 : 2));
@@ -1237,7 +1286,7 @@ static int bind_softmax_xent(const tally_kernel_args* a, Instance* inst) {
   p.dl = static_cast<__nv_bfloat16*>(a->ptr[4]);
   p.dl32 = static_cast<float*>(a->ptr[5]);
   p.B = (int)a->i[0]; p.Npad = (int)a->i[1]; p.ncls = (int)a->i[2];
-  if (!p.logits || !p.bias || !p.labels || !p.loss || !p.dl || !p.dl32 || p.B < 1 || p.ncls < 1 || p.Npad < p.ncls) {
+  if (!p.logits || !p.bias || !p.labels || !p.loss || !p.dl || p.B < 1 || p.ncls < 1 || p.Npad < p.ncls) {
     set_error("softmax_xent: bad arguments");
     return TALLY_EINVAL;
   }
@@ -1288,13 +1337,14 @@ static KernelKind nn_kind(const char* name, int (*bind)(const tally_kernel_args*
 }
 
 int register_nn_kernels(KernelKind* out, int cap) {
-  if (cap < 15) return 0;
+  if (cap < 16) return 0;
   int n = 0;
   out[n++] = nn_kind<nn::Im2Col>("im2col_bf16", bind_im2col);
   out[n++] = nn_kind<nn::Col2Im>("col2im_bf16", bind_col2im);
   out[n++] = nn_kind<nn::Transpose>("transpose_bf16", bind_transpose);
   out[n++] = nn_kind<nn::BnStats<0>>("bn_stats", bind_bn_stats<0>);
   out[n++] = nn_kind<nn::BnStats<1>>("bn_stats_bwd", bind_bn_stats<1>);
+  out[n++] = nn_kind<nn::BnStats<2>>("colstats", bind_bn_stats<2>);
   out[n++] = nn_kind<nn::BnFinalize>("bn_finalize", bind_bn_finalize);
   out[n++] = nn_kind<nn::BnAct>("bn_act", bind_bn_act);
   out[n++] = nn_kind<nn::BnBwd>("bn_bwd", bind_bn_bwd);

@@ -90,6 +90,7 @@ int register_basic_kernels(KernelKind* out, int cap);
 int register_gemm_kernels(KernelKind* out, int cap);
 int register_copy_kernels(KernelKind* out, int cap);
 int register_nn_kernels(KernelKind* out, int cap);
+int register_tf_kernels(KernelKind* out, int cap);
 int launch_l2_prefetch(cudaStream_t s, const void* base, long long bytes);
 
 }  // namespace tally

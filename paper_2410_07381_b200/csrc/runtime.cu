@@ -109,6 +109,7 @@ int Runtime::init(int dev, tally_gpu_info* out) {
   nkinds += register_gemm_kernels(kinds + nkinds, kMaxKinds - nkinds);
   nkinds += register_copy_kernels(kinds + nkinds, kMaxKinds - nkinds);
   nkinds += register_nn_kernels(kinds + nkinds, kMaxKinds - nkinds);
+  nkinds += register_tf_kernels(kinds + nkinds, kMaxKinds - nkinds);
   for (int k = 0; k < nkinds; ++k)
     if (kinds[k].setup) {
       int rc = kinds[k].setup();

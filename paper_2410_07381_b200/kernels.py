@@ -464,3 +464,50 @@ def sgd_update(segs, blockmap, blocks, nbytes, lr, momentum) -> DeviceKernel:
     """``segs``: device tensor of packed SgdSeg records; ``blockmap``: int32
     [blocks, 2] (segment, chunk) pairs -- see resnet.SgdTable."""
     return DeviceKernel("sgd_update", (segs, blockmap), (blocks, int(nbytes)), (lr, momentum))
+
+
+# -- best-effort transformer-training kinds (config C3, kernels_tf.cu) ---------
+def bias_act(x, y, bias, P, C, act=0, res=None, pre=None) -> DeviceKernel:
+    """y = act(x + bias [+ res]); act 0 none, 1 ReLU, 2 GELU (tanh); ``pre``
+    receives the pre-activation values (GELU backward input)."""
+    return DeviceKernel("bn_act", (x, res, y, None, bias, pre), (P, C, act))
+
+
+def colstats(g, part, P, C, rb, dbeta, dgamma=None, x=None, mean=None, rstd=None, g2=None) -> DeviceKernel:
+    """Column sums over rows, finalised in-kernel: dbeta = sum_r g (+ g2);
+    with ``x``: dgamma = sum_r g * (x - mean[r]) * rstd[r] (LayerNorm)."""
+    return DeviceKernel("colstats", (x, g, g2, None, mean, rstd, part, None),
+                        (P, C, 2, rb, _ptr(dgamma) or 0, _ptr(dbeta)),
+                        keep=tuple(t for t in (dgamma, dbeta) if t is not None))
+
+
+def layernorm_fwd(x, y, gamma, beta, mean, rstd, eps=1e-5) -> DeviceKernel:
+    rows, C = x.shape
+    return DeviceKernel("layernorm_fwd", (x, y, gamma, beta, mean, rstd), (rows, C), (eps,))
+
+
+def layernorm_bwd(dy, x, gamma, mean, rstd, dx, g2=None) -> DeviceKernel:
+    rows, C = x.shape
+    return DeviceKernel("layernorm_bwd", (dy, g2, x, gamma, mean, rstd, dx), (rows, C))
+
+
+def gelu_bwd(g, pre, dx) -> DeviceKernel:
+    return DeviceKernel("gelu_bwd", (g, pre, dx), (g.numel(),))
+
+
+def softmax_causal(s, p, T, scale) -> DeviceKernel:
+    return DeviceKernel("softmax_causal", (s, p), (s.shape[0], T), (scale,))
+
+
+def softmax_causal_bwd(p, dp, ds, T, scale) -> DeviceKernel:
+    return DeviceKernel("softmax_causal_bwd", (p, dp, ds), (p.shape[0], T), (scale,))
+
+
+def embedding_fwd(tok, wte, wpe, x, T) -> DeviceKernel:
+    rows, C = x.shape
+    return DeviceKernel("embedding_fwd", (tok, wte, wpe, x), (rows, T, C))
+
+
+def embedding_bwd(tok, dx, dwte) -> DeviceKernel:
+    rows, C = dx.shape
+    return DeviceKernel("embedding_bwd", (tok, dx, dwte), (rows, C))

@@ -110,19 +110,23 @@ class SgdTable:
     def __init__(self):
         self.segs = []
 
-    def add(self, w, v, grad, S, gstride, wd, wb=None, wt=None, rows=1, cols=1):
-        self.segs.append((w, v, grad, S, gstride, wd, wb, wt, rows, cols))
+    def add(self, w, v, grad, S, gstride, wd, wb=None, wt=None, rows=1, cols=1, zero_from=-1):
+        """``zero_from`` >= 0: gradient slices [zero_from, S) are atomic
+        accumulators, zeroed by sgd_update after it reads them."""
+        self.segs.append((w, v, grad, S, gstride, wd, wb, wt, rows, cols, zero_from))
 
     def build(self, device):
         import numpy as np
         import torch
-        dt = np.dtype({"names": ["w", "v", "grad", "n", "gstride", "S", "wd", "wb", "wt", "rows", "cols", "chunk"],
-                       "formats": ["<u8", "<u8", "<u8", "<i8", "<i8", "<i4", "<f4", "<u8", "<u8", "<i4", "<i4", "<i4"],
-                       "offsets": [0, 8, 16, 24, 32, 40, 44, 48, 56, 64, 68, 72], "itemsize": 80})
+        dt = np.dtype({"names": ["w", "v", "grad", "n", "gstride", "S", "wd", "wb", "wt", "rows", "cols", "chunk",
+                                 "zero_from"],
+                       "formats": ["<u8", "<u8", "<u8", "<i8", "<i8", "<i4", "<f4", "<u8", "<u8", "<i4", "<i4", "<i4",
+                                   "<i4"],
+                       "offsets": [0, 8, 16, 24, 32, 40, 44, 48, 56, 64, 68, 72, 76], "itemsize": 80})
         rec = np.zeros(len(self.segs), dtype=dt)
         bmap = []
         nbytes = 0
-        for i, (w, v, g, S, gs, wd, wb, wt, rows, cols) in enumerate(self.segs):
+        for i, (w, v, g, S, gs, wd, wb, wt, rows, cols, zf) in enumerate(self.segs):
             n = w.numel()
             if n % 4 or gs % 4:
                 raise ValueError("sgd_update segments need sizes and gradient strides divisible by 4")
@@ -133,7 +137,7 @@ class SgdTable:
                 chunk //= 2
             rec[i] = (w.data_ptr(), v.data_ptr(), g.data_ptr(), n, gs, S, wd,
                       wb.data_ptr() if wb is not None else 0, wt.data_ptr() if wt is not None else 0,
-                      rows, cols, chunk)
+                      rows, cols, chunk, zf)
             for c in range((n + chunk - 1) // chunk):
                 bmap.append((i, c))
             nbytes += n * (4 * S + 16 + (2 if wb is not None else 0) + (2 if wt is not None else 0))
