@@ -64,14 +64,15 @@ def parse():
     ap.add_argument("--steps", type=int, default=5)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--config", default="c2", choices=["c1", "c2"],
+    ap.add_argument("--config", default="c2", choices=["c1", "c2", "c3"],
                     help="c2 = BASELINE configs[1] (ResNet-50 HP bs=1 + ResNet-50 training bs=64); "
+                         "c3 = configs[2] (BERT-base HP seq 128 + GPT-2 small training); "
                          "c1 = the synthetic vecadd + SGEMM pair")
     ap.add_argument("--window-ms", type=float, default=None, help="default 100 (c1) / 2000 (c2)")
     ap.add_argument("--load", type=float, default=None, help="mean HP load; default 0.5 (c1) / 0.25 (c2)")
     ap.add_argument("--burst", type=float, default=4.0, help="c2: MMPP burst-rate factor")
-    ap.add_argument("--batch", type=int, default=64, help="c2: BE training batch")
-    ap.add_argument("--lr", type=float, default=0.01, help="c2: BE SGD learning rate")
+    ap.add_argument("--batch", type=int, default=None, help="BE training batch (default 64 for c2, 8 for c3)")
+    ap.add_argument("--lr", type=float, default=0.01, help="BE SGD learning rate")
     ap.add_argument("--profile-runs", type=int, default=3)
     # The paper's 0.0316 ms default.  With block-granular PTB no
     # configuration of C1's SGEMM (one 128x64 3xTF32 tile ~ 70 us) met it and
@@ -543,7 +544,17 @@ def main_c1(args):
 C2_WORKLOAD = ("C2 on B200 (BASELINE configs[1]): HP ResNet-50 inference bs=1 (torchvision, bf16, CUDA graph, "
                "unmodified) on a bursty MMPP trace + BE ResNet-50 training bs=64 (bf16, our transformable "
                "sm_100a kernel program, momentum SGD), Tally policy")
-C2_COSTS = os.path.join(ROOT, "profiles", "c2_costs.json")
+C3_WORKLOAD = ("C3 on B200 (BASELINE configs[2]): HP BERT-base inference seq=128 bs=1 (HuggingFace, bf16, CUDA "
+               "graph, unmodified) on a bursty MMPP trace + BE GPT-2 small training seq=1024 (bf16, our "
+               "transformable sm_100a kernel program with PTB preemption, momentum SGD), Tally policy")
+WORKLOADS = {"c2": C2_WORKLOAD, "c3": C3_WORKLOAD}
+
+
+def costs_path(config):
+    return os.path.join(ROOT, "profiles", f"{config}_costs.json")
+
+
+C2_COSTS = costs_path("c2")
 
 
 def c2_trace(load, hp_lat_ns, window_ns, seed, burst):
@@ -584,7 +595,7 @@ def cpu_c2_sample(costs, sample_ms, load, burst, seed, be_kernels=24, profiler=N
     horizon = int(sample_ms * 1e6)
     gap = int(hp_lat / load)
     arr = tuple(range(200_000 + seed * 1000, horizon, gap))
-    hp = pol.TaskScript("hp", gm.HIGH, (pol.KernelWork("resnet50_infer", hp_cost),), arr)
+    hp = pol.TaskScript("hp", gm.HIGH, (pol.KernelWork("hp_infer", hp_cost),), arr)
     be = pol.TaskScript("be", gm.BEST_EFFORT, tuple(works))
     # one tuner per process, as the reference shares it across runs (its
     # profiles are cached for the process lifetime, ref profiler.py:176-248)
@@ -607,7 +618,7 @@ def run_reference_arm_c2(args):
         return
     from oracle import gpu_model as gm
     from oracle import tuner as tu
-    costs = json.load(open(C2_COSTS))
+    costs = json.load(open(costs_path(args.config)))
     prof = tu.Profiler(gm.GpuSpec(148, 2048, 32), runs=1)
     vals, walls, sim_ns, evs = [], [], 0, 0
     for w in range(args.warmup):     # the first sample also profiles the BE kernels (cached after)
@@ -624,13 +635,13 @@ def run_reference_arm_c2(args):
     value = sum(vals) / len(vals) if vals else None
     sample = (f"{args.cpu_sample_ms} ms simulated C2 window per step (solo HP + co-located Tally; HP every "
               f"latency/load, BE = first 24 of the {len(costs['be'])} training-step kernels with B200-measured "
-              f"costs from profiles/c2_costs.json) on GpuSpec(148,2048,32), oracle port of tallysim, 1 thread")
+              f"costs from profiles/{args.config}_costs.json) on GpuSpec(148,2048,32), oracle port of tallysim, 1 thread")
     print(json.dumps({
         "impl": "reference", "metric": METRIC, "value": value, "unit": "%",
         "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
         "ms_per_step": 1e3 * total / max(1, args.steps), "higher_is_better": False,
         "scaling": "weak", "vs_baseline": None, "dtype": "int64 (ns event times)",
-        "data": "synthetic", "config": {"workload": C2_WORKLOAD + " -- simulated by the CPU reference",
+        "data": "synthetic", "config": {"workload": WORKLOADS[args.config] + " -- simulated by the CPU reference",
                                         "load": args.load, "burst_factor": args.burst},
         "cpu_baseline": {"value": value, "unit": "%", "cores": 1, "kind": "port", "sample": sample,
                          "sim_ms_per_wall_s": sim_ns / 1e6 / sum(walls), "events_per_s": evs / sum(walls)},
@@ -678,7 +689,9 @@ def drain_us(res_list):
             if r["parked"] and r["gt_first_stop"] and r["gt_last_exit"]]
 
 
-def main_c2(args):
+def main_colocate(args):
+    """Configs C2 / C3: an unmodified HP inference graph next to a BE training
+    program of this package's kernels, under the Tally policy."""
     import collections
     import torch
     world = int(os.environ.get("WORLD_SIZE", "1"))
@@ -693,16 +706,32 @@ def main_c2(args):
     gpu = dev.spec
     window = int(args.window_ms * 1e6)
     B = args.batch
-    hp = resnet.ResNet50Infer(batch=1, image=224, seed=1 + rank)
-    tr = resnet.ResNet50Train(batch=B, image=224, lr=args.lr, seed=rank)
     g = torch.Generator(device="cuda").manual_seed(1000 + rank)
-    tr.set_batch(torch.randn(B, 3, 224, 224, device="cuda", generator=g),
-                 torch.randint(0, 1000, (B,), device="cuda", generator=g))
+    if args.config == "c2":
+        hp = resnet.ResNet50Infer(batch=1, image=224, seed=1 + rank)
+        tr = resnet.ResNet50Train(batch=B, image=224, lr=args.lr, seed=rank)
+        tr.set_batch(torch.randn(B, 3, 224, 224, device="cuda", generator=g),
+                     torch.randint(0, 1000, (B,), device="cuda", generator=g))
+        hp_name, hp_in = "resnet50_infer_bs1", hp.inp
+        desc = {"hp": "ResNet-50 bs=1 3x224x224", "be": f"ResNet-50 training bs={B}",
+                "data": "synthetic (random-init torchvision ResNet-50 weights, N(0,1) images, random labels; "
+                        "MMPP arrivals)",
+                "e2e": "H2D image (3x224x224 bf16, pinned) + ResNet-50 graph + D2H logits (pinned)"}
+    else:
+        from paper_2410_07381_b200 import gpt2
+        hp = gpt2.BertInfer(seq=128, seed=1 + rank)
+        tr = gpt2.GPT2Train(batch=B, seq=1024, lr=args.lr, seed=rank)
+        tr.set_batch(torch.randint(0, tr.V, (B, 1025), device="cuda", generator=g))
+        hp_name, hp_in = "bert_base_infer_seq128", hp.ids
+        desc = {"hp": "BERT-base bs=1 seq=128", "be": f"GPT-2 small (124M) training bs={B} seq=1024",
+                "data": "synthetic (random-init HuggingFace BERT-base / GPT-2 weights, uniform random tokens; "
+                        "MMPP arrivals)",
+                "e2e": "H2D token ids (1x128 int64, pinned) + BERT graph + D2H hidden states (pinned)"}
 
     prof = P.Profiler(gpu, runs=args.profile_runs)
     if args.profile_cache and os.path.exists(args.profile_cache):
         prof.load_cache(open(args.profile_cache).read())    # ref profiler.py:252-291
-    hp_w = P.KernelWork("resnet50_infer_bs1", hp.kernel.cost(), exempt=True, kernel=hp.kernel)
+    hp_w = P.KernelWork(hp_name, hp.kernel.cost(), exempt=True, kernel=hp.kernel)
     be_ws = []
     for name, dk in tr.program:
         sig = tr.work_signature(name, dk)
@@ -875,9 +904,9 @@ def main_c2(args):
     # --- e2e: HP requests carry their input / logits over PCIe ---------------------
     e2e = None
     if not args.no_e2e:
-        host_in = hp.inp.cpu().pin_memory()
+        host_in = hp_in.cpu().pin_memory()
         host_out = torch.empty(hp.out.shape, dtype=hp.out.dtype).pin_memory()
-        h2d = kernels.memcpy(hp.inp, host_in)
+        h2d = kernels.memcpy(hp_in, host_in)
         d2h = kernels.memcpy(host_out, hp.out)
         pipe = (P.KernelWork("h2d_image", h2d.cost(), exempt=True, kernel=h2d), hp_w,
                 P.KernelWork("d2h_logits", d2h.cost(), exempt=True, kernel=d2h))
@@ -895,7 +924,7 @@ def main_c2(args):
                    "h2d_bytes_per_step": int(reqs / args.steps * host_in.numel() * host_in.element_size()),
                    "d2h_bytes_per_step": int(reqs / args.steps * host_out.numel() * host_out.element_size()),
                    "p99_solo_us": p99(e_solo) / 1e3, "p99_co_us": p99(e_co) / 1e3, "requests": len(e_co),
-                   "pipeline": "H2D image (3x224x224 bf16, pinned) + ResNet-50 graph + D2H logits (pinned)"}
+                   "pipeline": desc["e2e"]}
 
     # --- baselines (same traffic, untimed) ---------------------------------------------
     baselines = {}
@@ -924,7 +953,7 @@ def main_c2(args):
                      "blocks": w.kernel.info.total_blocks, "occupancy": w.kernel.info.occupancy_original,
                      "ns": int(recs[w.kernel_id])} for w in be_ws]}
     os.makedirs(os.path.join(ROOT, "gpurun_out"), exist_ok=True)
-    with open(os.path.join(ROOT, "gpurun_out", "c2_costs.json"), "w") as fh:
+    with open(os.path.join(ROOT, "gpurun_out", f"{args.config}_costs.json"), "w") as fh:
         json.dump(costs, fh)
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
@@ -952,8 +981,8 @@ def main_c2(args):
         "metric": METRIC, "value": worst["overhead"], "unit": "%", "n_gpus": world,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": elapsed_ms / args.steps,
         "higher_is_better": False, "scaling": "weak", "vs_baseline": None, "dtype": "bf16",
-        "data": "synthetic (random-init torchvision ResNet-50 weights, N(0,1) images, random labels; MMPP arrivals)",
-        "config": {"workload": C2_WORKLOAD, "hp": "ResNet-50 bs=1 3x224x224", "be": f"ResNet-50 training bs={B}",
+        "data": desc["data"],
+        "config": {"workload": WORKLOADS[args.config], "hp": desc["hp"], "be": desc["be"],
                    "trace": f"MMPP bursty (burst x{args.burst}, 10% burst time), mean load {args.load}",
                    "window_ms": args.window_ms, "turnaround_threshold_us": args.threshold_us,
                    "policy": "Tally (reference semantics)",
@@ -997,12 +1026,14 @@ def main():
         args.window_ms = 100.0 if args.config == "c1" else 2000.0
     if args.load is None:
         args.load = 0.5 if args.config == "c1" else 0.25
+    if args.batch is None:
+        args.batch = 8 if args.config == "c3" else 64
     if args.cpu_sample_ms is None:
         args.cpu_sample_ms = 1.0 if args.config == "c1" else 4.0
     if args.impl == "reference":
         (run_reference_arm if args.config == "c1" else run_reference_arm_c2)(args)
     else:
-        (main_c1 if args.config == "c1" else main_c2)(args)
+        (main_c1 if args.config == "c1" else main_colocate)(args)
 
 
 if __name__ == "__main__":
