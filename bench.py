@@ -633,7 +633,7 @@ def run_reference_arm_c2(args):
             vals.append(v)
     total = time.perf_counter() - t0
     value = sum(vals) / len(vals) if vals else None
-    sample = (f"{args.cpu_sample_ms} ms simulated C2 window per step (solo HP + co-located Tally; HP every "
+    sample = (f"{args.cpu_sample_ms} ms simulated {args.config.upper()} window per step (solo HP + co-located Tally; HP every "
               f"latency/load, BE = first 24 of the {len(costs['be'])} training-step kernels with B200-measured "
               f"costs from profiles/{args.config}_costs.json) on GpuSpec(148,2048,32), oracle port of tallysim, 1 thread")
     print(json.dumps({
@@ -959,7 +959,7 @@ def main_colocate(args):
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         v, wall, hz, ne = cpu_c2_sample(costs, args.cpu_sample_ms, args.load, args.burst, 0)
         cpu = {"value": v, "unit": "%", "cores": 1, "kind": "port",
-               "sample": f"{args.cpu_sample_ms} ms simulated C2 window (solo + Tally co-run; HP every latency/load, "
+               "sample": f"{args.cpu_sample_ms} ms simulated {args.config.upper()} window (solo + Tally co-run; HP every latency/load, "
                          f"BE = first 24 training-step kernels), oracle port of tallysim on GpuSpec(148,2048,32) "
                          f"with the B200-measured kernel costs",
                "wall_s": wall, "sim_ms_per_wall_s": hz / 1e6 / wall, "events_per_s": ne / wall}

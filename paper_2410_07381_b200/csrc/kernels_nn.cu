@@ -816,46 +816,125 @@ struct AvgPoolBwd {
 
 // ---------------------------------------------------------------- loss
 struct SoftmaxXent {   // one row per logical block
+  // One HBM read of the row: pass 1 streams it (16-byte vectors, 4 in flight
+  // per thread) into shared memory while folding an online (max, sum-exp);
+  // pass 2 writes dlogits from the staged copy.  Rows above kCacheMax bytes
+  // are re-read from global memory instead.  bf16 logits (the GPT-2 LM head,
+  // 100 KB rows) halve the traffic and keep a logical block ~10 us.
   static constexpr int kThreads = 256;
+  static constexpr int kUnroll = 4;
+  static constexpr int kCacheMax = 104 * 1024;
+  static constexpr int kRed = 128;   // bytes of reduction scratch ahead of the row
   struct Params {
-    const float* logits;   // [B, Npad] fp32 (GEMM output)
-    const float* bias;     // [Npad]
+    const uint4* logits;   // [B, Npad] fp32 or bf16 (GEMM output)
+    const float* bias;     // [Npad] or null
     const int* labels;     // [B]
     float* loss;           // [B]
-    __nv_bfloat16* dl;     // [B, Npad], zero in the pad columns
-    float* dl32;           // [B, Npad]: the bias-gradient partials (summed over B by sgd_update)
-    int B, Npad, ncls;
+    uint4* dl;             // [B, Npad] bf16, zero in the pad columns
+    float4* dl32;          // [B, Npad] fp32 or null: the bias-gradient partials (summed over B by sgd_update)
+    int B, Npad, ncls, bf16, cache;
   };
-  static __device__ __forceinline__ void run(const Params& p, uint3 bidx, uint3, char* smem) {
-    float* red = reinterpret_cast<float*>(smem);   // [kThreads / 32]
-    const int b = bidx.x;
-    const float* z = p.logits + (long long)b * p.Npad;
-    float m = -INFINITY;
-    for (int j = threadIdx.x; j < p.ncls; j += kThreads) m = fmaxf(m, z[j] + p.bias[j]);
-#pragma unroll
-    for (int o = 16; o > 0; o >>= 1) m = fmaxf(m, __shfl_xor_sync(0xffffffffu, m, o));
-    if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = m;
-    __syncthreads();
-    m = red[0];
-    for (int w = 1; w < kThreads / 32; ++w) m = fmaxf(m, red[w]);
-    __syncthreads();
-    float s = 0.f;
-    for (int j = threadIdx.x; j < p.ncls; j += kThreads) s += __expf(z[j] + p.bias[j] - m);
-#pragma unroll
-    for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
-    if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = s;
-    __syncthreads();
-    s = 0.f;
-    for (int w = 0; w < kThreads / 32; ++w) s += red[w];
-    const int lab = p.labels[b];
-    const float inv_b = 1.f / (float)p.B;
-    for (int j = threadIdx.x; j < p.Npad; j += kThreads) {
-      float d = 0.f;
-      if (j < p.ncls) d = (__expf(z[j] + p.bias[j] - m) / s - (j == lab ? 1.f : 0.f)) * inv_b;
-      p.dl[(long long)b * p.Npad + j] = __float2bfloat16_rn(d);
-      if (p.dl32) p.dl32[(long long)b * p.Npad + j] = d;
+  static __device__ __forceinline__ void to_f32(const Params& p, const uint4 (&r)[2], int j0, float (&x)[8]) {
+    if (p.bf16) {
+      unpack8(r[0], x);
+    } else {
+      x[0] = __uint_as_float(r[0].x); x[1] = __uint_as_float(r[0].y);
+      x[2] = __uint_as_float(r[0].z); x[3] = __uint_as_float(r[0].w);
+      x[4] = __uint_as_float(r[1].x); x[5] = __uint_as_float(r[1].y);
+      x[6] = __uint_as_float(r[1].z); x[7] = __uint_as_float(r[1].w);
     }
-    if (threadIdx.x == 0) p.loss[b] = logf(s) + m - (z[lab] + p.bias[lab]);
+    if (p.bias) {
+      const float4 b0 = __ldg(reinterpret_cast<const float4*>(p.bias + j0));
+      const float4 b1 = __ldg(reinterpret_cast<const float4*>(p.bias + j0) + 1);
+      x[0] += b0.x; x[1] += b0.y; x[2] += b0.z; x[3] += b0.w;
+      x[4] += b1.x; x[5] += b1.y; x[6] += b1.z; x[7] += b1.w;
+    }
+#pragma unroll
+    for (int e = 0; e < 8; ++e)
+      if (j0 + e >= p.ncls) x[e] = -INFINITY;
+  }
+  static __device__ __forceinline__ void merge(float& m, float& s, float m2, float s2) {
+    const float mm = fmaxf(m, m2);
+    if (mm == -INFINITY) return;
+    s = s * __expf(m - mm) + s2 * __expf(m2 - mm);
+    m = mm;
+  }
+  static __device__ __forceinline__ void run(const Params& p, uint3 bidx, uint3, char* smem) {
+    float* red = reinterpret_cast<float*>(smem);   // [2][kThreads / 32]
+    uint4* cache = reinterpret_cast<uint4*>(smem + kRed);
+    const int b = bidx.x;
+    const int cpv = p.bf16 ? 1 : 2;                // 16-byte chunks per 8 logits
+    const int nv = p.Npad >> 3;
+    const uint4* row = p.logits + (long long)b * nv * cpv;
+    float m = -INFINITY, s = 0.f;
+    for (int v0 = threadIdx.x; v0 < nv; v0 += kUnroll * kThreads) {
+      uint4 r[kUnroll][2];
+#pragma unroll
+      for (int u = 0; u < kUnroll; ++u) {
+        const int v = v0 + u * kThreads;
+        if (v < nv) {
+          r[u][0] = p.cache ? __ldcs(row + v * cpv) : __ldg(row + v * cpv);
+          if (!p.bf16) r[u][1] = p.cache ? __ldcs(row + v * cpv + 1) : __ldg(row + v * cpv + 1);
+        }
+      }
+#pragma unroll
+      for (int u = 0; u < kUnroll; ++u) {
+        const int v = v0 + u * kThreads;
+        if (v >= nv) break;
+        if (p.cache) {
+          cache[v * cpv] = r[u][0];
+          if (!p.bf16) cache[v * cpv + 1] = r[u][1];
+        }
+        float x[8];
+        to_f32(p, r[u], v * 8, x);
+        float mv = x[0];
+#pragma unroll
+        for (int e = 1; e < 8; ++e) mv = fmaxf(mv, x[e]);
+        if (mv == -INFINITY) continue;
+        if (mv > m) { s *= __expf(m - mv); m = mv; }
+#pragma unroll
+        for (int e = 0; e < 8; ++e) s += __expf(x[e] - m);
+      }
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+      const float m2 = __shfl_xor_sync(0xffffffffu, m, o), s2 = __shfl_xor_sync(0xffffffffu, s, o);
+      merge(m, s, m2, s2);
+    }
+    if ((threadIdx.x & 31) == 0) { red[threadIdx.x >> 5] = m; red[kThreads / 32 + (threadIdx.x >> 5)] = s; }
+    __syncthreads();
+    m = red[0]; s = red[kThreads / 32];
+    for (int w = 1; w < kThreads / 32; ++w) merge(m, s, red[w], red[kThreads / 32 + w]);
+    const int lab = p.labels[b];
+    const float inv_s = 1.f / s, inv_b = 1.f / (float)p.B;
+    for (int v = threadIdx.x; v < nv; v += kThreads) {
+      uint4 r[2];
+      if (p.cache) {
+        r[0] = cache[v * cpv];
+        if (!p.bf16) r[1] = cache[v * cpv + 1];
+      } else {
+        r[0] = ld16(row + v * cpv);
+        if (!p.bf16) r[1] = ld16(row + v * cpv + 1);
+      }
+      float x[8];
+      to_f32(p, r, v * 8, x);
+#pragma unroll
+      for (int e = 0; e < 8; ++e) {
+        const int j = v * 8 + e;
+        x[e] = j < p.ncls ? (__expf(x[e] - m) * inv_s - (j == lab ? 1.f : 0.f)) * inv_b : 0.f;
+      }
+      st16(p.dl + (long long)b * nv + v, pack8(x));
+      if (p.dl32) {
+        float4* d = p.dl32 + ((long long)b * nv + v) * 2;
+        __stcs(d, make_float4(x[0], x[1], x[2], x[3]));
+        __stcs(d + 1, make_float4(x[4], x[5], x[6], x[7]));
+      }
+    }
+    if (threadIdx.x == 0) {
+      const float zl = p.bf16 ? __bfloat162float(reinterpret_cast<const __nv_bfloat16*>(row)[lab])
+                              : reinterpret_cast<const float*>(row)[lab];
+      p.loss[b] = logf(s) + m - (zl + (p.bias ? p.bias[lab] : 0.f));
+    }
     __syncthreads();
   }
 };
@@ -1277,20 +1356,37 @@ static int bind_avgpool_bwd(const tally_kernel_args* a, Instance* inst) {
 }
 
 // ptr: logits, bias, labels, loss, dl, dl32.  i: B, Npad, ncls
+// ptr: logits, bias (or null), labels, loss, dl, dl32 (or null).  i: B, Npad, ncls, logits_bf16
 static int bind_softmax_xent(const tally_kernel_args* a, Instance* inst) {
   nn::SoftmaxXent::Params p{};
-  p.logits = static_cast<const float*>(a->ptr[0]);
+  p.logits = static_cast<const uint4*>(a->ptr[0]);
   p.bias = static_cast<const float*>(a->ptr[1]);
   p.labels = static_cast<const int*>(a->ptr[2]);
   p.loss = static_cast<float*>(a->ptr[3]);
-  p.dl = static_cast<__nv_bfloat16*>(a->ptr[4]);
-  p.dl32 = static_cast<float*>(a->ptr[5]);
-  p.B = (int)a->i[0]; p.Npad = (int)a->i[1]; p.ncls = (int)a->i[2];
-  if (!p.logits || !p.bias || !p.labels || !p.loss || !p.dl || p.B < 1 || p.ncls < 1 || p.Npad < p.ncls) {
-    set_error("softmax_xent: bad arguments");
+  p.dl = static_cast<uint4*>(a->ptr[4]);
+  p.dl32 = static_cast<float4*>(a->ptr[5]);
+  p.B = (int)a->i[0]; p.Npad = (int)a->i[1]; p.ncls = (int)a->i[2]; p.bf16 = a->i[3] ? 1 : 0;
+  if (!p.logits || !p.labels || !p.loss || !p.dl || p.B < 1 || p.ncls < 1 || p.Npad < p.ncls || p.Npad % 8 ||
+      !aligned16(p.logits) || !aligned16(p.dl) || (p.bias && !aligned16(p.bias)) || (p.dl32 && !aligned16(p.dl32))) {
+    set_error("softmax_xent: bad arguments (Npad % 8 == 0, 16-byte aligned buffers)");
     return TALLY_EINVAL;
   }
-  finish(inst, p, p.B, nn::SoftmaxXent::kThreads, 64, (double)p.B * p.Npad * 10.0);
+  const size_t row = (size_t)p.Npad * (p.bf16 ? 2 : 4);
+  p.cache = row <= (size_t)nn::SoftmaxXent::kCacheMax;
+  finish(inst, p, p.B, nn::SoftmaxXent::kThreads, nn::SoftmaxXent::kRed + (p.cache ? row : 0),
+         (double)p.B * ((double)row + 2.0 * p.Npad + (p.dl32 ? 4.0 * p.Npad : 0.0)));
+  return TALLY_OK;
+}
+
+static int setup_softmax_xent() {
+  const void* fns[3] = {reinterpret_cast<const void*>(&k_original<nn::SoftmaxXent>),
+                        reinterpret_cast<const void*>(&k_sliced<nn::SoftmaxXent>),
+                        reinterpret_cast<const void*>(&k_ptb<nn::SoftmaxXent>)};
+  for (const void* f : fns) {
+    cudaError_t e = cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         nn::SoftmaxXent::kRed + nn::SoftmaxXent::kCacheMax);
+    if (e != cudaSuccess) return cuda_fail(e, "softmax_xent smem attribute");
+  }
   return TALLY_OK;
 }
 
@@ -1353,6 +1449,7 @@ int register_nn_kernels(KernelKind* out, int cap) {
   out[n++] = nn_kind<nn::AvgPoolFwd>("avgpool_fwd", bind_avgpool_fwd);
   out[n++] = nn_kind<nn::AvgPoolBwd>("avgpool_bwd", bind_avgpool_bwd);
   out[n++] = nn_kind<nn::SoftmaxXent>("softmax_xent", bind_softmax_xent);
+  out[n - 1].setup = setup_softmax_xent;
   out[n++] = nn_kind<nn::SgdUpdate>("sgd_update", bind_sgd);
   out[n++] = nn_kind<nn::SplitKReduce>("splitk_reduce", bind_splitk_reduce);
   return n;

@@ -13,7 +13,8 @@ transformable sm_100a kernels (like resnet.ResNet50Train): activations are
                       colstats for dgamma / dbeta
   backward            dX = dY . W reads W as stored (MN-major B); dW = dY^T . X
                       reads both activations as stored (MN-major A and B), split-K
-  head                tied embedding: logits = LN(x) . wte^T (fp32), softmax_xent;
+  head                tied embedding: logits = LN(x) . wte^T (bf16), softmax_xent;
+                      dX = dlogits . wte split-K (K = vocab) + splitk_reduce;
                       the wte gradient = head wgrad partials + an embedding
                       scatter slice (fp32 atomics), summed by sgd_update
 
@@ -165,6 +166,18 @@ class GPT2Train:
             self._add(name + ".wgrad", K.gemm_mn(dy, x, p.gpart, splits=S))
         self.sgd.add(p.w, p.v, p.gpart, S, M * Nn, WEIGHT_DECAY, p.wb, None, M, Nn)
 
+    def _gemm_ex_splitk(self, name, A, B, out, M, N, Kd, b_mn=False):
+        """out (bf16) = A . B^T; a long-K GEMM (the LM-head dgrad, K = vocab)
+        runs split-K into an fp32 workspace + splitk_reduce so its logical
+        blocks stay preemptible (resnet._gemm_splits)."""
+        S = _gemm_splits(M, N, Kd)
+        if S == 1:
+            self._add(name, K.gemm_ex(A, B, out, M, N, Kd, b_mn=b_mn))
+            return
+        ws = self.torch.empty(S * M, N, dtype=self.torch.float32, device=self.device)
+        self._add(name, K.gemm_ex(A, B, ws, M, N, Kd, b_mn=b_mn, splits=S))
+        self._add(name + ".reduce", K.splitk_reduce(ws.view(S, M, N), out))
+
     def _linear_bwd(self, name, lin, dy, x, need_dx=True):
         lin.b.g = self.torch.zeros(lin.out, device=self.device)
         self._colsum(name + ".dbias", dy, lin.b.g)
@@ -252,15 +265,14 @@ class GPT2Train:
             x = x_next
         self.x_final = x
         hf = self._ln_fwd("transformer.ln_f", self.lnf, x)
-        logits = torch.empty(N, self.Vp, dtype=torch.float32, device=self.device)
+        logits = self._buf(N, self.Vp)
         self._add("lm_head", K.gemm(hf, self.wte.wb, logits))
-        self.zero_bias = torch.zeros(self.Vp, device=self.device)
         dl = self._buf(N, self.Vp)
-        self._add("softmax_xent", K.softmax_xent(logits, self.zero_bias, self.targets, self.loss, dl, None, self.V))
+        self._add("softmax_xent", K.softmax_xent(logits, None, self.targets, self.loss, dl, None, self.V))
         self.logits = logits
         # backward: head (tied wte: wgrad partials + one embedding-scatter slice)
         dhf = self._buf(N, d)
-        self._add("lm_head.dgrad", K.gemm_ex(dl, self.wte.wb, dhf, N, d, self.Vp, b_mn=True))
+        self._gemm_ex_splitk("lm_head.dgrad", dl, self.wte.wb, dhf, N, d, self.Vp, b_mn=True)
         Sw = _gemm_splits(self.Vp, d, N)
         self.wte.gpart = torch.zeros(Sw + 1, self.Vp, d, dtype=torch.float32, device=self.device)
         if Sw == 1:

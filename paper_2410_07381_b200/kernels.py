@@ -456,8 +456,14 @@ def avgpool_bwd(dy, dx, n, hw, c) -> DeviceKernel:
 
 
 def softmax_xent(logits, bias, labels, loss, dl, dl32, ncls) -> DeviceKernel:
+    """Per-row softmax cross-entropy over the first ``ncls`` of ``Npad``
+    columns (Npad % 8 == 0): ``loss`` [B], ``dl`` [B, Npad] bf16 = (softmax -
+    onehot) / B, optional fp32 copy ``dl32``.  ``logits`` fp32 or bf16;
+    ``bias`` [Npad] fp32 or None."""
+    import torch
     B, Npad = logits.shape
-    return DeviceKernel("softmax_xent", (logits, bias, labels, loss, dl, dl32), (B, Npad, ncls))
+    return DeviceKernel("softmax_xent", (logits, bias, labels, loss, dl, dl32),
+                        (B, Npad, ncls, int(logits.dtype == torch.bfloat16)))
 
 
 def sgd_update(segs, blockmap, blocks, nbytes, lr, momentum) -> DeviceKernel:

@@ -253,23 +253,27 @@ def test_avgpool(env):
     assert nerr(gdx, (dy.float() / hw).unsqueeze(1).expand(n, hw, c)) < 1e-2
 
 
-def test_softmax_xent(env):
+@pytest.mark.parametrize("B,npad,ncls,dt,with_bias", [
+    (16, 1024, 1000, torch.float32, True),        # ResNet head: fp32 row staged in smem
+    (6, 50304, 50257, torch.bfloat16, False),     # GPT-2 LM head: 100 KB bf16 row staged in smem
+    (3, 50304, 50257, torch.float32, True),       # 200 KB fp32 row: above the stage limit, re-read
+    (5, 24, 17, torch.bfloat16, True)])           # ragged: fewer vectors than threads
+def test_softmax_xent(env, B, npad, ncls, dt, with_bias):
     P, kernels, stream = env
-    B, npad, ncls = 16, 1024, 1000
-    logits = torch.randn(B, npad, device="cuda") * 3
-    bias = torch.randn(npad, device="cuda")
+    logits = (torch.randn(B, npad, device="cuda") * 3).to(dt)
+    bias = torch.randn(npad, device="cuda") if with_bias else None
     labels = torch.randint(0, ncls, (B,), device="cuda", dtype=torch.int32)
     loss = torch.zeros(B, device="cuda")
     dl = torch.zeros(B, npad, dtype=torch.bfloat16, device="cuda")
     dl32 = torch.zeros(B, npad, device="cuda")
     gl, gdl, gdl32 = shapes(P, kernels.softmax_xent(logits, bias, labels, loss, dl, dl32, ncls), stream,
                             [loss, dl, dl32])
-    z = (logits + bias)[:, :ncls].clone().requires_grad_(True)
+    z = (logits.float() + (bias if with_bias else 0))[:, :ncls].clone().requires_grad_(True)
     ref = F.cross_entropy(z, labels.long(), reduction="none")
     ref.mean().backward()
     assert nerr(gl, ref) < 1e-5
     assert nerr(gdl32[:, :ncls], z.grad) < 1e-4 and not gdl32[:, ncls:].any()
-    assert nerr(gdl[:, :ncls], z.grad) < 1e-2
+    assert nerr(gdl[:, :ncls], z.grad) < 1e-2 and not gdl[:, ncls:].any()
 
 
 def test_sgd_update(env):

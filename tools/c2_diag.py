@@ -48,11 +48,17 @@ def main():
     window = int(arg("--ms", 500.0) * 1e6)
     load, burst = arg("--load", 0.25), arg("--burst", 4.0)
     threshold = int(arg("--threshold-us", 31.6) * 1000)
-    hp = resnet.ResNet50Infer(batch=1, image=224)
-    tr = resnet.ResNet50Train(batch=64, image=224, lr=0.01)
     g = torch.Generator(device="cuda").manual_seed(0)
-    tr.set_batch(torch.randn(64, 3, 224, 224, device="cuda", generator=g),
-                 torch.randint(0, 1000, (64,), device="cuda", generator=g))
+    if "--c3" in sys.argv:
+        from paper_2410_07381_b200 import gpt2
+        hp = gpt2.BertInfer(seq=128)
+        tr = gpt2.GPT2Train(batch=8, seq=1024, lr=1e-3)
+        tr.set_batch(torch.randint(0, tr.V, (8, 1025), device="cuda", generator=g))
+    else:
+        hp = resnet.ResNet50Infer(batch=1, image=224)
+        tr = resnet.ResNet50Train(batch=64, image=224, lr=0.01)
+        tr.set_batch(torch.randn(64, 3, 224, 224, device="cuda", generator=g),
+                     torch.randint(0, 1000, (64,), device="cuda", generator=g))
     prof = P.Profiler(gpu, runs=2)
     hp_w = P.KernelWork("resnet50_infer_bs1", hp.kernel.cost(), exempt=True, kernel=hp.kernel)
     be_ws = []
