@@ -533,7 +533,7 @@ struct BnAct {
     const float* shift;
     uint4* pre;           // optional: the pre-activation values (GELU backward input)
     long long nvec;
-    int C, relu;          // activation: 0 none, 1 ReLU, 2 GELU (tanh approximation)
+    int C, relu;          // activation: 0 none, 1 ReLU, 2 GELU (tanh approximation), 3 GELU (erf)
   };
   static __device__ __forceinline__ void run(const Params& p, uint3 bidx, uint3, char*) {
     const int cv = p.C >> 3;
@@ -583,6 +583,9 @@ struct BnAct {
           const float u = 0.7978845608028654f * (x[e] + 0.044715f * x[e] * x[e] * x[e]);
           x[e] = 0.5f * x[e] * (1.f + tanhf(u));
         }
+      } else if (p.relu == 3) {
+#pragma unroll
+        for (int e = 0; e < 8; ++e) x[e] = 0.5f * x[e] * (1.f + erff(x[e] * 0.7071067811865476f));
       }
       st16(p.y + v, pack8(x));
     }
@@ -1261,8 +1264,8 @@ static int bind_bn_act(const tally_kernel_args* a, Instance* inst) {
   const long long P = a->i[0];
   p.C = (int)a->i[1];
   p.relu = (int)a->i[2];
-  if (!p.x || !p.y || !p.shift || P < 1 || p.C < 8 || p.C % 8 || p.relu < 0 || p.relu > 2) {
-    set_error("bn_act: need x, y, shift, C %% 8 == 0, act in {0 none, 1 relu, 2 gelu}");
+  if (!p.x || !p.y || !p.shift || P < 1 || p.C < 8 || p.C % 8 || p.relu < 0 || p.relu > 3) {
+    set_error("bn_act: need x, y, shift, C %% 8 == 0, act in {0 none, 1 relu, 2 gelu tanh, 3 gelu erf}");
     return TALLY_EINVAL;
   }
   p.nvec = P * (p.C / 8);

@@ -7,8 +7,8 @@
 //   layernorm_fwd      y = (x - mean) * rstd * gamma + beta, one warp per row;
 //                      saves mean / rstd per row
 //   layernorm_bwd      dx = rstd * (dy*g - mean(dy*g) - xhat * mean(dy*g*xhat)) [+ residual grad]
-//   gelu_bwd           dx = g * gelu'(pre)  (tanh approximation, GPT-2 "gelu_new")
-//   softmax_causal     P = softmax(scale * S) over keys j <= i, one warp per row
+//   gelu_bwd           dx = g * gelu'(pre)  (tanh approximation, GPT-2 "gelu_new"; or exact erf, BERT)
+//   softmax_causal     P = softmax(scale * S) over keys j <= i (or all keys), one warp per row
 //   softmax_causal_bwd dS = P * (dP - sum_j P dP) * scale
 //   embedding_fwd      x = wte[token] + wpe[position]
 //   embedding_bwd      dwte[token] += dx  (fp32 atomics)
@@ -186,6 +186,9 @@ __device__ __forceinline__ float gelu_grad(float x) {
   const float t = tanhf(u);
   return 0.5f * (1.f + t) + 0.5f * x * (1.f - t * t) * k0 * (1.f + 3.f * k1 * x * x);
 }
+__device__ __forceinline__ float gelu_erf_grad(float x) {   // BERT "gelu": x * Phi(x)
+  return 0.5f * (1.f + erff(x * 0.7071067811865476f)) + x * 0.3989422804014327f * __expf(-0.5f * x * x);
+}
 
 struct GeluBwd {
   static constexpr int kThreads = 256;
@@ -195,6 +198,7 @@ struct GeluBwd {
     const uint4* pre;
     uint4* dx;
     long long nvec;
+    int erf;                 // 0: tanh approximation (GPT-2), 1: exact erf (BERT)
   };
   static __device__ __forceinline__ void run(const Params& p, uint3 bidx, uint3, char*) {
     const long long v0 = (long long)bidx.x * (kThreads * kVec) + threadIdx.x;
@@ -212,7 +216,7 @@ struct GeluBwd {
       unpack8(gv[u], g);
       unpack8(hv[u], h);
 #pragma unroll
-      for (int e = 0; e < 8; ++e) g[e] *= gelu_grad(h[e]);
+      for (int e = 0; e < 8; ++e) g[e] *= p.erf ? gelu_erf_grad(h[e]) : gelu_grad(h[e]);
       p.dx[v] = pack8(g);
     }
   }
@@ -227,12 +231,13 @@ struct SoftmaxCausal {
     long long rows;
     int T;
     float scale;
+    int causal;              // 0: every key visible (BERT encoder)
   };
   static __device__ __forceinline__ void run(const Params& p, uint3 bidx, uint3, char*) {
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const long long r = (long long)bidx.x * kRowsPerBlock + warp;
     if (r >= p.rows) return;
-    const int i = (int)(r % p.T);               // query position: keys 0..i are visible
+    const int i = p.causal ? (int)(r % p.T) : p.T - 1;   // keys 0..i are visible
     const float* sr = p.s + r * p.T;
     float m = -INFINITY;
     for (int j = lane * 4; j <= i; j += 128) {
@@ -279,12 +284,13 @@ struct SoftmaxCausalBwd {
     long long rows;
     int T;
     float scale;
+    int causal;
   };
   static __device__ __forceinline__ void run(const Params& p, uint3 bidx, uint3, char*) {
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const long long r = (long long)bidx.x * kRowsPerBlock + warp;
     if (r >= p.rows) return;
-    const int i = (int)(r % p.T);
+    const int i = p.causal ? (int)(r % p.T) : p.T - 1;
     const __nv_bfloat16* pr = p.p + r * p.T;
     const float* dr = p.dp + r * p.T;
     float dot = 0.f;
@@ -426,7 +432,7 @@ static int bind_ln_bwd(const tally_kernel_args* a, Instance* inst) {
   return TALLY_OK;
 }
 
-// ptr: g, pre, dx.  i: n (elements)
+// ptr: g, pre, dx.  i: n (elements), erf
 static int bind_gelu_bwd(const tally_kernel_args* a, Instance* inst) {
   tf::GeluBwd::Params p{};
   p.g = static_cast<const uint4*>(a->ptr[0]);
@@ -435,12 +441,13 @@ static int bind_gelu_bwd(const tally_kernel_args* a, Instance* inst) {
   const long long n = a->i[0];
   if (!p.g || !p.pre || !p.dx || n < 8 || n % 8) { set_error("gelu_bwd: need g, pre, dx, n %% 8 == 0"); return TALLY_EINVAL; }
   p.nvec = n / 8;
+  p.erf = a->i[1] ? 1 : 0;
   const long long per = tf::GeluBwd::kThreads * tf::GeluBwd::kVec;
   tf_finish(inst, p, (p.nvec + per - 1) / per, 0, 6.0 * (double)n);
   return TALLY_OK;
 }
 
-// ptr: s (fp32), p (bf16).  i: rows, T.  f: scale
+// ptr: s (fp32), p (bf16).  i: rows, T, causal.  f: scale
 static int bind_softmax_causal(const tally_kernel_args* a, Instance* inst) {
   tf::SoftmaxCausal::Params p{};
   p.s = static_cast<const float*>(a->ptr[0]);
@@ -448,6 +455,7 @@ static int bind_softmax_causal(const tally_kernel_args* a, Instance* inst) {
   p.rows = a->i[0];
   p.T = (int)a->i[1];
   p.scale = (float)a->f[0];
+  p.causal = a->i[2] ? 1 : 0;
   if (!p.s || !p.p || p.rows < 1 || p.T < 4 || p.T % 4 || p.rows % p.T) {
     set_error("softmax_causal: need s, p, T %% 4 == 0, rows a multiple of T");
     return TALLY_EINVAL;
@@ -456,7 +464,7 @@ static int bind_softmax_causal(const tally_kernel_args* a, Instance* inst) {
   return TALLY_OK;
 }
 
-// ptr: p (bf16), dp (fp32), ds (bf16).  i: rows, T.  f: scale
+// ptr: p (bf16), dp (fp32), ds (bf16).  i: rows, T, causal.  f: scale
 static int bind_softmax_causal_bwd(const tally_kernel_args* a, Instance* inst) {
   tf::SoftmaxCausalBwd::Params p{};
   p.p = static_cast<const __nv_bfloat16*>(a->ptr[0]);
@@ -465,6 +473,7 @@ static int bind_softmax_causal_bwd(const tally_kernel_args* a, Instance* inst) {
   p.rows = a->i[0];
   p.T = (int)a->i[1];
   p.scale = (float)a->f[0];
+  p.causal = a->i[2] ? 1 : 0;
   if (!p.p || !p.dp || !p.ds || p.rows < 1 || p.T < 4 || p.T % 4 || p.rows % p.T) {
     set_error("softmax_causal_bwd: need p, dp, ds, T %% 4 == 0, rows a multiple of T");
     return TALLY_EINVAL;

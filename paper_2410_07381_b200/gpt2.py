@@ -25,32 +25,24 @@ is padded to a multiple of 128 (zero rows; their gradient stays zero).
 
 from __future__ import annotations
 
-import math
-
 from . import kernels as K
-from .resnet import SgdTable, _gemm_splits
+from .transformer import MOMENTUM, WEIGHT_DECAY, TransformerTrain, _gemm_splits  # noqa: F401
 
-MOMENTUM = 0.9
-WEIGHT_DECAY = 0.0
 LN_EPS = 1e-5
 
 
-def _rb_cols(P, C):
-    """Rows per colstats logical block (~128 KB of gradient per block)."""
-    base = 1024 if C < 128 else (512 if C < 256 else 256)
-    cblocks = (C + 255) // 256
-    return max(8, min(base, P * cblocks // 296 // 8 * 8))
-
-
-class GPT2Train:
+class GPT2Train(TransformerTrain):
     """One GPT-2 training step as a fixed sequence of device kernels.
 
     ``tokens`` [B, T] int32 input ids and ``targets`` [B*T] int32 next-token
     labels (refill between steps); ``loss`` [B*T] fp32 per-token losses."""
 
+    gelu_act = 2          # GPT-2 "gelu_new" (tanh approximation)
+    causal = True
+    ln_eps = LN_EPS
+
     def __init__(self, batch=8, seq=1024, lr=1e-3, model=None, seed=0, device="cuda", n_layer=None):
         import torch
-        self.torch = torch
         if model is None:
             from transformers import GPT2Config, GPT2LMHeadModel
             torch.manual_seed(seed)
@@ -71,9 +63,7 @@ class GPT2Train:
         dev = device
         N, d = batch * seq, self.d
         self.N = N
-        self.sgd = SgdTable()
-        self.program = []
-        self.params = []
+        self._init_common()
         self.tokens = torch.zeros(batch, seq, dtype=torch.int32, device=dev)
         self.targets = torch.zeros(N, dtype=torch.int32, device=dev)
         self.loss = torch.zeros(N, dtype=torch.float32, device=dev)
@@ -95,149 +85,14 @@ class GPT2Train:
             self.layers.append(lay)
         self.lnf = self._ln("transformer.ln_f", sd)
         self._build()
-        self.sgd.build(dev)
-        self._add("sgd_update", K.sgd_update(self.sgd.dev_segs, self.sgd.dev_map, self.sgd.blocks, self.sgd.nbytes,
-                                             self.lr, MOMENTUM))
-
-    # ---- parameters -------------------------------------------------------------
-    def _param(self, name, w32, bf16=True):
-        torch = self.torch
-
-        class Prm:
-            pass
-        p = Prm()
-        p.name, p.w, p.v = name, w32.contiguous(), torch.zeros_like(w32)
-        p.wb = p.w.bfloat16() if bf16 else None
-        self.params.append((name, p.w))
-        return p
+        self._finish(self.lr)
 
     def _linear(self, name, sd):
         """HF Conv1D (y = x W + b, W [in, out]) -> W [out, in] (y = x W^T)."""
-        w = sd[name + ".weight"].t().contiguous().to(self.device)
-        b = sd[name + ".bias"].to(self.device).clone()
-        lin = self._param(name + ".weight", w)
-        lin.b = self._param(name + ".bias", b, bf16=False)
-        lin.out, lin.inp = w.shape
-        return lin
+        return self._linear_w(name, sd[name + ".weight"].t(), sd[name + ".bias"])
 
     def _ln(self, name, sd):
-        torch = self.torch
-
-        class LN:
-            pass
-        ln = LN()
-        ln.g = self._param(name + ".weight", sd[name + ".weight"].to(self.device).clone(), bf16=False)
-        ln.b = self._param(name + ".bias", sd[name + ".bias"].to(self.device).clone(), bf16=False)
-        ln.mean = torch.zeros(self.N, device=self.device)
-        ln.rstd = torch.zeros(self.N, device=self.device)
-        return ln
-
-    def _buf(self, *shape, dtype=None):
-        return self.torch.empty(*shape, dtype=dtype or self.torch.bfloat16, device=self.device)
-
-    def _add(self, name, dk):
-        self.program.append((name, dk))
-
-    # ---- building blocks ------------------------------------------------------------
-    def _colsum(self, name, g, dbeta, dgamma=None, x=None, mean=None, rstd=None, g2=None):
-        torch = self.torch
-        P, C = g.shape
-        rb = _rb_cols(P, C)
-        nrb = (P + rb - 1) // rb
-        part = torch.empty(2 * nrb * C, device=self.device)
-        self._add(name, K.colstats(g, part, P, C, rb, dbeta, dgamma=dgamma, x=x, mean=mean, rstd=rstd, g2=g2))
-
-    def _linear_fwd(self, name, lin, x, act=0, res=None, pre=None):
-        u = self._buf(self.N, lin.out)
-        self._add(name + ".gemm", K.gemm(x, lin.wb, u))
-        y = self._buf(self.N, lin.out)
-        self._add(name + ".bias", K.bias_act(u, y, lin.b.w, self.N, lin.out, act=act, res=res, pre=pre))
-        return y
-
-    def _wgrad(self, name, p, dy, x):
-        """dW[out, in] = dy^T . x, split-K fp32 partials -> sgd_update."""
-        torch = self.torch
-        M, Nn, Kd = dy.shape[1], x.shape[1], self.N
-        S = _gemm_splits(M, Nn, Kd)
-        p.gpart = torch.empty(S, M, Nn, dtype=torch.float32, device=self.device)
-        if S == 1:
-            self._add(name + ".wgrad", K.gemm_ex(dy, x, p.gpart[0], M, Nn, Kd, a_mn=True, b_mn=True))
-        else:
-            self._add(name + ".wgrad", K.gemm_mn(dy, x, p.gpart, splits=S))
-        self.sgd.add(p.w, p.v, p.gpart, S, M * Nn, WEIGHT_DECAY, p.wb, None, M, Nn)
-
-    def _gemm_ex_splitk(self, name, A, B, out, M, N, Kd, b_mn=False):
-        """out (bf16) = A . B^T; a long-K GEMM (the LM-head dgrad, K = vocab)
-        runs split-K into an fp32 workspace + splitk_reduce so its logical
-        blocks stay preemptible (resnet._gemm_splits)."""
-        S = _gemm_splits(M, N, Kd)
-        if S == 1:
-            self._add(name, K.gemm_ex(A, B, out, M, N, Kd, b_mn=b_mn))
-            return
-        ws = self.torch.empty(S * M, N, dtype=self.torch.float32, device=self.device)
-        self._add(name, K.gemm_ex(A, B, ws, M, N, Kd, b_mn=b_mn, splits=S))
-        self._add(name + ".reduce", K.splitk_reduce(ws.view(S, M, N), out))
-
-    def _linear_bwd(self, name, lin, dy, x, need_dx=True):
-        lin.b.g = self.torch.zeros(lin.out, device=self.device)
-        self._colsum(name + ".dbias", dy, lin.b.g)
-        self.sgd.add(lin.b.w, lin.b.v, lin.b.g.view(1, -1), 1, lin.out, WEIGHT_DECAY)
-        self._wgrad(name, lin, dy, x)
-        if not need_dx:
-            return None
-        dx = self._buf(self.N, lin.inp)
-        self._add(name + ".dgrad", K.gemm_ex(dy, lin.wb, dx, self.N, lin.inp, lin.out, b_mn=True))
-        return dx
-
-    def _ln_fwd(self, name, ln, x):
-        y = self._buf(self.N, self.d)
-        self._add(name, K.layernorm_fwd(x, y, ln.g.w, ln.b.w, ln.mean, ln.rstd, LN_EPS))
-        return y
-
-    def _ln_bwd(self, name, ln, dy, x, g2=None):
-        torch = self.torch
-        ln.g.g = torch.zeros(self.d, device=self.device)
-        ln.b.g = torch.zeros(self.d, device=self.device)
-        self._colsum(name + ".dparams", dy, ln.b.g, dgamma=ln.g.g, x=x, mean=ln.mean, rstd=ln.rstd)
-        self.sgd.add(ln.g.w, ln.g.v, ln.g.g.view(1, -1), 1, self.d, WEIGHT_DECAY)
-        self.sgd.add(ln.b.w, ln.b.v, ln.b.g.view(1, -1), 1, self.d, WEIGHT_DECAY)
-        dx = self._buf(self.N, self.d)
-        self._add(name + ".bwd", K.layernorm_bwd(dy, x, ln.g.w, ln.mean, ln.rstd, dx, g2=g2))
-        return dx
-
-    # attention over (sequence, head) blocks of the fused QKV activation
-    def _views(self, qkv):
-        d = self.d
-        return qkv[:, :d], qkv[:, d:2 * d], qkv[:, 2 * d:]
-
-    def _attn_fwd(self, name, qkv, S, Pm):
-        T, H, D = self.T, self.H, self.D
-        q, k, v = self._views(qkv)
-        z = dict(batches=self.B * H, hdiv=H)
-        self._add(name + ".qk", K.gemm_ex(q, k, S, T, T, D, a_off=((T, 0), (0, D)), b_off=((T, 0), (0, D)),
-                                          c_off=((H * T, T), (0, 0)), **z))
-        self._add(name + ".softmax", K.softmax_causal(S, Pm, T, 1.0 / math.sqrt(D)))
-        o = self._buf(self.N, self.d)
-        self._add(name + ".pv", K.gemm_ex(Pm, v, o, T, D, T, b_mn=True, a_off=((H * T, T), (0, 0)),
-                                          b_off=((T, 0), (0, D)), c_off=((T, 0), (0, D)), **z))
-        return o
-
-    def _attn_bwd(self, name, qkv, Pm, do, dP, dS):
-        T, H, D = self.T, self.H, self.D
-        q, k, v = self._views(qkv)
-        z = dict(batches=self.B * H, hdiv=H)
-        dqkv = self._buf(self.N, 3 * self.d)
-        dq, dk_, dv = self._views(dqkv)
-        self._add(name + ".dp", K.gemm_ex(do, v, dP, T, T, D, a_off=((T, 0), (0, D)), b_off=((T, 0), (0, D)),
-                                          c_off=((H * T, T), (0, 0)), **z))
-        self._add(name + ".softmax_bwd", K.softmax_causal_bwd(Pm, dP, dS, T, 1.0 / math.sqrt(D)))
-        self._add(name + ".dq", K.gemm_ex(dS, k, dq, T, D, T, b_mn=True, a_off=((H * T, T), (0, 0)),
-                                          b_off=((T, 0), (0, D)), c_off=((T, 0), (0, D)), **z))
-        self._add(name + ".dk", K.gemm_ex(dS, q, dk_, T, D, T, a_mn=True, b_mn=True, a_off=((H * T, T), (0, 0)),
-                                          b_off=((T, 0), (0, D)), c_off=((T, 0), (0, D)), **z))
-        self._add(name + ".dv", K.gemm_ex(Pm, do, dv, T, D, T, a_mn=True, b_mn=True, a_off=((H * T, T), (0, 0)),
-                                          b_off=((T, 0), (0, D)), c_off=((T, 0), (0, D)), **z))
-        return dqkv
+        return self._ln_w(name, sd[name + ".weight"], sd[name + ".bias"])
 
     # ---- the step ----------------------------------------------------------------------
     def _build(self):
@@ -305,20 +160,10 @@ class GPT2Train:
         self.sgd.add(self.wpe.w, self.wpe.v, self.wpe.g.view(1, -1), 1, T * d, WEIGHT_DECAY, self.wpe.wb, None, T, d)
 
     # ---- running it -------------------------------------------------------------------
-    def step_original(self, stream):
-        launches = [dk.original(stream) for _, dk in self.program]
-        for L in launches:
-            L.wait()
-        return launches[-1]
-
     def set_batch(self, tokens):
         """tokens [B, T+1] int: inputs are tokens[:, :-1], targets tokens[:, 1:]."""
         self.tokens.copy_(tokens[:, :-1].to(self.torch.int32))
         self.targets.copy_(tokens[:, 1:].reshape(-1).to(self.torch.int32))
-
-    def work_signature(self, name, dk):
-        i = dk.info
-        return f"{dk.kind}:{i.grid[0]}x{i.grid[1]}x{i.grid[2]}:{int(i.alg_bytes)}:{int(i.alg_flops)}"
 
 
 class BertInfer:

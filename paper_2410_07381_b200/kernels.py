@@ -474,7 +474,7 @@ def sgd_update(segs, blockmap, blocks, nbytes, lr, momentum) -> DeviceKernel:
 
 # -- best-effort transformer-training kinds (config C3, kernels_tf.cu) ---------
 def bias_act(x, y, bias, P, C, act=0, res=None, pre=None) -> DeviceKernel:
-    """y = act(x + bias [+ res]); act 0 none, 1 ReLU, 2 GELU (tanh); ``pre``
+    """y = act(x + bias [+ res]); act 0 none, 1 ReLU, 2 GELU (tanh), 3 GELU (erf); ``pre``
     receives the pre-activation values (GELU backward input)."""
     return DeviceKernel("bn_act", (x, res, y, None, bias, pre), (P, C, act))
 
@@ -497,16 +497,18 @@ def layernorm_bwd(dy, x, gamma, mean, rstd, dx, g2=None) -> DeviceKernel:
     return DeviceKernel("layernorm_bwd", (dy, g2, x, gamma, mean, rstd, dx), (rows, C))
 
 
-def gelu_bwd(g, pre, dx) -> DeviceKernel:
-    return DeviceKernel("gelu_bwd", (g, pre, dx), (g.numel(),))
+def gelu_bwd(g, pre, dx, erf=False) -> DeviceKernel:
+    """dx = g * GELU'(pre): tanh approximation (GPT-2) or exact erf (BERT)."""
+    return DeviceKernel("gelu_bwd", (g, pre, dx), (g.numel(), int(erf)))
 
 
-def softmax_causal(s, p, T, scale) -> DeviceKernel:
-    return DeviceKernel("softmax_causal", (s, p), (s.shape[0], T), (scale,))
+def softmax_causal(s, p, T, scale, causal=True) -> DeviceKernel:
+    """P = softmax(scale * S) per row of T keys; ``causal``: keys j <= i only."""
+    return DeviceKernel("softmax_causal", (s, p), (s.shape[0], T, int(causal)), (scale,))
 
 
-def softmax_causal_bwd(p, dp, ds, T, scale) -> DeviceKernel:
-    return DeviceKernel("softmax_causal_bwd", (p, dp, ds), (p.shape[0], T), (scale,))
+def softmax_causal_bwd(p, dp, ds, T, scale, causal=True) -> DeviceKernel:
+    return DeviceKernel("softmax_causal_bwd", (p, dp, ds), (p.shape[0], T, int(causal)), (scale,))
 
 
 def embedding_fwd(tok, wte, wpe, x, T) -> DeviceKernel:

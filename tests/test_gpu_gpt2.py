@@ -88,37 +88,39 @@ def test_layernorm_fwd_bwd_and_param_grads(env):
     assert nerr(gdg, gmf.grad) < 1e-4 and nerr(gdb, btf.grad) < 1e-4
 
 
-def test_bias_gelu_and_backward(env):
+@pytest.mark.parametrize("erf", [False, True])     # GPT-2 tanh approximation / BERT exact erf
+def test_bias_gelu_and_backward(env, erf):
     P, kernels, stream = env
     N, C = 200, 3072
     u, bias = rnd(N, C, seed=4), torch.randn(C, device="cuda")
     y, pre = torch.zeros_like(u), torch.zeros_like(u)
-    gy, gp = shapes(P, kernels.bias_act(u, y, bias, N, C, act=2, pre=pre), stream, [y, pre])
+    gy, gp = shapes(P, kernels.bias_act(u, y, bias, N, C, act=3 if erf else 2, pre=pre), stream, [y, pre])
     h = (u.float() + bias).requires_grad_(True)
-    ref = F.gelu(h, approximate="tanh")
+    ref = F.gelu(h, approximate="none" if erf else "tanh")
     assert nerr(gy, ref) < 1e-2 and nerr(gp, h) < 1e-2
     g = rnd(N, C, seed=5)
     ref.backward(g.float())
     dx = torch.zeros_like(u)
-    (gdx,) = shapes(P, kernels.gelu_bwd(g, gp, dx), stream, [dx])
+    (gdx,) = shapes(P, kernels.gelu_bwd(g, gp, dx, erf=erf), stream, [dx])
     assert nerr(gdx, h.grad) < 2e-2
 
 
-def test_softmax_causal_fwd_bwd(env):
+@pytest.mark.parametrize("causal", [True, False])   # GPT-2 / BERT encoder
+def test_softmax_causal_fwd_bwd(env, causal):
     P, kernels, stream = env
     BH, T = 6, 256
     S = torch.randn(BH * T, T, device="cuda") * 3
     Pm = torch.zeros(BH * T, T, dtype=torch.bfloat16, device="cuda")
     scale = 0.125
-    (gp,) = shapes(P, kernels.softmax_causal(S, Pm, T, scale), stream, [Pm])
-    mask = torch.ones(T, T, device="cuda").tril().bool()
+    (gp,) = shapes(P, kernels.softmax_causal(S, Pm, T, scale, causal=causal), stream, [Pm])
+    mask = torch.ones(T, T, device="cuda").tril().bool() if causal else torch.ones(T, T, device="cuda").bool()
     s3 = (S.view(BH, T, T) * scale).masked_fill(~mask, float("-inf")).requires_grad_(True)
     ref = torch.softmax(s3, -1)
     assert nerr(gp.view(BH, T, T), ref) < 1e-2
     dP = torch.randn(BH * T, T, device="cuda")
     ref.backward(dP.view(BH, T, T))
     dS = torch.zeros_like(Pm)
-    (gds,) = shapes(P, kernels.softmax_causal_bwd(gp, dP, dS, T, scale), stream, [dS])
+    (gds,) = shapes(P, kernels.softmax_causal_bwd(gp, dP, dS, T, scale, causal=causal), stream, [dS])
     # reference from the bf16 probabilities the program keeps (d/dS of softmax(scale*S))
     pf = gp.float().view(BH, T, T)
     dref = pf * (dP.view(BH, T, T) - (pf * dP.view(BH, T, T)).sum(-1, keepdim=True)) * scale
