@@ -64,14 +64,18 @@ def parse():
     ap.add_argument("--steps", type=int, default=5)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--config", default="c2", choices=["c1", "c2", "c3"],
+    ap.add_argument("--config", default="c2", choices=["c1", "c2", "c3", "c4"],
                     help="c2 = BASELINE configs[1] (ResNet-50 HP bs=1 + ResNet-50 training bs=64); "
                          "c3 = configs[2] (BERT-base HP seq 128 + GPT-2 small training); "
+                         "c4 = configs[3] (Llama-2-7B decode bs=1 HP + BERT-large training); "
                          "c1 = the synthetic vecadd + SGEMM pair")
-    ap.add_argument("--window-ms", type=float, default=None, help="default 100 (c1) / 2000 (c2)")
+    ap.add_argument("--window-ms", type=float, default=None, help="default 100 (c1) / 2000 (c2, c3) / 8000 (c4)")
+    ap.add_argument("--gen", type=int, default=16, help="c4: tokens generated per HP request (after a 32-token "
+                                                        "prompt)")
     ap.add_argument("--load", type=float, default=None, help="mean HP load; default 0.5 (c1) / 0.25 (c2)")
     ap.add_argument("--burst", type=float, default=4.0, help="c2: MMPP burst-rate factor")
-    ap.add_argument("--batch", type=int, default=None, help="BE training batch (default 64 for c2, 8 for c3)")
+    ap.add_argument("--batch", type=int, default=None,
+                    help="BE training batch (default 64 for c2, 8 for c3 and c4)")
     ap.add_argument("--lr", type=float, default=0.01, help="BE SGD learning rate")
     ap.add_argument("--profile-runs", type=int, default=3)
     # The paper's 0.0316 ms default.  With block-granular PTB no
@@ -287,7 +291,7 @@ def main_c1(args):
     if args.profile_cache and os.path.exists(args.profile_cache):
         prof.load_cache(open(args.profile_cache).read())    # ref profiler.py:252-291
     threshold = int(args.threshold_us * 1000)
-    hp_lat = workloads.isolated_request_latency_ns(prof, (hp_w,))
+    hp_lat = workloads.isolated_request_latency_ns(prof, hp_pipe)
     choices = {w.kernel_id: prof.select(w.profile_key(), w.cost, threshold).describe() for w in be_ws}
     sg_recs = {r.candidate.describe(): r for r in prof.profile(be_ws[2].profile_key(), be_ws[2].cost)}
     if args.profile_cache and not os.path.exists(args.profile_cache) and rank == 0:
@@ -547,7 +551,11 @@ C2_WORKLOAD = ("C2 on B200 (BASELINE configs[1]): HP ResNet-50 inference bs=1 (t
 C3_WORKLOAD = ("C3 on B200 (BASELINE configs[2]): HP BERT-base inference seq=128 bs=1 (HuggingFace, bf16, CUDA "
                "graph, unmodified) on a bursty MMPP trace + BE GPT-2 small training seq=1024 (bf16, our "
                "transformable sm_100a kernel program with PTB preemption, momentum SGD), Tally policy")
-WORKLOADS = {"c2": C2_WORKLOAD, "c3": C3_WORKLOAD}
+C4_WORKLOAD = ("C4 on B200 (BASELINE configs[3]): HP Llama-2-7B greedy decode bs=1 (random-init bf16, 32-token "
+               "prompt + per-token decode steps, prefill / decode-step CUDA graphs, unmodified) on a bursty MMPP "
+               "trace + BE BERT-large masked-LM training seq=512 (bf16, our transformable sm_100a kernel "
+               "program, momentum SGD), Tally policy")
+WORKLOADS = {"c2": C2_WORKLOAD, "c3": C3_WORKLOAD, "c4": C4_WORKLOAD}
 
 
 def costs_path(config):
@@ -717,6 +725,20 @@ def main_colocate(args):
                 "data": "synthetic (random-init torchvision ResNet-50 weights, N(0,1) images, random labels; "
                         "MMPP arrivals)",
                 "e2e": "H2D image (3x224x224 bf16, pinned) + ResNet-50 graph + D2H logits (pinned)"}
+    elif args.config == "c4":
+        from paper_2410_07381_b200 import bert, llama
+        hp = llama.LlamaDecode(prompt=32, gen=args.gen, seed=1 + rank)
+        tr = bert.BertTrain(batch=B, seq=512, lr=args.lr, seed=rank)
+        tr.set_batch(torch.randint(0, tr.V, (B, 512), device="cuda", generator=g),
+                     torch.randint(0, tr.V, (B, 512), device="cuda", generator=g))
+        hp.prompt_ids.copy_(torch.randint(0, hp.V, (32,), device="cuda", generator=g))
+        hp_name, hp_in = "llama2_7b_decode_bs1", hp.prompt_ids
+        desc = {"hp": f"Llama-2-7B bs=1, 32-token prompt + {args.gen} generated tokens",
+                "be": f"BERT-large masked-LM training bs={B} seq=512",
+                "data": "synthetic (random-init Llama-2-7B bf16 weights N(0, 0.02), random-init HuggingFace "
+                        "BERT-large, uniform random tokens and labels; MMPP arrivals)",
+                "e2e": "H2D prompt (32 int64, pinned) + prefill graph + decode-step graphs + D2H generated "
+                       "tokens (pinned)"}
     else:
         from paper_2410_07381_b200 import gpt2
         hp = gpt2.BertInfer(seq=128, seed=1 + rank)
@@ -731,14 +753,19 @@ def main_colocate(args):
     prof = P.Profiler(gpu, runs=args.profile_runs)
     if args.profile_cache and os.path.exists(args.profile_cache):
         prof.load_cache(open(args.profile_cache).read())    # ref profiler.py:252-291
-    hp_w = P.KernelWork(hp_name, hp.kernel.cost(), exempt=True, kernel=hp.kernel)
+    if args.config == "c4":    # one request = prefill + G decode steps, each an exempt graph launch
+        dec_w = P.KernelWork(hp_name + ":decode_step", hp.decode_kernel.cost(), exempt=True, kernel=hp.decode_kernel)
+        hp_pipe = (P.KernelWork(hp_name + ":prefill", hp.prefill_kernel.cost(), exempt=True,
+                                kernel=hp.prefill_kernel),) + (dec_w,) * args.gen
+    else:
+        hp_pipe = (P.KernelWork(hp_name, hp.kernel.cost(), exempt=True, kernel=hp.kernel),)
     be_ws = []
     for name, dk in tr.program:
         sig = tr.work_signature(name, dk)
         prof.bind(sig, dk)
         be_ws.append(P.KernelWork(sig, dk.cost(), kernel=dk))
     threshold = int(args.threshold_us * 1000)
-    hp_lat = workloads.isolated_request_latency_ns(prof, (hp_w,))
+    hp_lat = workloads.isolated_request_latency_ns(prof, hp_pipe)
     t_prof = time.perf_counter()
     chosen = [prof.select(w.profile_key(), w.cost, threshold) for w in be_ws]
     t_prof = time.perf_counter() - t_prof
@@ -750,7 +777,7 @@ def main_colocate(args):
     def run_(tasks, cfg, horizon, **kw):
         return P.run_policy(gpu, tasks, cfg, horizon, profiler=prof, record_events=False, **kw)
 
-    def hp_task(seed, pipe=(hp_w,), lat=hp_lat, horizon=window):
+    def hp_task(seed, pipe=hp_pipe, lat=hp_lat, horizon=window):
         return P.TaskScript("hp", P.HIGH, pipe, c2_trace(args.load, lat, horizon, seed, args.burst))
 
     be_task = P.TaskScript("be", P.BEST_EFFORT, tuple(be_ws))
@@ -886,8 +913,9 @@ def main_colocate(args):
     traffic = None
     try:   # per-launch DRAM bytes from an ncu --set full capture of this kernel (shape-independent to ~1 %)
         tr_db = json.load(open(os.path.join(ROOT, "profiles", "ncu_traffic.json")))
-        for key in (f"c2:{top_name}:{top_cand.describe()}", f"c2:{top_name}:Ptb(full occupancy)",
-                    f"c2:{top_name}:Original"):
+        c = args.config
+        for key in (f"{c}:{top_name}:{top_cand.describe()}", f"{c}:{top_name}:Ptb(full occupancy)",
+                    f"{c}:{top_name}:Original"):
             if key in tr_db:
                 traffic = tr_db[key]
                 break
@@ -908,8 +936,8 @@ def main_colocate(args):
         host_out = torch.empty(hp.out.shape, dtype=hp.out.dtype).pin_memory()
         h2d = kernels.memcpy(hp_in, host_in)
         d2h = kernels.memcpy(host_out, hp.out)
-        pipe = (P.KernelWork("h2d_image", h2d.cost(), exempt=True, kernel=h2d), hp_w,
-                P.KernelWork("d2h_logits", d2h.cost(), exempt=True, kernel=d2h))
+        pipe = (P.KernelWork("h2d_image", h2d.cost(), exempt=True, kernel=h2d),) + hp_pipe + \
+            (P.KernelWork("d2h_logits", d2h.cost(), exempt=True, kernel=d2h),)
         prof.bind("h2d_image", h2d)
         prof.bind("d2h_logits", d2h)
         e2e_lat = workloads.isolated_request_latency_ns(prof, pipe)
@@ -1023,11 +1051,11 @@ def main_colocate(args):
 def main():
     args = parse()
     if args.window_ms is None:
-        args.window_ms = 100.0 if args.config == "c1" else 2000.0
+        args.window_ms = {"c1": 100.0, "c4": 8000.0}.get(args.config, 2000.0)
     if args.load is None:
         args.load = 0.5 if args.config == "c1" else 0.25
     if args.batch is None:
-        args.batch = 8 if args.config == "c3" else 64
+        args.batch = 8 if args.config in ("c3", "c4") else 64
     if args.cpu_sample_ms is None:
         args.cpu_sample_ms = 1.0 if args.config == "c1" else 4.0
     if args.impl == "reference":

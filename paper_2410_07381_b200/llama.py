@@ -81,6 +81,7 @@ class LlamaDecode:
         self.prompt_ids = torch.zeros(prompt, device=device, dtype=torch.int64)
         self.tok = torch.zeros(1, device=device, dtype=torch.int64)
         self.pos = torch.zeros(1, device=device, dtype=torch.int64)
+        self.cur = torch.zeros(1, device=device, dtype=torch.int64)
         self.out = torch.zeros(gen + 1, device=device, dtype=torch.int64)
         self.logits = torch.zeros(1, self.V, device=device, dtype=torch.float32)
         self.keys = torch.arange(self.max_len, device=device)
@@ -115,10 +116,10 @@ class LlamaDecode:
                 self.v_cache[li, :, :T] = v
                 a = F.scaled_dot_product_attention(q[None], k[None], v[None], is_causal=True)[0]
             else:
-                self.k_cache[li].index_copy_(1, self.pos, k)
-                self.v_cache[li].index_copy_(1, self.pos, v)
+                self.k_cache[li].index_copy_(1, self.cur, k)
+                self.v_cache[li].index_copy_(1, self.cur, v)
                 s = (q @ self.k_cache[li].transpose(1, 2)).float() * (1.0 / math.sqrt(D))   # [H, 1, max_len]
-                s = s.masked_fill((self.keys > self.pos)[None, None, :], float("-inf"))
+                s = s.masked_fill((self.keys > self.cur)[None, None, :], float("-inf"))
                 a = (s.softmax(-1).to(x.dtype) @ self.v_cache[li])                           # [H, 1, D]
             x = x + a.permute(1, 0, 2).reshape(T, d) @ lay["wo"].t()
             h2 = self._rms(x, lay["ln2"])
@@ -140,12 +141,16 @@ class LlamaDecode:
         self.pos.fill_(P)
 
     def _decode(self):
+        # the position saturates at the cache end: replaying the step graph on
+        # its own (profiling, cost measurement) never indexes out of bounds;
+        # a request (prefill first) never reaches it
+        self.cur.copy_(self.pos.clamp(max=self.max_len - 1))
         x = self.embed.index_select(0, self.tok)
-        cos = self.cos.index_select(0, self.pos)
-        sin = self.sin.index_select(0, self.pos)
+        cos = self.cos.index_select(0, self.cur)
+        sin = self.sin.index_select(0, self.cur)
         x = self._forward(x, cos, sin, prefill=False)
         nt = self._head(x)
-        self.out.index_copy_(0, self.pos - (self.P - 1), nt)
+        self.out.index_copy_(0, (self.cur - (self.P - 1)).clamp(max=self.G), nt)
         self.tok.copy_(nt)
         self.pos.add_(1)
 

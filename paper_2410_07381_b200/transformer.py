@@ -106,7 +106,7 @@ class TransformerTrain:
 
     def _linear_fwd(self, name, lin, x, act=0, res=None, pre=None):
         u = self._buf(self.N, lin.out)
-        self._add(name + ".gemm", K.gemm(x, lin.wb, u))
+        self._gemm_ex_splitk(name + ".gemm", x, lin.wb, u, self.N, lin.out, lin.inp)
         y = self._buf(self.N, lin.out)
         self._add(name + ".bias", K.bias_act(u, y, lin.b.w, self.N, lin.out, act=act, res=res, pre=pre))
         return y
@@ -131,15 +131,28 @@ class TransformerTrain:
             self._add(name + ".wgrad", K.gemm_mn(dy, x, p.gpart, splits=S))
         self.sgd.add(p.w, p.v, p.gpart, S, M * Nn, WEIGHT_DECAY, p.wb, None, M, Nn)
 
+    def _ws(self, numel):
+        """Shared fp32 split-K workspace: the program's kernels run strictly in
+        order, so one buffer serves every split-K GEMM; it grows by
+        reallocation (earlier kernels keep their buffer alive)."""
+        cur = getattr(self, "_wsbuf", None)
+        if cur is None or cur.numel() < numel:
+            self._wsbuf = cur = self.torch.empty(numel, dtype=self.torch.float32, device=self.device)
+        return cur[:numel]
+
     def _gemm_ex_splitk(self, name, A, B, out, M, N, Kd, b_mn=False):
-        """out (bf16) = A . B^T; a long-K GEMM (an LM-head dgrad, K = vocab)
-        runs split-K into an fp32 workspace + splitk_reduce so its logical
-        blocks stay preemptible (resnet._gemm_splits)."""
+        """out (bf16) = A . B^T.  GEMMs with few, long output tiles (an LM-head
+        dgrad with K = vocab; BERT-large's K = 4096 FFN GEMMs: 256 tiles of
+        134 MFLOP) run split-K into an fp32 workspace + splitk_reduce, so their
+        logical blocks are <= ~40 MFLOP (resnet._gemm_splits): short enough
+        for a PTB configuration to meet the turnaround threshold, where the
+        reference's fallback (least turnaround) would otherwise pick a 1/256
+        slicing at 200x the latency."""
         S = _gemm_splits(M, N, Kd)
         if S == 1:
             self._add(name, K.gemm_ex(A, B, out, M, N, Kd, b_mn=b_mn))
             return
-        ws = self.torch.empty(S * M, N, dtype=self.torch.float32, device=self.device)
+        ws = self._ws(S * M * N).view(S * M, N)
         self._add(name, K.gemm_ex(A, B, ws, M, N, Kd, b_mn=b_mn, splits=S))
         self._add(name + ".reduce", K.splitk_reduce(ws.view(S, M, N), out))
 
@@ -151,7 +164,7 @@ class TransformerTrain:
         if not need_dx:
             return None
         dx = self._buf(self.N, lin.inp)
-        self._add(name + ".dgrad", K.gemm_ex(dy, lin.wb, dx, self.N, lin.inp, lin.out, b_mn=True))
+        self._gemm_ex_splitk(name + ".dgrad", dy, lin.wb, dx, self.N, lin.inp, lin.out, b_mn=True)
         return dx
 
     def _ln_fwd(self, name, ln, x):

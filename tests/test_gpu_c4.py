@@ -95,6 +95,8 @@ def test_llama_pipeline_runs_through_runner(env):
     ref = dec.generate(dec.prompt_ids.clone())
     dec.out.zero_()
     hs = kernels.Stream(high_priority=True)
+    for _ in range(3 * dec.max_len):      # the decode step alone (as the profiler times it) stays in bounds
+        dec.decode_kernel.original(hs).wait()
     for dk in dec.pipeline():
         dk.original(hs).wait()
     assert torch.equal(dec.out, ref)

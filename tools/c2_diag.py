@@ -49,7 +49,13 @@ def main():
     load, burst = arg("--load", 0.25), arg("--burst", 4.0)
     threshold = int(arg("--threshold-us", 31.6) * 1000)
     g = torch.Generator(device="cuda").manual_seed(0)
-    if "--c3" in sys.argv:
+    if "--c4" in sys.argv:
+        from paper_2410_07381_b200 import bert, llama
+        hp = llama.LlamaDecode(prompt=32, gen=arg("--gen", 16))
+        tr = bert.BertTrain(batch=8, seq=512, lr=1e-3)
+        tr.set_batch(torch.randint(0, tr.V, (8, 512), device="cuda", generator=g),
+                     torch.randint(0, tr.V, (8, 512), device="cuda", generator=g))
+    elif "--c3" in sys.argv:
         from paper_2410_07381_b200 import gpt2
         hp = gpt2.BertInfer(seq=128)
         tr = gpt2.GPT2Train(batch=8, seq=1024, lr=1e-3)
@@ -60,13 +66,18 @@ def main():
         tr.set_batch(torch.randn(64, 3, 224, 224, device="cuda", generator=g),
                      torch.randint(0, 1000, (64,), device="cuda", generator=g))
     prof = P.Profiler(gpu, runs=2)
-    hp_w = P.KernelWork("resnet50_infer_bs1", hp.kernel.cost(), exempt=True, kernel=hp.kernel)
+    if "--c4" in sys.argv:
+        dec_w = P.KernelWork("decode_step", hp.decode_kernel.cost(), exempt=True, kernel=hp.decode_kernel)
+        hp_pipe = (P.KernelWork("prefill", hp.prefill_kernel.cost(), exempt=True, kernel=hp.prefill_kernel),) + \
+            (dec_w,) * hp.G
+    else:
+        hp_pipe = (P.KernelWork("hp_graph", hp.kernel.cost(), exempt=True, kernel=hp.kernel),)
     be_ws = []
     for name, dk in tr.program:
         sig = tr.work_signature(name, dk)
         prof.bind(sig, dk)
         be_ws.append(P.KernelWork(sig, dk.cost(), kernel=dk))
-    hp_lat = workloads.isolated_request_latency_ns(prof, (hp_w,))
+    hp_lat = workloads.isolated_request_latency_ns(prof, hp_pipe)
     chosen = [prof.select(w.profile_key(), w.cost, threshold) for w in be_ws]
     out = {"hp_isolated_us": hp_lat / 1e3,
            "choices": dict(collections.Counter(c.describe().split("(")[0] for c in chosen))}
@@ -82,20 +93,23 @@ def main():
         worst.append((ch.kernel_latency_ns - o.kernel_latency_ns, w.kernel_id, c.describe(), o.kernel_latency_ns,
                       ch.kernel_latency_ns, ch.turnaround_estimate_ns))
     worst.sort(reverse=True)
+    out["sliced_choices"] = sorted({(x[1], x[2], x[3], x[4], x[5]) for x in worst if x[2].startswith("Sliced")},
+                                   key=lambda t: -t[3])[:20]
     out["profiled_step_ms"] = {"original": lat_o / 1e6, "chosen": lat_c / 1e6}
     out["worst_choices"] = [list(x) for x in worst[:12]]
     arr = c2_trace(load, hp_lat, window, 0, burst)
-    hp_task = P.TaskScript("hp", P.HIGH, (hp_w,), arr)
+    hp_task = P.TaskScript("hp", P.HIGH, hp_pipe, arr)
     be_task = P.TaskScript("be", P.BEST_EFFORT, tuple(be_ws))
-    for label, tasks, pol in (("solo", [hp_task], "Tally"), ("tally", [hp_task, be_task], "Tally"),
+    for label, tasks, pol in (("be_solo", [be_task], "Tally"), ("solo", [hp_task], "Tally"),
+                              ("tally", [hp_task, be_task], "Tally"),
                               ("kp", [hp_task, be_task], "KernelPriority")):
         cfg = P.SchedulerConfig(policy=pol, turnaround_threshold_ns=threshold)
         clk = ClockMap(dev)
         res = P.run_policy(gpu, tasks, cfg, window, profiler=prof, record_events=False, options={"trace": 1})
         clk.close()
-        hp_l = [r for r in res.launches if r["priority"] == 0]
+        hp_l = [r for r in res.launches if r["priority"] == 0][::len(hp_pipe)]   # first step of each request
         be_l = [r for r in res.launches if r["priority"] != 0]
-        reqs = res.requests["hp"]
+        reqs = res.requests.get("hp", [])
         q, iss, st, run, nt, tot = [], [], [], [], [], []
         for (a, c), L in zip(reqs, hp_l):
             q.append(L["submit_ns"] - a)
