@@ -12,7 +12,8 @@ import ctypes as C
 import os
 
 HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(HERE, "_lib", "libtally_b200.so")
+# TALLY_LIB_PATH: an alternative build of the same library (tools/gemm_variants.py experiments)
+LIB_PATH = os.environ.get("TALLY_LIB_PATH") or os.path.join(HERE, "_lib", "libtally_b200.so")
 
 OK = 0
 EINVAL = -22

@@ -26,6 +26,7 @@
 #include <cuda_bf16.h>
 
 #include <cstdio>
+#include <cstdlib>
 
 #include "registry.h"
 #include "runtime.h"
@@ -206,6 +207,18 @@ using CfgTf32x3N64 = CfgTf32x3T<64, 4>;
 // bf16 operands, fp32 TMEM accumulation; BN = 128 or 64 (N % 128 != 0, e.g.
 // 64-channel convolutions), output bf16 (activations) or fp32 (split-K
 // weight-gradient partials, logits)
+#ifndef TALLY_STAGES_BF16_N128
+#define TALLY_STAGES_BF16_N128 2
+#endif
+#ifndef TALLY_STAGES_F32_N128
+#define TALLY_STAGES_F32_N128 3
+#endif
+#ifndef TALLY_STAGES_BF16_N64
+#define TALLY_STAGES_BF16_N64 3
+#endif
+#ifndef TALLY_STAGES_F32_N64
+#define TALLY_STAGES_F32_N64 4
+#endif
 template <int BN_, class OutT_, bool A_MN_ = false, bool B_MN_ = false>
 struct CfgBf16T {
   static constexpr int KIND = 1;
@@ -220,7 +233,8 @@ struct CfgBf16T {
   // untransformed launch (one output tile per CTA) overlaps one CTA's
   // prologue / pipeline fill with the other's tile, and high-priority CTAs
   // find room next to a best-effort one
-  static constexpr int STAGES = BN == 128 ? (sizeof(OutT_) == 2 ? 2 : 3) : (sizeof(OutT_) == 2 ? 3 : 4);
+  static constexpr int STAGES = BN == 128 ? (sizeof(OutT_) == 2 ? TALLY_STAGES_BF16_N128 : TALLY_STAGES_F32_N128)
+                                          : (sizeof(OutT_) == 2 ? TALLY_STAGES_BF16_N64 : TALLY_STAGES_F32_N64);
   static constexpr int UMMA_K = 16;
   // the whole (split) K range accumulates in one TMEM buffer (no fp32
   // promotion chunks at the 1e-2 bf16 budget): 2 x BN columns, leaving TMEM
@@ -280,40 +294,49 @@ struct alignas(64) GemmParams {
   long long off[6][2];          // (row, col) origins of A, B, C: [a_row, a_col, b_row, b_col, c_row, c_col]
 };
 
-__device__ __forceinline__ void tile_coords(long long t, const GemmParams& p, int& mb, int& nb) {
+__device__ __forceinline__ void tile_coords(unsigned t, const GemmParams& p, int& mb, int& nb) {
   // grouped rasterisation: GROUP_M row-blocks share each column sweep
-  const int per_group = GROUP_M * p.tiles_n;
-  const int g = (int)(t / per_group);
-  const int first_m = g * GROUP_M;
-  const int gm = min(p.tiles_m - first_m, GROUP_M);
-  const int r = (int)(t % per_group);
-  mb = first_m + r % gm;
-  nb = r / gm;
+  const unsigned per_group = GROUP_M * (unsigned)p.tiles_n;
+  const unsigned g = t / per_group;
+  const int first_m = (int)g * GROUP_M;
+  const unsigned gm = (unsigned)min(p.tiles_m - first_m, GROUP_M);
+  const unsigned r = t - g * per_group;
+  const unsigned nq = r / gm;
+  mb = first_m + (int)(r - nq * gm);
+  nb = (int)nq;
 }
 
-// Logical block t -> (output tile, K range).  With split-K the block index is
-// split-major: t = split * tiles + tile; split s covers k-blocks
-// [s * kb_per_split, min(KB, (s + 1) * kb_per_split)).
+// Logical block t -> (output tile, K range, batch).  With split-K the block
+// index is split-major: t = split * tiles + tile; split s covers k-blocks
+// [s * kb_per_split, min(KB, (s + 1) * kb_per_split)).  The producer warp
+// computes it once per tile (32-bit divisions; total_tiles < 2^31 is checked
+// at bind time) and publishes it to the MMA and epilogue warps in shared
+// memory: recomputing it per warp with 64-bit divisions was ~35 % of the
+// stall samples of short-K tiles (ncu, K = 64 dgrad).
 struct TileWork {
-  int mb, nb, split, kbeg, kend, nch, z;
+  int mb, nb, split, kbeg, kend, nch, zb, zh;
 };
-__device__ __forceinline__ TileWork tile_work(long long t, const GemmParams& p, int KB) {
+__device__ __forceinline__ TileWork tile_work(long long t_, const GemmParams& p, int KB) {
   TileWork w;
-  const long long tiles = (long long)p.tiles_m * p.tiles_n;
-  const long long per_batch = tiles * p.splits;
-  w.z = (int)(t / per_batch);
-  t -= (long long)w.z * per_batch;
-  w.split = (int)(t / tiles);
-  tile_coords(t - (long long)w.split * tiles, p, w.mb, w.nb);
+  const unsigned tiles = (unsigned)p.tiles_m * (unsigned)p.tiles_n;
+  const unsigned per_batch = tiles * (unsigned)p.splits;
+  unsigned t = (unsigned)t_;
+  const unsigned z = t / per_batch;
+  t -= z * per_batch;
+  const unsigned split = t / tiles;
+  w.split = (int)split;
+  tile_coords(t - split * tiles, p, w.mb, w.nb);
   w.kbeg = w.split * p.kb_per_split;
   w.kend = min(KB, w.kbeg + p.kb_per_split);
-  w.nch = (w.kend - w.kbeg + p.kchunk - 1) / p.kchunk;
+  w.nch = p.kchunk == p.kb_per_split ? 1 : (w.kend - w.kbeg + p.kchunk - 1) / p.kchunk;
+  w.zb = (int)(z / (unsigned)p.hdiv);
+  w.zh = (int)(z - (unsigned)w.zb * (unsigned)p.hdiv);
   return w;
 }
 
-// origin offset (elements) of operand coordinate `which` for batch z
-__device__ __forceinline__ int goff(const GemmParams& p, int which, int z) {
-  return (int)(p.off[which][0] * (z / p.hdiv) + p.off[which][1] * (z % p.hdiv));
+// origin offset (elements) of operand coordinate `which` for batch (zb, zh)
+__device__ __forceinline__ int goff(const GemmParams& p, int which, const TileWork& w) {
+  return (int)(p.off[which][0] * w.zb + p.off[which][1] * w.zh);
 }
 
 template <class Cfg, int MODE, class ShapeArgs>
@@ -331,6 +354,7 @@ __global__ void __launch_bounds__(kThreads, Cfg::KIND == 1 ? 2 : 1) k_gemm(const
   int* tile_c0 = reinterpret_cast<int*>(tile_slot + kSlots);                  // first chunk (resumed tiles)
   int* tile_cut = tile_c0 + kSlots;                                           // chunk the tile stops before
   uint32_t* tmem_base_slot = reinterpret_cast<uint32_t*>(tile_cut + kSlots);
+  TileWork* tile_w = reinterpret_cast<TileWork*>(tmem_base_slot + 4);          // [kSlots], producer-computed
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int KB = (p.k + Cfg::BK - 1) / Cfg::BK;
@@ -435,6 +459,7 @@ __global__ void __launch_bounds__(kThreads, Cfg::KIND == 1 ? 2 : 1) k_gemm(const
         tile_slot[j] = t;
         tile_c0[j] = c0;
         const TileWork w = tile_work(t < 0 ? 0 : t, p, KB);
+        tile_w[j] = w;
         tile_cut[j] = w.nch;
         mbar_arrive(&tile_full[j]);
         if (t < 0) break;
@@ -475,7 +500,7 @@ __global__ void __launch_bounds__(kThreads, Cfg::KIND == 1 ? 2 : 1) k_gemm(const
               tma_load_2d(base + 2 * Cfg::A_BYTES + Cfg::B_BYTES, &p.b_lo, &full[st], kx, nb * Cfg::BN);
             } else {
               // (batched layouts: every operand's origin moves with the batch)
-              const int ar = goff(p, 0, w.z), ac = goff(p, 1, w.z), br = goff(p, 2, w.z), bc = goff(p, 3, w.z);
+              const int ar = goff(p, 0, w), ac = goff(p, 1, w), br = goff(p, 2, w), bc = goff(p, 3, w);
               if constexpr (Cfg::A_MN) {
                 // boxes of 64 M-elements x BK K-rows, 8 KB each
 #pragma unroll
@@ -515,7 +540,7 @@ __global__ void __launch_bounds__(kThreads, Cfg::KIND == 1 ? 2 : 1) k_gemm(const
           mbar_arrive(&tile_empty[j]);
           break;
         }
-        const TileWork w = tile_work(t, p, KB);
+        const TileWork w = tile_w[j];
         for (int c = c0; c < w.nch; ++c, ++ci) {
           const int acc = ci & 1;
           if (ci >= 2) mbar_wait(&tmem_empty[acc], ((ci >> 1) - 1) & 1);
@@ -583,10 +608,10 @@ __global__ void __launch_bounds__(kThreads, Cfg::KIND == 1 ? 2 : 1) k_gemm(const
         if (lane == 0) mbar_arrive(&tile_empty[j]);
         break;
       }
-      const TileWork w = tile_work(t, p, KB);
+      const TileWork w = tile_w[j];
       const int row = w.mb * Cfg::BM + q * 32 + lane;
       const bool row_ok = row < p.m;   // M tail: TMA zero-fills the rows past M, stores skip them
-      const int cr = goff(p, 4, w.z), cc = goff(p, 5, w.z);
+      const int cr = goff(p, 4, w), cc = goff(p, 5, w);
       typename Cfg::OutT* crow = reinterpret_cast<typename Cfg::OutT*>(p.c) + (size_t)w.split * p.split_stride +
                                  (size_t)(cr + (row_ok ? row : 0)) * p.ldc + (size_t)(cc + w.nb * Cfg::BN);
       const uint32_t lane_base = tmem_base + ((uint32_t)(q * 32) << 16);
@@ -857,8 +882,21 @@ static int bind_gemm(const tally_kernel_args* a, Instance* inst, bool split) {
   // short-K tiles (<= 2 k-blocks, ~1 us each): 4 tiles per logical block, so
   // an untransformed CTA pipelines 4 tiles behind one prologue and a PTB
   // claim covers ~4 us of work; longer tiles are one logical block each
-  p.tpb = (Cfg::KIND == 1 && p.kb_per_split <= 2) ? 4 : 1;
+  {
+    static const int target = [] {
+      const char* e = getenv("TALLY_GEMM_BLOCK_KB");   // experiment knob: k-blocks per logical block
+      return e ? atoi(e) : 8;
+    }();
+    static const int old_rule = getenv("TALLY_GEMM_TPB_OLD") != nullptr;
+    p.tpb = Cfg::KIND != 1 ? 1
+          : old_rule ? (p.kb_per_split <= 2 ? 4 : 1)
+                     : max(1, min(8, (target + p.kb_per_split - 1) / p.kb_per_split));
+  }
   p.total_tiles = (long long)p.tiles_m * p.tiles_n * p.splits * p.batches;
+  if (p.total_tiles >= (1ll << 31)) {
+    set_error("gemm: %lld tiles (>= 2^31)", p.total_tiles);
+    return TALLY_EINVAL;
+  }
   p.resume = nullptr;
   // i[3] = 1: block-granular preemption only (no resume ring)
   if (Cfg::KIND == 0 && a->i[3] == 0) {
