@@ -245,9 +245,9 @@ struct CfgBf16T {
   // as stored (no transposes); P . V and dY . W read V / W as stored
   static constexpr bool A_MN = A_MN_, B_MN = B_MN_;
   using OutT = OutT_;
-  // bf16 output: each epilogue warp stages its 32 x BN tile rows in shared
-  // memory (XOR-swizzled 16 B chunks) and writes whole rows, coalesced
-  static constexpr int EPI_BYTES = sizeof(OutT_) == 2 ? 4 * 32 * BN * 2 : 0;
+  // bf16 output: each epilogue warp stages 32 rows x 64 columns at a time in
+  // shared memory (XOR-swizzled 16 B chunks) and writes whole row segments
+  static constexpr int EPI_BYTES = sizeof(OutT_) == 2 ? 8 * 32 * 64 * 2 : 0;   // 4 KB per epilogue warp (32 KB)
 };
 using CfgBf16 = CfgBf16T<128, __nv_bfloat16>;
 using CfgBf16N64 = CfgBf16T<64, __nv_bfloat16>;
@@ -365,7 +365,7 @@ __global__ void __launch_bounds__(kThreads, Cfg::KIND == 1 ? 2 : 1) k_gemm(const
     for (int i = 0; i < Cfg::STAGES; ++i) { mbar_init(&full[i], 1); mbar_init(&empty[i], 1); }
     for (int i = 0; i < 2; ++i) {
       mbar_init(&tmem_full[i], 1);
-      mbar_init(&tmem_empty[i], kEpiWarps);
+      mbar_init(&tmem_empty[i], (Cfg::KIND == 1 && Cfg::BN == 64) ? kEpiWarps / 2 : kEpiWarps);   // one group per tile
     }
     for (int i = 0; i < kSlots; ++i) {
       mbar_init(&tile_full[i], 1);
@@ -592,6 +592,93 @@ __global__ void __launch_bounds__(kThreads, Cfg::KIND == 1 ? 2 : 1) k_gemm(const
       }
     }
     __syncwarp();
+  } else if constexpr (Cfg::KIND == 1 && Cfg::BN == 64) {
+    // -------------------------------------------------- epilogue (warps 2..9), 64-wide bf16-operand tiles
+    // Two groups of four warps take alternate tiles (= the two TMEM
+    // accumulators: one K chunk per tile), so two tiles drain concurrently;
+    // each warp owns its TMEM lane quarter (32 rows) across all BN columns.
+    // bf16 output is staged 64 columns at a time in the warp's own 4 KB of
+    // shared memory (16 B chunks XOR-swizzled by row) and written back as
+    // whole 128 B row segments; fp32 rows go straight from registers.  (For
+    // 64-wide tiles this beats eight warps on one tile: K = 64 dgrad 78 -> 74
+    // us; for 128-wide tiles it does not -- 35 -> 39 us at K = 64, N = 256.)
+    const int q = warp & 3;
+    const int grp = (warp - 2) >> 2;
+    unsigned char* wstage = epi_smem + (size_t)(warp - 2) * (32 * 64 * 2);
+    for (int i = 0;; ++i) {
+      const int j = i % kSlots;
+      mbar_wait(&tile_full[j], (i / kSlots) & 1);
+      const long long t = tile_slot[j];
+      if (t < 0) {
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&tile_empty[j]);
+        break;
+      }
+      if ((i & 1) == grp) {
+        const int acc = i & 1;
+        const TileWork w = tile_w[j];
+        const int row0 = w.mb * Cfg::BM + q * 32;
+        const int cr = goff(p, 4, w), cc = goff(p, 5, w);
+        typename Cfg::OutT* cbase = reinterpret_cast<typename Cfg::OutT*>(p.c) + (size_t)w.split * p.split_stride +
+                                    (size_t)cr * p.ldc + (size_t)(cc + w.nb * Cfg::BN);
+        const uint32_t lane_base = tmem_base + ((uint32_t)(q * 32) << 16) + (uint32_t)(acc * Cfg::BN);
+        mbar_wait(&tmem_full[acc], (i >> 1) & 1);
+        fence_after();
+        if constexpr (sizeof(typename Cfg::OutT) == 4) {
+          const bool row_ok = row0 + lane < p.m;
+          float* crow = reinterpret_cast<float*>(cbase) + (size_t)(row_ok ? row0 + lane : 0) * p.ldc;
+#pragma unroll 1
+          for (int c1 = 0; c1 < Cfg::BN; c1 += 32) {
+            uint32_t r[32];
+            tmem_ld32(lane_base + (uint32_t)c1, r);
+            if (row_ok) {
+#pragma unroll
+              for (int v = 0; v < 8; ++v)
+                st_out16(crow + c1 + 4 * v, make_uint4(r[4 * v], r[4 * v + 1], r[4 * v + 2], r[4 * v + 3]));
+            }
+          }
+          fence_before();
+          __syncwarp();
+          if (lane == 0) mbar_arrive(&tmem_empty[acc]);
+        } else {
+#pragma unroll 1
+          for (int h = 0; h < Cfg::BN; h += 64) {
+            uint32_t r[2][32];
+            tmem_ld32(lane_base + (uint32_t)h, r[0]);
+            tmem_ld32(lane_base + (uint32_t)(h + 32), r[1]);
+            if (h + 64 >= Cfg::BN) {   // the accumulator is drained: hand it back to the MMA warp
+              fence_before();
+              __syncwarp();
+              if (lane == 0) mbar_arrive(&tmem_empty[acc]);
+            }
+            unsigned char* srow = wstage + (size_t)lane * 128;
+#pragma unroll
+            for (int v = 0; v < 8; ++v) {
+              uint32_t wv[4];
+#pragma unroll
+              for (int e = 0; e < 4; ++e) {
+                const int k = 8 * (v & 3) + 2 * e;
+                __nv_bfloat162 b = __floats2bfloat162_rn(__uint_as_float(r[v >> 2][k]), __uint_as_float(r[v >> 2][k + 1]));
+                wv[e] = *reinterpret_cast<uint32_t*>(&b);
+              }
+              *reinterpret_cast<uint4*>(srow + ((v ^ (lane & 7)) << 4)) = make_uint4(wv[0], wv[1], wv[2], wv[3]);
+            }
+            __syncwarp();
+            // 32 rows x 8 chunks: each instruction writes 4 whole 128 B row segments
+            __nv_bfloat16* cb = reinterpret_cast<__nv_bfloat16*>(cbase) + h;
+#pragma unroll
+            for (int it2 = 0; it2 < 8; ++it2) {
+              const int rr = it2 * 4 + (lane >> 3), ch = lane & 7;
+              const uint4 v = *reinterpret_cast<const uint4*>(wstage + (size_t)rr * 128 + ((ch ^ (rr & 7)) << 4));
+              if (row0 + rr < p.m) st_out16(cb + (size_t)(row0 + rr) * p.ldc + ch * 8, v);
+            }
+            __syncwarp();
+          }
+        }
+      }
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&tile_empty[j]);
+    }
   } else {
     // -------------------------------------------------- epilogue (warps 2..9)
     const int q = warp & 3;                     // TMEM lane quarter this warp may access
