@@ -69,7 +69,7 @@ def parse():
                          "c3 = configs[2] (BERT-base HP seq 128 + GPT-2 small training); "
                          "c4 = configs[3] (Llama-2-7B decode bs=1 HP + BERT-large training); "
                          "c1 = the synthetic vecadd + SGEMM pair")
-    ap.add_argument("--window-ms", type=float, default=None, help="default 100 (c1) / 2000 (c2, c3) / 8000 (c4)")
+    ap.add_argument("--window-ms", type=float, default=None, help="default 100 (c1) / 2000 (c2) / 4000 (c3) / 8000 (c4)")
     ap.add_argument("--gen", type=int, default=16, help="c4: tokens generated per HP request (after a 32-token "
                                                         "prompt)")
     ap.add_argument("--load", type=float, default=None, help="mean HP load; default 0.5 (c1) / 0.25 (c2)")
@@ -127,7 +127,7 @@ class Clocks:
             self.fh = open(self.path, "w")
             self.proc = subprocess.Popen(
                 ["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.FIELDS}",
-                 "--format=csv,noheader,nounits", "-lms", "200"], stdout=self.fh,
+                 "--format=csv,noheader,nounits", "-lms", "1000"], stdout=self.fh,
                 stderr=subprocess.DEVNULL)
         except OSError:
             self.proc = None
@@ -800,9 +800,10 @@ def main_colocate(args):
     clkmap = ClockMap(dev)
 
     # --- timed region: K co-located windows ----------------------------------------
-    # Each step k is preceded by the solo-HP window of the same arrival trace
-    # (paired measurement: the HP graph's speed drifts by a few percent over a
-    # run, so solo and co-located p99 are taken side by side).  Every step is
+    # Each step k is paired with the solo-HP window of the same arrival trace,
+    # run just before it (k even) or just after it (k odd) (paired
+    # measurement: the HP graph's speed drifts by a few percent over a run, so
+    # solo and co-located p99 are taken side by side).  Every step is
     # bracketed by a barrier + synchronize; ms_per_step is the sum of the K
     # co-located windows' device time / K.
     clocks = Clocks(local)
@@ -812,8 +813,10 @@ def main_colocate(args):
     elapsed_ms = 0.0
     host_s = 0.0
     for k in range(args.steps):
-        solo_res.append(run_([hp_task(k)], tally, window))
-        solo_lat += lat_after_warm(solo_res[-1])
+        # ABBA order (solo-co, co-solo, ...): a slow drift of the HP graph's
+        # speed over the run does not bias the paired difference
+        if k % 2 == 0:
+            solo_res.append(run_([hp_task(k)], tally, window))
         if dist is not None:
             dist.barrier()
         torch.cuda.synchronize()
@@ -824,6 +827,9 @@ def main_colocate(args):
         torch.cuda.synchronize()
         host_s += time.perf_counter() - t_host0
         elapsed_ms += ev0.elapsed_time(ev1)
+        if k % 2 == 1:
+            solo_res.append(run_([hp_task(k)], tally, window))
+        solo_lat += lat_after_warm(solo_res[-1])
     clk = clocks.stop()
     if dist is not None:
         t = torch.tensor([elapsed_ms], device=red_dev)
@@ -943,10 +949,13 @@ def main_colocate(args):
         e2e_lat = workloads.isolated_request_latency_ns(prof, pipe)
         e_solo, e_co, reqs = [], [], 0
         for k in range(args.steps):
-            e_solo += lat_after_warm(run_([hp_task(k, pipe, e2e_lat)], tally, window))
+            if k % 2 == 0:
+                e_solo += lat_after_warm(run_([hp_task(k, pipe, e2e_lat)], tally, window))
             r = run_([hp_task(k, pipe, e2e_lat), be_task], tally, window)
             reqs += len(r.requests["hp"])
             e_co += lat_after_warm(r)
+            if k % 2 == 1:
+                e_solo += lat_after_warm(run_([hp_task(k, pipe, e2e_lat)], tally, window))
         if e_solo and e_co:
             e2e = {"value": 100.0 * (p99(e_co) / p99(e_solo) - 1.0), "unit": "%",
                    "h2d_bytes_per_step": int(reqs / args.steps * host_in.numel() * host_in.element_size()),
@@ -962,11 +971,14 @@ def main_colocate(args):
             cfg = P.SchedulerConfig(policy=pol)
             lat, rate = [], []
             sl = []
-            for k in range(args.steps):     # paired, as the Tally measurement
-                sl += lat_after_warm(run_([hp_task(k)], cfg, window))
+            for k in range(args.steps):     # paired (ABBA), as the Tally measurement
+                if k % 2 == 0:
+                    sl += lat_after_warm(run_([hp_task(k)], cfg, window))
                 r = run_([hp_task(k), be_task], cfg, window)
                 lat += lat_after_warm(r)
                 rate.append(be_rate(r))
+                if k % 2 == 1:
+                    sl += lat_after_warm(run_([hp_task(k)], cfg, window))
             baselines[pol] = {"p99_overhead_pct": 100.0 * (p99(lat) / p99(sl) - 1.0),
                               "be_throughput_pct": frac(sum(rate) / len(rate), be_untransformed)}
 
@@ -1051,7 +1063,7 @@ def main_colocate(args):
 def main():
     args = parse()
     if args.window_ms is None:
-        args.window_ms = {"c1": 100.0, "c4": 8000.0}.get(args.config, 2000.0)
+        args.window_ms = {"c1": 100.0, "c3": 4000.0, "c4": 8000.0}.get(args.config, 2000.0)
     if args.load is None:
         args.load = 0.5 if args.config == "c1" else 0.25
     if args.batch is None:
