@@ -1,7 +1,8 @@
-"""Build variants of libtally_b200.so that differ only in kernels_gemm.cu
-compile-time constants (experiments; the product build is build.py):
+"""Build variants of libtally_b200.so that differ only in one source file's
+compile-time constants (default kernels_gemm.cu; experiments -- the product
+build is build.py):
 
-    python tools/gemm_variants.py NAME -DTALLY_STAGES_BF16_N128=4 ...
+    python tools/gemm_variants.py NAME [--src=kernels_nn.cu] -DTALLY_STAGES_BF16_N128=4 ...
     TALLY_LIB_PATH=paper_2410_07381_b200/_lib/variants/NAME.so python tools/gemm_shapes.py
 """
 
@@ -19,13 +20,16 @@ from paper_2410_07381_b200 import build as B  # noqa: E402
 
 def main():
     name, defs = sys.argv[1], sys.argv[2:]
+    src = "kernels_gemm.cu"
+    if defs and defs[0].startswith("--src="):
+        src, defs = defs[0][6:], defs[1:]
     B.build()
     vdir = os.path.join(B.HERE, "_lib", "variants")
     os.makedirs(vdir, exist_ok=True)
-    obj = os.path.join(vdir, name + "_gemm.o")
-    cmd = [B.NVCC] + B.CU_FLAGS + defs + ["-c", os.path.join(B.CSRC, "kernels_gemm.cu"), "-o", obj]
+    obj = os.path.join(vdir, name + "_" + src + ".o")
+    cmd = [B.NVCC] + B.CU_FLAGS + defs + ["-c", os.path.join(B.CSRC, src), "-o", obj]
     subprocess.run(cmd, check=True)
-    objs = [obj if s == "kernels_gemm.cu" else os.path.join(B.OBJ, s + ".o") for s in B.SOURCES]
+    objs = [obj if s == src else os.path.join(B.OBJ, s + ".o") for s in B.SOURCES]
     lib = os.path.join(vdir, name + ".so")
     subprocess.run([B.NVCC] + B.ARCH + ["-shared", "-o", lib] + objs + ["-lcudart", "-lpthread", "-ldl", "-lrt"],
                    check=True)
