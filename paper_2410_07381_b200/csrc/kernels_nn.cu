@@ -96,8 +96,16 @@ struct Geometry {
 };
 
 struct Im2Col {
+  // Index math once per block, not per vector: the block's output rows
+  // (n, oh, ow) and the column vectors (kh, kw, c) are decoded into two
+  // shared-memory tables first (32-bit divisions), then every thread streams
+  // 16 B vectors with one division per vector.  (Per-vector 64-bit divisions
+  // made the kernel instruction-bound at ~2 TB/s.)
   static constexpr int kThreads = 256;
   static constexpr int kMinBlocks = 4;   // register cap: 4+ resident CTAs per SM
+  static constexpr int kMaxRows = kVecPerBlock / 8;   // rpb <= 1024 / kv, kv >= 8
+  static constexpr int kMaxKv = 1024;
+  static constexpr int kSmem = kMaxRows * 16 + kMaxKv * 4;
   struct Params {
     const uint4* x;
     uint4* col;
@@ -105,39 +113,58 @@ struct Im2Col {
     long long rows;   // N*OH*OW
     int rpb;          // output rows per logical block
   };
-  static __device__ __forceinline__ void run(const Params& p, uint3 bidx, uint3, char*) {
+  static __device__ __forceinline__ void run(const Params& p, uint3 bidx, uint3, char* smem) {
     const Geometry& g = p.g;
-    const int kv = g.Kp >> 3, cv = g.C >> 3;
+    const unsigned kv = (unsigned)(g.Kp >> 3);
+    const int cv = g.C >> 3;
     const long long r0 = (long long)bidx.x * p.rpb;
-    const int total = p.rpb * kv;
-    const int kwc = g.KW * g.C;
-    for (int i0 = 0; i0 < total; i0 += kThreads * kIlp) {
+    const int nrow = (int)min((long long)p.rpb, p.rows - r0);
+    int4* rowt = reinterpret_cast<int4*>(smem);                       // {pixel base, ih0, iw0, -}
+    int* colt = reinterpret_cast<int*>(smem + kMaxRows * 16);         // kh | kw << 8 | c8 << 16, or -1
+    for (int rr = threadIdx.x; rr < nrow; rr += kThreads) {
+      const unsigned r = (unsigned)(r0 + rr);
+      const unsigned t = r / (unsigned)g.OW, ow = r - t * (unsigned)g.OW;
+      const unsigned n = t / (unsigned)g.OH, oh = t - n * (unsigned)g.OH;
+      rowt[rr] = make_int4((int)n * g.H, (int)oh * g.stride - g.pad, (int)ow * g.stride - g.pad, 0);
+    }
+    const unsigned kwc = (unsigned)(g.KW * g.C);
+    for (unsigned j = threadIdx.x; j < kv; j += kThreads) {
+      const unsigned k = j << 3;
+      int e = -1;
+      if (k < (unsigned)g.K) {
+        const unsigned kh = k / kwc, rem = k - kh * kwc;
+        const unsigned kw = rem / (unsigned)g.C, c = rem - kw * (unsigned)g.C;
+        e = (int)(kh | (kw << 8) | ((c >> 3) << 16));
+      }
+      colt[j] = e;
+    }
+    __syncthreads();
+    const unsigned total = (unsigned)nrow * kv;
+    uint4* dst0 = p.col + r0 * kv;
+    for (unsigned i0 = 0; i0 < total; i0 += kThreads * kIlp) {
       uint4 v[kIlp];
-      long long dst[kIlp];
 #pragma unroll
       for (int u = 0; u < kIlp; ++u) {
-        const int i = i0 + u * kThreads + threadIdx.x;
-        const int rr = i / kv, j = i - rr * kv;
-        const long long r = r0 + rr;
-        dst[u] = (i < total && r < p.rows) ? r * kv + j : -1;
+        const unsigned i = i0 + u * kThreads + threadIdx.x;
         v[u] = make_uint4(0u, 0u, 0u, 0u);
-        const int k = j << 3;
-        if (dst[u] >= 0 && k < g.K) {
-          const int ow = (int)(r % g.OW);
-          const long long t = r / g.OW;
-          const int oh = (int)(t % g.OH);
-          const int n = (int)(t / g.OH);
-          const int kh = k / kwc, rem = k - kh * kwc;
-          const int kw = rem / g.C, c = rem - kw * g.C;
-          const int ih = oh * g.stride - g.pad + kh, iw = ow * g.stride - g.pad + kw;
-          if (ih >= 0 && ih < g.H && iw >= 0 && iw < g.W)
-            v[u] = ld16(p.x + (((long long)n * g.H + ih) * g.W + iw) * cv + (c >> 3));
+        if (i < total) {
+          const unsigned rr = i / kv, j = i - rr * kv;
+          const int e = colt[j];
+          if (e >= 0) {
+            const int4 rw = rowt[rr];
+            const int ih = rw.y + (e & 0xff), iw = rw.z + ((e >> 8) & 0xff);
+            if (ih >= 0 && ih < g.H && iw >= 0 && iw < g.W)
+              v[u] = ld16(p.x + ((long long)(rw.x + ih) * g.W + iw) * cv + (e >> 16));
+          }
         }
       }
 #pragma unroll
-      for (int u = 0; u < kIlp; ++u)
-        if (dst[u] >= 0) st16(p.col + dst[u], v[u]);
+      for (int u = 0; u < kIlp; ++u) {
+        const unsigned i = i0 + u * kThreads + threadIdx.x;
+        if (i < total) st16(dst0 + i, v[u]);
+      }
     }
+    __syncthreads();   // the tables are rebuilt by the next logical block of a PTB worker
   }
 };
 
@@ -158,12 +185,14 @@ struct Col2Im {
     for (int i = threadIdx.x; i < kCol2ImVec; i += kThreads) {
       const long long v = v0 + i;
       if (v >= p.nvec) break;
-      const int c8 = (int)(v % cv);
-      const long long pix = v / cv;
-      const int iw = (int)(pix % g.W);
-      const long long t = pix / g.W;
-      const int ih = (int)(t % g.H);
-      const int n = (int)(t / g.H);
+      // 32-bit decode (nvec < 2^31, checked at bind time)
+      const unsigned pix = (unsigned)v / (unsigned)cv;
+      const int c8 = (int)((unsigned)v - pix * (unsigned)cv);
+      const unsigned t = pix / (unsigned)g.W;
+      const int iw = (int)(pix - t * (unsigned)g.W);
+      const unsigned n_ = t / (unsigned)g.H;
+      const int ih = (int)(t - n_ * (unsigned)g.H);
+      const int n = (int)n_;
       float acc[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
       for (int kh = 0; kh < g.KH; ++kh) {
         const int ohn = ih + g.pad - kh;
@@ -1125,7 +1154,12 @@ static int bind_im2col(const tally_kernel_args* a, Instance* inst) {
   if (!p.x || !p.col || !aligned16(p.x) || !aligned16(p.col)) { set_error("im2col: 16-byte aligned x, col"); return TALLY_EINVAL; }
   p.rows = (long long)p.g.N * p.g.OH * p.g.OW;
   p.rpb = max(1, nn::kVecPerBlock / (p.g.Kp / 8));
-  finish(inst, p, (p.rows + p.rpb - 1) / p.rpb, nn::Im2Col::kThreads, 0,
+  if (p.g.Kp / 8 > nn::Im2Col::kMaxKv || p.rows * (p.g.Kp / 8) >= (1ll << 31) ||
+      (long long)p.g.N * p.g.H * p.g.W >= (1ll << 31)) {
+    set_error("im2col: K <= 8192 and fewer than 2^31 column vectors / pixels");
+    return TALLY_EINVAL;
+  }
+  finish(inst, p, (p.rows + p.rpb - 1) / p.rpb, nn::Im2Col::kThreads, nn::Im2Col::kSmem,
          2.0 * ((double)p.rows * p.g.Kp + (double)p.g.N * p.g.H * p.g.W * p.g.C));
   return TALLY_OK;
 }
@@ -1139,6 +1173,7 @@ static int bind_col2im(const tally_kernel_args* a, Instance* inst) {
   p.dx = static_cast<uint4*>(a->ptr[1]);
   if (!p.col || !p.dx || !aligned16(p.col) || !aligned16(p.dx)) { set_error("col2im: 16-byte aligned col, dx"); return TALLY_EINVAL; }
   p.nvec = (long long)p.g.N * p.g.H * p.g.W * (p.g.C / 8);
+  if (p.nvec >= (1ll << 31)) { set_error("col2im: fewer than 2^31 vectors"); return TALLY_EINVAL; }
   finish(inst, p, (p.nvec + nn::kCol2ImVec - 1) / nn::kCol2ImVec, nn::Col2Im::kThreads, 0,
          2.0 * ((double)p.g.N * p.g.OH * p.g.OW * p.g.Kp + 8.0 * p.nvec));
   return TALLY_OK;
