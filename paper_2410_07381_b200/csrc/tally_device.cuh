@@ -127,8 +127,18 @@ __device__ __forceinline__ float4 ld_stream(const float4* p) {
 }
 
 __device__ __forceinline__ uint3 delinearize(unsigned long long t, uint3 g) {
-  // ref ir/core.py:59-65: x fastest
+  // ref ir/core.py:59-65: x fastest.  1-D grids (every built-in kind but the
+  // channel-blocked statistics) need no division; 32-bit math when the index
+  // fits (a 64-bit division is ~70 instructions -- as much as a small body)
   uint3 b;
+  if (g.y == 1 && g.z == 1) return make_uint3((unsigned)t, 0u, 0u);
+  if (t < (1ull << 32)) {
+    const unsigned t32 = (unsigned)t, q = t32 / g.x;
+    b.x = t32 - q * g.x;
+    b.y = q % g.y;
+    b.z = q / g.y;
+    return b;
+  }
   b.x = (unsigned)(t % g.x);
   unsigned long long q = t / g.x;
   b.y = (unsigned)(q % g.y);
@@ -195,42 +205,50 @@ __device__ __forceinline__ unsigned long long resume_pending(const unsigned long
   return tail > head ? tail - head : 0ull;
 }
 
+__device__ __forceinline__ unsigned atom_add_acq_rel_gpu(unsigned* p, unsigned v) {
+  unsigned old;
+  asm volatile("atom.add.acq_rel.gpu.u32 %0, [%1], %2;" : "=r"(old) : "l"(p), "r"(v) : "memory");
+  return old;
+}
+
+// Worker retirement.  One acq_rel atomic per worker on the exit counter (it
+// releases the worker's outputs and, for the last worker, acquires everyone
+// else's): the last worker to exit is by construction the latest exit, so it
+// stamps t_last_exit itself and publishes the mirror, `serial` last with a
+// system-scope release store.  (Three fences and four atomics per worker
+// here cost a short PTB launch ~5-9 us, ~40 % of an 18 us elementwise
+// kernel.)
 __device__ __forceinline__ void ptb_worker_exit(const PtbArgs& a, bool stopped,
                                                 unsigned long long t_entry,
                                                 const unsigned long long* resume_ring = nullptr) {
-  const unsigned long long now = globaltimer();
   LaunchRec* r = a.rec;
   if (stopped) {
+    const unsigned long long now = globaltimer();
     atomicAdd(&r->stops, 1ull);
     // first observation of the flag: min over workers
     unsigned long long prev = atomicCAS(&r->t_first_stop, 0ull, now);
     if (prev != 0ull && now < prev) atomicMin(&r->t_first_stop, now);
   }
-  atomicMax(&r->t_last_exit, now);
-  __threadfence();
   const unsigned nworkers = gridDim.x * gridDim.y * gridDim.z;
-  if (atomicAdd(&r->exited, 1u) + 1u == nworkers) {
+  if (atom_add_acq_rel_gpu(&r->exited, 1u) + 1u == nworkers) {
     // last worker: publish and recycle the record
-    __threadfence();
+    const unsigned long long now = globaltimer();
     const unsigned long long claims = atomicAdd(&r->claims, 0ull);
     const unsigned long long progress = a.start + claims;
     volatile LaunchMirror* m = a.mirror;
     m->claims = claims;
     m->t_first_stop = atomicAdd(&r->t_first_stop, 0ull);
-    m->t_last_exit = atomicAdd(&r->t_last_exit, 0ull);
+    m->t_last_exit = now;
     m->stops = atomicAdd(&r->stops, 0ull);
     m->t_first_start = t_entry;
     // work can only remain if some worker stopped on the flag
     m->status = (progress < a.total || resume_pending(resume_ring) > 0) ? kMirrorParked : kMirrorDone;
-    __threadfence_system();
-    m->serial = a.serial;
-    __threadfence_system();
+    st_release_sys(const_cast<unsigned*>(&m->serial), a.serial);
     r->claims = 0ull;
     r->exited = 0u;
     r->t_first_stop = 0ull;
     r->t_last_exit = 0ull;
     r->stops = 0ull;
-    __threadfence();
   }
 }
 

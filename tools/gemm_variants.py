@@ -2,7 +2,7 @@
 compile-time constants (default kernels_gemm.cu; experiments -- the product
 build is build.py):
 
-    python tools/gemm_variants.py NAME [--src=kernels_nn.cu] -DTALLY_STAGES_BF16_N128=4 ...
+    python tools/gemm_variants.py NAME [--src=kernels_nn.cu,kernels_tf.cu] -DTALLY_STAGES_BF16_N128=4 ...
     TALLY_LIB_PATH=paper_2410_07381_b200/_lib/variants/NAME.so python tools/gemm_shapes.py
 """
 
@@ -20,18 +20,20 @@ from paper_2410_07381_b200 import build as B  # noqa: E402
 
 def main():
     name, defs = sys.argv[1], sys.argv[2:]
-    src = "kernels_gemm.cu"
+    srcs = ["kernels_gemm.cu"]
     if defs and defs[0].startswith("--src="):
-        src, defs = defs[0][6:], defs[1:]
+        srcs, defs = defs[0][6:].split(","), defs[1:]
     B.build()
     vdir = os.path.join(B.HERE, "_lib", "variants")
     os.makedirs(vdir, exist_ok=True)
-    obj = os.path.join(vdir, name + "_" + src + ".o")
-    cmd = [B.NVCC] + B.CU_FLAGS + defs + ["-c", os.path.join(B.CSRC, src), "-o", obj]
-    subprocess.run(cmd, check=True)
-    objs = [obj if s == src else os.path.join(B.OBJ, s + ".o") for s in B.SOURCES]
+    objs = {}
+    for src in srcs:
+        obj = os.path.join(vdir, name + "_" + src + ".o")
+        subprocess.run([B.NVCC] + B.CU_FLAGS + defs + ["-c", os.path.join(B.CSRC, src), "-o", obj], check=True)
+        objs[src] = obj
+    allobjs = [objs.get(s, os.path.join(B.OBJ, s + ".o")) for s in B.SOURCES]
     lib = os.path.join(vdir, name + ".so")
-    subprocess.run([B.NVCC] + B.ARCH + ["-shared", "-o", lib] + objs + ["-lcudart", "-lpthread", "-ldl", "-lrt"],
+    subprocess.run([B.NVCC] + B.ARCH + ["-shared", "-o", lib] + allobjs + ["-lcudart", "-lpthread", "-ldl", "-lrt"],
                    check=True)
     print(lib)
 
