@@ -69,7 +69,7 @@ def parse():
                          "c3 = configs[2] (BERT-base HP seq 128 + GPT-2 small training); "
                          "c4 = configs[3] (Llama-2-7B decode bs=1 HP + BERT-large training); "
                          "c1 = the synthetic vecadd + SGEMM pair")
-    ap.add_argument("--window-ms", type=float, default=None, help="default 100 (c1) / 2000 (c2) / 4000 (c3) / 8000 (c4)")
+    ap.add_argument("--window-ms", type=float, default=None, help="default 100 (c1) / 4000 (c2, c3) / 8000 (c4)")
     ap.add_argument("--gen", type=int, default=16, help="c4: tokens generated per HP request (after a 32-token "
                                                         "prompt)")
     ap.add_argument("--load", type=float, default=None, help="mean HP load; default 0.5 (c1) / 0.25 (c2)")
@@ -920,11 +920,11 @@ def main_colocate(args):
     try:   # per-launch DRAM bytes from an ncu --set full capture of this kernel (shape-independent to ~1 %)
         tr_db = json.load(open(os.path.join(ROOT, "profiles", "ncu_traffic.json")))
         c = args.config
-        for key in (f"{c}:{top_name}:{top_cand.describe()}", f"{c}:{top_name}:Ptb(full occupancy)",
-                    f"{c}:{top_name}:Original"):
-            if key in tr_db:
-                traffic = tr_db[key]
-                break
+        # any launch of the same work signature (same kind, geometry and bytes) shares the capture
+        top_sig = tr.work_signature(top_name, top_dk)
+        same = [top_name] + [n for n, dk in tr.program if n != top_name and tr.work_signature(n, dk) == top_sig]
+        keys = [f"{c}:{n}:{shape}" for shape in (top_cand.describe(), "Ptb(full occupancy)", "Original") for n in same]
+        traffic = next((tr_db[k] for k in keys if k in tr_db), None)
     except (OSError, ValueError):
         pass
     roofline = {"bound": bound, "kernel": f"{top_name} ({top_dk.kind}, {top_cand.describe()})",
@@ -1063,7 +1063,7 @@ def main_colocate(args):
 def main():
     args = parse()
     if args.window_ms is None:
-        args.window_ms = {"c1": 100.0, "c3": 4000.0, "c4": 8000.0}.get(args.config, 2000.0)
+        args.window_ms = {"c1": 100.0, "c2": 4000.0, "c3": 4000.0, "c4": 8000.0}[args.config]
     if args.load is None:
         args.load = 0.5 if args.config == "c1" else 0.25
     if args.batch is None:

@@ -48,10 +48,10 @@ def _rb(P, C, streams=1):
     """Rows per bn_stats logical block: ~128 KB of traffic per block (the
     per-block fixed cost -- partial write, fence, counter -- stays small) while
     a block still streams in a few microseconds; backward statistics read up
-    to four streams (and get 2x the bytes per block: their fold and counter
-    cost more; bn_stats_bwd 1.89 -> 1.75 ms per step).  Small tensors get
+    to four streams.  (2x bigger backward blocks saved 0.14 ms per step but
+    put bn_stats_bwd's preemption latency at ~58 us.)  Small tensors get
     shorter blocks so that at least ~2 waves of blocks (296) run in parallel."""
-    base = (1024 if C < 128 else (512 if C < 256 else 256)) * (2 if streams > 1 else 1) // streams
+    base = (1024 if C < 128 else (512 if C < 256 else 256)) // streams
     cblocks = (C + 255) // 256
     return max(32, min(base, P * cblocks // 296 // 8 * 8))
 

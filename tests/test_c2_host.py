@@ -44,8 +44,8 @@ def test_gemm_splits_never_empty(M, N, K):
 
 
 def test_bn_rows_per_block():
-    assert resnet._rb(802816, 64) == 1024 and resnet._rb(802816, 64, 4) == 512
-    assert resnet._rb(3136, 2048) == 80 and resnet._rb(3136, 2048, 4) == 80
+    assert resnet._rb(802816, 64) == 1024 and resnet._rb(802816, 64, 4) == 256
+    assert resnet._rb(3136, 2048) == 80 and resnet._rb(3136, 2048, 4) == 64
     assert resnet._rb(3136, 512) == 32
 
 
