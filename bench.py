@@ -291,7 +291,7 @@ def main_c1(args):
     if args.profile_cache and os.path.exists(args.profile_cache):
         prof.load_cache(open(args.profile_cache).read())    # ref profiler.py:252-291
     threshold = int(args.threshold_us * 1000)
-    hp_lat = workloads.isolated_request_latency_ns(prof, hp_pipe)
+    hp_lat = workloads.isolated_request_latency_ns(prof, (hp_w,))
     choices = {w.kernel_id: prof.select(w.profile_key(), w.cost, threshold).describe() for w in be_ws}
     sg_recs = {r.candidate.describe(): r for r in prof.profile(be_ws[2].profile_key(), be_ws[2].cost)}
     if args.profile_cache and not os.path.exists(args.profile_cache) and rank == 0:
@@ -679,14 +679,20 @@ class ClockMap:
 
 def preempt_latencies_us(res_list, clk):
     """Host signal -> last worker exit (ref sim.py:509-517 measured_turnaround),
-    for PTB launches that parked (were running when the flag was raised);
-    device times mapped to the host clock by ``clk`` (a ClockMap)."""
+    for PTB launches that parked while running: the first worker entered
+    before the signal.  A launch whose workers had not started (queued behind
+    the high-priority kernels that now hold the SMs) parks without running
+    anything -- the reference parks it at the signal (sim.py:344-345) -- and
+    its "last exit" only says when the request let it start, so it is not a
+    preemption latency.  Device times mapped to the host clock by ``clk``."""
     out = []
     for res in res_list:
         for r in res.launches:
             if r["preempt_ns"] < 0 or not r["parked"] or not r["gt_last_exit"]:
                 continue
             sig = r["preempt_ns"] + res.origin_ns
+            if r["gt_first_start"] and r["gt_first_start"] + clk.off(sig) >= sig:
+                continue
             out.append((r["gt_last_exit"] + clk.off(sig) - sig) / 1e3)
     return out
 

@@ -93,6 +93,8 @@ def main():
         worst.append((ch.kernel_latency_ns - o.kernel_latency_ns, w.kernel_id, c.describe(), o.kernel_latency_ns,
                       ch.kernel_latency_ns, ch.turnaround_estimate_ns))
     worst.sort(reverse=True)
+    out["long_original_choices"] = sorted({(x[1], x[3], x[5]) for x in worst if x[2] == "Original" and x[3] > threshold},
+                                          key=lambda t: -t[1])[:20]
     out["sliced_choices"] = sorted({(x[1], x[2], x[3], x[4], x[5]) for x in worst if x[2].startswith("Sliced")},
                                    key=lambda t: -t[3])[:20]
     out["profiled_step_ms"] = {"original": lat_o / 1e6, "chosen": lat_c / 1e6}
@@ -124,6 +126,8 @@ def main():
             if r["preempt_ns"] < 0 or not r["parked"] or not r["gt_last_exit"]:
                 continue
             sig = r["preempt_ns"] + res.origin_ns
+            if r["gt_first_start"] and r["gt_first_start"] + clk.off(sig) >= sig:
+                continue   # parked before any worker started (see bench.preempt_latencies_us)
             kind = be_ws[r["kernel_index"]].kernel_id.split(":")[0] if 0 <= r["kernel_index"] < len(be_ws) else "?"
             lat = (r["gt_last_exit"] + clk.off(sig) - sig) / 1e3
             drain = (r["gt_last_exit"] - r["gt_first_stop"]) / 1e3 if r["gt_first_stop"] else None
