@@ -975,9 +975,14 @@ static int bind_gemm(const tally_kernel_args* a, Instance* inst, bool split) {
       return e ? atoi(e) : 8;
     }();
     static const int old_rule = getenv("TALLY_GEMM_TPB_OLD") != nullptr;
+    // ... and at most ~128 KB of output per logical block (fp32 128 x 128
+    // tiles: 2 per block) -- a K = 64 fp32 score GEMM at 8 tiles per block
+    // had ~30 us logical blocks (preemption latency)
+    constexpr int kTileOut = Cfg::BM * Cfg::BN * (int)sizeof(typename Cfg::OutT);
     p.tpb = Cfg::KIND != 1 ? 1
           : old_rule ? (p.kb_per_split <= 2 ? 4 : 1)
-                     : max(1, min(8, (target + p.kb_per_split - 1) / p.kb_per_split));
+                     : max(1, min(min(8, (131072 + kTileOut - 1) / kTileOut),
+                                  (target + p.kb_per_split - 1) / p.kb_per_split));
   }
   p.total_tiles = (long long)p.tiles_m * p.tiles_n * p.splits * p.batches;
   if (p.total_tiles >= (1ll << 31)) {

@@ -863,7 +863,7 @@ struct SoftmaxXent {   // one row per logical block
   // pass 2 writes dlogits from the staged copy.  Rows above kCacheMax bytes
   // are re-read from global memory instead.  bf16 logits (the GPT-2 LM head,
   // 100 KB rows) halve the traffic and keep a logical block ~10 us.
-  static constexpr int kThreads = 256;
+  static constexpr int kThreads = 512;   // 32 KB of loads in flight per row (256 threads: ~20 us rows)
   static constexpr int kUnroll = 4;
   static constexpr int kCacheMax = 104 * 1024;
   static constexpr int kRed = 128;   // bytes of reduction scratch ahead of the row
@@ -986,44 +986,84 @@ struct SoftmaxXent {   // one row per logical block
 // split-K activation GEMM (few output tiles, long K -> more, shorter logical
 // blocks for the scheduler)
 struct SplitKReduce {
+  // A logical block covers vpb output vectors (8 x bf16) and all S partials
+  // (~64 KB of partial reads): with many splits (the LM-head dgrad: S = 42)
+  // the block's threads split the S dimension into G = 256 / vpb groups, each
+  // summing partials g, g + G, ... in order, then the groups are added in
+  // order through shared memory -- deterministic, and ~10 us per block
+  // (4096 outputs x 42 partials per block made it ~30 us: preemption latency)
   static constexpr int kThreads = 256;
   static constexpr int kMinBlocks = 3;
-  static constexpr int kVec = 2;   // output vectors (8 x bf16) per thread
+  static constexpr int kSmem = kThreads * 8 * 4;
   struct Params {
     const float4* in;    // [S][n / 4]
     uint4* out;          // [n / 8]
     long long n8;
     long long stride4;   // n / 4
     int S;
+    int vpb;             // output vectors per logical block: 512 (2 per thread) or 32..256
   };
-  static __device__ __forceinline__ void run(const Params& p, uint3 bidx, uint3, char*) {
-    const long long v0 = (long long)bidx.x * (kThreads * kVec) + threadIdx.x;
-    float acc[kVec][8];
+  static __device__ __forceinline__ void add8(float (&acc)[8], const float4& a, const float4& b) {
+    acc[0] += a.x; acc[1] += a.y; acc[2] += a.z; acc[3] += a.w;
+    acc[4] += b.x; acc[5] += b.y; acc[6] += b.z; acc[7] += b.w;
+  }
+  static __device__ __forceinline__ void run(const Params& p, uint3 bidx, uint3, char* smem) {
+    if (p.vpb == 2 * kThreads) {
+      const long long v0 = (long long)bidx.x * (2 * kThreads) + threadIdx.x;
+      float acc[2][8];
 #pragma unroll
-    for (int u = 0; u < kVec; ++u)
+      for (int u = 0; u < 2; ++u)
 #pragma unroll
-      for (int e = 0; e < 8; ++e) acc[u][e] = 0.f;
-    for (int sp = 0; sp < p.S; ++sp) {
-      float4 t[kVec][2];
+        for (int e = 0; e < 8; ++e) acc[u][e] = 0.f;
+      for (int sp = 0; sp < p.S; ++sp) {
+        float4 t[2][2];
 #pragma unroll
-      for (int u = 0; u < kVec; ++u) {
-        const long long v = v0 + u * kThreads;
-        if (v < p.n8) {
-          t[u][0] = __ldcs(p.in + sp * p.stride4 + 2 * v);
-          t[u][1] = __ldcs(p.in + sp * p.stride4 + 2 * v + 1);
+        for (int u = 0; u < 2; ++u) {
+          const long long v = v0 + u * kThreads;
+          if (v < p.n8) {
+            t[u][0] = __ldcs(p.in + sp * p.stride4 + 2 * v);
+            t[u][1] = __ldcs(p.in + sp * p.stride4 + 2 * v + 1);
+          }
         }
+#pragma unroll
+        for (int u = 0; u < 2; ++u) add8(acc[u], t[u][0], t[u][1]);
       }
 #pragma unroll
-      for (int u = 0; u < kVec; ++u) {
-        acc[u][0] += t[u][0].x; acc[u][1] += t[u][0].y; acc[u][2] += t[u][0].z; acc[u][3] += t[u][0].w;
-        acc[u][4] += t[u][1].x; acc[u][5] += t[u][1].y; acc[u][6] += t[u][1].z; acc[u][7] += t[u][1].w;
+      for (int u = 0; u < 2; ++u) {
+        const long long v = v0 + u * kThreads;
+        if (v < p.n8) st16(p.out + v, pack8(acc[u]));
       }
+      return;
+    }
+    float* red = reinterpret_cast<float*>(smem);   // [G][vpb][8]
+    const int G = kThreads / p.vpb, lv = threadIdx.x % p.vpb, g = threadIdx.x / p.vpb;
+    const long long v = (long long)bidx.x * p.vpb + lv;
+    float acc[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
+    if (v < p.n8) {
+      const float4* src = p.in + 2 * v;
+      int sp = g;
+      for (; sp + 3 * G < p.S; sp += 4 * G) {   // four partials in flight, summed in order
+        float4 t[4][2];
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+          t[u][0] = __ldcs(src + (sp + u * G) * p.stride4);
+          t[u][1] = __ldcs(src + (sp + u * G) * p.stride4 + 1);
+        }
+#pragma unroll
+        for (int u = 0; u < 4; ++u) add8(acc, t[u][0], t[u][1]);
+      }
+      for (; sp < p.S; sp += G) add8(acc, __ldcs(src + sp * p.stride4), __ldcs(src + sp * p.stride4 + 1));
     }
 #pragma unroll
-    for (int u = 0; u < kVec; ++u) {
-      const long long v = v0 + u * kThreads;
-      if (v < p.n8) st16(p.out + v, pack8(acc[u]));
+    for (int e = 0; e < 8; ++e) red[(g * p.vpb + lv) * 8 + e] = acc[e];
+    __syncthreads();
+    if (g == 0 && v < p.n8) {
+      for (int k = 1; k < G; ++k)
+#pragma unroll
+        for (int e = 0; e < 8; ++e) acc[e] += red[(k * p.vpb + lv) * 8 + e];
+      st16(p.out + v, pack8(acc));
     }
+    __syncthreads();   // red is reused by the next logical block of a PTB worker
   }
 };
 
@@ -1464,8 +1504,12 @@ static int bind_splitk_reduce(const tally_kernel_args* a, Instance* inst) {
   }
   p.n8 = n / 8;
   p.stride4 = n / 4;
-  const long long per = nn::SplitKReduce::kThreads * nn::SplitKReduce::kVec;
-  finish(inst, p, (p.n8 + per - 1) / per, nn::SplitKReduce::kThreads, 0, (4.0 * p.S + 2.0) * (double)n);
+  // ~64 KB of partials per logical block: 512 vectors up to S = 4, then
+  // halving down to 32 vectors (S >= 33)
+  p.vpb = 2 * nn::SplitKReduce::kThreads;
+  while (p.vpb > 32 && (long long)p.vpb * 32 * p.S > 65536) p.vpb >>= 1;
+  finish(inst, p, (p.n8 + p.vpb - 1) / p.vpb, nn::SplitKReduce::kThreads, nn::SplitKReduce::kSmem,
+         (4.0 * p.S + 2.0) * (double)n);
   return TALLY_OK;
 }
 
