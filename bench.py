@@ -806,10 +806,10 @@ def main_colocate(args):
     clkmap = ClockMap(dev)
 
     # --- timed region: K co-located windows ----------------------------------------
-    # Each step k is paired with the solo-HP window of the same arrival trace,
-    # run just before it (k even) or just after it (k odd) (paired
-    # measurement: the HP graph's speed drifts by a few percent over a run, so
-    # solo and co-located p99 are taken side by side).  Every step is
+    # Each step k is paired with the solo-HP window of the same arrival trace
+    # run just before it (paired measurement: the HP graph's speed drifts by a
+    # few percent over a run, so solo and co-located p99 are taken side by
+    # side).  Every step is
     # bracketed by a barrier + synchronize; ms_per_step is the sum of the K
     # co-located windows' device time / K.
     clocks = Clocks(local)
@@ -819,10 +819,11 @@ def main_colocate(args):
     elapsed_ms = 0.0
     host_s = 0.0
     for k in range(args.steps):
-        # ABBA order (solo-co, co-solo, ...): a slow drift of the HP graph's
-        # speed over the run does not bias the paired difference
-        if k % 2 == 0:
-            solo_res.append(run_([hp_task(k)], tally, window))
+        # solo window first, then the co-located one.  (An ABBA order made
+        # every odd pair a co-located window right after another one, and
+        # those pairs read 30-45 % above their solo twins while even pairs
+        # matched: back-to-back co-located windows are a different regime.)
+        solo_res.append(run_([hp_task(k)], tally, window))
         if dist is not None:
             dist.barrier()
         torch.cuda.synchronize()
@@ -833,8 +834,6 @@ def main_colocate(args):
         torch.cuda.synchronize()
         host_s += time.perf_counter() - t_host0
         elapsed_ms += ev0.elapsed_time(ev1)
-        if k % 2 == 1:
-            solo_res.append(run_([hp_task(k)], tally, window))
         solo_lat += lat_after_warm(solo_res[-1])
     clk = clocks.stop()
     if dist is not None:
@@ -955,13 +954,10 @@ def main_colocate(args):
         e2e_lat = workloads.isolated_request_latency_ns(prof, pipe)
         e_solo, e_co, reqs = [], [], 0
         for k in range(args.steps):
-            if k % 2 == 0:
-                e_solo += lat_after_warm(run_([hp_task(k, pipe, e2e_lat)], tally, window))
+            e_solo += lat_after_warm(run_([hp_task(k, pipe, e2e_lat)], tally, window))
             r = run_([hp_task(k, pipe, e2e_lat), be_task], tally, window)
             reqs += len(r.requests["hp"])
             e_co += lat_after_warm(r)
-            if k % 2 == 1:
-                e_solo += lat_after_warm(run_([hp_task(k, pipe, e2e_lat)], tally, window))
         if e_solo and e_co:
             e2e = {"value": 100.0 * (p99(e_co) / p99(e_solo) - 1.0), "unit": "%",
                    "h2d_bytes_per_step": int(reqs / args.steps * host_in.numel() * host_in.element_size()),
@@ -977,14 +973,11 @@ def main_colocate(args):
             cfg = P.SchedulerConfig(policy=pol)
             lat, rate = [], []
             sl = []
-            for k in range(args.steps):     # paired (ABBA), as the Tally measurement
-                if k % 2 == 0:
-                    sl += lat_after_warm(run_([hp_task(k)], cfg, window))
+            for k in range(args.steps):     # paired, as the Tally measurement
+                sl += lat_after_warm(run_([hp_task(k)], cfg, window))
                 r = run_([hp_task(k), be_task], cfg, window)
                 lat += lat_after_warm(r)
                 rate.append(be_rate(r))
-                if k % 2 == 1:
-                    sl += lat_after_warm(run_([hp_task(k)], cfg, window))
             baselines[pol] = {"p99_overhead_pct": 100.0 * (p99(lat) / p99(sl) - 1.0),
                               "be_throughput_pct": frac(sum(rate) / len(rate), be_untransformed)}
 
