@@ -803,6 +803,9 @@ def main_colocate(args):
     be_same_policy = be_rate(run_([be_task], tally, window))
     for w in range(args.warmup):
         run_([hp_task(100 + w), be_task], tally, window)
+    # one untimed solo window too: the first solo window after co-located
+    # ones ran the HP graph ~7 % slower (p50) than every later one
+    run_([hp_task(99)], tally, window)
     clkmap = ClockMap(dev)
 
     # --- timed region: K co-located windows ----------------------------------------
