@@ -181,6 +181,17 @@ __device__ __forceinline__ void tmem_ld32(uint32_t taddr, uint32_t (&r)[32]) {
   asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
 }
 
+// TMA tensor store of a staged box (bf16 epilogue), L2 evict-first like every
+// best-effort store; bulk-group completion tracked by the issuing thread
+__device__ __forceinline__ void tma_store_2d(const CUtensorMap* map, uint32_t src, int x, int y) {
+  uint64_t pol;
+  asm("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(pol));
+  asm volatile("cp.async.bulk.tensor.2d.global.shared::cta.bulk_group.L2::cache_hint [%0, {%1, %2}], [%3], %4;"
+               ::"l"(map), "r"(x), "r"(y), "r"(src), "l"(pol)
+               : "memory");
+  asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+}
+
 // ---------------------------------------------------------------- configs
 template <int BN_, int STAGES_>
 struct CfgTf32x3T {
@@ -291,6 +302,7 @@ struct alignas(64) GemmParams {
   int tpb;                      // tiles per logical block
   long long total_tiles;        // tiles * splits * batches
   int batches, hdiv;            // batched layout (tally_gemm_layout): z = (zb, zh)
+  int c_tma;                    // bf16 C stored by TMA through the map in a_lo (plain, unbatched GEMMs)
   long long off[6][2];          // (row, col) origins of A, B, C: [a_row, a_col, b_row, b_col, c_row, c_col]
 };
 
@@ -679,6 +691,61 @@ __global__ void __launch_bounds__(kThreads, Cfg::KIND == 1 ? 2 : 1) k_gemm(const
       __syncwarp();
       if (lane == 0) mbar_arrive(&tile_empty[j]);
     }
+  } else if (Cfg::KIND == 1 && sizeof(typename Cfg::OutT) == 2 && p.c_tma) {
+    // -------------------------------------------------- epilogue (warps 2..9), TMA store
+    // 128-wide bf16 tiles of a plain GEMM: each warp drains its lane quarter
+    // x column half (32 rows x 64 columns), releases the accumulator, stages
+    // the box in its own 4 KB (the 128B-swizzle layout) and one lane issues a
+    // TMA store -- the warp never waits for global writes, only (before the
+    // next tile) for the previous store to finish reading its staging box
+    const int q = warp & 3;
+    const int half = (warp - 2) >> 2;
+    unsigned char* wstage = epi_smem + (size_t)(warp - 2) * 4096;
+    const uint32_t wst = smem_u32(wstage);
+    uint32_t ci = 0;
+    for (int i = 0;; ++i) {
+      const int j = i % kSlots;
+      mbar_wait(&tile_full[j], (i / kSlots) & 1);
+      const long long t = tile_slot[j];
+      if (t < 0) {
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&tile_empty[j]);
+        break;
+      }
+      const TileWork w = tile_w[j];
+      const int acc = ci & 1;   // one K chunk per tile for the bf16 kinds
+      mbar_wait(&tmem_full[acc], (ci >> 1) & 1);
+      fence_after();
+      uint32_t r[2][32];
+      const uint32_t lb = tmem_base + ((uint32_t)(q * 32) << 16) + (uint32_t)(acc * Cfg::BN + half * 64);
+      tmem_ld32(lb, r[0]);
+      tmem_ld32(lb + 32, r[1]);
+      fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&tmem_empty[acc]);
+      ++ci;
+      if (lane == 0) asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
+      __syncwarp();
+      unsigned char* srow = wstage + (size_t)lane * 128;
+#pragma unroll
+      for (int v = 0; v < 8; ++v) {
+        uint32_t wv[4];
+#pragma unroll
+        for (int e = 0; e < 4; ++e) {
+          const int k = 8 * (v & 3) + 2 * e;
+          __nv_bfloat162 b = __floats2bfloat162_rn(__uint_as_float(r[v >> 2][k]), __uint_as_float(r[v >> 2][k + 1]));
+          wv[e] = *reinterpret_cast<uint32_t*>(&b);
+        }
+        *reinterpret_cast<uint4*>(srow + ((v ^ (lane & 7)) << 4)) = make_uint4(wv[0], wv[1], wv[2], wv[3]);
+      }
+      asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+      __syncwarp();
+      if (lane == 0) tma_store_2d(&p.a_lo, wst, w.nb * Cfg::BN + half * 64, w.mb * Cfg::BM + q * 32);
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&tile_empty[j]);
+    }
+    if (lane == 0) asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
+    __syncwarp();
   } else {
     // -------------------------------------------------- epilogue (warps 2..9)
     const int q = warp & 3;                     // TMEM lane quarter this warp may access
@@ -882,6 +949,12 @@ static EncodeTiledFn encode_fn() {
 }
 
 // rows x cols (K innermost) row-major matrix, box = box_rows x 128 bytes, 128 B swizzle
+static bool aligned16_(const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15) == 0; }
+static bool getenv_flag(const char* name) {   // experiment switches, read at bind time
+  const char* e = getenv(name);
+  return e != nullptr && e[0] != '\0' && e[0] != '0';
+}
+
 static int make_map(CUtensorMap* m, const void* ptr, CUtensorMapDataType dt, int esz, long long rows,
                     long long cols, int box_rows, long long ld = 0) {
   EncodeTiledFn enc = encode_fn();
@@ -948,6 +1021,7 @@ static int bind_gemm(const tally_kernel_args* a, Instance* inst, bool split) {
   p.m = (int)M;
   p.n = (int)N;
   p.k = (int)K;
+  p.c_tma = 0;
   p.tiles_m = (int)((M + Cfg::BM - 1) / Cfg::BM);
   p.tiles_n = (int)(N / Cfg::BN);
   const tally_gemm_layout* lay = split ? nullptr : static_cast<const tally_gemm_layout*>(a->ptr[3]);
@@ -956,6 +1030,17 @@ static int bind_gemm(const tally_kernel_args* a, Instance* inst, bool split) {
   p.ldc = lay ? lay->ldc : N;
   p.split_stride = M * N;
   p.splits = (int)splits;
+  if constexpr (Cfg::KIND == 1 && Cfg::BN == 128 && sizeof(typename Cfg::OutT) == 2) {
+    // TMA-store epilogue for plain (unbatched, unsplit, zero-offset) GEMMs:
+    // the map's bounds clip the M tail; batched layouts keep the guarded stores
+    bool plain = p.batches == 1 && splits == 1 && aligned16_(p.c) && (p.ldc * 2) % 16 == 0;
+    for (int w = 4; w < 6; ++w) plain = plain && p.off[w][0] == 0 && p.off[w][1] == 0;
+    if (plain && !getenv_flag("TALLY_GEMM_NO_TMA_STORE")) {
+      int rc = make_map(&p.a_lo, p.c, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, M, N, 32, p.ldc);
+      if (rc) return rc;
+      p.c_tma = 1;
+    }
+  }
   p.kb_per_split = (int)((KBlocks + splits - 1) / splits);
   if ((KBlocks + p.kb_per_split - 1) / p.kb_per_split != splits) {
     set_error("gemm: %lld splits of %lld k-blocks leave an empty split (use ceil(KB / ceil(KB / splits)))",
