@@ -431,9 +431,9 @@ struct BnStats {
     const int gi = bidx.y / kGroup;
     if (threadIdx.x == 0) {
       const unsigned in_group = (unsigned)min(kGroup, p.nrb - gi * kGroup);
-      __threadfence();
-      flag[0] = atomicAdd(&p.cnt1[bidx.x * p.ngroups + gi], 1u) + 1u == in_group;
-      __threadfence();
+      // one acq_rel RMW: releases this block's partials (ordered before it
+      // by the barrier), acquires the group's for the folder
+      flag[0] = atom_add_acq_rel_gpu(&p.cnt1[bidx.x * p.ngroups + gi], 1u) + 1u == in_group;
     }
     __syncthreads();
     if (flag[0]) {
@@ -446,9 +446,7 @@ struct BnStats {
       __syncthreads();
       if (threadIdx.x == 0) {
         p.cnt1[bidx.x * p.ngroups + gi] = 0u;   // ready for the next launch
-        __threadfence();
-        flag[1] = atomicAdd(&p.cnt2[bidx.x], 1u) + 1u == (unsigned)p.ngroups;
-        __threadfence();
+        flag[1] = atom_add_acq_rel_gpu(&p.cnt2[bidx.x], 1u) + 1u == (unsigned)p.ngroups;
       }
       __syncthreads();
       if (flag[1]) {
