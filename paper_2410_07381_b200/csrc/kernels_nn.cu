@@ -103,7 +103,8 @@ struct Im2Col {
   // made the kernel instruction-bound at ~2 TB/s.)
   static constexpr int kThreads = 256;
   static constexpr int kMinBlocks = 4;   // register cap: 4+ resident CTAs per SM
-  static constexpr int kMaxRows = kVecPerBlock / 8;   // rpb <= 1024 / kv, kv >= 8
+  static constexpr int kVecs = 2 * kVecPerBlock;       // 2048 vectors per logical block (amortises the tables)
+  static constexpr int kMaxRows = kVecs / 8;           // rpb <= 2048 / kv, kv >= 8
   static constexpr int kMaxKv = 1024;
   static constexpr int kSmem = kMaxRows * 16 + kMaxKv * 4;
   struct Params {
@@ -1191,7 +1192,7 @@ static int bind_im2col(const tally_kernel_args* a, Instance* inst) {
   p.col = static_cast<uint4*>(a->ptr[1]);
   if (!p.x || !p.col || !aligned16(p.x) || !aligned16(p.col)) { set_error("im2col: 16-byte aligned x, col"); return TALLY_EINVAL; }
   p.rows = (long long)p.g.N * p.g.OH * p.g.OW;
-  p.rpb = max(1, nn::kVecPerBlock / (p.g.Kp / 8));
+  p.rpb = max(1, nn::Im2Col::kVecs / (p.g.Kp / 8));
   if (p.g.Kp / 8 > nn::Im2Col::kMaxKv || p.rows * (p.g.Kp / 8) >= (1ll << 31) ||
       (long long)p.g.N * p.g.H * p.g.W >= (1ll << 31)) {
     set_error("im2col: K <= 8192 and fewer than 2^31 column vectors / pixels");
