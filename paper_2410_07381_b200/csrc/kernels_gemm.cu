@@ -25,6 +25,7 @@
 #include <cuda.h>
 #include <cuda_bf16.h>
 
+#include <algorithm>
 #include <cstdio>
 #include <cstdlib>
 
@@ -303,6 +304,8 @@ struct alignas(64) GemmParams {
   long long total_tiles;        // tiles * splits * batches
   int batches, hdiv;            // batched layout (tally_gemm_layout): z = (zb, zh)
   int c_tma;                    // bf16 C stored by TMA through the map in a_lo (plain, unbatched GEMMs)
+  int causal;                   // causal-attention tile / K-range rule (tile_work), 0 = dense
+  int bn, bk;                   // tile width and K block of the kind (for the causal rule)
   long long off[6][2];          // (row, col) origins of A, B, C: [a_row, a_col, b_row, b_col, c_row, c_col]
 };
 
@@ -328,6 +331,7 @@ __device__ __forceinline__ void tile_coords(unsigned t, const GemmParams& p, int
 struct TileWork {
   int mb, nb, split, kbeg, kend, nch, zb, zh;
 };
+__device__ __forceinline__ int Cfg_BN(const GemmParams& p) { return p.bn; }
 __device__ __forceinline__ TileWork tile_work(long long t_, const GemmParams& p, int KB) {
   TileWork w;
   const unsigned tiles = (unsigned)p.tiles_m * (unsigned)p.tiles_n;
@@ -340,7 +344,15 @@ __device__ __forceinline__ TileWork tile_work(long long t_, const GemmParams& p,
   tile_coords(t - split * tiles, p, w.mb, w.nb);
   w.kbeg = w.split * p.kb_per_split;
   w.kend = min(KB, w.kbeg + p.kb_per_split);
-  w.nch = p.kchunk == p.kb_per_split ? 1 : (w.kend - w.kbeg + p.kchunk - 1) / p.kchunk;
+  // causal attention (T x T blocks of one (sequence, head)): 1 = scores
+  // S = Q K^T / dP = dO V^T -- tiles wholly above the diagonal are skipped
+  // (nch = 0: no loads, no MMA, no store; softmax reads only j <= i);
+  // 2 = P V / dS K -- K (the key index) stops at the tile's last query row;
+  // 3 = dS^T Q / P^T dO -- K (the query index) starts at the tile's first key
+  if (p.causal == 1 && w.nb * Cfg_BN(p) >= (w.mb + 1) * 128) w.kend = w.kbeg;
+  if (p.causal == 2) w.kend = min(w.kend, ((w.mb + 1) * 128 + p.bk - 1) / p.bk);
+  if (p.causal == 3) w.kbeg = max(w.kbeg, (w.mb * 128) / p.bk);
+  w.nch = w.kend <= w.kbeg ? 0 : p.kchunk == p.kb_per_split ? 1 : (w.kend - w.kbeg + p.kchunk - 1) / p.kchunk;
   w.zb = (int)(z / (unsigned)p.hdiv);
   w.zh = (int)(z - (unsigned)w.zb * (unsigned)p.hdiv);
   return w;
@@ -1022,6 +1034,13 @@ static int bind_gemm(const tally_kernel_args* a, Instance* inst, bool split) {
   p.n = (int)N;
   p.k = (int)K;
   p.c_tma = 0;
+  p.bn = Cfg::BN;
+  p.bk = Cfg::BK;
+  p.causal = (int)a->i[5];
+  if (p.causal < 0 || p.causal > 3 || (p.causal && (Cfg::KIND != 1 || splits != 1 || M % Cfg::BM))) {
+    set_error("gemm: causal mode 0-3, bf16 kinds, no split-K, M %% 128 == 0");
+    return TALLY_EINVAL;
+  }
   p.tiles_m = (int)((M + Cfg::BM - 1) / Cfg::BM);
   p.tiles_n = (int)(N / Cfg::BN);
   const tally_gemm_layout* lay = split ? nullptr : static_cast<const tally_gemm_layout*>(a->ptr[3]);
@@ -1093,6 +1112,21 @@ static int bind_gemm(const tally_kernel_args* a, Instance* inst, bool split) {
   inst->alg_flops = 2.0 * (double)M * (double)N * (double)K * (double)p.batches;
   inst->alg_bytes = ((double)Cfg::ESZ * (double)(M * K + N * K) * (split ? 2.0 : 1.0) +
                      (double)sizeof(typename Cfg::OutT) * (double)(M * N) * (double)splits) * (double)p.batches;
+  if (p.causal) {
+    // the work actually done: k-blocks over all tiles of one batch under the rule
+    const long long KBt = (K + Cfg::BK - 1) / Cfg::BK;
+    double done = 0.0, full = (double)p.tiles_m * p.tiles_n * KBt;
+    for (int mb = 0; mb < p.tiles_m; ++mb)
+      for (int nb = 0; nb < p.tiles_n; ++nb) {
+        long long kb0 = 0, kb1 = KBt;
+        if (p.causal == 1 && nb * Cfg::BN >= (mb + 1) * 128) kb1 = 0;
+        if (p.causal == 2) kb1 = std::min(kb1, (long long)(((mb + 1) * 128 + Cfg::BK - 1) / Cfg::BK));
+        if (p.causal == 3) kb0 = std::max(kb0, (long long)((mb * 128) / Cfg::BK));
+        done += (double)std::max(0ll, kb1 - kb0);
+      }
+    inst->alg_flops *= done / full;
+    inst->alg_bytes *= done / full;
+  }
   return TALLY_OK;
 }
 

@@ -339,7 +339,7 @@ def gemm(A, B, C, splits: int = 1) -> DeviceKernel:
 
 
 def gemm_ex(A, B, Cout, M, N, K, a_mn=False, b_mn=False, splits=1, batches=1, hdiv=1,
-            a_off=((0, 0), (0, 0)), b_off=((0, 0), (0, 0)), c_off=((0, 0), (0, 0))) -> DeviceKernel:
+            a_off=((0, 0), (0, 0)), b_off=((0, 0), (0, 0)), c_off=((0, 0), (0, 0)), causal=0) -> DeviceKernel:
     """General bf16 GEMM on tcgen05: per batch, C[M,N] = A . B^T with A
     K-major (A[M,K] row-major) or MN-major (stored as A^T [K,M]), likewise B
     ([N,K] or [K,N]).  ``A``, ``B``, ``Cout`` are 2-D row-major views (any
@@ -347,7 +347,11 @@ def gemm_ex(A, B, Cout, M, N, K, a_mn=False, b_mn=False, splits=1, batches=1, hd
     activation).  Batch z = (zb, zh) = (z // hdiv, z % hdiv) moves each
     operand's (row, col) origin by off[0] * zb + off[1] * zh, with
     ``a_off = ((row_per_zb, row_per_zh), (col_per_zb, col_per_zh))``.
-    bf16 or fp32 output; fp32 allows split-K."""
+    bf16 or fp32 output; fp32 allows split-K.  ``causal`` (causal attention,
+    T x T per batch, T % 128 == 0): 1 = S = Q.K^T / dP = dO.V^T, tiles wholly
+    above the diagonal skipped (left unwritten); 2 = P.V / dS.K, K limited to
+    keys <= the tile's last query; 3 = dS^T.Q / P^T.dO, K from the tile's
+    first key."""
     import torch
     kinds = {(False, False): "", (True, True): "_mn", (False, True): "_kmn"}
     if (a_mn, b_mn) not in kinds:
@@ -366,7 +370,7 @@ def gemm_ex(A, B, Cout, M, N, K, a_mn=False, b_mn=False, splits=1, batches=1, hd
         getattr(lay, name + "_row_off")[0], getattr(lay, name + "_row_off")[1] = r
         getattr(lay, name + "_col_off")[0], getattr(lay, name + "_col_off")[1] = c
     return DeviceKernel(kind, (A.data_ptr(), B.data_ptr(), Cout.data_ptr(), C.addressof(lay)),
-                        (M, N, K, 0, splits), keep=(A, B, Cout, lay))
+                        (M, N, K, 0, splits, causal), keep=(A, B, Cout, lay))
 
 
 def gemm_mn(At, Bt, C, splits: int = 1) -> DeviceKernel:

@@ -192,29 +192,31 @@ class TransformerTrain:
         T, H, D = self.T, self.H, self.D
         q, k, v = self._views(qkv)
         z = dict(batches=self.B * H, hdiv=H)
+        c1, c2 = (1, 2) if self.causal else (0, 0)   # causal tile / K-range rules (kernels.gemm_ex)
         self._add(name + ".qk", K.gemm_ex(q, k, S, T, T, D, a_off=((T, 0), (0, D)), b_off=((T, 0), (0, D)),
-                                          c_off=((H * T, T), (0, 0)), **z))
+                                          c_off=((H * T, T), (0, 0)), causal=c1, **z))
         self._add(name + ".softmax", K.softmax_causal(S, Pm, T, 1.0 / math.sqrt(D), causal=self.causal))
         o = self._buf(self.N, self.d)
         self._add(name + ".pv", K.gemm_ex(Pm, v, o, T, D, T, b_mn=True, a_off=((H * T, T), (0, 0)),
-                                          b_off=((T, 0), (0, D)), c_off=((T, 0), (0, D)), **z))
+                                          b_off=((T, 0), (0, D)), c_off=((T, 0), (0, D)), causal=c2, **z))
         return o
 
     def _attn_bwd(self, name, qkv, Pm, do, dP, dS):
         T, H, D = self.T, self.H, self.D
         q, k, v = self._views(qkv)
         z = dict(batches=self.B * H, hdiv=H)
+        c1, c2, c3 = (1, 2, 3) if self.causal else (0, 0, 0)
         dqkv = self._buf(self.N, 3 * self.d)
         dq, dk_, dv = self._views(dqkv)
         self._add(name + ".dp", K.gemm_ex(do, v, dP, T, T, D, a_off=((T, 0), (0, D)), b_off=((T, 0), (0, D)),
-                                          c_off=((H * T, T), (0, 0)), **z))
+                                          c_off=((H * T, T), (0, 0)), causal=c1, **z))
         self._add(name + ".softmax_bwd", K.softmax_causal_bwd(Pm, dP, dS, T, 1.0 / math.sqrt(D), causal=self.causal))
         self._add(name + ".dq", K.gemm_ex(dS, k, dq, T, D, T, b_mn=True, a_off=((H * T, T), (0, 0)),
-                                          b_off=((T, 0), (0, D)), c_off=((T, 0), (0, D)), **z))
+                                          b_off=((T, 0), (0, D)), c_off=((T, 0), (0, D)), causal=c2, **z))
         self._add(name + ".dk", K.gemm_ex(dS, q, dk_, T, D, T, a_mn=True, b_mn=True, a_off=((H * T, T), (0, 0)),
-                                          b_off=((T, 0), (0, D)), c_off=((T, 0), (0, D)), **z))
+                                          b_off=((T, 0), (0, D)), c_off=((T, 0), (0, D)), causal=c3, **z))
         self._add(name + ".dv", K.gemm_ex(Pm, do, dv, T, D, T, a_mn=True, b_mn=True, a_off=((H * T, T), (0, 0)),
-                                          b_off=((T, 0), (0, D)), c_off=((T, 0), (0, D)), **z))
+                                          b_off=((T, 0), (0, D)), c_off=((T, 0), (0, D)), causal=c3, **z))
         return dqkv
 
     # ---- running it -------------------------------------------------------------------

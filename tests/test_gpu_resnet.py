@@ -509,6 +509,62 @@ def test_gemm_ex_attention_shapes(env):
     assert nerr(got, ref) < 1e-2
 
 
+def test_gemm_ex_causal_rules(env):
+    """Causal attention tile / K-range rules (kernels.gemm_ex causal=1/2/3):
+    S = Q K^T computed on and below the diagonal (tiles wholly above left
+    untouched); P V and dS^T Q with P / dS zero above the diagonal equal the
+    dense products -- in all three shapes."""
+    P, kernels, stream = env
+    B_, T, H, D = 2, 512, 2, 64
+    HD = H * D
+    qkv = rnd(B_ * T, 3 * HD, seed=41)
+    q, k, v = qkv[:, :HD], qkv[:, HD:2 * HD], qkv[:, 2 * HD:]
+    qh = q.float().view(B_, T, H, D).permute(0, 2, 1, 3)
+    vh = v.float().view(B_, T, H, D).permute(0, 2, 1, 3)
+    kh = k.float().view(B_, T, H, D).permute(0, 2, 1, 3)
+    z = dict(batches=B_ * H, hdiv=H)
+    tri = torch.ones(T, T, device="cuda").tril().bool()
+    # mode 1: scores on/below the diagonal; above-diagonal 128 x 128 tiles untouched (NaN sentinel)
+    S = torch.full((B_ * H * T, T), float("nan"), device="cuda")
+    dk = kernels.gemm_ex(q, k, S, T, T, D, a_off=((T, 0), (0, D)), b_off=((T, 0), (0, D)),
+                         c_off=((H * T, T), (0, 0)), causal=1, **z)
+    outs = {}
+    for shape in ("original", "sliced", "ptb"):
+        S.fill_(float("nan"))
+        if shape == "original":
+            dk.original(stream).wait()
+        elif shape == "sliced":
+            for off, cnt in P.slice_plan(dk.total_blocks, Fraction(1, 3)):
+                dk.sliced(stream, off, cnt).wait()
+        else:
+            dk.ptb(stream, min(dk.total_blocks, 148)).wait()
+        outs[shape] = S.clone()
+    ref = (qh @ kh.transpose(-1, -2)).reshape(B_ * H, T, T)
+    got = outs["original"].view(B_ * H, T, T)
+    assert nerr(got[:, tri], ref[:, tri]) < 1e-4
+    blk = torch.arange(T, device="cuda") // 128
+    above = blk[None, :] > blk[:, None]
+    assert bool(torch.isnan(got[:, above]).all())
+    for sh in ("sliced", "ptb"):
+        assert torch.equal(torch.nan_to_num(outs[sh], 7.0), torch.nan_to_num(outs["original"], 7.0))
+    # mode 2: O = P V with P lower-triangular
+    Pm = (rnd(B_ * H * T, T, seed=42).float().view(B_ * H, T, T) * tri).bfloat16().view(B_ * H * T, T)
+    O = torch.zeros(B_ * T, HD, dtype=torch.bfloat16, device="cuda")
+    (got,) = shapes(P, kernels.gemm_ex(Pm, v, O, T, D, T, b_mn=True, a_off=((H * T, T), (0, 0)),
+                                       b_off=((T, 0), (0, D)), c_off=((T, 0), (0, D)), causal=2, **z),
+                    stream, [O])
+    ref = (Pm.float().view(B_, H, T, T) @ vh).permute(0, 2, 1, 3).reshape(B_ * T, HD)
+    assert nerr(got, ref) < 1e-2
+    # mode 3: dK = dS^T Q with dS lower-triangular
+    dS = (rnd(B_ * H * T, T, seed=43).float().view(B_ * H, T, T) * tri).bfloat16().view(B_ * H * T, T)
+    dK = torch.zeros(B_ * T, HD, dtype=torch.bfloat16, device="cuda")
+    (got,) = shapes(P, kernels.gemm_ex(dS, q, dK, T, D, T, a_mn=True, b_mn=True, a_off=((H * T, T), (0, 0)),
+                                       b_off=((T, 0), (0, D)), c_off=((T, 0), (0, D)), causal=3, **z),
+                    stream, [dK])
+    ref = (dS.float().view(B_, H, T, T).transpose(-1, -2) @ qh).permute(0, 2, 1, 3).reshape(B_ * T, HD)
+    assert nerr(got, ref) < 1e-2
+
+
 def test_gemm_ex_linear_backward_input(env):
     """dX = dY . W with W [out, in] read as stored (MN-major B)."""
     P, kernels, stream = env
