@@ -29,6 +29,7 @@
 #include <cuda_bf16.h>
 
 #include <cstdio>
+#include <cstdlib>
 
 #include "registry.h"
 
@@ -863,6 +864,7 @@ struct SoftmaxXent {   // one row per logical block
   // are re-read from global memory instead.  bf16 logits (the GPT-2 LM head,
   // 100 KB rows) halve the traffic and keep a logical block ~10 us.
   static constexpr int kThreads = 512;   // 32 KB of loads in flight per row (256 threads: ~20 us rows)
+  static constexpr int kMinBlocks = 2;   // register cap 64: two rows per SM (uncapped: 1 row, 973 -> 685 us)
   static constexpr int kUnroll = 4;
   static constexpr int kCacheMax = 104 * 1024;
   static constexpr int kRed = 128;   // bytes of reduction scratch ahead of the row
@@ -890,14 +892,22 @@ struct SoftmaxXent {   // one row per logical block
       x[0] += b0.x; x[1] += b0.y; x[2] += b0.z; x[3] += b0.w;
       x[4] += b1.x; x[5] += b1.y; x[6] += b1.z; x[7] += b1.w;
     }
+    if (j0 + 8 > p.ncls) {   // only the row's last valid vector straddles ncls (a uniform test per vector)
 #pragma unroll
-    for (int e = 0; e < 8; ++e)
-      if (j0 + e >= p.ncls) x[e] = -INFINITY;
+      for (int e = 0; e < 8; ++e)
+        if (j0 + e >= p.ncls) x[e] = -INFINITY;
+    }
   }
-  static __device__ __forceinline__ void merge(float& m, float& s, float m2, float s2) {
+  static constexpr float kLog2e = 1.4426950408889634f;
+  static __device__ __forceinline__ float exp2f_fast(float x) {
+    float y;
+    asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+    return y;
+  }
+  static __device__ __forceinline__ void merge(float& m, float& s, float m2, float s2) {   // base-2 maxima
     const float mm = fmaxf(m, m2);
     if (mm == -INFINITY) return;
-    s = s * __expf(m - mm) + s2 * __expf(m2 - mm);
+    s = s * exp2f_fast(m - mm) + s2 * exp2f_fast(m2 - mm);
     m = mm;
   }
   static __device__ __forceinline__ void run(const Params& p, uint3 bidx, uint3, char* smem) {
@@ -928,13 +938,16 @@ struct SoftmaxXent {   // one row per logical block
         }
         float x[8];
         to_f32(p, r[u], v * 8, x);
+        // base-2 domain (m is the running max of x * log2 e): one FFMA + one
+        // MUFU.EX2 per element; the kernel is instruction-bound, not HBM-bound
         float mv = x[0];
 #pragma unroll
         for (int e = 1; e < 8; ++e) mv = fmaxf(mv, x[e]);
         if (mv == -INFINITY) continue;
-        if (mv > m) { s *= __expf(m - mv); m = mv; }
+        mv *= kLog2e;
+        if (mv > m) { s *= exp2f_fast(m - mv); m = mv; }
 #pragma unroll
-        for (int e = 0; e < 8; ++e) s += __expf(x[e] - m);
+        for (int e = 0; e < 8; ++e) s += exp2f_fast(fmaf(x[e], kLog2e, -m));
       }
     }
 #pragma unroll
@@ -947,7 +960,7 @@ struct SoftmaxXent {   // one row per logical block
     m = red[0]; s = red[kThreads / 32];
     for (int w = 1; w < kThreads / 32; ++w) merge(m, s, red[w], red[kThreads / 32 + w]);
     const int lab = p.labels[b];
-    const float inv_s = 1.f / s, inv_b = 1.f / (float)p.B;
+    const float inv_b = 1.f / (float)p.B, scale = inv_b / s;
     for (int v = threadIdx.x; v < nv; v += kThreads) {
       uint4 r[2];
       if (p.cache) {
@@ -960,9 +973,11 @@ struct SoftmaxXent {   // one row per logical block
       float x[8];
       to_f32(p, r, v * 8, x);
 #pragma unroll
-      for (int e = 0; e < 8; ++e) {
-        const int j = v * 8 + e;
-        x[e] = j < p.ncls ? (__expf(x[e] - m) * inv_s - (j == lab ? 1.f : 0.f)) * inv_b : 0.f;
+      for (int e = 0; e < 8; ++e) x[e] = exp2f_fast(fmaf(x[e], kLog2e, -m)) * scale;   // masked: ex2(-inf) = 0
+      if (v == (lab >> 3)) {
+#pragma unroll
+        for (int e = 0; e < 8; ++e)
+          if (e == (lab & 7)) x[e] -= inv_b;
       }
       st16(p.dl + (long long)b * nv + v, pack8(x));
       if (p.dl32) {
@@ -974,7 +989,7 @@ struct SoftmaxXent {   // one row per logical block
     if (threadIdx.x == 0) {
       const float zl = p.bf16 ? __bfloat162float(reinterpret_cast<const __nv_bfloat16*>(row)[lab])
                               : reinterpret_cast<const float*>(row)[lab];
-      p.loss[b] = logf(s) + m - (zl + (p.bias ? p.bias[lab] : 0.f));
+      p.loss[b] = logf(s) + m * 0.6931471805599453f - (zl + (p.bias ? p.bias[lab] : 0.f));
     }
     __syncthreads();
   }
@@ -1459,7 +1474,7 @@ static int bind_softmax_xent(const tally_kernel_args* a, Instance* inst) {
     return TALLY_EINVAL;
   }
   const size_t row = (size_t)p.Npad * (p.bf16 ? 2 : 4);
-  p.cache = row <= (size_t)nn::SoftmaxXent::kCacheMax;
+  p.cache = row <= (size_t)nn::SoftmaxXent::kCacheMax && getenv("TALLY_XENT_NO_STAGE") == nullptr;
   finish(inst, p, p.B, nn::SoftmaxXent::kThreads, nn::SoftmaxXent::kRed + (p.cache ? row : 0),
          (double)p.B * ((double)row + 2.0 * p.Npad + (p.dl32 ? 4.0 * p.Npad : 0.0)));
   return TALLY_OK;
