@@ -212,10 +212,13 @@ def test_bn_backward(env, P_, C, with_g2):
     assert nerr(gdz, up * (y.float() > 0)) < 1e-2
 
 
-def test_splitk_reduce(env):
+@pytest.mark.parametrize("S,rows,cols", [(2, 300, 64), (5, 300, 64), (16, 1000, 72), (42, 777, 128)])
+def test_splitk_reduce(env, S, rows, cols):
+    """fp32 partials -> bf16; S >= 5 splits the partials across thread groups
+    (blocks of 32-256 vectors), summed in a fixed order in every shape."""
     P, kernels, stream = env
-    parts = torch.randn(5, 300, 64, device="cuda")
-    out = torch.zeros(300, 64, dtype=torch.bfloat16, device="cuda")
+    parts = torch.randn(S, rows, cols, device="cuda")
+    out = torch.zeros(rows, cols, dtype=torch.bfloat16, device="cuda")
     (got,) = shapes(P, kernels.splitk_reduce(parts, out), stream, [out])
     assert torch.equal(got, parts.sum(0).bfloat16()) or nerr(got, parts.sum(0)) < 1e-2
 
