@@ -267,7 +267,7 @@ struct Transpose {
 #define TALLY_BN_BWD_MINBLOCKS 3
 #endif
 #ifndef TALLY_BN_BWD_ROWS
-#define TALLY_BN_BWD_ROWS 1
+#define TALLY_BN_BWD_ROWS 2
 #endif
 template <int MODE>
 struct BnStats {
@@ -340,11 +340,6 @@ struct BnStats {
     const long long rend = min(p.P, rbeg + p.RB);
     const int cvec = p.C >> 3;
     float s1[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f}, s2[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
-    float mu[8], is[8];
-    if constexpr (MODE == 1) {
-#pragma unroll
-      for (int e = 0; e < 8; ++e) { mu[e] = p.mean[c + e]; is[e] = p.invstd[c + e]; }
-    }
     for (long long r0 = rbeg + lane_r; r0 < rend; r0 += (long long)rl * kRows) {
       uint4 xv[kRows], gv[kRows], g2v[kRows], yv[kRows];
       bool ok[kRows];
@@ -406,7 +401,9 @@ struct BnStats {
             for (int e = 0; e < 8; ++e) dz[e] = t[e] > 0.f ? dz[e] : 0.f;
           }
 #pragma unroll
-          for (int e = 0; e < 8; ++e) { s1[e] += dz[e]; s2[e] += dz[e] * ((x[e] - mu[e]) * is[e]); }
+          // raw sum dz * x: the per-channel (x - mean) * invstd is applied once
+          // per block below (linear), freeing 16 registers for rows in flight
+          for (int e = 0; e < 8; ++e) { s1[e] += dz[e]; s2[e] = fmaf(dz[e], x[e], s2[e]); }
         }
       }
     }
@@ -422,6 +419,7 @@ struct BnStats {
       float a = 0.f, b = 0.f;
       for (int k = 0; k < rl; ++k) { a += red[k * CB + threadIdx.x]; b += red[rl * CB + k * CB + threadIdx.x]; }
       const int ch = c0 + threadIdx.x;
+      if constexpr (MODE == 1) b = p.invstd[ch] * fmaf(-p.mean[ch], a, b);   // sum dz * xhat
       p.part[(long long)bidx.y * p.C + ch] = a;
       p.part[((long long)p.nrb + bidx.y) * p.C + ch] = b;
     }
