@@ -1104,32 +1104,54 @@ struct SgdUpdate {
     float lr, momentum;
   };
   static __device__ __forceinline__ float4 ld4(const float* p) { return __ldg(reinterpret_cast<const float4*>(p)); }
-  static __device__ __forceinline__ void run(const Params& p, uint3 bidx, uint3, char*) {
+  static __device__ __forceinline__ void run(const Params& p, uint3 bidx, uint3, char* smem) {
     const int2 m = p.map[bidx.x];
     const SgdSeg& s = p.segs[m.x];
-    if (threadIdx.x * 4 >= s.chunk) return;   // no barrier in this body
-    const long long i = (long long)m.y * s.chunk + threadIdx.x * 4;
-    if (i >= s.n) return;   // segment sizes are multiples of 4
-    // split-K / per-row gradient partials, summed in a fixed order
+    // chunk / 4 element-threads; with few elements per block (many gradient
+    // partials: chunk shrinks to keep ~32 KB of partials per block) the other
+    // threads split the S partials into G groups -- group g sums partials
+    // g, g + G, ... in order, then the groups are added in order through
+    // shared memory (deterministic; 16 threads looping over 329 partials made
+    // the stem weight's blocks ~65 us long)
+    const int nthr = min(kThreads, s.chunk / 4);
+    const int G = kThreads / nthr;
+    const int lt = threadIdx.x % nthr, grp = threadIdx.x / nthr;
+    const long long i = (long long)m.y * s.chunk + lt * 4;
+    const bool valid = i < s.n;   // segment sizes are multiples of 4
     float4 g = make_float4(0.f, 0.f, 0.f, 0.f);
-    int j = 0;
-    for (; j + 4 <= s.S; j += 4) {
-      const float4 a0 = ld4(s.grad + (long long)j * s.gstride + i);
-      const float4 a1 = ld4(s.grad + (long long)(j + 1) * s.gstride + i);
-      const float4 a2 = ld4(s.grad + (long long)(j + 2) * s.gstride + i);
-      const float4 a3 = ld4(s.grad + (long long)(j + 3) * s.gstride + i);
-      g.x = (((g.x + a0.x) + a1.x) + a2.x) + a3.x;
-      g.y = (((g.y + a0.y) + a1.y) + a2.y) + a3.y;
-      g.z = (((g.z + a0.z) + a1.z) + a2.z) + a3.z;
-      g.w = (((g.w + a0.w) + a1.w) + a2.w) + a3.w;
+    if (valid) {
+      int j = grp;
+      for (; j + 3 * G < s.S; j += 4 * G) {
+        const float4 a0 = ld4(s.grad + (long long)j * s.gstride + i);
+        const float4 a1 = ld4(s.grad + (long long)(j + G) * s.gstride + i);
+        const float4 a2 = ld4(s.grad + (long long)(j + 2 * G) * s.gstride + i);
+        const float4 a3 = ld4(s.grad + (long long)(j + 3 * G) * s.gstride + i);
+        g.x = (((g.x + a0.x) + a1.x) + a2.x) + a3.x;
+        g.y = (((g.y + a0.y) + a1.y) + a2.y) + a3.y;
+        g.z = (((g.z + a0.z) + a1.z) + a2.z) + a3.z;
+        g.w = (((g.w + a0.w) + a1.w) + a2.w) + a3.w;
+      }
+      for (; j < s.S; j += G) {
+        const float4 a = ld4(s.grad + (long long)j * s.gstride + i);
+        g.x += a.x; g.y += a.y; g.z += a.z; g.w += a.w;
+      }
+      if (s.zero_from >= 0)
+        for (int z = s.zero_from + grp; z < s.S; z += G)
+          *reinterpret_cast<float4*>(const_cast<float*>(s.grad) + (long long)z * s.gstride + i) = make_float4(0.f, 0.f, 0.f, 0.f);
     }
-    for (; j < s.S; ++j) {
-      const float4 a = ld4(s.grad + (long long)j * s.gstride + i);
-      g.x += a.x; g.y += a.y; g.z += a.z; g.w += a.w;
+    if (G > 1) {
+      float4* red = reinterpret_cast<float4*>(smem);   // [G][nthr]
+      red[grp * nthr + lt] = g;
+      __syncthreads();
+      if (grp == 0) {
+        for (int k = 1; k < G; ++k) {
+          const float4 t = red[k * nthr + lt];
+          g.x += t.x; g.y += t.y; g.z += t.z; g.w += t.w;
+        }
+      }
+      __syncthreads();   // red is reused by the next logical block of a PTB worker
     }
-    if (s.zero_from >= 0)
-      for (int z = s.zero_from; z < s.S; ++z)
-        *reinterpret_cast<float4*>(const_cast<float*>(s.grad) + (long long)z * s.gstride + i) = make_float4(0.f, 0.f, 0.f, 0.f);
+    if (grp != 0 || !valid) return;
     const float4 w = *reinterpret_cast<const float4*>(s.w + i);
     const float4 v = *reinterpret_cast<const float4*>(s.v + i);
     const float gw[4] = {g.x + s.wd * w.x, g.y + s.wd * w.y, g.z + s.wd * w.z, g.w + s.wd * w.w};
@@ -1499,7 +1521,7 @@ static int bind_sgd(const tally_kernel_args* a, Instance* inst) {
   p.lr = (float)a->f[0];
   p.momentum = (float)a->f[1];
   if (!p.segs || !p.map || blocks < 1) { set_error("sgd_update: need segs, map, blocks >= 1"); return TALLY_EINVAL; }
-  finish(inst, p, blocks, nn::SgdUpdate::kThreads, 0, (double)a->i[1]);   // i[1]: bytes (host computed)
+  finish(inst, p, blocks, nn::SgdUpdate::kThreads, nn::SgdUpdate::kThreads * 16, (double)a->i[1]);   // i[1]: bytes (host computed)
   return TALLY_OK;
 }
 
