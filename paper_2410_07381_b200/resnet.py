@@ -62,10 +62,19 @@ def _gemm_splits(M, N, Kdim):
     preemptible configuration under the turnaround threshold, without empty
     splits.  (20 MFLOP blocks cut the wgrad drain from ~19 to ~12 us but cost
     ~0.4 ms per step in split-K partial traffic.)"""
-    tiles = math.ceil(M / 128) * (N // (128 if N % 128 == 0 else 64))
+    bn = 128 if N % 128 == 0 else 64
+    tiles = math.ceil(M / 128) * (N // bn)
     kb = math.ceil(Kdim / 64)
-    flops = 2.0 * tiles * 128 * (128 if N % 128 == 0 else 64) * Kdim
+    flops = 2.0 * tiles * 128 * bn * Kdim
     want = max(tiles, math.ceil(flops / 40e6))
+    # ... and, for half-empty tiles (M < 128: the weight gradients of
+    # 64-channel layers, K = N*H*W), <= ~256 KB of operand bytes per block:
+    # they are memory-bound, and 40 MFLOP blocks streamed ~620 KB each
+    # (45-95 us: the C2 preemption tail).  sgd_update splits the resulting
+    # many partials across thread groups.
+    if M < 128:
+        per_kb = 2 * (M + bn) * 64
+        want = max(want, tiles * math.ceil(kb / max(2, 262144 // per_kb)))
     s = max(1, min(kb // 2, math.ceil(want / tiles)))
     return math.ceil(kb / math.ceil(kb / s))
 
