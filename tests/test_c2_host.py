@@ -43,6 +43,18 @@ def test_gemm_splits_never_empty(M, N, K):
     assert S == 1 or flops_per_block <= 80e6 or S == kb // 2
 
 
+@pytest.mark.parametrize("M,N,K", [(64, 576, 200704), (64, 448, 802816), (64, 256, 200704), (64, 64, 802816)])
+def test_gemm_splits_bound_bytes_for_half_empty_tiles(M, N, K):
+    """Weight gradients of 64-channel layers (M = 64 < 128: half-empty,
+    memory-bound tiles) get <= ~256 KB of operands per logical block."""
+    S = resnet._gemm_splits(M, N, K)
+    kb = math.ceil(K / 64)
+    per = math.ceil(kb / S)
+    bn = 128 if N % 128 == 0 else 64
+    assert math.ceil(kb / per) == S
+    assert per * 2 * (M + bn) * 64 <= 262144
+
+
 def test_bn_rows_per_block():
     assert resnet._rb(802816, 64) == 1024 and resnet._rb(802816, 64, 4) == 256
     assert resnet._rb(3136, 2048) == 80 and resnet._rb(3136, 2048, 4) == 64
