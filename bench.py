@@ -89,7 +89,7 @@ def parse():
                     help="Tally with cooperative suspension of pausable BE kernels (B200 extension)")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
-    ap.add_argument("--cpu-sample-ms", type=float, default=None, help="default 1 (c1) / 2 (c2) / 4 (c3, c4)")
+    ap.add_argument("--cpu-sample-ms", type=float, default=None, help="default 1 (c1) / 4 (c2-c4): a few HP requests (2 ms at 0.8 ms / 25 %% load held ~one)")
     ap.add_argument("--profile-cache", default=None,
                     help="tuner cache JSON: loaded if present, else written after profiling")
     return ap.parse_args()
@@ -1071,7 +1071,7 @@ def main():
     if args.batch is None:
         args.batch = 8 if args.config in ("c3", "c4") else 64
     if args.cpu_sample_ms is None:
-        args.cpu_sample_ms = {"c1": 1.0, "c2": 2.0}.get(args.config, 4.0)
+        args.cpu_sample_ms = 1.0 if args.config == "c1" else 4.0
     if args.impl == "reference":
         (run_reference_arm if args.config == "c1" else run_reference_arm_c2)(args)
     else:
