@@ -64,7 +64,7 @@ def parse():
     ap.add_argument("--steps", type=int, default=5)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--config", default="c2", choices=["c1", "c2", "c3", "c4"],
+    ap.add_argument("--config", default="c4", choices=["c1", "c2", "c3", "c4"],
                     help="c2 = BASELINE configs[1] (ResNet-50 HP bs=1 + ResNet-50 training bs=64); "
                          "c3 = configs[2] (BERT-base HP seq 128 + GPT-2 small training); "
                          "c4 = configs[3] (Llama-2-7B decode bs=1 HP + BERT-large training); "
@@ -72,8 +72,16 @@ def parse():
     ap.add_argument("--window-ms", type=float, default=None, help="default 100 (c1) / 4000 (c2, c3) / 8000 (c4)")
     ap.add_argument("--gen", type=int, default=16, help="c4: tokens generated per HP request (after a 32-token "
                                                         "prompt)")
-    ap.add_argument("--load", type=float, default=None, help="mean HP load; default 0.5 (c1) / 0.25 (c2)")
-    ap.add_argument("--burst", type=float, default=4.0, help="c2: MMPP burst-rate factor")
+    ap.add_argument("--load", type=float, default=0.5,
+                    help="mean HP load (fraction of the isolated request latency); the paper's 50%% (PAPER.md:99)")
+    ap.add_argument("--burst", type=float, default=20.0,
+                    help="c2-c4: MMPP burst-rate factor (MAF-style bursts, PAPER.md:99, :291)")
+    ap.add_argument("--burst-gaps", type=float, default=2.0,
+                    help="c2-c4: mean burst length in mean inter-arrival gaps (10%% of the time in bursts)")
+    ap.add_argument("--baseline-windows", type=int, default=3,
+                    help="paired windows per baseline policy (KernelPriority, Eager), capped at --steps")
+    ap.add_argument("--e2e-windows", type=int, default=6,
+                    help="paired windows for the end-to-end (host buffers) measurement, capped at --steps")
     ap.add_argument("--batch", type=int, default=None,
                     help="BE training batch (default 64 for c2, 8 for c3 and c4)")
     ap.add_argument("--lr", type=float, default=0.01, help="BE SGD learning rate")
@@ -565,13 +573,20 @@ def costs_path(config):
 C2_COSTS = costs_path("c2")
 
 
-def c2_trace(load, hp_lat_ns, window_ns, seed, burst):
+def c2_trace(load, hp_lat_ns, window_ns, seed, burst, burst_gaps=2.0, keep=None):
     """MMPP arrivals (ref workloads.bursty_trace semantics via CSV + load_trace)
-    with mean load ``load`` of the isolated request latency."""
+    with mean load ``load`` of the isolated request latency; bursts ``burst``x
+    the calm rate, ``burst_gaps`` mean gaps long on average, 10% of the time.
+    ``keep``: also copy the CSV there (the CPU reference arm replays it)."""
     from paper_2410_07381_b200 import workloads
+    gap_ms = hp_lat_ns / 1e6 / load
     path = tempfile.mktemp(suffix=".csv")
-    workloads.bursty_trace(path, hp_lat_ns / 1e6 / load, window_ns / 1e6, seed=seed, burst_factor=burst)
+    workloads.bursty_trace(path, gap_ms, window_ns / 1e6, seed=seed, burst_factor=burst,
+                           mean_burst_ms=burst_gaps * gap_ms)
     arr = workloads.load_trace(path)
+    if keep:
+        import shutil
+        shutil.copyfile(path, keep)
     os.unlink(path)
     return tuple(t for t in arr if t < window_ns)
 
@@ -677,21 +692,31 @@ class ClockMap:
         return o0 + (o1 - o0) * (host_ns - t0) / (t1 - t0)
 
 
-def preempt_latencies_us(res_list, clk):
-    """Host signal -> last worker exit (ref sim.py:509-517 measured_turnaround),
-    for PTB launches that parked while running: the first worker entered
-    before the signal.  A launch whose workers had not started (queued behind
-    the high-priority kernels that now hold the SMs) parks without running
-    anything -- the reference parks it at the signal (sim.py:344-345) -- and
-    its "last exit" only says when the request let it start, so it is not a
-    preemption latency.  Device times mapped to the host clock by ``clk``."""
+PTB_SHAPE = 2   # tally_launch_record.shape of a PTB launch (include/tally_b200.h)
+
+
+def preempt_latencies_us(res_list, clk, queued=None):
+    """Host signal -> last worker exit (ref sim.py:509-517 measured_turnaround:
+    max park time - signal, or finish - signal when the preempt came after
+    the last claim), for every preempted PTB launch that was running at the
+    signal: its earliest worker entered before it (``gt_first_start`` is the
+    min over workers, kept on the device).  Launches that parked *and*
+    launches that ran to completion after the signal both count -- the
+    request waited for either.  A launch whose workers had not started
+    (queued behind the high-priority kernels that now hold the SMs) parks
+    without running anything -- the reference parks it at the signal
+    (sim.py:344-345) -- and its "last exit" only says when the request let it
+    start; those are counted in ``queued[0]`` instead.  Device times mapped
+    to the host clock by ``clk``."""
     out = []
     for res in res_list:
         for r in res.launches:
-            if r["preempt_ns"] < 0 or not r["parked"] or not r["gt_last_exit"]:
+            if r["preempt_ns"] < 0 or r["shape"] != PTB_SHAPE or not r["gt_last_exit"]:
                 continue
             sig = r["preempt_ns"] + res.origin_ns
-            if r["gt_first_start"] and r["gt_first_start"] + clk.off(sig) >= sig:
+            if not r["gt_first_start"] or r["gt_first_start"] + clk.off(sig) >= sig:
+                if queued is not None:
+                    queued[0] += 1
                 continue
             out.append((r["gt_last_exit"] + clk.off(sig) - sig) / 1e3)
     return out
@@ -781,10 +806,24 @@ def main_colocate(args):
             fh.write(prof.dump_cache())
 
     def run_(tasks, cfg, horizon, **kw):
-        return P.run_policy(gpu, tasks, cfg, horizon, profiler=prof, record_events=False, **kw)
+        opts = {"suspend": 1} if (args.suspend and cfg.policy == "Tally") else None
+        return P.run_policy(gpu, tasks, cfg, horizon, profiler=prof, record_events=False, options=opts, **kw)
 
-    def hp_task(seed, pipe=hp_pipe, lat=hp_lat, horizon=window):
-        return P.TaskScript("hp", P.HIGH, pipe, c2_trace(args.load, lat, horizon, seed, args.burst))
+    # Arrival traces: MMPP at the mean load of the isolated request latency
+    # committed in profiles/<config>_costs.json (the CPU reference arm replays
+    # the very same CSVs: same generator, seeds and mean gap); the latency
+    # measured in this run is reported beside it.
+    try:
+        trace_lat = int(json.load(open(costs_path(args.config)))["hp_latency_ns"])
+    except (OSError, ValueError, KeyError):
+        trace_lat = hp_lat
+    trace_dir = os.path.join(ROOT, "gpurun_out", f"traces_{args.config}")
+    os.makedirs(trace_dir, exist_ok=True)
+
+    def hp_task(seed, pipe=hp_pipe, lat=None, horizon=window):
+        keep = os.path.join(trace_dir, f"seed{seed}.csv") if pipe is hp_pipe else None
+        return P.TaskScript("hp", P.HIGH, pipe, c2_trace(args.load, trace_lat, horizon, seed, args.burst,
+                                                         args.burst_gaps, keep=keep))
 
     be_task = P.TaskScript("be", P.BEST_EFFORT, tuple(be_ws))
     tally = P.SchedulerConfig(policy="Tally", turnaround_threshold_ns=threshold)
@@ -857,7 +896,8 @@ def main_colocate(args):
     be_co = sum(be_rate(r) for r in results) / len(results)
     overhead = 100.0 * (p99(co_lat) / p99(solo_lat) - 1.0)
     clkmap.close()
-    pl_us = preempt_latencies_us(results, clkmap)
+    n_queued = [0]
+    pl_us = preempt_latencies_us(results, clkmap, n_queued)
     dr_us = drain_us(results)
     launches = sum(len(r.launches) for r in results)
 
@@ -935,12 +975,21 @@ def main_colocate(args):
         traffic = next((tr_db[k] for k in keys if k in tr_db), None)
     except (OSError, ValueError):
         pass
+    # step-level roofline: each untransformed launch's time at peak (the longer
+    # of its tensor and HBM times for its algorithmic flops / bytes), summed over
+    # the step, over the step's measured kernel time
+    ideal_ns = sum(max(dk.info.alg_flops / (pk_t * 1e3), dk.info.alg_bytes / pk_b) for _ns, _n, dk, _c in per)
+    step_roofline = {"ideal_ms": ideal_ns / 1e6, "kernel_ms": step_kernel_ns / 1e6,
+                     "frac": ideal_ns / step_kernel_ns,
+                     "note": "sum over the step's untransformed launches of max(alg_flops / bf16 peak, "
+                             "alg_bytes / HBM peak), over the sum of their measured times (L2 warm from the "
+                             "previous kernel, as in a real step)"}
     roofline = {"bound": bound, "kernel": f"{top_name} ({top_dk.kind}, {top_cand.describe()})",
                 "algorithmic_work_per_launch": {"bytes": top_dk.info.alg_bytes, "flops": top_dk.info.alg_flops},
                 "achieved": achieved, "peak": peak, "unit": unit, "frac": achieved / peak,
                 "traffic": traffic, "vs_untransformed": orig_ns / chosen_ns,
                 "untransformed_ns": orig_ns, "chosen_ns": chosen_ns,
-                "share_of_step": top_ns / step_kernel_ns,
+                "share_of_step": top_ns / step_kernel_ns, "step": step_roofline,
                 "peak_note": "MEASURED_PEAKS.json (burst figure; kernel timed alone, L2 flushed)"}
 
     # --- e2e: HP requests carry their input / logits over PCIe ---------------------
@@ -956,15 +1005,17 @@ def main_colocate(args):
         prof.bind("d2h_logits", d2h)
         e2e_lat = workloads.isolated_request_latency_ns(prof, pipe)
         e_solo, e_co, reqs = [], [], 0
-        for k in range(args.steps):
-            e_solo += lat_after_warm(run_([hp_task(k, pipe, e2e_lat)], tally, window))
-            r = run_([hp_task(k, pipe, e2e_lat), be_task], tally, window)
+        n_e2e = max(1, min(args.steps, args.e2e_windows))
+        for k in range(n_e2e):
+            e_solo += lat_after_warm(run_([hp_task(k, pipe)], tally, window))
+            r = run_([hp_task(k, pipe), be_task], tally, window)
             reqs += len(r.requests["hp"])
             e_co += lat_after_warm(r)
         if e_solo and e_co:
             e2e = {"value": 100.0 * (p99(e_co) / p99(e_solo) - 1.0), "unit": "%",
-                   "h2d_bytes_per_step": int(reqs / args.steps * host_in.numel() * host_in.element_size()),
-                   "d2h_bytes_per_step": int(reqs / args.steps * host_out.numel() * host_out.element_size()),
+                   "h2d_bytes_per_step": int(reqs / n_e2e * host_in.numel() * host_in.element_size()),
+                   "d2h_bytes_per_step": int(reqs / n_e2e * host_out.numel() * host_out.element_size()),
+                   "windows": n_e2e, "isolated_latency_us": e2e_lat / 1e3,
                    "p99_solo_us": p99(e_solo) / 1e3, "p99_co_us": p99(e_co) / 1e3, "requests": len(e_co),
                    "pipeline": desc["e2e"]}
 
@@ -976,7 +1027,7 @@ def main_colocate(args):
             cfg = P.SchedulerConfig(policy=pol)
             lat, rate = [], []
             sl = []
-            for k in range(args.steps):     # paired, as the Tally measurement
+            for k in range(max(1, min(args.steps, args.baseline_windows))):     # paired, as the Tally measurement
                 sl += lat_after_warm(run_([hp_task(k)], cfg, window))
                 r = run_([hp_task(k), be_task], cfg, window)
                 lat += lat_after_warm(r)
@@ -990,7 +1041,10 @@ def main_colocate(args):
         if w.kernel_id not in recs:
             recs[w.kernel_id] = next(r for r in prof.profile(w.profile_key(), w.cost)
                                      if r.candidate.variant == "Original").kernel_latency_ns
+    hp_ns = [int(next(r for r in prof.profile(w.profile_key(), w.cost)
+                      if r.candidate.variant == "Original").kernel_latency_ns) for w in hp_pipe]
     costs = {"hp_latency_ns": hp_lat,
+             "hp_pipeline": [{"sig": w.kernel_id, "ns": ns} for w, ns in zip(hp_pipe, hp_ns)],
              "be": [{"sig": w.kernel_id, "threads": w.kernel.info.threads_per_block,
                      "blocks": w.kernel.info.total_blocks, "occupancy": w.kernel.info.occupancy_original,
                      "ns": int(recs[w.kernel_id])} for w in be_ws]}
@@ -1012,6 +1066,7 @@ def main_colocate(args):
         "p99_solo_us": p99(solo_lat) / 1e3, "p99_co_us": p99(co_lat) / 1e3,
         "preempt_us": [pct(pl_us, 0.5), pct(pl_us, 0.99), max(pl_us)] if pl_us else None,
         "drain_us": [pct(dr_us, 0.5), pct(dr_us, 0.99)] if dr_us else None, "preemptions": len(pl_us),
+        "preemptions_queued": n_queued[0],
         "delta_us": [round(pct(deltas, q) / 1e3, 1) for q in (0.5, 0.9, 0.99, 1.0)] if deltas else None,
         "window_p99_us_solo_co": win_p99,
     }
@@ -1025,7 +1080,12 @@ def main_colocate(args):
         "higher_is_better": False, "scaling": "weak", "vs_baseline": None, "dtype": "bf16",
         "data": desc["data"],
         "config": {"workload": WORKLOADS[args.config], "hp": desc["hp"], "be": desc["be"],
-                   "trace": f"MMPP bursty (burst x{args.burst}, 10% burst time), mean load {args.load}",
+                   "trace": f"MMPP bursty (burst x{args.burst}, 10% burst time, mean burst {args.burst_gaps} mean "
+                            f"gaps), mean load {args.load} of the isolated request latency "
+                            f"{trace_lat / 1e3:.0f} us (profiles/{args.config}_costs.json; measured in this run: "
+                            f"{hp_lat / 1e3:.0f} us); CSVs in gpurun_out/traces_{args.config}/",
+                   "load": args.load, "burst_factor": args.burst, "burst_gaps": args.burst_gaps,
+                   "trace_seeds": list(range(args.steps)),
                    "window_ms": args.window_ms, "turnaround_threshold_us": args.threshold_us,
                    "policy": "Tally (reference semantics)",
                    "tuner_choice_histogram": dict(choice_hist), "profiling_s": round(t_prof, 1),
@@ -1043,6 +1103,7 @@ def main_colocate(args):
             "be_throughput_pct_vs_native": 100.0 * be_co * native_step_s,
             "preempt_latency_us_p50_p99_max": worst["preempt_us"],
             "preempt_drain_us_p50_p99": worst["drain_us"], "preemptions": worst["preemptions"],
+            "preemptions_of_queued_launches": worst["preemptions_queued"],
             "request_delta_us_p50_p90_p99_max": worst["delta_us"],
             "window_p99_us_solo_co": worst["window_p99_us_solo_co"],
             "preempt_note": "host signal -> last worker exit (device clock mapped to host, linear drift "
@@ -1066,8 +1127,6 @@ def main():
     args = parse()
     if args.window_ms is None:
         args.window_ms = {"c1": 100.0, "c2": 4000.0, "c3": 4000.0, "c4": 8000.0}[args.config]
-    if args.load is None:
-        args.load = 0.5 if args.config == "c1" else 0.25
     if args.batch is None:
         args.batch = 8 if args.config in ("c3", "c4") else 64
     if args.cpu_sample_ms is None:

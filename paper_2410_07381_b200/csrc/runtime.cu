@@ -443,7 +443,24 @@ bool Runtime::poll(Launch* L) {
   if (L->finished) return true;
   if (L->shape == TALLY_SHAPE_PTB) {
     volatile LaunchMirror* m = &h_mirrors[L->rec];
-    if (m->serial != L->serial) return false;
+    if (m->serial != L->serial) {
+      // The last worker publishes the mirror; a kernel that faulted or was
+      // aborted never does.  Every 256th poll (the mirror read is a plain
+      // load, the event query a driver call) ask the end event: an error, or
+      // a completed kernel whose mirror is still unpublished, is a failure
+      // the caller must see instead of waiting forever.
+      if ((++L->polls & 255u) != 0u) return false;
+      const cudaError_t e = cudaEventQuery(L->ev_end);
+      if (e == cudaErrorNotReady) return false;
+      if (e == cudaSuccess) {
+        std::atomic_thread_fence(std::memory_order_acquire);
+        if (m->serial == L->serial) return poll(L);
+        L->error = cudaErrorLaunchFailure;
+      } else {
+        L->error = e;
+      }
+      return false;
+    }
     std::atomic_thread_fence(std::memory_order_acquire);
     L->claims = (long long)m->claims;
     L->gt_first_stop = (long long)m->t_first_stop;

@@ -40,6 +40,7 @@ struct Launch {
   long long host_submit = 0, host_preempt = 0;
   cudaEvent_t ev_start = nullptr, ev_end = nullptr;
   cudaError_t error = cudaSuccess;
+  unsigned polls = 0;   // PTB: mirror polls since the last end-event check
 };
 
 struct Runtime {

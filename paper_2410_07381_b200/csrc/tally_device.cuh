@@ -37,7 +37,8 @@ struct alignas(64) LaunchRec {
   unsigned long long t_first_stop;  // %globaltimer when the first worker saw the flag (0 = none)
   unsigned long long t_last_exit;   // %globaltimer of the last worker exit
   unsigned long long stops;         // workers that stopped because of the flag
-  unsigned long long pad[3];
+  unsigned long long t_first_start; // %globaltimer of the earliest worker entry (0 = none yet)
+  unsigned long long pad[2];
 };
 
 // Host-visible outcome of a launch (pinned, mapped; written once by the last worker).
@@ -222,6 +223,11 @@ __device__ __forceinline__ void ptb_worker_exit(const PtbArgs& a, bool stopped,
                                                 unsigned long long t_entry,
                                                 const unsigned long long* resume_ring = nullptr) {
   LaunchRec* r = a.rec;
+  {
+    // earliest worker entry: min over workers (the record is zero between launches)
+    const unsigned long long prev = atomicCAS(&r->t_first_start, 0ull, t_entry);
+    if (prev != 0ull && t_entry < prev) atomicMin(&r->t_first_start, t_entry);
+  }
   if (stopped) {
     const unsigned long long now = globaltimer();
     atomicAdd(&r->stops, 1ull);
@@ -240,7 +246,7 @@ __device__ __forceinline__ void ptb_worker_exit(const PtbArgs& a, bool stopped,
     m->t_first_stop = atomicAdd(&r->t_first_stop, 0ull);
     m->t_last_exit = now;
     m->stops = atomicAdd(&r->stops, 0ull);
-    m->t_first_start = t_entry;
+    m->t_first_start = atomicAdd(&r->t_first_start, 0ull);
     // work can only remain if some worker stopped on the flag
     m->status = (progress < a.total || resume_pending(resume_ring) > 0) ? kMirrorParked : kMirrorDone;
     st_release_sys(const_cast<unsigned*>(&m->serial), a.serial);
@@ -249,6 +255,7 @@ __device__ __forceinline__ void ptb_worker_exit(const PtbArgs& a, bool stopped,
     r->t_first_stop = 0ull;
     r->t_last_exit = 0ull;
     r->stops = 0ull;
+    r->t_first_start = 0ull;
   }
 }
 
