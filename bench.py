@@ -98,6 +98,7 @@ def parse():
     ap.add_argument("--suspend", type=int, default=0,
                     help="Tally with cooperative suspension of pausable BE kernels (B200 extension)")
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--selftest-pairs", action="store_true", help=argparse.SUPPRESS)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-sample-ms", type=float, default=None, help="default 1 (c1) / 4 (c2-c4): a few HP requests (2 ms at 0.8 ms / 25 %% load held ~one)")
     ap.add_argument("--profile-cache", default=None,
@@ -231,22 +232,78 @@ def run_reference_arm(args):
 
 
 def init_dist(local, world):
-    """One process per GPU; the only cross-rank traffic is the barrier, the
-    timing max and the metric gather (NCCL by default).
-    TALLY_BENCH_DIST_BACKEND=gloo allows a functional multi-rank run with
-    several ranks on one GPU (ranks map to local % device_count)."""
+    """One process per GPU.  The pairs share nothing on the data path (SURVEY
+    §8e: no collective, no NCCL); the only cross-rank traffic is the control
+    plane -- the barrier around the timed region, the max of the timing
+    scalar and the gather of each pair's metrics -- over a gloo group on the
+    host.  Ranks map to local % device_count (CUDA_VISIBLE_DEVICES=i per pair
+    when spawned by this script, every GPU visible under torchrun)."""
     import torch
     dev_index = local % max(1, torch.cuda.device_count())
-    torch.cuda.set_device(dev_index)
+    if torch.cuda.is_available():
+        torch.cuda.set_device(dev_index)
     if world <= 1:
-        return None, dev_index, "cuda"
+        return None, dev_index, "cpu"
     import torch.distributed as dist
-    backend = os.environ.get("TALLY_BENCH_DIST_BACKEND", "nccl")
-    if backend == "nccl":
-        dist.init_process_group("nccl", device_id=torch.device("cuda", dev_index))
-        return dist, dev_index, "cuda"
-    dist.init_process_group(backend)
+    dist.init_process_group("gloo")
     return dist, dev_index, "cpu"
+
+
+def free_port():
+    import socket
+    with socket.socket() as so:
+        so.bind(("127.0.0.1", 0))
+        return so.getsockname()[1]
+
+
+def spawn_pairs(n, argv):
+    """``bench.py --gpus N`` without torchrun: N independent HP/BE pairs, one
+    process per GPU (CUDA_VISIBLE_DEVICES=i), joined by a gloo group for the
+    barrier / timing max / metric gather only.  Rank 0's JSON line is
+    printed; every pair's metrics are in its ``per_rank``."""
+    port = free_port()
+    procs = []
+    for i in range(n):
+        env = dict(os.environ, RANK=str(i), LOCAL_RANK="0", WORLD_SIZE=str(n), LOCAL_WORLD_SIZE=str(n),
+                   MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port), TALLY_BENCH_SPAWNED="1")
+        if "--selftest-pairs" not in argv:
+            env["CUDA_VISIBLE_DEVICES"] = str(i)
+        procs.append(subprocess.Popen([sys.executable, os.path.abspath(__file__)] + argv, env=env,
+                                      stdout=subprocess.PIPE if i == 0 else sys.stderr, text=True))
+    out, _ = procs[0].communicate()
+    rcs = [procs[0].returncode] + [p.wait() for p in procs[1:]]
+    sys.stdout.write(out)
+    sys.stdout.flush()
+    return max(rcs)
+
+
+def selftest_pairs(args):
+    """Launcher self-test (no GPU): every rank runs the bench's control plane
+    -- init, barrier, max-over-ranks timing, metric gather, worst-pair
+    report -- around a stand-in measurement (a host sleep of 10 + rank ms)."""
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    dist, _local, red_dev = init_dist(int(os.environ.get("LOCAL_RANK", "0")), world)
+    import torch
+    if dist is not None:
+        dist.barrier()
+    t0 = time.perf_counter()
+    time.sleep((10 + rank) / 1e3)
+    elapsed_ms = 1e3 * (time.perf_counter() - t0)
+    if dist is not None:
+        t = torch.tensor([elapsed_ms], device=red_dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        elapsed_ms = float(t.item())
+    local_out = {"rank": rank, "overhead": float(rank), "be_frac": 100.0 - rank,
+                 "visible_devices": os.environ.get("CUDA_VISIBLE_DEVICES")}
+    gathered, worst = gather_pairs(local_out, dist)
+    if rank == 0:
+        print(json.dumps({"metric": METRIC, "value": worst["overhead"], "unit": "%", "n_gpus": world,
+                          "steps": 1, "ms_per_step": elapsed_ms, "selftest": True,
+                          "components": {"per_rank": gathered,
+                                         "be_throughput_pct": min(d["be_frac"] for d in gathered)}}))
+    if dist is not None:
+        dist.destroy_process_group()
 
 
 # ----------------------------------------------------------------- GPU arm
@@ -1260,6 +1317,10 @@ def main_colocate(args):
 
 def main():
     args = parse()
+    if args.gpus > 1 and "WORLD_SIZE" not in os.environ and args.impl == "ours":
+        sys.exit(spawn_pairs(args.gpus, sys.argv[1:]))
+    if args.selftest_pairs:
+        return selftest_pairs(args)
     if args.window_ms is None:
         args.window_ms = {"c1": 100.0, "c2": 4000.0, "c3": 4000.0, "c4": 8000.0}[args.config]
     if args.batch is None:

@@ -52,3 +52,29 @@ def test_reference_traces_are_the_gpu_arms():
     a = bench.c2_trace(0.5, lat, int(300e6), 0, 20.0, 2.0)
     b = bench.c2_trace(0.5, lat, int(300e6), 0, 20.0, 2.0)
     assert a == b and len(a) > 0 and all(x < 300e6 for x in a)
+
+
+def test_gpus_n_spawns_independent_pairs():
+    """`bench.py --gpus 2` without torchrun: two pair processes joined by a
+    gloo control-plane group (no NCCL); rank 0 reports both pairs."""
+    out = subprocess.run([sys.executable, os.path.join(ROOT, "bench.py"), "--gpus", "2", "--selftest-pairs"],
+                         capture_output=True, text=True, timeout=300, cwd=ROOT,
+                         env={k: v for k, v in os.environ.items() if k not in ("WORLD_SIZE", "RANK")})
+    assert out.returncode == 0, out.stderr[-2000:]
+    line = json.loads(out.stdout.strip().splitlines()[-1])
+    assert line["n_gpus"] == 2
+    per = line["components"]["per_rank"]
+    assert [d["rank"] for d in per] == [0, 1]
+    assert line["value"] == 1.0                      # the worst pair
+    assert line["components"]["be_throughput_pct"] == 99.0
+    assert line["ms_per_step"] >= 11.0               # max over ranks (rank 1 sleeps 11 ms)
+
+
+def test_gpus_n_under_torchrun_uses_gloo():
+    out = subprocess.run([sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node", "2",
+                          "--master-addr", "127.0.0.1", "--master-port", str(bench.free_port()),
+                          os.path.join(ROOT, "bench.py"), "--gpus", "2", "--selftest-pairs"],
+                         capture_output=True, text=True, timeout=300, cwd=ROOT)
+    assert out.returncode == 0, out.stderr[-2000:]
+    line = json.loads([l for l in out.stdout.splitlines() if l.startswith("{")][-1])
+    assert line["n_gpus"] == 2 and len(line["components"]["per_rank"]) == 2
