@@ -22,7 +22,7 @@
 extern "C" {
 #endif
 
-#define TALLY_ABI_VERSION 1
+#define TALLY_ABI_VERSION 2
 
 #define TALLY_OK 0
 #define TALLY_EINVAL (-22)     /* bad argument / state            -> ValueError     */
@@ -181,6 +181,11 @@ typedef struct {
   unsigned long long* worker_log; /* PTB, optional device array[workers * 4]: per-worker
                                      {smid << 32 | tasks, t_entry, t_exit, stopped} (%globaltimer) */
   int timed;                /* 1: bracket with timing events (tally_launch_elapsed_ns) */
+  int chain;                /* PTB: park on the stream's shared chain word instead of a
+                               per-launch flag -- tally_preempt then parks this launch and
+                               every PTB launch queued behind it on the stream (B200
+                               real-time look-ahead; a parked launch raises the word for
+                               its successors before it exits) */
 } tally_launch_desc;
 
 typedef struct {
@@ -225,6 +230,8 @@ typedef struct {
   int device_kernel;        /* instance id on the B200 device (-1 under a foreign device) */
   int has_config;           /* tuner's choice for Tally best-effort submission        */
   tally_candidate config;
+  long long est_ns;         /* untransformed latency (the tuner's Original record) for the
+                               real-time look-ahead budget; 0 = unknown                  */
 } tally_work;
 
 /* What the runner submits (SimLaunch, ref sim.py:140-153). */

@@ -75,7 +75,8 @@ class c_launch_desc(C.Structure):
                 ("off_z", C.c_uint), ("sub_x", C.c_uint), ("sub_y", C.c_uint),
                 ("sub_z", C.c_uint), ("workers", C.c_int), ("start_count", C.c_longlong),
                 ("preempt_at", C.c_longlong), ("exec_count", C.c_void_p),
-                ("pausable", C.c_int), ("worker_log", C.c_void_p), ("timed", C.c_int)]
+                ("pausable", C.c_int), ("worker_log", C.c_void_p), ("timed", C.c_int),
+                ("chain", C.c_int)]
 
 
 class c_launch_state(C.Structure):
@@ -99,7 +100,8 @@ class c_candidate(C.Structure):
 
 class c_work(C.Structure):
     _fields_ = [("kernel_id", C.c_char_p), ("cost", c_cost), ("exempt", C.c_int),
-                ("device_kernel", C.c_int), ("has_config", C.c_int), ("config", c_candidate)]
+                ("device_kernel", C.c_int), ("has_config", C.c_int), ("config", c_candidate),
+                ("est_ns", C.c_longlong)]
 
 
 class c_submit_desc(C.Structure):

@@ -50,6 +50,7 @@ class CudaDevice : public Device {
     Runtime& R = rt();
     if (!R.inited) throw Error(TALLY_EINVAL, "tally_init must be called before running on the B200");
     trace_ = r_->option("trace", 0) != 0;
+    chain_ = r_->option("lookahead", 1) > 1;
     const int n_hp = (int)r_->option("hp_streams", 4);
     for (int i = 0; i < n_hp; ++i) {
       int s;
@@ -217,6 +218,7 @@ class CudaDevice : public Device {
   bool filter_ = false;
   bool trace_ = false;
   bool held_ = false;
+  bool chain_ = false;   // look-ahead: best-effort PTB launches park on their stream's chain word
   std::map<int, bool> pausable_cache_;
 
   bool pausable(int kernel) {
@@ -271,12 +273,17 @@ class CudaDevice : public Device {
     r_->log.events.push_back(e);
   }
 
-  int be_stream(int task) {
-    auto it = be_streams_.find(task);
+  // One stream per (task, priority class) for everything but high-priority
+  // inference: a training task's kernels must run in order (with look-ahead
+  // several of them are queued at once), and a best-effort inference task's
+  // requests share its lowest-priority stream.
+  int task_stream(int task, int priority) {
+    const int key = 2 * task + (priority == TALLY_HIGH ? 1 : 0);
+    auto it = be_streams_.find(key);
     if (it != be_streams_.end()) return it->second;
     int s;
-    if (tally_stream_create(TALLY_BEST_EFFORT, &s) != TALLY_OK) throw Error(TALLY_ECUDA, tally_last_error());
-    be_streams_[task] = s;
+    if (tally_stream_create(priority, &s) != TALLY_OK) throw Error(TALLY_ECUDA, tally_last_error());
+    be_streams_[key] = s;
     return s;
   }
 
@@ -312,6 +319,7 @@ class CudaDevice : public Device {
     struct { long long total_blocks; } ki{kit->second};
     if (h.d.shape == TALLY_SHAPE_PTB) {
       ld.shape = TALLY_SHAPE_PTB;
+      ld.chain = (chain_ && h.d.priority == TALLY_BEST_EFFORT) ? 1 : 0;
       ld.pausable = r_->option("suspend", 0) ? 1 : 0;
       ld.workers = h.d.worker_count;
       ld.start_count = h.d.start_count;
@@ -328,7 +336,10 @@ class CudaDevice : public Device {
     }
     int stream;
     ld.timed = trace_ ? 1 : 0;
-    if (h.d.priority == TALLY_HIGH) {
+    const bool training = r_->tasks[(size_t)h.d.task].arrivals.empty();
+    if (training) {
+      stream = task_stream(h.d.task, h.d.priority);
+    } else if (h.d.priority == TALLY_HIGH) {
       // an idle high-priority stream if there is one (no head-of-line blocking
       // behind another request), else the least loaded
       size_t best = 0;
@@ -342,7 +353,7 @@ class CudaDevice : public Device {
       ++hp_load_[best];
       stream = hp_streams_[best];
     } else {
-      stream = be_stream(h.d.task);
+      stream = task_stream(h.d.task, TALLY_BEST_EFFORT);
     }
     int lid = -1;
     int rc = tally_launch(h.d.device_kernel, stream, &ld, &lid);

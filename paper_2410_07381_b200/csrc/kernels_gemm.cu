@@ -437,7 +437,7 @@ __global__ void __launch_bounds__(kThreads, Cfg::KIND == 1 ? 2 : 1) k_gemm(const
             // resume a tile a preempted worker left half-done
             ptb_hold_while_paused(s);
             const unsigned f = s.flag_is_host ? ld_acquire_sys(s.flag) : ld_acquire_gpu(s.flag);
-            if (f != s.serial) {
+            if (!ptb_park_requested(s, f)) {
               unsigned long long* ring = p.resume;
               for (;;) {
                 const unsigned long long h = atomicAdd(ring + 1, 0ull), tl = atomicAdd(ring, 0ull);
@@ -492,7 +492,7 @@ __global__ void __launch_bounds__(kThreads, Cfg::KIND == 1 ? 2 : 1) k_gemm(const
           if constexpr (kChunkPreempt) {
             // flag_seen was loaded three k-blocks ago; the L2 load has completed
             if (p.resume != nullptr && c > c0) {
-              if (flag_seen == s.serial) {
+              if (ptb_park_requested(s, flag_seen)) {
                 // cut the tile before chunk c: publish the cut, then wake the
                 // MMA issuer with an empty ("poisoned") stage
                 *reinterpret_cast<volatile int*>(&tile_cut[j]) = c;

@@ -55,6 +55,8 @@ long long Runner::token(int kind, int task, long long t) {
 void Runner::run(Device* dev) {
   dev_ = dev;
   suspend_ = policy == TALLY_POLICY_TALLY && option("suspend", 0) != 0;
+  lookahead_ = (int)std::max(1LL, option("lookahead", 1));
+  if (policy == TALLY_POLICY_TIME_SLICED) lookahead_ = 1;
   hp_.clear();
   be_.clear();
   for (size_t i = 0; i < tasks.size(); ++i) {
@@ -138,21 +140,107 @@ void Runner::absorb() {
         st.reqs.erase(st.reqs.begin() + (long)*it);
       continue;
     }
-    if (st.h < 0) continue;
-    const tally_handle_state hs = dev_->query(st.h);
-    if (hs.parked) {
-      st.ptb_counter = hs.task_counter;   // resume point (ref scheduler.py:275-277)
-      st.h = -1;
-    } else if (hs.done) {
+    while (st.h >= 0) {
+      const tally_handle_state hs = dev_->query(st.h);
+      if (hs.parked) {
+        st.ptb_counter = hs.task_counter;   // resume point (ref scheduler.py:275-277)
+        st.h = -1;
+        break;
+      }
+      if (!hs.done) break;
       const bool was_slice = st.h_is_slice;
       st.h = -1;
       st.h_is_slice = false;
       if (was_slice) {
         st.slice_i += 1;
-        if (st.slice_i < (int)st.tiling.size()) continue;   // more slices remain
+        if (st.slice_i < (int)st.tiling.size()) break;   // more slices remain
       }
       kernel_done(st);
+      if (st.ahead.empty()) break;
+      // real-time look-ahead: the next queued launch becomes the head
+      const Task::Ahead a = st.ahead.front();
+      st.ahead.pop_front();
+      if (a.k != st.k) throw Error(TALLY_EINVAL, st.id + ": look-ahead launch out of order");
+      st.h = a.h;
+      st.cfg = a.cfg;
+      st.has_cfg = true;
+      st.ptb_counter = 0;
     }
+    settle_ahead(st);
+  }
+}
+
+// Look-ahead launches queued behind a head that parked park too (they share
+// the stream's chain word, and a parked launch raises it before it exits);
+// once all have reported they are dropped and re-queued behind the resumed
+// head.  Returns true when none remain.
+bool Runner::settle_ahead(Task& st) {
+  if (st.ahead.empty()) return true;
+  if (st.h >= 0) return false;
+  for (const auto& a : st.ahead) {
+    const tally_handle_state s = dev_->query(a.h);
+    if (s.done || (s.parked && s.task_counter != 0))
+      throw Error(TALLY_EINVAL, st.id + ": a look-ahead launch ran behind a parked one");
+    if (!s.parked) return false;
+  }
+  st.ahead.clear();
+  return true;
+}
+
+// Real-time look-ahead (runner option "lookahead" = L > 1; the reference
+// keeps one kernel in flight per task, which the parity tests keep): up to
+// L - 1 further kernels of a training task are queued behind the in-flight
+// head on the task's stream, so the GPU never idles between best-effort
+// kernels waiting for the host to observe a completion and launch the next.
+// What may be queued keeps the policy's bound on high-priority delay:
+//   * PTB launches (Tally) -- they share the stream's chain preemption word,
+//     so preempting the head parks the whole queue (before any claim);
+//   * untransformed launches only ahead of every PTB launch in the queue (a
+//     launch that cannot park must never overtake a parked one) and, except
+//     under Eager, only while their summed latency stays within the
+//     turnaround threshold -- what a high-priority arrival may wait for;
+//   * never a Sliced kernel (its slices go one at a time), never past the
+//     end of the iteration, never a second launch of a kernel instance
+//     already in flight (per-instance chain state).
+void Runner::fill_ahead(int task) {
+  Task& st = tasks[(size_t)task];
+  if (lookahead_ <= 1 || st.inference() || st.concurrent || st.h < 0 || st.h_is_slice) return;
+  const bool tally = policy == TALLY_POLICY_TALLY;
+  const int prio = (policy == TALLY_POLICY_TALLY || policy == TALLY_POLICY_KERNEL_PRIORITY) ? st.priority : TALLY_HIGH;
+  bool ptb_queued = st.has_cfg && st.cfg.variant == TALLY_SHAPE_PTB;
+  long long budget = 0;
+  for (const auto& a : st.ahead) {
+    if (a.cfg.variant == TALLY_SHAPE_PTB) ptb_queued = true;
+    else budget += st.kernels[(size_t)a.k].est_ns;
+  }
+  while ((int)st.ahead.size() + 1 < lookahead_) {
+    const int j = st.k + 1 + (int)st.ahead.size();
+    if (j >= (int)st.kernels.size()) break;
+    const Work& w = st.kernels[(size_t)j];
+    bool busy = w.device_kernel == st.kernels[(size_t)st.k].device_kernel;
+    for (const auto& a : st.ahead) busy = busy || st.kernels[(size_t)a.k].device_kernel == w.device_kernel;
+    if (busy) break;
+    tally_candidate cfg;
+    memset(&cfg, 0, sizeof(cfg));
+    cfg.variant = TALLY_SHAPE_ORIGINAL;
+    if (tally && st.priority == TALLY_BEST_EFFORT && !w.exempt) {
+      if (!w.has_config) break;
+      cfg = w.config;
+    }
+    if (cfg.variant == TALLY_SHAPE_SLICED) break;
+    if (cfg.variant == TALLY_SHAPE_PTB) {
+      ptb_queued = true;
+    } else {
+      if (ptb_queued) break;
+      if (policy != TALLY_POLICY_EAGER) {
+        if (w.est_ns <= 0 || budget + w.est_ns > threshold) break;
+        budget += w.est_ns;
+      }
+    }
+    const long long h = cfg.variant == TALLY_SHAPE_PTB
+        ? submit(task, w, prio, TALLY_SHAPE_PTB, cfg.worker_count, 0, w.cost.total_blocks, 0, false)
+        : submit(task, w, prio, TALLY_SHAPE_ORIGINAL, 0, 0, w.cost.total_blocks, 0, false);
+    st.ahead.push_back(Task::Ahead{j, h, cfg});
   }
 }
 
@@ -227,7 +315,11 @@ void Runner::advance(int task, int pclass) {
     }
     return;
   }
-  if (st.h >= 0) return;
+  if (st.h >= 0) {
+    fill_ahead(task);
+    return;
+  }
+  if (!st.ahead.empty()) return;   // queued look-ahead launches are still parking
   const Work* w = next_work(st);
   if (!w) return;
   if (pclass == TALLY_BEST_EFFORT && policy == TALLY_POLICY_TALLY && !w->exempt) {
@@ -238,6 +330,7 @@ void Runner::advance(int task, int pclass) {
     tasks[(size_t)task].h_is_slice = false;
     if (pclass == TALLY_HIGH && policy == TALLY_POLICY_TALLY) preempt_be();
   }
+  fill_ahead(task);
   auto it = std::find(be_.begin(), be_.end(), task);
   if (it != be_.end()) rr_ = (int)(((it - be_.begin()) + 1) % (long)be_.size());
 }
@@ -250,6 +343,10 @@ void Runner::preempt_be() {
     if (s.is_ptb && !s.done && !s.preempted) {
       if (suspend_ && dev_->hold(h)) continue;   // suspended in place, resumes when HP is idle
       dev_->signal_preempt(h);
+    }
+    for (const auto& a : tasks[(size_t)i].ahead) {   // the queued look-ahead launches too
+      const tally_handle_state q = dev_->query(a.h);
+      if (q.is_ptb && !q.done && !q.preempted) dev_->signal_preempt(a.h);
     }
   }
 }
@@ -291,6 +388,8 @@ bool Runner::filter(long long h) {
     for (int i : be_) {
       const long long bh = tasks[(size_t)i].h;
       if (bh >= 0 && !done(bh)) return false;
+      for (const auto& a : tasks[(size_t)i].ahead)
+        if (!done(a.h)) return false;
     }
     return true;
   }
@@ -411,6 +510,7 @@ int tally_runner_add_task(int runner, const char* task_id, int priority, const t
       w.device_kernel = works[i].device_kernel;
       w.has_config = works[i].has_config != 0;
       w.config = works[i].config;
+      w.est_ns = works[i].est_ns;
       if (w.cost.total_blocks < 1 || w.cost.threads_per_block < 1)
         throw Error(TALLY_EINVAL, "block counts must be >= 1");
       t.kernels.push_back(std::move(w));
@@ -492,7 +592,11 @@ int tally_runner_set_option(int runner, const char* key, long long value) {
   if (!r) return TALLY_EINVAL;
   if (!key) { set_error("null option key"); return TALLY_EINVAL; }
   const std::string k(key);
-  if (k != "trace" && k != "hp_streams" && k != "suspend") { set_error("unknown runner option '%s'", key); return TALLY_EINVAL; }
+  if (k != "trace" && k != "hp_streams" && k != "suspend" && k != "lookahead") {
+    set_error("unknown runner option '%s'", key);
+    return TALLY_EINVAL;
+  }
+  if (k == "lookahead" && (value < 1 || value > 64)) { set_error("lookahead must be in [1, 64]"); return TALLY_EINVAL; }
   if (k == "hp_streams" && (value < 1 || value > 64)) { set_error("hp_streams must be in [1, 64]"); return TALLY_EINVAL; }
   r->options[k] = value;
   return TALLY_OK;

@@ -45,6 +45,7 @@ struct Work {
   int device_kernel = -1;
   bool has_config = false;
   tally_candidate config{};
+  long long est_ns = 0;      // untransformed latency (look-ahead budget), 0 = unknown
 };
 
 struct Task {
@@ -72,6 +73,14 @@ struct Task {
   std::vector<long long> tiling;
   int slice_i = 0;
   long long ptb_counter = 0;
+  // Real-time look-ahead (runner option "lookahead" > 1): kernels k+1, k+2,
+  // ... submitted behind the in-flight head on the task's stream.
+  struct Ahead {
+    int k;
+    long long h;
+    tally_candidate cfg;
+  };
+  std::deque<Ahead> ahead;
   std::vector<std::pair<long long, long long>> requests;
   std::vector<long long> iterations;
   bool in_service() const { return in_arrival || !reqs.empty(); }
@@ -142,6 +151,9 @@ class Runner {
                    long long start, long long total_blocks, long long offset, bool is_slice);
   void preempt_be();
   void submit_be(int task, const Work& w);
+  int lookahead_ = 1;
+  void fill_ahead(int task);
+  bool settle_ahead(Task& st);
   bool ts_has_work(const Task& st);
   void ts_arm();
   void ts_rotate();

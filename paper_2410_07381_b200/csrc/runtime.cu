@@ -140,6 +140,12 @@ int Runtime::init(int dev, tally_gpu_info* out) {
      "cudaHostAlloc(flags)");
   memset((void*)h_flags, 0, sizeof(unsigned) * kMaxRecs);
   CK(cudaHostGetDevicePointer(&d_hflags, (void*)h_flags, 0), "flag device pointer");
+  CK(cudaMalloc(&d_chain, sizeof(unsigned) * kMaxChainStreams), "cudaMalloc(chain words)");
+  CK(cudaMemset(d_chain, 0, sizeof(unsigned) * kMaxChainStreams), "cudaMemset(chain words)");
+  CK(cudaHostAlloc(&h_chain, sizeof(unsigned) * kMaxChainStreams, cudaHostAllocMapped), "cudaHostAlloc(chain)");
+  memset((void*)h_chain, 0, sizeof(unsigned) * kMaxChainStreams);
+  CK(cudaHostGetDevicePointer(&d_hchain, (void*)h_chain, 0), "chain device pointer");
+  chain_epoch.assign(kMaxChainStreams, 0u);
   CK(cudaMalloc(&d_pause, 64), "cudaMalloc(pause)");
   CK(cudaMemset(d_pause, 0, 64), "cudaMemset(pause)");
   CK(cudaHostAlloc(&h_stamp, 64, cudaHostAllocMapped), "cudaHostAlloc(stamp)");
@@ -372,7 +378,26 @@ int Runtime::launch(int kernel, int stream, const tally_launch_desc* d, int* out
       // can live in mapped host memory: ~2 us propagation instead of ~6 us
       const int use_host = flag_host || kk.host_flag;
       pa.flag_is_host = use_host;
-      pa.flag = use_host ? (d_hflags + rec) : &d_recs[rec].flag;
+      pa.park_at = ser;
+      pa.chain_dev = nullptr;
+      pa.chain_host = nullptr;
+      if (d->chain) {
+        // every launch queued on this stream shares one preemption word: a
+        // single write parks the running launch and the ones behind it
+        if (stream >= kMaxChainStreams) { free_recs.push_back(rec); set_error("chain stream id out of range"); return TALLY_EINVAL; }
+        {
+          std::lock_guard<std::mutex> g(mu);
+          pa.park_at = chain_epoch[(size_t)stream] + 1u;
+        }
+        pa.chain_dev = d_chain + stream;
+        pa.chain_host = d_hchain + stream;
+        pa.flag = use_host ? (d_hchain + stream) : (d_chain + stream);
+        L->chain = true;
+        L->chain_stream = stream;
+      } else {
+        pa.flag = use_host ? (d_hflags + rec) : &d_recs[rec].flag;
+      }
+      L->park_at = pa.park_at;
       L->flag_host = use_host;
       pa.mirror = d_mirrors + rec;
       pa.serial = ser;
@@ -502,6 +527,24 @@ int Runtime::preempt(int id) {
   bool expected = false;
   if (!L->preempted.compare_exchange_strong(expected, true)) return TALLY_OK;
   L->host_preempt = host_now_ns();
+  if (L->chain) {
+    // raise the stream's epoch to this launch's park_at (once per epoch): the
+    // mapped host word first (GEMM producers poll it, ~2 us), then the device
+    // word the streaming kinds poll
+    unsigned& cur = chain_epoch[(size_t)L->chain_stream];
+    if ((int)(cur - L->park_at) >= 0) return TALLY_OK;
+    cur = L->park_at;
+    h_chain[L->chain_stream] = cur;
+    std::atomic_thread_fence(std::memory_order_seq_cst);
+    if (!write32) {
+      CK(cudaMemcpyAsync(d_chain + L->chain_stream, &cur, sizeof(unsigned), cudaMemcpyHostToDevice, sig_stream),
+         "chain flag write");
+      return TALLY_OK;
+    }
+    CUresult r = write32((CUstream)sig_stream, (CUdeviceptr)(d_chain + L->chain_stream), cur, 0u);
+    if (r != CUDA_SUCCESS) { set_error("cuStreamWriteValue32 failed (%d)", (int)r); return TALLY_ECUDA; }
+    return TALLY_OK;
+  }
   if (L->flag_host) {
     reinterpret_cast<volatile unsigned*>(h_flags)[L->rec] = L->serial;
     std::atomic_thread_fence(std::memory_order_seq_cst);

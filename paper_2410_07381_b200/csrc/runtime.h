@@ -41,6 +41,9 @@ struct Launch {
   cudaEvent_t ev_start = nullptr, ev_end = nullptr;
   cudaError_t error = cudaSuccess;
   unsigned polls = 0;   // PTB: mirror polls since the last end-event check
+  bool chain = false;   // PTB on its stream's chain word (park_at = epoch)
+  int chain_stream = -1;
+  unsigned park_at = 0;
 };
 
 struct Runtime {
@@ -64,6 +67,13 @@ struct Runtime {
   volatile unsigned* h_flags = nullptr;
   unsigned* d_hflags = nullptr;
   unsigned* d_pause = nullptr;        // global suspension word (device memory)
+  // Chain preemption words, one per stream (PtbArgs::park_at): device word,
+  // its mapped host mirror, and the epoch last written per stream.
+  static constexpr int kMaxChainStreams = 4096;
+  unsigned* d_chain = nullptr;
+  volatile unsigned* h_chain = nullptr;
+  unsigned* d_hchain = nullptr;
+  std::vector<unsigned> chain_epoch;
   int pause_on = 0;
   volatile unsigned long long* h_stamp = nullptr;
   unsigned long long* d_stamp = nullptr;

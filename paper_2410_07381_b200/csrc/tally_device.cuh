@@ -76,8 +76,16 @@ struct PtbArgs {
   LaunchRec* rec;
   const unsigned int* flag;        // where the preemption flag lives (device or mapped host)
   LaunchMirror* mirror;            // mapped host outcome slot
-  unsigned int serial;             // this launch's identity; flag == serial means "park"
+  unsigned int serial;             // this launch's identity (the mirror is valid when it holds it)
   unsigned int flag_is_host;       // 1: flag is in mapped host memory (sys-scope loads)
+  // Park when the flag has reached park_at (wrap-around compare; flags only
+  // grow).  Per-launch flag: park_at = serial, the host writes the serial.
+  // Chain flag (one word per best-effort stream, shared by every launch
+  // queued on it): park_at = the stream's next preemption epoch, so one write
+  // parks the running launch and everything queued behind it.
+  unsigned int park_at;
+  unsigned int* chain_dev;         // chain mode: the stream's device word (else null)
+  unsigned int* chain_host;        // chain mode: its mapped host mirror (else null)
   unsigned long long start;        // persisted task counter to resume from
   unsigned long long total;        // total logical blocks
   long long preempt_at;            // test trigger: raise flag when counter reaches this (-1 off)
@@ -86,6 +94,10 @@ struct PtbArgs {
   unsigned long long* worker_log;  // optional [workers * 4] per-worker telemetry
   const unsigned int* pause;       // optional suspension word (device memory); non-zero = hold
 };
+
+__device__ __forceinline__ bool ptb_park_requested(const PtbArgs& a, unsigned f) {
+  return (int)(f - a.park_at) >= 0;
+}
 
 __device__ __forceinline__ unsigned long long globaltimer() {
   unsigned long long t;
@@ -248,7 +260,15 @@ __device__ __forceinline__ void ptb_worker_exit(const PtbArgs& a, bool stopped,
     m->stops = atomicAdd(&r->stops, 0ull);
     m->t_first_start = atomicAdd(&r->t_first_start, 0ull);
     // work can only remain if some worker stopped on the flag
-    m->status = (progress < a.total || resume_pending(resume_ring) > 0) ? kMirrorParked : kMirrorDone;
+    const bool parked = progress < a.total || resume_pending(resume_ring) > 0;
+    m->status = parked ? kMirrorParked : kMirrorDone;
+    if (parked && a.chain_dev != nullptr) {
+      // a parked chain launch parks everything queued behind it on the stream:
+      // the next launch starts after this one exits (stream order) and reads
+      // the raised word, whichever of the host's two writes it would poll
+      atomicMax(a.chain_dev, a.park_at);
+      if (a.chain_host != nullptr) st_release_sys(a.chain_host, a.park_at);
+    }
     st_release_sys(const_cast<unsigned*>(&m->serial), a.serial);
     r->claims = 0ull;
     r->exited = 0u;
@@ -270,7 +290,7 @@ __device__ __forceinline__ bool ptb_hold_while_paused(const PtbArgs& a) {
   for (;;) {
     __nanosleep(256);
     const unsigned f = a.flag_is_host ? ld_acquire_sys(a.flag) : ld_acquire_gpu(a.flag);
-    if (f == a.serial) return true;
+    if (ptb_park_requested(a, f)) return true;
     if (ld_acquire_gpu(a.pause) == 0u) return false;
   }
 }
@@ -278,11 +298,11 @@ __device__ __forceinline__ bool ptb_hold_while_paused(const PtbArgs& a) {
 __device__ __forceinline__ long long ptb_claim(const PtbArgs& a) {
   ptb_hold_while_paused(a);
   const unsigned f = a.flag_is_host ? ld_acquire_sys(a.flag) : ld_acquire_gpu(a.flag);
-  if (f == a.serial) return -1;   // flag gates the claim: a parked launch never over-claims
+  if (ptb_park_requested(a, f)) return -1;   // flag gates the claim: a parked launch never over-claims
   const unsigned long long c = atomicAdd(&a.rec->claims, 1ull);
   const long long task = (long long)(a.start + c);
   if (a.preempt_at >= 0 && task + 1 == a.preempt_at)
-    st_release_sys(const_cast<unsigned*>(a.flag), a.serial);   // test trigger (MemTrigger)
+    st_release_sys(const_cast<unsigned*>(a.flag), a.park_at);   // test trigger (MemTrigger)
   if (a.exec_count != nullptr && (unsigned long long)task < a.total)
     atomicAdd(&a.exec_count[task], 1ull);
   return task;
@@ -294,11 +314,11 @@ __device__ __forceinline__ long long ptb_claim_n(const PtbArgs& a, int n) {
   if (n <= 1) return ptb_claim(a);
   ptb_hold_while_paused(a);
   const unsigned f = a.flag_is_host ? ld_acquire_sys(a.flag) : ld_acquire_gpu(a.flag);
-  if (f == a.serial) return -1;
+  if (ptb_park_requested(a, f)) return -1;
   const unsigned long long c = atomicAdd(&a.rec->claims, (unsigned long long)n);
   const long long task = (long long)(a.start + c);
   if (a.preempt_at >= 0 && task < a.preempt_at && a.preempt_at <= task + n)
-    st_release_sys(const_cast<unsigned*>(a.flag), a.serial);   // test trigger (MemTrigger)
+    st_release_sys(const_cast<unsigned*>(a.flag), a.park_at);   // test trigger (MemTrigger)
   if (a.exec_count != nullptr)
     for (int k = 0; k < n; ++k)
       if ((unsigned long long)(task + k) < a.total) atomicAdd(&a.exec_count[task + k], 1ull);

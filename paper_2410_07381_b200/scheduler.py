@@ -254,6 +254,13 @@ class PolicyRunner:
                 w.config.frac_num = cand.fraction.numerator
                 w.config.frac_den = cand.fraction.denominator
             w.config.worker_count = cand.worker_count or 0
+        if (task.priority == BEST_EFFORT and work.kernel is not None and self.device_factory is None
+                and int(self.options.get("lookahead", 1)) > 1):
+            # the look-ahead budget: the kernel's untransformed latency (tuner record)
+            if self.config.policy != TALLY:
+                self.profiler.bind(work.kernel_id, work.kernel)
+            w.est_ns = next(r.kernel_latency_ns for r in self.profiler.profile(work.profile_key(), work.cost)
+                            if r.candidate.variant == "Original")
         return w
 
     def run(self) -> RunResult:

@@ -40,7 +40,7 @@ def test_python_binding_covers_header():
 
 
 def test_abi_version_and_kinds():
-    assert _lib.lib.tally_abi_version() == 1
+    assert _lib.lib.tally_abi_version() == 2
     names = [_lib.lib.tally_kernel_kind_name(i).decode()
              for i in range(_lib.lib.tally_kernel_kind_count())]
     for k in ("vecadd_i64", "vecadd_f32", "rowsum_f32"):

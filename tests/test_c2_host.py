@@ -106,11 +106,13 @@ def test_c2_trace_is_deterministic_and_loaded():
     assert 0.12 < load < 0.45      # MMPP: mean load 0.25, bursty
 
 
-def test_cpu_reference_sample_runs():
-    """The bounded CPU reference sample (oracle port of tallysim) bench.py
-    reports as cpu_baseline, on the committed B200-measured costs."""
+def test_cpu_reference_models_every_kernel():
+    """The CPU reference arm models every best-effort kernel of the step (not
+    a prefix) and the HP request, from the committed B200-measured costs."""
     import bench
-    costs = json.load(open(os.path.join(ROOT, "profiles", "c2_costs.json")))
-    v, wall, horizon, events = bench.cpu_c2_sample(costs, 2.0, 0.5, 4.0, 0, be_kernels=3)
-    assert horizon == 2_000_000 and events > 0 and wall > 0
-    assert v is None or v > -50
+    for cfg in ("c2", "c3", "c4"):
+        costs = json.load(open(os.path.join(ROOT, "profiles", f"{cfg}_costs.json")))
+        hp, be = bench.ref_tasks(costs)
+        assert len(be) == len(costs["be"]) and len(hp) >= 1
+        assert all(w.cost.total_blocks == k["blocks"] for w, k in zip(be, costs["be"]))
+        assert all(w.exempt for w in hp)

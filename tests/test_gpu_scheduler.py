@@ -72,3 +72,49 @@ def test_tally_keeps_hp_tail_close_to_solo(env):
           f"BE iterations {len(co.iterations['be'])}")
     assert co.iterations["be"]
     assert c < 4 * s + 100_000
+
+
+@pytest.mark.parametrize("policy", ["Tally", "KernelPriority", "Eager"])
+def test_lookahead_keeps_dependent_kernels_in_order(env, policy):
+    """Real-time look-ahead (runner option lookahead=4): a training step of
+    dependent kernels -- a chain of large vector adds (tuner: PTB) each
+    feeding a small one (Original) -- co-located with HP requests that
+    preempt it.  Queued launches behind a parked one must park too (chain
+    flag), so every output equals the sequential computation bit for bit,
+    and launches really were queued behind in-flight ones."""
+    P, workloads, dev, hp, be, bufs = env
+    from paper_2410_07381_b200 import kernels
+    g = torch.Generator(device="cuda").manual_seed(7)
+    nb, ns, depth = 1 << 25, 1 << 18, 6
+    b0 = torch.rand(nb, device="cuda", generator=g)
+    y = torch.rand(nb, device="cuda", generator=g)
+    ys = torch.rand(ns, device="cuda", generator=g)
+    big = [torch.empty(nb, device="cuda") for _ in range(depth)]
+    small = [torch.empty(ns, device="cuda") for _ in range(depth)]
+    works = []
+    for k in range(depth):
+        kb = kernels.vecadd_f32(b0 if k == 0 else big[k - 1], y, big[k])
+        ks = kernels.vecadd_f32(big[k][:ns], ys, small[k])
+        works += [P.KernelWork(f"big{k}", kb.cost(), kernel=kb), P.KernelWork(f"small{k}", ks.cost(), kernel=ks)]
+    prof = P.Profiler(dev.spec, runs=3)
+    horizon = 80_000_000
+    arr = workloads.generate_arrivals(0.3, 200_000, horizon, seed=3)
+    tasks = [P.TaskScript("hp", P.HIGH, (P.KernelWork("vadd_hp", hp.cost(), kernel=hp),), arr),
+             P.TaskScript("be", P.BEST_EFFORT, tuple(works))]
+    res = P.run_policy(dev.spec, tasks, P.SchedulerConfig(policy=policy), horizon, profiler=prof,
+                       record_events=False, options={"lookahead": 4})
+    torch.cuda.synchronize()
+    assert len(res.requests["hp"]) == len(arr) and res.iterations["be"]
+    ref = b0
+    for k in range(depth):
+        ref = ref + y
+        assert torch.equal(big[k], ref), k
+        assert torch.equal(small[k], ref[:ns] + ys), k
+    be_l = sorted((r for r in res.launches if r["task"] == 1), key=lambda r: r["issue_ns"])
+    queued = sum(1 for a, b in zip(be_l, be_l[1:]) if b["issue_ns"] < a["complete_ns"])
+    assert queued > len(be_l) // 4, (queued, len(be_l))
+    if policy == "Tally":
+        cfgs = {w.kernel_id: prof.select(w.profile_key(), w.cost).variant for w in works}
+        print(cfgs)
+        if "Ptb" in cfgs.values():
+            assert any(r["parked"] for r in be_l)
