@@ -97,6 +97,9 @@ def parse():
     ap.add_argument("--no-baselines", action="store_true")
     ap.add_argument("--suspend", type=int, default=0,
                     help="Tally with cooperative suspension of pausable BE kernels (B200 extension)")
+    ap.add_argument("--lookahead", type=int, default=4,
+                    help="best-effort launches in flight per training task (real-time look-ahead, every "
+                         "policy; 1 = the reference's one kernel in flight)")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--selftest-pairs", action="store_true", help=argparse.SUPPRESS)
     ap.add_argument("--no-cpu-baseline", action="store_true")
@@ -918,6 +921,7 @@ def run_config(args):
             "window_ms": args.window_ms, "trace_seeds": list(range(args.steps)),
             "warmup_trace_seeds": [100 + w for w in range(args.warmup)],
             "turnaround_threshold_us": args.threshold_us, "policy": "Tally (reference semantics)",
+            "lookahead": args.lookahead,
             "p99": "nearest rank over all timed windows, requests arriving after the first 10% of a window",
             "l2": "inputs larger than L2 (BE activations >= 1 GB per step)",
             "parallelism": f"{args.gpus} independent HP/BE pair(s), one per GPU"}
@@ -1001,7 +1005,9 @@ def main_colocate(args):
             fh.write(prof.dump_cache())
 
     def run_(tasks, cfg, horizon, **kw):
-        opts = {"suspend": 1} if (args.suspend and cfg.policy == "Tally") else None
+        opts = {"lookahead": args.lookahead}
+        if args.suspend and cfg.policy == "Tally":
+            opts["suspend"] = 1
         return P.run_policy(gpu, tasks, cfg, horizon, profiler=prof, record_events=False, options=opts, **kw)
 
     # Arrival traces: MMPP at the mean load of the isolated request latency

@@ -16,7 +16,7 @@ import bench  # noqa: E402
 
 def _args(**kw):
     a = dict(config="c2", steps=2, warmup=0, gpus=1, load=0.5, burst=20.0, burst_gaps=2.0, window_ms=300.0,
-             threshold_us=31.6, batch=64, gen=16, ref_profile_runs=1)
+             threshold_us=31.6, batch=64, gen=16, ref_profile_runs=1, lookahead=4)
     a.update(kw)
     return SimpleNamespace(**a)
 
