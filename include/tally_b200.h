@@ -158,6 +158,7 @@ int tally_jit_register(const char* name, const void* cubin, const char* sym_orig
 /* ==== streams (per-priority CUDA streams) ================================== */
 int tally_stream_create(int priority_class, int* out_stream);   /* TALLY_HIGH / TALLY_BEST_EFFORT */
 int tally_stream_sync(int stream);
+int tally_stream_handle(int stream, void** out_cuda_stream);   /* the cudaStream_t, borrowed */
 int tally_stream_destroy(int stream);
 
 /* ==== launches (ref sim.py:114-153 shapes, :304-351 submit/preempt;

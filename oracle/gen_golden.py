@@ -209,6 +209,23 @@ def gen_transforms():
 
 
 # --------------------------------------------------------------------------
+def gen_acceptance():
+    """Acceptance criterion 1 (ref tests/test_acceptance.py:98-120):
+    the 200 random kernels (max_blocks=16, max_threads=8), their inputs, the
+    reference interpreter's final image, and the reference's unified-sync
+    rewrite of each (what the product's unify_synchronization must equal)."""
+    ir, randgen, tr, *_ = _ref()
+    from tallysim.ir import interpret
+    cases = []
+    for seed in range(200):
+        c = randgen.random_kernel(seed, max_blocks=16, max_threads=8)
+        base = interpret(c.launch)
+        cases.append({"seed": seed, "kernel": kjson(c.kernel), "args": list(c.arg_values),
+                      "memory": list(c.initial_memory), "status": base.status,
+                      "base": list(base.final_memory), "unified": kjson(tr.unify_synchronization(c.kernel))})
+    return {"cases": cases, "fractions": ["1/2", "1/4", "1/8", "1/16", "1/32"], "workers": [1, 2, 4, 8]}
+
+
 def _shape_json(s):
     n = type(s).__name__
     if n == "SlicedShape":
@@ -438,8 +455,12 @@ def gen_traffic():
 
 def main():
     os.makedirs(OUT, exist_ok=True)
+    only = sys.argv[1:]
     for name, fn in (("ir", gen_ir), ("transforms", gen_transforms), ("sim", gen_sim),
-                     ("tuner", gen_tuner), ("policy", gen_policy), ("traffic", gen_traffic)):
+                     ("tuner", gen_tuner), ("policy", gen_policy), ("traffic", gen_traffic),
+                     ("acceptance", gen_acceptance)):
+        if only and name not in only:
+            continue
         doc = fn()
         doc["_generated_by"] = "oracle/gen_golden.py from /root/reference/pkg/src (tallysim 0.1.0)"
         with open(os.path.join(OUT, f"{name}.json"), "w") as fh:

@@ -151,6 +151,7 @@ class c_launch_record(C.Structure):
 
 _SIGNATURES = {
     "tally_abi_version": (C.c_int, []),
+    "tally_stream_handle": (C.c_int, [C.c_int, C.POINTER(C.c_void_p)]),
     "tally_last_error": (C.c_char_p, []),
     "tally_now_ns": (C.c_longlong, []),
     "tally_init": (C.c_int, [C.c_int, C.POINTER(c_gpu_info)]),

@@ -583,9 +583,18 @@ int Runtime::jit_register(const char* name, const void* image, const char* syms[
     set_error("jit kernel geometry out of range");
     return TALLY_EINVAL;
   }
+  // one module per image: a batch of IR kernels compiled into one cubin
+  // registers each kind against the same image
   CUmodule mod;
-  CUresult r = cu_module_load(&mod, image);
-  if (r != CUDA_SUCCESS) { set_error("cuModuleLoadData failed (%d)", (int)r); return TALLY_ECUDA; }
+  CUresult r = CUDA_SUCCESS;
+  auto mit = jit_modules.find(image);
+  if (mit != jit_modules.end()) {
+    mod = (CUmodule)mit->second;
+  } else {
+    r = cu_module_load(&mod, image);
+    if (r != CUDA_SUCCESS) { set_error("cuModuleLoadData failed (%d)", (int)r); return TALLY_ECUDA; }
+    jit_modules[image] = (void*)mod;
+  }
   KernelKind& k = kinds[nkinds];
   memset(&k, 0, sizeof(k));
   snprintf(k.jit_name, sizeof(k.jit_name), "%s", name);
@@ -956,6 +965,13 @@ int tally_stream_sync(int stream) {
   Runtime& r = rt();
   if (stream < 0 || stream >= (int)r.streams.size() || !r.streams[stream]) { set_error("unknown stream %d", stream); return TALLY_EINVAL; }
   CK(cudaStreamSynchronize(r.streams[stream]), "cudaStreamSynchronize");
+  return TALLY_OK;
+}
+
+int tally_stream_handle(int stream, void** out) {
+  Runtime& r = rt();
+  if (stream < 0 || stream >= (int)r.streams.size() || !r.streams[stream] || !out) { set_error("unknown stream %d", stream); return TALLY_EINVAL; }
+  *out = (void*)r.streams[stream];
   return TALLY_OK;
 }
 

@@ -89,6 +89,7 @@ struct Runtime {
   int jit_register(const char* name, const void* image, const char* syms[3], const unsigned grid[3],
                    int threads, long long smem, int* out_kind);
 
+  std::unordered_map<const void*, void*> jit_modules;   // cubin image -> CUmodule
   std::vector<std::unique_ptr<Launch>> launches;
   std::vector<int> free_launch_ids;
   std::vector<cudaEvent_t> timed_events, plain_events;

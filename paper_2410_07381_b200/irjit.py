@@ -65,13 +65,17 @@ def _norm_operand(o):
 
 
 def normalize(kernel) -> dict:
-    """Accept a reference KernelDef, an oracle Kernel or the JSON encoding."""
+    """Accept a reference KernelDef, an oracle Kernel, the JSON encoding, or
+    an already normalised kernel (e.g. ``transforms.unify_synchronization``'s
+    output)."""
+    if isinstance(kernel, dict) and "nparams" in kernel:
+        return kernel
     if isinstance(kernel, dict):
         d = kernel
         body = [(op, tuple(_norm_operand(a) for a in args), lab) for op, args, lab in d["body"]]
-        return {"name": d["name"], "nparams": len(d["params"]), "grid": tuple(d["grid"]),
-                "block": tuple(d["block"]), "regs": d["regs"], "shared": d["shared"],
-                "dependent": bool(d.get("dependent", False)), "body": body}
+        return {"name": d["name"], "params": tuple(d["params"]), "nparams": len(d["params"]),
+                "grid": tuple(d["grid"]), "block": tuple(d["block"]), "regs": d["regs"],
+                "shared": d["shared"], "dependent": bool(d.get("dependent", False)), "body": body}
     regs = getattr(kernel, "register_count", None)
     regs = kernel.regs if regs is None else regs
     shared = getattr(kernel, "shared_words", None)
@@ -83,7 +87,8 @@ def normalize(kernel) -> dict:
         ops.append((ins.opcode, tuple(_norm_operand(a) for a in args), ins.label))
     dep = getattr(kernel, "inter_block_dependent", None)
     dep = getattr(kernel, "dependent", False) if dep is None else dep
-    return {"name": kernel.name, "nparams": len(kernel.params), "grid": tuple(kernel.grid),
+    return {"name": kernel.name, "params": tuple(kernel.params), "nparams": len(kernel.params),
+            "grid": tuple(kernel.grid),
             "block": tuple(kernel.block), "regs": regs, "shared": shared, "dependent": bool(dep),
             "body": ops}
 
@@ -119,6 +124,18 @@ def _special(kind, axis, k):
     if kind == "blockDim":
         return str({"x": bx, "y": by, "z": bz}[axis])
     return {"x": "tx", "y": "ty", "z": "tz"}[axis]
+
+
+def _shared_increment(body, i, targets) -> bool:
+    """body[i:i+3] == LOAD_SHARED rX, [W]; ADD rX, rX, 1; STORE_SHARED [W], rX
+    with W an immediate and no branch target inside."""
+    if i + 2 >= len(body) or (i + 1) in targets or (i + 2) in targets:
+        return False
+    (o0, a0, _), (o1, a1, _), (o2, a2, _) = body[i], body[i + 1], body[i + 2]
+    if o1 != "ADD" or o2 != "STORE_SHARED" or a0[1][0] != "i":
+        return False
+    rx, w = a0[0], a0[1]
+    return (a1[0] == rx and a1[1] == rx and a1[2] == ("i", 1) and a2[0] == w and a2[1] == rx)
 
 
 def codegen(k: dict, ns: str) -> str:
@@ -157,9 +174,22 @@ def codegen(k: dict, ns: str) -> str:
         return f"goto L{t};"
 
     targets = {labels[a[-1][1]] for op, a, _l in k["body"] if op in ("BRANCH", "JUMP")}
-    for i, (op, a, _lab) in enumerate(k["body"]):
+    body = k["body"]
+    fused = set()
+    for i, (op, a, _lab) in enumerate(body):
         if i in targets:
             emit(f"  L{i}:")
+        if i in fused:
+            continue
+        if op == "LOAD_SHARED" and _shared_increment(body, i, targets):
+            # load / add 1 / store back on one shared word (the unified-sync
+            # returned count): one atomic, or a warp returning together would
+            # count once
+            w = a[1][1]
+            emit(f"    {{ if ({w} < 0 || {w} >= {k['shared']}) {{ atomicOr(p.fault, 1ull); }} else "
+                 f"r[{a[0][1]}] = (long long)atomicAdd(reinterpret_cast<unsigned long long*>(sh + {w}), 1ull) + 1; }}")
+            fused.update((i + 1, i + 2))
+            continue
         if op in ("CONST", "MOV"):
             emit(f"    r[{a[0][1]}] = {_val(a[1])};")
         elif op in ("ADD", "SUB", "MUL"):
@@ -267,43 +297,73 @@ class _Nvrtc:
 
 _nvrtc = None
 _kinds: dict = {}
+_images: list = []   # registered cubins stay alive: the runtime caches one module per image address
+
+
+def _prepare(kernel):
+    k = normalize(kernel)
+    if k["dependent"]:
+        raise TransformError(f"{k['name']}: inter-block dependent kernels are exempt")
+    if k["nparams"] > 7:
+        raise TransformError(f"{k['name']}: at most 7 IR parameters")
+    digest = hashlib.sha256(repr(sorted((kk, str(v)) for kk, v in k.items())).encode()).hexdigest()[:16]
+    return k, digest
+
+
+def _compile_register(items):
+    """items: [(normalised kernel, digest)] -> kind ids, one NVRTC program and
+    one module for all of them."""
+    global _nvrtc
+    B200Device.get()
+    if _nvrtc is None:
+        _nvrtc = _Nvrtc()
+    src = ['#include "tally_device.cuh"\n']
+    exprs = []
+    for k, digest in items:
+        ns = f"tally_jit_{digest}"
+        src.append(codegen(k, ns))
+        exprs += [f"tally::k_original<{ns}::Body>", f"tally::k_sliced<{ns}::Body>", f"tally::k_ptb<{ns}::Body>"]
+    cubin, lowered = _nvrtc.compile("".join(src), f"tally_jit_{items[0][1]}_x{len(items)}.cu", exprs)
+    _images.append(cubin)
+    ids = []
+    for i, (k, digest) in enumerate(items):
+        gx, gy, gz = k["grid"]
+        bx, by, bz = k["block"]
+        out = C.c_int()
+        _lib.check(_lib.lib.tally_jit_register(f"ir_{digest}".encode(), C.cast(cubin, C.c_void_p),
+                                               *[x.encode() for x in lowered[3 * i:3 * i + 3]], gx, gy, gz,
+                                               bx * by * bz, 8 * k["shared"], C.byref(out)),
+                   "jit register")
+        _kinds[f"ir_{digest}"] = out.value
+        ids.append(out.value)
+    return ids
 
 
 class JitKernel:
     """A compiled IR kernel kind; ``bind`` it to a memory image to launch."""
 
-    def __init__(self, kernel):
-        global _nvrtc
-        k = normalize(kernel)
-        if k["dependent"]:
-            raise TransformError(f"{k['name']}: inter-block dependent kernels are exempt")
-        if k["nparams"] > 7:
-            raise TransformError(f"{k['name']}: at most 7 IR parameters")
+    def __init__(self, kernel, _prepared=None):
+        k, digest = _prepared or _prepare(kernel)
         self.ir = k
         self.ptb_ok = ptb_safe(k)
-        digest = hashlib.sha256(repr(sorted((kk, str(v)) for kk, v in k.items())).encode()).hexdigest()[:16]
         self.kind_name = f"ir_{digest}"
-        if self.kind_name in _kinds:
-            self.kind_id = _kinds[self.kind_name]
-            return
-        B200Device.get()
-        if _nvrtc is None:
-            _nvrtc = _Nvrtc()
-        ns = f"tally_jit_{digest}"
-        src = '#include "tally_device.cuh"\n' + codegen(k, ns)
-        exprs = [f"tally::k_original<{ns}::Body>", f"tally::k_sliced<{ns}::Body>",
-                 f"tally::k_ptb<{ns}::Body>"]
-        cubin, lowered = _nvrtc.compile(src, ns + ".cu", exprs)
-        self._cubin = cubin
-        gx, gy, gz = k["grid"]
-        bx, by, bz = k["block"]
-        out = C.c_int()
-        _lib.check(_lib.lib.tally_jit_register(self.kind_name.encode(), C.cast(cubin, C.c_void_p),
-                                               *[s.encode() for s in lowered], gx, gy, gz,
-                                               bx * by * bz, 8 * k["shared"], C.byref(out)),
-                   "jit register")
-        self.kind_id = out.value
-        _kinds[self.kind_name] = out.value
+        if self.kind_name not in _kinds:
+            _compile_register([(k, digest)])
+        self.kind_id = _kinds[self.kind_name]
+
+    @classmethod
+    def compile_many(cls, kernels, chunk: int = 64) -> list:
+        """Compile many IR kernels with one NVRTC program per ``chunk`` of them
+        (the acceptance gate's 400 kinds in a few programs instead of 400)."""
+        prepared = [_prepare(k) for k in kernels]
+        todo, seen = [], set()
+        for k, d in prepared:
+            if f"ir_{d}" not in _kinds and d not in seen:
+                seen.add(d)
+                todo.append((k, d))
+        for i in range(0, len(todo), chunk):
+            _compile_register(todo[i:i + chunk])
+        return [cls(None, p) for p in prepared]
 
     def bind(self, mem, fault, args) -> DeviceKernel:
         """mem: int64 CUDA tensor (the word image); fault: int64 CUDA tensor [1]."""

@@ -50,6 +50,12 @@ class Stream:
     def synchronize(self):
         _lib.check(_lib.lib.tally_stream_sync(self.id), "stream sync")
 
+    def handle(self) -> int:
+        """The cudaStream_t (e.g. for torch.cuda.ExternalStream)."""
+        h = C.c_void_p()
+        _lib.check(_lib.lib.tally_stream_handle(self.id, C.byref(h)), "stream handle")
+        return h.value or 0
+
     def close(self):
         if self.id >= 0:
             _lib.lib.tally_stream_destroy(self.id)
@@ -191,14 +197,16 @@ class DeviceKernel:
         return self._launch(stream, d)
 
     def ptb(self, stream: Stream, workers: int, start_count: int = 0, preempt_at=None,
-            exec_count=None, timed=False, worker_log=None) -> Launch:
+            exec_count=None, timed=False, worker_log=None, chain=False) -> Launch:
         """``worker_log``: optional int64 CUDA tensor [workers, 4] receiving per
         worker ``(smid << 32 | blocks done, t_entry, t_exit, stopped)`` on the
-        device %globaltimer clock."""
+        device %globaltimer clock.  ``chain``: park on the stream's shared
+        chain word (preempting this launch parks every chain launch queued
+        behind it on the stream)."""
         d = _lib.c_launch_desc(shape=_lib.SHAPE_PTB, workers=workers, start_count=start_count,
                                preempt_at=-1 if preempt_at is None else preempt_at,
                                exec_count=_ptr(exec_count), worker_log=_ptr(worker_log),
-                               timed=int(timed))
+                               timed=int(timed), chain=int(chain))
         return self._launch(stream, d)
 
     def cost(self, block_duration_ns: int = 0, launch_overhead_ns: int = DEFAULT_LAUNCH_OVERHEAD_NS,

@@ -93,21 +93,63 @@ def test_ptb_preempt_at_every_counter_then_resume(P, stream, gold):
             dk.close()
 
 
+def _hold(stream, ms=60):
+    """Queue ~ms of spinning in front of the next launch on ``stream``."""
+    with torch.cuda.stream(torch.cuda.ExternalStream(stream.handle())):
+        torch.cuda._sleep(int(ms * 2.0e6))
+
+
 def test_ptb_flag_before_launch_is_noop(P, stream, gold):
-    """ref tests/test_transforms.py:174-183: preempted before any claim ->
-    counter stays at the start value and memory is untouched."""
+    """ref tests/test_transforms.py:174-183: the flag is raised before any
+    worker starts (the launch waits behind ~60 ms of spinning on its stream)
+    -> no claim, counter == start, memory untouched; a resume then completes
+    the kernel exactly once."""
     case = _ir_case(gold, "vecadd")
     mem, dk = _vecadd_kernel(P, case)
-    L = dk.ptb(stream, 4, preempt_at=None)
+    before = mem.cpu().tolist()
+    n = case["kernel"]["grid"][0]
+    ec = torch.zeros(n, dtype=torch.int64, device="cuda")
+    _hold(stream)
+    L = dk.ptb(stream, 4, exec_count=ec)
     L.preempt()
     st = L.wait()
-    # the flag races the launch; whatever was claimed ran exactly once and
-    # a resume completes the rest
-    ctr = st.task_counter
-    if st.parked:
-        dk.ptb(stream, 4, start_count=ctr).wait()
+    assert st.parked and not st.done
+    assert st.claims == 0 and st.task_counter == 0
+    assert mem.cpu().tolist() == before
+    assert int(ec.sum().item()) == 0
+    st2 = dk.ptb(stream, 4, start_count=st.task_counter, exec_count=ec).wait()
+    assert st2.done
     assert mem.cpu().tolist() == case["expect"]["memory"]
+    assert ec.cpu().tolist() == [1] * n
 
+
+def test_chain_flag_parks_the_queue_behind_a_preempted_launch(P, stream, gold):
+    """Look-ahead chain mode: three PTB launches queued on one stream behind
+    ~60 ms of spinning; preempting the first parks all three before any
+    claim (one shared word), and resuming them in order completes each
+    exactly once."""
+    from paper_2410_07381_b200 import kernels
+    g = torch.Generator(device="cuda").manual_seed(3)
+    n = 1 << 20
+    x = torch.rand(n, device="cuda", generator=g)
+    y = torch.rand(n, device="cuda", generator=g)
+    outs = [torch.zeros(n, device="cuda") for _ in range(3)]
+    ks = [kernels.vecadd_f32(x if i == 0 else outs[i - 1], y, outs[i]) for i in range(3)]
+    ecs = [torch.zeros(k.total_blocks, dtype=torch.int64, device="cuda") for k in ks]
+    _hold(stream)
+    Ls = [k.ptb(stream, 148, exec_count=e, chain=True) for k, e in zip(ks, ecs)]
+    Ls[0].preempt()
+    sts = [L.wait() for L in Ls]
+    assert all(st.parked and st.claims == 0 for st in sts)
+    assert all(int(e.sum().item()) == 0 for e in ecs)
+    assert all(int(o.abs().sum().item()) == 0 for o in outs)
+    for k, e in zip(ks, ecs):
+        assert k.ptb(stream, 148, exec_count=e, chain=True).wait().done
+    ref = x
+    for i in range(3):
+        ref = ref + y
+        assert torch.equal(outs[i], ref)
+        assert bool((ecs[i] == 1).all())
 
 def test_vecadd_f32_bit_exact_all_shapes(P, stream):
     g = torch.Generator(device="cuda").manual_seed(0)
