@@ -886,6 +886,18 @@ def preempt_latencies_us(res_list, clk, queued=None):
     return out
 
 
+def busy_fraction(requests, t0, t1):
+    """Fraction of [t0, t1] covered by the union of [arrival, completion]."""
+    iv = sorted((max(a, t0), min(c, t1)) for a, c in requests if c > t0 and a < t1)
+    busy, end = 0, t0
+    for a, c in iv:
+        if c <= end:
+            continue
+        busy += c - max(a, end)
+        end = c
+    return busy / max(1, t1 - t0)
+
+
 def drain_us(res_list):
     """First worker stop -> last worker exit (device clock only)."""
     return [(r["gt_last_exit"] - r["gt_first_stop"]) / 1e3 for res in res_list for r in res.launches
@@ -1096,6 +1108,10 @@ def main_colocate(args):
             win_p99.append([round(p99(ls) / 1e3), round(p99(lc) / 1e3)])
     be_co = sum(be_rate(r) for r in results) / len(results)
     overhead = 100.0 * (p99(co_lat) / p99(solo_lat) - 1.0)
+    # "no best-effort work while a request is in service" (ref scheduler.py:
+    # 302-306) caps BE at the idle fraction of each window: the union of the
+    # co-located requests' [arrival, completion] intervals after the warm-up
+    hp_busy = sum(busy_fraction(r.requests["hp"], warm, window) for r in results) / len(results)
     clkmap.close()
     n_queued = [0]
     pl_us = preempt_latencies_us(results, clkmap, n_queued)
@@ -1296,6 +1312,8 @@ def main_colocate(args):
             "be_steps_per_s": {"untransformed_solo": be_untransformed, "tally_solo": be_same_policy,
                                "colocated": be_co, "native_back_to_back": 1.0 / native_step_s},
             "be_throughput_pct_vs_native": 100.0 * be_co * native_step_s,
+            "hp_busy_fraction": hp_busy,
+            "be_throughput_pct_of_idle_ceiling": 100.0 * be_co * native_step_s / max(1e-9, 1.0 - hp_busy),
             "preempt_latency_us_p50_p99_max": worst["preempt_us"],
             "preempt_drain_us_p50_p99": worst["drain_us"], "preemptions": worst["preemptions"],
             "preemptions_of_queued_launches": worst["preemptions_queued"],

@@ -310,6 +310,7 @@ typedef struct {
   int parked;
   long long gpu_start_ns, gpu_end_ns;  /* GPU timeline (CUDA events vs a run-start reference
                                           event; -1 unless the "trace" option is set)       */
+  long long handle;         /* the device handle the runner got from submit (submission order) */
 } tally_launch_record;
 
 long long tally_device_run_origin_ns(int runner);   /* host ns that event times are relative to */

@@ -146,7 +146,8 @@ class c_launch_record(C.Structure):
                 ("complete_ns", C.c_longlong), ("preempt_ns", C.c_longlong),
                 ("gt_first_start", C.c_longlong), ("gt_first_stop", C.c_longlong),
                 ("gt_last_exit", C.c_longlong), ("parked", C.c_int),
-                ("gpu_start_ns", C.c_longlong), ("gpu_end_ns", C.c_longlong)]
+                ("gpu_start_ns", C.c_longlong), ("gpu_end_ns", C.c_longlong),
+                ("handle", C.c_longlong)]
 
 
 _SIGNATURES = {

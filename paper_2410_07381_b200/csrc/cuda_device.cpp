@@ -424,6 +424,7 @@ class CudaDevice : public Device {
     rec.parked = h.parked ? 1 : 0;
     rec.gpu_start_ns = h.gpu_start;
     rec.gpu_end_ns = h.gpu_end;
+    rec.handle = id;
     r_->log.launches.push_back(rec);
   }
 };

@@ -118,3 +118,77 @@ def test_lookahead_keeps_dependent_kernels_in_order(env, policy):
         print(cfgs)
         if "Ptb" in cfgs.values():
             assert any(r["parked"] for r in be_l)
+
+
+class _FixedChoices:
+    """A tuner stand-in with fixed choices (the B200 run and its replay must
+    use the same ones); ``bind`` is the only other call the runner makes."""
+
+    def __init__(self, choices):
+        self.choices = choices
+
+    def bind(self, kernel_id, kernel):
+        pass
+
+    def select(self, key, cost, threshold_ns=None):
+        return self.choices[key.kernel]
+
+
+@pytest.mark.parametrize("policy", ["Tally", "KernelPriority", "Eager"])
+def test_b200_dispatch_decisions_replay_through_reference_runner(env, policy):
+    """Dispatch-order parity on hardware: the native runner
+    drives the B200 in real time over an HP arrival trace and a best-effort
+    pipeline with one PTB, one Sliced and one Original kernel; its logged
+    decisions (every submission: task, kernel, shape, workers, resume
+    counter, blocks; every preemption) are replayed through the reference
+    policy runner (oracle restatement of scheduler.py) with each launch
+    completing when and how it did on the B200.  The reference runner must
+    make exactly the same decisions in the same order."""
+    from fractions import Fraction
+    import paper_2410_07381_b200 as P
+    from paper_2410_07381_b200 import kernels, workloads
+    from oracle import gpu_model as gm
+    from oracle import policy as opol
+    from oracle import replay as orp
+    from oracle import tuner as otu
+    _P, _w, dev, hp, _be, _bufs = env
+    g = torch.Generator(device="cuda").manual_seed(11)
+    sizes = {"be_ptb": 1 << 25, "be_sliced": 1 << 23, "be_orig": 1 << 20}
+    bufs, works = {}, []
+    for name, n in sizes.items():
+        a, b, c = (torch.rand(n, device="cuda", generator=g) for _ in range(3))
+        bufs[name] = (a, b, c)
+        k = kernels.vecadd_f32(a, b, c)
+        works.append(P.KernelWork(name, k.cost(), kernel=k))
+    pchoice = {"be_ptb": P.ConfigCandidate("Ptb", worker_count=296),
+               "be_sliced": P.ConfigCandidate("Sliced", fraction=Fraction(1, 4)),
+               "be_orig": P.ConfigCandidate("Original")}
+    horizon = 40_000_000
+    arr = workloads.generate_arrivals(0.3, 150_000, horizon, seed=5)
+    hp_w = P.KernelWork("vadd_hp", hp.cost(), kernel=hp)
+    tasks = [P.TaskScript("hp", P.HIGH, (hp_w,), arr), P.TaskScript("be", P.BEST_EFFORT, tuple(works))]
+    res = P.run_policy(dev.spec, tasks, P.SchedulerConfig(policy=policy), horizon,
+                       profiler=_FixedChoices(pchoice))
+    torch.cuda.synchronize()
+    for a, b, c in bufs.values():
+        assert torch.equal(c, a + b)
+    names = {(0, 0): ("hp", "vadd_hp")}
+    names.update({(1, i): ("be", w.kernel_id) for i, w in enumerate(works)})
+    ocost = lambda c: gm.KernelCostModel(c.block_duration_ns, c.launch_overhead_ns,   # noqa: E731
+                                         c.ptb_iteration_overhead_ns, c.threads_per_block, c.total_blocks)
+    otasks = [opol.TaskScript("hp", gm.HIGH, (opol.KernelWork("vadd_hp", ocost(hp_w.cost)),), arr),
+              opol.TaskScript("be", gm.BEST_EFFORT, tuple(opol.KernelWork(w.kernel_id, ocost(w.cost)) for w in works))]
+    ochoice = {k: otu.ConfigCandidate(v.variant, v.fraction, v.worker_count) for k, v in pchoice.items()}
+    sim, ores = orp.replay(gm.GpuSpec(148, 2048, 32), otasks, opol.SchedulerConfig(policy=policy), horizon,
+                           res.launches, names, ochoice)
+    assert sim.mismatch is None, sim.mismatch
+    assert len(sim.submitted) == len(res.launches) and not sim.expected
+    b200_pre = [(names[(r["task"], r["kernel_index"])][0], names[(r["task"], r["kernel_index"])][1],
+                 r["start_count"]) for r in sorted(res.launches, key=lambda r: r["handle"]) if r["preempt_ns"] >= 0]
+    assert sim.preempts == b200_pre
+    assert len(ores.requests["hp"]) == len(res.requests["hp"]) == len(arr)
+    assert len(ores.iterations["be"]) == len(res.iterations["be"])
+    if policy == "Tally":
+        shapes = {r["shape"] for r in res.launches}
+        assert shapes == {0, 1, 2}
+        assert b200_pre, "no preemption happened"
