@@ -46,6 +46,11 @@ extern "C" {
 #define TALLY_EV_KERNEL_FINISHED 3
 #define TALLY_EV_PREEMPT_SIGNALED 4
 #define TALLY_EV_WORKER_PARKED 5
+/* B200 device log only (not a reference event kind): a runner timer fired --
+ * block = the time it was scheduled for, time_ns = when the daemon ran it.
+ * Arrivals fire at the first loop pass at or after their trace time; the
+ * replay parity test needs the order in which they met completions. */
+#define TALLY_EV_TIMER_FIRED 6
 
 #define TALLY_POLICY_TALLY 0
 #define TALLY_POLICY_EAGER 1
@@ -187,6 +192,10 @@ typedef struct {
                                every PTB launch queued behind it on the stream (B200
                                real-time look-ahead; a parked launch raises the word for
                                its successors before it exits) */
+  unsigned long long* block_log; /* optional device array[total_blocks * 3]: per logical block
+                               {start, end} on the device %globaltimer and {worker << 32 | smid}
+                               (BlockStarted / BlockFinished, ref sim.py:436-505; the
+                               hand-written streaming kinds and IR-JIT kinds -- not the GEMMs) */
 } tally_launch_desc;
 
 typedef struct {

@@ -44,8 +44,13 @@ class ReplaySim:
     the B200 run's did.  ``records``: the B200 ``RunResult.launches`` dicts;
     ``names``: (task index, kernel index) -> (task_id, kernel_id)."""
 
-    def __init__(self, records, names):
+    def __init__(self, records, names, timers=()):
         self.now = 0
+        # runner timers run when the B200 daemon ran them (an arrival meets a
+        # completion in the order the daemon saw them, not in trace order)
+        self._fired = {}
+        for t, f in timers:
+            self._fired.setdefault(t, []).append(f)
         self._q, self._tie = [], 0
         self.observer = None
         self.dispatch_filter = None
@@ -62,7 +67,8 @@ class ReplaySim:
         self._tie += 1
 
     def call_at(self, t, fn):
-        self._at(t, fn)
+        q = self._fired.get(t)
+        self._at(q.pop(0) if q else t, fn)
 
     def kick(self):
         pass
@@ -134,14 +140,15 @@ class FixedProfiler:
         return self.choices[key.kernel]
 
 
-def replay(gpu, tasks, config, horizon_ns, records, names, choices):
+def replay(gpu, tasks, config, horizon_ns, records, names, choices, timers=()):
     """Run the reference policy runner on ``ReplaySim``; returns the sim
-    (``submitted``, ``preempts``, ``mismatch``) and the RunResult."""
+    (``submitted``, ``preempts``, ``mismatch``) and the RunResult.
+    ``timers``: the B200 run's (scheduled, fired) timer log."""
     from . import policy as pol
     sims = []
 
     def factory(g, placement_seed=0, record_events=True):
-        s = ReplaySim(records, names)
+        s = ReplaySim(records, names, timers)
         sims.append(s)
         return s
     r = pol.PolicyRunner(gpu, tasks, config, horizon_ns, profiler=FixedProfiler(choices), sim_cls=factory)

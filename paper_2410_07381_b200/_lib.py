@@ -76,7 +76,7 @@ class c_launch_desc(C.Structure):
                 ("sub_z", C.c_uint), ("workers", C.c_int), ("start_count", C.c_longlong),
                 ("preempt_at", C.c_longlong), ("exec_count", C.c_void_p),
                 ("pausable", C.c_int), ("worker_log", C.c_void_p), ("timed", C.c_int),
-                ("chain", C.c_int)]
+                ("chain", C.c_int), ("block_log", C.c_void_p)]
 
 
 class c_launch_state(C.Structure):

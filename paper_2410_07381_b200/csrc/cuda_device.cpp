@@ -160,6 +160,15 @@ class CudaDevice : public Device {
         Tm tm = timers_.top();
         timers_.pop();
         last_fired_ = tm.t;
+        {
+          tally_event e;
+          e.time_ns = now();
+          e.kind = TALLY_EV_TIMER_FIRED;
+          e.task = -1;
+          e.kernel_index = -1;
+          e.block = tm.t;
+          r_->log.events.push_back(e);
+        }
         r_->fire(tm.token);
         dispatch();
         progress = true;

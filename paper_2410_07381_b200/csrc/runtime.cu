@@ -281,6 +281,7 @@ int Runtime::launch(int kernel, int stream, const tally_launch_desc* d, int* out
   SliceArgs s{};
   s.grid = in.grid;
   s.exec_count = d->exec_count;
+  s.block_log = d->block_log;
   PtbArgs pa{};
   const void* fn = nullptr;
   dim3 grid;
@@ -407,6 +408,7 @@ int Runtime::launch(int kernel, int stream, const tally_launch_desc* d, int* out
       pa.grid = in.grid;
       pa.exec_count = d->exec_count;
       pa.worker_log = d->worker_log;
+      pa.block_log = d->block_log;
       pa.pause = (d->pausable && kk.pausable) ? d_pause : nullptr;
       fn = kk.fn_ptb;
       grid = dim3((unsigned)d->workers, 1, 1);

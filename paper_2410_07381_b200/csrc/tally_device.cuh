@@ -70,6 +70,7 @@ struct SliceArgs {
   unsigned long long linear_offset;  // linear mode: first task index of the slice
   unsigned int linear;               // 1: 1-D sub-grid over task indices
   unsigned long long* exec_count;  // optional exactly-once counters [total]
+  unsigned long long* block_log;   // optional [total * 3]: start, end (%globaltimer), smid per logical block
 };
 
 struct PtbArgs {
@@ -93,6 +94,7 @@ struct PtbArgs {
   unsigned long long* exec_count;  // optional exactly-once counters [total]
   unsigned long long* worker_log;  // optional [workers * 4] per-worker telemetry
   const unsigned int* pause;       // optional suspension word (device memory); non-zero = hold
+  unsigned long long* block_log;   // optional [total * 3]: start, end, (worker << 32 | smid) per logical block
 };
 
 __device__ __forceinline__ bool ptb_park_requested(const PtbArgs& a, unsigned f) {
@@ -177,6 +179,17 @@ struct MinBlocks<B, void_t_<decltype(B::kMinBlocks)>> {
   static constexpr int value = B::kMinBlocks;
 };
 
+__device__ __forceinline__ unsigned smid();
+
+// Per-logical-block event log (ref sim.py:436-505 BlockStarted / BlockFinished
+// on the device clock), written by thread 0 once the whole block is done.
+__device__ __forceinline__ void log_block(unsigned long long* log, unsigned long long i, unsigned long long t0,
+                                          unsigned long long who) {
+  log[3 * i] = t0;
+  log[3 * i + 1] = globaltimer();
+  log[3 * i + 2] = who;
+}
+
 // --- Original: the untransformed kernel --------------------------------------
 template <class Body>
 __global__ void __launch_bounds__(Body::kThreads, MinBlocks<Body>::value)
@@ -185,7 +198,12 @@ k_original(const typename Body::Params p, const SliceArgs s) {
   const uint3 g = make_uint3(gridDim.x, gridDim.y, gridDim.z);
   if (s.exec_count != nullptr && threadIdx.x == 0)
     atomicAdd(&s.exec_count[linear_index(blockIdx, g)], 1ull);
+  const unsigned long long t0 = s.block_log != nullptr ? globaltimer() : 0ull;
   Body::run(p, blockIdx, g, smem);
+  if (s.block_log != nullptr) {   // uniform across the block
+    __syncthreads();
+    if (threadIdx.x == 0) log_block(s.block_log, linear_index(blockIdx, g), t0, smid());
+  }
 }
 
 // --- Sliced: block offset + pinned gridDim ------------------------------------
@@ -198,7 +216,12 @@ k_sliced(const typename Body::Params p, const SliceArgs s) {
                                         blockIdx.z + s.offset.z);
   if (s.exec_count != nullptr && threadIdx.x == 0)
     atomicAdd(&s.exec_count[linear_index(b, s.grid)], 1ull);
+  const unsigned long long t0 = s.block_log != nullptr ? globaltimer() : 0ull;
   Body::run(p, b, s.grid, smem);
+  if (s.block_log != nullptr) {
+    __syncthreads();
+    if (threadIdx.x == 0) log_block(s.block_log, linear_index(b, s.grid), t0, smid());
+  }
 }
 
 // --- PTB: persistent, preemptible workers -------------------------------------
@@ -355,10 +378,13 @@ k_ptb(const typename Body::Params p, const PtbArgs a) {
       break;
     }
     if (leader) next = ptb_claim(a);   // in flight while the body runs
+    const unsigned long long t0 = (leader && a.block_log != nullptr) ? globaltimer() : 0ull;
     Body::run(p, delinearize((unsigned long long)task, a.grid), a.grid, smem);
     ++done;
     if (leader) s_task[(it + 1) & 1] = next;
     __syncthreads();
+    if (leader && a.block_log != nullptr)
+      log_block(a.block_log, (unsigned long long)task, t0, ((unsigned long long)blockIdx.x << 32) | smid());
   }
   if (leader) {
     if (a.worker_log != nullptr) {

@@ -175,17 +175,19 @@ class DeviceKernel:
                    f"{self.kind} launch")
         return Launch(lid.value, desc.shape)
 
-    def original(self, stream: Stream, exec_count=None, timed=False) -> Launch:
+    def original(self, stream: Stream, exec_count=None, timed=False, block_log=None) -> Launch:
+        """``block_log``: optional uint64/int64 CUDA tensor [total_blocks, 3]
+        receiving per logical block (start, end, smid) on the device clock."""
         d = _lib.c_launch_desc(shape=_lib.SHAPE_ORIGINAL, preempt_at=-1,
-                               exec_count=_ptr(exec_count), timed=int(timed))
+                               exec_count=_ptr(exec_count), timed=int(timed), block_log=_ptr(block_log))
         return self._launch(stream, d)
 
     def sliced(self, stream: Stream, offset: int, count: int, exec_count=None,
-               timed=False) -> Launch:
+               timed=False, block_log=None) -> Launch:
         """Logical blocks [offset, offset + count) of the x-fastest order."""
         d = _lib.c_launch_desc(shape=_lib.SHAPE_SLICED, linear=1, linear_offset=offset,
                                count=count, preempt_at=-1, exec_count=_ptr(exec_count),
-                               timed=int(timed))
+                               timed=int(timed), block_log=_ptr(block_log))
         return self._launch(stream, d)
 
     def sliced_rect(self, stream: Stream, offset, sub_grid, exec_count=None) -> Launch:
@@ -197,7 +199,7 @@ class DeviceKernel:
         return self._launch(stream, d)
 
     def ptb(self, stream: Stream, workers: int, start_count: int = 0, preempt_at=None,
-            exec_count=None, timed=False, worker_log=None, chain=False) -> Launch:
+            exec_count=None, timed=False, worker_log=None, chain=False, block_log=None) -> Launch:
         """``worker_log``: optional int64 CUDA tensor [workers, 4] receiving per
         worker ``(smid << 32 | blocks done, t_entry, t_exit, stopped)`` on the
         device %globaltimer clock.  ``chain``: park on the stream's shared
@@ -206,7 +208,7 @@ class DeviceKernel:
         d = _lib.c_launch_desc(shape=_lib.SHAPE_PTB, workers=workers, start_count=start_count,
                                preempt_at=-1 if preempt_at is None else preempt_at,
                                exec_count=_ptr(exec_count), worker_log=_ptr(worker_log),
-                               timed=int(timed), chain=int(chain))
+                               timed=int(timed), chain=int(chain), block_log=_ptr(block_log))
         return self._launch(stream, d)
 
     def cost(self, block_duration_ns: int = 0, launch_overhead_ns: int = DEFAULT_LAUNCH_OVERHEAD_NS,

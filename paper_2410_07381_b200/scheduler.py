@@ -112,8 +112,10 @@ class RunResult:
     horizon_ns: int
     launches: list = field(default_factory=list)
     origin_ns: int = 0
+    timers: list = field(default_factory=list)   # B200: (scheduled for, fired at) of every runner timer
 
 
+TIMER_FIRED = 6   # TALLY_EV_TIMER_FIRED: a B200 device-log record, not a reference event kind
 _VARIANT_CODE = {ORIGINAL: _lib.SHAPE_ORIGINAL, SLICED: _lib.SHAPE_SLICED, PTB: _lib.SHAPE_PTB}
 
 
@@ -325,9 +327,12 @@ class PolicyRunner:
         n = lib.tally_device_event_count(rid)
         evs = (_lib.c_event * max(1, n))()
         lib.tally_device_events(rid, evs, n)
-        events = []
+        events, timers = [], []
         for k in range(n):
             e = evs[k]
+            if e.kind == TIMER_FIRED:
+                timers.append((e.block, e.time_ns))   # (scheduled for, ran at)
+                continue
             t = self.tasks[e.task]
             kid = t.kernels[e.kernel_index].kernel_id if e.kernel_index >= 0 else "?"
             events.append(SimEvent(e.time_ns, k, EVENT_KINDS[e.kind], t.task_id, kid, e.block))
@@ -337,7 +342,7 @@ class PolicyRunner:
         launches = [{f: getattr(recs[k], f) for f, _ in _lib.c_launch_record._fields_}
                     for k in range(n)]
         return RunResult(events if self.record_events else [], requests, iterations,
-                         self.horizon_ns, launches, lib.tally_device_run_origin_ns(rid))
+                         self.horizon_ns, launches, lib.tally_device_run_origin_ns(rid), timers)
 
 
 def run_policy(gpu, tasks, config: SchedulerConfig, horizon_ns: int, profiler=None,

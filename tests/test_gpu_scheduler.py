@@ -71,6 +71,9 @@ def test_tally_keeps_hp_tail_close_to_solo(env):
     print(f"solo p99 {s / 1e3:.1f} us, co-located p99 {c / 1e3:.1f} us, "
           f"BE iterations {len(co.iterations['be'])}")
     assert co.iterations["be"]
+    if c >= 4 * s + 100_000:   # diagnose: the slowest requests and what BE was doing then
+        slow = sorted(((c2 - a2, a2) for a2, c2 in co.requests["hp"]), reverse=True)[:5]
+        print("slowest", slow)
     assert c < 4 * s + 100_000
 
 
@@ -180,7 +183,7 @@ def test_b200_dispatch_decisions_replay_through_reference_runner(env, policy):
               opol.TaskScript("be", gm.BEST_EFFORT, tuple(opol.KernelWork(w.kernel_id, ocost(w.cost)) for w in works))]
     ochoice = {k: otu.ConfigCandidate(v.variant, v.fraction, v.worker_count) for k, v in pchoice.items()}
     sim, ores = orp.replay(gm.GpuSpec(148, 2048, 32), otasks, opol.SchedulerConfig(policy=policy), horizon,
-                           res.launches, names, ochoice)
+                           res.launches, names, ochoice, res.timers)
     assert sim.mismatch is None, sim.mismatch
     assert len(sim.submitted) == len(res.launches) and not sim.expected
     b200_pre = [(names[(r["task"], r["kernel_index"])][0], names[(r["task"], r["kernel_index"])][1],
@@ -192,3 +195,64 @@ def test_b200_dispatch_decisions_replay_through_reference_runner(env, policy):
         shapes = {r["shape"] for r in res.launches}
         assert shapes == {0, 1, 2}
         assert b200_pre, "no preemption happened"
+
+
+@pytest.mark.parametrize("policy", ["Tally", "KernelPriority", "Eager"])
+def test_reference_runner_drives_the_b200_through_b200sim(env, policy):
+    """The GpuSim surface over the C ABI (b200sim.B200Sim): the reference
+    policy runner (oracle restatement of scheduler.py, unchanged) drives the
+    B200 in real time -- HP requests complete, BE outputs are exact, and the
+    event log has the reference's kinds including per-logical-block
+    BlockStarted / BlockFinished from the device clock, each block of every
+    finished launch exactly once."""
+    from fractions import Fraction
+    import collections
+    from paper_2410_07381_b200 import b200sim, kernels, workloads
+    from oracle import gpu_model as gm
+    from oracle import policy as opol
+    from oracle import replay as orp
+    from oracle import tuner as otu
+    _P, _w, dev, hp, _be, _bufs = env
+    g = torch.Generator(device="cuda").manual_seed(12)
+    sizes = {"be_ptb": 1 << 24, "be_sliced": 1 << 22, "be_orig": 1 << 20}
+    bufs, dks = {}, {"vadd_hp": hp}
+    for name, n in sizes.items():
+        a, b, c = (torch.rand(n, device="cuda", generator=g) for _ in range(3))
+        bufs[name] = (a, b, c)
+        dks[name] = kernels.vecadd_f32(a, b, c)
+    cost = lambda dk: gm.KernelCostModel(1000, 5000, 1000, dk.info.threads_per_block, dk.total_blocks)  # noqa: E731
+    horizon = 30_000_000
+    arr = workloads.generate_arrivals(0.3, 150_000, horizon, seed=9)
+    tasks = [opol.TaskScript("hp", gm.HIGH, (opol.KernelWork("vadd_hp", cost(hp)),), arr),
+             opol.TaskScript("be", gm.BEST_EFFORT, tuple(opol.KernelWork(k, cost(dks[k])) for k in sizes))]
+    choice = {"be_ptb": otu.ConfigCandidate("Ptb", worker_count=296),
+              "be_sliced": otu.ConfigCandidate("Sliced", fraction=Fraction(1, 4)),
+              "be_orig": otu.ConfigCandidate("Original")}
+    sims = []
+
+    def make(gpu, placement_seed=0, record_events=True):
+        s = b200sim.B200Sim(gpu, record_events=record_events, kernels=dks)
+        sims.append(s)
+        return s
+    r = opol.PolicyRunner(dev.spec, tasks, opol.SchedulerConfig(policy=policy), horizon,
+                          profiler=orp.FixedProfiler(choice), sim_cls=make)
+    r.start_policy_clock()
+    res = r.run()
+    torch.cuda.synchronize()
+    assert len(res.requests["hp"]) == len(arr)
+    assert res.iterations["be"]
+    for a, b, c in bufs.values():
+        assert torch.equal(c, a + b)
+    evs = res.events
+    kinds = collections.Counter(e.kind for e in evs)
+    assert kinds["BlockStarted"] == kinds["BlockFinished"] > 0
+    assert kinds["LaunchIssued"] and kinds["KernelFinished"]
+    if policy == "Tally":
+        assert kinds["PreemptSignaled"] and kinds["WorkerParked"]
+    # every logical block of the Original best-effort kernel: once per launch
+    n_orig = sum(1 for e in evs if e.kind == "KernelFinished" and e.kernel == "be_orig")
+    fin = collections.Counter(e.block for e in evs if e.kind == "BlockFinished" and e.kernel == "be_orig")
+    assert set(fin.values()) == {n_orig} and len(fin) == dks["be_orig"].total_blocks
+    assert gm.events_to_csv(evs).startswith("time_ns,kind,task,kernel,block\n")
+    assert all(a.time <= b.time for a, b in zip(evs, evs[1:]))
+    sims[0].close()
