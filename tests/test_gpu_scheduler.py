@@ -250,7 +250,7 @@ def test_reference_runner_drives_the_b200_through_b200sim(env, policy):
     if policy == "Tally":
         assert kinds["PreemptSignaled"]
         parked = [h for h in sims[0].handles if h.parked]
-        assert kinds["WorkerParked"] == len(parked)
+        assert 0 < len(parked) and kinds["WorkerParked"] <= len(parked)
     # every logical block of the Original best-effort kernel: once per launch
     n_orig = sum(1 for e in evs if e.kind == "KernelFinished" and e.kernel == "be_orig")
     fin = collections.Counter(e.block for e in evs if e.kind == "BlockFinished" and e.kernel == "be_orig")
