@@ -112,7 +112,7 @@ class ReplaySim:
         h.finish_time = self.now
         if r["parked"]:
             h.parked = True
-            h.task_counter = min(r["task_counter"], h.cost.total_blocks)
+            h.task_counter = r["task_counter"]
             self._emit(WORKER_PARKED, h)
         else:
             h.done = True

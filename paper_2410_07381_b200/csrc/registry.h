@@ -28,11 +28,16 @@ struct Instance {
   // new PTB chain starts (start_count == 0); freed with the instance.
   void* resume_ring = nullptr;
   size_t resume_bytes = 0;
+  // k_ptb return ring (bounded retirement, tally_device.cuh): allocated at the
+  // first PTB launch; ret_pending = entries the last parked launch left
+  unsigned long long* ret_ring = nullptr;
+  unsigned long long ret_pending = 0;
   Instance() = default;
   Instance(const Instance&) = delete;
   Instance& operator=(const Instance&) = delete;
   ~Instance() {
     if (resume_ring) cudaFree(resume_ring);
+    if (ret_ring) cudaFree(ret_ring);
   }
   unsigned long long total() const {
     return (unsigned long long)grid.x * grid.y * grid.z;

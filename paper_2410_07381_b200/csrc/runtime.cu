@@ -373,6 +373,27 @@ int Runtime::launch(int kernel, int stream, const tally_launch_desc* d, int* out
         cudaError_t me = cudaMemsetAsync(in.resume_ring, 0, in.resume_bytes, st);
         if (me != cudaSuccess) { free_recs.push_back(rec); return cuda_fail(me, "resume ring reset"); }
       }
+      pa.ret_ring = nullptr;
+      pa.ret_pending = 0;
+      if (kk.tmem_cols == 0 && !kk.copy) {
+        // generic k_ptb workers: the instance's return ring (bounded retirement)
+        Instance& mi = *instances[kernel];
+        if (mi.ret_ring == nullptr) {
+          const size_t bytes = (2 + kRetCap) * sizeof(unsigned long long);
+          cudaError_t me = cudaMalloc(&mi.ret_ring, bytes);
+          if (me == cudaSuccess) me = cudaMemset(mi.ret_ring, 0, bytes);
+          if (me != cudaSuccess) { free_recs.push_back(rec); return cuda_fail(me, "return ring"); }
+          mi.ret_pending = 0;
+        }
+        if (d->start_count == 0 && mi.ret_pending > 0) {
+          // a new chain: drop blocks an abandoned one handed back
+          cudaError_t me = cudaMemsetAsync(mi.ret_ring, 0, 2 * sizeof(unsigned long long), st);
+          if (me != cudaSuccess) { free_recs.push_back(rec); return cuda_fail(me, "return ring reset"); }
+          mi.ret_pending = 0;
+        }
+        pa.ret_ring = mi.ret_ring;
+        pa.ret_pending = mi.ret_pending;
+      }
       std::atomic_thread_fence(std::memory_order_seq_cst);
       pa.rec = d_recs + rec;
       // few, rare readers (a GEMM producer per SM, once per tile) -> the flag
@@ -495,6 +516,9 @@ bool Runtime::poll(Launch* L) {
     L->gt_first_start = (long long)m->t_first_start;
     L->parked = (m->status == kMirrorParked);
     L->finished = true;
+    if (L->kernel >= 0 && L->kernel < (int)instances.size() && instances[L->kernel] &&
+        instances[L->kernel]->ret_ring != nullptr)
+      instances[L->kernel]->ret_pending = m->ret_pending;
     return true;
   }
   cudaError_t e = cudaEventQuery(L->ev_end);

@@ -50,7 +50,8 @@ struct alignas(64) LaunchMirror {
   unsigned long long t_first_start;  // %globaltimer at first worker entry
   unsigned int serial;               // written last: == launch serial when valid
   unsigned int status;               // 1 = exhausted (done), 2 = parked
-  unsigned long long pad[2];
+  unsigned long long ret_pending;    // logical blocks handed back to the chain (k_ptb), not yet run
+  unsigned long long pad;
 };
 
 enum : unsigned { kMirrorDone = 1, kMirrorParked = 2 };
@@ -95,7 +96,15 @@ struct PtbArgs {
   unsigned long long* worker_log;  // optional [workers * 4] per-worker telemetry
   const unsigned int* pause;       // optional suspension word (device memory); non-zero = hold
   unsigned long long* block_log;   // optional [total * 3]: start, end, (worker << 32 | smid) per logical block
+  // Bounded retirement (k_ptb): a worker that sees the flag after a block
+  // hands its pre-claimed block back through the kernel instance's return
+  // ring ([0] pushes, [1] pops, [2 + i % kRetCap] block + 1) instead of
+  // running it; the next launch of the chain pops those first.
+  unsigned long long* ret_ring;
+  unsigned long long ret_pending;  // entries the previous launch of the chain left (0: skip the ring)
 };
+
+constexpr unsigned kRetCap = 8192;   // >= the most resident workers of any launch (148 x 32)
 
 __device__ __forceinline__ bool ptb_park_requested(const PtbArgs& a, unsigned f) {
   return (int)(f - a.park_at) >= 0;
@@ -283,7 +292,9 @@ __device__ __forceinline__ void ptb_worker_exit(const PtbArgs& a, bool stopped,
     m->stops = atomicAdd(&r->stops, 0ull);
     m->t_first_start = atomicAdd(&r->t_first_start, 0ull);
     // work can only remain if some worker stopped on the flag
-    const bool parked = progress < a.total || resume_pending(resume_ring) > 0;
+    const unsigned long long pending = resume_pending(resume_ring);
+    m->ret_pending = pending;
+    const bool parked = progress < a.total || pending > 0;
     m->status = parked ? kMirrorParked : kMirrorDone;
     if (parked && a.chain_dev != nullptr) {
       // a parked chain launch parks everything queued behind it on the stream:
@@ -318,6 +329,7 @@ __device__ __forceinline__ bool ptb_hold_while_paused(const PtbArgs& a) {
   }
 }
 
+template <bool kCountExec = true>
 __device__ __forceinline__ long long ptb_claim(const PtbArgs& a) {
   ptb_hold_while_paused(a);
   const unsigned f = a.flag_is_host ? ld_acquire_sys(a.flag) : ld_acquire_gpu(a.flag);
@@ -326,9 +338,43 @@ __device__ __forceinline__ long long ptb_claim(const PtbArgs& a) {
   const long long task = (long long)(a.start + c);
   if (a.preempt_at >= 0 && task + 1 == a.preempt_at)
     st_release_sys(const_cast<unsigned*>(a.flag), a.park_at);   // test trigger (MemTrigger)
-  if (a.exec_count != nullptr && (unsigned long long)task < a.total)
+  if (kCountExec && a.exec_count != nullptr && (unsigned long long)task < a.total)
     atomicAdd(&a.exec_count[task], 1ull);
   return task;
+}
+
+// A block an earlier launch of the chain handed back; -1 when none is left.
+__device__ __forceinline__ long long ptb_pop(const PtbArgs& a) {
+  unsigned long long* ring = a.ret_ring;
+  for (;;) {
+    const unsigned long long h = atomicAdd(ring + 1, 0ull), t = atomicAdd(ring, 0ull);
+    if (h >= t) return -1;
+    if (atomicCAS(ring + 1, h, h + 1) != h) continue;
+    volatile unsigned long long* e = ring + 2 + (h % kRetCap);
+    unsigned long long v;
+    while ((v = *e) == 0ull) __nanosleep(32);
+    *e = 0ull;
+    return (long long)v - 1;
+  }
+}
+
+__device__ __forceinline__ void ptb_return(const PtbArgs& a, long long task) {
+  const unsigned long long i = atomicAdd(a.ret_ring, 1ull);
+  reinterpret_cast<volatile unsigned long long*>(a.ret_ring)[2 + (i % kRetCap)] = (unsigned long long)task + 1ull;
+}
+
+// The next block of a k_ptb worker: a handed-back one while the host says
+// some are pending (flag first, as for a claim), else a fresh claim.
+__device__ __forceinline__ long long ptb_next(const PtbArgs& a, bool& try_pop) {
+  if (try_pop) {
+    ptb_hold_while_paused(a);
+    const unsigned f = a.flag_is_host ? ld_acquire_sys(a.flag) : ld_acquire_gpu(a.flag);
+    if (ptb_park_requested(a, f)) return -1;
+    const long long t = ptb_pop(a);
+    if (t >= 0) return t;
+    try_pop = false;
+  }
+  return ptb_claim<false>(a);
 }
 
 // Batched claim: n consecutive task indices with one flag-gated atomic.
@@ -356,9 +402,10 @@ __device__ __forceinline__ unsigned smid() {
 
 // Persistent worker loop.  The leader claims task i+1 while the CTA executes
 // task i (claim-ahead), so the flag load and the L2 atomic overlap the body
-// instead of serialising with it; a claimed task is always executed, so on
-// preemption a worker retires after at most its current and its pre-claimed
-// logical block.
+// instead of serialising with it.  Retirement stays bounded by one logical
+// block: after block i the leader re-reads the flag, and if it rose meanwhile
+// the pre-claimed block i+1 is handed back through the return ring (encoded
+// as -(task + 2) in the broadcast) instead of being run.
 template <class Body>
 __global__ void __launch_bounds__(Body::kThreads, MinBlocks<Body>::value)
 k_ptb(const typename Body::Params p, const PtbArgs a) {
@@ -367,21 +414,37 @@ k_ptb(const typename Body::Params p, const PtbArgs a) {
   const bool leader = (threadIdx.x == 0);
   const unsigned long long t_entry = leader ? globaltimer() : 0ull;
   bool stopped = false;
+  bool try_pop = a.ret_ring != nullptr && a.ret_pending > 0;
   unsigned long long done = 0;
   long long next = 0;
-  if (leader) s_task[0] = ptb_claim(a);
+  if (leader) s_task[0] = ptb_next(a, try_pop);
   __syncthreads();
   for (unsigned it = 0;; ++it) {
     const long long task = s_task[it & 1];
+    if (task < -1) {   // the flag rose during the previous block: hand this one back
+      if (leader) ptb_return(a, -task - 2);
+      stopped = true;
+      break;
+    }
     if (task < 0 || (unsigned long long)task >= a.total) {
       stopped = task < 0;
       break;
     }
-    if (leader) next = ptb_claim(a);   // in flight while the body runs
+    if (leader) {
+      next = ptb_next(a, try_pop);   // in flight while the body runs
+      if (a.exec_count != nullptr) atomicAdd(&a.exec_count[task], 1ull);
+    }
     const unsigned long long t0 = (leader && a.block_log != nullptr) ? globaltimer() : 0ull;
     Body::run(p, delinearize((unsigned long long)task, a.grid), a.grid, smem);
     ++done;
-    if (leader) s_task[(it + 1) & 1] = next;
+    if (leader) {
+      long long nx = next;
+      if (a.ret_ring != nullptr && nx >= 0 && (unsigned long long)nx < a.total) {
+        const unsigned f = a.flag_is_host ? ld_relaxed_sys(a.flag) : ld_relaxed_gpu(a.flag);
+        if (ptb_park_requested(a, f)) nx = -nx - 2;
+      }
+      s_task[(it + 1) & 1] = nx;
+    }
     __syncthreads();
     if (leader && a.block_log != nullptr)
       log_block(a.block_log, (unsigned long long)task, t0, ((unsigned long long)blockIdx.x << 32) | smid());
@@ -394,7 +457,7 @@ k_ptb(const typename Body::Params p, const PtbArgs a) {
       w[2] = globaltimer();
       w[3] = stopped ? 1ull : 0ull;
     }
-    ptb_worker_exit(a, stopped, t_entry);
+    ptb_worker_exit(a, stopped, t_entry, a.ret_ring);
   }
 }
 

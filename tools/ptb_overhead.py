@@ -1,0 +1,86 @@
+"""Transformation cost per kernel kind on the B200 (diagnostics, not the bench
+contract): every kernel of a configuration's training step launched
+untransformed and as PTB at full resident occupancy, each launch timed alone
+with CUDA events (L2 not flushed: the step's own order warms it), summed per
+kind; PTB / Original time per kind is the inverse of the "transformed kernel
+at >= 0.90 of untransformed" target.
+
+    python tools/ptb_overhead.py [--config c2|c3|c4] [--reps 3] [--out FILE]
+"""
+
+from __future__ import annotations
+
+import argparse
+import collections
+import json
+import os
+import sys
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+
+import torch  # noqa: E402
+
+import paper_2410_07381_b200 as P  # noqa: E402
+from paper_2410_07381_b200 import kernels  # noqa: E402
+
+
+def program(config):
+    g = torch.Generator(device="cuda").manual_seed(0)
+    if config == "c2":
+        from paper_2410_07381_b200 import resnet
+        tr = resnet.ResNet50Train(batch=64, image=224)
+        tr.set_batch(torch.randn(64, 3, 224, 224, device="cuda", generator=g),
+                     torch.randint(0, 1000, (64,), device="cuda", generator=g))
+    elif config == "c3":
+        from paper_2410_07381_b200 import gpt2
+        tr = gpt2.GPT2Train(batch=8, seq=1024)
+        tr.set_batch(torch.randint(0, tr.V, (8, 1025), device="cuda", generator=g))
+    else:
+        from paper_2410_07381_b200 import bert
+        tr = bert.BertTrain(batch=8, seq=512)
+        tr.set_batch(torch.randint(0, tr.V, (8, 512), device="cuda", generator=g),
+                     torch.randint(0, tr.V, (8, 512), device="cuda", generator=g))
+    return tr
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--config", default="c4", choices=["c2", "c3", "c4"])
+    ap.add_argument("--reps", type=int, default=3)
+    ap.add_argument("--out", default=None)
+    args = ap.parse_args()
+    P.B200Device.get(0)
+    s = kernels.Stream(high_priority=False)
+    tr = program(args.config)
+    tr.step_original(s)
+    tr.step_original(s)
+    torch.cuda.synchronize()
+    orig = collections.defaultdict(float)
+    ptb = collections.defaultdict(float)
+    n = collections.Counter()
+    for _ in range(args.reps):
+        for name, dk in tr.program:
+            L = dk.original(s, timed=True)
+            L.wait()
+            orig[dk.kind] += L.elapsed_ns / 1e3 / args.reps
+            w = min(dk.total_blocks, 148 * max(1, dk.info.occupancy_ptb))
+            L = dk.ptb(s, w, timed=True)
+            L.wait()
+            ptb[dk.kind] += L.elapsed_ns / 1e3 / args.reps
+    for name, dk in tr.program:
+        n[dk.kind] += 1
+    tot_o, tot_p = sum(orig.values()), sum(ptb.values())
+    out = {"config": args.config, "kernels": len(tr.program), "step_us_original": tot_o, "step_us_ptb": tot_p,
+           "ptb_vs_original_speed": tot_o / tot_p,
+           "by_kind": {k: {"n": n[k], "original_us": round(orig[k], 1), "ptb_us": round(ptb[k], 1),
+                           "speed_ratio": round(orig[k] / ptb[k], 3)}
+                       for k in sorted(orig, key=lambda k: -orig[k])}}
+    txt = json.dumps(out, indent=1)
+    print(txt)
+    if args.out:
+        with open(args.out, "w") as fh:
+            fh.write(txt)
+
+
+if __name__ == "__main__":
+    main()
