@@ -1,0 +1,217 @@
+"""Generic best-effort routing: any PyTorch training step as a Tally program.
+
+The reference schedules a best-effort job as a pipeline of ``KernelWork``s,
+running untransformable kernels "exempt" -- whole, untransformed (ref
+``scheduler.py:345-349``).  The hand-written programs in
+``resnet.py`` / ``gpt2.py`` / ``bert.py`` are such pipelines written by hand;
+this module derives one from an unmodified PyTorch step function:
+
+1. ``capture(step_fn, *args)`` runs the step once eagerly under a
+   ``TorchDispatchMode`` and records every ATen call (forward, autograd
+   backward and optimizer) with the tensors it read and produced.  Those
+   tensors stay alive: the program is static, like a CUDA graph.
+2. Dense contractions become this package's transformable tcgen05 GEMM
+   kernels (Original / Sliced / PTB): ``aten.mm`` and ``aten.addmm`` on
+   bf16 with a supported operand layout (A K-major or MN-major, B K-major or
+   MN-major, not A MN-major with B K-major) and N, K multiples of 64, and
+   ``aten.bmm`` on contiguous batches.  ``addmm``'s bias is added by the next
+   exempt segment.
+3. Every maximal run of other ops (elementwise, normalisation, softmax,
+   reductions, optimizer foreach ops, copies) is captured into one CUDA graph
+   that re-executes them on the recorded tensors (results copied into the
+   recorded outputs, view ops skipped -- the recorded views alias static
+   storage) and becomes one exempt ``cuda_graph`` step.
+
+The result is a ``Program`` whose ``works()`` are ``KernelWork``s for
+``TaskScript``: the profile-guided tuner shapes the GEMMs like any other
+kernel, and the scheduler preempts them by flag; the exempt graphs run whole.
+Requirements are those of CUDA-graph capture: the step must be graph-safe
+(no host synchronisation, no data-dependent shapes, no CPU-side state the
+replay would have to advance).
+"""
+
+from __future__ import annotations
+
+import threading
+
+import torch
+from torch.utils._python_dispatch import TorchDispatchMode
+from torch.utils._pytree import tree_flatten
+
+from . import kernels
+from .scheduler import KernelWork
+
+aten = torch.ops.aten
+_GEMM_OPS = {aten.mm.default, aten.addmm.default, aten.bmm.default}
+
+
+class _Record:
+    __slots__ = ("func", "args", "kwargs", "out")
+
+    def __init__(self, func, args, kwargs, out):
+        self.func, self.args, self.kwargs, self.out = func, args, kwargs, out
+
+
+class _Recorder(TorchDispatchMode):
+    """Records every ATen call in execution order (the autograd engine's
+    worker thread inherits the mode, so backward ops are seen too)."""
+
+    def __init__(self):
+        super().__init__()
+        self.records = []
+        self._lock = threading.Lock()
+
+    def __torch_dispatch__(self, func, types, args=(), kwargs=None):
+        kwargs = kwargs or {}
+        out = func(*args, **kwargs)
+        with self._lock:
+            self.records.append(_Record(func, args, kwargs, out))
+        return out
+
+
+def _cuda_tensors(x):
+    return [t for t in tree_flatten(x)[0] if isinstance(t, torch.Tensor) and t.is_cuda]
+
+
+def _mn_major(t):
+    """2-D t stored transposed (column-major): t.t() is a row-major view."""
+    return t.dim() == 2 and t.stride(0) == 1 and t.stride(1) >= t.shape[0]
+
+
+def _k_major(t):
+    return t.dim() == 2 and t.stride(1) == 1 and t.stride(0) >= t.shape[1]
+
+
+def _gemm_kernel(rec):
+    """The transformable kernel for a recorded mm / addmm / bmm, or None."""
+    f, a = rec.func, rec.args
+    if f is aten.bmm.default:
+        X, Y = a
+        out = rec.out
+        if not (X.dtype == Y.dtype == out.dtype == torch.bfloat16 and X.is_contiguous() and Y.is_contiguous()
+                and out.is_contiguous()):
+            return None
+        Bn, M, K = X.shape
+        N = Y.shape[2]
+        if K % 64 or N % 64 or M % 8:
+            return None
+        # C_z[M,N] = X_z[M,K] . Y_z[K,N]: A K-major, B MN-major (stored [K,N]); batch z moves rows
+        return kernels.gemm_ex(X.view(Bn * M, K), Y.view(Bn * K, N), out.view(Bn * M, N), M, N, K,
+                               a_mn=False, b_mn=True, batches=Bn,
+                               a_off=((M, 0), (0, 0)), b_off=((K, 0), (0, 0)), c_off=((M, 0), (0, 0)))
+    X, Y = (a[1], a[2]) if f is aten.addmm.default else (a[0], a[1])
+    out = rec.out
+    if f is aten.addmm.default and (rec.kwargs.get("beta", 1) != 1 or rec.kwargs.get("alpha", 1) != 1):
+        return None
+    if not (X.dtype == Y.dtype == out.dtype == torch.bfloat16 and out.is_contiguous() and out.dim() == 2):
+        return None
+    M, K = X.shape
+    N = Y.shape[1]
+    if K % 64 or N % 64 or M % 8:
+        return None
+    if _k_major(X):
+        A, a_mn = X, False
+    elif _mn_major(X):
+        A, a_mn = X.t(), True
+    else:
+        return None
+    if _mn_major(Y):
+        B, b_mn = Y.t(), False          # Y = W^T of a row-major W[N,K] (nn.Linear)
+    elif _k_major(Y):
+        B, b_mn = Y, True               # Y row-major [K,N]
+    else:
+        return None
+    if a_mn and not b_mn:
+        return None                     # no A MN-major x B K-major kind
+    return kernels.gemm_ex(A, B, out, M, N, K, a_mn=a_mn, b_mn=b_mn)
+
+
+class Program:
+    """A captured step: ``items`` in order, each ("gemm", DeviceKernel, record)
+    or ("graph", DeviceKernel, records).  ``works(prefix)`` -> KernelWorks."""
+
+    def __init__(self, items, records):
+        self.items = items
+        self.records = records          # keeps every recorded tensor alive
+
+    def works(self, prefix="step"):
+        out = []
+        for i, (what, dk, _r) in enumerate(self.items):
+            if what == "gemm":
+                kid = f"{prefix}.{i}:{dk.kind}:{dk.info.grid}"
+                out.append(KernelWork(kid, dk.cost(), kernel=dk))
+            else:
+                out.append(KernelWork(f"{prefix}.{i}:graph", dk.cost(), exempt=True, kernel=dk))
+        return tuple(out)
+
+    @property
+    def n_gemm(self):
+        return sum(1 for w, _d, _r in self.items if w == "gemm")
+
+    def run_original(self, stream):
+        """The program once, every step untransformed, in order."""
+        for _w, dk, _r in self.items:
+            dk.original(stream).wait()
+
+
+def _replay(records):
+    """Re-execute recorded non-view ops on the recorded tensors (inside a
+    CUDA-graph capture), writing results into the recorded outputs."""
+    for r in records:
+        if r.func.is_view:
+            continue
+        res = r.func(*r.args, **r.kwargs)
+        outs = tree_flatten(r.out)[0]
+        got = tree_flatten(res)[0]
+        for o, g in zip(outs, got):
+            if isinstance(o, torch.Tensor) and isinstance(g, torch.Tensor) and o.is_cuda and \
+                    o.data_ptr() != g.data_ptr():
+                o.copy_(g)
+
+
+def _bias_add(rec):
+    """addmm's bias, added after the GEMM in the next exempt segment."""
+    bias, out = rec.args[0], rec.out
+    return _Record(aten.add_.Tensor, (out, bias), {}, out)
+
+
+def capture(step_fn, *args, **kwargs) -> Program:
+    """Run ``step_fn(*args, **kwargs)`` once (eagerly, with its real effects)
+    and return the Tally program that re-executes it."""
+    rec = _Recorder()
+    with rec:
+        step_fn(*args, **kwargs)
+    torch.cuda.synchronize()
+    records = [r for r in rec.records if _cuda_tensors((r.args, r.kwargs, r.out))]
+    items, segment = [], []
+    side = torch.cuda.Stream()
+
+    def flush():
+        if not [r for r in segment if not r.func.is_view]:
+            segment.clear()
+            return
+        g = torch.cuda.CUDAGraph()
+        seg = list(segment)
+        # capture only -- no warm-up replay: re-running the segment would
+        # apply its in-place updates (optimizer) a second time
+        side.wait_stream(torch.cuda.current_stream())
+        with torch.cuda.graph(g, stream=side):
+            _replay(seg)
+        torch.cuda.synchronize()
+        items.append(("graph", kernels.cuda_graph(g), seg))
+        segment.clear()
+
+    for r in records:
+        dk = _gemm_kernel(r) if r.func in _GEMM_OPS else None
+        if dk is None:
+            segment.append(r)
+            continue
+        flush()
+        items.append(("gemm", dk, r))
+        if r.func is aten.addmm.default:
+            segment.append(_bias_add(r))
+    flush()
+    return Program(items, records)
+
+
+__all__ = ["capture", "Program"]

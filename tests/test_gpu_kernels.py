@@ -80,11 +80,15 @@ def test_ptb_preempt_at_every_counter_then_resume(P, stream, gold):
             first = dk.ptb(stream, workers, preempt_at=c, exec_count=ec).wait()
             ctr = first.task_counter
             assert ctr >= min(c, 16) if c > 0 else ctr >= 16
-            assert first.parked == (ctr < 16)
-            # every block below the counter ran exactly once, none above it
+            # every block below the counter ran exactly once or was handed
+            # back unrun (bounded retirement: at most one per worker), none
+            # above it ran
             counts = ec.cpu().tolist()
-            assert counts[:min(ctr, 16)] == [1] * min(ctr, 16)
+            below = counts[:min(ctr, 16)]
+            returned = below.count(0)
+            assert set(below) <= {0, 1} and returned <= workers
             assert counts[min(ctr, 16):] == [0] * (16 - min(ctr, 16))
+            assert first.parked == (ctr < 16 or returned > 0)
             if first.parked:
                 second = dk.ptb(stream, workers, start_count=ctr, exec_count=ec).wait()
                 assert second.done and second.task_counter >= 16
