@@ -132,6 +132,8 @@ int Runtime::init(int dev, tally_gpu_info* out) {
 
   CK(cudaMalloc(&d_recs, sizeof(LaunchRec) * kMaxRecs), "cudaMalloc(launch records)");
   CK(cudaMemset(d_recs, 0, sizeof(LaunchRec) * kMaxRecs), "cudaMemset(launch records)");
+  CK(cudaMalloc(&d_groups, sizeof(ExitGroup) * kMaxRecs * kMaxExitGroups), "cudaMalloc(exit groups)");
+  CK(cudaMemset(d_groups, 0, sizeof(ExitGroup) * kMaxRecs * kMaxExitGroups), "cudaMemset(exit groups)");
   CK(cudaHostAlloc(&h_mirrors, sizeof(LaunchMirror) * kMaxRecs, cudaHostAllocMapped),
      "cudaHostAlloc(mirrors)");
   memset(h_mirrors, 0, sizeof(LaunchMirror) * kMaxRecs);
@@ -375,6 +377,7 @@ int Runtime::launch(int kernel, int stream, const tally_launch_desc* d, int* out
       }
       pa.ret_ring = nullptr;
       pa.ret_pending = 0;
+      pa.static_n = 0;
       if (kk.tmem_cols == 0 && !kk.copy) {
         // generic k_ptb workers: the instance's return ring (bounded retirement)
         Instance& mi = *instances[kernel];
@@ -393,6 +396,17 @@ int Runtime::launch(int kernel, int stream, const tally_launch_desc* d, int* out
         }
         pa.ret_ring = mi.ret_ring;
         pa.ret_pending = mi.ret_pending;
+        // static first blocks (no claim round trip) unless the launch resumes
+        // handed-back blocks or runs the counter-triggered test preemption
+        if (mi.ret_pending == 0 && d->preempt_at < 0 && (unsigned long long)d->start_count < total)
+          pa.static_n = std::min<unsigned long long>((unsigned long long)d->workers,
+                                                     total - (unsigned long long)d->start_count);
+      }
+      pa.grp = d_groups + (size_t)rec * kMaxExitGroups;
+      if (d->workers > kMaxExitGroups * kExitGroupSize) {
+        free_recs.push_back(rec);
+        set_error("at most %d PTB workers", kMaxExitGroups * kExitGroupSize);
+        return TALLY_EINVAL;
       }
       std::atomic_thread_fence(std::memory_order_seq_cst);
       pa.rec = d_recs + rec;

@@ -62,6 +62,7 @@ struct Runtime {
   cudaStream_t sig_stream = nullptr;
 
   LaunchRec* d_recs = nullptr;
+  ExitGroup* d_groups = nullptr;      // [kMaxRecs][kMaxExitGroups] two-level worker retirement
   LaunchMirror* h_mirrors = nullptr;
   LaunchMirror* d_mirrors = nullptr;
   volatile unsigned* h_flags = nullptr;

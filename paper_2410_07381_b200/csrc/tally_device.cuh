@@ -31,14 +31,28 @@ namespace tally {
 // publishes the outcome to the host mirror and re-zeroes the record so it can
 // be reused without a host-side memset.
 struct alignas(64) LaunchRec {
-  unsigned long long claims;        // atomicAdd target: tasks claimed by this launch
-  unsigned int exited;              // workers that have left the loop
+  unsigned long long claims;        // atomicAdd target: dynamic claims of this launch
+  unsigned int exited;              // exit groups that have folded into this record
   unsigned int flag;                // device-resident preemption flag (holds a serial)
-  unsigned long long t_first_stop;  // %globaltimer when the first worker saw the flag (0 = none)
-  unsigned long long t_last_exit;   // %globaltimer of the last worker exit
+  unsigned long long neg_first_stop;   // ~min %globaltimer a worker saw the flag (0 = none)
+  unsigned long long executed;      // logical blocks run by this launch
   unsigned long long stops;         // workers that stopped because of the flag
-  unsigned long long t_first_start; // %globaltimer of the earliest worker entry (0 = none yet)
+  unsigned long long neg_first_start;  // ~min worker entry %globaltimer (0 = none yet)
   unsigned long long pad[2];
+};
+
+// Worker retirement is two-level: workers fold into their group of 32
+// (blockIdx.x / 32), the last of a group folds the group into the launch
+// record -- ~32 + W/32 same-address atomics instead of W (one L2 atomic unit
+// serialises same-address atomics: ~1 us per 1184 workers).
+constexpr int kExitGroupSize = 32;
+constexpr int kMaxExitGroups = 160;   // >= 148 x 32 resident workers / 32
+struct alignas(16) ExitGroup {
+  unsigned int exited;
+  unsigned int pad;
+  unsigned long long neg_first_start;
+  unsigned long long executed;
+  unsigned long long pad2;
 };
 
 // Host-visible outcome of a launch (pinned, mapped; written once by the last worker).
@@ -102,6 +116,11 @@ struct PtbArgs {
   // running it; the next launch of the chain pops those first.
   unsigned long long* ret_ring;
   unsigned long long ret_pending;  // entries the previous launch of the chain left (0: skip the ring)
+  // Static first blocks (k_ptb): worker b < static_n runs block start + b
+  // without a claim (the flag still gates it; a worker that sees it hands
+  // the block back); dynamic claims continue from start + static_n.
+  unsigned long long static_n;
+  ExitGroup* grp;                  // this launch's exit groups [kMaxExitGroups]
 };
 
 constexpr unsigned kRetCap = 8192;   // >= the most resident workers of any launch (148 x 32)
@@ -243,10 +262,19 @@ k_sliced(const typename Body::Params p, const SliceArgs s) {
 // resident workers, so the ring never overflows.
 constexpr unsigned kResumeCap = 1024;
 
+__device__ __forceinline__ unsigned long long ld_relaxed_gpu_u64(const unsigned long long* p) {
+  unsigned long long v;
+  asm volatile("ld.relaxed.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+  return v;
+}
+
+// Entries pending in a resume / return ring.  Called after an acquire that
+// orders every push and pop of the launch before it, so plain (relaxed)
+// loads suffice -- no read-modify-write round trips.
 __device__ __forceinline__ unsigned long long resume_pending(const unsigned long long* ring) {
   if (ring == nullptr) return 0ull;
-  const unsigned long long tail = atomicAdd(const_cast<unsigned long long*>(ring), 0ull);
-  const unsigned long long head = atomicAdd(const_cast<unsigned long long*>(ring + 1), 0ull);
+  const unsigned long long tail = ld_relaxed_gpu_u64(ring);
+  const unsigned long long head = ld_relaxed_gpu_u64(ring + 1);
   return tail > head ? tail - head : 0ull;
 }
 
@@ -256,61 +284,82 @@ __device__ __forceinline__ unsigned atom_add_acq_rel_gpu(unsigned* p, unsigned v
   return old;
 }
 
-// Worker retirement.  One acq_rel atomic per worker on the exit counter (it
-// releases the worker's outputs and, for the last worker, acquires everyone
-// else's): the last worker to exit is by construction the latest exit, so it
-// stamps t_last_exit itself and publishes the mirror, `serial` last with a
-// system-scope release store.  (Three fences and four atomics per worker
-// here cost a short PTB launch ~5-9 us, ~40 % of an 18 us elementwise
-// kernel.)
+// Worker retirement (thread 0 of every worker).  Minima are kept as maxima of
+// the complement (records are zero between launches) and every per-worker
+// update is a fire-and-forget reduction; the only round trips are the
+// group's and the record's acq_rel exit counters.  The last group's last
+// worker is by construction the latest exit: it stamps t_last_exit, decides
+// done / parked and publishes the host mirror, `serial` last with a
+// system-scope release store, then recycles the record.
+// `executed`: logical blocks this worker ran; `static_returned`: static
+// first blocks it handed back on the flag.
 __device__ __forceinline__ void ptb_worker_exit(const PtbArgs& a, bool stopped,
                                                 unsigned long long t_entry,
-                                                const unsigned long long* resume_ring = nullptr) {
+                                                const unsigned long long* resume_ring = nullptr,
+                                                unsigned long long executed = 0) {
   LaunchRec* r = a.rec;
-  {
-    // earliest worker entry: min over workers (the record is zero between launches)
-    const unsigned long long prev = atomicCAS(&r->t_first_start, 0ull, t_entry);
-    if (prev != 0ull && t_entry < prev) atomicMin(&r->t_first_start, t_entry);
-  }
-  if (stopped) {
-    const unsigned long long now = globaltimer();
-    atomicAdd(&r->stops, 1ull);
-    // first observation of the flag: min over workers
-    unsigned long long prev = atomicCAS(&r->t_first_stop, 0ull, now);
-    if (prev != 0ull && now < prev) atomicMin(&r->t_first_stop, now);
-  }
   const unsigned nworkers = gridDim.x * gridDim.y * gridDim.z;
-  if (atom_add_acq_rel_gpu(&r->exited, 1u) + 1u == nworkers) {
-    // last worker: publish and recycle the record
-    const unsigned long long now = globaltimer();
-    const unsigned long long claims = atomicAdd(&r->claims, 0ull);
-    const unsigned long long progress = a.start + claims;
-    volatile LaunchMirror* m = a.mirror;
-    m->claims = claims;
-    m->t_first_stop = atomicAdd(&r->t_first_stop, 0ull);
-    m->t_last_exit = now;
-    m->stops = atomicAdd(&r->stops, 0ull);
-    m->t_first_start = atomicAdd(&r->t_first_start, 0ull);
-    // work can only remain if some worker stopped on the flag
-    const unsigned long long pending = resume_pending(resume_ring);
-    m->ret_pending = pending;
-    const bool parked = progress < a.total || pending > 0;
-    m->status = parked ? kMirrorParked : kMirrorDone;
-    if (parked && a.chain_dev != nullptr) {
-      // a parked chain launch parks everything queued behind it on the stream:
-      // the next launch starts after this one exits (stream order) and reads
-      // the raised word, whichever of the host's two writes it would poll
-      atomicMax(a.chain_dev, a.park_at);
-      if (a.chain_host != nullptr) st_release_sys(a.chain_host, a.park_at);
-    }
-    st_release_sys(const_cast<unsigned*>(&m->serial), a.serial);
-    r->claims = 0ull;
-    r->exited = 0u;
-    r->t_first_stop = 0ull;
-    r->t_last_exit = 0ull;
-    r->stops = 0ull;
-    r->t_first_start = 0ull;
+  const unsigned g = blockIdx.x / kExitGroupSize;
+  const unsigned ngroups = (nworkers + kExitGroupSize - 1) / kExitGroupSize;
+  const unsigned gsize = min((unsigned)kExitGroupSize, nworkers - g * kExitGroupSize);
+  ExitGroup* eg = a.grp + g;
+  atomicMax(&eg->neg_first_start, ~t_entry);
+  if (executed) atomicAdd(&eg->executed, executed);
+  if (stopped) {
+    atomicAdd(&r->stops, 1ull);
+    atomicMax(&r->neg_first_stop, ~globaltimer());
   }
+  if (atom_add_acq_rel_gpu(&eg->exited, 1u) + 1u != gsize) return;
+  // last of the group: fold the group into the record and reset it
+  const unsigned long long gs = ld_relaxed_gpu_u64(&eg->neg_first_start);
+  const unsigned long long ge = ld_relaxed_gpu_u64(&eg->executed);
+  eg->neg_first_start = 0ull;
+  eg->executed = 0ull;
+  eg->exited = 0u;
+  atomicMax(&r->neg_first_start, gs);
+  if (ge) atomicAdd(&r->executed, ge);
+  if (atom_add_acq_rel_gpu(&r->exited, 1u) + 1u != ngroups) return;
+  // last worker: publish and recycle the record
+  const unsigned long long now = globaltimer();
+  unsigned long long claims = a.static_n + ld_relaxed_gpu_u64(&r->claims);
+  const unsigned long long nfs = ld_relaxed_gpu_u64(&r->neg_first_stop);
+  const unsigned long long nst = ld_relaxed_gpu_u64(&r->neg_first_start);
+  const unsigned long long stops = ld_relaxed_gpu_u64(&r->stops);
+  const unsigned long long ran = ld_relaxed_gpu_u64(&r->executed);
+  if (a.static_n && ran == 0ull && claims == a.static_n && a.ret_ring != nullptr) {
+    // preempted before any block ran (e.g. queued behind a parked launch):
+    // every static block was handed back -- take them back out of the ring
+    // and report the launch untouched (counter == start, like a flag seen
+    // before the first claim)
+    atomicAdd(a.ret_ring, (unsigned long long)(0ull - a.static_n));
+    claims = 0ull;
+  }
+  const unsigned long long pending = resume_pending(resume_ring);
+  const unsigned long long progress = a.start + claims;
+  volatile LaunchMirror* m = a.mirror;
+  m->claims = claims;
+  m->t_first_stop = nfs ? ~nfs : 0ull;
+  m->t_last_exit = now;
+  m->stops = stops;
+  m->t_first_start = nst ? ~nst : 0ull;
+  m->ret_pending = pending;
+  // work can only remain if some worker stopped on the flag
+  const bool parked = progress < a.total || pending > 0;
+  m->status = parked ? kMirrorParked : kMirrorDone;
+  if (parked && a.chain_dev != nullptr) {
+    // a parked chain launch parks everything queued behind it on the stream:
+    // the next launch starts after this one exits (stream order) and reads
+    // the raised word, whichever of the host's two writes it would poll
+    atomicMax(a.chain_dev, a.park_at);
+    if (a.chain_host != nullptr) st_release_sys(a.chain_host, a.park_at);
+  }
+  st_release_sys(const_cast<unsigned*>(&m->serial), a.serial);
+  r->claims = 0ull;
+  r->exited = 0u;
+  r->neg_first_stop = 0ull;
+  r->executed = 0ull;
+  r->stops = 0ull;
+  r->neg_first_start = 0ull;
 }
 
 // One claim by the leader thread: check the flag first, then fetch-and-add
@@ -335,11 +384,24 @@ __device__ __forceinline__ long long ptb_claim(const PtbArgs& a) {
   const unsigned f = a.flag_is_host ? ld_acquire_sys(a.flag) : ld_acquire_gpu(a.flag);
   if (ptb_park_requested(a, f)) return -1;   // flag gates the claim: a parked launch never over-claims
   const unsigned long long c = atomicAdd(&a.rec->claims, 1ull);
-  const long long task = (long long)(a.start + c);
+  const long long task = (long long)(a.start + a.static_n + c);
   if (a.preempt_at >= 0 && task + 1 == a.preempt_at)
     st_release_sys(const_cast<unsigned*>(a.flag), a.park_at);   // test trigger (MemTrigger)
   if (kCountExec && a.exec_count != nullptr && (unsigned long long)task < a.total)
     atomicAdd(&a.exec_count[task], 1ull);
+  return task;
+}
+
+// The claim-ahead inside the k_ptb loop: the flag was read at the end of the
+// previous block (or at entry), so the claim is issued without another load
+// (one exposed L2 round trip per block instead of two); a claim that races a
+// flag raised in between is handed back after the block.
+__device__ __forceinline__ long long ptb_claim_gated(const PtbArgs& a) {
+  ptb_hold_while_paused(a);
+  const unsigned long long c = atomicAdd(&a.rec->claims, 1ull);
+  const long long task = (long long)(a.start + a.static_n + c);
+  if (a.preempt_at >= 0 && task + 1 == a.preempt_at)
+    st_release_sys(const_cast<unsigned*>(a.flag), a.park_at);   // test trigger (MemTrigger)
   return task;
 }
 
@@ -385,7 +447,7 @@ __device__ __forceinline__ long long ptb_claim_n(const PtbArgs& a, int n) {
   const unsigned f = a.flag_is_host ? ld_acquire_sys(a.flag) : ld_acquire_gpu(a.flag);
   if (ptb_park_requested(a, f)) return -1;
   const unsigned long long c = atomicAdd(&a.rec->claims, (unsigned long long)n);
-  const long long task = (long long)(a.start + c);
+  const long long task = (long long)(a.start + a.static_n + c);
   if (a.preempt_at >= 0 && task < a.preempt_at && a.preempt_at <= task + n)
     st_release_sys(const_cast<unsigned*>(a.flag), a.park_at);   // test trigger (MemTrigger)
   if (a.exec_count != nullptr)
@@ -417,11 +479,20 @@ k_ptb(const typename Body::Params p, const PtbArgs a) {
   bool try_pop = a.ret_ring != nullptr && a.ret_pending > 0;
   unsigned long long done = 0;
   long long next = 0;
-  if (leader) s_task[0] = ptb_next(a, try_pop);
+  if (leader) {
+    if (blockIdx.x < a.static_n) {
+      // static first block: no claim round trip, the flag still gates it
+      const unsigned f = a.flag_is_host ? ld_acquire_sys(a.flag) : ld_acquire_gpu(a.flag);
+      const long long mine = (long long)(a.start + blockIdx.x);
+      s_task[0] = ptb_park_requested(a, f) ? -mine - 2 : mine;
+    } else {
+      s_task[0] = ptb_next(a, try_pop);
+    }
+  }
   __syncthreads();
   for (unsigned it = 0;; ++it) {
     const long long task = s_task[it & 1];
-    if (task < -1) {   // the flag rose during the previous block: hand this one back
+    if (task < -1) {   // the flag rose before this block started: hand it back
       if (leader) ptb_return(a, -task - 2);
       stopped = true;
       break;
@@ -431,18 +502,19 @@ k_ptb(const typename Body::Params p, const PtbArgs a) {
       break;
     }
     if (leader) {
-      next = ptb_next(a, try_pop);   // in flight while the body runs
+      // in flight while the body runs (the flag was clear when this block began)
+      next = try_pop ? ptb_next(a, try_pop) : ptb_claim_gated(a);
       if (a.exec_count != nullptr) atomicAdd(&a.exec_count[task], 1ull);
     }
     const unsigned long long t0 = (leader && a.block_log != nullptr) ? globaltimer() : 0ull;
     Body::run(p, delinearize((unsigned long long)task, a.grid), a.grid, smem);
     ++done;
     if (leader) {
+      // bounded retirement: a flag raised while this block ran hands the
+      // pre-claimed block back instead of running it
       long long nx = next;
-      if (a.ret_ring != nullptr && nx >= 0 && (unsigned long long)nx < a.total) {
-        const unsigned f = a.flag_is_host ? ld_relaxed_sys(a.flag) : ld_relaxed_gpu(a.flag);
-        if (ptb_park_requested(a, f)) nx = -nx - 2;
-      }
+      const unsigned f = a.flag_is_host ? ld_relaxed_sys(a.flag) : ld_relaxed_gpu(a.flag);
+      if (ptb_park_requested(a, f) && nx >= 0 && (unsigned long long)nx < a.total) nx = -nx - 2;
       s_task[(it + 1) & 1] = nx;
     }
     __syncthreads();
@@ -457,7 +529,7 @@ k_ptb(const typename Body::Params p, const PtbArgs a) {
       w[2] = globaltimer();
       w[3] = stopped ? 1ull : 0ull;
     }
-    ptb_worker_exit(a, stopped, t_entry, a.ret_ring);
+    ptb_worker_exit(a, stopped, t_entry, a.ret_ring, done);
   }
 }
 

@@ -36,7 +36,7 @@ import threading
 
 import torch
 from torch.utils._python_dispatch import TorchDispatchMode
-from torch.utils._pytree import tree_flatten
+from torch.utils._pytree import tree_flatten, tree_map
 
 from . import kernels
 from .scheduler import KernelWork
@@ -84,10 +84,11 @@ def _k_major(t):
 
 def _gemm_kernel(rec):
     """The transformable kernel for a recorded mm / addmm / bmm, or None."""
-    f, a = rec.func, rec.args
+    f = rec.func
+    a = tuple(t.detach() if isinstance(t, torch.Tensor) else t for t in rec.args)
     if f is aten.bmm.default:
         X, Y = a
-        out = rec.out
+        out = rec.out.detach()
         if not (X.dtype == Y.dtype == out.dtype == torch.bfloat16 and X.is_contiguous() and Y.is_contiguous()
                 and out.is_contiguous()):
             return None
@@ -100,7 +101,7 @@ def _gemm_kernel(rec):
                                a_mn=False, b_mn=True, batches=Bn,
                                a_off=((M, 0), (0, 0)), b_off=((K, 0), (0, 0)), c_off=((M, 0), (0, 0)))
     X, Y = (a[1], a[2]) if f is aten.addmm.default else (a[0], a[1])
-    out = rec.out
+    out = rec.out.detach()
     if f is aten.addmm.default and (rec.kwargs.get("beta", 1) != 1 or rec.kwargs.get("alpha", 1) != 1):
         return None
     if not (X.dtype == Y.dtype == out.dtype == torch.bfloat16 and out.is_contiguous() and out.dim() == 2):
@@ -160,7 +161,10 @@ def _replay(records):
     for r in records:
         if r.func.is_view:
             continue
-        res = r.func(*r.args, **r.kwargs)
+        # detached aliases: same storage, no autograd metadata (the replay is
+        # data movement, not a differentiable program)
+        det = lambda t: t.detach() if isinstance(t, torch.Tensor) else t   # noqa: E731
+        res = r.func(*tree_map(det, r.args), **tree_map(det, r.kwargs))
         outs = tree_flatten(r.out)[0]
         got = tree_flatten(res)[0]
         for o, g in zip(outs, got):
@@ -182,6 +186,11 @@ def capture(step_fn, *args, **kwargs) -> Program:
     with rec:
         step_fn(*args, **kwargs)
     torch.cuda.synchronize()
+    with torch.no_grad():
+        return _build(rec)
+
+
+def _build(rec) -> Program:
     records = [r for r in rec.records if _cuda_tensors((r.args, r.kwargs, r.out))]
     items, segment = [], []
     side = torch.cuda.Stream()
