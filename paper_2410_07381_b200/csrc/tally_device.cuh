@@ -477,6 +477,9 @@ k_ptb(const typename Body::Params p, const PtbArgs a) {
   const unsigned long long t_entry = leader ? globaltimer() : 0ull;
   bool stopped = false;
   bool try_pop = a.ret_ring != nullptr && a.ret_pending > 0;
+  // the static blocks cover the rest of the kernel: no claim (it could only
+  // fail) and no end-of-block flag read (nothing is pre-claimed)
+  const bool covered = a.static_n > 0 && a.start + a.static_n >= a.total;
   unsigned long long done = 0;
   long long next = 0;
   if (leader) {
@@ -503,7 +506,7 @@ k_ptb(const typename Body::Params p, const PtbArgs a) {
     }
     if (leader) {
       // in flight while the body runs (the flag was clear when this block began)
-      next = try_pop ? ptb_next(a, try_pop) : ptb_claim_gated(a);
+      next = covered ? (long long)a.total : try_pop ? ptb_next(a, try_pop) : ptb_claim_gated(a);
       if (a.exec_count != nullptr) atomicAdd(&a.exec_count[task], 1ull);
     }
     const unsigned long long t0 = (leader && a.block_log != nullptr) ? globaltimer() : 0ull;
@@ -513,8 +516,10 @@ k_ptb(const typename Body::Params p, const PtbArgs a) {
       // bounded retirement: a flag raised while this block ran hands the
       // pre-claimed block back instead of running it
       long long nx = next;
-      const unsigned f = a.flag_is_host ? ld_relaxed_sys(a.flag) : ld_relaxed_gpu(a.flag);
-      if (ptb_park_requested(a, f) && nx >= 0 && (unsigned long long)nx < a.total) nx = -nx - 2;
+      if (nx >= 0 && (unsigned long long)nx < a.total) {
+        const unsigned f = a.flag_is_host ? ld_relaxed_sys(a.flag) : ld_relaxed_gpu(a.flag);
+        if (ptb_park_requested(a, f)) nx = -nx - 2;
+      }
       s_task[(it + 1) & 1] = nx;
     }
     __syncthreads();

@@ -56,7 +56,7 @@ def test_captured_step_matches_eager(env):
     _step(ref_m, ref_opt, x, y)
     prog = intercept.capture(_step, m, opt, x, y)      # eager step 2, recorded
     _step(ref_m, ref_opt, x, y)
-    assert prog.n_gemm >= 6             # 2 forward + 4 backward matmuls
+    assert prog.n_gemm >= 5             # 2 forward + 3 backward matmuls (no grad for the input)
     kinds = {it[1].kind for it in prog.items if it[0] == "gemm"}
     assert any(k.startswith("gemm_bf16") for k in kinds)
     s = kernels.Stream(high_priority=False)
@@ -69,16 +69,18 @@ def test_captured_step_matches_eager(env):
 
 
 def test_captured_step_under_tally_with_preemption(env):
+    """The captured program as the best-effort task of a Tally co-location
+    (its GEMMs in the tuner's shapes, parked and resumed at HP arrivals):
+    after n iterations the parameters are bit-identical to n untransformed
+    in-order runs of the same program from the same state."""
     P, x, y = env
     from paper_2410_07381_b200 import intercept, kernels, workloads
     dev = P.B200Device.get(0)
     m, opt = _model(3)
-    ref_m = copy.deepcopy(m)
-    ref_opt = torch.optim.SGD(ref_m.parameters(), lr=0.05, momentum=0.9)
     _step(m, opt, x, y)
-    _step(ref_m, ref_opt, x, y)
     prog = intercept.capture(_step, m, opt, x, y)
-    _step(ref_m, ref_opt, x, y)
+    state = [p for p in m.parameters()] + [opt.state[p]["momentum_buffer"] for p in m.parameters()]
+    snap = [t.detach().clone() for t in state]
     works = prog.works("mlp")
     g = torch.Generator(device="cuda").manual_seed(2)
     ha, hb, hc = (torch.rand(1 << 22, device="cuda", generator=g) for _ in range(3))
@@ -94,7 +96,15 @@ def test_captured_step_under_tally_with_preemption(env):
     n = len(res.iterations["be"])
     assert n >= 2 and len(res.requests["hp"]) == len(arr)
     assert torch.equal(hc, ha + hb)
+    shapes = {r["shape"] for r in res.launches if r["task"] == 1}
+    assert 2 in shapes, "no best-effort GEMM ran as PTB"
+    after_tally = [t.detach().clone() for t in state]
+    with torch.no_grad():
+        for t, v in zip(state, snap):
+            t.copy_(v)
+    s = kernels.Stream(high_priority=False)
     for _ in range(n):
-        _step(ref_m, ref_opt, x, y)
-    for (name, p), rp in zip(m.named_parameters(), ref_m.parameters()):
-        assert _rel(p, rp) < 3e-2, (name, n)
+        prog.run_original(s)
+    torch.cuda.synchronize()
+    for i, (a, b) in enumerate(zip(after_tally, state)):
+        assert torch.equal(a, b), (i, n)
