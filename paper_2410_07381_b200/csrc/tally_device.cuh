@@ -489,7 +489,7 @@ k_ptb(const typename Body::Params p, const PtbArgs a) {
       const long long mine = (long long)(a.start + blockIdx.x);
       s_task[0] = ptb_park_requested(a, f) ? -mine - 2 : mine;
     } else {
-      s_task[0] = ptb_next(a, try_pop);
+      s_task[0] = covered ? (long long)a.total : ptb_next(a, try_pop);   // surplus worker: nothing left
     }
   }
   __syncthreads();
