@@ -26,6 +26,9 @@ ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 COMMON = ["-O3", "-std=c++17", "-lineinfo", "-Xcompiler", "-fPIC,-Wall,-Wno-format-truncation",
           "-I", os.path.join(ROOT, "include"), "-I", CSRC]
 CU_FLAGS = ARCH + COMMON + ["-Xptxas", "-warn-spills", "--expt-relaxed-constexpr"]
+# experiments only: extra -D flags (e.g. TALLY_NVCC_DEFINES="-DFOO=1"); a
+# build with them is a different library -- force a rebuild after changing it
+CU_FLAGS += os.environ.get("TALLY_NVCC_DEFINES", "").split()
 
 SOURCES = ["runtime.cu", "kernels_basic.cu", "kernels_gemm.cu", "kernels_nn.cu", "kernels_tf.cu", "runner.cpp", "cuda_device.cpp"]
 HEADERS = ["tally_device.cuh", "registry.h", "runtime.h", "runner.h", "gemm_sm100.cuh"]

@@ -302,39 +302,38 @@ __device__ __forceinline__ void ptb_worker_exit(const PtbArgs& a, bool stopped,
   const unsigned g = blockIdx.x / kExitGroupSize;
   const unsigned ngroups = (nworkers + kExitGroupSize - 1) / kExitGroupSize;
   const unsigned gsize = min((unsigned)kExitGroupSize, nworkers - g * kExitGroupSize);
-  ExitGroup* eg = a.grp + g;
-  atomicMax(&eg->neg_first_start, ~t_entry);
-  if (executed) atomicAdd(&eg->executed, executed);
+  // fire-and-forget reductions straight into the record: the acq_rel exit
+  // counters below order them before the last worker's reads
+  atomicMax(&r->neg_first_start, ~t_entry);
+  if (executed) atomicAdd(&r->executed, executed);
   if (stopped) {
     atomicAdd(&r->stops, 1ull);
     atomicMax(&r->neg_first_stop, ~globaltimer());
   }
+  ExitGroup* eg = a.grp + g;
   if (atom_add_acq_rel_gpu(&eg->exited, 1u) + 1u != gsize) return;
-  // last of the group: fold the group into the record and reset it
-  const unsigned long long gs = ld_relaxed_gpu_u64(&eg->neg_first_start);
-  const unsigned long long ge = ld_relaxed_gpu_u64(&eg->executed);
-  eg->neg_first_start = 0ull;
-  eg->executed = 0ull;
-  eg->exited = 0u;
-  atomicMax(&r->neg_first_start, gs);
-  if (ge) atomicAdd(&r->executed, ge);
+  eg->exited = 0u;   // last of its group: recycle the group slot
   if (atom_add_acq_rel_gpu(&r->exited, 1u) + 1u != ngroups) return;
-  // last worker: publish and recycle the record
+  // last worker: one batch of independent loads, publish, recycle the record
   const unsigned long long now = globaltimer();
-  unsigned long long claims = a.static_n + ld_relaxed_gpu_u64(&r->claims);
+  const unsigned long long dyn = ld_relaxed_gpu_u64(&r->claims);
   const unsigned long long nfs = ld_relaxed_gpu_u64(&r->neg_first_stop);
   const unsigned long long nst = ld_relaxed_gpu_u64(&r->neg_first_start);
   const unsigned long long stops = ld_relaxed_gpu_u64(&r->stops);
   const unsigned long long ran = ld_relaxed_gpu_u64(&r->executed);
-  if (a.static_n && ran == 0ull && claims == a.static_n && a.ret_ring != nullptr) {
+  const unsigned long long tail = resume_ring ? ld_relaxed_gpu_u64(resume_ring) : 0ull;
+  const unsigned long long head = resume_ring ? ld_relaxed_gpu_u64(resume_ring + 1) : 0ull;
+  unsigned long long claims = a.static_n + dyn;
+  unsigned long long pending = tail > head ? tail - head : 0ull;
+  if (a.static_n && ran == 0ull && dyn == 0ull && a.ret_ring != nullptr) {
     // preempted before any block ran (e.g. queued behind a parked launch):
     // every static block was handed back -- take them back out of the ring
     // and report the launch untouched (counter == start, like a flag seen
     // before the first claim)
     atomicAdd(a.ret_ring, (unsigned long long)(0ull - a.static_n));
+    pending -= a.static_n;
     claims = 0ull;
   }
-  const unsigned long long pending = resume_pending(resume_ring);
   const unsigned long long progress = a.start + claims;
   volatile LaunchMirror* m = a.mirror;
   m->claims = claims;
@@ -353,13 +352,17 @@ __device__ __forceinline__ void ptb_worker_exit(const PtbArgs& a, bool stopped,
     atomicMax(a.chain_dev, a.park_at);
     if (a.chain_host != nullptr) st_release_sys(a.chain_host, a.park_at);
   }
-  st_release_sys(const_cast<unsigned*>(&m->serial), a.serial);
   r->claims = 0ull;
   r->exited = 0u;
   r->neg_first_stop = 0ull;
   r->executed = 0ull;
   r->stops = 0ull;
   r->neg_first_start = 0ull;
+#ifdef TALLY_MIRROR_RELAXED   // timing experiment only: no ordering for the host
+  asm volatile("st.relaxed.sys.global.u32 [%0], %1;" :: "l"(&m->serial), "r"(a.serial) : "memory");
+#else
+  st_release_sys(const_cast<unsigned*>(&m->serial), a.serial);
+#endif
 }
 
 // One claim by the leader thread: check the flag first, then fetch-and-add
