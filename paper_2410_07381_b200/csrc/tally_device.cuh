@@ -335,13 +335,6 @@ __device__ __forceinline__ void ptb_worker_exit(const PtbArgs& a, bool stopped,
     claims = 0ull;
   }
   const unsigned long long progress = a.start + claims;
-#ifdef TALLY_MIRROR_NONE   // timing experiment only: the host never learns the outcome
-  if (progress < 0ull) return;
-  r->claims = 0ull; r->exited = 0u; r->neg_first_stop = 0ull; r->executed = 0ull; r->stops = 0ull;
-  r->neg_first_start = 0ull;
-  (void)nfs; (void)nst; (void)stops; (void)now; (void)pending;
-  return;
-#endif
   volatile LaunchMirror* m = a.mirror;
   m->claims = claims;
   m->t_first_stop = nfs ? ~nfs : 0ull;
@@ -365,11 +358,7 @@ __device__ __forceinline__ void ptb_worker_exit(const PtbArgs& a, bool stopped,
   r->executed = 0ull;
   r->stops = 0ull;
   r->neg_first_start = 0ull;
-#ifdef TALLY_MIRROR_RELAXED   // timing experiment only: no ordering for the host
-  asm volatile("st.relaxed.sys.global.u32 [%0], %1;" :: "l"(&m->serial), "r"(a.serial) : "memory");
-#else
   st_release_sys(const_cast<unsigned*>(&m->serial), a.serial);
-#endif
 }
 
 // One claim by the leader thread: check the flag first, then fetch-and-add
