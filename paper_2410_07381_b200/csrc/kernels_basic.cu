@@ -8,6 +8,8 @@
 //               one logical block = elems_per_block contiguous floats
 //   rowsum_f32  out[r] = sum_c in[r, c], one warp per row, fixed reduction
 //               order (bit-identical across shapes)
+#include <cuda_bf16.h>
+
 #include <algorithm>
 #include <cstdio>
 
@@ -160,6 +162,110 @@ static int bind_rowsum_f32(const tally_kernel_args* a, Instance* inst) {
   return TALLY_OK;
 }
 
+// ---------------------------------------------------------------- ewise
+// Generic elementwise op over contiguous fp32 / bf16 tensors -- the
+// transformable kind the generic PyTorch routing (intercept.py) maps
+// aten.add / mul / relu / gelu / silu onto.  fp32 arithmetic, one rounding
+// to the output type (PyTorch's bf16 elementwise semantics); 16 B vectors,
+// 8 per thread: a logical block is 32 KB of each operand stream.
+struct Ewise {
+  static constexpr int kThreads = 256;
+  static constexpr int kVec = 8;
+  enum Op { kAdd = 0, kMul = 1, kRelu = 2, kGeluErf = 3, kGeluTanh = 4, kSilu = 5 };
+  struct Params {
+    const uint4* a;
+    const uint4* b;   // null for unary ops
+    uint4* out;
+    long long nvec;   // 16 B vectors
+    int op;
+    int bf16;         // 1: bf16 elements (8 per vector), 0: fp32 (4 per vector)
+    float alpha;      // add: a + alpha * b
+  };
+  static __device__ __forceinline__ float apply(int op, float x, float y, float alpha) {
+    switch (op) {
+      case kAdd: return x + alpha * y;
+      case kMul: return x * y;
+      case kRelu: return x > 0.f ? x : 0.f;
+      case kGeluErf: return 0.5f * x * (1.f + erff(x * 0.70710678118654752f));
+      case kGeluTanh: {
+        const float u = 0.79788456080286536f * (x + 0.044715f * x * x * x);
+        return 0.5f * x * (1.f + tanhf(u));
+      }
+      default: return x / (1.f + expf(-x));
+    }
+  }
+  static __device__ __forceinline__ uint4 vapply(const Params& p, uint4 va, uint4 vb) {
+    uint4 r;
+    if (p.bf16) {
+      const __nv_bfloat162* xa = reinterpret_cast<const __nv_bfloat162*>(&va);
+      const __nv_bfloat162* xb = reinterpret_cast<const __nv_bfloat162*>(&vb);
+      __nv_bfloat162* o = reinterpret_cast<__nv_bfloat162*>(&r);
+#pragma unroll
+      for (int i = 0; i < 4; ++i) {
+        const float2 fa = __bfloat1622float2(xa[i]), fb = __bfloat1622float2(xb[i]);
+        o[i] = __floats2bfloat162_rn(apply(p.op, fa.x, fb.x, p.alpha), apply(p.op, fa.y, fb.y, p.alpha));
+      }
+    } else {
+      const float* xa = reinterpret_cast<const float*>(&va);
+      const float* xb = reinterpret_cast<const float*>(&vb);
+      float* o = reinterpret_cast<float*>(&r);
+#pragma unroll
+      for (int i = 0; i < 4; ++i) o[i] = apply(p.op, xa[i], xb[i], p.alpha);
+    }
+    return r;
+  }
+  static __device__ __forceinline__ void run(const Params& p, uint3 bidx, uint3, char*) {
+    const long long base = (long long)bidx.x * (kThreads * kVec) + threadIdx.x;
+    uint4 va[kVec], vb[kVec];
+#pragma unroll
+    for (int j = 0; j < kVec; ++j) {
+      const long long k = base + (long long)j * kThreads;
+      if (k < p.nvec) {
+        va[j] = *reinterpret_cast<const uint4*>(reinterpret_cast<const float4*>(p.a) + k);
+        vb[j] = p.b ? p.b[k] : make_uint4(0, 0, 0, 0);
+      }
+    }
+#pragma unroll
+    for (int j = 0; j < kVec; ++j) {
+      const long long k = base + (long long)j * kThreads;
+      if (k < p.nvec) p.out[k] = vapply(p, va[j], vb[j]);
+    }
+  }
+};
+
+static int bind_ewise(const tally_kernel_args* a, Instance* inst) {
+  Ewise::Params p{};
+  p.a = static_cast<const uint4*>(a->ptr[0]);
+  p.b = static_cast<const uint4*>(a->ptr[1]);
+  p.out = static_cast<uint4*>(a->ptr[2]);
+  const long long n = a->i[0];
+  p.op = (int)a->i[1];
+  p.bf16 = a->i[2] ? 1 : 0;
+  p.alpha = a->f[0];
+  const int per = p.bf16 ? 8 : 4;
+  if (!p.a || !p.out || n < per || n % per || p.op < 0 || p.op > Ewise::kSilu ||
+      ((p.op == Ewise::kAdd || p.op == Ewise::kMul) && !p.b)) {
+    set_error("ewise: need a, out (and b for add / mul), n a multiple of %d, op in [0, 5]", per);
+    return TALLY_EINVAL;
+  }
+  for (int k = 0; k < 3; ++k)
+    if (reinterpret_cast<uintptr_t>(a->ptr[k]) % 16) {
+      set_error("ewise: pointers must be 16-byte aligned");
+      return TALLY_EINVAL;
+    }
+  p.nvec = n / per;
+  const long long per_block = (long long)Ewise::kThreads * Ewise::kVec;
+  const long long blocks = (p.nvec + per_block - 1) / per_block;
+  if (blocks > 0x7fffffffLL) { set_error("ewise: grid too large"); return TALLY_EINVAL; }
+  memcpy(inst->params, &p, sizeof(p));
+  inst->grid = make_uint3((unsigned)blocks, 1, 1);
+  inst->threads = Ewise::kThreads;
+  inst->smem = 0;
+  inst->alg_bytes = 16.0 * (double)p.nvec * (p.b ? 3.0 : 2.0);
+  inst->alg_flops = (double)n;
+  return TALLY_OK;
+}
+
 // ---------------------------------------------------------------- spin
 // A cost-model kernel: every logical block occupies its CTA slot for exactly
 // block_ns of device time.  It runs the reference's abstract workloads
@@ -239,12 +345,13 @@ static KernelKind make_kind(const char* name, int (*bind)(const tally_kernel_arg
 }
 
 int register_basic_kernels(KernelKind* out, int cap) {
-  if (cap < 4) return 0;
+  if (cap < 5) return 0;
   out[0] = make_kind<VecAddI64>("vecadd_i64", bind_vecadd_i64);
   out[1] = make_kind<VecAddF32>("vecadd_f32", bind_vecadd_f32);
   out[2] = make_kind<RowSumF32>("rowsum_f32", bind_rowsum_f32);
   out[3] = make_kind<SpinKernel>("spin", bind_spin);
-  return 4;
+  out[4] = make_kind<Ewise>("ewise", bind_ewise);
+  return 5;
 }
 
 }  // namespace tally

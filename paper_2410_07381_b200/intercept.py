@@ -15,7 +15,9 @@ this module derives one from an unmodified PyTorch step function:
    bf16 with a supported operand layout (A K-major or MN-major, B K-major or
    MN-major, not A MN-major with B K-major) and N, K multiples of 64, and
    ``aten.bmm`` on contiguous batches.  ``addmm``'s bias is added by the next
-   exempt segment.
+   exempt segment.  Elementwise ``add`` / ``mul`` / ``relu`` / ``gelu`` /
+   ``silu`` (and their in-place forms) on same-shape contiguous fp32 / bf16
+   tensors become the transformable ``ewise`` kind.
 3. Every maximal run of other ops (elementwise, normalisation, softmax,
    reductions, optimizer foreach ops, copies) is captured into one CUDA graph
    that re-executes them on the recorded tensors (results copied into the
@@ -43,6 +45,14 @@ from .scheduler import KernelWork
 
 aten = torch.ops.aten
 _GEMM_OPS = {aten.mm.default, aten.addmm.default, aten.bmm.default}
+# elementwise ops -> the transformable `ewise` kind: (op, binary, in-place)
+_EWISE_OPS = {
+    aten.add.Tensor: ("add", True, False), aten.add_.Tensor: ("add", True, True),
+    aten.mul.Tensor: ("mul", True, False), aten.mul_.Tensor: ("mul", True, True),
+    aten.relu.default: ("relu", False, False), aten.relu_.default: ("relu", False, True),
+    aten.silu.default: ("silu", False, False), aten.silu_.default: ("silu", False, True),
+    aten.gelu.default: ("gelu", False, False),
+}
 
 
 class _Record:
@@ -127,6 +137,33 @@ def _gemm_kernel(rec):
     return kernels.gemm_ex(A, B, out, M, N, K, a_mn=a_mn, b_mn=b_mn)
 
 
+def _ewise_kernel(rec):
+    """The transformable kernel for a recorded elementwise op on same-shape
+    contiguous fp32 / bf16 tensors (no broadcasting, no type promotion), or None."""
+    op, binary, inplace = _EWISE_OPS[rec.func]
+    args = [t.detach() if isinstance(t, torch.Tensor) else t for t in rec.args]
+    x = args[0]
+    out = rec.out.detach() if isinstance(rec.out, torch.Tensor) else None
+    if out is None or not isinstance(x, torch.Tensor) or x.dtype not in (torch.float32, torch.bfloat16):
+        return None
+    y = args[1] if binary and len(args) > 1 else None
+    if binary and not (isinstance(y, torch.Tensor) and y.shape == x.shape and y.dtype == x.dtype
+                       and y.is_contiguous()):
+        return None
+    alpha = float(rec.kwargs.get("alpha", 1.0))
+    if op == "gelu":
+        approx = rec.kwargs.get("approximate", args[1] if len(args) > 1 else "none")
+        op = "gelu_tanh" if approx == "tanh" else "gelu"
+    per = 8 if x.dtype == torch.bfloat16 else 4
+    tensors = [x, out] + ([y] if y is not None else [])
+    if (out.shape != x.shape or out.dtype != x.dtype or not x.is_contiguous() or not out.is_contiguous()
+            or x.numel() % per or any(t.data_ptr() % 16 for t in tensors)):
+        return None
+    if inplace and out.data_ptr() != x.data_ptr():
+        return None
+    return kernels.ewise(op, x, y, out, alpha)
+
+
 class Program:
     """A captured step: ``items`` in order, each ("gemm", DeviceKernel, record)
     or ("graph", DeviceKernel, records).  ``works(prefix)`` -> KernelWorks."""
@@ -138,7 +175,7 @@ class Program:
     def works(self, prefix="step"):
         out = []
         for i, (what, dk, _r) in enumerate(self.items):
-            if what == "gemm":
+            if what != "graph":
                 kid = f"{prefix}.{i}:{dk.kind}:{dk.info.grid}"
                 out.append(KernelWork(kid, dk.cost(), kernel=dk))
             else:
@@ -148,6 +185,10 @@ class Program:
     @property
     def n_gemm(self):
         return sum(1 for w, _d, _r in self.items if w == "gemm")
+
+    @property
+    def n_ewise(self):
+        return sum(1 for w, _d, _r in self.items if w == "ewise")
 
     def run_original(self, stream):
         """The program once, every step untransformed, in order."""
@@ -211,12 +252,13 @@ def _build(rec) -> Program:
         segment.clear()
 
     for r in records:
-        dk = _gemm_kernel(r) if r.func in _GEMM_OPS else None
+        dk = _gemm_kernel(r) if r.func in _GEMM_OPS else \
+            _ewise_kernel(r) if r.func in _EWISE_OPS else None
         if dk is None:
             segment.append(r)
             continue
         flush()
-        items.append(("gemm", dk, r))
+        items.append(("gemm" if r.func in _GEMM_OPS else "ewise", dk, r))
         if r.func is aten.addmm.default:
             segment.append(_bias_add(r))
     flush()

@@ -317,6 +317,19 @@ def cuda_graph(graph) -> DeviceKernel:
     return DeviceKernel("cuda_graph", (int(exec_handle),), (), keep=(graph,))
 
 
+EWISE_OPS = {"add": 0, "mul": 1, "relu": 2, "gelu": 3, "gelu_tanh": 4, "silu": 5}
+
+
+def ewise(op: str, a, b, out, alpha: float = 1.0) -> DeviceKernel:
+    """out = op(a[, b]) elementwise over contiguous fp32 or bf16 tensors of the
+    same shape (``add``: a + alpha * b; ``mul``; unary ``relu``, ``gelu``
+    (erf), ``gelu_tanh``, ``silu``): fp32 arithmetic, one rounding to the
+    output type.  ``out`` may alias ``a`` (in-place ops)."""
+    import torch
+    bf16 = a.dtype == torch.bfloat16
+    return DeviceKernel("ewise", (a, b, out), (a.numel(), EWISE_OPS[op], int(bf16)), (alpha,))
+
+
 def spin(total_blocks: int, threads_per_block: int, block_duration_ns: int) -> DeviceKernel:
     """A cost-model kernel (ref ``KernelCostModel``): ``total_blocks`` logical
     blocks of ``threads_per_block`` threads, each holding its slot for
