@@ -108,3 +108,52 @@ def test_captured_step_under_tally_with_preemption(env):
     torch.cuda.synchronize()
     for i, (a, b) in enumerate(zip(after_tally, state)):
         assert torch.equal(a, b), (i, n)
+
+
+@pytest.mark.parametrize("dtype", ["float32", "bfloat16"])
+def test_ewise_kind_matches_torch_in_every_shape(env, dtype):
+    """The transformable elementwise kind against PyTorch's own op on the
+    same inputs (fp32 arithmetic, one rounding): add / mul / relu exactly,
+    gelu / silu within 2 ulp of the output type; Original, Sliced and PTB
+    bit-identical to each other."""
+    P, _x, _y = env
+    from paper_2410_07381_b200 import kernels
+    dt = getattr(torch, dtype)
+    g = torch.Generator(device="cuda").manual_seed(5)
+    n = (1 << 20) + 64
+    a = torch.randn(n, device="cuda", generator=g).to(dt)
+    b = torch.randn(n, device="cuda", generator=g).to(dt)
+    s = kernels.Stream(high_priority=False)
+    F = torch.nn.functional
+    refs = {"add": a + 0.5 * b, "mul": a * b, "relu": F.relu(a), "gelu": F.gelu(a),
+            "gelu_tanh": F.gelu(a, approximate="tanh"), "silu": F.silu(a)}
+    refs["add"] = torch.add(a, b, alpha=0.5)
+    for op, ref in refs.items():
+        outs = []
+        for shape in ("original", "sliced", "ptb"):
+            out = torch.empty_like(a)
+            dk = kernels.ewise(op, a, b if op in ("add", "mul") else None, out, alpha=0.5)
+            if shape == "original":
+                dk.original(s).wait()
+            elif shape == "sliced":
+                for off, cnt in P.slice_plan(dk.total_blocks, 0.25):
+                    dk.sliced(s, off, cnt).wait()
+            else:
+                dk.ptb(s, 148).wait()
+            outs.append(out)
+        assert torch.equal(outs[0], outs[1]) and torch.equal(outs[0], outs[2]), op
+        if op in ("add", "mul", "relu"):
+            assert torch.equal(outs[0], ref), (op, dtype)
+        else:
+            ulp = 2 * (2.0 ** -7 if dt == torch.bfloat16 else 2.0 ** -23)
+            err = ((outs[0].float() - ref.float()).abs() / ref.float().abs().clamp_min(1e-3)).max().item()
+            assert err <= ulp, (op, dtype, err)
+
+
+def test_capture_routes_elementwise_ops(env):
+    P, x, y = env
+    from paper_2410_07381_b200 import intercept
+    m, opt = _model(5)
+    _step(m, opt, x, y)
+    prog = intercept.capture(_step, m, opt, x, y)
+    assert prog.n_ewise >= 1 and prog.n_gemm >= 5
