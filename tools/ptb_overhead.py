@@ -48,6 +48,7 @@ def main():
     ap.add_argument("--config", default="c4", choices=["c2", "c3", "c4"])
     ap.add_argument("--reps", type=int, default=3)
     ap.add_argument("--out", default=None)
+    ap.add_argument("--chosen", action="store_true", help="also time the tuner's chosen shape of every kernel")
     args = ap.parse_args()
     P.B200Device.get(0)
     s = kernels.Stream(high_priority=False)
@@ -69,12 +70,43 @@ def main():
             ptb[dk.kind] += L.elapsed_ns / 1e3 / args.reps
     for name, dk in tr.program:
         n[dk.kind] += 1
+    chosen = collections.defaultdict(float)
+    if args.chosen:
+        # the shapes the profile-guided tuner picks at the 31.6 us threshold
+        from fractions import Fraction
+        prof = P.Profiler(P.B200Device.get(0).spec, runs=3)
+        for _ in range(args.reps):
+            for name, dk in tr.program:
+                sig = tr.work_signature(name, dk)
+                prof.bind(sig, dk)
+                w = P.KernelWork(sig, dk.cost(), kernel=dk)
+                c = prof.select(w.profile_key(), w.cost, 31_600)
+                if c.variant == "Ptb":
+                    L = dk.ptb(s, c.worker_count, timed=True)
+                    L.wait()
+                    us = L.elapsed_ns / 1e3
+                elif c.variant == "Sliced":
+                    us = 0.0
+                    for off, cnt in P.slice_plan(dk.total_blocks, Fraction(c.fraction)):
+                        L = dk.sliced(s, off, cnt, timed=True)
+                        L.wait()
+                        us += L.elapsed_ns / 1e3
+                else:
+                    L = dk.original(s, timed=True)
+                    L.wait()
+                    us = L.elapsed_ns / 1e3
+                chosen[dk.kind] += us / args.reps
     tot_o, tot_p = sum(orig.values()), sum(ptb.values())
     out = {"config": args.config, "kernels": len(tr.program), "step_us_original": tot_o, "step_us_ptb": tot_p,
            "ptb_vs_original_speed": tot_o / tot_p,
            "by_kind": {k: {"n": n[k], "original_us": round(orig[k], 1), "ptb_us": round(ptb[k], 1),
-                           "speed_ratio": round(orig[k] / ptb[k], 3)}
+                           "speed_ratio": round(orig[k] / ptb[k], 3),
+                           **({"chosen_us": round(chosen[k], 1), "chosen_speed_ratio": round(orig[k] / chosen[k], 3)}
+                              if chosen else {})}
                        for k in sorted(orig, key=lambda k: -orig[k])}}
+    if chosen:
+        out["step_us_chosen"] = sum(chosen.values())
+        out["chosen_vs_original_speed"] = tot_o / sum(chosen.values())
     txt = json.dumps(out, indent=1)
     print(txt)
     if args.out:
