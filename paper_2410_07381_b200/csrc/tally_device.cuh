@@ -335,6 +335,12 @@ __device__ __forceinline__ void ptb_worker_exit(const PtbArgs& a, bool stopped,
     claims = 0ull;
   }
   const unsigned long long progress = a.start + claims;
+#ifdef TALLY_EXPERIMENT_NO_MIRROR   // timing experiment only (tools/ptb_publish_cost.py): no host writes
+  r->claims = 0ull; r->exited = 0u; r->neg_first_stop = 0ull; r->executed = 0ull; r->stops = 0ull;
+  r->neg_first_start = 0ull;
+  if (progress == ~0ull) r->pad[0] = nfs + nst + stops + now + pending;
+  return;
+#endif
   volatile LaunchMirror* m = a.mirror;
   m->claims = claims;
   m->t_first_stop = nfs ? ~nfs : 0ull;
