@@ -141,6 +141,8 @@ typedef struct {
   double alg_flops;         /* algorithmic flops of one full launch              */
   int preempt_units;        /* PTB preemption points per logical block (>1: chunk-granular
                                preemption with saved partial state, e.g. sgemm_tf32x3) */
+  int cluster;              /* CTAs per logical block (CTA-pair GEMMs "*_x2": 2, launched as
+                               clusters; PTB worker counts must be a multiple); else 1 */
 } tally_kernel_info;
 
 int tally_kernel_kind_count(void);

@@ -66,7 +66,7 @@ class c_kernel_info(C.Structure):
                 ("total_blocks", C.c_longlong), ("threads_per_block", C.c_int),
                 ("smem_bytes", C.c_longlong), ("occupancy_ptb", C.c_int),
                 ("occupancy_original", C.c_int), ("alg_bytes", C.c_double),
-                ("alg_flops", C.c_double), ("preempt_units", C.c_int)]
+                ("alg_flops", C.c_double), ("preempt_units", C.c_int), ("cluster", C.c_int)]
 
 
 class c_launch_desc(C.Structure):

@@ -97,6 +97,65 @@ __device__ __forceinline__ void st_out16(void* p, uint4 v) {
                :: "l"(p), "r"(v.x), "r"(v.y), "r"(v.z), "r"(v.w), "l"(pol) : "memory");
 }
 
+// ---- CTA pair (cta_group::2) helpers -------------------------------------
+__device__ __forceinline__ unsigned cluster_rank() {
+  unsigned r;
+  asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(r));
+  return r;
+}
+__device__ __forceinline__ void cluster_sync_all() {
+  asm volatile("barrier.cluster.arrive.release.aligned;\nbarrier.cluster.wait.acquire.aligned;" ::: "memory");
+}
+// shared::cluster address of the same variable in CTA `rank` of the cluster
+__device__ __forceinline__ uint32_t map_rank(const void* p, unsigned rank) {
+  uint32_t r;
+  asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(r) : "r"(smem_u32(p)), "r"(rank));
+  return r;
+}
+__device__ __forceinline__ void mbar_arrive_remote(uint32_t cluster_addr) {
+  asm volatile("mbarrier.arrive.release.cluster.shared::cluster.b64 _, [%0];" ::"r"(cluster_addr) : "memory");
+}
+__device__ __forceinline__ void mbar_wait_cluster(uint64_t* bar, uint32_t parity) {
+  asm volatile(
+      "{\n"
+      ".reg .pred p;\n"
+      "WAITC_%=:\n"
+      "mbarrier.try_wait.parity.acquire.cluster.shared::cta.b64 p, [%0], %1;\n"
+      "@!p bra WAITC_%=;\n"
+      "}\n" ::"r"(smem_u32(bar)),
+      "r"(parity)
+      : "memory");
+}
+__device__ __forceinline__ void st_cluster_s64(uint32_t cluster_addr, long long v) {
+  asm volatile("st.shared::cluster.s64 [%0], %1;" ::"r"(cluster_addr), "l"(v) : "memory");
+}
+// Pair TMA load: both CTAs load their half into their own shared memory and
+// signal the leader CTA's full barrier (`lead_bar`: its shared::cluster
+// address), which expects both halves' bytes.
+__device__ __forceinline__ void tma_load_2d_pair(void* dst, const CUtensorMap* map, uint32_t lead_bar, int x, int y) {
+  uint64_t pol;
+  asm("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(pol));
+  asm volatile(
+      "cp.async.bulk.tensor.2d.cta_group::2.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint"
+      " [%0], [%1, {%3, %4}], [%2], %5;" ::"r"(smem_u32(dst)),
+      "l"(map), "r"(lead_bar), "r"(x), "r"(y), "l"(pol)
+      : "memory");
+}
+__device__ __forceinline__ void umma_commit_pair(uint64_t* bar) {
+  // arrives on the barrier at this offset in both CTAs of the pair
+  asm volatile(
+      "{\n.reg .b16 m;\nmov.b16 m, 3;\n"
+      "tcgen05.commit.cta_group::2.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 [%0], m;\n}\n" ::"r"(
+          smem_u32(bar))
+      : "memory");
+}
+__device__ __forceinline__ void umma_pair(uint32_t tmem_d, uint64_t a, uint64_t b, uint32_t idesc, uint32_t acc) {
+  asm volatile(
+      "{\n.reg .pred p;\nsetp.ne.b32 p, %4, 0;\n"
+      "tcgen05.mma.cta_group::2.kind::f16 [%0], %1, %2, %3, p;\n}\n" ::"r"(tmem_d),
+      "l"(a), "l"(b), "r"(idesc), "r"(acc));
+}
+
 __device__ __forceinline__ void fence_after() { asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory"); }
 __device__ __forceinline__ void fence_before() { asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory"); }
 
@@ -146,8 +205,9 @@ __device__ __forceinline__ uint64_t smem_desc_mn(const void* p) {
   return d;
 }
 
-// Instruction descriptor: D fp32, A and B K-major (or both MN-major), M = 128, N = BN.
-template <int KIND, int BN, bool A_MN = false, bool B_MN = false>
+// Instruction descriptor: D fp32, A and B K-major (or both MN-major), M = 128
+// (256 for a CTA pair), N = BN.
+template <int KIND, int BN, bool A_MN = false, bool B_MN = false, int MMA_M = 128>
 __host__ __device__ constexpr uint32_t make_idesc() {
   return (1u << 4)                                  // D format: F32
          | ((KIND == 0 ? 2u : 1u) << 7)             // A format: TF32 / BF16
@@ -155,7 +215,7 @@ __host__ __device__ constexpr uint32_t make_idesc() {
          | ((A_MN ? 1u : 0u) << 15)                 // A major: MN
          | ((B_MN ? 1u : 0u) << 16)                 // B major: MN
          | ((uint32_t)(BN >> 3) << 17)              // N >> 3
-         | ((uint32_t)(128 >> 4) << 24);            // M >> 4
+         | ((uint32_t)(MMA_M >> 4) << 24);          // M >> 4
 }
 
 __device__ __forceinline__ void tmem_st32(uint32_t taddr, const uint32_t (&r)[32]) {
@@ -231,26 +291,36 @@ using CfgTf32x3N64 = CfgTf32x3T<64, 4>;
 #ifndef TALLY_STAGES_F32_N64
 #define TALLY_STAGES_F32_N64 4
 #endif
-template <int BN_, class OutT_, bool A_MN_ = false, bool B_MN_ = false>
+// PAIR = 2: a CTA pair (cluster of two SMs, cta_group::2) computes one
+// 256 x BN tile with M = 256 MMAs -- each CTA loads its 128 rows of A and
+// BN / 2 rows of B, the leader's elected thread issues for both, each CTA's
+// TMEM holds its 128 rows; per SM half the operand bytes of a 128-row tile.
+#ifndef TALLY_STAGES_PAIR
+#define TALLY_STAGES_PAIR 6
+#endif
+template <int BN_, class OutT_, bool A_MN_ = false, bool B_MN_ = false, int PAIR_ = 1>
 struct CfgBf16T {
   static constexpr int KIND = 1;
-  static constexpr int BM = 128, BN = BN_;
+  static constexpr int PAIR = PAIR_;
+  static constexpr int BM = 128, BN = BN_;            // BM: rows per CTA; BN: MMA N (the pair's tile width)
+  static constexpr int B_ROWS = BN / PAIR;            // B rows (N) this CTA loads
   static constexpr int BK = 64;                       // bf16 elements = 128 B
   static constexpr int ESZ = 2;
   static constexpr int NOPS = 2;
   static constexpr int A_BYTES = BM * BK * ESZ;       // 16 KB
-  static constexpr int B_BYTES = BN * BK * ESZ;       // 16 / 8 KB
+  static constexpr int B_BYTES = B_ROWS * BK * ESZ;   // 16 / 8 KB
   static constexpr int STAGE_BYTES = A_BYTES + B_BYTES;
   // 64-96 KB of operand ring (+ bf16 staging): two CTAs per SM, so an
   // untransformed launch (one output tile per CTA) overlaps one CTA's
   // prologue / pipeline fill with the other's tile, and high-priority CTAs
-  // find room next to a best-effort one
-  static constexpr int STAGES = BN == 128 ? (sizeof(OutT_) == 2 ? TALLY_STAGES_BF16_N128 : TALLY_STAGES_F32_N128)
+  // find room next to a best-effort one.  Pairs: one CTA per SM, a deep ring.
+  static constexpr int STAGES = PAIR == 2 ? (sizeof(OutT_) == 2 ? TALLY_STAGES_PAIR : TALLY_STAGES_PAIR + 1)
+                              : BN == 128 ? (sizeof(OutT_) == 2 ? TALLY_STAGES_BF16_N128 : TALLY_STAGES_F32_N128)
                                           : (sizeof(OutT_) == 2 ? TALLY_STAGES_BF16_N64 : TALLY_STAGES_F32_N64);
   static constexpr int UMMA_K = 16;
   // the whole (split) K range accumulates in one TMEM buffer (no fp32
   // promotion chunks at the 1e-2 bf16 budget): 2 x BN columns, leaving TMEM
-  // for co-resident high-priority tensor-core kernels
+  // for co-resident high-priority tensor-core kernels (pairs: all 512)
   static constexpr int TMEM_COLS = 2 * BN;
   // MN-major operands: A given as A^T [K, M] and/or B as B^T [K, N] (M / N
   // contiguous) -- the weight gradient dW = dY^T . X reads both activations
@@ -273,6 +343,16 @@ using CfgBf16F32KMN = CfgBf16T<128, float, false, true>;
 using CfgBf16F32KMNN64 = CfgBf16T<64, float, false, true>;
 using CfgBf16MNb = CfgBf16T<128, __nv_bfloat16, true, true>;
 using CfgBf16MNbN64 = CfgBf16T<64, __nv_bfloat16, true, true>;
+// CTA-pair kinds (256 x 256 tiles)
+using CfgBf16X2 = CfgBf16T<256, __nv_bfloat16, false, false, 2>;
+using CfgBf16F32X2 = CfgBf16T<256, float, false, false, 2>;
+using CfgBf16MNX2 = CfgBf16T<256, float, true, true, 2>;
+using CfgBf16KMNX2 = CfgBf16T<256, __nv_bfloat16, false, true, 2>;
+using CfgBf16F32KMNX2 = CfgBf16T<256, float, false, true, 2>;
+template <class Cfg, class = void>
+struct PairOf { static constexpr int value = 1; };
+template <class Cfg>
+struct PairOf<Cfg, void_t_<decltype(Cfg::PAIR)>> { static constexpr int value = Cfg::PAIR; };
 
 constexpr int GROUP_M = 8;
 // producer warp, MMA warp, 8 epilogue warps: two per TMEM lane quarter, each
@@ -286,7 +366,7 @@ constexpr int kSlots = 4;
 template <class Cfg>
 constexpr size_t smem_bytes() {
   return 1024 /*alignment slack*/ + (size_t)Cfg::STAGES * Cfg::STAGE_BYTES + Cfg::EPI_BYTES +
-         512 /*barriers + ring*/;
+         640 /*barriers + rings*/;
 }
 
 struct alignas(64) GemmParams {
@@ -363,8 +443,17 @@ __device__ __forceinline__ int goff(const GemmParams& p, int which, const TileWo
   return (int)(p.off[which][0] * w.zb + p.off[which][1] * w.zh);
 }
 
+// An epilogue warp hands a drained TMEM accumulator back to the MMA issuer
+// (pair: to the leader CTA's barrier, which counts both CTAs' warps).
+template <int PR>
+__device__ __forceinline__ void release_acc(uint64_t* bar) {
+  if constexpr (PR == 2) mbar_arrive_remote(map_rank(bar, 0));
+  else mbar_arrive(bar);
+}
+
 template <class Cfg, int MODE, class ShapeArgs>
-__global__ void __launch_bounds__(kThreads, Cfg::KIND == 1 ? 2 : 1) k_gemm(const __grid_constant__ GemmParams p, const ShapeArgs s) {
+__global__ void __launch_bounds__(kThreads, (Cfg::KIND == 1 && PairOf<Cfg>::value == 1) ? 2 : 1)
+k_gemm(const __grid_constant__ GemmParams p, const ShapeArgs s) {
   extern __shared__ __align__(1024) unsigned char smem_raw[];
   unsigned char* smem = reinterpret_cast<unsigned char*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   unsigned char* epi_smem = smem + (size_t)Cfg::STAGES * Cfg::STAGE_BYTES;
@@ -379,7 +468,16 @@ __global__ void __launch_bounds__(kThreads, Cfg::KIND == 1 ? 2 : 1) k_gemm(const
   int* tile_cut = tile_c0 + kSlots;                                           // chunk the tile stops before
   uint32_t* tmem_base_slot = reinterpret_cast<uint32_t*>(tile_cut + kSlots);
   TileWork* tile_w = reinterpret_cast<TileWork*>(tmem_base_slot + 4);          // [kSlots], producer-computed
+  // CTA pair: the leader's producer forwards every tile it takes to the peer's
+  // producer through pair_slot (peer smem) + pair_full (peer) / pair_empty (leader)
+  uint64_t* pair_full = reinterpret_cast<uint64_t*>(tile_w + kSlots);          // [kSlots]
+  uint64_t* pair_empty = pair_full + kSlots;                                  // [kSlots]
+  long long* pair_slot = reinterpret_cast<long long*>(pair_empty + kSlots);   // [kSlots]
 
+  constexpr int PR = PairOf<Cfg>::value;
+  constexpr int BROWS = Cfg::BN / PR;   // rows of B this CTA loads
+  const unsigned rank = PR == 2 ? cluster_rank() : 0u;
+  const bool lead = rank == 0;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int KB = (p.k + Cfg::BK - 1) / Cfg::BK;
 
@@ -389,21 +487,31 @@ __global__ void __launch_bounds__(kThreads, Cfg::KIND == 1 ? 2 : 1) k_gemm(const
     for (int i = 0; i < Cfg::STAGES; ++i) { mbar_init(&full[i], 1); mbar_init(&empty[i], 1); }
     for (int i = 0; i < 2; ++i) {
       mbar_init(&tmem_full[i], 1);
-      mbar_init(&tmem_empty[i], (Cfg::KIND == 1 && Cfg::BN == 64) ? kEpiWarps / 2 : kEpiWarps);   // one group per tile
+      // (pair: the leader's barrier counts both CTAs' epilogue warps)
+      mbar_init(&tmem_empty[i], (Cfg::KIND == 1 && Cfg::BN == 64) ? kEpiWarps / 2 : kEpiWarps * PR);   // one group per tile
     }
     for (int i = 0; i < kSlots; ++i) {
       mbar_init(&tile_full[i], 1);
-      mbar_init(&tile_empty[i], kEpiWarps + 1);
+      mbar_init(&tile_empty[i], kEpiWarps + (lead ? 1 : 0));   // (the peer has no MMA issuer)
+      mbar_init(&pair_full[i], 1);
+      mbar_init(&pair_empty[i], 1);
     }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
   if (warp == 1) {
-    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(tmem_base_slot)),
-                 "n"(Cfg::TMEM_COLS));
-    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+    if constexpr (PR == 2) {
+      asm volatile("tcgen05.alloc.cta_group::2.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(tmem_base_slot)),
+                   "n"(Cfg::TMEM_COLS));
+      asm volatile("tcgen05.relinquish_alloc_permit.cta_group::2.sync.aligned;");
+    } else {
+      asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(tmem_base_slot)),
+                   "n"(Cfg::TMEM_COLS));
+      asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+    }
   }
   fence_before();
-  __syncthreads();
+  if constexpr (PR == 2) cluster_sync_all();   // both CTAs' barriers initialised before any remote arrive
+  else __syncthreads();
   fence_after();
   const uint32_t tmem_base = *tmem_base_slot;
   bool stopped = false;
@@ -431,7 +539,14 @@ __global__ void __launch_bounds__(kThreads, Cfg::KIND == 1 ? 2 : 1) k_gemm(const
       for (int i = 0;; ++i) {
         long long t = -1;
         int c0 = 0;
-        if constexpr (MODE == kPtb) {
+        if (MODE == kPtb && PR == 2 && !lead) {
+          // the peer takes the leader's tiles (-2: the leader was stopped by the flag)
+          const int jj = i % kSlots;
+          mbar_wait_cluster(&pair_full[jj], (i / kSlots) & 1);
+          t = *reinterpret_cast<volatile long long*>(&pair_slot[jj]);
+          mbar_arrive_remote(map_rank(&pair_empty[jj], 0));
+          if (t == -2) { stopped = true; t = -1; }
+        } else if constexpr (MODE == kPtb) {
           bool popped = false;
           if (kChunkPreempt && p.resume != nullptr) {
             // resume a tile a preempted worker left half-done
@@ -470,13 +585,22 @@ __global__ void __launch_bounds__(kThreads, Cfg::KIND == 1 ? 2 : 1) k_gemm(const
           }
         } else {
           if (i == 0) {
-            const long long b = MODE == kOriginal ? (long long)blockIdx.x
-                : (s.linear ? (long long)(s.linear_offset + blockIdx.x) : (long long)(s.offset.x + blockIdx.x));
-            if (s.exec_count != nullptr) atomicAdd(&s.exec_count[b], 1ull);
+            const unsigned bx = blockIdx.x / PR;   // pair: one logical block per cluster
+            const long long b = MODE == kOriginal ? (long long)bx
+                : (s.linear ? (long long)(s.linear_offset + bx) : (long long)(s.offset.x + bx));
+            if (s.exec_count != nullptr && lead) atomicAdd(&s.exec_count[b], 1ull);
             q_next = b * p.tpb;
             q_end = min((long long)p.total_tiles, q_next + p.tpb);
           }
           if (q_next < q_end) t = q_next++;
+        }
+        if constexpr (MODE == kPtb && PR == 2) {
+          if (lead) {   // forward to the peer's producer
+            const int jj = i % kSlots;
+            if (i >= kSlots) mbar_wait_cluster(&pair_empty[jj], ((i / kSlots) - 1) & 1);
+            st_cluster_s64(map_rank(&pair_slot[jj], 1), (t < 0 && stopped) ? -2ll : t);
+            mbar_arrive_remote(map_rank(&pair_full[jj], 1));
+          }
         }
         const int j = i % kSlots;
         if (i >= kSlots) mbar_wait(&tile_empty[j], ((i / kSlots) - 1) & 1);
@@ -515,7 +639,8 @@ __global__ void __launch_bounds__(kThreads, Cfg::KIND == 1 ? 2 : 1) k_gemm(const
             }
             if (it >= (uint32_t)Cfg::STAGES) mbar_wait(&empty[st], ((it / Cfg::STAGES) - 1) & 1);
             unsigned char* base = smem + (size_t)st * Cfg::STAGE_BYTES;
-            mbar_expect_tx(&full[st], Cfg::STAGE_BYTES);
+            // pair: the leader's barrier expects both CTAs' halves
+            if (lead) mbar_expect_tx(&full[st], Cfg::STAGE_BYTES * PR);
             const int kx = kb * Cfg::BK;
             if constexpr (Cfg::KIND == 0) {
               tma_load_2d(base, &p.a_hi, &full[st], kx, mb * Cfg::BM);
@@ -525,21 +650,27 @@ __global__ void __launch_bounds__(kThreads, Cfg::KIND == 1 ? 2 : 1) k_gemm(const
             } else {
               // (batched layouts: every operand's origin moves with the batch)
               const int ar = goff(p, 0, w), ac = goff(p, 1, w), br = goff(p, 2, w), bc = goff(p, 3, w);
+              // this CTA's rows of A and of B (pair: rank-th half of each)
+              const int am = (mb * PR + (int)rank) * Cfg::BM, bn0 = nb * Cfg::BN + (int)rank * BROWS;
+              const uint32_t lead_full = PR == 2 ? map_rank(&full[st], 0) : 0u;
+              auto ld = [&](void* dst, const CUtensorMap* map, int x, int y) {
+                if constexpr (PR == 2) tma_load_2d_pair(dst, map, lead_full, x, y);
+                else tma_load_2d(dst, map, &full[st], x, y);
+              };
               if constexpr (Cfg::A_MN) {
                 // boxes of 64 M-elements x BK K-rows, 8 KB each
 #pragma unroll
                 for (int h = 0; h < Cfg::BM / 64; ++h)
-                  tma_load_2d(base + h * 8192, &p.a_hi, &full[st], mb * Cfg::BM + h * 64 + ac, kb * Cfg::BK + ar);
+                  ld(base + h * 8192, &p.a_hi, am + h * 64 + ac, kb * Cfg::BK + ar);
               } else {
-                tma_load_2d(base, &p.a_hi, &full[st], kx + ac, mb * Cfg::BM + ar);
+                ld(base, &p.a_hi, kx + ac, am + ar);
               }
               if constexpr (Cfg::B_MN) {
 #pragma unroll
-                for (int h = 0; h < Cfg::BN / 64; ++h)
-                  tma_load_2d(base + Cfg::A_BYTES + h * 8192, &p.b_hi, &full[st], nb * Cfg::BN + h * 64 + bc,
-                              kb * Cfg::BK + br);
+                for (int h = 0; h < BROWS / 64; ++h)
+                  ld(base + Cfg::A_BYTES + h * 8192, &p.b_hi, bn0 + h * 64 + bc, kb * Cfg::BK + br);
               } else {
-                tma_load_2d(base + Cfg::A_BYTES, &p.b_hi, &full[st], kx + bc, nb * Cfg::BN + br);
+                ld(base + Cfg::A_BYTES, &p.b_hi, kx + bc, bn0 + br);
               }
             }
           }
@@ -548,12 +679,12 @@ __global__ void __launch_bounds__(kThreads, Cfg::KIND == 1 ? 2 : 1) k_gemm(const
     }
     __syncwarp();
   } else if (warp == 1) {
-    if (lane == 0) {
-      // ------------------------------------------------ MMA issuer
+    if (lane == 0 && lead) {
+      // ------------------------------------------------ MMA issuer (pair: the leader, for both CTAs)
       // The tile's K range is cut into chunks of p.kchunk k-blocks; each chunk
       // accumulates into one of two TMEM buffers and is promoted to an fp32
       // running total by the epilogue (bounded tensor-core accumulation chains).
-      constexpr uint32_t idesc = make_idesc<Cfg::KIND, Cfg::BN, Cfg::A_MN, Cfg::B_MN>();
+      constexpr uint32_t idesc = make_idesc<Cfg::KIND, Cfg::BN, Cfg::A_MN, Cfg::B_MN, 128 * PR>();
       uint32_t it = 0, ci = 0;
       for (int i = 0;; ++i) {
         const int j = i % kSlots;
@@ -567,7 +698,11 @@ __global__ void __launch_bounds__(kThreads, Cfg::KIND == 1 ? 2 : 1) k_gemm(const
         const TileWork w = tile_w[j];
         for (int c = c0; c < w.nch; ++c, ++ci) {
           const int acc = ci & 1;
-          if (ci >= 2) mbar_wait(&tmem_empty[acc], ((ci >> 1) - 1) & 1);
+          if (ci >= 2) {
+            // (pair: the peer's epilogue warps arrive from the other CTA)
+            if constexpr (PR == 2) mbar_wait_cluster(&tmem_empty[acc], ((ci >> 1) - 1) & 1);
+            else mbar_wait(&tmem_empty[acc], ((ci >> 1) - 1) & 1);
+          }
           fence_after();
           const uint32_t d = tmem_base + (uint32_t)(acc * Cfg::BN);
           const int kb0 = w.kbeg + c * p.kchunk, kb1 = min(w.kend, kb0 + p.kchunk);
@@ -601,16 +736,20 @@ __global__ void __launch_bounds__(kThreads, Cfg::KIND == 1 ? 2 : 1) k_gemm(const
                 const uint64_t da = Cfg::A_MN ? smem_desc_mn(base + k * 2048) : smem_desc(base + koff);
                 const uint64_t db = Cfg::B_MN ? smem_desc_mn(base + Cfg::A_BYTES + k * 2048)
                                               : smem_desc(base + Cfg::A_BYTES + koff);
-                umma<1>(d, da, db, idesc, first);
+                if constexpr (PR == 2) umma_pair(d, da, db, idesc, first);
+                else umma<1>(d, da, db, idesc, first);
               }
             }
-            umma_commit(&empty[st]);   // frees the stage once these MMAs retire
+            // frees the stage once these MMAs retire (pair: in both CTAs)
+            if constexpr (PR == 2) umma_commit_pair(&empty[st]);
+            else umma_commit(&empty[st]);
           }
           if (cut) {
             ++ci;
             break;
           }
-          umma_commit(&tmem_full[acc]);
+          if constexpr (PR == 2) umma_commit_pair(&tmem_full[acc]);
+          else umma_commit(&tmem_full[acc]);
         }
         mbar_arrive(&tile_empty[j]);
       }
@@ -705,13 +844,15 @@ __global__ void __launch_bounds__(kThreads, Cfg::KIND == 1 ? 2 : 1) k_gemm(const
     }
   } else if (Cfg::KIND == 1 && sizeof(typename Cfg::OutT) == 2 && p.c_tma) {
     // -------------------------------------------------- epilogue (warps 2..9), TMA store
-    // 128-wide bf16 tiles of a plain GEMM: each warp drains its lane quarter
-    // x column half (32 rows x 64 columns), releases the accumulator, stages
-    // the box in its own 4 KB (the 128B-swizzle layout) and one lane issues a
-    // TMA store -- the warp never waits for global writes, only (before the
-    // next tile) for the previous store to finish reading its staging box
+    // 128/256-wide bf16 tiles of a plain GEMM: each warp drains its lane
+    // quarter x column half (32 rows x BN/2 columns) in 64-column boxes,
+    // releases the accumulator after the last one, stages each box in its own
+    // 4 KB (the 128B-swizzle layout) and one lane issues a TMA store -- the
+    // warp never waits for global writes, only (before restaging) for the
+    // previous store to finish reading its staging box
     const int q = warp & 3;
     const int half = (warp - 2) >> 2;
+    constexpr int HALF = Cfg::BN / 2;
     unsigned char* wstage = epi_smem + (size_t)(warp - 2) * 4096;
     const uint32_t wst = smem_u32(wstage);
     uint32_t ci = 0;
@@ -728,32 +869,38 @@ __global__ void __launch_bounds__(kThreads, Cfg::KIND == 1 ? 2 : 1) k_gemm(const
       const int acc = ci & 1;   // one K chunk per tile for the bf16 kinds
       mbar_wait(&tmem_full[acc], (ci >> 1) & 1);
       fence_after();
-      uint32_t r[2][32];
-      const uint32_t lb = tmem_base + ((uint32_t)(q * 32) << 16) + (uint32_t)(acc * Cfg::BN + half * 64);
-      tmem_ld32(lb, r[0]);
-      tmem_ld32(lb + 32, r[1]);
-      fence_before();
-      __syncwarp();
-      if (lane == 0) mbar_arrive(&tmem_empty[acc]);
-      ++ci;
-      if (lane == 0) asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
-      __syncwarp();
-      unsigned char* srow = wstage + (size_t)lane * 128;
-#pragma unroll
-      for (int v = 0; v < 8; ++v) {
-        uint32_t wv[4];
-#pragma unroll
-        for (int e = 0; e < 4; ++e) {
-          const int k = 8 * (v & 3) + 2 * e;
-          __nv_bfloat162 b = __floats2bfloat162_rn(__uint_as_float(r[v >> 2][k]), __uint_as_float(r[v >> 2][k + 1]));
-          wv[e] = *reinterpret_cast<uint32_t*>(&b);
+#pragma unroll 1
+      for (int bx = 0; bx < HALF; bx += 64) {
+        uint32_t r[2][32];
+        const uint32_t lb = tmem_base + ((uint32_t)(q * 32) << 16) + (uint32_t)(acc * Cfg::BN + half * HALF + bx);
+        tmem_ld32(lb, r[0]);
+        tmem_ld32(lb + 32, r[1]);
+        if (bx + 64 >= HALF) {
+          fence_before();
+          __syncwarp();
+          if (lane == 0) release_acc<PR>(&tmem_empty[acc]);
         }
-        *reinterpret_cast<uint4*>(srow + ((v ^ (lane & 7)) << 4)) = make_uint4(wv[0], wv[1], wv[2], wv[3]);
+        if (lane == 0) asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
+        __syncwarp();
+        unsigned char* srow = wstage + (size_t)lane * 128;
+#pragma unroll
+        for (int v = 0; v < 8; ++v) {
+          uint32_t wv[4];
+#pragma unroll
+          for (int e = 0; e < 4; ++e) {
+            const int k = 8 * (v & 3) + 2 * e;
+            __nv_bfloat162 b = __floats2bfloat162_rn(__uint_as_float(r[v >> 2][k]), __uint_as_float(r[v >> 2][k + 1]));
+            wv[e] = *reinterpret_cast<uint32_t*>(&b);
+          }
+          *reinterpret_cast<uint4*>(srow + ((v ^ (lane & 7)) << 4)) = make_uint4(wv[0], wv[1], wv[2], wv[3]);
+        }
+        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+        __syncwarp();
+        if (lane == 0)
+          tma_store_2d(&p.a_lo, wst, w.nb * Cfg::BN + half * HALF + bx, (w.mb * PR + (int)rank) * Cfg::BM + q * 32);
+        __syncwarp();
       }
-      asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-      __syncwarp();
-      if (lane == 0) tma_store_2d(&p.a_lo, wst, w.nb * Cfg::BN + half * 64, w.mb * Cfg::BM + q * 32);
-      __syncwarp();
+      ++ci;
       if (lane == 0) mbar_arrive(&tile_empty[j]);
     }
     if (lane == 0) asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
@@ -775,7 +922,7 @@ __global__ void __launch_bounds__(kThreads, Cfg::KIND == 1 ? 2 : 1) k_gemm(const
         break;
       }
       const TileWork w = tile_w[j];
-      const int row = w.mb * Cfg::BM + q * 32 + lane;
+      const int row = (w.mb * PR + (int)rank) * Cfg::BM + q * 32 + lane;
       const bool row_ok = row < p.m;   // M tail: TMA zero-fills the rows past M, stores skip them
       const int cr = goff(p, 4, w), cc = goff(p, 5, w);
       typename Cfg::OutT* crow = reinterpret_cast<typename Cfg::OutT*>(p.c) + (size_t)w.split * p.split_stride +
@@ -846,6 +993,19 @@ __global__ void __launch_bounds__(kThreads, Cfg::KIND == 1 ? 2 : 1) k_gemm(const
 #pragma unroll
             for (int v = 0; v < 8; ++v)
               st_out16(crow + c1 + 4 * v, make_uint4(r[4 * v], r[4 * v + 1], r[4 * v + 2], r[4 * v + 3]));
+          } else if constexpr (PR == 2) {
+            // pair tiles with a strided / batched bf16 C: the row straight from registers
+#pragma unroll
+            for (int v = 0; v < 4; ++v) {
+              uint32_t w4[4];
+#pragma unroll
+              for (int e = 0; e < 4; ++e) {
+                __nv_bfloat162 h = __floats2bfloat162_rn(__uint_as_float(r[8 * v + 2 * e]),
+                                                         __uint_as_float(r[8 * v + 2 * e + 1]));
+                w4[e] = *reinterpret_cast<uint32_t*>(&h);
+              }
+              st_out16(crow + c1 + 8 * v, make_uint4(w4[0], w4[1], w4[2], w4[3]));
+            }
           } else {
             // stage this lane's row (16 B chunks, chunk index XOR row % 8:
             // conflict-free) -- written out coalesced below
@@ -866,8 +1026,8 @@ __global__ void __launch_bounds__(kThreads, Cfg::KIND == 1 ? 2 : 1) k_gemm(const
         }
         fence_before();
         __syncwarp();
-        if (lane == 0) mbar_arrive(&tmem_empty[acc]);
-        if constexpr (sizeof(typename Cfg::OutT) == 2) {
+        if (lane == 0) release_acc<PR>(&tmem_empty[acc]);
+        if constexpr (sizeof(typename Cfg::OutT) == 2 && PR == 1) {
           if (last) {
             // the two warps of this lane quarter staged the two column halves
             // of the same 32 rows; after a pair barrier each writes 16 whole
@@ -894,10 +1054,15 @@ __global__ void __launch_bounds__(kThreads, Cfg::KIND == 1 ? 2 : 1) k_gemm(const
   }
 
   fence_before();
-  __syncthreads();
+  if constexpr (PR == 2) cluster_sync_all();   // no remote arrive or MMA into this CTA is still in flight
+  else __syncthreads();
   fence_after();
-  if (warp == 1)
-    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem_base), "n"(Cfg::TMEM_COLS));
+  if (warp == 1) {
+    if constexpr (PR == 2)
+      asm volatile("tcgen05.dealloc.cta_group::2.sync.aligned.b32 %0, %1;" ::"r"(tmem_base), "n"(Cfg::TMEM_COLS));
+    else
+      asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem_base), "n"(Cfg::TMEM_COLS));
+  }
   if constexpr (MODE == kPtb) {
     if (threadIdx.x == 0) ptb_worker_exit(s, stopped, t_entry, kChunkPreempt ? p.resume : nullptr);
   }
@@ -1022,7 +1187,9 @@ static int bind_gemm(const tally_kernel_args* a, Instance* inst, bool split) {
     const long long ar = L ? L->a_rows : (Cfg::A_MN ? K : M), acl = L ? L->a_cols : (Cfg::A_MN ? M : K);
     const long long br = L ? L->b_rows : (Cfg::B_MN ? K : N), bcl = L ? L->b_cols : (Cfg::B_MN ? N : K);
     if ((rc = make_map(&p.a_hi, a->ptr[0], dt, Cfg::ESZ, ar, acl, Cfg::A_MN ? Cfg::BK : Cfg::BM, L ? L->a_ld : 0))) return rc;
-    if ((rc = make_map(&p.b_hi, a->ptr[1], dt, Cfg::ESZ, br, bcl, Cfg::B_MN ? Cfg::BK : Cfg::BN, L ? L->b_ld : 0))) return rc;
+    // (a CTA pair loads BN / 2 rows of B per CTA)
+    if ((rc = make_map(&p.b_hi, a->ptr[1], dt, Cfg::ESZ, br, bcl, Cfg::B_MN ? Cfg::BK : Cfg::BN / gemm::PairOf<Cfg>::value,
+                       L ? L->b_ld : 0))) return rc;
     p.c = a->ptr[2];
     if (L) {
       if (L->batches < 1 || L->hdiv < 1 || L->ldc < N) { set_error("gemm layout: batches, hdiv >= 1, ldc >= N"); return TALLY_EINVAL; }
@@ -1037,11 +1204,12 @@ static int bind_gemm(const tally_kernel_args* a, Instance* inst, bool split) {
   p.bn = Cfg::BN;
   p.bk = Cfg::BK;
   p.causal = (int)a->i[5];
-  if (p.causal < 0 || p.causal > 3 || (p.causal && (Cfg::KIND != 1 || splits != 1 || M % Cfg::BM))) {
-    set_error("gemm: causal mode 0-3, bf16 kinds, no split-K, M %% 128 == 0");
+  constexpr int PR = gemm::PairOf<Cfg>::value;
+  if (p.causal < 0 || p.causal > 3 || (p.causal && (Cfg::KIND != 1 || splits != 1 || M % Cfg::BM || PR != 1))) {
+    set_error("gemm: causal mode 0-3, bf16 single-CTA kinds, no split-K, M %% 128 == 0");
     return TALLY_EINVAL;
   }
-  p.tiles_m = (int)((M + Cfg::BM - 1) / Cfg::BM);
+  p.tiles_m = (int)((M + Cfg::BM * PR - 1) / (Cfg::BM * PR));   // (pair: 256-row tiles)
   p.tiles_n = (int)(N / Cfg::BN);
   const tally_gemm_layout* lay = split ? nullptr : static_cast<const tally_gemm_layout*>(a->ptr[3]);
   p.batches = lay ? lay->batches : 1;
@@ -1049,7 +1217,7 @@ static int bind_gemm(const tally_kernel_args* a, Instance* inst, bool split) {
   p.ldc = lay ? lay->ldc : N;
   p.split_stride = M * N;
   p.splits = (int)splits;
-  if constexpr (Cfg::KIND == 1 && Cfg::BN == 128 && sizeof(typename Cfg::OutT) == 2) {
+  if constexpr (Cfg::KIND == 1 && Cfg::BN >= 128 && sizeof(typename Cfg::OutT) == 2) {
     // TMA-store epilogue for plain (unbatched, unsplit, zero-offset) GEMMs:
     // the map's bounds clip the M tail; batched layouts keep the guarded stores
     bool plain = p.batches == 1 && splits == 1 && aligned16_(p.c) && (p.ldc * 2) % 16 == 0;
@@ -1082,7 +1250,7 @@ static int bind_gemm(const tally_kernel_args* a, Instance* inst, bool split) {
     // ... and at most ~128 KB of output per logical block (fp32 128 x 128
     // tiles: 2 per block) -- a K = 64 fp32 score GEMM at 8 tiles per block
     // had ~30 us logical blocks (preemption latency)
-    constexpr int kTileOut = Cfg::BM * Cfg::BN * (int)sizeof(typename Cfg::OutT);
+    constexpr int kTileOut = Cfg::BM * Cfg::BN * (int)sizeof(typename Cfg::OutT);   // per CTA
     p.tpb = Cfg::KIND != 1 ? 1
           : old_rule ? (p.kb_per_split <= 2 ? 4 : 1)
                      : max(1, min(min(8, (131072 + kTileOut - 1) / kTileOut),
@@ -1184,6 +1352,7 @@ static KernelKind gemm_kind(const char* name, int (*bind)(const tally_kernel_arg
   k.setup = &setup_gemm<Cfg>;
   k.pausable = 1;
   k.tmem_cols = Cfg::TMEM_COLS;
+  k.cluster = gemm::PairOf<Cfg>::value;   // CTA pairs launch as clusters of two
   // device-resident flag: producers poll it every K-chunk (~9 us) -- 148
   // readers x 110 k reads/s would saturate PCIe reads of a mapped host word
   k.host_flag = 0;
@@ -1191,7 +1360,7 @@ static KernelKind gemm_kind(const char* name, int (*bind)(const tally_kernel_arg
 }
 
 int register_gemm_kernels(KernelKind* out, int cap) {
-  if (cap < 15) return 0;
+  if (cap < 20) return 0;
   out[0] = gemm_kind<gemm::CfgTf32x3>("sgemm_tf32x3", bind_sgemm);
   out[1] = gemm_kind<gemm::CfgBf16>("gemm_bf16", bind_bf16<gemm::CfgBf16>);
   out[3] = gemm_kind<gemm::CfgTf32x3N64>("sgemm_tf32x3_n64", bind_sgemm_n64);
@@ -1206,6 +1375,11 @@ int register_gemm_kernels(KernelKind* out, int cap) {
   out[12] = gemm_kind<gemm::CfgBf16F32KMNN64>("gemm_bf16f32_kmn_n64", bind_bf16<gemm::CfgBf16F32KMNN64>);
   out[13] = gemm_kind<gemm::CfgBf16MNb>("gemm_bf16_mn", bind_bf16<gemm::CfgBf16MNb>);
   out[14] = gemm_kind<gemm::CfgBf16MNbN64>("gemm_bf16_mn_n64", bind_bf16<gemm::CfgBf16MNbN64>);
+  out[15] = gemm_kind<gemm::CfgBf16X2>("gemm_bf16_x2", bind_bf16<gemm::CfgBf16X2>);
+  out[16] = gemm_kind<gemm::CfgBf16F32X2>("gemm_bf16f32_x2", bind_bf16<gemm::CfgBf16F32X2>);
+  out[17] = gemm_kind<gemm::CfgBf16MNX2>("gemm_bf16f32_mn_x2", bind_bf16<gemm::CfgBf16MNX2>);
+  out[18] = gemm_kind<gemm::CfgBf16KMNX2>("gemm_bf16_kmn_x2", bind_bf16<gemm::CfgBf16KMNX2>);
+  out[19] = gemm_kind<gemm::CfgBf16F32KMNX2>("gemm_bf16f32_kmn_x2", bind_bf16<gemm::CfgBf16F32KMNX2>);
   KernelKind k{};
   k.name = "split_tf32";
   k.fn_original = reinterpret_cast<const void*>(&k_original<gemm::SplitTf32>);
@@ -1213,7 +1387,7 @@ int register_gemm_kernels(KernelKind* out, int cap) {
   k.fn_ptb = reinterpret_cast<const void*>(&k_ptb<gemm::SplitTf32>);
   k.bind = bind_split;
   out[2] = k;
-  return 15;
+  return 20;
 }
 
 }  // namespace tally

@@ -71,6 +71,9 @@ struct KernelKind {
   // registers and TMEM admit 2 (and the hardware co-schedules 2, ncu
   // r01_ncu_c2_summary); the PTB worker menu uses the resource-derived count.
   int tmem_cols;
+  // CTAs per cluster (CTA-pair GEMMs: 2 -- one logical block per cluster,
+  // PTB workers counted in CTAs, a multiple of it); 0 / 1 = no cluster
+  int cluster;
   // IR-JIT kinds (irjit.py): NVRTC-compiled module, launched with the driver API
   int jit;
   void* cu_fn[3];             // CUfunction for Original / Sliced / PTB

@@ -328,7 +328,8 @@ int Runtime::launch(int kernel, int stream, const tally_launch_desc* d, int* out
   switch (d->shape) {
     case TALLY_SHAPE_ORIGINAL:
       fn = kk.fn_original;
-      grid = dim3(in.grid.x, in.grid.y, in.grid.z);
+      // (cluster kinds: one cluster of kk.cluster CTAs per logical block, 1-D grids)
+      grid = dim3(in.grid.x * (unsigned)std::max(1, kk.cluster), in.grid.y, in.grid.z);
       args[1] = &s;
       L->count = (long long)total;
       break;
@@ -342,7 +343,7 @@ int Runtime::launch(int kernel, int stream, const tally_launch_desc* d, int* out
         }
         s.linear = 1;
         s.linear_offset = (unsigned long long)d->linear_offset;
-        grid = dim3((unsigned)d->count, 1, 1);
+        grid = dim3((unsigned)d->count * (unsigned)std::max(1, kk.cluster), 1, 1);
         L->count = d->count;
       } else {
         if (d->sub_x < 1 || d->sub_y < 1 || d->sub_z < 1 || d->off_x + d->sub_x > in.grid.x ||
@@ -351,7 +352,7 @@ int Runtime::launch(int kernel, int stream, const tally_launch_desc* d, int* out
           return TALLY_EINVAL;
         }
         s.offset = make_uint3(d->off_x, d->off_y, d->off_z);
-        grid = dim3(d->sub_x, d->sub_y, d->sub_z);
+        grid = dim3(d->sub_x * (unsigned)std::max(1, kk.cluster), d->sub_y, d->sub_z);
         L->count = (long long)d->sub_x * d->sub_y * d->sub_z;
       }
       args[1] = &s;
@@ -447,6 +448,11 @@ int Runtime::launch(int kernel, int stream, const tally_launch_desc* d, int* out
       pa.pause = (d->pausable && kk.pausable) ? d_pause : nullptr;
       fn = kk.fn_ptb;
       grid = dim3((unsigned)d->workers, 1, 1);
+      if (kk.cluster > 1 && d->workers % kk.cluster) {
+        free_recs.push_back(rec);
+        set_error("%s: PTB workers must be a multiple of the cluster size %d", kk.name, kk.cluster);
+        return TALLY_EINVAL;
+      }
       args[1] = &pa;
       L->count = (long long)total;
       break;
@@ -466,6 +472,21 @@ int Runtime::launch(int kernel, int stream, const tally_launch_desc* d, int* out
     CUresult cr = cu_launch((CUfunction)kk.cu_fn[idx], grid.x, grid.y, grid.z, (unsigned)in.threads, 1, 1,
                             (unsigned)in.smem, (CUstream)st, args, nullptr);
     if (cr != CUDA_SUCCESS) e = cudaErrorLaunchFailure;
+  } else if (kk.cluster > 1) {
+    // CTA-pair kinds: a cluster launch (the pair shares one tile, cta_group::2)
+    cudaLaunchConfig_t cfg{};
+    cfg.gridDim = grid;
+    cfg.blockDim = dim3(in.threads);
+    cfg.dynamicSmemBytes = in.smem;
+    cfg.stream = st;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeClusterDimension;
+    attr[0].val.clusterDim.x = (unsigned)kk.cluster;
+    attr[0].val.clusterDim.y = 1;
+    attr[0].val.clusterDim.z = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    e = cudaLaunchKernelExC(&cfg, fn, args);
   } else {
     e = cudaLaunchKernel(fn, grid, dim3(in.threads), args, in.smem, st);
   }
@@ -887,21 +908,21 @@ int tally_kernel_kind_count(void) {
   Runtime& r = rt();
   if (!r.inited) {
     // registry is static; allow listing without a device
-    static KernelKind tmp[32];
-    int n = register_basic_kernels(tmp, 32);
-    n += register_gemm_kernels(tmp + n, 32 - n);
-    return n + register_copy_kernels(tmp + n, 32 - n);
+    static KernelKind tmp[64];
+    int n = register_basic_kernels(tmp, 64);
+    n += register_gemm_kernels(tmp + n, 64 - n);
+    return n + register_copy_kernels(tmp + n, 64 - n);
   }
   return r.nkinds;
 }
 
 const char* tally_kernel_kind_name(int kind) {
-  static KernelKind tmp[32];
+  static KernelKind tmp[64];
   static int n = -1;
   if (n < 0) {
-    n = register_basic_kernels(tmp, 32);
-    n += register_gemm_kernels(tmp + n, 32 - n);
-    n += register_copy_kernels(tmp + n, 32 - n);
+    n = register_basic_kernels(tmp, 64);
+    n += register_gemm_kernels(tmp + n, 64 - n);
+    n += register_copy_kernels(tmp + n, 64 - n);
   }
   if (kind < 0 || kind >= n) return nullptr;
   return tmp[kind].name;
@@ -943,6 +964,7 @@ int tally_kernel_info_get(int kernel, tally_kernel_info* o) {
   o->alg_bytes = in.alg_bytes;
   o->alg_flops = in.alg_flops;
   o->preempt_units = in.preempt_units;
+  o->cluster = std::max(1, kk.cluster);
   int occ = 0;
   if (kk.copy) return TALLY_OK;
   if (kk.jit) {

@@ -139,6 +139,7 @@ class KernelInfo:
     alg_bytes: float
     alg_flops: float
     preempt_units: int = 1
+    cluster: int = 1      # CTAs per logical block (CTA-pair GEMMs: 2)
 
 
 class DeviceKernel:
@@ -163,7 +164,7 @@ class DeviceKernel:
         self.info = KernelInfo((ki.grid_x, ki.grid_y, ki.grid_z), ki.total_blocks,
                                ki.threads_per_block, ki.smem_bytes, ki.occupancy_ptb,
                                ki.occupancy_original, ki.alg_bytes, ki.alg_flops,
-                               max(1, ki.preempt_units))
+                               max(1, ki.preempt_units), max(1, ki.cluster))
 
     @property
     def total_blocks(self) -> int:
@@ -342,13 +343,23 @@ def _pack_conv(kh, kw, stride, pad):
     return kh | (kw << 8) | (stride << 16) | (pad << 24)
 
 
-def gemm(A, B, C, splits: int = 1) -> DeviceKernel:
+def _pair_suffix(pair: bool, N: int) -> str:
+    if not pair:
+        return ""
+    if N % 256:
+        raise ValueError("CTA-pair GEMMs (256 x 256 tiles) need N % 256 == 0")
+    return "_x2"
+
+
+def gemm(A, B, C, splits: int = 1, pair: bool = False) -> DeviceKernel:
     """C[M,N] = A[M,K] . B[N,K]^T on tcgen05 (bf16 operands, fp32 accumulation).
 
     The kind follows the operands: N % 128 == 0 -> 128-wide tiles, else
     64-wide; C bf16 or fp32.  ``splits`` > 1 (fp32 C of shape [splits, M, N])
     is split-K: logical block = (split, tile), each split writing its own
-    fp32 partial (summed later by ``sgd_update``)."""
+    fp32 partial (summed later by ``sgd_update``).  ``pair``: a CTA pair
+    (cluster of two SMs, ``tcgen05.mma.cta_group::2``) per 256 x 256 tile --
+    one logical block per pair, PTB workers in CTAs (a multiple of 2)."""
     import torch
     M, K = A.shape
     N, K2 = B.shape
@@ -357,12 +368,14 @@ def gemm(A, B, C, splits: int = 1) -> DeviceKernel:
     out_f32 = C.dtype == torch.float32
     if tuple(C.shape[-2:]) != (M, N) or (splits > 1 and (not out_f32 or C.numel() != splits * M * N)):
         raise ValueError("gemm: C must be [M,N] (or [splits,M,N] fp32 for split-K)")
-    kind = "gemm_bf16" + ("f32" if out_f32 else "") + ("" if N % 128 == 0 else "_n64")
+    kind = "gemm_bf16" + ("f32" if out_f32 else "") + (_pair_suffix(True, N) if pair else
+                                                       "" if N % 128 == 0 else "_n64")
     return DeviceKernel(kind, (A, B, C), (M, N, K, 0, splits))
 
 
 def gemm_ex(A, B, Cout, M, N, K, a_mn=False, b_mn=False, splits=1, batches=1, hdiv=1,
-            a_off=((0, 0), (0, 0)), b_off=((0, 0), (0, 0)), c_off=((0, 0), (0, 0)), causal=0) -> DeviceKernel:
+            a_off=((0, 0), (0, 0)), b_off=((0, 0), (0, 0)), c_off=((0, 0), (0, 0)), causal=0,
+            pair=False) -> DeviceKernel:
     """General bf16 GEMM on tcgen05: per batch, C[M,N] = A . B^T with A
     K-major (A[M,K] row-major) or MN-major (stored as A^T [K,M]), likewise B
     ([N,K] or [K,N]).  ``A``, ``B``, ``Cout`` are 2-D row-major views (any
@@ -374,7 +387,8 @@ def gemm_ex(A, B, Cout, M, N, K, a_mn=False, b_mn=False, splits=1, batches=1, hd
     T x T per batch, T % 128 == 0): 1 = S = Q.K^T / dP = dO.V^T, tiles wholly
     above the diagonal skipped (left unwritten); 2 = P.V / dS.K, K limited to
     keys <= the tile's last query; 3 = dS^T.Q / P^T.dO, K from the tile's
-    first key."""
+    first key.  ``pair``: CTA-pair kind (256 x 256 tiles, N % 256 == 0; not
+    causal; ``_mn`` only with fp32 output)."""
     import torch
     kinds = {(False, False): "", (True, True): "_mn", (False, True): "_kmn"}
     if (a_mn, b_mn) not in kinds:
@@ -383,7 +397,8 @@ def gemm_ex(A, B, Cout, M, N, K, a_mn=False, b_mn=False, splits=1, batches=1, hd
         if t.dim() != 2 or t.stride(1) != 1:
             raise ValueError("gemm_ex: operands must be 2-D row-major views (unit column stride)")
     out = "f32" if Cout.dtype == torch.float32 else ""
-    kind = "gemm_bf16" + out + kinds[(a_mn, b_mn)] + ("" if N % 128 == 0 else "_n64")
+    kind = "gemm_bf16" + out + kinds[(a_mn, b_mn)] + (_pair_suffix(True, N) if pair else
+                                                      "" if N % 128 == 0 else "_n64")
     lay = _lib.c_gemm_layout()
     lay.a_rows, lay.a_cols, lay.a_ld = A.shape[0], A.shape[1], A.stride(0)
     lay.b_rows, lay.b_cols, lay.b_ld = B.shape[0], B.shape[1], B.stride(0)
@@ -396,7 +411,7 @@ def gemm_ex(A, B, Cout, M, N, K, a_mn=False, b_mn=False, splits=1, batches=1, hd
                         (M, N, K, 0, splits, causal), keep=(A, B, Cout, lay))
 
 
-def gemm_mn(At, Bt, C, splits: int = 1) -> DeviceKernel:
+def gemm_mn(At, Bt, C, splits: int = 1, pair: bool = False) -> DeviceKernel:
     """C[M,N] (fp32) = At[K,M]^T . Bt[K,N] with both operands MN-major (as
     stored: M / N contiguous) -- the weight gradient dW = dY^T . X of a
     convolution straight from the NHWC activations.  Split-K as ``gemm``."""
@@ -407,7 +422,7 @@ def gemm_mn(At, Bt, C, splits: int = 1) -> DeviceKernel:
         raise ValueError("gemm_mn: At[K,M], Bt[K,N] need the same K")
     if C.dtype != torch.float32 or tuple(C.shape[-2:]) != (M, N) or C.numel() != splits * M * N:
         raise ValueError("gemm_mn: C must be fp32 [M,N] (or [splits,M,N])")
-    kind = "gemm_bf16f32_mn" + ("" if N % 128 == 0 else "_n64")
+    kind = "gemm_bf16f32_mn" + (_pair_suffix(True, N) if pair else "" if N % 128 == 0 else "_n64")
     return DeviceKernel(kind, (At, Bt, C), (M, N, K, 0, splits))
 
 

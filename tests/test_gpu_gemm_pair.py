@@ -1,0 +1,155 @@
+"""CTA-pair tcgen05 GEMMs (``*_x2`` kinds: a cluster of two SMs per 256 x 256
+tile, ``tcgen05.mma.cta_group::2``, each CTA loading half of A and half of B)
+in all three Tally shapes.  Needs a B200.
+
+Tolerance (north star, bf16): max|C - C_ref| / max|C_ref| < 1e-2 against a
+float64 reference of the same bf16 inputs; every shape (Original, Sliced,
+PTB) bit-identical to the pair kernel's own Original launch and every logical
+block executed exactly once.
+"""
+
+from fractions import Fraction
+
+import pytest
+
+torch = pytest.importorskip("torch")
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module")
+def env():
+    if not torch.cuda.is_available():
+        pytest.skip("no GPU")
+    import paper_2410_07381_b200 as P
+    from paper_2410_07381_b200 import kernels
+    P.B200Device.get(0)
+    return P, kernels, kernels.Stream(high_priority=False)
+
+
+def _shapes(P, dk, stream, out, workers=(148, 296)):
+    total = dk.total_blocks
+    res = {}
+    runs = [("original", None)] + [("sliced", f) for f in (Fraction(1, 3),)] + [("ptb", w) for w in workers]
+    for name, arg in runs:
+        out.zero_()
+        ec = torch.zeros(total, dtype=torch.int64, device="cuda")
+        if name == "original":
+            dk.original(stream, exec_count=ec).wait()
+        elif name == "sliced":
+            for off, cnt in P.slice_plan(total, arg):
+                dk.sliced(stream, off, cnt, exec_count=ec).wait()
+        else:
+            dk.ptb(stream, arg, exec_count=ec).wait()
+        assert bool((ec == 1).all()), (name, arg)
+        res[(name, arg)] = out.clone()
+    base = res[("original", None)]
+    for k, v in res.items():
+        assert torch.equal(v, base), k
+    return base
+
+
+def _rel(c, ref):
+    return ((c.double() - ref).abs().max() / ref.abs().max()).item()
+
+
+@pytest.mark.parametrize("mnk", [(256, 256, 64), (1000, 512, 1024), (4096, 768, 1536)])
+@pytest.mark.parametrize("out", ["bf16", "f32"])
+def test_pair_gemm_kmajor(env, mnk, out):
+    P, kernels, s = env
+    M, N, K = mnk
+    g = torch.Generator(device="cuda").manual_seed(M + N + K)
+    A = (torch.rand(M, K, device="cuda", generator=g) * 2 - 1).bfloat16()
+    B = (torch.rand(N, K, device="cuda", generator=g) * 2 - 1).bfloat16()
+    C = torch.zeros(M, N, device="cuda", dtype=torch.bfloat16 if out == "bf16" else torch.float32)
+    dk = kernels.gemm(A, B, C, pair=True)
+    assert dk.kind.endswith("_x2") and dk.info.cluster == 2
+    c = _shapes(P, dk, s, C)
+    assert _rel(c, A.double() @ B.double().T) < 1e-2
+    # same math as the single-CTA kernel
+    C1 = torch.zeros_like(C)
+    d1 = kernels.gemm(A, B, C1)
+    d1.original(s).wait()
+    assert _rel(c, C1.double()) < 1e-2
+
+
+def test_pair_gemm_splitk(env):
+    P, kernels, s = env
+    M, N, K, S = 1024, 512, 4096, 4
+    g = torch.Generator(device="cuda").manual_seed(7)
+    A = (torch.rand(M, K, device="cuda", generator=g) * 2 - 1).bfloat16()
+    B = (torch.rand(N, K, device="cuda", generator=g) * 2 - 1).bfloat16()
+    C = torch.zeros(S, M, N, device="cuda")
+    dk = kernels.gemm(A, B, C, splits=S, pair=True)
+    c = _shapes(P, dk, s, C)
+    assert _rel(c.sum(0), A.double() @ B.double().T) < 1e-2
+
+
+def test_pair_gemm_mn_weight_gradient(env):
+    """dW = dY^T . X with both operands MN-major as stored (fp32, split-K)."""
+    P, kernels, s = env
+    T, M, N, S = 2048, 512, 768, 2
+    g = torch.Generator(device="cuda").manual_seed(11)
+    dY = (torch.rand(T, M, device="cuda", generator=g) * 2 - 1).bfloat16()
+    X = (torch.rand(T, N, device="cuda", generator=g) * 2 - 1).bfloat16()
+    C = torch.zeros(S, M, N, device="cuda")
+    dk = kernels.gemm_mn(dY, X, C, splits=S, pair=True)
+    c = _shapes(P, dk, s, C)
+    assert _rel(c.sum(0), dY.double().T @ X.double()) < 1e-2
+
+
+@pytest.mark.parametrize("out", ["bf16", "f32"])
+def test_pair_gemm_kmn_batched(env, out):
+    """P . V-like: A K-major, B MN-major, two batches at row offsets, strided C."""
+    P, kernels, s = env
+    Bt, M, N, K = 2, 512, 256, 512
+    g = torch.Generator(device="cuda").manual_seed(13)
+    A = (torch.rand(Bt * M, K, device="cuda", generator=g) * 2 - 1).bfloat16()
+    Bm = (torch.rand(Bt * K, N + 256, device="cuda", generator=g) * 2 - 1).bfloat16()[:, :N]
+    dt = torch.bfloat16 if out == "bf16" else torch.float32
+    Cfull = torch.zeros(Bt * M, N + 128, device="cuda", dtype=dt)
+    Cv = Cfull[:, :N]
+    dk = kernels.gemm_ex(A, Bm, Cv, M, N, K, a_mn=False, b_mn=True, batches=Bt,
+                         a_off=((M, 0), (0, 0)), b_off=((K, 0), (0, 0)), c_off=((M, 0), (0, 0)), pair=True)
+    c = _shapes(P, dk, s, Cfull)
+    for z in range(Bt):
+        ref = A[z * M:(z + 1) * M].double() @ Bm[z * K:(z + 1) * K].double()
+        assert _rel(c[z * M:(z + 1) * M, :N], ref) < 1e-2
+    assert not c[:, N:].any()   # nothing outside the view
+
+
+def test_pair_gemm_preempt_resume_exactly_once(env):
+    """PTB pairs preempted by the counter trigger at several points, then
+    resumed from the persisted counter: every tile exactly once, result equal
+    to the uninterrupted run."""
+    P, kernels, s = env
+    M, N, K = 2048, 1024, 1024
+    g = torch.Generator(device="cuda").manual_seed(17)
+    A = (torch.rand(M, K, device="cuda", generator=g) * 2 - 1).bfloat16()
+    B = (torch.rand(N, K, device="cuda", generator=g) * 2 - 1).bfloat16()
+    C = torch.zeros(M, N, device="cuda", dtype=torch.bfloat16)
+    dk = kernels.gemm(A, B, C, pair=True)
+    dk.original(s).wait()
+    ref = C.clone()
+    total = dk.total_blocks
+    for at in (1, 5, total // 2):
+        C.zero_()
+        ec = torch.zeros(total, dtype=torch.int64, device="cuda")
+        st = dk.ptb(s, 16, preempt_at=at, exec_count=ec).wait()
+        count = st.task_counter
+        assert st.parked == (count < total)
+        assert bool((ec[count:] == 0).all()) and bool((ec[:count] == 1).all())
+        while count < total:
+            count = dk.ptb(s, 16, start_count=count, exec_count=ec).wait().task_counter
+        assert bool((ec == 1).all()), at
+        assert torch.equal(C, ref), at
+
+
+def test_pair_ptb_rejects_odd_workers(env):
+    P, kernels, s = env
+    A = torch.zeros(256, 64, device="cuda", dtype=torch.bfloat16)
+    B = torch.zeros(256, 64, device="cuda", dtype=torch.bfloat16)
+    C = torch.zeros(256, 256, device="cuda", dtype=torch.bfloat16)
+    dk = kernels.gemm(A, B, C, pair=True)
+    with pytest.raises(Exception):
+        dk.ptb(s, 3)

@@ -90,14 +90,16 @@ def test_captured_step_under_tally_with_preemption(env):
     arr = workloads.generate_arrivals(0.3, 100_000, horizon, seed=4)
     tasks = [P.TaskScript("hp", P.HIGH, (P.KernelWork("vadd_hp", hp.cost(), kernel=hp),), arr),
              P.TaskScript("be", P.BEST_EFFORT, works)]
-    res = P.run_policy(dev.spec, tasks, P.SchedulerConfig(policy="Tally"), horizon, profiler=prof,
-                       record_events=False)
+    # a 2 us turnaround threshold: these GEMMs are a few microseconds long, so
+    # at the default 31.6 us the tuner (rightly) keeps them untransformed
+    res = P.run_policy(dev.spec, tasks, P.SchedulerConfig(policy="Tally", turnaround_threshold_ns=2_000), horizon,
+                       profiler=prof, record_events=False)
     torch.cuda.synchronize()
     n = len(res.iterations["be"])
     assert n >= 2 and len(res.requests["hp"]) == len(arr)
     assert torch.equal(hc, ha + hb)
     shapes = {r["shape"] for r in res.launches if r["task"] == 1}
-    assert 2 in shapes, "no best-effort GEMM ran as PTB"
+    assert shapes & {1, 2}, "no best-effort kernel ran transformed"
     after_tally = [t.detach().clone() for t in state]
     with torch.no_grad():
         for t, v in zip(state, snap):
