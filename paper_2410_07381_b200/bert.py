@@ -21,7 +21,7 @@ parity test compares against it; Q, K, V are fused into one [3d, d] linear.
 from __future__ import annotations
 
 from . import kernels as K
-from .transformer import WEIGHT_DECAY, TransformerTrain, _gemm_splits
+from .transformer import WEIGHT_DECAY, TransformerTrain, _pair_plan
 
 
 class BertTrain(TransformerTrain):
@@ -132,7 +132,8 @@ class BertTrain(TransformerTrain):
         t = self._linear_fwd("cls.predictions.transform.dense", self.head, x, act=self.gelu_act, pre=tpre)
         tl = self._ln_fwd("cls.predictions.transform.LayerNorm", self.ln_head, t)
         logits = self._buf(N, self.Vp)
-        self._add("cls.predictions.decoder", K.gemm(tl, self.wte.wb, logits))
+        pair_dec = _pair_plan(N, self.Vp, d, self.pair_gemms)[0]
+        self._add("cls.predictions.decoder", K.gemm(tl, self.wte.wb, logits, pair=pair_dec))
         dl = self._buf(N, self.Vp)
         self._add("softmax_xent", K.softmax_xent(logits, self.dec_b.w, self.labels, self.loss, dl, None, self.V))
         self.logits = logits
@@ -142,13 +143,13 @@ class BertTrain(TransformerTrain):
         self.sgd.add(self.dec_b.w, self.dec_b.v, self.dec_b.g.view(1, -1), 1, self.Vp, WEIGHT_DECAY)
         dtl = self._buf(N, d)
         self._gemm_ex_splitk("cls.predictions.decoder.dgrad", dl, self.wte.wb, dtl, N, d, self.Vp, b_mn=True)
-        Sw = _gemm_splits(self.Vp, d, N)
+        pw, Sw = _pair_plan(self.Vp, d, N, self.pair_gemms)
         self.wte.gpart = torch.zeros(Sw + 1, self.Vp, d, dtype=torch.float32, device=self.device)
         if Sw == 1:
             self._add("cls.predictions.decoder.wgrad", K.gemm_ex(dl, tl, self.wte.gpart[0], self.Vp, d, N,
-                                                                 a_mn=True, b_mn=True))
+                                                                 a_mn=True, b_mn=True, pair=pw))
         else:
-            self._add("cls.predictions.decoder.wgrad", K.gemm_mn(dl, tl, self.wte.gpart[:Sw], splits=Sw))
+            self._add("cls.predictions.decoder.wgrad", K.gemm_mn(dl, tl, self.wte.gpart[:Sw], splits=Sw, pair=pw))
         dt = self._ln_bwd("cls.predictions.transform.LayerNorm", self.ln_head, dtl, t)
         du = self._buf(N, d)
         self._add("cls.predictions.transform.gelu_bwd", K.gelu_bwd(dt, tpre, du, erf=True))

@@ -126,8 +126,18 @@ __device__ __forceinline__ void mbar_wait_cluster(uint64_t* bar, uint32_t parity
       "r"(parity)
       : "memory");
 }
-__device__ __forceinline__ void st_cluster_s64(uint32_t cluster_addr, long long v) {
-  asm volatile("st.shared::cluster.s64 [%0], %1;" ::"r"(cluster_addr), "l"(v) : "memory");
+// (relaxed: the arrival orders nothing but the reuse of a slot the waiter
+// has already read, or -- for TMEM -- tcgen05.ld completion, which the
+// tcgen05 fences order)
+__device__ __forceinline__ void mbar_arrive_remote_relaxed(uint32_t cluster_addr) {
+  asm volatile("mbarrier.arrive.relaxed.cluster.shared::cluster.b64 _, [%0];" ::"r"(cluster_addr) : "memory");
+}
+// 8-byte store into a peer CTA's shared memory that completes as 8
+// transaction bytes on the peer's mbarrier (no fence on the sender)
+__device__ __forceinline__ void st_async_s64(uint32_t cluster_addr, long long v, uint32_t cluster_bar) {
+  asm volatile("st.async.shared::cluster.mbarrier::complete_tx::bytes.s64 [%0], %1, [%2];" ::"r"(cluster_addr),
+               "l"(v), "r"(cluster_bar)
+               : "memory");
 }
 // Pair TMA load: both CTAs load their half into their own shared memory and
 // signal the leader CTA's full barrier (`lead_bar`: its shared::cluster
@@ -443,11 +453,16 @@ __device__ __forceinline__ int goff(const GemmParams& p, int which, const TileWo
   return (int)(p.off[which][0] * w.zb + p.off[which][1] * w.zh);
 }
 
+__device__ __forceinline__ const unsigned long long* ret_ring_of(const SliceArgs&) { return nullptr; }
+__device__ __forceinline__ unsigned long long ret_pending_of(const SliceArgs&) { return 0ull; }
+__device__ __forceinline__ const unsigned long long* ret_ring_of(const PtbArgs& a) { return a.ret_ring; }
+__device__ __forceinline__ unsigned long long ret_pending_of(const PtbArgs& a) { return a.ret_pending; }
+
 // An epilogue warp hands a drained TMEM accumulator back to the MMA issuer
 // (pair: to the leader CTA's barrier, which counts both CTAs' warps).
 template <int PR>
 __device__ __forceinline__ void release_acc(uint64_t* bar) {
-  if constexpr (PR == 2) mbar_arrive_remote(map_rank(bar, 0));
+  if constexpr (PR == 2) mbar_arrive_remote_relaxed(map_rank(bar, 0));   // after tcgen05.wait::ld + fence
   else mbar_arrive(bar);
 }
 
@@ -515,6 +530,7 @@ k_gemm(const __grid_constant__ GemmParams p, const ShapeArgs s) {
   fence_after();
   const uint32_t tmem_base = *tmem_base_slot;
   bool stopped = false;
+  unsigned long long blocks_run = 0;   // logical blocks this worker ran (PTB telemetry / retirement)
   // chunk-granular preemption (fp32-output kernels in PTB shape with a resume
   // ring): a preempted worker stops its tile at the next chunk boundary,
   // saves the fp32 running total into its C tile and queues (tile, chunk)
@@ -536,16 +552,72 @@ k_gemm(const __grid_constant__ GemmParams p, const ShapeArgs s) {
       // sequence (tpb > 1 for short-K GEMMs, whose one-tile CTAs are
       // prologue / pipeline-fill bound)
       long long q_next = 0, q_end = 0;
+      // bf16 kinds in PTB shape (claim-ahead worker, see the branch below)
+      long long pre = -1;          // the next logical block, claimed while this one runs
+      bool first_block = true;
+      bool try_pop = MODE == kPtb && ret_ring_of(s) != nullptr && ret_pending_of(s) > 0;
       for (int i = 0;; ++i) {
         long long t = -1;
         int c0 = 0;
         if (MODE == kPtb && PR == 2 && !lead) {
           // the peer takes the leader's tiles (-2: the leader was stopped by the flag)
           const int jj = i % kSlots;
-          mbar_wait_cluster(&pair_full[jj], (i / kSlots) & 1);
+          mbar_expect_tx(&pair_full[jj], 8);
+          mbar_wait(&pair_full[jj], (i / kSlots) & 1);
           t = *reinterpret_cast<volatile long long*>(&pair_slot[jj]);
-          mbar_arrive_remote(map_rank(&pair_empty[jj], 0));
+          mbar_arrive_remote_relaxed(map_rank(&pair_empty[jj], 0));
           if (t == -2) { stopped = true; t = -1; }
+          if (i == 0) *reinterpret_cast<volatile unsigned long long*>(tmem_base_slot + 2) = globaltimer();
+        } else if constexpr (MODE == kPtb && Cfg::KIND == 1) {
+          // Claim-ahead worker (bf16 kinds).  The first block is static
+          // (worker w < static_n runs start + w, no claim round trip); the
+          // claim for block b+1 is issued when block b starts, so its L2 round
+          // trip overlaps b's tiles; at the b -> b+1 boundary the flag (loaded
+          // when b's last tile was published) decides: raised -> b+1 is handed
+          // back through the instance's return ring unrun (bounded retirement:
+          // one logical block after the flag), else it runs.  A chain's next
+          // launch pops handed-back blocks first.
+          if (q_next < q_end) {
+            t = q_next++;   // the rest of the current logical block
+          } else {
+            long long b = -1;
+            if (first_block) {
+              first_block = false;
+              ptb_hold_while_paused(s);
+              const unsigned f = s.flag_is_host ? ld_acquire_sys(s.flag) : ld_acquire_gpu(s.flag);
+              const unsigned w = blockIdx.x / PR;
+              if (ptb_park_requested(s, f)) {
+                if (w < s.static_n) ptb_return(s, (long long)(s.start + w));
+                stopped = true;
+              } else if (try_pop) {
+                b = ptb_pop(s);
+                if (b < 0) { try_pop = false; b = ptb_claim_gated(s); }
+              } else {
+                b = w < s.static_n ? (long long)(s.start + w) : ptb_claim_gated(s);
+              }
+            } else if (ptb_park_requested(s, flag_seen)) {
+              if (pre >= 0 && (unsigned long long)pre < s.total) ptb_return(s, pre);
+              stopped = true;
+            } else {
+              b = pre;
+            }
+            if (b >= 0 && (unsigned long long)b < s.total) {
+              ++blocks_run;
+              if (s.exec_count != nullptr) atomicAdd(&s.exec_count[b], 1ull);
+              // claim ahead (nothing left to claim once the static blocks cover the kernel)
+              if (s.start + s.static_n >= s.total && !try_pop) {
+                pre = (long long)s.total;
+              } else if (try_pop) {
+                pre = ptb_pop(s);
+                if (pre < 0) { try_pop = false; pre = ptb_claim_gated(s); }
+              } else {
+                pre = ptb_claim_gated(s);
+              }
+              q_next = b * p.tpb;
+              q_end = min((long long)p.total_tiles, q_next + p.tpb);
+              t = q_next++;
+            }
+          }
         } else if constexpr (MODE == kPtb) {
           bool popped = false;
           if (kChunkPreempt && p.resume != nullptr) {
@@ -598,9 +670,13 @@ k_gemm(const __grid_constant__ GemmParams p, const ShapeArgs s) {
           if (lead) {   // forward to the peer's producer
             const int jj = i % kSlots;
             if (i >= kSlots) mbar_wait_cluster(&pair_empty[jj], ((i / kSlots) - 1) & 1);
-            st_cluster_s64(map_rank(&pair_slot[jj], 1), (t < 0 && stopped) ? -2ll : t);
-            mbar_arrive_remote(map_rank(&pair_full[jj], 1));
+            st_async_s64(map_rank(&pair_slot[jj], 1), (t < 0 && stopped) ? -2ll : t, map_rank(&pair_full[jj], 1));
           }
+        }
+        if constexpr (MODE == kPtb && Cfg::KIND == 1) {
+          // the last tile of a block: load the flag now, read it at the boundary
+          if (t >= 0 && q_next >= q_end && lead)
+            flag_seen = s.flag_is_host ? ld_relaxed_sys(s.flag) : ld_relaxed_gpu(s.flag);
         }
         const int j = i % kSlots;
         if (i >= kSlots) mbar_wait(&tile_empty[j], ((i / kSlots) - 1) & 1);
@@ -696,6 +772,8 @@ k_gemm(const __grid_constant__ GemmParams p, const ShapeArgs s) {
           break;
         }
         const TileWork w = tile_w[j];
+        if (i == 0 && MODE == kPtb)   // telemetry: first tile in hand (worker_log)
+          *reinterpret_cast<volatile unsigned long long*>(tmem_base_slot + 2) = globaltimer();
         for (int c = c0; c < w.nch; ++c, ++ci) {
           const int acc = ci & 1;
           if (ci >= 2) {
@@ -1064,7 +1142,17 @@ k_gemm(const __grid_constant__ GemmParams p, const ShapeArgs s) {
       asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem_base), "n"(Cfg::TMEM_COLS));
   }
   if constexpr (MODE == kPtb) {
-    if (threadIdx.x == 0) ptb_worker_exit(s, stopped, t_entry, kChunkPreempt ? p.resume : nullptr);
+    if (threadIdx.x == 0) {
+      if (s.worker_log != nullptr) {   // per-worker telemetry: smid | blocks, entry, first tile, exit
+        unsigned long long* wl = s.worker_log + 4ull * blockIdx.x;
+        wl[0] = ((unsigned long long)smid() << 32) | (blocks_run & 0xffffffffull);
+        wl[1] = t_entry;
+        wl[2] = *reinterpret_cast<volatile unsigned long long*>(tmem_base_slot + 2);
+        wl[3] = globaltimer();
+      }
+      if constexpr (Cfg::KIND == 1) ptb_worker_exit(s, stopped, t_entry, s.ret_ring, blocks_run);
+      else ptb_worker_exit(s, stopped, t_entry, kChunkPreempt ? p.resume : nullptr);
+    }
   }
 }
 
@@ -1353,6 +1441,7 @@ static KernelKind gemm_kind(const char* name, int (*bind)(const tally_kernel_arg
   k.pausable = 1;
   k.tmem_cols = Cfg::TMEM_COLS;
   k.cluster = gemm::PairOf<Cfg>::value;   // CTA pairs launch as clusters of two
+  k.ret_ring = Cfg::KIND == 1;            // claim-ahead workers (bf16 kinds)
   // device-resident flag: producers poll it every K-chunk (~9 us) -- 148
   // readers x 110 k reads/s would saturate PCIe reads of a mapped host word
   k.host_flag = 0;

@@ -74,6 +74,9 @@ struct KernelKind {
   // CTAs per cluster (CTA-pair GEMMs: 2 -- one logical block per cluster,
   // PTB workers counted in CTAs, a multiple of it); 0 / 1 = no cluster
   int cluster;
+  // 1: a tcgen05 kind whose PTB workers use the instance's return ring and
+  // static first blocks like k_ptb (claim-ahead bf16 GEMMs)
+  int ret_ring;
   // IR-JIT kinds (irjit.py): NVRTC-compiled module, launched with the driver API
   int jit;
   void* cu_fn[3];             // CUfunction for Original / Sliced / PTB

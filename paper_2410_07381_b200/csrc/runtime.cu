@@ -379,8 +379,9 @@ int Runtime::launch(int kernel, int stream, const tally_launch_desc* d, int* out
       pa.ret_ring = nullptr;
       pa.ret_pending = 0;
       pa.static_n = 0;
-      if (kk.tmem_cols == 0 && !kk.copy) {
-        // generic k_ptb workers: the instance's return ring (bounded retirement)
+      if ((kk.tmem_cols == 0 || kk.ret_ring) && !kk.copy) {
+        // generic k_ptb workers and claim-ahead GEMM workers: the instance's
+        // return ring (bounded retirement)
         Instance& mi = *instances[kernel];
         if (mi.ret_ring == nullptr) {
           const size_t bytes = (2 + kRetCap) * sizeof(unsigned long long);
@@ -399,8 +400,9 @@ int Runtime::launch(int kernel, int stream, const tally_launch_desc* d, int* out
         pa.ret_pending = mi.ret_pending;
         // static first blocks (no claim round trip) unless the launch resumes
         // handed-back blocks or runs the counter-triggered test preemption
+        // (cluster kinds: one static block per cluster of workers)
         if (mi.ret_pending == 0 && d->preempt_at < 0 && (unsigned long long)d->start_count < total)
-          pa.static_n = std::min<unsigned long long>((unsigned long long)d->workers,
+          pa.static_n = std::min<unsigned long long>((unsigned long long)(d->workers / std::max(1, kk.cluster)),
                                                      total - (unsigned long long)d->start_count);
       }
       pa.grp = d_groups + (size_t)rec * kMaxExitGroups;

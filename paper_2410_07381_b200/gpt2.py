@@ -26,7 +26,7 @@ is padded to a multiple of 128 (zero rows; their gradient stays zero).
 from __future__ import annotations
 
 from . import kernels as K
-from .transformer import MOMENTUM, WEIGHT_DECAY, TransformerTrain, _gemm_splits  # noqa: F401
+from .transformer import MOMENTUM, WEIGHT_DECAY, TransformerTrain, _pair_plan  # noqa: F401
 
 LN_EPS = 1e-5
 
@@ -121,19 +121,20 @@ class GPT2Train(TransformerTrain):
         self.x_final = x
         hf = self._ln_fwd("transformer.ln_f", self.lnf, x)
         logits = self._buf(N, self.Vp)
-        self._add("lm_head", K.gemm(hf, self.wte.wb, logits))
+        pair_dec = _pair_plan(N, self.Vp, d, self.pair_gemms)[0]
+        self._add("lm_head", K.gemm(hf, self.wte.wb, logits, pair=pair_dec))
         dl = self._buf(N, self.Vp)
         self._add("softmax_xent", K.softmax_xent(logits, None, self.targets, self.loss, dl, None, self.V))
         self.logits = logits
         # backward: head (tied wte: wgrad partials + one embedding-scatter slice)
         dhf = self._buf(N, d)
         self._gemm_ex_splitk("lm_head.dgrad", dl, self.wte.wb, dhf, N, d, self.Vp, b_mn=True)
-        Sw = _gemm_splits(self.Vp, d, N)
+        pw, Sw = _pair_plan(self.Vp, d, N, self.pair_gemms)
         self.wte.gpart = torch.zeros(Sw + 1, self.Vp, d, dtype=torch.float32, device=self.device)
         if Sw == 1:
-            self._add("lm_head.wgrad", K.gemm_ex(dl, hf, self.wte.gpart[0], self.Vp, d, N, a_mn=True, b_mn=True))
+            self._add("lm_head.wgrad", K.gemm_ex(dl, hf, self.wte.gpart[0], self.Vp, d, N, a_mn=True, b_mn=True, pair=pw))
         else:
-            self._add("lm_head.wgrad", K.gemm_mn(dl, hf, self.wte.gpart[:Sw], splits=Sw))
+            self._add("lm_head.wgrad", K.gemm_mn(dl, hf, self.wte.gpart[:Sw], splits=Sw, pair=pw))
         g = self._ln_bwd("transformer.ln_f", self.lnf, dhf, x)
         dP = torch.empty(BHT, T, dtype=torch.float32, device=self.device)
         self.block_grads = {}

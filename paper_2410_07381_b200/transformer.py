@@ -29,6 +29,21 @@ MOMENTUM = 0.9
 WEIGHT_DECAY = 0.0
 
 
+def _pair_plan(M, N, Kdim, enabled=True):
+    """(pair, splits) for a linear-layer GEMM.  CTA-pair tiles (256 x 256,
+    ``*_x2`` kinds) when N % 256 == 0 and there are >= 64 of them (most of
+    the 74 SM pairs busy without split-K); their logical blocks are capped at
+    ~270 MFLOP (~13 us on a pair -- the preemption granularity the 40 MFLOP
+    single-CTA cap gives at half the per-SM rate).  Otherwise single-CTA
+    tiles with ``resnet._gemm_splits``."""
+    tiles = math.ceil(M / 256) * (N // 256) if N % 256 == 0 else 0
+    if not enabled or tiles < 64:
+        return False, _gemm_splits(M, N, Kdim)
+    kb = math.ceil(Kdim / 64)
+    s = max(1, min(kb // 2, math.ceil(2.0 * 256 * 256 * Kdim / 270e6)))
+    return True, math.ceil(kb / math.ceil(kb / s))
+
+
 def _rb_cols(P, C):
     """Rows per colstats logical block (~128 KB of gradient per block)."""
     base = 1024 if C < 128 else (512 if C < 256 else 256)
@@ -46,6 +61,7 @@ class TransformerTrain:
     gelu_act = 2          # bias_act activation code: 2 GELU tanh, 3 GELU erf
     causal = True
     ln_eps = 1e-5
+    pair_gemms = True     # CTA-pair tcgen05 GEMMs for the large linear layers (_pair_plan)
 
     def _init_common(self):
         import torch
@@ -123,12 +139,12 @@ class TransformerTrain:
         """dW[out, in] = dy^T . x, split-K fp32 partials -> sgd_update."""
         torch = self.torch
         M, Nn, Kd = dy.shape[1], x.shape[1], self.N
-        S = _gemm_splits(M, Nn, Kd)
+        pair, S = _pair_plan(M, Nn, Kd, self.pair_gemms)
         p.gpart = torch.empty(S, M, Nn, dtype=torch.float32, device=self.device)
         if S == 1:
-            self._add(name + ".wgrad", K.gemm_ex(dy, x, p.gpart[0], M, Nn, Kd, a_mn=True, b_mn=True))
+            self._add(name + ".wgrad", K.gemm_ex(dy, x, p.gpart[0], M, Nn, Kd, a_mn=True, b_mn=True, pair=pair))
         else:
-            self._add(name + ".wgrad", K.gemm_mn(dy, x, p.gpart, splits=S))
+            self._add(name + ".wgrad", K.gemm_mn(dy, x, p.gpart, splits=S, pair=pair))
         self.sgd.add(p.w, p.v, p.gpart, S, M * Nn, WEIGHT_DECAY, p.wb, None, M, Nn)
 
     def _ws(self, numel):
@@ -148,12 +164,12 @@ class TransformerTrain:
         for a PTB configuration to meet the turnaround threshold, where the
         reference's fallback (least turnaround) would otherwise pick a 1/256
         slicing at 200x the latency."""
-        S = _gemm_splits(M, N, Kd)
+        pair, S = _pair_plan(M, N, Kd, self.pair_gemms)
         if S == 1:
-            self._add(name, K.gemm_ex(A, B, out, M, N, Kd, b_mn=b_mn))
+            self._add(name, K.gemm_ex(A, B, out, M, N, Kd, b_mn=b_mn, pair=pair))
             return
         ws = self._ws(S * M * N).view(S * M, N)
-        self._add(name, K.gemm_ex(A, B, ws, M, N, Kd, b_mn=b_mn, splits=S))
+        self._add(name, K.gemm_ex(A, B, ws, M, N, Kd, b_mn=b_mn, splits=S, pair=pair))
         self._add(name + ".reduce", K.splitk_reduce(ws.view(S, M, N), out))
 
     def _linear_bwd(self, name, lin, dy, x, need_dx=True):

@@ -137,10 +137,15 @@ def test_pair_gemm_preempt_resume_exactly_once(env):
         ec = torch.zeros(total, dtype=torch.int64, device="cuda")
         st = dk.ptb(s, 16, preempt_at=at, exec_count=ec).wait()
         count = st.task_counter
-        assert st.parked == (count < total)
-        assert bool((ec[count:] == 0).all()) and bool((ec[:count] == 1).all())
-        while count < total:
-            count = dk.ptb(s, 16, start_count=count, exec_count=ec).wait().task_counter
+        # blocks below the counter ran once or were handed back unrun (at
+        # most one per worker pair: bounded retirement); none above it ran
+        below = ec[:count].cpu().tolist()
+        assert set(below) <= {0, 1} and below.count(0) <= 8
+        assert bool((ec[count:] == 0).all())
+        assert st.parked
+        while not st.done:
+            st = dk.ptb(s, 16, start_count=count, exec_count=ec).wait()
+            count = st.task_counter
         assert bool((ec == 1).all()), at
         assert torch.equal(C, ref), at
 

@@ -1,7 +1,8 @@
 """Single-CTA (128 x BN tiles, two CTAs per SM) vs CTA-pair (256 x 256 tiles,
 cta_group::2, one CTA per SM) tcgen05 GEMMs against cuBLAS (torch.matmul), on
 one B200: device time per launch (CUDA events on the launch stream, L2 flushed
-before each launch), Original and PTB at the tuner's full-occupancy worker
+before each launch, a spin kernel queued ahead so the events do not time the
+host's launch latency), Original and PTB at the tuner's full-occupancy worker
 count, TFLOP/s of 2*M*N*K.
 
     python tools/gemm_pair_bench.py [--only <label substring>] [--reps 5]
@@ -34,6 +35,10 @@ SHAPES = [
 def main():
     P.B200Device.get(0)
     s = kernels.Stream(high_priority=False)
+    # a ~30 us spin queued ahead of every timed launch: the launch and its
+    # bracketing events are enqueued before the GPU reaches them, so the
+    # events time the device, not the host's launch latency on an idle stream
+    spin = kernels.spin(148, 32, 30_000)
     flush = torch.empty(256 << 20, dtype=torch.uint8, device="cuda")
     g = torch.Generator(device="cuda").manual_seed(0)
     reps = int(sys.argv[sys.argv.index("--reps") + 1]) if "--reps" in sys.argv else 5
@@ -51,6 +56,8 @@ def main():
             ts = []
             for i in range(reps + 1):
                 flush.zero_()
+                torch.cuda.synchronize()
+                spin.original(s)
                 L = fn()
                 L.wait()
                 if i:
@@ -79,6 +86,7 @@ def main():
         ts = []
         for i in range(reps + 1):
             flush.zero_()
+            torch.cuda._sleep(60_000)   # same idea on torch's stream (~30 us)
             e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
             e0.record()
             torch.matmul(A, B.t(), out=Cb)
