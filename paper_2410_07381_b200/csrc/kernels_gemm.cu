@@ -590,7 +590,9 @@ k_gemm(const __grid_constant__ GemmParams p, const ShapeArgs s) {
                 if (w < s.static_n) ptb_return(s, (long long)(s.start + w));
                 stopped = true;
               } else if (try_pop) {
-                b = ptb_pop(s);
+                int cnt = 1;
+                b = ptb_pop_range(s, cnt);
+                if (b >= 0 && cnt > 1) ptb_return_range(s, b + 1, cnt - 1);   // (GEMM workers take one)
                 if (b < 0) { try_pop = false; b = ptb_claim_gated(s); }
               } else {
                 b = w < s.static_n ? (long long)(s.start + w) : ptb_claim_gated(s);
@@ -608,7 +610,9 @@ k_gemm(const __grid_constant__ GemmParams p, const ShapeArgs s) {
               if (s.start + s.static_n >= s.total && !try_pop) {
                 pre = (long long)s.total;
               } else if (try_pop) {
-                pre = ptb_pop(s);
+                int cnt = 1;
+                pre = ptb_pop_range(s, cnt);
+                if (pre >= 0 && cnt > 1) ptb_return_range(s, pre + 1, cnt - 1);
                 if (pre < 0) { try_pop = false; pre = ptb_claim_gated(s); }
               } else {
                 pre = ptb_claim_gated(s);

@@ -192,7 +192,7 @@ __device__ __forceinline__ float gelu_erf_grad(float x) {   // BERT "gelu": x * 
 
 struct GeluBwd {
   static constexpr int kThreads = 256;
-  static constexpr int kVec = 4;
+  static constexpr int kVec = 4;   // (8 measured slower untransformed: 33 -> 48 us per BERT-large launch)
   struct Params {
     const uint4* g;
     const uint4* pre;
@@ -223,8 +223,18 @@ struct GeluBwd {
 };
 
 // ---------------------------------------------------------------- causal softmax
+// One HBM pass per row: each lane holds its float4s of the row in registers
+// (V = ceil(T / 128) per row), R rows per warp with all their loads issued
+// before any arithmetic (R * V 16 B loads in flight per lane); R * V = 16
+// (forward) / 8 (backward) keeps the register budget fixed, so a logical
+// block is 8 * R rows: T = 512 -> 32 (forward) / 16 (backward) rows.
+constexpr int softmax_v(int T) { return T <= 512 ? 4 : T <= 1024 ? 8 : 16; }
+constexpr int softmax_rpw(int T, int budget) { return budget / softmax_v(T) > 0 ? budget / softmax_v(T) : 1; }
+
 struct SoftmaxCausal {
   static constexpr int kThreads = 256;
+  static constexpr int kMinBlocks = 2;  // <= 128 registers: two CTAs (16 warps) per SM
+  static constexpr int kBudget = 16;   // float4 registers per lane
   struct Params {
     const float* s;          // [rows, T] scores (fp32 GEMM output)
     __nv_bfloat16* p;        // [rows, T] probabilities (0 past the diagonal)
@@ -233,50 +243,83 @@ struct SoftmaxCausal {
     float scale;
     int causal;              // 0: every key visible (BERT encoder)
   };
-  static __device__ __forceinline__ void run(const Params& p, uint3 bidx, uint3, char*) {
-    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    const long long r = (long long)bidx.x * kRowsPerBlock + warp;
-    if (r >= p.rows) return;
-    const int i = p.causal ? (int)(r % p.T) : p.T - 1;   // keys 0..i are visible
-    const float* sr = p.s + r * p.T;
-    float m = -INFINITY;
-    for (int j = lane * 4; j <= i; j += 128) {
-      const float4 v = __ldg(reinterpret_cast<const float4*>(sr + j));
-      const float a[4] = {v.x, v.y, v.z, v.w};
+  template <int V, int R>
+  static __device__ __forceinline__ void rows_(const Params& p, long long r0) {
+    const int lane = threadIdx.x & 31;
+    float4 a[R][V];
+    int vis[R];
 #pragma unroll
-      for (int e = 0; e < 4; ++e)
-        if (j + e <= i) m = fmaxf(m, a[e] * p.scale);
-    }
-    m = warp_max(m);
-    float sum = 0.f;
-    for (int j = lane * 4; j <= i; j += 128) {
-      const float4 v = __ldg(reinterpret_cast<const float4*>(sr + j));
-      const float a[4] = {v.x, v.y, v.z, v.w};
+    for (int rr = 0; rr < R; ++rr) {
+      const long long r = r0 + rr;
+      vis[rr] = r < p.rows ? (p.causal ? (int)(r % p.T) : p.T - 1) : -1;   // keys 0..vis are visible
+      const float* sr = p.s + (r < p.rows ? r : 0) * p.T;
 #pragma unroll
-      for (int e = 0; e < 4; ++e)
-        if (j + e <= i) sum += __expf(a[e] * p.scale - m);
-    }
-    const float inv = 1.f / warp_sum(sum);
-    __nv_bfloat16* pr = p.p + r * p.T;
-    for (int j = lane * 4; j < p.T; j += 128) {
-      float o[4] = {0.f, 0.f, 0.f, 0.f};
-      if (j <= i) {
-        const float4 v = __ldg(reinterpret_cast<const float4*>(sr + j));
-        const float a[4] = {v.x, v.y, v.z, v.w};
-#pragma unroll
-        for (int e = 0; e < 4; ++e) o[e] = (j + e <= i) ? __expf(a[e] * p.scale - m) * inv : 0.f;
+      for (int k = 0; k < V; ++k) {
+        const int j = 4 * (lane + 32 * k);
+        a[rr][k] = (j <= vis[rr] && j < p.T) ? __ldg(reinterpret_cast<const float4*>(sr + j))
+                                             : make_float4(0.f, 0.f, 0.f, 0.f);
       }
-      __nv_bfloat162 h0 = __floats2bfloat162_rn(o[0], o[1]), h1 = __floats2bfloat162_rn(o[2], o[3]);
-      uint2 w;
-      w.x = *reinterpret_cast<uint32_t*>(&h0);
-      w.y = *reinterpret_cast<uint32_t*>(&h1);
-      *reinterpret_cast<uint2*>(pr + j) = w;
+    }
+#pragma unroll
+    for (int rr = 0; rr < R; ++rr) {
+      if (vis[rr] < 0) continue;   // warp-uniform (rows past the end)
+      const long long r = r0 + rr;
+      float m = -INFINITY;
+#pragma unroll
+      for (int k = 0; k < V; ++k) {
+        const int j = 4 * (lane + 32 * k);
+        const float e[4] = {a[rr][k].x, a[rr][k].y, a[rr][k].z, a[rr][k].w};
+#pragma unroll
+        for (int q = 0; q < 4; ++q)
+          if (j + q <= vis[rr] && j + q < p.T) m = fmaxf(m, e[q] * p.scale);
+      }
+      m = warp_max(m);
+      float sum = 0.f;
+#pragma unroll
+      for (int k = 0; k < V; ++k) {
+        const int j = 4 * (lane + 32 * k);
+        float* e = reinterpret_cast<float*>(&a[rr][k]);
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+          e[q] = (j + q <= vis[rr] && j + q < p.T) ? __expf(e[q] * p.scale - m) : 0.f;
+          sum += e[q];
+        }
+      }
+      const float inv = 1.f / warp_sum(sum);
+      __nv_bfloat16* pr = p.p + r * p.T;
+#pragma unroll
+      for (int k = 0; k < V; ++k) {
+        const int j = 4 * (lane + 32 * k);
+        if (j >= p.T) continue;
+        __nv_bfloat162 h0 = __floats2bfloat162_rn(a[rr][k].x * inv, a[rr][k].y * inv);
+        __nv_bfloat162 h1 = __floats2bfloat162_rn(a[rr][k].z * inv, a[rr][k].w * inv);
+        uint2 w;
+        w.x = *reinterpret_cast<uint32_t*>(&h0);
+        w.y = *reinterpret_cast<uint32_t*>(&h1);
+        *reinterpret_cast<uint2*>(pr + j) = w;
+      }
     }
   }
+  static __device__ __forceinline__ void run(const Params& p, uint3 bidx, uint3, char*) {
+    const int warp = threadIdx.x >> 5;
+    if (p.T <= 512) {
+      constexpr int R = softmax_rpw(512, kBudget);
+      rows_<4, R>(p, ((long long)bidx.x * 8 + warp) * R);
+    } else if (p.T <= 1024) {
+      constexpr int R = softmax_rpw(1024, kBudget);
+      rows_<8, R>(p, ((long long)bidx.x * 8 + warp) * R);
+    } else {
+      constexpr int R = softmax_rpw(2048, kBudget);
+      rows_<16, R>(p, ((long long)bidx.x * 8 + warp) * R);
+    }
+  }
+  static long long rows_per_block(int T) { return 8ll * softmax_rpw(T, kBudget); }
 };
 
 struct SoftmaxCausalBwd {
   static constexpr int kThreads = 256;
+  static constexpr int kMinBlocks = 2;
+  static constexpr int kBudget = 8;    // (float4 + bf16x4) register pairs per lane
   struct Params {
     const __nv_bfloat16* p;  // [rows, T]
     const float* dp;         // [rows, T] (fp32 GEMM output)
@@ -286,42 +329,64 @@ struct SoftmaxCausalBwd {
     float scale;
     int causal;
   };
-  static __device__ __forceinline__ void run(const Params& p, uint3 bidx, uint3, char*) {
-    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    const long long r = (long long)bidx.x * kRowsPerBlock + warp;
-    if (r >= p.rows) return;
-    const int i = p.causal ? (int)(r % p.T) : p.T - 1;
-    const __nv_bfloat16* pr = p.p + r * p.T;
-    const float* dr = p.dp + r * p.T;
-    float dot = 0.f;
-    for (int j = lane * 4; j <= i; j += 128) {
-      const uint2 w = *reinterpret_cast<const uint2*>(pr + j);
-      const float2 a = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&w.x));
-      const float2 b = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&w.y));
-      const float4 d = __ldg(reinterpret_cast<const float4*>(dr + j));
-      dot += a.x * d.x + a.y * d.y + b.x * d.z + b.y * d.w;   // P is 0 past the diagonal
-    }
-    dot = warp_sum(dot);
-    __nv_bfloat16* sr = p.ds + r * p.T;
-    for (int j = lane * 4; j < p.T; j += 128) {
-      float o[4] = {0.f, 0.f, 0.f, 0.f};
-      if (j <= i) {
-        const uint2 w = *reinterpret_cast<const uint2*>(pr + j);
-        const float2 a = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&w.x));
-        const float2 b = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&w.y));
-        const float4 d = __ldg(reinterpret_cast<const float4*>(dr + j));
-        o[0] = a.x * (d.x - dot) * p.scale;
-        o[1] = a.y * (d.y - dot) * p.scale;
-        o[2] = b.x * (d.z - dot) * p.scale;
-        o[3] = b.y * (d.w - dot) * p.scale;
+  template <int V, int R>
+  static __device__ __forceinline__ void rows_(const Params& p, long long r0) {
+    const int lane = threadIdx.x & 31;
+    float4 d[R][V];
+    uint2 pv[R][V];
+    int vis[R];
+#pragma unroll
+    for (int rr = 0; rr < R; ++rr) {
+      const long long r = r0 + rr;
+      vis[rr] = r < p.rows ? (p.causal ? (int)(r % p.T) : p.T - 1) : -1;
+      const long long ro = (r < p.rows ? r : 0) * p.T;
+#pragma unroll
+      for (int k = 0; k < V; ++k) {
+        const int j = 4 * (lane + 32 * k);
+        const bool ok = j <= vis[rr] && j < p.T;
+        d[rr][k] = ok ? __ldg(reinterpret_cast<const float4*>(p.dp + ro + j)) : make_float4(0.f, 0.f, 0.f, 0.f);
+        pv[rr][k] = ok ? __ldg(reinterpret_cast<const uint2*>(p.p + ro + j)) : make_uint2(0u, 0u);
       }
-      __nv_bfloat162 h0 = __floats2bfloat162_rn(o[0], o[1]), h1 = __floats2bfloat162_rn(o[2], o[3]);
-      uint2 w;
-      w.x = *reinterpret_cast<uint32_t*>(&h0);
-      w.y = *reinterpret_cast<uint32_t*>(&h1);
-      *reinterpret_cast<uint2*>(sr + j) = w;
+    }
+#pragma unroll
+    for (int rr = 0; rr < R; ++rr) {
+      if (vis[rr] < 0) continue;
+      const long long r = r0 + rr;
+      float dot = 0.f;   // P is 0 past the diagonal
+#pragma unroll
+      for (int k = 0; k < V; ++k) {
+        const float2 a = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&pv[rr][k].x));
+        const float2 b = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&pv[rr][k].y));
+        dot += a.x * d[rr][k].x + a.y * d[rr][k].y + b.x * d[rr][k].z + b.y * d[rr][k].w;
+      }
+      dot = warp_sum(dot);
+      __nv_bfloat16* sr = p.ds + r * p.T;
+#pragma unroll
+      for (int k = 0; k < V; ++k) {
+        const int j = 4 * (lane + 32 * k);
+        if (j >= p.T) continue;
+        const float2 a = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&pv[rr][k].x));
+        const float2 b = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&pv[rr][k].y));
+        __nv_bfloat162 h0 = __floats2bfloat162_rn(a.x * (d[rr][k].x - dot) * p.scale, a.y * (d[rr][k].y - dot) * p.scale);
+        __nv_bfloat162 h1 = __floats2bfloat162_rn(b.x * (d[rr][k].z - dot) * p.scale, b.y * (d[rr][k].w - dot) * p.scale);
+        uint2 w;
+        w.x = *reinterpret_cast<uint32_t*>(&h0);
+        w.y = *reinterpret_cast<uint32_t*>(&h1);
+        *reinterpret_cast<uint2*>(sr + j) = w;
+      }
     }
   }
+  static __device__ __forceinline__ void run(const Params& p, uint3 bidx, uint3, char*) {
+    const int warp = threadIdx.x >> 5;
+    if (p.T <= 512) {
+      constexpr int R = softmax_rpw(512, kBudget);
+      rows_<4, R>(p, ((long long)bidx.x * 8 + warp) * R);
+    } else {   // T <= 1024 (bind)
+      constexpr int R = softmax_rpw(1024, kBudget);
+      rows_<8, R>(p, ((long long)bidx.x * 8 + warp) * R);
+    }
+  }
+  static long long rows_per_block(int T) { return 8ll * softmax_rpw(T, kBudget); }
 };
 
 // ---------------------------------------------------------------- embedding
@@ -456,11 +521,12 @@ static int bind_softmax_causal(const tally_kernel_args* a, Instance* inst) {
   p.T = (int)a->i[1];
   p.scale = (float)a->f[0];
   p.causal = a->i[2] ? 1 : 0;
-  if (!p.s || !p.p || p.rows < 1 || p.T < 4 || p.T % 4 || p.rows % p.T) {
-    set_error("softmax_causal: need s, p, T %% 4 == 0, rows a multiple of T");
+  if (!p.s || !p.p || p.rows < 1 || p.T < 4 || p.T % 4 || p.T > 2048 || p.rows % p.T) {
+    set_error("softmax_causal: need s, p, T %% 4 == 0, T <= 2048, rows a multiple of T");
     return TALLY_EINVAL;
   }
-  tf_finish(inst, p, (p.rows + 7) / 8, 0, 6.0 * (double)p.rows * p.T);
+  const long long rpb = tf::SoftmaxCausal::rows_per_block(p.T);
+  tf_finish(inst, p, (p.rows + rpb - 1) / rpb, 0, 6.0 * (double)p.rows * p.T);
   return TALLY_OK;
 }
 
@@ -474,11 +540,12 @@ static int bind_softmax_causal_bwd(const tally_kernel_args* a, Instance* inst) {
   p.T = (int)a->i[1];
   p.scale = (float)a->f[0];
   p.causal = a->i[2] ? 1 : 0;
-  if (!p.p || !p.dp || !p.ds || p.rows < 1 || p.T < 4 || p.T % 4 || p.rows % p.T) {
-    set_error("softmax_causal_bwd: need p, dp, ds, T %% 4 == 0, rows a multiple of T");
+  if (!p.p || !p.dp || !p.ds || p.rows < 1 || p.T < 4 || p.T % 4 || p.T > 1024 || p.rows % p.T) {
+    set_error("softmax_causal_bwd: need p, dp, ds, T %% 4 == 0, T <= 1024, rows a multiple of T");
     return TALLY_EINVAL;
   }
-  tf_finish(inst, p, (p.rows + 7) / 8, 0, 8.0 * (double)p.rows * p.T);
+  const long long rpb = tf::SoftmaxCausalBwd::rows_per_block(p.T);
+  tf_finish(inst, p, (p.rows + rpb - 1) / rpb, 0, 8.0 * (double)p.rows * p.T);
   return TALLY_OK;
 }
 

@@ -379,6 +379,7 @@ int Runtime::launch(int kernel, int stream, const tally_launch_desc* d, int* out
       pa.ret_ring = nullptr;
       pa.ret_pending = 0;
       pa.static_n = 0;
+      pa.claim_n = 1;
       if ((kk.tmem_cols == 0 || kk.ret_ring) && !kk.copy) {
         // generic k_ptb workers and claim-ahead GEMM workers: the instance's
         // return ring (bounded retirement)
@@ -404,6 +405,16 @@ int Runtime::launch(int kernel, int stream, const tally_launch_desc* d, int* out
         if (mi.ret_pending == 0 && d->preempt_at < 0 && (unsigned long long)d->start_count < total)
           pa.static_n = std::min<unsigned long long>((unsigned long long)(d->workers / std::max(1, kk.cluster)),
                                                      total - (unsigned long long)d->start_count);
+        // batched claims for generic workers with many short blocks each:
+        // ~8+ blocks per worker -> up to 4 per claim, bounded so that every
+        // worker's handed-back blocks (< 2 batches) fit the return ring
+        if (kk.tmem_cols == 0 && d->preempt_at < 0) {
+          const unsigned long long left = total - std::min<unsigned long long>(total, (unsigned long long)d->start_count);
+          const unsigned long long per = left / (unsigned long long)std::max(1, d->workers);
+          int cn = (int)std::min<unsigned long long>(4ull, std::max<unsigned long long>(1ull, per / 8ull));
+          while (cn > 1 && (unsigned long long)d->workers * (2ull * cn - 1ull) > kRetCap) --cn;
+          pa.claim_n = cn;
+        }
       }
       pa.grp = d_groups + (size_t)rec * kMaxExitGroups;
       if (d->workers > kMaxExitGroups * kExitGroupSize) {

@@ -121,6 +121,11 @@ struct PtbArgs {
   // the block back); dynamic claims continue from start + static_n.
   unsigned long long static_n;
   ExitGroup* grp;                  // this launch's exit groups [kMaxExitGroups]
+  // Batched claims (k_ptb): one atomic claims claim_n consecutive blocks (the
+  // L2 serialises same-address atomics: ~2 ns each, so 1184 workers claiming
+  // 1-2 us blocks one at a time were claim-throughput bound); the flag is
+  // still checked between blocks and unrun blocks of a batch are handed back.
+  int claim_n;
 };
 
 constexpr unsigned kRetCap = 8192;   // >= the most resident workers of any launch (148 x 32)
@@ -410,8 +415,12 @@ __device__ __forceinline__ long long ptb_claim_gated(const PtbArgs& a) {
   return task;
 }
 
-// A block an earlier launch of the chain handed back; -1 when none is left.
-__device__ __forceinline__ long long ptb_pop(const PtbArgs& a) {
+// Return-ring entries are ranges of consecutive blocks: (first + 1) | (count << 48)
+// -- a worker hands back at most two (the rest of its batch, the pre-claimed
+// next batch), so the ring holds <= 2 entries per worker and one pop takes a
+// whole range.
+// A range an earlier launch of the chain handed back; -1 when none is left.
+__device__ __forceinline__ long long ptb_pop_range(const PtbArgs& a, int& count) {
   unsigned long long* ring = a.ret_ring;
   for (;;) {
     const unsigned long long h = atomicAdd(ring + 1, 0ull), t = atomicAdd(ring, 0ull);
@@ -421,27 +430,36 @@ __device__ __forceinline__ long long ptb_pop(const PtbArgs& a) {
     unsigned long long v;
     while ((v = *e) == 0ull) __nanosleep(32);
     *e = 0ull;
-    return (long long)v - 1;
+    count = (int)(v >> 48);
+    return (long long)(v & 0xFFFFFFFFFFFFull) - 1;
   }
 }
-
-__device__ __forceinline__ void ptb_return(const PtbArgs& a, long long task) {
+__device__ __forceinline__ void ptb_return_range(const PtbArgs& a, long long first, long long count) {
+  if (count <= 0) return;
   const unsigned long long i = atomicAdd(a.ret_ring, 1ull);
-  reinterpret_cast<volatile unsigned long long*>(a.ret_ring)[2 + (i % kRetCap)] = (unsigned long long)task + 1ull;
+  reinterpret_cast<volatile unsigned long long*>(a.ret_ring)[2 + (i % kRetCap)] =
+      ((unsigned long long)first + 1ull) | ((unsigned long long)count << 48);
+}
+__device__ __forceinline__ void ptb_return(const PtbArgs& a, long long task) { ptb_return_range(a, task, 1); }
+
+// Claim-ahead of a batch of n blocks (flag read separately, see k_ptb).
+__device__ __forceinline__ long long ptb_claim_batch_gated(const PtbArgs& a, int n) {
+  if (n <= 1) return ptb_claim_gated(a);
+  ptb_hold_while_paused(a);
+  const unsigned long long c = atomicAdd(&a.rec->claims, (unsigned long long)n);
+  return (long long)(a.start + a.static_n + c);
 }
 
-// The next block of a k_ptb worker: a handed-back one while the host says
-// some are pending (flag first, as for a claim), else a fresh claim.
-__device__ __forceinline__ long long ptb_next(const PtbArgs& a, bool& try_pop) {
+// The next batch of a k_ptb worker: one handed-back block while the host
+// says some are pending (count 1), else a fresh claim of n blocks.
+__device__ __forceinline__ long long ptb_take(const PtbArgs& a, bool& try_pop, int n, int& count) {
   if (try_pop) {
-    ptb_hold_while_paused(a);
-    const unsigned f = a.flag_is_host ? ld_acquire_sys(a.flag) : ld_acquire_gpu(a.flag);
-    if (ptb_park_requested(a, f)) return -1;
-    const long long t = ptb_pop(a);
+    const long long t = ptb_pop_range(a, count);
     if (t >= 0) return t;
     try_pop = false;
   }
-  return ptb_claim<false>(a);
+  count = n;
+  return ptb_claim_batch_gated(a, n);
 }
 
 // Batched claim: n consecutive task indices with one flag-gated atomic.
@@ -467,12 +485,12 @@ __device__ __forceinline__ unsigned smid() {
   return r;
 }
 
-// Persistent worker loop.  The leader claims task i+1 while the CTA executes
-// task i (claim-ahead), so the flag load and the L2 atomic overlap the body
-// instead of serialising with it.  Retirement stays bounded by one logical
-// block: after block i the leader re-reads the flag, and if it rose meanwhile
-// the pre-claimed block i+1 is handed back through the return ring (encoded
-// as -(task + 2) in the broadcast) instead of being run.
+// Persistent worker loop.  The leader claims the next batch while the CTA
+// executes the last block of the current one (claim-ahead), so the L2 atomic
+// overlaps the body instead of serialising with it.  Retirement stays bounded
+// by one logical block: after every block the leader re-reads the flag, and
+// if it rose meanwhile every claimed-but-unrun block (the rest of the batch,
+// the pre-claimed next batch) is handed back through the return ring.
 template <class Body>
 __global__ void __launch_bounds__(Body::kThreads, MinBlocks<Body>::value)
 k_ptb(const typename Body::Params p, const PtbArgs a) {
@@ -482,25 +500,42 @@ k_ptb(const typename Body::Params p, const PtbArgs a) {
   const unsigned long long t_entry = leader ? globaltimer() : 0ull;
   bool stopped = false;
   bool try_pop = a.ret_ring != nullptr && a.ret_pending > 0;
+  const int n = a.claim_n > 1 ? a.claim_n : 1;
   // the static blocks cover the rest of the kernel: no claim (it could only
   // fail) and no end-of-block flag read (nothing is pre-claimed)
   const bool covered = a.static_n > 0 && a.start + a.static_n >= a.total;
   unsigned long long done = 0;
-  long long next = 0;
+  long long cur = 0, end = 0;   // leader: unrun blocks [cur, end) of the current batch
+  long long pre = -1;           // leader: first block of the pre-claimed next batch (-1: not claimed yet)
+  int pre_cnt = 0;
   if (leader) {
     if (blockIdx.x < a.static_n) {
       // static first block: no claim round trip, the flag still gates it
       const unsigned f = a.flag_is_host ? ld_acquire_sys(a.flag) : ld_acquire_gpu(a.flag);
       const long long mine = (long long)(a.start + blockIdx.x);
       s_task[0] = ptb_park_requested(a, f) ? -mine - 2 : mine;
+    } else if (covered) {
+      s_task[0] = (long long)a.total;   // surplus worker: nothing left
     } else {
-      s_task[0] = covered ? (long long)a.total : ptb_next(a, try_pop);   // surplus worker: nothing left
+      ptb_hold_while_paused(a);
+      const unsigned f = a.flag_is_host ? ld_acquire_sys(a.flag) : ld_acquire_gpu(a.flag);
+      if (ptb_park_requested(a, f)) {
+        s_task[0] = -1;   // flag before the first claim: nothing claimed
+      } else {
+        int cnt = 1;
+        const long long b = ptb_take(a, try_pop, n, cnt);
+        if (a.preempt_at >= 0 && b < a.preempt_at && a.preempt_at <= b + cnt)
+          st_release_sys(const_cast<unsigned*>(a.flag), a.park_at);   // test trigger (MemTrigger)
+        s_task[0] = b;
+        cur = b + 1;
+        end = b + cnt;
+      }
     }
   }
   __syncthreads();
   for (unsigned it = 0;; ++it) {
     const long long task = s_task[it & 1];
-    if (task < -1) {   // the flag rose before this block started: hand it back
+    if (task < -1) {   // the flag rose before this (static) block started: hand it back
       if (leader) ptb_return(a, -task - 2);
       stopped = true;
       break;
@@ -510,20 +545,38 @@ k_ptb(const typename Body::Params p, const PtbArgs a) {
       break;
     }
     if (leader) {
-      // in flight while the body runs (the flag was clear when this block began)
-      next = covered ? (long long)a.total : try_pop ? ptb_next(a, try_pop) : ptb_claim_gated(a);
+      // the last block of this batch: claim the next batch while it runs
+      // (the flag was clear when this block began)
+      if (!covered && cur >= end && pre < 0) {
+        pre = ptb_take(a, try_pop, n, pre_cnt);
+        if (a.preempt_at >= 0 && pre < a.preempt_at && a.preempt_at <= pre + pre_cnt)
+          st_release_sys(const_cast<unsigned*>(a.flag), a.park_at);   // test trigger (MemTrigger)
+      }
       if (a.exec_count != nullptr) atomicAdd(&a.exec_count[task], 1ull);
     }
     const unsigned long long t0 = (leader && a.block_log != nullptr) ? globaltimer() : 0ull;
     Body::run(p, delinearize((unsigned long long)task, a.grid), a.grid, smem);
     ++done;
     if (leader) {
-      // bounded retirement: a flag raised while this block ran hands the
-      // pre-claimed block back instead of running it
-      long long nx = next;
+      long long nx;
+      if (covered) {
+        nx = (long long)a.total;
+      } else if (cur < end) {
+        nx = cur++;
+      } else {
+        nx = pre;
+        cur = pre + 1;
+        end = pre + pre_cnt;
+        pre = -1;
+      }
       if (nx >= 0 && (unsigned long long)nx < a.total) {
+        // bounded retirement: a flag raised while this block ran hands every
+        // claimed-but-unrun block back instead of running it
         const unsigned f = a.flag_is_host ? ld_relaxed_sys(a.flag) : ld_relaxed_gpu(a.flag);
-        if (ptb_park_requested(a, f)) nx = -nx - 2;
+        if (ptb_park_requested(a, f)) {
+          ptb_return_range(a, nx, min(end, (long long)a.total) - nx);
+          nx = -1;
+        }
       }
       s_task[(it + 1) & 1] = nx;
     }

@@ -33,14 +33,16 @@ def _pair_plan(M, N, Kdim, enabled=True):
     """(pair, splits) for a linear-layer GEMM.  CTA-pair tiles (256 x 256,
     ``*_x2`` kinds) when N % 256 == 0 and there are >= 64 of them (most of
     the 74 SM pairs busy without split-K); their logical blocks are capped at
-    ~270 MFLOP (~13 us on a pair -- the preemption granularity the 40 MFLOP
-    single-CTA cap gives at half the per-SM rate).  Otherwise single-CTA
-    tiles with ``resnet._gemm_splits``."""
+    ~180 MFLOP (~8 us on a pair), so K = 3072 / 4096 GEMMs split three ways:
+    at 270 MFLOP their PTB(148) Eq. 1 estimate sat at the 31.6 us threshold
+    and measurement noise sometimes sent the tuner to its least-turnaround
+    fallback (a 1/128 slicing).  Otherwise single-CTA tiles with
+    ``resnet._gemm_splits``."""
     tiles = math.ceil(M / 256) * (N // 256) if N % 256 == 0 else 0
     if not enabled or tiles < 64:
         return False, _gemm_splits(M, N, Kdim)
     kb = math.ceil(Kdim / 64)
-    s = max(1, min(kb // 2, math.ceil(2.0 * 256 * 256 * Kdim / 270e6)))
+    s = max(1, min(kb // 2, math.ceil(2.0 * 256 * 256 * Kdim / 180e6)))
     return True, math.ceil(kb / math.ceil(kb / s))
 
 

@@ -1,7 +1,8 @@
 """Transformation cost per kernel kind on the B200 (diagnostics, not the bench
 contract): every kernel of a configuration's training step launched
 untransformed and as PTB at full resident occupancy, each launch timed alone
-with CUDA events (L2 not flushed: the step's own order warms it), summed per
+with CUDA events behind a queued spin kernel (device time, not the host's
+launch latency; L2 not flushed: the step's own order warms it), summed per
 kind; PTB / Original time per kind is the inverse of the "transformed kernel
 at >= 0.90 of untransformed" target.
 
@@ -49,9 +50,19 @@ def main():
     ap.add_argument("--reps", type=int, default=3)
     ap.add_argument("--out", default=None)
     ap.add_argument("--chosen", action="store_true", help="also time the tuner's chosen shape of every kernel")
+    ap.add_argument("--no-spin", action="store_true",
+                    help="time launches on an idle stream (the events then include the host's launch latency)")
     args = ap.parse_args()
     P.B200Device.get(0)
     s = kernels.Stream(high_priority=False)
+    # a short spin queued ahead of every timed launch: the launch and its
+    # events are enqueued before the GPU reaches them, so the events time the
+    # device (as in a step, where the runtime keeps launches queued ahead)
+    spin = kernels.spin(148, 32, 15_000)
+
+    def ahead():
+        if not args.no_spin:
+            spin.original(s)
     tr = program(args.config)
     tr.step_original(s)
     tr.step_original(s)
@@ -61,10 +72,12 @@ def main():
     n = collections.Counter()
     for _ in range(args.reps):
         for name, dk in tr.program:
+            ahead()
             L = dk.original(s, timed=True)
             L.wait()
             orig[dk.kind] += L.elapsed_ns / 1e3 / args.reps
-            w = min(dk.total_blocks, 148 * max(1, dk.info.occupancy_ptb))
+            w = min(dk.total_blocks * dk.info.cluster, 148 * max(1, dk.info.occupancy_ptb))
+            ahead()
             L = dk.ptb(s, w, timed=True)
             L.wait()
             ptb[dk.kind] += L.elapsed_ns / 1e3 / args.reps
@@ -81,6 +94,7 @@ def main():
                 prof.bind(sig, dk)
                 w = P.KernelWork(sig, dk.cost(), kernel=dk)
                 c = prof.select(w.profile_key(), w.cost, 31_600)
+                ahead()
                 if c.variant == "Ptb":
                     L = dk.ptb(s, c.worker_count, timed=True)
                     L.wait()
