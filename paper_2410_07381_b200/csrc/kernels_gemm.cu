@@ -293,7 +293,7 @@ using CfgTf32x3N64 = CfgTf32x3T<64, 4>;
 #define TALLY_STAGES_BF16_N128 2
 #endif
 #ifndef TALLY_STAGES_F32_N128
-#define TALLY_STAGES_F32_N128 3
+#define TALLY_STAGES_F32_N128 2   // (+ 32 KB of fp32 staging for the TMA-store epilogue, two CTAs per SM)
 #endif
 #ifndef TALLY_STAGES_BF16_N64
 #define TALLY_STAGES_BF16_N64 3
@@ -324,7 +324,7 @@ struct CfgBf16T {
   // untransformed launch (one output tile per CTA) overlaps one CTA's
   // prologue / pipeline fill with the other's tile, and high-priority CTAs
   // find room next to a best-effort one.  Pairs: one CTA per SM, a deep ring.
-  static constexpr int STAGES = PAIR == 2 ? (sizeof(OutT_) == 2 ? TALLY_STAGES_PAIR : TALLY_STAGES_PAIR + 1)
+  static constexpr int STAGES = PAIR == 2 ? TALLY_STAGES_PAIR
                               : BN == 128 ? (sizeof(OutT_) == 2 ? TALLY_STAGES_BF16_N128 : TALLY_STAGES_F32_N128)
                                           : (sizeof(OutT_) == 2 ? TALLY_STAGES_BF16_N64 : TALLY_STAGES_F32_N64);
   static constexpr int UMMA_K = 16;
@@ -339,7 +339,10 @@ struct CfgBf16T {
   using OutT = OutT_;
   // bf16 output: each epilogue warp stages 32 rows x 64 columns at a time in
   // shared memory (XOR-swizzled 16 B chunks) and writes whole row segments
-  static constexpr int EPI_BYTES = sizeof(OutT_) == 2 ? 8 * 32 * 64 * 2 : 0;   // 4 KB per epilogue warp (32 KB)
+  // fp32 output (128/256-wide tiles): each warp stages 32 rows x 32 columns
+  // (4 KB) for a TMA tensor store -- the per-lane row stores of fp32 tiles
+  // were L1/LSU-bound (ncu: attention score GEMM at 1.6 TB/s of DRAM, L1 61 %)
+  static constexpr int EPI_BYTES = (sizeof(OutT_) == 2 || BN_ >= 128) ? 8 * 32 * 64 * 2 : 0;   // 4 KB per epilogue warp
 };
 using CfgBf16 = CfgBf16T<128, __nv_bfloat16>;
 using CfgBf16N64 = CfgBf16T<64, __nv_bfloat16>;
@@ -1070,11 +1073,30 @@ k_gemm(const __grid_constant__ GemmParams p, const ShapeArgs s) {
           }
           if (!last) {
             tmem_st32(lane_base + (uint32_t)(2 * Cfg::BN + c1), r);
-          } else if (!row_ok) {
           } else if constexpr (sizeof(typename Cfg::OutT) == 4) {
+            if (Cfg::KIND == 1 && p.c_tma == 2) {
+              // stage this warp's 32 x 32 fp32 box (128B-swizzle layout) and
+              // store it with one TMA tensor store; rows past M are clipped by
+              // the map (bind enables this only where that is exact)
+              unsigned char* wst = epi_smem + (size_t)(warp - 2) * 4096;
+              if (lane == 0) asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
+              __syncwarp();
+              unsigned char* srow = wst + (size_t)lane * 128;
 #pragma unroll
-            for (int v = 0; v < 8; ++v)
-              st_out16(crow + c1 + 4 * v, make_uint4(r[4 * v], r[4 * v + 1], r[4 * v + 2], r[4 * v + 3]));
+              for (int v = 0; v < 8; ++v)
+                *reinterpret_cast<uint4*>(srow + ((v ^ (lane & 7)) << 4)) =
+                    make_uint4(r[4 * v], r[4 * v + 1], r[4 * v + 2], r[4 * v + 3]);
+              asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+              __syncwarp();
+              if (lane == 0)
+                tma_store_2d(&p.a_lo, smem_u32(wst), cc + w.nb * Cfg::BN + c1,
+                             (int)(w.split * (p.split_stride / p.ldc)) + cr + (w.mb * PR + (int)rank) * Cfg::BM + q * 32);
+            } else if (row_ok) {
+#pragma unroll
+              for (int v = 0; v < 8; ++v)
+                st_out16(crow + c1 + 4 * v, make_uint4(r[4 * v], r[4 * v + 1], r[4 * v + 2], r[4 * v + 3]));
+            }
+          } else if (!row_ok) {
           } else if constexpr (PR == 2) {
             // pair tiles with a strided / batched bf16 C: the row straight from registers
 #pragma unroll
@@ -1133,6 +1155,8 @@ k_gemm(const __grid_constant__ GemmParams p, const ShapeArgs s) {
       __syncwarp();
       if (lane == 0) mbar_arrive(&tile_empty[j]);
     }
+    if (lane == 0) asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");   // (TMA-store epilogue)
+    __syncwarp();
   }
 
   fence_before();
@@ -1318,6 +1342,29 @@ static int bind_gemm(const tally_kernel_args* a, Instance* inst, bool split) {
       int rc = make_map(&p.a_lo, p.c, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, M, N, 32, p.ldc);
       if (rc) return rc;
       p.c_tma = 1;
+    }
+  }
+  if constexpr (Cfg::KIND == 1 && Cfg::BN >= 128 && sizeof(typename Cfg::OutT) == 4) {
+    // fp32 TMA-store epilogue: C seen as one 2-D [rows, ldc] fp32 map that
+    // covers every split and batch origin; rows past M only where the map
+    // clips them exactly (unsplit, unbatched), else M a multiple of the tile
+    const long long tile_rows = (long long)Cfg::BM * gemm::PairOf<Cfg>::value;
+    const long long ss_rows = p.ldc > 0 && p.split_stride % p.ldc == 0 ? p.split_stride / p.ldc : -1;
+    // batch z = (z / hdiv, z % hdiv): origins are linear in both with
+    // non-negative steps, so the largest indices bound every origin
+    const long long zb_max = (p.batches - 1) / p.hdiv, zh_max = std::min(p.hdiv, p.batches) - 1;
+    const long long max_r = p.off[4][0] * zb_max + p.off[4][1] * zh_max;
+    const long long max_c = p.off[5][0] * zb_max + p.off[5][1] * zh_max;
+    bool ok = aligned16_(p.c) && (p.ldc * 4) % 16 == 0 && ss_rows >= 0 && max_c + N <= p.ldc &&
+              !getenv_flag("TALLY_GEMM_NO_TMA_STORE");
+    for (int w = 4; w < 6; ++w) ok = ok && p.off[w][0] >= 0 && p.off[w][1] >= 0;
+    const bool plain = splits == 1 && p.batches == 1 && max_r == 0;
+    ok = ok && (plain || M % tile_rows == 0);
+    if (ok) {
+      const long long rows = plain ? M : (splits - 1) * ss_rows + max_r + M;
+      int rc = make_map(&p.a_lo, p.c, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 4, rows, p.ldc, 32, p.ldc);
+      if (rc) return rc;
+      p.c_tma = 2;
     }
   }
   p.kb_per_split = (int)((KBlocks + splits - 1) / splits);

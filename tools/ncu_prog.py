@@ -45,14 +45,14 @@ def main():
             L = dk.original(s, timed=True)
             L.wait()
             per.append((L.elapsed_ns / 1e3, name, dk.kind))
-        for us, name, kind in sorted(per, reverse=True)[:15]:
+        for us, name, kind in sorted(per, reverse=True)[:40]:
             print(f"{us:9.1f} us  {kind:20s} {name}")
     else:
         progs = dict(tr.program)
         for n in args.names:
             dk = progs[n]
             dk.original(s).wait()
-            dk.ptb(s, min(dk.total_blocks, 148 * max(1, dk.info.occupancy_ptb))).wait()
+            dk.ptb(s, min(dk.total_blocks * dk.info.cluster, 148 * max(1, dk.info.occupancy_ptb))).wait()
     torch.cuda.synchronize()
     print("ncu_prog done:", args.config, args.mode)
 
