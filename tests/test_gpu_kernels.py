@@ -260,3 +260,36 @@ def test_preemption_latency_under_50us(P, stream):
           f"(clock uncertainty {unc / 1000:.1f} us)")
     assert lat[len(lat) // 2] < 50.0
     dk.close()
+
+
+def test_hp_blocks_dominate_queued_be_blocks(P):
+    """Row a17, HP dominance (ref sim.py:370-384: no best-effort block starts
+    while a high-priority launch has unplaced blocks), on the device: a
+    best-effort spin kernel with four waves of blocks queued on the
+    lowest-priority stream, then a high-priority spin kernel with two waves;
+    the hardware CTA scheduler (stream priorities) places every HP block
+    before any further BE block -- from the first HP block's start to the last
+    HP block's start, no BE block starts (block logs on %globaltimer; a
+    handful racing the very first HP dispatch are tolerated)."""
+    import time
+    K = P.kernels
+    lo, hi = K.Stream(high_priority=False), K.Stream(high_priority=True)
+    probe = K.spin(148, 256, 0)
+    slots = 148 * max(1, probe.info.occupancy_original)
+    be = K.spin(4 * slots, 256, 1_000_000)   # 4 waves of 1 ms blocks
+    hp = K.spin(2 * slots, 256, 100_000)
+    for _ in range(2):
+        bl = torch.zeros(be.total_blocks, 3, dtype=torch.int64, device="cuda")
+        hl = torch.zeros(hp.total_blocks, 3, dtype=torch.int64, device="cuda")
+        Lb = be.original(lo, block_log=bl)
+        time.sleep(0.0015)   # the BE kernel's second wave is resident, two more queued
+        Lh = hp.original(hi, block_log=hl)
+        Lh.wait()
+        Lb.wait()
+        b, h = bl.cpu(), hl.cpu()
+        h0, h1 = h[:, 0].min().item(), h[:, 0].max().item()
+        assert b[:, 0].min().item() < h0 < b[:, 0].max().item()   # HP arrived while BE blocks were queued
+        inside = ((b[:, 0] > h0) & (b[:, 0] < h1)).sum().item()
+        assert inside <= 8, (inside, be.total_blocks)
+        # and the HP blocks were not starved: all placed within ~one BE block time
+        assert h1 - h0 < 1_000_000 + 3 * 100_000
