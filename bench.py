@@ -859,7 +859,7 @@ class ClockMap:
 PTB_SHAPE = 2   # tally_launch_record.shape of a PTB launch (include/tally_b200.h)
 
 
-def preempt_latencies_us(res_list, clk, queued=None):
+def preempt_latencies_us(res_list, clk, queued=None, busy=True):
     """Host signal -> last worker exit (ref sim.py:509-517 measured_turnaround:
     max park time - signal, or finish - signal when the preempt came after
     the last claim), for every preempted PTB launch that was running at the
@@ -870,8 +870,12 @@ def preempt_latencies_us(res_list, clk, queued=None):
     (queued behind the high-priority kernels that now hold the SMs) parks
     without running anything -- the reference parks it at the signal
     (sim.py:344-345) -- and its "last exit" only says when the request let it
-    start; those are counted in ``queued[0]`` instead.  Device times mapped
-    to the host clock by ``clk``."""
+    start; those are counted in ``queued[0]`` instead.  ``busy``: the last
+    exit of a worker that ran a block (``gt_last_busy_exit``) -- a worker
+    that was itself launched only after the flag (its SM slot held by the
+    request's CTAs until then) hands its block back and exits without having
+    held anything at the signal; ``busy=False``: every worker's exit.
+    Device times mapped to the host clock by ``clk``."""
     out = []
     for res in res_list:
         for r in res.launches:
@@ -882,7 +886,10 @@ def preempt_latencies_us(res_list, clk, queued=None):
                 if queued is not None:
                     queued[0] += 1
                 continue
-            out.append((r["gt_last_exit"] + clk.off(sig) - sig) / 1e3)
+            last = r["gt_last_exit"]
+            if busy and r.get("gt_last_busy_exit"):
+                last = r["gt_last_busy_exit"]
+            out.append((last + clk.off(sig) - sig) / 1e3)
     return out
 
 
@@ -1115,6 +1122,7 @@ def main_colocate(args):
     clkmap.close()
     n_queued = [0]
     pl_us = preempt_latencies_us(results, clkmap, n_queued)
+    pl_all_us = preempt_latencies_us(results, clkmap, busy=False)
     dr_us = drain_us(results)
     launches = sum(len(r.launches) for r in results)
 
@@ -1290,6 +1298,7 @@ def main_colocate(args):
         "be_frac_same_policy": frac(be_co, be_same_policy),
         "p99_solo_us": p99(solo_lat) / 1e3, "p99_co_us": p99(co_lat) / 1e3,
         "preempt_us": [pct(pl_us, 0.5), pct(pl_us, 0.99), max(pl_us)] if pl_us else None,
+        "preempt_all_us": [pct(pl_all_us, 0.5), pct(pl_all_us, 0.99), max(pl_all_us)] if pl_all_us else None,
         "drain_us": [pct(dr_us, 0.5), pct(dr_us, 0.99)] if dr_us else None, "preemptions": len(pl_us),
         "preemptions_queued": n_queued[0],
         "delta_us": [round(pct(deltas, q) / 1e3, 1) for q in (0.5, 0.9, 0.99, 1.0)] if deltas else None,
@@ -1317,12 +1326,15 @@ def main_colocate(args):
             "hp_busy_fraction": hp_busy,
             "be_throughput_pct_of_idle_ceiling": 100.0 * be_co * native_step_s / max(1e-9, 1.0 - hp_busy),
             "preempt_latency_us_p50_p99_max": worst["preempt_us"],
+            "preempt_latency_all_workers_us_p50_p99_max": worst.get("preempt_all_us"),
             "preempt_drain_us_p50_p99": worst["drain_us"], "preemptions": worst["preemptions"],
             "preemptions_of_queued_launches": worst["preemptions_queued"],
             "request_delta_us_p50_p90_p99_max": worst["delta_us"],
             "window_p99_us_solo_co": worst["window_p99_us_solo_co"],
-            "preempt_note": "host signal -> last worker exit (device clock mapped to host, linear drift "
-                            "correction); drain = first worker stop -> last exit on the device clock",
+            "preempt_note": "host signal -> last exit of a worker that ran a block (device clock mapped to "
+                            "host, linear drift correction; _all_workers: also workers launched only after "
+                            "the flag, which held nothing at the signal); drain = first worker stop -> "
+                            "last exit on the device clock",
             "hp_isolated_latency_us": hp_lat / 1e3,
             "trace_hp_latency_us": trace_lat / 1e3,
             "tuner_choice_histogram": dict(choice_hist), "profiling_s": round(t_prof, 1),

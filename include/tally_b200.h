@@ -209,6 +209,8 @@ typedef struct {
   long long claims;
   long long gt_first_start, gt_first_stop, gt_last_exit;   /* device %globaltimer ns */
   long long host_submit_ns, host_preempt_ns;
+  long long gt_last_busy_exit;  /* PTB: last exit of a worker that ran a block (0 = none / not
+                                   tracked); workers launched only after the flag do not count */
 } tally_launch_state;
 
 int tally_launch(int kernel, int stream, const tally_launch_desc* desc, int* out_launch);
@@ -322,6 +324,7 @@ typedef struct {
   long long gpu_start_ns, gpu_end_ns;  /* GPU timeline (CUDA events vs a run-start reference
                                           event; -1 unless the "trace" option is set)       */
   long long handle;         /* the device handle the runner got from submit (submission order) */
+  long long gt_last_busy_exit;   /* see tally_launch_state */
 } tally_launch_record;
 
 long long tally_device_run_origin_ns(int runner);   /* host ns that event times are relative to */

@@ -84,7 +84,7 @@ class c_launch_state(C.Structure):
                 ("task_counter", C.c_longlong), ("claims", C.c_longlong),
                 ("gt_first_start", C.c_longlong), ("gt_first_stop", C.c_longlong),
                 ("gt_last_exit", C.c_longlong), ("host_submit_ns", C.c_longlong),
-                ("host_preempt_ns", C.c_longlong)]
+                ("host_preempt_ns", C.c_longlong), ("gt_last_busy_exit", C.c_longlong)]
 
 
 class c_cost(C.Structure):
@@ -147,7 +147,7 @@ class c_launch_record(C.Structure):
                 ("gt_first_start", C.c_longlong), ("gt_first_stop", C.c_longlong),
                 ("gt_last_exit", C.c_longlong), ("parked", C.c_int),
                 ("gpu_start_ns", C.c_longlong), ("gpu_end_ns", C.c_longlong),
-                ("handle", C.c_longlong)]
+                ("handle", C.c_longlong), ("gt_last_busy_exit", C.c_longlong)]
 
 
 _SIGNATURES = {

@@ -37,7 +37,7 @@ struct Handle {
   long long task_counter = 0;
   long long finish_time = -1;
   long long submit_ns = 0, issue_ns = 0, complete_ns = 0, preempt_ns = 0;
-  long long gt_first_start = 0, gt_first_stop = 0, gt_last_exit = 0;
+  long long gt_first_start = 0, gt_first_stop = 0, gt_last_exit = 0, gt_last_busy_exit = 0;
   long long count = 0;
   long long gpu_start = -1, gpu_end = -1;
   int kernel_index = -1;   // position of the work in its task's pipeline
@@ -386,6 +386,7 @@ class CudaDevice : public Device {
     h.gt_first_start = L->gt_first_start;
     h.gt_first_stop = L->gt_first_stop;
     h.gt_last_exit = L->gt_last_exit;
+    h.gt_last_busy_exit = L->gt_last_busy_exit;
     --inflight_;
     if (trace_ && L->ev_start && L->ev_end) {
       float ms0 = 0, ms1 = 0;
@@ -434,6 +435,7 @@ class CudaDevice : public Device {
     rec.gpu_start_ns = h.gpu_start;
     rec.gpu_end_ns = h.gpu_end;
     rec.handle = id;
+    rec.gt_last_busy_exit = h.gt_last_busy_exit;
     r_->log.launches.push_back(rec);
   }
 };

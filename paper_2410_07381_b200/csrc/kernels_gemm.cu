@@ -456,6 +456,18 @@ __device__ __forceinline__ int goff(const GemmParams& p, int which, const TileWo
   return (int)(p.off[which][0] * w.zb + p.off[which][1] * w.zh);
 }
 
+__device__ __forceinline__ unsigned long long* block_log_of(const SliceArgs& a) { return a.block_log; }
+__device__ __forceinline__ unsigned long long* block_log_of(const PtbArgs& a) { return a.block_log; }
+// Per-logical-block device events (ref sim.py:156-172 BlockStarted /
+// BlockFinished): start = the block's first MMA issued, end = its last tile's
+// output issued by epilogue warp 2; (worker << 32 | smid).  Leader CTA only.
+__device__ __forceinline__ void gemm_log_end(unsigned long long* log, long long t, const GemmParams& p) {
+  if (log != nullptr && (t % p.tpb == p.tpb - 1 || t == p.total_tiles - 1)) {
+    const long long b = t / p.tpb;
+    log[3 * b + 1] = globaltimer();
+    log[3 * b + 2] = ((unsigned long long)blockIdx.x << 32) | smid();
+  }
+}
 __device__ __forceinline__ const unsigned long long* ret_ring_of(const SliceArgs&) { return nullptr; }
 __device__ __forceinline__ unsigned long long ret_pending_of(const SliceArgs&) { return 0ull; }
 __device__ __forceinline__ const unsigned long long* ret_ring_of(const PtbArgs& a) { return a.ret_ring; }
@@ -781,6 +793,7 @@ k_gemm(const __grid_constant__ GemmParams p, const ShapeArgs s) {
         const TileWork w = tile_w[j];
         if (i == 0 && MODE == kPtb)   // telemetry: first tile in hand (worker_log)
           *reinterpret_cast<volatile unsigned long long*>(tmem_base_slot + 2) = globaltimer();
+        if (block_log_of(s) != nullptr && t % p.tpb == 0) block_log_of(s)[3 * (t / p.tpb)] = globaltimer();
         for (int c = c0; c < w.nch; ++c, ++ci) {
           const int acc = ci & 1;
           if (ci >= 2) {
@@ -923,6 +936,7 @@ k_gemm(const __grid_constant__ GemmParams p, const ShapeArgs s) {
             __syncwarp();
           }
         }
+        if (q == 0 && lane == 0) gemm_log_end(block_log_of(s), t, p);   // (the group's first warp)
       }
       __syncwarp();
       if (lane == 0) mbar_arrive(&tile_empty[j]);
@@ -986,6 +1000,7 @@ k_gemm(const __grid_constant__ GemmParams p, const ShapeArgs s) {
         __syncwarp();
       }
       ++ci;
+      if (warp == 2 && lane == 0 && lead) gemm_log_end(block_log_of(s), t, p);
       if (lane == 0) mbar_arrive(&tile_empty[j]);
     }
     if (lane == 0) asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
@@ -1153,6 +1168,7 @@ k_gemm(const __grid_constant__ GemmParams p, const ShapeArgs s) {
         }
       }
       __syncwarp();
+      if (warp == 2 && lane == 0 && lead) gemm_log_end(block_log_of(s), t, p);
       if (lane == 0) mbar_arrive(&tile_empty[j]);
     }
     if (lane == 0) asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");   // (TMA-store epilogue)

@@ -561,6 +561,7 @@ bool Runtime::poll(Launch* L) {
     L->claims = (long long)m->claims;
     L->gt_first_stop = (long long)m->t_first_stop;
     L->gt_last_exit = (long long)m->t_last_exit;
+    L->gt_last_busy_exit = (long long)m->t_last_busy_exit;
     L->gt_first_start = (long long)m->t_first_start;
     L->parked = (m->status == kMirrorParked);
     L->finished = true;
@@ -588,6 +589,7 @@ void Runtime::fill_state(const Launch* L, tally_launch_state* o) {
   o->gt_first_start = L->gt_first_start;
   o->gt_first_stop = L->gt_first_stop;
   o->gt_last_exit = L->gt_last_exit;
+  o->gt_last_busy_exit = L->gt_last_busy_exit;
   o->host_submit_ns = L->host_submit;
   o->host_preempt_ns = L->host_preempt;
 }

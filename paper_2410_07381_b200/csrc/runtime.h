@@ -36,7 +36,7 @@ struct Launch {
   std::atomic<bool> preempted{false};
   long long start_count = 0, workers = 0, count = 0;
   long long claims = 0;
-  long long gt_first_start = 0, gt_first_stop = 0, gt_last_exit = 0;
+  long long gt_first_start = 0, gt_first_stop = 0, gt_last_exit = 0, gt_last_busy_exit = 0;
   long long host_submit = 0, host_preempt = 0;
   cudaEvent_t ev_start = nullptr, ev_end = nullptr;
   cudaError_t error = cudaSuccess;

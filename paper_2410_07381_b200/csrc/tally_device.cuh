@@ -38,7 +38,8 @@ struct alignas(64) LaunchRec {
   unsigned long long executed;      // logical blocks run by this launch
   unsigned long long stops;         // workers that stopped because of the flag
   unsigned long long neg_first_start;  // ~min worker entry %globaltimer (0 = none yet)
-  unsigned long long pad[2];
+  unsigned long long last_busy_exit;   // max exit %globaltimer of workers that ran a block
+  unsigned long long pad[1];
 };
 
 // Worker retirement is two-level: workers fold into their group of 32
@@ -64,8 +65,12 @@ struct alignas(64) LaunchMirror {
   unsigned long long t_first_start;  // %globaltimer at first worker entry
   unsigned int serial;               // written last: == launch serial when valid
   unsigned int status;               // 1 = exhausted (done), 2 = parked
-  unsigned long long ret_pending;    // logical blocks handed back to the chain (k_ptb), not yet run
-  unsigned long long pad;
+  unsigned long long ret_pending;    // return-ring entries handed back to the chain, not yet run
+  // last exit of a worker that ran a block: a worker that only launched after
+  // the flag (its SM slot was busy with high-priority CTAs until then) reads
+  // the flag, hands its static block back and exits -- it held no resources
+  // at the signal, so it is not part of the preemption latency
+  unsigned long long t_last_busy_exit;
 };
 
 enum : unsigned { kMirrorDone = 1, kMirrorParked = 2 };
@@ -310,7 +315,10 @@ __device__ __forceinline__ void ptb_worker_exit(const PtbArgs& a, bool stopped,
   // fire-and-forget reductions straight into the record: the acq_rel exit
   // counters below order them before the last worker's reads
   atomicMax(&r->neg_first_start, ~t_entry);
-  if (executed) atomicAdd(&r->executed, executed);
+  if (executed) {
+    atomicAdd(&r->executed, executed);
+    atomicMax(&r->last_busy_exit, globaltimer());
+  }
   if (stopped) {
     atomicAdd(&r->stops, 1ull);
     atomicMax(&r->neg_first_stop, ~globaltimer());
@@ -326,6 +334,7 @@ __device__ __forceinline__ void ptb_worker_exit(const PtbArgs& a, bool stopped,
   const unsigned long long nst = ld_relaxed_gpu_u64(&r->neg_first_start);
   const unsigned long long stops = ld_relaxed_gpu_u64(&r->stops);
   const unsigned long long ran = ld_relaxed_gpu_u64(&r->executed);
+  const unsigned long long busy = ld_relaxed_gpu_u64(&r->last_busy_exit);
   const unsigned long long tail = resume_ring ? ld_relaxed_gpu_u64(resume_ring) : 0ull;
   const unsigned long long head = resume_ring ? ld_relaxed_gpu_u64(resume_ring + 1) : 0ull;
   unsigned long long claims = a.static_n + dyn;
@@ -353,6 +362,7 @@ __device__ __forceinline__ void ptb_worker_exit(const PtbArgs& a, bool stopped,
   m->stops = stops;
   m->t_first_start = nst ? ~nst : 0ull;
   m->ret_pending = pending;
+  m->t_last_busy_exit = busy;
   // work can only remain if some worker stopped on the flag
   const bool parked = progress < a.total || pending > 0;
   m->status = parked ? kMirrorParked : kMirrorDone;
@@ -369,6 +379,7 @@ __device__ __forceinline__ void ptb_worker_exit(const PtbArgs& a, bool stopped,
   r->executed = 0ull;
   r->stops = 0ull;
   r->neg_first_start = 0ull;
+  r->last_busy_exit = 0ull;
   st_release_sys(const_cast<unsigned*>(&m->serial), a.serial);
 }
 

@@ -74,12 +74,13 @@ class LaunchState:
     gt_last_exit: int
     host_submit_ns: int
     host_preempt_ns: int
+    gt_last_busy_exit: int = 0   # last exit of a worker that ran a block (late starters excluded)
 
 
 def _state(s: _lib.c_launch_state) -> LaunchState:
     return LaunchState(bool(s.done), bool(s.parked), bool(s.preempted), s.task_counter, s.claims,
                        s.gt_first_start, s.gt_first_stop, s.gt_last_exit, s.host_submit_ns,
-                       s.host_preempt_ns)
+                       s.host_preempt_ns, s.gt_last_busy_exit)
 
 
 class Launch:

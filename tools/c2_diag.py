@@ -129,7 +129,7 @@ def main():
             if r["gt_first_start"] and r["gt_first_start"] + clk.off(sig) >= sig:
                 continue   # parked before any worker started (see bench.preempt_latencies_us)
             kind = be_ws[r["kernel_index"]].kernel_id.split(":")[0] if 0 <= r["kernel_index"] < len(be_ws) else "?"
-            lat = (r["gt_last_exit"] + clk.off(sig) - sig) / 1e3
+            lat = ((r.get("gt_last_busy_exit") or r["gt_last_exit"]) + clk.off(sig) - sig) / 1e3
             drain = (r["gt_last_exit"] - r["gt_first_stop"]) / 1e3 if r["gt_first_stop"] else None
             bykind[kind].append((lat, drain, be_ws[r["kernel_index"]].kernel_id if 0 <= r["kernel_index"] < len(be_ws) else "?"))
         out[label + "_preempt_by_kind"] = {

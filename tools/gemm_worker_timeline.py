@@ -33,10 +33,22 @@ def main():
     out = {"shape": [M, N, K], "kind": dk.kind, "blocks": dk.total_blocks, "workers": W, "runs": []}
     for rep in range(4):
         wl = torch.zeros(W * 4, dtype=torch.int64, device="cuda")
-        L = dk.ptb(s, W, worker_log=wl, timed=True)
+        bl = torch.zeros(dk.total_blocks * 3, dtype=torch.int64, device="cuda")
+        L = dk.ptb(s, W, worker_log=wl, timed=True, block_log=bl)
         L.wait()
         if rep == 0:
             continue
+        b = bl.view(-1, 3).cpu().tolist()
+        per_worker = {}
+        for st, en, who in b:
+            per_worker.setdefault(who >> 32, []).append((st, en))
+        steps, spans = [], []
+        for lst in per_worker.values():
+            lst.sort()
+            steps += [lst[k + 1][0] - lst[k][0] for k in range(len(lst) - 1)]
+            spans += [en - st for st, en in lst]
+        steps.sort()
+        spans.sort()
         w = wl.view(W, 4).cpu().tolist()
         t0 = min(r[1] for r in w)
         entry = sorted((r[1] - t0) / 1e3 for r in w)
@@ -51,6 +63,9 @@ def main():
             "exit_us_p0_p50_max": [q(exit_, 0), q(exit_, .5), exit_[-1]],
             "blocks_run_hist": {str(b): blocks.count(b) for b in sorted(set(blocks))},
             "smids_distinct": len({r[0] >> 32 for r in w}),
+            # block_log: consecutive blocks of one worker -- first-MMA to first-MMA
+            "block_step_us_p10_p50_p90": [steps[int(f * (len(steps) - 1))] / 1e3 for f in (.1, .5, .9)] if steps else None,
+            "block_first_mma_to_last_store_us_p50": spans[len(spans) // 2] / 1e3 if spans else None,
         })
     print(json.dumps(out, indent=1))
 
