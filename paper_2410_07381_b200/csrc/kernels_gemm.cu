@@ -1410,6 +1410,15 @@ static int bind_gemm(const tally_kernel_args* a, Instance* inst, bool split) {
           : old_rule ? (p.kb_per_split <= 2 ? 4 : 1)
                      : max(1, min(min(8, (131072 + kTileOut - 1) / kTileOut),
                                   (target + p.kb_per_split - 1) / p.kb_per_split));
+    if constexpr (gemm::PairOf<Cfg>::value == 2) {
+      // pairs: one CTA per SM, so an untransformed launch pays a CTA's
+      // prologue and its last epilogue per logical block; with many tiles, a
+      // block of ~32 k-blocks (2 tiles at K = 1024) overlaps the first tile's
+      // epilogue with the second's MMAs (BERT-large decoder: 282 us as one
+      // tile per cluster vs 196 us persistent) while leaving >= 2 blocks per pair
+      const long long tiles_all = (long long)p.tiles_m * p.tiles_n * p.splits * p.batches;
+      p.tpb = (int)std::max(1ll, std::min<long long>({4ll, (32 + p.kb_per_split - 1) / p.kb_per_split, tiles_all / 148}));
+    }
   }
   p.total_tiles = (long long)p.tiles_m * p.tiles_n * p.splits * p.batches;
   if (p.total_tiles >= (1ll << 31)) {

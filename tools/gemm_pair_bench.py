@@ -29,6 +29,7 @@ SHAPES = [
     ("c4 ffn up fwd", 4096, 4096, 1024, torch.bfloat16, 1),
     ("c4 ffn down fwd (split 4)", 4096, 1024, 4096, torch.float32, 4),
     ("c4 ffn down fwd", 4096, 1024, 4096, torch.bfloat16, 1),
+    ("c4 decoder fwd", 4096, 30720, 1024, torch.bfloat16, 1),
 ]
 
 
