@@ -70,6 +70,18 @@ def main():
     orig = collections.defaultdict(float)
     ptb = collections.defaultdict(float)
     n = collections.Counter()
+    alg_b = collections.defaultdict(float)
+    alg_f = collections.defaultdict(float)
+    for name, dk in tr.program:
+        alg_b[dk.kind] += dk.info.alg_bytes
+        alg_f[dk.kind] += dk.info.alg_flops
+    peaks = {}
+    try:
+        peaks = json.load(open(os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))),
+                                            "MEASURED_PEAKS.json")))
+    except OSError:
+        pass
+    pk_t, pk_b = peaks.get("bf16_tflops", 1590.0), peaks.get("hbm_gbs", 6650.0)
     for _ in range(args.reps):
         for name, dk in tr.program:
             ahead()
@@ -112,9 +124,17 @@ def main():
                 chosen[dk.kind] += us / args.reps
     tot_o, tot_p = sum(orig.values()), sum(ptb.values())
     out = {"config": args.config, "kernels": len(tr.program), "step_us_original": tot_o, "step_us_ptb": tot_p,
+           "peaks": {"bf16_tflops": pk_t, "hbm_gbs": pk_b, "source": "MEASURED_PEAKS.json" if peaks else
+                     "fallback (B200_PROFILING.md)"},
            "ptb_vs_original_speed": tot_o / tot_p,
            "by_kind": {k: {"n": n[k], "original_us": round(orig[k], 1), "ptb_us": round(ptb[k], 1),
                            "speed_ratio": round(orig[k] / ptb[k], 3),
+                           # roofline of the untransformed kind: algorithmic work over its device time
+                           "alg_GB": round(alg_b[k] / 1e9, 3), "alg_GFLOP": round(alg_f[k] / 1e9, 1),
+                           "achieved_TBps": round(alg_b[k] / (orig[k] * 1e3) / 1e3, 2),
+                           "achieved_TFLOPs": round(alg_f[k] / (orig[k] * 1e3) / 1e3, 1),
+                           "roofline_frac": round(max(alg_f[k] / (pk_t * 1e12), alg_b[k] / (pk_b * 1e9))
+                                                  / (orig[k] * 1e-6), 3),
                            **({"chosen_us": round(chosen[k], 1), "chosen_speed_ratio": round(orig[k] / chosen[k], 3)}
                               if chosen else {})}
                        for k in sorted(orig, key=lambda k: -orig[k])}}
