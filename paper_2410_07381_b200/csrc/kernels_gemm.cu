@@ -29,6 +29,7 @@
 #include <cstdio>
 #include <cstdlib>
 
+#include "epilogue.cuh"
 #include "registry.h"
 #include "runtime.h"
 
@@ -400,6 +401,10 @@ struct alignas(64) GemmParams {
   int causal;                   // causal-attention tile / K-range rule (tile_work), 0 = dense
   int bn, bk;                   // tile width and K block of the kind (for the causal rule)
   long long off[6][2];          // (row, col) origins of A, B, C: [a_row, a_col, b_row, b_col, c_row, c_col]
+  // fused linear-layer epilogue (TMA-store bf16 path): y = act(acc + bias (+ res));
+  // ep_pre: the pre-activation is also stored, through the map in b_lo
+  EpArgs ep;
+  int ep_pre;
 };
 
 __device__ __forceinline__ void tile_coords(unsigned t, const GemmParams& p, int& mb, int& nb) {
@@ -979,25 +984,50 @@ k_gemm(const __grid_constant__ GemmParams p, const ShapeArgs s) {
           __syncwarp();
           if (lane == 0) release_acc<PR>(&tmem_empty[acc]);
         }
-        if (lane == 0) asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
-        __syncwarp();
+        const int ycol = w.nb * Cfg::BN + half * HALF + bx, yrow = (w.mb * PR + (int)rank) * Cfg::BM + q * 32;
         unsigned char* srow = wstage + (size_t)lane * 128;
+        // stage 64 values of this lane's row (bf16, 128B-swizzle) and TMA-store the box
+        auto stage_store = [&](const CUtensorMap* map) {
+          if (lane == 0) asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
+          __syncwarp();
 #pragma unroll
-        for (int v = 0; v < 8; ++v) {
-          uint32_t wv[4];
+          for (int v = 0; v < 8; ++v) {
+            uint32_t wv[4];
 #pragma unroll
-          for (int e = 0; e < 4; ++e) {
-            const int k = 8 * (v & 3) + 2 * e;
-            __nv_bfloat162 b = __floats2bfloat162_rn(__uint_as_float(r[v >> 2][k]), __uint_as_float(r[v >> 2][k + 1]));
-            wv[e] = *reinterpret_cast<uint32_t*>(&b);
+            for (int e = 0; e < 4; ++e) {
+              const int k = 8 * (v & 3) + 2 * e;
+              __nv_bfloat162 b = __floats2bfloat162_rn(__uint_as_float(r[v >> 2][k]), __uint_as_float(r[v >> 2][k + 1]));
+              wv[e] = *reinterpret_cast<uint32_t*>(&b);
+            }
+            *reinterpret_cast<uint4*>(srow + ((v ^ (lane & 7)) << 4)) = make_uint4(wv[0], wv[1], wv[2], wv[3]);
           }
-          *reinterpret_cast<uint4*>(srow + ((v ^ (lane & 7)) << 4)) = make_uint4(wv[0], wv[1], wv[2], wv[3]);
+          asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+          __syncwarp();
+          if (lane == 0) tma_store_2d(map, wst, ycol, yrow);
+          __syncwarp();
+        };
+        if (p.ep.bias != nullptr) {
+          // fused linear-layer epilogue on the fp32 accumulator
+          const long long row = min((long long)(yrow + lane), (long long)p.m - 1);   // (rows past M: clipped by the map)
+#pragma unroll
+          for (int g8 = 0; g8 < 8; ++g8) {
+            float x[8];
+#pragma unroll
+            for (int e = 0; e < 8; ++e) x[e] = __uint_as_float(r[g8 >> 2][8 * (g8 & 3) + e]);
+            ep_bias_res8(p.ep, row, ycol + 8 * g8, x);
+#pragma unroll
+            for (int e = 0; e < 8; ++e) r[g8 >> 2][8 * (g8 & 3) + e] = __float_as_uint(x[e]);
+          }
+          if (p.ep_pre) stage_store(&p.b_lo);
+          if (p.ep.act) {
+#pragma unroll
+            for (int k = 0; k < 32; ++k) {
+              r[0][k] = __float_as_uint(ep_act(__uint_as_float(r[0][k]), p.ep.act));
+              r[1][k] = __float_as_uint(ep_act(__uint_as_float(r[1][k]), p.ep.act));
+            }
+          }
         }
-        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-        __syncwarp();
-        if (lane == 0)
-          tma_store_2d(&p.a_lo, wst, w.nb * Cfg::BN + half * HALF + bx, (w.mb * PR + (int)rank) * Cfg::BM + q * 32);
-        __syncwarp();
+        stage_store(&p.a_lo);
       }
       ++ci;
       if (warp == 2 && lane == 0 && lead) gemm_log_end(block_log_of(s), t, p);
@@ -1383,6 +1413,27 @@ static int bind_gemm(const tally_kernel_args* a, Instance* inst, bool split) {
       p.c_tma = 2;
     }
   }
+  // fused linear-layer epilogue: ptr[4] bias (fp32 [N]), ptr[5] residual (bf16,
+  // pitch ldc), ptr[6] pre-activation output (bf16, pitch ldc); i[6] activation
+  if (!split && (a->ptr[4] || a->ptr[5] || a->ptr[6] || a->i[6])) {
+    if (Cfg::KIND != 1 || sizeof(typename Cfg::OutT) != 2 || !p.c_tma || !a->ptr[4] || a->i[6] < 0 || a->i[6] > 3 ||
+        !aligned16_(a->ptr[4]) || (a->ptr[5] && !aligned16_(a->ptr[5]))) {
+      set_error("gemm: a fused epilogue (bias, residual, pre, act) needs a plain bf16 GEMM with the TMA-store "
+                "epilogue, 16-byte aligned fp32 bias, act 0-3");
+      return TALLY_EINVAL;
+    }
+    p.ep.bias = static_cast<const float*>(a->ptr[4]);
+    p.ep.res = static_cast<const __nv_bfloat16*>(a->ptr[5]);
+    p.ep.ldr = p.ldc;
+    p.ep.act = (int)a->i[6];
+    if (a->ptr[6]) {
+      if (!aligned16_(a->ptr[6])) { set_error("gemm: pre-activation output not 16-byte aligned"); return TALLY_EINVAL; }
+      int rc = make_map(&p.b_lo, a->ptr[6], CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, M, N, 32, p.ldc);
+      if (rc) return rc;
+      p.ep_pre = 1;
+    }
+    inst->alg_bytes_extra_ep = 4.0 * N + (a->ptr[5] ? 2.0 * M * N : 0.0) + (a->ptr[6] ? 2.0 * M * N : 0.0);
+  }
   p.kb_per_split = (int)((KBlocks + splits - 1) / splits);
   if ((KBlocks + p.kb_per_split - 1) / p.kb_per_split != splits) {
     set_error("gemm: %lld splits of %lld k-blocks leave an empty split (use ceil(KB / ceil(KB / splits)))",
@@ -1443,7 +1494,8 @@ static int bind_gemm(const tally_kernel_args* a, Instance* inst, bool split) {
   inst->smem = gemm::smem_bytes<Cfg>();
   inst->alg_flops = 2.0 * (double)M * (double)N * (double)K * (double)p.batches;
   inst->alg_bytes = ((double)Cfg::ESZ * (double)(M * K + N * K) * (split ? 2.0 : 1.0) +
-                     (double)sizeof(typename Cfg::OutT) * (double)(M * N) * (double)splits) * (double)p.batches;
+                     (double)sizeof(typename Cfg::OutT) * (double)(M * N) * (double)splits) * (double)p.batches +
+                    inst->alg_bytes_extra_ep;
   if (p.causal) {
     // the work actually done: k-blocks over all tiles of one batch under the rule
     const long long KBt = (K + Cfg::BK - 1) / Cfg::BK;

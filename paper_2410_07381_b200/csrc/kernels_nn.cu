@@ -31,6 +31,7 @@
 #include <cstdio>
 #include <cstdlib>
 
+#include "epilogue.cuh"
 #include "registry.h"
 
 namespace tally {
@@ -1014,7 +1015,24 @@ struct SplitKReduce {
     long long stride4;   // n / 4
     int S;
     int vpb;             // output vectors per logical block: 512 (2 per thread) or 32..256
+    EpArgs ep;           // optional fused linear-layer epilogue (bias null: plain sum)
+    int C;               // output columns (bias index) when ep.bias is set
   };
+  // the finished sum of output vector v (8 bf16 of a row-major [rows, C] output)
+  static __device__ __forceinline__ void finish8(const Params& p, long long v, float (&acc)[8]) {
+    if (p.ep.bias != nullptr) {
+      const long long e0 = 8 * v;
+      const long long row = e0 / p.C;
+      const int col = (int)(e0 - row * p.C);
+      ep_bias_res8(p.ep, row, col, acc);
+      if (p.ep.pre != nullptr) st16(reinterpret_cast<uint4*>(p.ep.pre) + v, pack8(acc));
+      if (p.ep.act) {
+#pragma unroll
+        for (int e = 0; e < 8; ++e) acc[e] = ep_act(acc[e], p.ep.act);
+      }
+    }
+    st16(p.out + v, pack8(acc));
+  }
   static __device__ __forceinline__ void add8(float (&acc)[8], const float4& a, const float4& b) {
     acc[0] += a.x; acc[1] += a.y; acc[2] += a.z; acc[3] += a.w;
     acc[4] += b.x; acc[5] += b.y; acc[6] += b.z; acc[7] += b.w;
@@ -1043,7 +1061,7 @@ struct SplitKReduce {
 #pragma unroll
       for (int u = 0; u < 2; ++u) {
         const long long v = v0 + u * kThreads;
-        if (v < p.n8) st16(p.out + v, pack8(acc[u]));
+        if (v < p.n8) finish8(p, v, acc[u]);
       }
       return;
     }
@@ -1073,7 +1091,7 @@ struct SplitKReduce {
       for (int k = 1; k < G; ++k)
 #pragma unroll
         for (int e = 0; e < 8; ++e) acc[e] += red[(k * p.vpb + lv) * 8 + e];
-      st16(p.out + v, pack8(acc));
+      finish8(p, v, acc);
     }
     __syncthreads();   // red is reused by the next logical block of a PTB worker
   }
@@ -1538,12 +1556,29 @@ static int bind_splitk_reduce(const tally_kernel_args* a, Instance* inst) {
   }
   p.n8 = n / 8;
   p.stride4 = n / 4;
+  // fused linear-layer epilogue: ptr[2] bias (fp32 [C]), ptr[3] residual and
+  // ptr[4] pre-activation output (bf16, row-major [n / C, C]); i[2] C, i[3] act
+  double ep_bytes = 0.0;
+  if (a->ptr[2] || a->ptr[3] || a->ptr[4] || a->i[3]) {
+    p.C = (int)a->i[2];
+    if (!a->ptr[2] || p.C < 8 || p.C % 8 || n % p.C || a->i[3] < 0 || a->i[3] > 3 || !aligned16(a->ptr[2]) ||
+        (a->ptr[3] && !aligned16(a->ptr[3])) || (a->ptr[4] && !aligned16(a->ptr[4]))) {
+      set_error("splitk_reduce: a fused epilogue needs an aligned fp32 bias, C %% 8 == 0 dividing n, act 0-3");
+      return TALLY_EINVAL;
+    }
+    p.ep.bias = static_cast<const float*>(a->ptr[2]);
+    p.ep.res = static_cast<const __nv_bfloat16*>(a->ptr[3]);
+    p.ep.pre = static_cast<__nv_bfloat16*>(a->ptr[4]);
+    p.ep.ldr = p.C;
+    p.ep.act = (int)a->i[3];
+    ep_bytes = 4.0 * p.C + (a->ptr[3] ? 2.0 * n : 0.0) + (a->ptr[4] ? 2.0 * n : 0.0);
+  }
   // ~64 KB of partials per logical block: 512 vectors up to S = 4, then
   // halving down to 32 vectors (S >= 33)
   p.vpb = 2 * nn::SplitKReduce::kThreads;
   while (p.vpb > 32 && (long long)p.vpb * 32 * p.S > 65536) p.vpb >>= 1;
   finish(inst, p, (p.n8 + p.vpb - 1) / p.vpb, nn::SplitKReduce::kThreads, nn::SplitKReduce::kSmem,
-         (4.0 * p.S + 2.0) * (double)n);
+         (4.0 * p.S + 2.0) * (double)n + ep_bytes);
   return TALLY_OK;
 }
 

@@ -21,6 +21,7 @@ struct Instance {
   size_t smem = 0;             // dynamic shared memory per CTA
   double alg_bytes = 0;        // algorithmic HBM bytes of the whole logical grid
   double alg_flops = 0;        // algorithmic flops of the whole logical grid
+  double alg_bytes_extra_ep = 0;   // fused-epilogue operand bytes (bias, residual, pre-activation)
   int preempt_units = 1;       // PTB preemption points per logical block (K-chunks for sgemm_tf32x3)
   // Per-instance device state that lives across the launches of one PTB
   // chain: the chunk-preemption resume ring (sgemm_tf32x3) or bn_stats'

@@ -376,7 +376,7 @@ def gemm(A, B, C, splits: int = 1, pair: bool = False) -> DeviceKernel:
 
 def gemm_ex(A, B, Cout, M, N, K, a_mn=False, b_mn=False, splits=1, batches=1, hdiv=1,
             a_off=((0, 0), (0, 0)), b_off=((0, 0), (0, 0)), c_off=((0, 0), (0, 0)), causal=0,
-            pair=False) -> DeviceKernel:
+            pair=False, bias=None, res=None, pre=None, act=0) -> DeviceKernel:
     """General bf16 GEMM on tcgen05: per batch, C[M,N] = A . B^T with A
     K-major (A[M,K] row-major) or MN-major (stored as A^T [K,M]), likewise B
     ([N,K] or [K,N]).  ``A``, ``B``, ``Cout`` are 2-D row-major views (any
@@ -389,7 +389,10 @@ def gemm_ex(A, B, Cout, M, N, K, a_mn=False, b_mn=False, splits=1, batches=1, hd
     above the diagonal skipped (left unwritten); 2 = P.V / dS.K, K limited to
     keys <= the tile's last query; 3 = dS^T.Q / P^T.dO, K from the tile's
     first key.  ``pair``: CTA-pair kind (256 x 256 tiles, N % 256 == 0; not
-    causal; ``_mn`` only with fp32 output)."""
+    causal; ``_mn`` only with fp32 output).  ``bias`` (fp32 [N]) fuses the
+    linear-layer epilogue into a plain bf16 GEMM: Cout = act(A.B^T + bias
+    (+ res)), ``pre`` receiving the pre-activation (``bias_act`` semantics on
+    the fp32 accumulator; res / pre share Cout's row pitch)."""
     import torch
     kinds = {(False, False): "", (True, True): "_mn", (False, True): "_kmn"}
     if (a_mn, b_mn) not in kinds:
@@ -408,8 +411,10 @@ def gemm_ex(A, B, Cout, M, N, K, a_mn=False, b_mn=False, splits=1, batches=1, hd
     for name, (r, c) in (("a", a_off), ("b", b_off), ("c", c_off)):
         getattr(lay, name + "_row_off")[0], getattr(lay, name + "_row_off")[1] = r
         getattr(lay, name + "_col_off")[0], getattr(lay, name + "_col_off")[1] = c
-    return DeviceKernel(kind, (A.data_ptr(), B.data_ptr(), Cout.data_ptr(), C.addressof(lay)),
-                        (M, N, K, 0, splits, causal), keep=(A, B, Cout, lay))
+    ep = tuple(t for t in (bias, res, pre) if t is not None)
+    return DeviceKernel(kind, (A.data_ptr(), B.data_ptr(), Cout.data_ptr(), C.addressof(lay),
+                               _ptr(bias), _ptr(res), _ptr(pre)),
+                        (M, N, K, 0, splits, causal, act), keep=(A, B, Cout, lay) + ep)
 
 
 def gemm_mn(At, Bt, C, splits: int = 1, pair: bool = False) -> DeviceKernel:
@@ -454,9 +459,14 @@ def bn_stats_bwd(x, g, part, P, C, rb, mean, invstd, gamma, dgamma, dbeta, coef,
                         (P, C, 1, rb, _ptr(dgamma), _ptr(dbeta), _ptr(coef)), keep=(dgamma, dbeta, coef))
 
 
-def splitk_reduce(parts, out) -> DeviceKernel:
-    """out (bf16) = parts.sum(0) for fp32 split-K partials [S, ...]."""
-    return DeviceKernel("splitk_reduce", (parts, out), (out.numel(), parts.shape[0]))
+def splitk_reduce(parts, out, bias=None, res=None, pre=None, act=0) -> DeviceKernel:
+    """out (bf16) = parts.sum(0) for fp32 split-K partials [S, ...].  With
+    ``bias`` (fp32 [C], out a row-major [rows, C]): the fused linear-layer
+    epilogue out = act(sum + bias (+ res)), ``pre`` receiving the
+    pre-activation values (as ``bias_act``)."""
+    C = out.shape[-1]
+    return DeviceKernel("splitk_reduce", (parts, out, bias, res, pre),
+                        (out.numel(), parts.shape[0], C if bias is not None else 0, act))
 
 
 def bn_finalize_fwd(part, nrb, C, count, gamma, beta, mean, invstd, scale, shift,

@@ -21,6 +21,7 @@ segment table of all parameters at the end.
 from __future__ import annotations
 
 import math
+import os
 
 from . import kernels as K
 from .resnet import SgdTable, _gemm_splits
@@ -64,6 +65,13 @@ class TransformerTrain:
     causal = True
     ln_eps = 1e-5
     pair_gemms = True     # CTA-pair tcgen05 GEMMs for the large linear layers (_pair_plan)
+    # which linear-layer epilogues run fused in the GEMM (or split-K reduce):
+    # "bias" (bias only), "res" (bias + residual), "act" (bias + activation).
+    # Measured (tools/step_time.py, BERT-large step): none 27.5 ms, bias 27.3,
+    # bias+res 27.1, +act 28.1 -- an erf GELU on 8 epilogue warps per SM (and
+    # the pre-activation's second store) costs the FFN-up GEMM more than the
+    # bias_act launch it replaces, so activations stay in bias_act
+    fuse_epilogue = frozenset(x for x in os.environ.get("TALLY_FUSE_EPILOGUE", "bias,res").split(",") if x)
 
     def _init_common(self):
         import torch
@@ -123,6 +131,25 @@ class TransformerTrain:
         self._add(name, K.colstats(g, part, P, C, rb, dbeta, dgamma=dgamma, x=x, mean=mean, rstd=rstd, g2=g2))
 
     def _linear_fwd(self, name, lin, x, act=0, res=None, pre=None):
+        fuse = "act" if act else "res" if res is not None else "bias"
+        if fuse in self.fuse_epilogue:
+            # y = act(x . W^T + b (+ res)) straight from the GEMM's TMA-store
+            # epilogue (no split) or from the split-K reduce -- no bf16
+            # intermediate, no bias_act launch
+            M, N, Kd = self.N, lin.out, lin.inp
+            pair, S = _pair_plan(M, N, Kd, self.pair_gemms)
+            if S == 1 and (pair or N % 128 == 0):
+                y = self._buf(M, N)
+                self._add(name + ".gemm", K.gemm_ex(x, lin.wb, y, M, N, Kd, pair=pair, bias=lin.b.w, res=res,
+                                                    pre=pre, act=act))
+                return y
+            if S > 1:
+                y = self._buf(M, N)
+                ws = self._ws(S * M * N).view(S * M, N)
+                self._add(name + ".gemm", K.gemm_ex(x, lin.wb, ws, M, N, Kd, splits=S, pair=pair))
+                self._add(name + ".reduce", K.splitk_reduce(ws.view(S, M, N), y, bias=lin.b.w, res=res, pre=pre,
+                                                            act=act))
+                return y
         u = self._buf(self.N, lin.out)
         self._gemm_ex_splitk(name + ".gemm", x, lin.wb, u, self.N, lin.out, lin.inp)
         y = self._buf(self.N, lin.out)

@@ -158,3 +158,57 @@ def test_pair_ptb_rejects_odd_workers(env):
     dk = kernels.gemm(A, B, C, pair=True)
     with pytest.raises(Exception):
         dk.ptb(s, 3)
+
+
+@pytest.mark.parametrize("pair", [False, True])
+@pytest.mark.parametrize("act", [0, 2, 3])
+def test_fused_linear_epilogue(env, pair, act):
+    """y = act(x . W^T + b (+ res)) from the GEMM's TMA-store epilogue and the
+    pre-activation beside it (bias_act semantics on the fp32 accumulator):
+    against PyTorch fp32 of the same bf16 inputs within the bf16 budget, all
+    shapes bit-identical."""
+    P, kernels, s = env
+    M, N, K = 1000, 512, 768
+    g = torch.Generator(device="cuda").manual_seed(23 + act)
+    x = (torch.rand(M, K, device="cuda", generator=g) * 2 - 1).bfloat16()
+    w = (torch.rand(N, K, device="cuda", generator=g) * 2 - 1).bfloat16() * 0.05
+    b = torch.rand(N, device="cuda", generator=g) - 0.5
+    res = (torch.rand(M, N, device="cuda", generator=g) * 2 - 1).bfloat16()
+    y = torch.zeros(M, N, device="cuda", dtype=torch.bfloat16)
+    pre = torch.zeros_like(y)
+    dk = kernels.gemm_ex(x, w, y, M, N, K, pair=pair, bias=b, res=res, pre=pre, act=act)
+    outs = []
+    for shape in ("original", "sliced", "ptb"):
+        y.zero_()
+        pre.zero_()
+        if shape == "original":
+            dk.original(s).wait()
+        elif shape == "sliced":
+            for off, cnt in P.slice_plan(dk.total_blocks, Fraction(1, 3)):
+                dk.sliced(s, off, cnt).wait()
+        else:
+            dk.ptb(s, 148).wait()
+        outs.append((y.clone(), pre.clone()))
+    for o in outs[1:]:
+        assert torch.equal(o[0], outs[0][0]) and torch.equal(o[1], outs[0][1])
+    ref_pre = x.float() @ w.float().T + b + res.float()
+    F = torch.nn.functional
+    ref = {0: ref_pre, 2: F.gelu(ref_pre, approximate="tanh"), 3: F.gelu(ref_pre)}[act]
+    assert _rel(outs[0][1], ref_pre.double()) < 1e-2
+    assert _rel(outs[0][0], ref.double()) < 1e-2
+
+
+def test_splitk_reduce_fused_epilogue(env):
+    P, kernels, s = env
+    S, M, N = 3, 512, 1024
+    g = torch.Generator(device="cuda").manual_seed(29)
+    parts = torch.randn(S, M, N, device="cuda", generator=g)
+    b = torch.randn(N, device="cuda", generator=g)
+    res = torch.randn(M, N, device="cuda", generator=g).bfloat16()
+    y = torch.zeros(M, N, device="cuda", dtype=torch.bfloat16)
+    pre = torch.zeros_like(y)
+    dk = kernels.splitk_reduce(parts, y, bias=b, res=res, pre=pre, act=3)
+    dk.original(s).wait()
+    ref_pre = parts.sum(0) + b + res.float()
+    assert _rel(pre, ref_pre.double()) < 1e-2
+    assert _rel(y, torch.nn.functional.gelu(ref_pre).double()) < 1e-2
