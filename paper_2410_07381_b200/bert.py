@@ -104,7 +104,8 @@ class BertTrain(TransformerTrain):
         torch = self.torch
         N, d, T, H = self.N, self.d, self.T, self.H
         BHT = self.B * H * T
-        S = torch.empty(BHT, T, dtype=torch.float32, device=self.device)
+        # fp32 scores only for the unfused attention path (_fused_attn keeps them in TMEM)
+        S = None if self._fused_attn() else torch.empty(BHT, T, dtype=torch.float32, device=self.device)
         dS = self._buf(BHT, T)
         # embeddings: word + position (embedding_fwd), + token type 0 (its fp32 row as the bias), LayerNorm
         e0 = self._buf(N, d)
@@ -154,7 +155,7 @@ class BertTrain(TransformerTrain):
         du = self._buf(N, d)
         self._add("cls.predictions.transform.gelu_bwd", K.gelu_bwd(dt, tpre, du, erf=True))
         g = self._linear_bwd("cls.predictions.transform.dense", self.head, du, x)
-        dP = torch.empty(BHT, T, dtype=torch.float32, device=self.device)
+        dP = None if self._fused_attn() else torch.empty(BHT, T, dtype=torch.float32, device=self.device)
         self.block_grads = {}
         for lay, sv in zip(reversed(self.layers), reversed(saved)):
             pre = lay["pre"]

@@ -1266,6 +1266,197 @@ struct SplitTf32 {
   }
 };
 
+
+// ---------------------------------------------------------------- fused attention softmax
+// One logical block = 128 query rows of one (sequence, head), all T <= 512 keys:
+//   forward  (MODE 0): S = Q K^T in TMEM (tcgen05, 128 x T fp32), P = softmax(scale * S)
+//                      row by row from TMEM, P (bf16) TMA-stored -- the fp32 score
+//                      matrix never reaches HBM (it was a GEMM output + a softmax pass);
+//   backward (MODE 1): dP = dO V^T in TMEM, dS = P * (dP - rowsum(P * dP)) * scale,
+//                      dS (bf16) TMA-stored (P read back per row).
+// Q / K / V / dO are head-D (= 64) column slices of row-major activations (the
+// fused QKV buffer), read by TMA; the Body runs under k_original / k_sliced /
+// k_ptb like every transformable kind.  8 warps: thread 0 issues the TMA loads
+// and the MMAs, then all warps drain TMEM (warp w: lane quarter w % 4, key
+// half w / 4; the two warps of a quarter exchange row max / sum through smem).
+template <int MODE>
+struct AttnSoftmax {
+  static constexpr int kThreads = 256;
+  static constexpr int kD = 64;                  // head dim = one 128 B swizzle atom of bf16
+  static constexpr int kTileBytes = 128 * kD * 2;   // 16 KB: 128 rows x 64 bf16
+  static constexpr int kSmem = 1024 + kTileBytes * 5 + 8 * 4096 + 2 * 2 * 128 * 4 + 64;
+  struct Params {
+    CUtensorMap a_map;     // MODE 0: Q; MODE 1: dO   (box 64 cols x 128 rows)
+    CUtensorMap b_map;     // MODE 0: K; MODE 1: V    (box 64 cols x 128 rows)
+    CUtensorMap out_map;   // P / dS [z * T + i, T] bf16 (box 64 cols x 32 rows)
+    const __nv_bfloat16* p_in;   // MODE 1: P [z * T + i, T]
+    long long a_col0, a_col_h, b_col0, b_col_h;   // operand column origin: col0 + h * col_h
+    int T, H;
+    float scale;
+  };
+
+  static __device__ __forceinline__ void run(const Params& p, uint3 bidx, uint3, char* smem_raw) {
+    unsigned char* sm = reinterpret_cast<unsigned char*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+    unsigned char* sa = sm;                          // A tile (128 x 64)
+    unsigned char* sb = sm + kTileBytes;             // B: T / 128 boxes of 128 keys
+    unsigned char* stg = sm + 5 * kTileBytes;        // 8 x 4 KB output staging
+    float* red = reinterpret_cast<float*>(stg + 8 * 4096);   // [2 halves][2 values][128 rows]
+    uint64_t* bar = reinterpret_cast<uint64_t*>(red + 2 * 2 * 128);   // [0] operands, [1] MMA done
+    uint32_t* tslot = reinterpret_cast<uint32_t*>(bar + 2);
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int z = (int)bidx.y, b = z / p.H, h = z - b * p.H, r0 = (int)bidx.x * 128;
+    const int nkb = p.T / 128;
+    if (threadIdx.x == 0) {
+      mbar_init(&bar[0], 1);
+      mbar_init(&bar[1], 1);
+      asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    if (warp == 0)   // (no relinquish: a PTB worker allocates again for its next logical block)
+      asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(tslot)), "n"(512));
+    fence_before();
+    __syncthreads();
+    fence_after();
+    const uint32_t tmem = *tslot;
+    if (threadIdx.x == 0) {
+      mbar_expect_tx(&bar[0], (uint32_t)(kTileBytes * (1 + nkb)));
+      tma_load_2d(sa, &p.a_map, &bar[0], (int)(p.a_col0 + h * p.a_col_h), b * p.T + r0);
+      for (int kb = 0; kb < nkb; ++kb)
+        tma_load_2d(sb + kb * kTileBytes, &p.b_map, &bar[0], (int)(p.b_col0 + h * p.b_col_h), b * p.T + kb * 128);
+      mbar_wait(&bar[0], 0);
+      fence_after();
+      constexpr uint32_t idesc = make_idesc<1, 128>();   // bf16, M = 128, N = 128
+#pragma unroll
+      for (int k = 0; k < kD / 16; ++k) {
+        const uint64_t da = smem_desc(sa + k * 32);
+        for (int kb = 0; kb < nkb; ++kb)
+          umma<1>(tmem + (uint32_t)(kb * 128), da, smem_desc(sb + kb * kTileBytes + k * 32), idesc, k > 0);
+      }
+      umma_commit(&bar[1]);
+    }
+    __syncwarp();
+    mbar_wait(&bar[1], 0);
+    fence_after();
+    // ---- row pass over TMEM: warp w drains lanes [32 q, 32 q + 32), keys [half * T/2, +T/2)
+    const int q = warp & 3, half = warp >> 2;
+    const int kcols = p.T / 2;
+    const uint32_t lb = tmem + ((uint32_t)(q * 32) << 16) + (uint32_t)(half * kcols);
+    const long long grow = (long long)z * p.T + r0 + q * 32 + lane;   // this lane's row of P / dS
+    float* mine = red + half * 256 + q * 32 + lane;
+    const float* other = red + (half ^ 1) * 256 + q * 32 + lane;
+    if constexpr (MODE == 0) {
+      float m = -INFINITY;
+      for (int c = 0; c < kcols; c += 32) {
+        uint32_t r[32];
+        tmem_ld32(lb + c, r);
+#pragma unroll
+        for (int e = 0; e < 32; ++e) m = fmaxf(m, __uint_as_float(r[e]) * p.scale);
+      }
+      mine[0] = m;
+      asm volatile("bar.sync %0, 64;" ::"r"(1 + q) : "memory");
+      m = fmaxf(m, other[0]);
+      float sum = 0.f;
+      for (int c = 0; c < kcols; c += 32) {
+        uint32_t r[32];
+        tmem_ld32(lb + c, r);
+#pragma unroll
+        for (int e = 0; e < 32; ++e) {
+          const float v = __expf(__uint_as_float(r[e]) * p.scale - m);
+          sum += v;
+          r[e] = __float_as_uint(v);
+        }
+        tmem_st32(lb + c, r);   // exp(scale s - m) back in place
+      }
+      mine[128] = sum;
+      asm volatile("bar.sync %0, 64;" ::"r"(1 + q) : "memory");
+      sum += other[128];
+      const float inv = 1.f / sum;
+      // ---- P = e / sum: bf16, staged 32 rows x 64 keys, TMA-stored
+      unsigned char* wst = stg + (size_t)warp * 4096;
+      for (int c = 0; c < kcols; c += 64) {
+        uint32_t r[2][32];
+        tmem_ld32(lb + c, r[0]);
+        tmem_ld32(lb + c + 32, r[1]);
+        if (lane == 0) asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
+        __syncwarp();
+        unsigned char* srow = wst + (size_t)lane * 128;
+#pragma unroll
+        for (int v = 0; v < 8; ++v) {
+          uint32_t wv[4];
+#pragma unroll
+          for (int e = 0; e < 4; ++e) {
+            const int k = 8 * (v & 3) + 2 * e;
+            __nv_bfloat162 bb = __floats2bfloat162_rn(__uint_as_float(r[v >> 2][k]) * inv, __uint_as_float(r[v >> 2][k + 1]) * inv);
+            wv[e] = *reinterpret_cast<uint32_t*>(&bb);
+          }
+          *reinterpret_cast<uint4*>(srow + ((v ^ (lane & 7)) << 4)) = make_uint4(wv[0], wv[1], wv[2], wv[3]);
+        }
+        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+        __syncwarp();
+        if (lane == 0) tma_store_2d(&p.out_map, smem_u32(wst), half * kcols + c, (int)(grow - lane));
+        __syncwarp();
+      }
+    } else {
+      // dS = P * (dP - delta) * scale, delta = sum_j P dP (P read back per row)
+      const __nv_bfloat16* prow = p.p_in + grow * p.T + half * kcols;
+      float dot = 0.f;
+      for (int c = 0; c < kcols; c += 32) {
+        uint32_t r[32];
+        tmem_ld32(lb + c, r);
+        uint4 pv[4];
+#pragma unroll
+        for (int v = 0; v < 4; ++v) pv[v] = __ldg(reinterpret_cast<const uint4*>(prow + c) + v);
+#pragma unroll
+        for (int v = 0; v < 4; ++v) {
+          const __nv_bfloat162* h2 = reinterpret_cast<const __nv_bfloat162*>(&pv[v]);
+#pragma unroll
+          for (int e = 0; e < 4; ++e) {
+            const float2 f = __bfloat1622float2(h2[e]);
+            dot += f.x * __uint_as_float(r[8 * v + 2 * e]) + f.y * __uint_as_float(r[8 * v + 2 * e + 1]);
+          }
+        }
+      }
+      mine[0] = dot;
+      asm volatile("bar.sync %0, 64;" ::"r"(1 + q) : "memory");
+      dot += other[0];
+      unsigned char* wst = stg + (size_t)warp * 4096;
+      for (int c = 0; c < kcols; c += 64) {
+        uint32_t r[2][32];
+        tmem_ld32(lb + c, r[0]);
+        tmem_ld32(lb + c + 32, r[1]);
+        uint4 pv[8];
+#pragma unroll
+        for (int v = 0; v < 8; ++v) pv[v] = __ldg(reinterpret_cast<const uint4*>(prow + c) + v);
+        if (lane == 0) asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
+        __syncwarp();
+        unsigned char* srow = wst + (size_t)lane * 128;
+#pragma unroll
+        for (int v = 0; v < 8; ++v) {
+          const __nv_bfloat162* h2 = reinterpret_cast<const __nv_bfloat162*>(&pv[v]);
+          uint32_t wv[4];
+#pragma unroll
+          for (int e = 0; e < 4; ++e) {
+            const int k = 8 * (v & 3) + 2 * e;
+            const float2 f = __bfloat1622float2(h2[e]);
+            __nv_bfloat162 bb = __floats2bfloat162_rn(f.x * (__uint_as_float(r[v >> 2][k]) - dot) * p.scale,
+                                                      f.y * (__uint_as_float(r[v >> 2][k + 1]) - dot) * p.scale);
+            wv[e] = *reinterpret_cast<uint32_t*>(&bb);
+          }
+          *reinterpret_cast<uint4*>(srow + ((v ^ (lane & 7)) << 4)) = make_uint4(wv[0], wv[1], wv[2], wv[3]);
+        }
+        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+        __syncwarp();
+        if (lane == 0) tma_store_2d(&p.out_map, smem_u32(wst), half * kcols + c, (int)(grow - lane));
+        __syncwarp();
+      }
+    }
+    if (lane == 0) asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
+    fence_before();
+    __syncthreads();
+    fence_after();
+    if (warp == 0) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "n"(512));
+  }
+};
+
 }  // namespace gemm
 
 // ---------------------------------------------------------------- host side
@@ -1576,8 +1767,74 @@ static KernelKind gemm_kind(const char* name, int (*bind)(const tally_kernel_arg
   return k;
 }
 
+// ptr: A operand tensor (Q or dO), B operand tensor (K or V), out (P / dS),
+// [MODE 1: P in].  i: B, H, T, a_rows_ld (row pitch of A's tensor), b_ld,
+// a_col0, b_col0 (column origin of head 0; head h at + h * 64).  f: scale.
+template <int MODE>
+static int bind_attn_softmax(const tally_kernel_args* a, Instance* inst) {
+  using Body = gemm::AttnSoftmax<MODE>;
+  typename Body::Params p;
+  memset(&p, 0, sizeof(p));
+  const long long B = a->i[0], H = a->i[1], T = a->i[2], lda = a->i[3], ldb = a->i[4];
+  p.a_col0 = a->i[5];
+  p.b_col0 = a->i[6];
+  p.a_col_h = p.b_col_h = Body::kD;
+  p.T = (int)T;
+  p.H = (int)H;
+  p.scale = (float)a->f[0];
+  if (!a->ptr[0] || !a->ptr[1] || !a->ptr[2] || (MODE == 1 && !a->ptr[3]) || B < 1 || H < 1 || T < 128 ||
+      T > 512 || T % 128 || lda % 8 || ldb % 8 || p.a_col0 + H * Body::kD > lda || p.b_col0 + H * Body::kD > ldb) {
+    set_error("attn_softmax: need A, B, out (and P), T in 128..512 (multiple of 128), head dim 64, "
+              "column slices inside the row pitch");
+    return TALLY_EINVAL;
+  }
+  int rc;
+  if ((rc = make_map(&p.a_map, a->ptr[0], CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, B * T, lda, 128, lda))) return rc;
+  if ((rc = make_map(&p.b_map, a->ptr[1], CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, B * T, ldb, 128, ldb))) return rc;
+  if ((rc = make_map(&p.out_map, a->ptr[2], CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, B * H * T, T, 32, T))) return rc;
+  p.p_in = static_cast<const __nv_bfloat16*>(a->ptr[3]);
+  static_assert(sizeof(p) <= kMaxParamBytes, "params too large");
+  memcpy(inst->params, &p, sizeof(p));
+  inst->grid = make_uint3((unsigned)(T / 128), (unsigned)(B * H), 1);
+  inst->threads = Body::kThreads;
+  inst->smem = Body::kSmem;
+  inst->alg_flops = 2.0 * (double)B * H * T * T * Body::kD;
+  // Q / dO and K / V once per block row, P / dS written (MODE 1: P read)
+  inst->alg_bytes = (double)B * H * T * Body::kD * 2.0 * (1.0 + T / 128.0) + (double)B * H * T * T * 2.0 * (MODE ? 2.0 : 1.0);
+  return TALLY_OK;
+}
+
+template <int MODE>
+static int setup_attn_softmax() {
+  using Body = gemm::AttnSoftmax<MODE>;
+  const void* fns[3] = {reinterpret_cast<const void*>(&k_original<Body>), reinterpret_cast<const void*>(&k_sliced<Body>),
+                        reinterpret_cast<const void*>(&k_ptb<Body>)};
+  for (const void* f : fns) {
+    cudaError_t e = cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, Body::kSmem);
+    if (e == cudaSuccess)
+      e = cudaFuncSetAttribute(f, cudaFuncAttributePreferredSharedMemoryCarveout, cudaSharedmemCarveoutMaxShared);
+    if (e != cudaSuccess) return cuda_fail(e, "attn_softmax smem attribute");
+  }
+  return TALLY_OK;
+}
+
+template <int MODE>
+static KernelKind attn_kind(const char* name) {
+  using Body = gemm::AttnSoftmax<MODE>;
+  KernelKind k{};
+  k.name = name;
+  k.fn_original = reinterpret_cast<const void*>(&k_original<Body>);
+  k.fn_sliced = reinterpret_cast<const void*>(&k_sliced<Body>);
+  k.fn_ptb = reinterpret_cast<const void*>(&k_ptb<Body>);
+  k.bind = bind_attn_softmax<MODE>;
+  k.setup = setup_attn_softmax<MODE>;
+  k.tmem_cols = 512;
+  k.ret_ring = 1;   // generic k_ptb workers: return ring and static first blocks
+  return k;
+}
+
 int register_gemm_kernels(KernelKind* out, int cap) {
-  if (cap < 20) return 0;
+  if (cap < 22) return 0;
   out[0] = gemm_kind<gemm::CfgTf32x3>("sgemm_tf32x3", bind_sgemm);
   out[1] = gemm_kind<gemm::CfgBf16>("gemm_bf16", bind_bf16<gemm::CfgBf16>);
   out[3] = gemm_kind<gemm::CfgTf32x3N64>("sgemm_tf32x3_n64", bind_sgemm_n64);
@@ -1604,7 +1861,9 @@ int register_gemm_kernels(KernelKind* out, int cap) {
   k.fn_ptb = reinterpret_cast<const void*>(&k_ptb<gemm::SplitTf32>);
   k.bind = bind_split;
   out[2] = k;
-  return 20;
+  out[20] = attn_kind<0>("attn_softmax");
+  out[21] = attn_kind<1>("attn_softmax_bwd");
+  return 22;
 }
 
 }  // namespace tally

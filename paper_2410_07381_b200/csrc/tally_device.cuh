@@ -231,7 +231,7 @@ __device__ __forceinline__ void log_block(unsigned long long* log, unsigned long
 // --- Original: the untransformed kernel --------------------------------------
 template <class Body>
 __global__ void __launch_bounds__(Body::kThreads, MinBlocks<Body>::value)
-k_original(const typename Body::Params p, const SliceArgs s) {
+k_original(const __grid_constant__ typename Body::Params p, const SliceArgs s) {
   extern __shared__ __align__(1024) char smem[];
   const uint3 g = make_uint3(gridDim.x, gridDim.y, gridDim.z);
   if (s.exec_count != nullptr && threadIdx.x == 0)
@@ -247,7 +247,7 @@ k_original(const typename Body::Params p, const SliceArgs s) {
 // --- Sliced: block offset + pinned gridDim ------------------------------------
 template <class Body>
 __global__ void __launch_bounds__(Body::kThreads, MinBlocks<Body>::value)
-k_sliced(const typename Body::Params p, const SliceArgs s) {
+k_sliced(const __grid_constant__ typename Body::Params p, const SliceArgs s) {
   extern __shared__ __align__(1024) char smem[];
   const uint3 b = s.linear ? delinearize(s.linear_offset + blockIdx.x, s.grid)
                            : make_uint3(blockIdx.x + s.offset.x, blockIdx.y + s.offset.y,
@@ -504,7 +504,7 @@ __device__ __forceinline__ unsigned smid() {
 // the pre-claimed next batch) is handed back through the return ring.
 template <class Body>
 __global__ void __launch_bounds__(Body::kThreads, MinBlocks<Body>::value)
-k_ptb(const typename Body::Params p, const PtbArgs a) {
+k_ptb(const __grid_constant__ typename Body::Params p, const PtbArgs a) {
   extern __shared__ __align__(1024) char smem[];
   __shared__ long long s_task[2];
   const bool leader = (threadIdx.x == 0);

@@ -417,6 +417,25 @@ def gemm_ex(A, B, Cout, M, N, K, a_mn=False, b_mn=False, splits=1, batches=1, hd
                         (M, N, K, 0, splits, causal, act), keep=(A, B, Cout, lay) + ep)
 
 
+def attn_softmax(qkv, P, B, H, T, scale, d=None) -> DeviceKernel:
+    """Fused S = Q.K^T and P = softmax(scale * S) for every (sequence, head),
+    all keys visible (T in 128..512, head dim 64): Q / K are the head slices
+    of the fused QKV activation [B*T, 3d]; P is [B*H*T, T] bf16.  The fp32
+    scores stay in TMEM."""
+    d = d if d is not None else qkv.shape[1] // 3
+    ld = qkv.stride(0)
+    return DeviceKernel("attn_softmax", (qkv, qkv, P, None), (B, H, T, ld, ld, 0, d), (scale,))
+
+
+def attn_softmax_bwd(dO, qkv, P, dS, B, H, T, scale, d=None) -> DeviceKernel:
+    """Fused dP = dO.V^T and dS = P * (dP - rowsum(P * dP)) * scale (the
+    softmax backward of ``attn_softmax``); dO [B*T, d], V the third head
+    slice of the fused QKV activation, P / dS [B*H*T, T] bf16."""
+    d = d if d is not None else qkv.shape[1] // 3
+    return DeviceKernel("attn_softmax_bwd", (dO, qkv, dS, P), (B, H, T, dO.stride(0), qkv.stride(0), 0, 2 * d),
+                        (scale,))
+
+
 def gemm_mn(At, Bt, C, splits: int = 1, pair: bool = False) -> DeviceKernel:
     """C[M,N] (fp32) = At[K,M]^T . Bt[K,N] with both operands MN-major (as
     stored: M / N contiguous) -- the weight gradient dW = dY^T . X of a

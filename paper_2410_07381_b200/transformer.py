@@ -65,6 +65,7 @@ class TransformerTrain:
     causal = True
     ln_eps = 1e-5
     pair_gemms = True     # CTA-pair tcgen05 GEMMs for the large linear layers (_pair_plan)
+    fuse_attention = os.environ.get("TALLY_FUSE_ATTENTION", "1") != "0"   # see _fused_attn
     # which linear-layer epilogues run fused in the GEMM (or split-K reduce):
     # "bias" (bias only), "res" (bias + residual), "act" (bias + activation).
     # Measured (tools/step_time.py, BERT-large step): none 27.5 ms, bias 27.3,
@@ -233,14 +234,23 @@ class TransformerTrain:
         d = self.d
         return qkv[:, :d], qkv[:, d:2 * d], qkv[:, 2 * d:]
 
+    def _fused_attn(self):
+        """S = Q.K^T + softmax (and dP + softmax backward) in one tcgen05 kernel
+        whose scores never leave TMEM: all keys visible, T <= 512, head dim 64."""
+        return self.fuse_attention and not self.causal and self.T % 128 == 0 and 128 <= self.T <= 512 \
+            and self.D == 64
+
     def _attn_fwd(self, name, qkv, S, Pm):
         T, H, D = self.T, self.H, self.D
         q, k, v = self._views(qkv)
         z = dict(batches=self.B * H, hdiv=H)
         c1, c2 = (1, 2) if self.causal else (0, 0)   # causal tile / K-range rules (kernels.gemm_ex)
-        self._add(name + ".qk", K.gemm_ex(q, k, S, T, T, D, a_off=((T, 0), (0, D)), b_off=((T, 0), (0, D)),
-                                          c_off=((H * T, T), (0, 0)), causal=c1, **z))
-        self._add(name + ".softmax", K.softmax_causal(S, Pm, T, 1.0 / math.sqrt(D), causal=self.causal))
+        if self._fused_attn():
+            self._add(name + ".qk_softmax", K.attn_softmax(qkv, Pm, self.B, H, T, 1.0 / math.sqrt(D), d=self.d))
+        else:
+            self._add(name + ".qk", K.gemm_ex(q, k, S, T, T, D, a_off=((T, 0), (0, D)), b_off=((T, 0), (0, D)),
+                                              c_off=((H * T, T), (0, 0)), causal=c1, **z))
+            self._add(name + ".softmax", K.softmax_causal(S, Pm, T, 1.0 / math.sqrt(D), causal=self.causal))
         o = self._buf(self.N, self.d)
         self._add(name + ".pv", K.gemm_ex(Pm, v, o, T, D, T, b_mn=True, a_off=((H * T, T), (0, 0)),
                                           b_off=((T, 0), (0, D)), c_off=((T, 0), (0, D)), causal=c2, **z))
@@ -253,9 +263,14 @@ class TransformerTrain:
         c1, c2, c3 = (1, 2, 3) if self.causal else (0, 0, 0)
         dqkv = self._buf(self.N, 3 * self.d)
         dq, dk_, dv = self._views(dqkv)
-        self._add(name + ".dp", K.gemm_ex(do, v, dP, T, T, D, a_off=((T, 0), (0, D)), b_off=((T, 0), (0, D)),
-                                          c_off=((H * T, T), (0, 0)), causal=c1, **z))
-        self._add(name + ".softmax_bwd", K.softmax_causal_bwd(Pm, dP, dS, T, 1.0 / math.sqrt(D), causal=self.causal))
+        if self._fused_attn():
+            self._add(name + ".dp_softmax_bwd", K.attn_softmax_bwd(do, qkv, Pm, dS, self.B, H, T, 1.0 / math.sqrt(D),
+                                                                   d=self.d))
+        else:
+            self._add(name + ".dp", K.gemm_ex(do, v, dP, T, T, D, a_off=((T, 0), (0, D)), b_off=((T, 0), (0, D)),
+                                              c_off=((H * T, T), (0, 0)), causal=c1, **z))
+            self._add(name + ".softmax_bwd", K.softmax_causal_bwd(Pm, dP, dS, T, 1.0 / math.sqrt(D),
+                                                                  causal=self.causal))
         self._add(name + ".dq", K.gemm_ex(dS, k, dq, T, D, T, b_mn=True, a_off=((H * T, T), (0, 0)),
                                           b_off=((T, 0), (0, D)), c_off=((T, 0), (0, D)), causal=c2, **z))
         self._add(name + ".dk", K.gemm_ex(dS, q, dk_, T, D, T, a_mn=True, b_mn=True, a_off=((H * T, T), (0, 0)),

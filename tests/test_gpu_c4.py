@@ -179,3 +179,53 @@ def test_bert_step_shapes_bit_identical(env):
             assert nerr(b, a) < 1e-6 and nerr(c, a) < 1e-6
         else:
             assert torch.equal(a, b) and torch.equal(a, c), n
+
+
+def test_fused_attention_softmax_kernels_match_unfused():
+    """attn_softmax / attn_softmax_bwd (scores and dP kept in TMEM) against
+    PyTorch fp32 of the same bf16 inputs: P and dS within the bf16 budget,
+    every launch shape bit-identical."""
+    if not torch.cuda.is_available():
+        pytest.skip("no GPU")
+    import math
+    from fractions import Fraction
+    import paper_2410_07381_b200 as P
+    from paper_2410_07381_b200 import kernels as K
+    P.B200Device.get(0)
+    s = K.Stream(high_priority=False)
+    B, H, T, D = 2, 4, 384, 64
+    d = H * D
+    g = torch.Generator(device="cuda").manual_seed(31)
+    qkv = (torch.randn(B * T, 3 * d, device="cuda", generator=g) * 0.5).bfloat16()
+    dO = (torch.randn(B * T, d, device="cuda", generator=g) * 0.5).bfloat16()
+    scale = 1.0 / math.sqrt(D)
+    Pm = torch.zeros(B * H * T, T, device="cuda", dtype=torch.bfloat16)
+    dS = torch.zeros_like(Pm)
+    fwd = K.attn_softmax(qkv, Pm, B, H, T, scale, d=d)
+    bwd = K.attn_softmax_bwd(dO, qkv, Pm, dS, B, H, T, scale, d=d)
+    q = qkv[:, :d].float().view(B, T, H, D).permute(0, 2, 1, 3)
+    k = qkv[:, d:2 * d].float().view(B, T, H, D).permute(0, 2, 1, 3)
+    v = qkv[:, 2 * d:].float().view(B, T, H, D).permute(0, 2, 1, 3)
+    do = dO.float().view(B, T, H, D).permute(0, 2, 1, 3)
+    ref_p = torch.softmax(q @ k.transpose(-1, -2) * scale, dim=-1)
+    outs = []
+    for shape in ("original", "sliced", "ptb"):
+        Pm.zero_()
+        dS.zero_()
+        for dk in (fwd, bwd):
+            if shape == "original":
+                dk.original(s).wait()
+            elif shape == "sliced":
+                for off, cnt in P.slice_plan(dk.total_blocks, Fraction(1, 5)):
+                    dk.sliced(s, off, cnt).wait()
+            else:
+                dk.ptb(s, 8).wait()   # several logical blocks per worker
+        outs.append((Pm.clone(), dS.clone()))
+    for o in outs[1:]:
+        assert torch.equal(o[0], outs[0][0]) and torch.equal(o[1], outs[0][1])
+    pm = outs[0][0].float().view(B, H, T, T)
+    assert ((pm - ref_p).abs().max() / ref_p.abs().max()).item() < 1e-2
+    dp = do @ v.transpose(-1, -2)
+    ref_ds = pm * (dp - (pm * dp).sum(-1, keepdim=True)) * scale
+    ds = outs[0][1].float().view(B, H, T, T)
+    assert ((ds - ref_ds).abs().max() / ref_ds.abs().max()).item() < 1e-2

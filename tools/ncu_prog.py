@@ -50,7 +50,8 @@ def main():
     else:
         progs = dict(tr.program)
         for n in args.names:
-            dk = progs[n]
+            # exact name, else the first program entry containing it
+            dk = progs[n] if n in progs else next(d for m, d in tr.program if n in m)
             dk.original(s).wait()
             dk.ptb(s, min(dk.total_blocks * dk.info.cluster, 148 * max(1, dk.info.occupancy_ptb))).wait()
     torch.cuda.synchronize()
