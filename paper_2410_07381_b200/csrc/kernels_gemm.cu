@@ -241,6 +241,19 @@ __device__ __forceinline__ void tmem_st32(uint32_t taddr, const uint32_t (&r)[32
   asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
 }
 
+// tcgen05.ld without the wait (the caller batches loads, then tmem_wait_ld)
+__device__ __forceinline__ void tmem_ld32_nw(uint32_t taddr, uint32_t (&r)[32]) {
+  asm volatile(
+      "tcgen05.ld.sync.aligned.32x32b.x32.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,"
+      "%16,%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31}, [%32];"
+      : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7]),
+        "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]), "=r"(r[15]),
+        "=r"(r[16]), "=r"(r[17]), "=r"(r[18]), "=r"(r[19]), "=r"(r[20]), "=r"(r[21]), "=r"(r[22]), "=r"(r[23]),
+        "=r"(r[24]), "=r"(r[25]), "=r"(r[26]), "=r"(r[27]), "=r"(r[28]), "=r"(r[29]), "=r"(r[30]), "=r"(r[31])
+      : "r"(taddr));
+}
+__device__ __forceinline__ void tmem_wait_ld() { asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory"); }
+
 __device__ __forceinline__ void tmem_ld32(uint32_t taddr, uint32_t (&r)[32]) {
   asm volatile(
       "tcgen05.ld.sync.aligned.32x32b.x32.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,"
@@ -1345,26 +1358,33 @@ struct AttnSoftmax {
     const float* other = red + (half ^ 1) * 256 + q * 32 + lane;
     if constexpr (MODE == 0) {
       float m = -INFINITY;
-      for (int c = 0; c < kcols; c += 32) {
-        uint32_t r[32];
-        tmem_ld32(lb + c, r);
+      for (int c = 0; c < kcols; c += 64) {   // two 32-column loads in flight per wait
+        uint32_t r[2][32];
+        tmem_ld32_nw(lb + c, r[0]);
+        tmem_ld32_nw(lb + c + 32, r[1]);
+        tmem_wait_ld();
 #pragma unroll
-        for (int e = 0; e < 32; ++e) m = fmaxf(m, __uint_as_float(r[e]) * p.scale);
+        for (int e = 0; e < 32; ++e) m = fmaxf(m, fmaxf(__uint_as_float(r[0][e]), __uint_as_float(r[1][e])) * p.scale);
       }
       mine[0] = m;
       asm volatile("bar.sync %0, 64;" ::"r"(1 + q) : "memory");
       m = fmaxf(m, other[0]);
       float sum = 0.f;
-      for (int c = 0; c < kcols; c += 32) {
-        uint32_t r[32];
-        tmem_ld32(lb + c, r);
+      for (int c = 0; c < kcols; c += 64) {
+        uint32_t r[2][32];
+        tmem_ld32_nw(lb + c, r[0]);
+        tmem_ld32_nw(lb + c + 32, r[1]);
+        tmem_wait_ld();
 #pragma unroll
         for (int e = 0; e < 32; ++e) {
-          const float v = __expf(__uint_as_float(r[e]) * p.scale - m);
-          sum += v;
-          r[e] = __float_as_uint(v);
+          const float v0 = __expf(__uint_as_float(r[0][e]) * p.scale - m);
+          const float v1 = __expf(__uint_as_float(r[1][e]) * p.scale - m);
+          sum += v0 + v1;
+          r[0][e] = __float_as_uint(v0);
+          r[1][e] = __float_as_uint(v1);
         }
-        tmem_st32(lb + c, r);   // exp(scale s - m) back in place
+        tmem_st32(lb + c, r[0]);   // exp(scale s - m) back in place
+        tmem_st32(lb + c + 32, r[1]);
       }
       mine[128] = sum;
       asm volatile("bar.sync %0, 64;" ::"r"(1 + q) : "memory");
@@ -1374,8 +1394,9 @@ struct AttnSoftmax {
       unsigned char* wst = stg + (size_t)warp * 4096;
       for (int c = 0; c < kcols; c += 64) {
         uint32_t r[2][32];
-        tmem_ld32(lb + c, r[0]);
-        tmem_ld32(lb + c + 32, r[1]);
+        tmem_ld32_nw(lb + c, r[0]);
+        tmem_ld32_nw(lb + c + 32, r[1]);
+        tmem_wait_ld();
         if (lane == 0) asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
         __syncwarp();
         unsigned char* srow = wst + (size_t)lane * 128;
@@ -1401,10 +1422,10 @@ struct AttnSoftmax {
       float dot = 0.f;
       for (int c = 0; c < kcols; c += 32) {
         uint32_t r[32];
-        tmem_ld32(lb + c, r);
         uint4 pv[4];
 #pragma unroll
         for (int v = 0; v < 4; ++v) pv[v] = __ldg(reinterpret_cast<const uint4*>(prow + c) + v);
+        tmem_ld32(lb + c, r);
 #pragma unroll
         for (int v = 0; v < 4; ++v) {
           const __nv_bfloat162* h2 = reinterpret_cast<const __nv_bfloat162*>(&pv[v]);
@@ -1421,11 +1442,12 @@ struct AttnSoftmax {
       unsigned char* wst = stg + (size_t)warp * 4096;
       for (int c = 0; c < kcols; c += 64) {
         uint32_t r[2][32];
-        tmem_ld32(lb + c, r[0]);
-        tmem_ld32(lb + c + 32, r[1]);
         uint4 pv[8];
 #pragma unroll
         for (int v = 0; v < 8; ++v) pv[v] = __ldg(reinterpret_cast<const uint4*>(prow + c) + v);
+        tmem_ld32_nw(lb + c, r[0]);
+        tmem_ld32_nw(lb + c + 32, r[1]);
+        tmem_wait_ld();
         if (lane == 0) asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
         __syncwarp();
         unsigned char* srow = wst + (size_t)lane * 128;
