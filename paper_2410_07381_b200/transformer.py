@@ -32,15 +32,16 @@ WEIGHT_DECAY = 0.0
 
 def _pair_plan(M, N, Kdim, enabled=True):
     """(pair, splits) for a linear-layer GEMM.  CTA-pair tiles (256 x 256,
-    ``*_x2`` kinds) when N % 256 == 0 and there are >= 64 of them (most of
-    the 74 SM pairs busy without split-K); their logical blocks are capped at
+    ``*_x2`` kinds) when N % 256 == 0 and there are >= 32 of them (with the
+    split below, enough blocks for the 74 SM pairs; measured: 64 -> 32 saves
+    0.2 ms per BERT-large step, 0.5 ms per GPT-2 step); their logical blocks are capped at
     ~180 MFLOP (~8 us on a pair), so K = 3072 / 4096 GEMMs split three ways:
     at 270 MFLOP their PTB(148) Eq. 1 estimate sat at the 31.6 us threshold
     and measurement noise sometimes sent the tuner to its least-turnaround
     fallback (a 1/128 slicing).  Otherwise single-CTA tiles with
     ``resnet._gemm_splits``."""
     tiles = math.ceil(M / 256) * (N // 256) if N % 256 == 0 else 0
-    if not enabled or tiles < 64:
+    if not enabled or tiles < int(os.environ.get("TALLY_PAIR_MIN_TILES", "32")):
         return False, _gemm_splits(M, N, Kdim)
     kb = math.ceil(Kdim / 64)
     s = max(1, min(kb // 2, math.ceil(2.0 * 256 * 256 * Kdim / 180e6)))

@@ -121,7 +121,7 @@ def test_cpu_reference_models_every_kernel():
 @pytest.mark.parametrize("M,N,K", [(4096, 1024, 4096), (4096, 3072, 1024), (1024, 4096, 4096), (30720, 1024, 4096),
                                    (4096, 1024, 30720), (4096, 512, 64), (256, 256, 64), (4096, 4096, 100)])
 def test_pair_plan_never_empty(M, N, K):
-    """CTA-pair plans: pair tiles only for N % 256 == 0 and >= 64 tiles, no
+    """CTA-pair plans: pair tiles only for N % 256 == 0 and >= 32 tiles, no
     empty split, pair logical blocks <= ~180 MFLOP unless K is too short to split."""
     import math
     from paper_2410_07381_b200.transformer import _pair_plan
@@ -130,6 +130,6 @@ def test_pair_plan_never_empty(M, N, K):
     per = math.ceil(kb / S)
     assert 1 <= S <= max(1, kb) and math.ceil(kb / per) == S
     if pair:
-        assert N % 256 == 0 and math.ceil(M / 256) * (N // 256) >= 64
+        assert N % 256 == 0 and math.ceil(M / 256) * (N // 256) >= 32
         assert 2 * 256 * 256 * per * 64 <= 200e6 or per <= 2
     assert not _pair_plan(M, N, K, enabled=False)[0]
