@@ -61,11 +61,15 @@ __device__ __forceinline__ void ld8f(const float* p, float (&f)[8]) {
 }
 
 constexpr int kRowsPerBlock = 8;   // one warp per row, 256 threads
-constexpr int kMaxVec = 8;         // row width <= 32 * 8 * 8 = 2048 elements
+// row width <= 32 * 8 * 4 = 1024 elements (BERT-large / GPT-2 / BERT-base):
+// the row lives in registers, and 2048-wide rows (kMaxVec 8) cost 168-197
+// registers -> one CTA (8 warps) per SM, layer norm at 0.2 of HBM
+constexpr int kMaxVec = 4;
 
 // ---------------------------------------------------------------- LayerNorm
 struct LayerNormFwd {
   static constexpr int kThreads = 256;
+  static constexpr int kMinBlocks = 2;
   struct Params {
     const uint4* x;
     uint4* y;
@@ -123,6 +127,7 @@ struct LayerNormFwd {
 
 struct LayerNormBwd {
   static constexpr int kThreads = 256;
+  static constexpr int kMinBlocks = 2;
   struct Params {
     const uint4* dy;
     const uint4* g2;     // optional gradient added to dx (the residual stream)
@@ -192,6 +197,7 @@ __device__ __forceinline__ float gelu_erf_grad(float x) {   // BERT "gelu": x * 
 
 struct GeluBwd {
   static constexpr int kThreads = 256;
+  static constexpr int kMinBlocks = 4;   // (PTB at 83 registers fitted 2 CTAs per SM: 0.7x of untransformed)
   static constexpr int kVec = 4;   // (8 measured slower untransformed: 33 -> 48 us per BERT-large launch)
   struct Params {
     const uint4* g;
