@@ -440,19 +440,22 @@ struct BnStats {
     if (flag[0]) {
       float a = 0.f, b = 0.f;
       fold(p.part, p.nrb, gi * kGroup, min(p.nrb, (gi + 1) * kGroup), p.C, c0, CB, red, &a, &b);
-      if (threadIdx.x < CB) {
-        p.part2[(long long)gi * p.C + c0 + threadIdx.x] = a;
-        p.part2[((long long)p.ngroups + gi) * p.C + c0 + threadIdx.x] = b;
+      const bool single = p.ngroups == 1;   // one group: its folder finalises (no level 2)
+      if (!single) {
+        if (threadIdx.x < CB) {
+          p.part2[(long long)gi * p.C + c0 + threadIdx.x] = a;
+          p.part2[((long long)p.ngroups + gi) * p.C + c0 + threadIdx.x] = b;
+        }
+        __syncthreads();
       }
-      __syncthreads();
       if (threadIdx.x == 0) {
         p.cnt1[bidx.x * p.ngroups + gi] = 0u;   // ready for the next launch
-        flag[1] = atom_add_acq_rel_gpu(&p.cnt2[bidx.x], 1u) + 1u == (unsigned)p.ngroups;
+        flag[1] = single || atom_add_acq_rel_gpu(&p.cnt2[bidx.x], 1u) + 1u == (unsigned)p.ngroups;
       }
       __syncthreads();
       if (flag[1]) {
         // ---- level 2: the last group finalises this channel block
-        fold(p.part2, p.ngroups, 0, p.ngroups, p.C, c0, CB, red, &a, &b);
+        if (!single) fold(p.part2, p.ngroups, 0, p.ngroups, p.C, c0, CB, red, &a, &b);
         if (threadIdx.x < CB) {
           const int ch = c0 + threadIdx.x;
           if constexpr (MODE == 0) {
@@ -478,7 +481,7 @@ struct BnStats {
             p.coef[2 * p.C + ch] = al * (k2 * isd * p.mean[ch] - k1);
           }
         }
-        if (threadIdx.x == 0) p.cnt2[bidx.x] = 0u;
+        if (threadIdx.x == 0 && !single) p.cnt2[bidx.x] = 0u;
       }
     }
     __syncthreads();

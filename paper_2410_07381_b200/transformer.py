@@ -52,7 +52,8 @@ def _rb_cols(P, C):
     """Rows per colstats logical block (~128 KB of gradient per block)."""
     base = 1024 if C < 128 else (512 if C < 256 else 256)
     cblocks = (C + 255) // 256
-    return max(8, min(base, P * cblocks // 296 // 8 * 8))
+    target = int(os.environ.get("TALLY_COLSTATS_BLOCKS", "296"))   # experiment knob
+    return max(8, min(base, P * cblocks // target // 8 * 8))
 
 
 class TransformerTrain:
