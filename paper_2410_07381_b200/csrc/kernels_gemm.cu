@@ -561,6 +561,9 @@ k_gemm(const __grid_constant__ GemmParams p, const ShapeArgs s) {
   if constexpr (PR == 2) cluster_sync_all();   // both CTAs' barriers initialised before any remote arrive
   else __syncthreads();
   fence_after();
+  // (programmatic dependent launch: the prologue above overlapped the predecessor's tail)
+  pdl_launch_dependents();
+  pdl_wait();
   const uint32_t tmem_base = *tmem_base_slot;
   bool stopped = false;
   unsigned long long blocks_run = 0;   // logical blocks this worker ran (PTB telemetry / retirement)

@@ -119,6 +119,13 @@ int Runtime::init(int dev, tally_gpu_info* out) {
   // Off by default -- measured on B200 (profiles/r01_summary.md): a max-shared
   // carveout costs the streaming HP kernel ~25 % (fewer L1 lines for loads
   // in flight), more than co-residency gains.
+  {
+    // programmatic dependent launch on best-effort streams (default on;
+    // TALLY_PDL=0 disables): BERT-large step 24.8 -> 23.1 ms, GPT-2 19.9 ->
+    // 19.4, ResNet-50 11.8 -> 11.4 (tools/step_time.py)
+    const char* pe = getenv("TALLY_PDL");
+    pdl = !(pe != nullptr && pe[0] == '0');
+  }
   const char* cv = getenv("TALLY_CARVEOUT");
   if (cv && strcmp(cv, "max") == 0) {
     for (int k = 0; k < nkinds; ++k) {
@@ -485,20 +492,30 @@ int Runtime::launch(int kernel, int stream, const tally_launch_desc* d, int* out
     CUresult cr = cu_launch((CUfunction)kk.cu_fn[idx], grid.x, grid.y, grid.z, (unsigned)in.threads, 1, 1,
                             (unsigned)in.smem, (CUstream)st, args, nullptr);
     if (cr != CUDA_SUCCESS) e = cudaErrorLaunchFailure;
-  } else if (kk.cluster > 1) {
-    // CTA-pair kinds: a cluster launch (the pair shares one tile, cta_group::2)
+  } else if (kk.cluster > 1 || (pdl && stream_be[(size_t)stream] && !L->timed)) {
+    // CTA-pair kinds: a cluster launch (the pair shares one tile, cta_group::2);
+    // best-effort streams with TALLY_PDL: programmatic dependent launch
     cudaLaunchConfig_t cfg{};
     cfg.gridDim = grid;
     cfg.blockDim = dim3(in.threads);
     cfg.dynamicSmemBytes = in.smem;
     cfg.stream = st;
-    cudaLaunchAttribute attr[1];
-    attr[0].id = cudaLaunchAttributeClusterDimension;
-    attr[0].val.clusterDim.x = (unsigned)kk.cluster;
-    attr[0].val.clusterDim.y = 1;
-    attr[0].val.clusterDim.z = 1;
+    cudaLaunchAttribute attr[2];
+    unsigned na = 0;
+    if (kk.cluster > 1) {
+      attr[na].id = cudaLaunchAttributeClusterDimension;
+      attr[na].val.clusterDim.x = (unsigned)kk.cluster;
+      attr[na].val.clusterDim.y = 1;
+      attr[na].val.clusterDim.z = 1;
+      ++na;
+    }
+    if (pdl && stream_be[(size_t)stream] && !L->timed) {
+      attr[na].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+      attr[na].val.programmaticStreamSerializationAllowed = 1;
+      ++na;
+    }
     cfg.attrs = attr;
-    cfg.numAttrs = 1;
+    cfg.numAttrs = na;
     e = cudaLaunchKernelExC(&cfg, fn, args);
   } else {
     e = cudaLaunchKernel(fn, grid, dim3(in.threads), args, in.smem, st);
@@ -1035,6 +1052,7 @@ int tally_stream_create(int prio, int* out) {
      "cudaStreamCreateWithPriority");
   *out = (int)r.streams.size();
   r.streams.push_back(s);
+  r.stream_be.push_back(prio == TALLY_BEST_EFFORT ? 1 : 0);
   return TALLY_OK;
 }
 

@@ -58,6 +58,8 @@ struct Runtime {
   int nkinds = 0;
   std::vector<std::unique_ptr<Instance>> instances;
   std::vector<cudaStream_t> streams;
+  std::vector<char> stream_be;   // best-effort class (programmatic dependent launch when enabled)
+  bool pdl = false;              // TALLY_PDL=1
   int prio_low = 0, prio_high = 0;
   cudaStream_t sig_stream = nullptr;
 

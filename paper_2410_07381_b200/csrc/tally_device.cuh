@@ -179,6 +179,14 @@ __device__ __forceinline__ float4 ld_stream(const float4* p) {
   return v;
 }
 
+// Programmatic dependent launch (best-effort streams, runtime option): a
+// kernel lets its successor's CTAs be scheduled as soon as all of its own
+// CTAs are running, and waits for its predecessor's completion (memory
+// visible) before touching global memory -- the successor's launch and
+// prologue overlap the predecessor's tail.  No-ops without the attribute.
+__device__ __forceinline__ void pdl_launch_dependents() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
+__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+
 __device__ __forceinline__ uint3 delinearize(unsigned long long t, uint3 g) {
   // ref ir/core.py:59-65: x fastest.  1-D grids (every built-in kind but the
   // channel-blocked statistics) need no division; 32-bit math when the index
@@ -233,6 +241,8 @@ template <class Body>
 __global__ void __launch_bounds__(Body::kThreads, MinBlocks<Body>::value)
 k_original(const __grid_constant__ typename Body::Params p, const SliceArgs s) {
   extern __shared__ __align__(1024) char smem[];
+  pdl_launch_dependents();
+  pdl_wait();
   const uint3 g = make_uint3(gridDim.x, gridDim.y, gridDim.z);
   if (s.exec_count != nullptr && threadIdx.x == 0)
     atomicAdd(&s.exec_count[linear_index(blockIdx, g)], 1ull);
@@ -249,6 +259,8 @@ template <class Body>
 __global__ void __launch_bounds__(Body::kThreads, MinBlocks<Body>::value)
 k_sliced(const __grid_constant__ typename Body::Params p, const SliceArgs s) {
   extern __shared__ __align__(1024) char smem[];
+  pdl_launch_dependents();
+  pdl_wait();
   const uint3 b = s.linear ? delinearize(s.linear_offset + blockIdx.x, s.grid)
                            : make_uint3(blockIdx.x + s.offset.x, blockIdx.y + s.offset.y,
                                         blockIdx.z + s.offset.z);
@@ -506,6 +518,8 @@ template <class Body>
 __global__ void __launch_bounds__(Body::kThreads, MinBlocks<Body>::value)
 k_ptb(const __grid_constant__ typename Body::Params p, const PtbArgs a) {
   extern __shared__ __align__(1024) char smem[];
+  pdl_launch_dependents();
+  pdl_wait();
   __shared__ long long s_task[2];
   const bool leader = (threadIdx.x == 0);
   const unsigned long long t_entry = leader ? globaltimer() : 0ull;
