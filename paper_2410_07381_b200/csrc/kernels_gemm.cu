@@ -1311,6 +1311,33 @@ struct AttnSoftmax {
     float scale;
   };
 
+  static __device__ __forceinline__ uint32_t* tmem_slot(char* smem_raw) {
+    unsigned char* sm = reinterpret_cast<unsigned char*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+    float* red = reinterpret_cast<float*>(sm + 5 * kTileBytes + 8 * 4096);
+    return reinterpret_cast<uint32_t*>(reinterpret_cast<uint64_t*>(red + 2 * 2 * 128) + 2);
+  }
+  // TMEM once per CTA (all 512 columns), taken before the CTA lets a
+  // programmatic dependent launch begin: a successor GEMM CTA waiting for this
+  // kernel can then never hold columns this CTA needs for its next block
+  static __device__ __forceinline__ void cta_init(char* smem_raw) {
+    if ((threadIdx.x >> 5) == 0)
+      asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(tmem_slot(smem_raw))),
+                   "n"(512));
+    fence_before();
+    __syncthreads();
+    fence_after();
+  }
+  static __device__ __forceinline__ void cta_exit(char* smem_raw) {
+    fence_before();
+    __syncthreads();
+    fence_after();
+    if ((threadIdx.x >> 5) == 0) {
+      const uint32_t t = *tmem_slot(smem_raw);
+      asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+      asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(t), "n"(512));
+    }
+  }
+
   static __device__ __forceinline__ void run(const Params& p, uint3 bidx, uint3, char* smem_raw) {
     unsigned char* sm = reinterpret_cast<unsigned char*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
     unsigned char* sa = sm;                          // A tile (128 x 64)
@@ -1327,12 +1354,8 @@ struct AttnSoftmax {
       mbar_init(&bar[1], 1);
       asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     }
-    if (warp == 0)   // (no relinquish: a PTB worker allocates again for its next logical block)
-      asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(tslot)), "n"(512));
-    fence_before();
     __syncthreads();
-    fence_after();
-    const uint32_t tmem = *tslot;
+    const uint32_t tmem = *tslot;   // allocated in cta_init
     if (threadIdx.x == 0) {
       mbar_expect_tx(&bar[0], (uint32_t)(kTileBytes * (1 + nkb)));
       tma_load_2d(sa, &p.a_map, &bar[0], (int)(p.a_col0 + h * p.a_col_h), b * p.T + r0);
@@ -1476,9 +1499,8 @@ struct AttnSoftmax {
     }
     if (lane == 0) asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
     fence_before();
-    __syncthreads();
+    __syncthreads();   // TMEM reads done, staging free, barriers reusable by the next block
     fence_after();
-    if (warp == 0) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "n"(512));
   }
 };
 

@@ -225,6 +225,20 @@ struct MinBlocks<B, void_t_<decltype(B::kMinBlocks)>> {
   static constexpr int value = B::kMinBlocks;
 };
 
+// Optional per-CTA hooks of a body: `static __device__ void cta_init(char*
+// smem)` runs once when the CTA starts -- before it lets a programmatic
+// dependent launch begin, so resources it takes there (TMEM) cannot be taken
+// first by a successor kernel that then waits for it -- and `cta_exit(char*
+// smem)` once after the CTA's last logical block.
+template <class B, class = void>
+struct HasCtaHooks {
+  static constexpr bool value = false;
+};
+template <class B>
+struct HasCtaHooks<B, void_t_<decltype(&B::cta_init)>> {
+  static constexpr bool value = true;
+};
+
 __device__ __forceinline__ unsigned smid();
 
 // Per-logical-block event log (ref sim.py:436-505 BlockStarted / BlockFinished
@@ -241,6 +255,7 @@ template <class Body>
 __global__ void __launch_bounds__(Body::kThreads, MinBlocks<Body>::value)
 k_original(const __grid_constant__ typename Body::Params p, const SliceArgs s) {
   extern __shared__ __align__(1024) char smem[];
+  if constexpr (HasCtaHooks<Body>::value) Body::cta_init(smem);
   pdl_launch_dependents();
   pdl_wait();
   const uint3 g = make_uint3(gridDim.x, gridDim.y, gridDim.z);
@@ -252,6 +267,7 @@ k_original(const __grid_constant__ typename Body::Params p, const SliceArgs s) {
     __syncthreads();
     if (threadIdx.x == 0) log_block(s.block_log, linear_index(blockIdx, g), t0, smid());
   }
+  if constexpr (HasCtaHooks<Body>::value) Body::cta_exit(smem);
 }
 
 // --- Sliced: block offset + pinned gridDim ------------------------------------
@@ -259,6 +275,7 @@ template <class Body>
 __global__ void __launch_bounds__(Body::kThreads, MinBlocks<Body>::value)
 k_sliced(const __grid_constant__ typename Body::Params p, const SliceArgs s) {
   extern __shared__ __align__(1024) char smem[];
+  if constexpr (HasCtaHooks<Body>::value) Body::cta_init(smem);
   pdl_launch_dependents();
   pdl_wait();
   const uint3 b = s.linear ? delinearize(s.linear_offset + blockIdx.x, s.grid)
@@ -272,6 +289,7 @@ k_sliced(const __grid_constant__ typename Body::Params p, const SliceArgs s) {
     __syncthreads();
     if (threadIdx.x == 0) log_block(s.block_log, linear_index(b, s.grid), t0, smid());
   }
+  if constexpr (HasCtaHooks<Body>::value) Body::cta_exit(smem);
 }
 
 // --- PTB: persistent, preemptible workers -------------------------------------
@@ -518,6 +536,7 @@ template <class Body>
 __global__ void __launch_bounds__(Body::kThreads, MinBlocks<Body>::value)
 k_ptb(const __grid_constant__ typename Body::Params p, const PtbArgs a) {
   extern __shared__ __align__(1024) char smem[];
+  if constexpr (HasCtaHooks<Body>::value) Body::cta_init(smem);
   pdl_launch_dependents();
   pdl_wait();
   __shared__ long long s_task[2];
@@ -609,6 +628,7 @@ k_ptb(const __grid_constant__ typename Body::Params p, const PtbArgs a) {
     if (leader && a.block_log != nullptr)
       log_block(a.block_log, (unsigned long long)task, t0, ((unsigned long long)blockIdx.x << 32) | smid());
   }
+  if constexpr (HasCtaHooks<Body>::value) Body::cta_exit(smem);
   if (leader) {
     if (a.worker_log != nullptr) {
       unsigned long long* w = a.worker_log + 4ull * blockIdx.x;
