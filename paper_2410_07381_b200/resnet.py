@@ -31,6 +31,7 @@ into a CUDA graph, launched as one exempt pipeline step at top priority.
 from __future__ import annotations
 
 import math
+import os
 from dataclasses import dataclass
 
 from . import kernels as K
@@ -77,6 +78,24 @@ def _gemm_splits(M, N, Kdim):
         want = max(want, tiles * math.ceil(kb / max(2, 262144 // per_kb)))
     s = max(1, min(kb // 2, math.ceil(want / tiles)))
     return math.ceil(kb / math.ceil(kb / s))
+
+
+def _pair_plan(M, N, Kdim, enabled=True):
+    """(pair, splits) for a linear-layer GEMM.  CTA-pair tiles (256 x 256,
+    ``*_x2`` kinds) when N % 256 == 0 and there are >= 32 of them (with the
+    split below, enough blocks for the 74 SM pairs; measured: 64 -> 32 saves
+    0.2 ms per BERT-large step, 0.5 ms per GPT-2 step); their logical blocks are capped at
+    ~180 MFLOP (~8 us on a pair), so K = 3072 / 4096 GEMMs split three ways:
+    at 270 MFLOP their PTB(148) Eq. 1 estimate sat at the 31.6 us threshold
+    and measurement noise sometimes sent the tuner to its least-turnaround
+    fallback (a 1/128 slicing).  Otherwise single-CTA tiles with
+    ``resnet._gemm_splits``."""
+    tiles = math.ceil(M / 256) * (N // 256) if N % 256 == 0 else 0
+    if not enabled or tiles < int(os.environ.get("TALLY_PAIR_MIN_TILES", "32")):
+        return False, _gemm_splits(M, N, Kdim)
+    kb = math.ceil(Kdim / 64)
+    s = max(1, min(kb // 2, math.ceil(2.0 * 256 * 256 * Kdim / 180e6)))
+    return True, math.ceil(kb / math.ceil(kb / s))
 
 
 @dataclass
@@ -167,6 +186,9 @@ class ResNet50Train:
     holds the input batch [B, 224, 224, 8] bf16 and labels [B] int32 (refill
     them between steps); ``loss`` [B] fp32 holds per-sample losses after a
     step.  ``image`` may be smaller than 224 for tests (>= 32)."""
+
+    # CTA-pair tcgen05 GEMMs where N % 256 == 0 and >= 32 pair tiles (_pair_plan)
+    pair_gemms = os.environ.get("TALLY_RESNET_PAIR", "1") != "0"
 
     def __init__(self, batch=64, image=224, lr=0.1, seed=0, device="cuda", model=None):
         import torch
@@ -318,12 +340,12 @@ class ResNet50Train:
         torch = self.torch
         M, Kd = A.shape
         N = B.shape[0]
-        S = _gemm_splits(M, N, Kd)
+        pair, S = _pair_plan(M, N, Kd, self.pair_gemms)
         if S == 1:
-            self._add(name, K.gemm(A, B, out))
+            self._add(name, K.gemm(A, B, out, pair=pair))
             return
         ws = self._scr("splitk", S * M * N, torch.float32).view(S, M, N)
-        self._add(name, K.gemm(A, B, ws, splits=S))
+        self._add(name, K.gemm(A, B, ws, splits=S, pair=pair))
         self._add(name + ".reduce", K.splitk_reduce(ws, out))
 
     def _bn_fwd(self, bn, y, P, relu, res=None):
@@ -357,9 +379,9 @@ class ResNet50Train:
         s = conv.spec
         P = self.B * s.oh * s.ow
         # weight gradient: dW[Cout, Kp] = dy^T . A, both read MN-major as stored
-        S = _gemm_splits(s.cout, s.kp, P)
+        pair, S = _pair_plan(s.cout, s.kp, P, self.pair_gemms)
         conv.gpart = torch.empty(S, s.cout, s.kp, dtype=torch.float32, device=self.device)
-        self._add(s.name + ".wgrad", K.gemm_mn(dy, A, conv.gpart, splits=S))
+        self._add(s.name + ".wgrad", K.gemm_mn(dy, A, conv.gpart, splits=S, pair=pair))
         self.sgd.add(conv.w, conv.v, conv.gpart, S, s.cout * s.kp, WEIGHT_DECAY, conv.wb, conv.wt,
                      s.cout, s.kp)
         if not need_dx:
@@ -389,7 +411,7 @@ class ResNet50Train:
             if not s.direct:
                 dcol = max(dcol, P * s.kp)
             for (M, N, Kd) in ((P, s.cout, s.kp), (P, s.kp, s.cout)):     # forward, dgrad
-                S = _gemm_splits(M, N, Kd)
+                S = _pair_plan(M, N, Kd, self.pair_gemms)[1]
                 if S > 1:
                     splitk = max(splitk, S * M * N)
         self._reserve("splitk", max(splitk, 8), torch.float32)

@@ -24,28 +24,10 @@ import math
 import os
 
 from . import kernels as K
-from .resnet import SgdTable, _gemm_splits
+from .resnet import SgdTable, _gemm_splits, _pair_plan  # noqa: F401
 
 MOMENTUM = 0.9
 WEIGHT_DECAY = 0.0
-
-
-def _pair_plan(M, N, Kdim, enabled=True):
-    """(pair, splits) for a linear-layer GEMM.  CTA-pair tiles (256 x 256,
-    ``*_x2`` kinds) when N % 256 == 0 and there are >= 32 of them (with the
-    split below, enough blocks for the 74 SM pairs; measured: 64 -> 32 saves
-    0.2 ms per BERT-large step, 0.5 ms per GPT-2 step); their logical blocks are capped at
-    ~180 MFLOP (~8 us on a pair), so K = 3072 / 4096 GEMMs split three ways:
-    at 270 MFLOP their PTB(148) Eq. 1 estimate sat at the 31.6 us threshold
-    and measurement noise sometimes sent the tuner to its least-turnaround
-    fallback (a 1/128 slicing).  Otherwise single-CTA tiles with
-    ``resnet._gemm_splits``."""
-    tiles = math.ceil(M / 256) * (N // 256) if N % 256 == 0 else 0
-    if not enabled or tiles < int(os.environ.get("TALLY_PAIR_MIN_TILES", "32")):
-        return False, _gemm_splits(M, N, Kdim)
-    kb = math.ceil(Kdim / 64)
-    s = max(1, min(kb // 2, math.ceil(2.0 * 256 * 256 * Kdim / 180e6)))
-    return True, math.ceil(kb / math.ceil(kb / s))
 
 
 def _rb_cols(P, C):
