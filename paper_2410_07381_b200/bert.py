@@ -163,13 +163,11 @@ class BertTrain(TransformerTrain):
             da = self._linear_bwd(pre + "output.dense", lay["fc2"], dh2, sv["a"])
             du = self._buf(N, lay["fc"].out)
             self._add(pre + "intermediate.gelu_bwd", K.gelu_bwd(da, sv["hpre"], du, erf=True))
-            dx1f = self._linear_bwd(pre + "intermediate.dense", lay["fc"], du, sv["x1"])
-            dx1 = self._add_tensors(pre + "output.residual_grad", dx1f, dh2)
+            dx1 = self._linear_bwd(pre + "intermediate.dense", lay["fc"], du, sv["x1"], res=dh2)   # + residual grad
             dh1 = self._ln_bwd(pre + "attention.output.LayerNorm", lay["ln1"], dx1, sv["h1"])
             do = self._linear_bwd(pre + "attention.output.dense", lay["proj"], dh1, sv["o"])
             dqkv = self._attn_bwd(pre + "attention.self", sv["qkv"], sv["P"], do, dP, dS)
-            dxa = self._linear_bwd(pre + "attention.self.qkv", lay["qkv"], dqkv, sv["x"])
-            dx = self._add_tensors(pre + "attention.residual_grad", dxa, dh1)
+            dx = self._linear_bwd(pre + "attention.self.qkv", lay["qkv"], dqkv, sv["x"], res=dh1)
             self.block_grads[pre] = dict(g=g, dx=dx)
             g = dx
         self.saved = saved

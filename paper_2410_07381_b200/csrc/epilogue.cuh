@@ -9,7 +9,8 @@
 namespace tally {
 
 struct EpArgs {
-  const float* bias;             // [C] fp32 (null: no fused epilogue)
+  int on;                        // 0: no fused epilogue
+  const float* bias;             // optional [C] fp32
   const __nv_bfloat16* res;      // optional residual, row-major with pitch ldr
   __nv_bfloat16* pre;            // optional pre-activation output (splitk_reduce; the GEMM uses a TMA map)
   long long ldr;                 // residual / pre row pitch (elements)
@@ -28,10 +29,12 @@ __device__ __forceinline__ float ep_act(float x, int act) {
 
 // 8 consecutive columns [col, col + 8) of row `row`: add bias (+ residual)
 __device__ __forceinline__ void ep_bias_res8(const EpArgs& e, long long row, int col, float (&x)[8]) {
-  const float4 b0 = __ldg(reinterpret_cast<const float4*>(e.bias + col));
-  const float4 b1 = __ldg(reinterpret_cast<const float4*>(e.bias + col + 4));
-  x[0] += b0.x; x[1] += b0.y; x[2] += b0.z; x[3] += b0.w;
-  x[4] += b1.x; x[5] += b1.y; x[6] += b1.z; x[7] += b1.w;
+  if (e.bias != nullptr) {
+    const float4 b0 = __ldg(reinterpret_cast<const float4*>(e.bias + col));
+    const float4 b1 = __ldg(reinterpret_cast<const float4*>(e.bias + col + 4));
+    x[0] += b0.x; x[1] += b0.y; x[2] += b0.z; x[3] += b0.w;
+    x[4] += b1.x; x[5] += b1.y; x[6] += b1.z; x[7] += b1.w;
+  }
   if (e.res != nullptr) {
     const uint4 r = __ldg(reinterpret_cast<const uint4*>(e.res + row * e.ldr + col));
     const __nv_bfloat162* h = reinterpret_cast<const __nv_bfloat162*>(&r);

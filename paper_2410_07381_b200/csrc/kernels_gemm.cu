@@ -1022,7 +1022,7 @@ k_gemm(const __grid_constant__ GemmParams p, const ShapeArgs s) {
           if (lane == 0) tma_store_2d(map, wst, ycol, yrow);
           __syncwarp();
         };
-        if (p.ep.bias != nullptr) {
+        if (p.ep.on) {
           // fused linear-layer epilogue on the fp32 accumulator
           const long long row = min((long long)(yrow + lane), (long long)p.m - 1);   // (rows past M: clipped by the map)
 #pragma unroll
@@ -1654,12 +1654,13 @@ static int bind_gemm(const tally_kernel_args* a, Instance* inst, bool split) {
   // fused linear-layer epilogue: ptr[4] bias (fp32 [N]), ptr[5] residual (bf16,
   // pitch ldc), ptr[6] pre-activation output (bf16, pitch ldc); i[6] activation
   if (!split && (a->ptr[4] || a->ptr[5] || a->ptr[6] || a->i[6])) {
-    if (Cfg::KIND != 1 || sizeof(typename Cfg::OutT) != 2 || !p.c_tma || !a->ptr[4] || a->i[6] < 0 || a->i[6] > 3 ||
-        !aligned16_(a->ptr[4]) || (a->ptr[5] && !aligned16_(a->ptr[5]))) {
+    if (Cfg::KIND != 1 || sizeof(typename Cfg::OutT) != 2 || !p.c_tma || a->i[6] < 0 || a->i[6] > 3 ||
+        (a->ptr[4] && !aligned16_(a->ptr[4])) || (a->ptr[5] && !aligned16_(a->ptr[5]))) {
       set_error("gemm: a fused epilogue (bias, residual, pre, act) needs a plain bf16 GEMM with the TMA-store "
-                "epilogue, 16-byte aligned fp32 bias, act 0-3");
+                "epilogue, 16-byte aligned fp32 bias / residual, act 0-3");
       return TALLY_EINVAL;
     }
+    p.ep.on = 1;
     p.ep.bias = static_cast<const float*>(a->ptr[4]);
     p.ep.res = static_cast<const __nv_bfloat16*>(a->ptr[5]);
     p.ep.ldr = p.ldc;
@@ -1670,7 +1671,7 @@ static int bind_gemm(const tally_kernel_args* a, Instance* inst, bool split) {
       if (rc) return rc;
       p.ep_pre = 1;
     }
-    inst->alg_bytes_extra_ep = 4.0 * N + (a->ptr[5] ? 2.0 * M * N : 0.0) + (a->ptr[6] ? 2.0 * M * N : 0.0);
+    inst->alg_bytes_extra_ep = (a->ptr[4] ? 4.0 * N : 0.0) + (a->ptr[5] ? 2.0 * M * N : 0.0) + (a->ptr[6] ? 2.0 * M * N : 0.0);
   }
   p.kb_per_split = (int)((KBlocks + splits - 1) / splits);
   if ((KBlocks + p.kb_per_split - 1) / p.kb_per_split != splits) {

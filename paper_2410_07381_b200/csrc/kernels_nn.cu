@@ -1023,7 +1023,7 @@ struct SplitKReduce {
   };
   // the finished sum of output vector v (8 bf16 of a row-major [rows, C] output)
   static __device__ __forceinline__ void finish8(const Params& p, long long v, float (&acc)[8]) {
-    if (p.ep.bias != nullptr) {
+    if (p.ep.on) {
       const long long e0 = 8 * v;
       const long long row = e0 / p.C;
       const int col = (int)(e0 - row * p.C);
@@ -1564,17 +1564,18 @@ static int bind_splitk_reduce(const tally_kernel_args* a, Instance* inst) {
   double ep_bytes = 0.0;
   if (a->ptr[2] || a->ptr[3] || a->ptr[4] || a->i[3]) {
     p.C = (int)a->i[2];
-    if (!a->ptr[2] || p.C < 8 || p.C % 8 || n % p.C || a->i[3] < 0 || a->i[3] > 3 || !aligned16(a->ptr[2]) ||
+    if (p.C < 8 || p.C % 8 || n % p.C || a->i[3] < 0 || a->i[3] > 3 || (a->ptr[2] && !aligned16(a->ptr[2])) ||
         (a->ptr[3] && !aligned16(a->ptr[3])) || (a->ptr[4] && !aligned16(a->ptr[4]))) {
-      set_error("splitk_reduce: a fused epilogue needs an aligned fp32 bias, C %% 8 == 0 dividing n, act 0-3");
+      set_error("splitk_reduce: a fused epilogue needs aligned fp32 bias / bf16 residual, C %% 8 == 0 dividing n, act 0-3");
       return TALLY_EINVAL;
     }
+    p.ep.on = 1;
     p.ep.bias = static_cast<const float*>(a->ptr[2]);
     p.ep.res = static_cast<const __nv_bfloat16*>(a->ptr[3]);
     p.ep.pre = static_cast<__nv_bfloat16*>(a->ptr[4]);
     p.ep.ldr = p.C;
     p.ep.act = (int)a->i[3];
-    ep_bytes = 4.0 * p.C + (a->ptr[3] ? 2.0 * n : 0.0) + (a->ptr[4] ? 2.0 * n : 0.0);
+    ep_bytes = (a->ptr[2] ? 4.0 * p.C : 0.0) + (a->ptr[3] ? 2.0 * n : 0.0) + (a->ptr[4] ? 2.0 * n : 0.0);
   }
   // ~64 KB of partials per logical block: 512 vectors up to S = 4, then
   // halving down to 32 vectors (S >= 33)

@@ -484,8 +484,9 @@ def splitk_reduce(parts, out, bias=None, res=None, pre=None, act=0) -> DeviceKer
     epilogue out = act(sum + bias (+ res)), ``pre`` receiving the
     pre-activation values (as ``bias_act``)."""
     C = out.shape[-1]
+    ep = bias is not None or res is not None or pre is not None or act
     return DeviceKernel("splitk_reduce", (parts, out, bias, res, pre),
-                        (out.numel(), parts.shape[0], C if bias is not None else 0, act))
+                        (out.numel(), parts.shape[0], C if ep else 0, act))
 
 
 def bn_finalize_fwd(part, nrb, C, count, gamma, beta, mean, invstd, scale, shift,

@@ -170,23 +170,31 @@ class TransformerTrain:
             self._wsbuf = cur = self.torch.empty(numel, dtype=self.torch.float32, device=self.device)
         return cur[:numel]
 
-    def _gemm_ex_splitk(self, name, A, B, out, M, N, Kd, b_mn=False):
+    def _gemm_ex_splitk(self, name, A, B, out, M, N, Kd, b_mn=False, res=None):
         """out (bf16) = A . B^T.  GEMMs with few, long output tiles (an LM-head
         dgrad with K = vocab; BERT-large's K = 4096 FFN GEMMs: 256 tiles of
         134 MFLOP) run split-K into an fp32 workspace + splitk_reduce, so their
         logical blocks are <= ~40 MFLOP (resnet._gemm_splits): short enough
         for a PTB configuration to meet the turnaround threshold, where the
         reference's fallback (least turnaround) would otherwise pick a 1/256
-        slicing at 200x the latency."""
+        slicing at 200x the latency.  ``res``: out = A . B^T + res (a
+        residual-stream gradient), fused into the split-K reduce or the GEMM's
+        TMA-store epilogue; returns False when it could not be fused."""
         pair, S = _pair_plan(M, N, Kd, self.pair_gemms)
         if S == 1:
-            self._add(name, K.gemm_ex(A, B, out, M, N, Kd, b_mn=b_mn, pair=pair))
-            return
+            fuse = res is not None and "res" in self.fuse_epilogue and (pair or N % 128 == 0)
+            self._add(name, K.gemm_ex(A, B, out, M, N, Kd, b_mn=b_mn, pair=pair, res=res if fuse else None))
+            return fuse or res is None
         ws = self._ws(S * M * N).view(S * M, N)
         self._add(name, K.gemm_ex(A, B, ws, M, N, Kd, b_mn=b_mn, splits=S, pair=pair))
-        self._add(name + ".reduce", K.splitk_reduce(ws.view(S, M, N), out))
+        fuse = res is not None and "res" in self.fuse_epilogue
+        self._add(name + ".reduce", K.splitk_reduce(ws.view(S, M, N), out, res=res if fuse else None))
+        return fuse or res is None
 
-    def _linear_bwd(self, name, lin, dy, x, need_dx=True):
+    def _linear_bwd(self, name, lin, dy, x, need_dx=True, res=None):
+        """Bias and weight gradients of a linear layer; returns dx (+ ``res``,
+        a residual-stream gradient added in the dgrad's epilogue when it can
+        be fused, else by bias_act)."""
         lin.b.g = self.torch.zeros(lin.out, device=self.device)
         self._colsum(name + ".dbias", dy, lin.b.g)
         self.sgd.add(lin.b.w, lin.b.v, lin.b.g.view(1, -1), 1, lin.out, WEIGHT_DECAY)
@@ -194,7 +202,8 @@ class TransformerTrain:
         if not need_dx:
             return None
         dx = self._buf(self.N, lin.inp)
-        self._gemm_ex_splitk(name + ".dgrad", dy, lin.wb, dx, self.N, lin.inp, lin.out, b_mn=True)
+        if not self._gemm_ex_splitk(name + ".dgrad", dy, lin.wb, dx, self.N, lin.inp, lin.out, b_mn=True, res=res):
+            return self._add_tensors(name + ".residual_grad", dx, res)
         return dx
 
     def _ln_fwd(self, name, ln, x):
