@@ -130,6 +130,17 @@ typedef struct {
   long long c_row_off[2], c_col_off[2];
 } tally_gemm_layout;
 
+/* Convolution geometry of the implicit-GEMM kinds (tally_kernel_args.ptr[3],
+ * host memory, read at tally_kernel_create): NHWC bf16 input [n, h, w, c],
+ * square k x k filter, stride, padding; c % 64 == 0.  "conv_fprop_*": A =
+ * im2col(x) by TMA im2col loads (no column matrix), B = weights [cout, k*k*c]
+ * in (kh, kw, c) order; "conv_wgrad_*": dW[cout, k*k*c] = dy^T . im2col(x),
+ * A = dy [P, cout] (MN-major), B = im2col(x) by TMA im2col loads. */
+typedef struct {
+  int n, h, w, c;
+  int k, stride, pad;
+} tally_conv_geometry;
+
 typedef struct {
   unsigned grid_x, grid_y, grid_z;  /* logical grid (the untransformed launch)  */
   long long total_blocks;

@@ -61,6 +61,11 @@ class c_gemm_layout(C.Structure):
                 ("c_row_off", C.c_longlong * 2), ("c_col_off", C.c_longlong * 2)]
 
 
+class c_conv_geometry(C.Structure):
+    _fields_ = [("n", C.c_int), ("h", C.c_int), ("w", C.c_int), ("c", C.c_int),
+                ("k", C.c_int), ("stride", C.c_int), ("pad", C.c_int)]
+
+
 class c_kernel_info(C.Structure):
     _fields_ = [("grid_x", C.c_uint), ("grid_y", C.c_uint), ("grid_z", C.c_uint),
                 ("total_blocks", C.c_longlong), ("threads_per_block", C.c_int),

@@ -167,6 +167,19 @@ __device__ __forceinline__ void umma_pair(uint32_t tmem_d, uint64_t a, uint64_t 
       "l"(a), "l"(b), "r"(idesc), "r"(acc));
 }
 
+// TMA im2col load: a box of pixels x 64 channels of an NHWC tensor, starting
+// at the output pixel whose input window origin is (w, h) of image n,
+// shifted by the filter tap (off_w, off_h); out-of-image pixels read zero
+__device__ __forceinline__ void tma_load_im2col(void* dst, const CUtensorMap* map, uint64_t* bar, int c, int w,
+                                                int h, int n, int off_w, int off_h) {
+  asm volatile(
+      "cp.async.bulk.tensor.4d.shared::cluster.global.im2col.mbarrier::complete_tx::bytes"
+      " [%0], [%1, {%3, %4, %5, %6}], [%2], {%7, %8};" ::"r"(smem_u32(dst)),
+      "l"(map), "r"(smem_u32(bar)), "r"(c), "r"(w), "r"(h), "r"(n), "h"((unsigned short)off_w),
+      "h"((unsigned short)off_h)
+      : "memory");
+}
+
 __device__ __forceinline__ void fence_after() { asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory"); }
 __device__ __forceinline__ void fence_before() { asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory"); }
 
@@ -322,10 +335,12 @@ using CfgTf32x3N64 = CfgTf32x3T<64, 4>;
 #ifndef TALLY_STAGES_PAIR
 #define TALLY_STAGES_PAIR 6
 #endif
-template <int BN_, class OutT_, bool A_MN_ = false, bool B_MN_ = false, int PAIR_ = 1>
+template <int BN_, class OutT_, bool A_MN_ = false, bool B_MN_ = false, int PAIR_ = 1, int CONV_ = 0>
 struct CfgBf16T {
   static constexpr int KIND = 1;
   static constexpr int PAIR = PAIR_;
+  // implicit-GEMM convolution: 1 = A by TMA im2col (forward), 2 = B by TMA im2col (weight gradient)
+  static constexpr int CONV = CONV_;
   static constexpr int BM = 128, BN = BN_;            // BM: rows per CTA; BN: MMA N (the pair's tile width)
   static constexpr int B_ROWS = BN / PAIR;            // B rows (N) this CTA loads
   static constexpr int BK = 64;                       // bf16 elements = 128 B
@@ -376,6 +391,17 @@ using CfgBf16F32X2 = CfgBf16T<256, float, false, false, 2>;
 using CfgBf16MNX2 = CfgBf16T<256, float, true, true, 2>;
 using CfgBf16KMNX2 = CfgBf16T<256, __nv_bfloat16, false, true, 2>;
 using CfgBf16F32KMNX2 = CfgBf16T<256, float, false, true, 2>;
+// implicit-GEMM convolution kinds (A / B operand gathered by TMA im2col)
+using CfgConvF = CfgBf16T<128, __nv_bfloat16, false, false, 1, 1>;
+using CfgConvFN64 = CfgBf16T<64, __nv_bfloat16, false, false, 1, 1>;
+using CfgConvF32 = CfgBf16T<128, float, false, false, 1, 1>;
+using CfgConvF32N64 = CfgBf16T<64, float, false, false, 1, 1>;
+using CfgConvW = CfgBf16T<128, float, true, true, 1, 2>;
+using CfgConvWN64 = CfgBf16T<64, float, true, true, 1, 2>;
+template <class Cfg, class = void>
+struct ConvOf { static constexpr int value = 0; };
+template <class Cfg>
+struct ConvOf<Cfg, void_t_<decltype(Cfg::CONV)>> { static constexpr int value = Cfg::CONV; };
 template <class Cfg, class = void>
 struct PairOf { static constexpr int value = 1; };
 template <class Cfg>
@@ -418,6 +444,9 @@ struct alignas(64) GemmParams {
   // ep_pre: the pre-activation is also stored, through the map in b_lo
   EpArgs ep;
   int ep_pre;
+  // implicit-GEMM convolution (CONV kinds): the im2col map is a_hi (forward)
+  // or b_hi (weight gradient); output pixels o = (n, p, q) with hw = ho * wo
+  int cv_c, cv_k, cv_cblocks, cv_stride, cv_pad, cv_wo, cv_hw;
 };
 
 __device__ __forceinline__ void tile_coords(unsigned t, const GemmParams& p, int& mb, int& nb) {
@@ -773,7 +802,14 @@ k_gemm(const __grid_constant__ GemmParams p, const ShapeArgs s) {
                 if constexpr (PR == 2) tma_load_2d_pair(dst, map, lead_full, x, y);
                 else tma_load_2d(dst, map, &full[st], x, y);
               };
-              if constexpr (Cfg::A_MN) {
+              if constexpr (ConvOf<Cfg>::value == 1) {
+                // A = im2col(x): 128 output pixels from am, k-block = (tap, 64 channels)
+                const int tap = kb / p.cv_cblocks, cb = kb - tap * p.cv_cblocks;
+                const int r = tap / p.cv_k, sx = tap - r * p.cv_k;
+                const int n0 = am / p.cv_hw, rem = am - n0 * p.cv_hw, p0 = rem / p.cv_wo, q0 = rem - p0 * p.cv_wo;
+                tma_load_im2col(base, &p.a_hi, &full[st], cb * 64, q0 * p.cv_stride - p.cv_pad,
+                                p0 * p.cv_stride - p.cv_pad, n0, sx, r);
+              } else if constexpr (Cfg::A_MN) {
                 // boxes of 64 M-elements x BK K-rows, 8 KB each
 #pragma unroll
                 for (int h = 0; h < Cfg::BM / 64; ++h)
@@ -781,7 +817,18 @@ k_gemm(const __grid_constant__ GemmParams p, const ShapeArgs s) {
               } else {
                 ld(base, &p.a_hi, kx + ac, am + ar);
               }
-              if constexpr (Cfg::B_MN) {
+              if constexpr (ConvOf<Cfg>::value == 2) {
+                // B = im2col(x) MN-major: K = BK output pixels from kb * BK, N = (tap, channel)
+                const int px = kb * Cfg::BK;
+                const int n0 = px / p.cv_hw, rem = px - n0 * p.cv_hw, p0 = rem / p.cv_wo, q0 = rem - p0 * p.cv_wo;
+#pragma unroll
+                for (int h = 0; h < BROWS / 64; ++h) {
+                  const int col = bn0 + h * 64, tap = col / p.cv_c, ch = col - tap * p.cv_c;
+                  const int r = tap / p.cv_k, sx = tap - r * p.cv_k;
+                  tma_load_im2col(base + Cfg::A_BYTES + h * 8192, &p.b_hi, &full[st], ch, q0 * p.cv_stride - p.cv_pad,
+                                  p0 * p.cv_stride - p.cv_pad, n0, sx, r);
+                }
+              } else if constexpr (Cfg::B_MN) {
 #pragma unroll
                 for (int h = 0; h < BROWS / 64; ++h)
                   ld(base + Cfg::A_BYTES + h * 8192, &p.b_hi, bn0 + h * 64 + bc, kb * Cfg::BK + br);
@@ -1532,6 +1579,37 @@ static bool getenv_flag(const char* name) {   // experiment switches, read at bi
   return e != nullptr && e[0] != '\0' && e[0] != '0';
 }
 
+typedef CUresult (*EncodeIm2colFn)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
+                                   const cuuint64_t*, const int*, const int*, cuuint32_t, cuuint32_t,
+                                   const cuuint32_t*, CUtensorMapInterleave, CUtensorMapSwizzle,
+                                   CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+
+// TMA im2col map over an NHWC bf16 tensor: boxes of `pixels` output pixels x
+// 64 channels (128 B rows, 128B swizzle -- the K-major / MN-major operand
+// tile layouts), traversal stride = the convolution stride, the pixel box
+// [-pad, W - 1 + pad - (k - 1)] per spatial dimension (zeros outside)
+static int make_im2col_map(CUtensorMap* m, const void* x, const tally_conv_geometry& g, int pixels) {
+  static EncodeIm2colFn enc = [] {
+    void* f = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPointByVersion("cuTensorMapEncodeIm2col", &f, 12000, cudaEnableDefault, &q) == cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      return reinterpret_cast<EncodeIm2colFn>(f);
+    return (EncodeIm2colFn) nullptr;
+  }();
+  if (!enc) { set_error("cuTensorMapEncodeIm2col unavailable"); return TALLY_ENODEV; }
+  cuuint64_t dims[4] = {(cuuint64_t)g.c, (cuuint64_t)g.w, (cuuint64_t)g.h, (cuuint64_t)g.n};
+  cuuint64_t strides[3] = {(cuuint64_t)g.c * 2, (cuuint64_t)g.w * g.c * 2, (cuuint64_t)g.h * g.w * g.c * 2};
+  int lower[2] = {-g.pad, -g.pad};
+  int upper[2] = {g.pad - (g.k - 1), g.pad - (g.k - 1)};
+  cuuint32_t estr[4] = {1, (cuuint32_t)g.stride, (cuuint32_t)g.stride, 1};
+  CUresult r = enc(m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 4, const_cast<void*>(x), dims, strides, lower, upper, 64,
+                   (cuuint32_t)pixels, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                   CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS) { set_error("cuTensorMapEncodeIm2col failed (%d)", (int)r); return TALLY_EINVAL; }
+  return TALLY_OK;
+}
+
 static int make_map(CUtensorMap* m, const void* ptr, CUtensorMapDataType dt, int esz, long long rows,
                     long long cols, int box_rows, long long ld = 0) {
   EncodeTiledFn enc = encode_fn();
@@ -1582,6 +1660,38 @@ static int bind_gemm(const tally_kernel_args* a, Instance* inst, bool split) {
     if ((rc = make_map(&p.b_hi, a->ptr[2], dt, Cfg::ESZ, N, K, Cfg::BN))) return rc;
     if ((rc = make_map(&p.b_lo, a->ptr[3], dt, Cfg::ESZ, N, K, Cfg::BN))) return rc;
     p.c = a->ptr[4];
+  } else if constexpr (gemm::ConvOf<Cfg>::value != 0) {
+    // implicit-GEMM convolution: ptr[3] = tally_conv_geometry
+    constexpr int CV = gemm::ConvOf<Cfg>::value;
+    const tally_conv_geometry* G = static_cast<const tally_conv_geometry*>(a->ptr[3]);
+    if (!G || G->n < 1 || G->h < 1 || G->w < 1 || G->c < 64 || G->c % 64 || G->k < 1 || G->stride < 1 ||
+        G->pad < 0 || G->k > 8 || G->pad >= G->k) {
+      set_error("conv: need a geometry with c %% 64 == 0, 1 <= k <= 8, stride >= 1, 0 <= pad < k");
+      return TALLY_EINVAL;
+    }
+    const long long ho = (G->h + 2 * G->pad - G->k) / G->stride + 1, wo = (G->w + 2 * G->pad - G->k) / G->stride + 1;
+    const long long P = (long long)G->n * ho * wo, Kd = (long long)G->k * G->k * G->c;
+    if (ho < 1 || wo < 1 || (CV == 1 && (M != P || K != Kd)) || (CV == 2 && (N != Kd || K != P)) ||
+        (CV == 2 && G->c % Cfg::BN != 0 && Cfg::BN > G->c)) {
+      set_error("conv: GEMM shape does not match the geometry (forward: M = n*ho*wo, K = k*k*c; weight "
+                "gradient: N = k*k*c, K = n*ho*wo)");
+      return TALLY_EINVAL;
+    }
+    if constexpr (CV == 1) {
+      if ((rc = make_im2col_map(&p.a_hi, a->ptr[0], *G, Cfg::BM))) return rc;
+      if ((rc = make_map(&p.b_hi, a->ptr[1], dt, Cfg::ESZ, N, K, Cfg::BN))) return rc;
+    } else {
+      if ((rc = make_map(&p.a_hi, a->ptr[0], dt, Cfg::ESZ, K, M, Cfg::BK))) return rc;   // dy [P, cout], MN-major
+      if ((rc = make_im2col_map(&p.b_hi, a->ptr[1], *G, Cfg::BK))) return rc;
+    }
+    p.c = a->ptr[2];
+    p.cv_c = G->c;
+    p.cv_k = G->k;
+    p.cv_cblocks = G->c / 64;
+    p.cv_stride = G->stride;
+    p.cv_pad = G->pad;
+    p.cv_wo = (int)wo;
+    p.cv_hw = (int)(ho * wo);
   } else {       // ptr: A, B, C [, layout]; MN-major operand = its transpose stored row-major
     const tally_gemm_layout* L = static_cast<const tally_gemm_layout*>(a->ptr[3]);
     const long long ar = L ? L->a_rows : (Cfg::A_MN ? K : M), acl = L ? L->a_cols : (Cfg::A_MN ? M : K);
@@ -1611,7 +1721,8 @@ static int bind_gemm(const tally_kernel_args* a, Instance* inst, bool split) {
   }
   p.tiles_m = (int)((M + Cfg::BM * PR - 1) / (Cfg::BM * PR));   // (pair: 256-row tiles)
   p.tiles_n = (int)(N / Cfg::BN);
-  const tally_gemm_layout* lay = split ? nullptr : static_cast<const tally_gemm_layout*>(a->ptr[3]);
+  const tally_gemm_layout* lay =
+      (split || gemm::ConvOf<Cfg>::value != 0) ? nullptr : static_cast<const tally_gemm_layout*>(a->ptr[3]);
   p.batches = lay ? lay->batches : 1;
   p.hdiv = lay ? lay->hdiv : 1;
   p.ldc = lay ? lay->ldc : N;
@@ -1882,7 +1993,7 @@ static KernelKind attn_kind(const char* name) {
 }
 
 int register_gemm_kernels(KernelKind* out, int cap) {
-  if (cap < 22) return 0;
+  if (cap < 28) return 0;
   out[0] = gemm_kind<gemm::CfgTf32x3>("sgemm_tf32x3", bind_sgemm);
   out[1] = gemm_kind<gemm::CfgBf16>("gemm_bf16", bind_bf16<gemm::CfgBf16>);
   out[3] = gemm_kind<gemm::CfgTf32x3N64>("sgemm_tf32x3_n64", bind_sgemm_n64);
@@ -1911,7 +2022,13 @@ int register_gemm_kernels(KernelKind* out, int cap) {
   out[2] = k;
   out[20] = attn_kind<0>("attn_softmax");
   out[21] = attn_kind<1>("attn_softmax_bwd");
-  return 22;
+  out[22] = gemm_kind<gemm::CfgConvF>("conv_fprop_bf16", bind_bf16<gemm::CfgConvF>);
+  out[23] = gemm_kind<gemm::CfgConvFN64>("conv_fprop_bf16_n64", bind_bf16<gemm::CfgConvFN64>);
+  out[24] = gemm_kind<gemm::CfgConvF32>("conv_fprop_bf16f32", bind_bf16<gemm::CfgConvF32>);
+  out[25] = gemm_kind<gemm::CfgConvF32N64>("conv_fprop_bf16f32_n64", bind_bf16<gemm::CfgConvF32N64>);
+  out[26] = gemm_kind<gemm::CfgConvW>("conv_wgrad_bf16f32", bind_bf16<gemm::CfgConvW>);
+  out[27] = gemm_kind<gemm::CfgConvWN64>("conv_wgrad_bf16f32_n64", bind_bf16<gemm::CfgConvWN64>);
+  return 28;
 }
 
 }  // namespace tally

@@ -451,6 +451,43 @@ def gemm_mn(At, Bt, C, splits: int = 1, pair: bool = False) -> DeviceKernel:
     return DeviceKernel(kind, (At, Bt, C), (M, N, K, 0, splits))
 
 
+def _conv_geom(n, h, w, c, k, stride, pad):
+    g = _lib.c_conv_geometry()
+    g.n, g.h, g.w, g.c, g.k, g.stride, g.pad = n, h, w, c, k, stride, pad
+    return g
+
+
+def conv_fprop(x, Wt, out, n, h, w, c, k, stride, pad, splits: int = 1) -> DeviceKernel:
+    """Implicit-GEMM convolution: out[P, cout] = im2col(x) . Wt^T with the
+    im2col operand gathered by TMA im2col loads straight from the NHWC input
+    x [n, h, w, c] (c % 64 == 0) -- no column matrix.  Wt [cout, k*k*c] in
+    (kh, kw, c) order.  bf16 out, or fp32 split-K partials [splits, P, cout]."""
+    import torch
+    cout = Wt.shape[0]
+    ho = (h + 2 * pad - k) // stride + 1
+    wo = (w + 2 * pad - k) // stride + 1
+    P = n * ho * wo
+    kind = "conv_fprop_bf16" + ("f32" if out.dtype == torch.float32 else "") + ("" if cout % 128 == 0 else "_n64")
+    g = _conv_geom(n, h, w, c, k, stride, pad)
+    return DeviceKernel(kind, (x.data_ptr(), Wt.data_ptr(), out.data_ptr(), C.addressof(g)),
+                        (P, cout, k * k * c, 0, splits), keep=(x, Wt, out, g))
+
+
+def conv_wgrad(dy, x, gpart, n, h, w, c, k, stride, pad, splits: int = 1) -> DeviceKernel:
+    """Implicit-GEMM weight gradient: dW[cout, k*k*c] (fp32 split-K partials
+    [splits, cout, k*k*c]) = dy^T . im2col(x), dy [P, cout] read MN-major as
+    stored, im2col(x) gathered by TMA im2col loads."""
+    cout = dy.shape[1]
+    ho = (h + 2 * pad - k) // stride + 1
+    wo = (w + 2 * pad - k) // stride + 1
+    P = n * ho * wo
+    kd = k * k * c
+    kind = "conv_wgrad_bf16f32" + ("" if kd % 128 == 0 and c % 128 == 0 else "_n64")
+    g = _conv_geom(n, h, w, c, k, stride, pad)
+    return DeviceKernel(kind, (dy.data_ptr(), x.data_ptr(), gpart.data_ptr(), C.addressof(g)),
+                        (cout, kd, P, 0, splits), keep=(dy, x, gpart, g))
+
+
 def im2col(x, col, n, h, w, c, kh, kw, stride, pad) -> DeviceKernel:
     return DeviceKernel("im2col_bf16", (x, col), (n, h, w, c, _pack_conv(kh, kw, stride, pad)))
 

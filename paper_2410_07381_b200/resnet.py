@@ -189,6 +189,8 @@ class ResNet50Train:
 
     # CTA-pair tcgen05 GEMMs where N % 256 == 0 and >= 32 pair tiles (_pair_plan)
     pair_gemms = os.environ.get("TALLY_RESNET_PAIR", "1") != "0"
+    # implicit-GEMM convolutions (TMA im2col; see _implicit)
+    implicit_conv = os.environ.get("TALLY_IMPLICIT_CONV", "1") != "0"
 
     def __init__(self, batch=64, image=224, lr=0.1, seed=0, device="cuda", model=None):
         import torch
@@ -321,16 +323,33 @@ class ResNet50Train:
         self.program.append((name, dk))
 
     # ---- building blocks -----------------------------------------------------
+    def _implicit(self, s):
+        """k x k / strided convolution as an implicit GEMM (TMA im2col loads of
+        the NHWC activation, no column matrix): every one but the stem (3
+        channels padded to 8: not a 64-channel box)."""
+        return self.implicit_conv and not s.direct and s.cin % 64 == 0
+
     def _conv_fwd(self, conv, x):
-        """x [P_in, Cin] -> (y [P_out, Cout], A operand [P_out, Kp])."""
+        """x [P_in, Cin] -> (y [P_out, Cout], A operand [P_out, Kp]; for an
+        implicit-GEMM convolution the input x itself)."""
         s = conv.spec
         P = self.B * s.oh * s.ow
+        y = self._buf(P, s.cout)
+        if self._implicit(s):
+            S = _gemm_splits(P, s.cout, s.kdim)
+            geo = (self.B, s.h, s.w, s.cin, s.k, s.stride, s.pad)
+            if S == 1:
+                self._add(s.name + ".gemm", K.conv_fprop(x, conv.wb, y, *geo))
+            else:
+                ws = self._scr("splitk", S * P * s.cout, self.torch.float32).view(S, P, s.cout)
+                self._add(s.name + ".gemm", K.conv_fprop(x, conv.wb, ws, *geo, splits=S))
+                self._add(s.name + ".gemm.reduce", K.splitk_reduce(ws, y))
+            return y, x
         if s.direct:
             A = x
         else:
             A = self._buf(P, s.kp)
             self._add(s.name + ".im2col", K.im2col(x, A, self.B, s.h, s.w, s.cin, s.k, s.k, s.stride, s.pad))
-        y = self._buf(P, s.cout)
         self._gemm(s.name + ".gemm", A, conv.wb, y)
         return y, A
 
@@ -379,9 +398,16 @@ class ResNet50Train:
         s = conv.spec
         P = self.B * s.oh * s.ow
         # weight gradient: dW[Cout, Kp] = dy^T . A, both read MN-major as stored
-        pair, S = _pair_plan(s.cout, s.kp, P, self.pair_gemms)
-        conv.gpart = torch.empty(S, s.cout, s.kp, dtype=torch.float32, device=self.device)
-        self._add(s.name + ".wgrad", K.gemm_mn(dy, A, conv.gpart, splits=S, pair=pair))
+        # (implicit GEMM: A = im2col(x) gathered by TMA im2col loads)
+        if self._implicit(s):
+            S = _gemm_splits(s.cout, s.kp, P)
+            conv.gpart = torch.empty(S, s.cout, s.kp, dtype=torch.float32, device=self.device)
+            self._add(s.name + ".wgrad", K.conv_wgrad(dy, A, conv.gpart, self.B, s.h, s.w, s.cin, s.k, s.stride,
+                                                      s.pad, splits=S))
+        else:
+            pair, S = _pair_plan(s.cout, s.kp, P, self.pair_gemms)
+            conv.gpart = torch.empty(S, s.cout, s.kp, dtype=torch.float32, device=self.device)
+            self._add(s.name + ".wgrad", K.gemm_mn(dy, A, conv.gpart, splits=S, pair=pair))
         self.sgd.add(conv.w, conv.v, conv.gpart, S, s.cout * s.kp, WEIGHT_DECAY, conv.wb, conv.wt,
                      s.cout, s.kp)
         if not need_dx:
@@ -412,6 +438,8 @@ class ResNet50Train:
                 dcol = max(dcol, P * s.kp)
             for (M, N, Kd) in ((P, s.cout, s.kp), (P, s.kp, s.cout)):     # forward, dgrad
                 S = _pair_plan(M, N, Kd, self.pair_gemms)[1]
+                if (M, N, Kd) == (P, s.cout, s.kp) and self._implicit(s):
+                    S = _gemm_splits(M, N, Kd)   # (implicit-GEMM kinds are single-CTA)
                 if S > 1:
                     splitk = max(splitk, S * M * N)
         self._reserve("splitk", max(splitk, 8), torch.float32)
