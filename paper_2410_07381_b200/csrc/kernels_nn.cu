@@ -1114,6 +1114,11 @@ struct SgdSeg {
   int rows, cols;
   int chunk;              // elements per logical block (64..1024, power of 2)
   int zero_from;          // >= 0: zero gradient slices [zero_from, S) after reading (atomic accumulators)
+  // optional bf16 flipped copy of a k x k conv weight [cout, (kh, kw, cin)]:
+  // wf[cin, (k-1-kh, k-1-kw, cout)] -- the weight of the data gradient as a
+  // stride-1 forward convolution of dy (implicit-GEMM dgrad)
+  __nv_bfloat16* wf;
+  int fk, fcin;
 };
 
 struct SgdUpdate {
@@ -1198,6 +1203,16 @@ struct SgdUpdate {
       for (int e = 0; e < 4; ++e) {
         const long long r = (i + e) / s.cols, c = (i + e) - r * s.cols;
         s.wt[c * s.rows + r] = __float2bfloat16_rn(nw[e]);
+      }
+    }
+    if (s.wf) {
+#pragma unroll
+      for (int e = 0; e < 4; ++e) {
+        const long long co = (i + e) / s.cols, kk = (i + e) - co * s.cols;
+        const int tap = (int)(kk / s.fcin), ci = (int)(kk - (long long)tap * s.fcin);
+        const int r = tap / s.fk, sx = tap - r * s.fk;
+        s.wf[(long long)ci * s.fk * s.fk * s.rows + ((long long)(s.fk - 1 - r) * s.fk + (s.fk - 1 - sx)) * s.rows + co] =
+            __float2bfloat16_rn(nw[e]);
       }
     }
   }

@@ -139,23 +139,25 @@ class SgdTable:
     def __init__(self):
         self.segs = []
 
-    def add(self, w, v, grad, S, gstride, wd, wb=None, wt=None, rows=1, cols=1, zero_from=-1):
+    def add(self, w, v, grad, S, gstride, wd, wb=None, wt=None, rows=1, cols=1, zero_from=-1, wf=None, fk=0,
+            fcin=0):
         """``zero_from`` >= 0: gradient slices [zero_from, S) are atomic
-        accumulators, zeroed by sgd_update after it reads them."""
-        self.segs.append((w, v, grad, S, gstride, wd, wb, wt, rows, cols, zero_from))
+        accumulators, zeroed by sgd_update after it reads them.  ``wf``: the
+        flipped bf16 copy of a k x k conv weight (``ResNet50Train._flip``)."""
+        self.segs.append((w, v, grad, S, gstride, wd, wb, wt, rows, cols, zero_from, wf, fk, fcin))
 
     def build(self, device):
         import numpy as np
         import torch
         dt = np.dtype({"names": ["w", "v", "grad", "n", "gstride", "S", "wd", "wb", "wt", "rows", "cols", "chunk",
-                                 "zero_from"],
+                                 "zero_from", "wf", "fk", "fcin"],
                        "formats": ["<u8", "<u8", "<u8", "<i8", "<i8", "<i4", "<f4", "<u8", "<u8", "<i4", "<i4", "<i4",
-                                   "<i4"],
-                       "offsets": [0, 8, 16, 24, 32, 40, 44, 48, 56, 64, 68, 72, 76], "itemsize": 80})
+                                   "<i4", "<u8", "<i4", "<i4"],
+                       "offsets": [0, 8, 16, 24, 32, 40, 44, 48, 56, 64, 68, 72, 76, 80, 88, 92], "itemsize": 96})
         rec = np.zeros(len(self.segs), dtype=dt)
         bmap = []
         nbytes = 0
-        for i, (w, v, g, S, gs, wd, wb, wt, rows, cols, zf) in enumerate(self.segs):
+        for i, (w, v, g, S, gs, wd, wb, wt, rows, cols, zf, wf, fk, fcin) in enumerate(self.segs):
             n = w.numel()
             if n % 4 or gs % 4:
                 raise ValueError("sgd_update segments need sizes and gradient strides divisible by 4")
@@ -166,10 +168,11 @@ class SgdTable:
                 chunk //= 2
             rec[i] = (w.data_ptr(), v.data_ptr(), g.data_ptr(), n, gs, S, wd,
                       wb.data_ptr() if wb is not None else 0, wt.data_ptr() if wt is not None else 0,
-                      rows, cols, chunk, zf)
+                      rows, cols, chunk, zf, wf.data_ptr() if wf is not None else 0, fk, fcin)
             for c in range((n + chunk - 1) // chunk):
                 bmap.append((i, c))
-            nbytes += n * (4 * S + 16 + (2 if wb is not None else 0) + (2 if wt is not None else 0))
+            nbytes += n * (4 * S + 16 + (2 if wb is not None else 0) + (2 if wt is not None else 0) +
+                           (2 if wf is not None else 0))
         self.dev_segs = torch.from_numpy(rec.view(np.uint8).copy()).to(device)
         self.dev_map = torch.tensor(bmap, dtype=torch.int32, device=device)
         self.blocks = len(bmap)
@@ -191,6 +194,7 @@ class ResNet50Train:
     pair_gemms = os.environ.get("TALLY_RESNET_PAIR", "1") != "0"
     # implicit-GEMM convolutions (TMA im2col; see _implicit)
     implicit_conv = os.environ.get("TALLY_IMPLICIT_CONV", "1") != "0"
+    implicit_dgrad = os.environ.get("TALLY_IMPLICIT_DGRAD", "1") != "0"
 
     def __init__(self, batch=64, image=224, lr=0.1, seed=0, device="cuda", model=None):
         import torch
@@ -276,8 +280,17 @@ class ResNet50Train:
         c.spec, c.w, c.v = spec, wm, torch.zeros_like(wm)
         c.wb = wm.bfloat16()
         c.wt = wm.t().contiguous().bfloat16()
+        c.wf = self._flip(wm, spec) if spec.cin % 64 == 0 and spec.k > 1 else None
         self.params.append((spec.name + ".weight", wm))
         return c
+
+    @staticmethod
+    def _flip(wm, spec):
+        """[cout, (kh, kw, cin)] -> [cin, (k-1-kh, k-1-kw, cout)] bf16: the
+        weight of dx as a stride-1 forward convolution of dy."""
+        k, cin = spec.k, spec.cin
+        w4 = wm[:, :spec.kdim].view(-1, k, k, cin)
+        return w4.flip(1, 2).permute(3, 1, 2, 0).contiguous().view(cin, -1).bfloat16()
 
     def _bn(self, name, C, sd):
         torch = self.torch
@@ -328,6 +341,12 @@ class ResNet50Train:
         the NHWC activation, no column matrix): every one but the stem (3
         channels padded to 8: not a 64-channel box)."""
         return self.implicit_conv and not s.direct and s.cin % 64 == 0
+
+    def _implicit_dgrad(self, s, conv):
+        """Stride-1 "same" k x k convolutions: dx as an implicit-GEMM forward
+        convolution of dy (cout % 64 == 0) with the flipped weight copy."""
+        return self._implicit(s) and s.stride == 1 and 2 * s.pad == s.k - 1 and s.cout % 64 == 0 \
+            and conv.wf is not None and self.implicit_dgrad
 
     def _conv_fwd(self, conv, x):
         """x [P_in, Cin] -> (y [P_out, Cout], A operand [P_out, Kp]; for an
@@ -409,13 +428,27 @@ class ResNet50Train:
             conv.gpart = torch.empty(S, s.cout, s.kp, dtype=torch.float32, device=self.device)
             self._add(s.name + ".wgrad", K.gemm_mn(dy, A, conv.gpart, splits=S, pair=pair))
         self.sgd.add(conv.w, conv.v, conv.gpart, S, s.cout * s.kp, WEIGHT_DECAY, conv.wb, conv.wt,
-                     s.cout, s.kp)
+                     s.cout, s.kp, wf=conv.wf if self._implicit_dgrad(s, conv) else None, fk=s.k, fcin=s.cin)
         if not need_dx:
             return None
         # data gradient: dcol[P_out, Kp] = dy . W  (B operand = W^T [Kp, Cout])
         if s.direct:
             dx = self._buf(P, s.cin)
             self._gemm(s.name + ".dgrad", dy, conv.wt, dx)
+            return dx
+        if self._implicit_dgrad(s, conv):
+            # dx = a stride-1 forward convolution of dy with the flipped weight
+            # (padding k - 1 - pad): implicit GEMM, no column matrix, no col2im
+            Pin = self.B * s.h * s.w
+            dx = self._buf(Pin, s.cin)
+            geo = (self.B, s.oh, s.ow, s.cout, s.k, 1, s.k - 1 - s.pad)
+            S = _gemm_splits(Pin, s.cin, s.k * s.k * s.cout)
+            if S == 1:
+                self._add(s.name + ".dgrad", K.conv_fprop(dy, conv.wf, dx, *geo))
+            else:
+                ws = self._scr("splitk", S * Pin * s.cin, torch.float32).view(S, Pin, s.cin)
+                self._add(s.name + ".dgrad", K.conv_fprop(dy, conv.wf, ws, *geo, splits=S))
+                self._add(s.name + ".dgrad.reduce", K.splitk_reduce(ws, dx))
             return dx
         dcol = self._scr("dcol", P * s.kp).view(P, s.kp)
         self._gemm(s.name + ".dgrad", dy, conv.wt, dcol)
@@ -440,6 +473,9 @@ class ResNet50Train:
                 S = _pair_plan(M, N, Kd, self.pair_gemms)[1]
                 if (M, N, Kd) == (P, s.cout, s.kp) and self._implicit(s):
                     S = _gemm_splits(M, N, Kd)   # (implicit-GEMM kinds are single-CTA)
+                if (M, N, Kd) == (P, s.kp, s.cout) and self._implicit_dgrad(s, c):
+                    Pin = self.B * s.h * s.w
+                    S, M, N = _gemm_splits(Pin, s.cin, s.k * s.k * s.cout), Pin, s.cin
                 if S > 1:
                     splitk = max(splitk, S * M * N)
         self._reserve("splitk", max(splitk, 8), torch.float32)

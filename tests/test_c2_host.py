@@ -62,9 +62,9 @@ def test_bn_rows_per_block():
 
 
 def test_sgd_table_layout():
-    """80-byte nn::SgdSeg records and a (segment, chunk) map covering every
-    element (kernels_nn.cu SgdUpdate); segments with many gradient partials
-    get smaller logical blocks."""
+    """96-byte nn::SgdSeg records (incl. the flipped conv-weight copy) and a
+    (segment, chunk) map covering every element (kernels_nn.cu SgdUpdate);
+    segments with many gradient partials get smaller logical blocks."""
     import numpy as np
     w = torch.zeros(96, 200)
     v = torch.zeros_like(w)
@@ -75,11 +75,12 @@ def test_sgd_table_layout():
     t.add(w2, torch.zeros_like(w2), torch.zeros(1, 5000), 1, 5000, 0.0)
     t.build("cpu")
     raw = t.dev_segs.numpy().view(np.uint8)
-    assert raw.size == 2 * 80
+    assert raw.size == 2 * 96
     rec = np.frombuffer(raw.tobytes(), dtype=np.dtype({
-        "names": ["w", "n", "gstride", "S", "rows", "cols", "chunk"],
-        "formats": ["<u8", "<i8", "<i8", "<i4", "<i4", "<i4", "<i4"],
-        "offsets": [0, 24, 32, 40, 64, 68, 72], "itemsize": 80}))
+        "names": ["w", "n", "gstride", "S", "rows", "cols", "chunk", "wf", "fk"],
+        "formats": ["<u8", "<i8", "<i8", "<i4", "<i4", "<i4", "<i4", "<u8", "<i4"],
+        "offsets": [0, 24, 32, 40, 64, 68, 72, 80, 88], "itemsize": 96}))
+    assert rec["wf"][0] == 0 and rec["fk"][0] == 0
     assert rec["w"][0] == w.data_ptr() and rec["n"][0] == 19200 and rec["S"][0] == 3
     assert rec["gstride"][1] == 5000 and rec["rows"][0] == 96 and rec["cols"][0] == 200
     m = t.dev_map.numpy()

@@ -101,3 +101,27 @@ def test_conv_wgrad_matches_gemm_mn_and_torch(env, geom):
     assert torch.equal(out, part2)
     ref = dy.double().T @ col.double()
     assert _rel(out.sum(0), ref) < 1e-2
+
+
+@pytest.mark.parametrize("geom", [(2, 14, 14, 64, 128, 3, 1, 1), (2, 8, 8, 256, 256, 3, 1, 1)])
+def test_conv_dgrad_as_flipped_forward_conv(env, geom):
+    """dx of a stride-1 'same' convolution as an implicit-GEMM forward
+    convolution of dy with the flipped weight (ResNet50Train._flip), against
+    PyTorch's conv2d input gradient."""
+    P, K, s = env
+    from paper_2410_07381_b200.resnet import ConvSpec, ResNet50Train
+    n, h, w, c, cout, k, stride, pad = geom
+    g = torch.Generator(device="cuda").manual_seed(3 + sum(geom))
+    wt = (torch.randn(cout, k * k * c, device="cuda", generator=g) * 0.05)
+    dy = (torch.randn(n * h * w, cout, device="cuda", generator=g) * 0.5).bfloat16()
+    spec = ConvSpec("t", c, cout, k, stride, pad, h, w)
+    wf = ResNet50Train._flip(wt, spec)
+    dx = torch.zeros(n * h * w, c, device="cuda", dtype=torch.bfloat16)
+    dk = K.conv_fprop(dy, wf, dx, n, h, w, cout, k, 1, k - 1 - pad)
+    out = _shapes(P, dk, s, dx)
+    x = torch.zeros(n, c, h, w, device="cuda", requires_grad=True)
+    wr = wt.bfloat16().float().view(cout, k, k, c).permute(0, 3, 1, 2)
+    y = torch.nn.functional.conv2d(x, wr, stride=stride, padding=pad)
+    y.backward(dy.float().view(n, h, w, cout).permute(0, 3, 1, 2))
+    ref = x.grad.permute(0, 2, 3, 1).reshape(n * h * w, c)
+    assert _rel(out, ref) < 1e-2
