@@ -141,6 +141,29 @@ typedef struct {
   int k, stride, pad;
 } tally_conv_geometry;
 
+/* Batch-norm statistics fused into the producer of a bf16 [P, C] tensor
+ * (tally_kernel_args.ptr[7] of the bf16 GEMM / conv_fprop kinds and of
+ * "splitk_reduce_bn"; host memory, read at tally_kernel_create).  The
+ * producer also writes what the "bn_stats" kind (mode 0) computes from its
+ * output: mean, invstd and scale_shift = [gamma * invstd; beta - mean *
+ * gamma * invstd] (ref: the batch-norm statistics pass of the ResNet-50 BE
+ * job).  GEMM / conv_fprop: part receives 2 x R partial
+ * rows of C floats (R = ceil(P / 128), x 4 for rb = 32) that the "bn_fold"
+ * kind folds; splitk_reduce_bn / bn_fold: part is their fold scratch of
+ * 2 * ceil(rows / rb) * C floats. */
+typedef struct {
+  float* part;
+  const float* gamma;
+  const float* beta;
+  float* mean;
+  float* invstd;
+  float* scale_shift;
+  double eps;
+  long long rb;   /* splitk_reduce_bn / bn_fold: rows per logical block; GEMM /
+                     conv_fprop: 32 = a partial row per 32 output rows (per
+                     epilogue warp, 4 * ceil(P / 128) rows), else per 128 */
+} tally_bn_stats;
+
 typedef struct {
   unsigned grid_x, grid_y, grid_z;  /* logical grid (the untransformed launch)  */
   long long total_blocks;

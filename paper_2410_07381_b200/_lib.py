@@ -66,6 +66,11 @@ class c_conv_geometry(C.Structure):
                 ("k", C.c_int), ("stride", C.c_int), ("pad", C.c_int)]
 
 
+class c_bn_stats(C.Structure):
+    _fields_ = [("part", C.c_void_p), ("gamma", C.c_void_p), ("beta", C.c_void_p), ("mean", C.c_void_p),
+                ("invstd", C.c_void_p), ("scale_shift", C.c_void_p), ("eps", C.c_double), ("rb", C.c_longlong)]
+
+
 class c_kernel_info(C.Structure):
     _fields_ = [("grid_x", C.c_uint), ("grid_y", C.c_uint), ("grid_z", C.c_uint),
                 ("total_blocks", C.c_longlong), ("threads_per_block", C.c_int),

@@ -31,7 +31,7 @@ CU_FLAGS = ARCH + COMMON + ["-Xptxas", "-warn-spills", "--expt-relaxed-constexpr
 CU_FLAGS += os.environ.get("TALLY_NVCC_DEFINES", "").split()
 
 SOURCES = ["runtime.cu", "kernels_basic.cu", "kernels_gemm.cu", "kernels_nn.cu", "kernels_tf.cu", "runner.cpp", "cuda_device.cpp"]
-HEADERS = ["tally_device.cuh", "registry.h", "runtime.h", "runner.h", "epilogue.cuh"]
+HEADERS = ["tally_device.cuh", "registry.h", "runtime.h", "runner.h", "epilogue.cuh", "bnfuse.cuh"]
 
 
 def _deps_mtime():

@@ -32,6 +32,7 @@
 #include "epilogue.cuh"
 #include "registry.h"
 #include "runtime.h"
+#include "bnfuse.cuh"
 
 namespace tally {
 
@@ -447,6 +448,8 @@ struct alignas(64) GemmParams {
   // implicit-GEMM convolution (CONV kinds): the im2col map is a_hi (forward)
   // or b_hi (weight gradient); output pixels o = (n, p, q) with hw = ho * wo
   int cv_c, cv_k, cv_cblocks, cv_stride, cv_pad, cv_wo, cv_hw;
+  // fused batch-norm statistics of the bf16 output (bnfuse.cuh; part null: off)
+  BnFuse bnf;
 };
 
 __device__ __forceinline__ void tile_coords(unsigned t, const GemmParams& p, int& mb, int& nb) {
@@ -980,7 +983,9 @@ k_gemm(const __grid_constant__ GemmParams p, const ShapeArgs s) {
               __syncwarp();
               if (lane == 0) mbar_arrive(&tmem_empty[acc]);
             }
-            unsigned char* srow = wstage + (size_t)lane * 128;
+            // (explicit shared-space accesses: generic ones cost 64-bit
+            // address arithmetic per access)
+            const uint32_t wst = smem_u32(wstage);
 #pragma unroll
             for (int v = 0; v < 8; ++v) {
               uint32_t wv[4];
@@ -990,7 +995,9 @@ k_gemm(const __grid_constant__ GemmParams p, const ShapeArgs s) {
                 __nv_bfloat162 b = __floats2bfloat162_rn(__uint_as_float(r[v >> 2][k]), __uint_as_float(r[v >> 2][k + 1]));
                 wv[e] = *reinterpret_cast<uint32_t*>(&b);
               }
-              *reinterpret_cast<uint4*>(srow + ((v ^ (lane & 7)) << 4)) = make_uint4(wv[0], wv[1], wv[2], wv[3]);
+              asm volatile("st.shared.v4.b32 [%0], {%1, %2, %3, %4};" ::"r"(wst + lane * 128 + ((v ^ (lane & 7)) << 4)),
+                           "r"(wv[0]), "r"(wv[1]), "r"(wv[2]), "r"(wv[3])
+                           : "memory");
             }
             __syncwarp();
             // 32 rows x 8 chunks: each instruction writes 4 whole 128 B row segments
@@ -998,10 +1005,23 @@ k_gemm(const __grid_constant__ GemmParams p, const ShapeArgs s) {
 #pragma unroll
             for (int it2 = 0; it2 < 8; ++it2) {
               const int rr = it2 * 4 + (lane >> 3), ch = lane & 7;
-              const uint4 v = *reinterpret_cast<const uint4*>(wstage + (size_t)rr * 128 + ((ch ^ (rr & 7)) << 4));
+              uint4 v;
+              asm volatile("ld.shared.v4.b32 {%0, %1, %2, %3}, [%4];"
+                           : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w)
+                           : "r"(wst + rr * 128 + ((ch ^ (rr & 7)) << 4))
+                           : "memory");
               if (row0 + rr < p.m) st_out16(cb + (size_t)(row0 + rr) * p.ldc + ch * 8, v);
             }
             __syncwarp();
+            if (p.bnf.part != nullptr) {
+              // batch-norm statistics of the box (see the TMA-store path); the
+              // staging box was read back synchronously: free
+              const float4 cs = p.bnf.dbg == 2 ? make_float4(0.f, 0.f, 0.f, 0.f)
+                                               : bn_box_colsum(wst, lane, p.m - row0);
+              __syncwarp();
+              bn_fuse_box(p.bnf, cs, w.mb, cc + w.nb * Cfg::BN + h, (warp - 2) & 3, lane,
+                          reinterpret_cast<float*>(epi_smem + (size_t)(4 * grp) * (32 * 64 * 2)), 1024, 2 + grp);
+            }
           }
         }
         if (q == 0 && lane == 0) gemm_log_end(block_log_of(s), t, p);   // (the group's first warp)
@@ -1023,6 +1043,21 @@ k_gemm(const __grid_constant__ GemmParams p, const ShapeArgs s) {
     unsigned char* wstage = epi_smem + (size_t)(warp - 2) * 4096;
     const uint32_t wst = smem_u32(wstage);
     uint32_t ci = 0;
+    // fused batch-norm statistics: a box's column sums are taken right after
+    // its store is issued and exchanged at the next restaging (or the end),
+    // when the unit's staging boxes are free anyway -- waiting for the
+    // store's read right away cost the CTA-pair kinds ~+50 %
+    float4 bn_cs = make_float4(0.f, 0.f, 0.f, 0.f);
+    int bn_prow = -1, bn_c0 = 0;
+    auto bn_flush = [&]() {
+      if (bn_prow >= 0) {
+        if (lane == 0) asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
+        __syncwarp();
+        bn_fuse_box(p.bnf, bn_cs, bn_prow, bn_c0, (warp - 2) & 3, lane,
+                    reinterpret_cast<float*>(epi_smem + (size_t)(4 * half) * 4096), 1024, 2 + half);
+        bn_prow = -1;
+      }
+    };
     for (int i = 0;; ++i) {
       const int j = i % kSlots;
       mbar_wait(&tile_full[j], (i / kSlots) & 1);
@@ -1051,6 +1086,7 @@ k_gemm(const __grid_constant__ GemmParams p, const ShapeArgs s) {
         unsigned char* srow = wstage + (size_t)lane * 128;
         // stage 64 values of this lane's row (bf16, 128B-swizzle) and TMA-store the box
         auto stage_store = [&](const CUtensorMap* map) {
+          bn_flush();
           if (lane == 0) asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
           __syncwarp();
 #pragma unroll
@@ -1062,7 +1098,9 @@ k_gemm(const __grid_constant__ GemmParams p, const ShapeArgs s) {
               __nv_bfloat162 b = __floats2bfloat162_rn(__uint_as_float(r[v >> 2][k]), __uint_as_float(r[v >> 2][k + 1]));
               wv[e] = *reinterpret_cast<uint32_t*>(&b);
             }
-            *reinterpret_cast<uint4*>(srow + ((v ^ (lane & 7)) << 4)) = make_uint4(wv[0], wv[1], wv[2], wv[3]);
+            asm volatile("st.shared.v4.b32 [%0], {%1, %2, %3, %4};" ::"r"(wst + lane * 128 + ((v ^ (lane & 7)) << 4)),
+                         "r"(wv[0]), "r"(wv[1]), "r"(wv[2]), "r"(wv[3])
+                         : "memory");
           }
           asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
           __syncwarp();
@@ -1091,11 +1129,19 @@ k_gemm(const __grid_constant__ GemmParams p, const ShapeArgs s) {
           }
         }
         stage_store(&p.a_lo);
+        if (p.bnf.part != nullptr && yrow - q * 32 < p.m) {
+          // batch-norm statistics of this 64-column box from the staged bf16
+          // values (rows past M excluded; tiles wholly past M skipped)
+          bn_cs = p.bnf.dbg == 2 ? make_float4(0.f, 0.f, 0.f, 0.f) : bn_box_colsum(wst, lane, p.m - yrow);
+          bn_prow = yrow / 128;
+          bn_c0 = ycol;
+        }
       }
       ++ci;
       if (warp == 2 && lane == 0 && lead) gemm_log_end(block_log_of(s), t, p);
       if (lane == 0) mbar_arrive(&tile_empty[j]);
     }
+    bn_flush();
     if (lane == 0) asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
     __syncwarp();
   } else {
@@ -1783,6 +1829,25 @@ static int bind_gemm(const tally_kernel_args* a, Instance* inst, bool split) {
       p.ep_pre = 1;
     }
     inst->alg_bytes_extra_ep = (a->ptr[4] ? 4.0 * N : 0.0) + (a->ptr[5] ? 2.0 * M * N : 0.0) + (a->ptr[6] ? 2.0 * M * N : 0.0);
+  }
+  // fused batch-norm statistics of the bf16 output: ptr[7] (tally_bn_stats)
+  if (a->ptr[7] != nullptr) {
+    const tally_bn_stats* bs = static_cast<const tally_bn_stats*>(a->ptr[7]);
+    bool plain = p.batches == 1;
+    for (int w = 4; w < 6; ++w) plain = plain && p.off[w][0] == 0 && p.off[w][1] == 0;
+    const bool path = Cfg::BN == 64 ? true : p.c_tma == 1;
+    if (Cfg::KIND != 1 || sizeof(typename Cfg::OutT) != 2 || split || !plain || !path || p.ldc != N || N % 64 ||
+        !bs->part) {
+      set_error("gemm: fused batch-norm statistics need a plain unsplit bf16 GEMM / convolution ([M, N] output, "
+                "N %% 64 == 0, TMA-store epilogue for 128/256-wide tiles) and the part scratch");
+      return TALLY_EINVAL;
+    }
+    p.bnf.C = (int)N;
+    p.bnf.rows32 = bs->rb == 32;
+    p.bnf.nrows = (int)(p.bnf.rows32 ? (M + 127) / 128 * 4 : (M + 127) / 128);
+    p.bnf.part = bs->part;
+    p.bnf.dbg = getenv("TALLY_BNFUSE_DBG") ? atoi(getenv("TALLY_BNFUSE_DBG")) : 0;
+    inst->alg_bytes_extra_ep += 8.0 * p.bnf.nrows * N;   // the partial rows
   }
   p.kb_per_split = (int)((KBlocks + splits - 1) / splits);
   if ((KBlocks + p.kb_per_split - 1) / p.kb_per_split != splits) {

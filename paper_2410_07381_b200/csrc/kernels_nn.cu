@@ -273,8 +273,8 @@ struct Transpose {
 template <int MODE>
 struct BnStats {
   static constexpr int kThreads = 256;
-  static constexpr int kMinBlocks = MODE == 0 ? 4 : TALLY_BN_BWD_MINBLOCKS;   // register cap: bytes in flight per SM
-  static constexpr int kRows = MODE == 0 ? kIlp : TALLY_BN_BWD_ROWS;   // rows in flight per thread (1 or 4 streams each)
+  static constexpr int kMinBlocks = MODE == 0 ? 4 : MODE >= 3 ? 3 : TALLY_BN_BWD_MINBLOCKS;   // register cap: bytes in flight per SM
+  static constexpr int kRows = MODE == 0 ? kIlp : MODE >= 3 ? 2 : TALLY_BN_BWD_ROWS;   // rows in flight per thread (1 or 4 streams each)
   static constexpr int kGroup = 32;
   struct Params {
     const uint4* x;        // pre-BN activations [P, C]
@@ -293,40 +293,49 @@ struct BnStats {
     float* dgamma;         // mode 1 outputs
     float* dbeta;
     float* coef;           // mode 1 output [3][C]: dx = ca*dz + cb*x + cc
+    const float4* sk_in;   // mode 3: split-K fp32 partials [S][P][C]; mode 4: partial rows [2][P][C]
+    uint4* sk_out;         // mode 3: their bf16 sum [P, C] (the statistics' input)
+    long long sk_stride4;  // mode 3: P * C / 4
+    int sk_S;
     long long P;
     int C, RB, nrb, ngroups, mode;
     float inv_count, eps;
   };
 
   // sum rows [r0, r1) of a [2][rows][C] partial array for this block's
-  // channels into red (first 2*CB floats), using every thread
+  // channels into red (first 2*CB floats), using every thread: float4 column
+  // lanes x 4-16 row lanes, 4 rows' loads of both arrays in flight per batch
+  // (a 32-row group is 1-2 batches, not ~8 dependent L2 round trips), then
+  // the row lanes added in order through shared memory (deterministic)
   static __device__ __forceinline__ void fold(const float* src, long long rows_total, int r0, int r1, int C,
                                               int c0, int CB, float* red, float* out_a, float* out_b) {
-    const int lanes_r = kThreads / CB;
-    const int lc = threadIdx.x % CB, lr = threadIdx.x / CB;
-    float a = 0.f, b = 0.f;
-    // 8 rows' loads in flight per batch, summed in row order (deterministic):
-    // a dependent load per row would put ~32 L2 round trips on the tail
-    for (int r = r0 + lr; r < r1; r += 8 * lanes_r) {
-      float va[8], vb[8];
+    const int cv4 = CB >> 2, lanes_r = kThreads / cv4;
+    const int lc = threadIdx.x % cv4, lr = threadIdx.x / cv4;
+    float4 a = make_float4(0.f, 0.f, 0.f, 0.f), b = a;
+    const float* pa = src + c0 + 4 * lc;
+    const float* pb = src + rows_total * C + c0 + 4 * lc;
+    for (int r = r0 + lr; r < r1; r += 4 * lanes_r) {
+      float4 va[4], vb[4];
 #pragma unroll
-      for (int u = 0; u < 8; ++u) {
+      for (int u = 0; u < 4; ++u) {
         const int rr = r + u * lanes_r;
-        va[u] = rr < r1 ? __ldcg(src + (long long)rr * C + c0 + lc) : 0.f;
-        vb[u] = rr < r1 ? __ldcg(src + (rows_total + rr) * C + c0 + lc) : 0.f;
+        va[u] = rr < r1 ? __ldcg(reinterpret_cast<const float4*>(pa + (long long)rr * C)) : make_float4(0.f, 0.f, 0.f, 0.f);
+        vb[u] = rr < r1 ? __ldcg(reinterpret_cast<const float4*>(pb + (long long)rr * C)) : make_float4(0.f, 0.f, 0.f, 0.f);
       }
 #pragma unroll
-      for (int u = 0; u < 8; ++u) { a += va[u]; b += vb[u]; }
+      for (int u = 0; u < 4; ++u) {
+        a.x += va[u].x; a.y += va[u].y; a.z += va[u].z; a.w += va[u].w;
+        b.x += vb[u].x; b.y += vb[u].y; b.z += vb[u].z; b.w += vb[u].w;
+      }
     }
-    red[lr * CB + lc] = a;
-    red[kThreads + lr * CB + lc] = b;
+    reinterpret_cast<float4*>(red + lr * CB)[lc] = a;
+    reinterpret_cast<float4*>(red + 1024 + lr * CB)[lc] = b;
     __syncthreads();
     if (threadIdx.x < CB) {
-      a = 0.f;
-      b = 0.f;
-      for (int k = 0; k < lanes_r; ++k) { a += red[k * CB + threadIdx.x]; b += red[kThreads + k * CB + threadIdx.x]; }
-      *out_a = a;
-      *out_b = b;
+      float sa = 0.f, sb = 0.f;
+      for (int k = 0; k < lanes_r; ++k) { sa += red[k * CB + threadIdx.x]; sb += red[1024 + k * CB + threadIdx.x]; }
+      *out_a = sa;
+      *out_b = sb;
     }
     __syncthreads();
   }
@@ -342,6 +351,93 @@ struct BnStats {
     const int cvec = p.C >> 3;
     float s1[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f}, s2[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
     for (long long r0 = rbeg + lane_r; r0 < rend; r0 += (long long)rl * kRows) {
+      if constexpr (MODE == 4) {
+        // mode 4 (bn_fold): rows are the fused epilogue's partial rows
+        // (s1, s2 of 128 output rows each), summed in row order
+        float4 t[kRows][4];
+        bool ok[kRows];
+#pragma unroll
+        for (int u = 0; u < kRows; ++u) {
+          const long long r = r0 + (long long)u * rl;
+          ok[u] = r < rend;
+          if (ok[u]) {
+            const float4* a = p.sk_in + ((r * p.C + c) >> 2);
+            const float4* b = p.sk_in + (((p.P + r) * p.C + c) >> 2);
+            t[u][0] = __ldcg(a);
+            t[u][1] = __ldcg(a + 1);
+            t[u][2] = __ldcg(b);
+            t[u][3] = __ldcg(b + 1);
+          }
+        }
+#pragma unroll
+        for (int u = 0; u < kRows; ++u) {
+          if (!ok[u]) continue;
+          s1[0] += t[u][0].x; s1[1] += t[u][0].y; s1[2] += t[u][0].z; s1[3] += t[u][0].w;
+          s1[4] += t[u][1].x; s1[5] += t[u][1].y; s1[6] += t[u][1].z; s1[7] += t[u][1].w;
+          s2[0] += t[u][2].x; s2[1] += t[u][2].y; s2[2] += t[u][2].z; s2[3] += t[u][2].w;
+          s2[4] += t[u][3].x; s2[5] += t[u][3].y; s2[6] += t[u][3].z; s2[7] += t[u][3].w;
+        }
+        continue;
+      }
+      if constexpr (MODE == 3) {
+        // mode 3 (splitk_reduce_bn): the split-K sum of kRows rows, two
+        // partials' loads in flight per row, summed in split order (as
+        // splitk_reduce), stored as bf16; the statistics of the stored values
+        float v[kRows][8];
+        bool ok[kRows];
+        long long off[kRows];
+#pragma unroll
+        for (int u = 0; u < kRows; ++u) {
+          const long long r = r0 + (long long)u * rl;
+          ok[u] = r < rend;
+          off[u] = (r * p.C + c) >> 2;
+#pragma unroll
+          for (int e = 0; e < 8; ++e) v[u][e] = 0.f;
+        }
+        int sp = 0;
+        for (; sp + 1 < p.sk_S; sp += 2) {
+          float4 t[kRows][4];
+#pragma unroll
+          for (int u = 0; u < kRows; ++u) {
+            if (ok[u]) {
+              const float4* src = p.sk_in + sp * p.sk_stride4 + off[u];
+              t[u][0] = __ldcs(src);
+              t[u][1] = __ldcs(src + 1);
+              t[u][2] = __ldcs(src + p.sk_stride4);
+              t[u][3] = __ldcs(src + p.sk_stride4 + 1);
+            }
+          }
+#pragma unroll
+          for (int u = 0; u < kRows; ++u) {
+            if (!ok[u]) continue;
+            v[u][0] += t[u][0].x; v[u][1] += t[u][0].y; v[u][2] += t[u][0].z; v[u][3] += t[u][0].w;
+            v[u][4] += t[u][1].x; v[u][5] += t[u][1].y; v[u][6] += t[u][1].z; v[u][7] += t[u][1].w;
+            v[u][0] += t[u][2].x; v[u][1] += t[u][2].y; v[u][2] += t[u][2].z; v[u][3] += t[u][2].w;
+            v[u][4] += t[u][3].x; v[u][5] += t[u][3].y; v[u][6] += t[u][3].z; v[u][7] += t[u][3].w;
+          }
+        }
+        if (sp < p.sk_S) {
+#pragma unroll
+          for (int u = 0; u < kRows; ++u) {
+            if (!ok[u]) continue;
+            const float4* src = p.sk_in + sp * p.sk_stride4 + off[u];
+            const float4 a = __ldcs(src), b = __ldcs(src + 1);
+            v[u][0] += a.x; v[u][1] += a.y; v[u][2] += a.z; v[u][3] += a.w;
+            v[u][4] += b.x; v[u][5] += b.y; v[u][6] += b.z; v[u][7] += b.w;
+          }
+        }
+#pragma unroll
+        for (int u = 0; u < kRows; ++u) {
+          if (!ok[u]) continue;
+          const uint4 o = pack8(v[u]);
+          st16(p.sk_out + (off[u] >> 1), o);
+          float x[8];
+          unpack8(o, x);
+#pragma unroll
+          for (int e = 0; e < 8; ++e) { s1[e] += x[e]; s2[e] += x[e] * x[e]; }
+        }
+        continue;
+      }
       uint4 xv[kRows], gv[kRows], g2v[kRows], yv[kRows];
       bool ok[kRows];
 #pragma unroll
@@ -458,7 +554,7 @@ struct BnStats {
         if (!single) fold(p.part2, p.ngroups, 0, p.ngroups, p.C, c0, CB, red, &a, &b);
         if (threadIdx.x < CB) {
           const int ch = c0 + threadIdx.x;
-          if constexpr (MODE == 0) {
+          if constexpr (MODE == 0 || MODE >= 3) {
             const float m = a * p.inv_count;
             const float var = fmaxf(b * p.inv_count - m * m, 0.f);
             const float isd = rsqrtf(var + p.eps);
@@ -1601,6 +1697,68 @@ static int bind_splitk_reduce(const tally_kernel_args* a, Instance* inst) {
   return TALLY_OK;
 }
 
+// splitk_reduce_bn -- ptr: parts [S][P][C] fp32, out [P, C] bf16; ptr[7]:
+// tally_bn_stats (part, gamma, beta, mean, invstd, scale_shift, eps, rb).
+// i: P, C, S.  The split-K sum of a convolution / GEMM feeding a training
+// batch norm, with that batch norm's statistics (bn_stats mode 0) fused.
+//
+// bn_fold -- ptr[0]: the fused epilogue's partial rows [2][R][C] fp32 (the
+// tally_bn_stats.part a GEMM / conv_fprop wrote); ptr[7]: tally_bn_stats
+// (its part = this kind's own fold scratch).  i: R, C, count (rows of the
+// normalised tensor).  bn_stats mode 0's fold and finalisation over them.
+template <int MODE>
+static int bind_splitk_bn(const tally_kernel_args* a, Instance* inst) {
+  using Body = nn::BnStats<MODE>;
+  typename Body::Params p{};
+  const tally_bn_stats* bs = static_cast<const tally_bn_stats*>(a->ptr[7]);
+  p.sk_in = static_cast<const float4*>(a->ptr[0]);
+  p.sk_out = static_cast<uint4*>(a->ptr[1]);
+  p.P = a->i[0];
+  p.C = (int)a->i[1];
+  p.sk_S = MODE == 3 ? (int)a->i[2] : 1;
+  const long long count = MODE == 3 ? p.P : a->i[2];
+  const bool c_ok = p.C >= 64 && (p.C < 256 ? (256 % p.C == 0) : (p.C % 256 == 0));
+  if (!bs || !p.sk_in || (MODE == 3 && !p.sk_out) || !aligned16(p.sk_in) || (MODE == 3 && !aligned16(p.sk_out)) ||
+      p.P < 1 || !c_ok || p.sk_S < 1 || count < 1 || bs->rb < 1 || !bs->part || !bs->gamma || !bs->beta ||
+      !bs->mean || !bs->invstd || !bs->scale_shift || p.P * p.C >= (1ll << 40)) {
+    set_error("%s: need 16-byte aligned inputs (and out), rows, S / count >= 1, C in {64, 128} or a multiple of "
+              "256, and tally_bn_stats (part, gamma, beta, mean, invstd, scale_shift, rb >= 1)",
+              MODE == 3 ? "splitk_reduce_bn" : "bn_fold");
+    return TALLY_EINVAL;
+  }
+  p.sk_stride4 = p.P * p.C / 4;
+  p.RB = (int)bs->rb;
+  p.part = bs->part;
+  p.gamma = bs->gamma;
+  p.beta = bs->beta;
+  p.mean = bs->mean;
+  p.invstd = bs->invstd;
+  p.scale_shift = bs->scale_shift;
+  p.eps = (float)bs->eps;
+  p.mode = MODE;
+  p.nrb = (int)((p.P + p.RB - 1) / p.RB);
+  p.ngroups = (p.nrb + Body::kGroup - 1) / Body::kGroup;
+  p.inv_count = (float)(1.0 / (double)count);
+  const int cblocks = (p.C + 255) / 256;
+  const size_t cnt_bytes = ((size_t)cblocks * (p.ngroups + 1) * sizeof(unsigned) + 255) / 256 * 256;
+  const size_t bytes = cnt_bytes + (size_t)2 * p.ngroups * p.C * sizeof(float);
+  void* st = nullptr;
+  cudaError_t e = cudaMalloc(&st, bytes);
+  if (e == cudaSuccess) e = cudaMemset(st, 0, cnt_bytes);
+  if (e != cudaSuccess) return cuda_fail(e, "splitk_reduce_bn state");
+  inst->resume_ring = st;
+  inst->resume_bytes = cnt_bytes;
+  p.cnt1 = static_cast<unsigned*>(st);
+  p.cnt2 = p.cnt1 + (size_t)cblocks * p.ngroups;
+  p.part2 = reinterpret_cast<float*>(static_cast<char*>(st) + cnt_bytes);
+  memcpy(inst->params, &p, sizeof(p));
+  inst->grid = make_uint3((unsigned)cblocks, (unsigned)p.nrb, 1);
+  inst->threads = Body::kThreads;
+  inst->smem = 2 * 2048 * sizeof(float) + 16;
+  inst->alg_bytes = (MODE == 3 ? (4.0 * p.sk_S + 2.0) : 8.0) * (double)p.P * p.C + 8.0 * p.nrb * p.C;
+  return TALLY_OK;
+}
+
 template <class B>
 static KernelKind nn_kind(const char* name, int (*bind)(const tally_kernel_args*, Instance*)) {
   KernelKind k{};
@@ -1613,7 +1771,7 @@ static KernelKind nn_kind(const char* name, int (*bind)(const tally_kernel_args*
 }
 
 int register_nn_kernels(KernelKind* out, int cap) {
-  if (cap < 16) return 0;
+  if (cap < 18) return 0;
   int n = 0;
   out[n++] = nn_kind<nn::Im2Col>("im2col_bf16", bind_im2col);
   out[n++] = nn_kind<nn::Col2Im>("col2im_bf16", bind_col2im);
@@ -1632,6 +1790,8 @@ int register_nn_kernels(KernelKind* out, int cap) {
   out[n - 1].setup = setup_softmax_xent;
   out[n++] = nn_kind<nn::SgdUpdate>("sgd_update", bind_sgd);
   out[n++] = nn_kind<nn::SplitKReduce>("splitk_reduce", bind_splitk_reduce);
+  out[n++] = nn_kind<nn::BnStats<3>>("splitk_reduce_bn", bind_splitk_bn<3>);
+  out[n++] = nn_kind<nn::BnStats<4>>("bn_fold", bind_splitk_bn<4>);
   return n;
 }
 

@@ -18,6 +18,8 @@ for its lifetime.
 from __future__ import annotations
 
 import ctypes as C
+
+_ctypes = C   # (gemm() names its output C)
 from dataclasses import dataclass
 
 from . import _lib
@@ -352,7 +354,33 @@ def _pair_suffix(pair: bool, N: int) -> str:
     return "_x2"
 
 
-def gemm(A, B, C, splits: int = 1, pair: bool = False) -> DeviceKernel:
+class BnStatsOut:
+    """Where a producer kernel writes the training batch-norm statistics of
+    its bf16 output [P, C] (``tally_bn_stats``): ``part`` fp32 scratch, the
+    layer's gamma / beta, and the outputs mean, invstd and scale_shift [2, C]
+    -- what ``bn_stats`` computes from the stored tensor, fused into the
+    GEMM / convolution epilogue or ``splitk_reduce_bn``."""
+
+    def __init__(self, part, gamma, beta, mean, invstd, scale_shift, eps=1e-5, rb=0):
+        self.tensors = (part, gamma, beta, mean, invstd, scale_shift)
+        s = _lib.c_bn_stats()
+        s.part, s.gamma, s.beta, s.mean, s.invstd, s.scale_shift = (t.data_ptr() for t in self.tensors)
+        s.eps, s.rb = float(eps), int(rb)
+        self.c = s
+
+    @staticmethod
+    def part_floats(P, C, rb=128):
+        """fp32 scratch floats of a fold over P rows, rb per block."""
+        return 2 * ((P + rb - 1) // rb) * C
+
+    @staticmethod
+    def gemm_rows(P, rb=128):
+        """Partial rows a GEMM / conv_fprop epilogue writes for P output rows:
+        one per 128-row tile, or (rb = 32) one per epilogue warp."""
+        return (P + 127) // 128 * (4 if rb == 32 else 1)
+
+
+def gemm(A, B, C, splits: int = 1, pair: bool = False, bn: "BnStatsOut | None" = None) -> DeviceKernel:
     """C[M,N] = A[M,K] . B[N,K]^T on tcgen05 (bf16 operands, fp32 accumulation).
 
     The kind follows the operands: N % 128 == 0 -> 128-wide tiles, else
@@ -371,7 +399,10 @@ def gemm(A, B, C, splits: int = 1, pair: bool = False) -> DeviceKernel:
         raise ValueError("gemm: C must be [M,N] (or [splits,M,N] fp32 for split-K)")
     kind = "gemm_bf16" + ("f32" if out_f32 else "") + (_pair_suffix(True, N) if pair else
                                                        "" if N % 128 == 0 else "_n64")
-    return DeviceKernel(kind, (A, B, C), (M, N, K, 0, splits))
+    if bn is None:
+        return DeviceKernel(kind, (A, B, C), (M, N, K, 0, splits))
+    return DeviceKernel(kind, (A, B, C, None, None, None, None, _ctypes.addressof(bn.c)), (M, N, K, 0, splits),
+                        keep=(bn, bn.tensors))
 
 
 def gemm_ex(A, B, Cout, M, N, K, a_mn=False, b_mn=False, splits=1, batches=1, hdiv=1,
@@ -457,7 +488,8 @@ def _conv_geom(n, h, w, c, k, stride, pad):
     return g
 
 
-def conv_fprop(x, Wt, out, n, h, w, c, k, stride, pad, splits: int = 1) -> DeviceKernel:
+def conv_fprop(x, Wt, out, n, h, w, c, k, stride, pad, splits: int = 1,
+               bn: "BnStatsOut | None" = None) -> DeviceKernel:
     """Implicit-GEMM convolution: out[P, cout] = im2col(x) . Wt^T with the
     im2col operand gathered by TMA im2col loads straight from the NHWC input
     x [n, h, w, c] (c % 64 == 0) -- no column matrix.  Wt [cout, k*k*c] in
@@ -469,8 +501,9 @@ def conv_fprop(x, Wt, out, n, h, w, c, k, stride, pad, splits: int = 1) -> Devic
     P = n * ho * wo
     kind = "conv_fprop_bf16" + ("f32" if out.dtype == torch.float32 else "") + ("" if cout % 128 == 0 else "_n64")
     g = _conv_geom(n, h, w, c, k, stride, pad)
-    return DeviceKernel(kind, (x.data_ptr(), Wt.data_ptr(), out.data_ptr(), C.addressof(g)),
-                        (P, cout, k * k * c, 0, splits), keep=(x, Wt, out, g))
+    extra = () if bn is None else (None, None, None, C.addressof(bn.c))
+    return DeviceKernel(kind, (x.data_ptr(), Wt.data_ptr(), out.data_ptr(), C.addressof(g)) + extra,
+                        (P, cout, k * k * c, 0, splits), keep=(x, Wt, out, g) + (() if bn is None else (bn,)))
 
 
 def conv_wgrad(dy, x, gpart, n, h, w, c, k, stride, pad, splits: int = 1) -> DeviceKernel:
@@ -524,6 +557,24 @@ def splitk_reduce(parts, out, bias=None, res=None, pre=None, act=0) -> DeviceKer
     ep = bias is not None or res is not None or pre is not None or act
     return DeviceKernel("splitk_reduce", (parts, out, bias, res, pre),
                         (out.numel(), parts.shape[0], C if ep else 0, act))
+
+
+def splitk_reduce_bn(parts, out, bn: BnStatsOut) -> DeviceKernel:
+    """out [P, C] (bf16) = parts.sum(0) (fp32 split-K partials [S, P, C]) and
+    the training batch-norm statistics of out (bn_stats mode 0) in one pass;
+    ``bn.c.rb`` rows per logical block."""
+    S, P, Cc = parts.shape
+    return DeviceKernel("splitk_reduce_bn", (parts, out, None, None, None, None, None, C.addressof(bn.c)),
+                        (P, Cc, S), keep=(bn,))
+
+
+def bn_fold(rows, R, Cn, count, bn: BnStatsOut) -> DeviceKernel:
+    """Training batch-norm statistics from the partial rows [2, R, Cn] a GEMM /
+    conv_fprop epilogue wrote through ``BnStatsOut`` (``rows`` = its part):
+    mean, invstd and scale_shift of ``count`` output rows into ``bn`` (whose
+    own part is this fold's scratch, ``bn.c.rb`` rows per logical block)."""
+    return DeviceKernel("bn_fold", (rows, None, None, None, None, None, None, C.addressof(bn.c)),
+                        (R, Cn, count), keep=(bn, rows))
 
 
 def bn_finalize_fwd(part, nrb, C, count, gamma, beta, mean, invstd, scale, shift,

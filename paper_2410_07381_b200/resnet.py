@@ -195,6 +195,12 @@ class ResNet50Train:
     # implicit-GEMM convolutions (TMA im2col; see _implicit)
     implicit_conv = os.environ.get("TALLY_IMPLICIT_CONV", "1") != "0"
     implicit_dgrad = os.environ.get("TALLY_IMPLICIT_DGRAD", "1") != "0"
+    # batch-norm statistics fused into the producing GEMM / convolution
+    # epilogue or split-K reduce (csrc/bnfuse.cuh): no bn_stats pass
+    fuse_bn_stats = os.environ.get("TALLY_BN_FUSE", "1") != "0"
+    # partial rows per 128 (one per tile, the epilogue warps combine through
+    # shared memory) or per 32 output rows (one per warp, no exchange)
+    bn_fuse_rows = int(os.environ.get("TALLY_BNFUSE_ROWS", "128"))
 
     def __init__(self, batch=64, image=224, lr=0.1, seed=0, device="cuda", model=None):
         import torch
@@ -348,9 +354,10 @@ class ResNet50Train:
         return self._implicit(s) and s.stride == 1 and 2 * s.pad == s.k - 1 and s.cout % 64 == 0 \
             and conv.wf is not None and self.implicit_dgrad
 
-    def _conv_fwd(self, conv, x):
+    def _conv_fwd(self, conv, x, bn=None):
         """x [P_in, Cin] -> (y [P_out, Cout], A operand [P_out, Kp]; for an
-        implicit-GEMM convolution the input x itself)."""
+        implicit-GEMM convolution the input x itself, fused): with ``bn`` the
+        producer also writes that batch norm's statistics (fused = True)."""
         s = conv.spec
         P = self.B * s.oh * s.ow
         y = self._buf(P, s.cout)
@@ -358,42 +365,74 @@ class ResNet50Train:
             S = _gemm_splits(P, s.cout, s.kdim)
             geo = (self.B, s.h, s.w, s.cin, s.k, s.stride, s.pad)
             if S == 1:
-                self._add(s.name + ".gemm", K.conv_fprop(x, conv.wb, y, *geo))
+                bno = self._bn_out(bn, P, self.bn_fuse_rows)
+                self._add(s.name + ".gemm", K.conv_fprop(x, conv.wb, y, *geo, bn=bno))
+                self._bn_fold(s.name + ".bnfold", bno, bn, P)
             else:
                 ws = self._scr("splitk", S * P * s.cout, self.torch.float32).view(S, P, s.cout)
                 self._add(s.name + ".gemm", K.conv_fprop(x, conv.wb, ws, *geo, splits=S))
-                self._add(s.name + ".gemm.reduce", K.splitk_reduce(ws, y))
-            return y, x
+                bno = self._reduce(s.name + ".gemm.reduce", ws, y, bn, P)
+            return y, x, bno is not None
         if s.direct:
             A = x
         else:
             A = self._buf(P, s.kp)
             self._add(s.name + ".im2col", K.im2col(x, A, self.B, s.h, s.w, s.cin, s.k, s.k, s.stride, s.pad))
-        self._gemm(s.name + ".gemm", A, conv.wb, y)
-        return y, A
+        fused = self._gemm(s.name + ".gemm", A, conv.wb, y, bn=bn)
+        return y, A, fused
 
-    def _gemm(self, name, A, B, out):
+    def _bn_out(self, bn, P, rb):
+        """The fused-statistics target of batch norm ``bn`` over P rows (None:
+        not fused)."""
+        if bn is None or not self.fuse_bn_stats:
+            return None
+        rows = K.BnStatsOut.gemm_rows(P, rb) if rb in (32, 128) else (P + rb - 1) // rb
+        part = self._scr("part", 2 * rows * bn.C, self.torch.float32)
+        return K.BnStatsOut(part, bn.gamma, bn.beta, bn.mean, bn.invstd, bn.scale_shift, BN_EPS, rb)
+
+    def _bn_fold(self, name, bno, bn, P):
+        """After a GEMM / convolution that wrote ``bno``'s partial rows: the
+        fold into ``bn``'s statistics (bn_fold, 64 partial rows per block)."""
+        if bno is None:
+            return
+        R = K.BnStatsOut.gemm_rows(P, bno.c.rb)
+        fpart = self._scr("bnfold", K.BnStatsOut.part_floats(R, bn.C, 64), self.torch.float32)
+        fo = K.BnStatsOut(fpart, bn.gamma, bn.beta, bn.mean, bn.invstd, bn.scale_shift, BN_EPS, 64)
+        self._add(name, K.bn_fold(bno.tensors[0], R, bn.C, P, fo))
+
+    def _reduce(self, name, ws, out, bn, P):
+        """Split-K sum into the bf16 ``out`` (with ``bn``'s statistics when
+        fused); returns the statistics target or None."""
+        bno = self._bn_out(bn, P, _rb(P, out.shape[1]))
+        self._add(name, K.splitk_reduce(ws, out) if bno is None else K.splitk_reduce_bn(ws, out, bno))
+        return bno
+
+    def _gemm(self, name, A, B, out, bn=None):
         """out[M,N] (bf16) = A . B^T, split-K through an fp32 workspace when the
-        GEMM has few, long output tiles (see _gemm_splits)."""
+        GEMM has few, long output tiles (see _gemm_splits); with ``bn`` the
+        batch-norm statistics of out are fused (returns whether they were)."""
         torch = self.torch
         M, Kd = A.shape
         N = B.shape[0]
         pair, S = _pair_plan(M, N, Kd, self.pair_gemms)
         if S == 1:
-            self._add(name, K.gemm(A, B, out, pair=pair))
-            return
+            bno = self._bn_out(bn, M, self.bn_fuse_rows)
+            self._add(name, K.gemm(A, B, out, pair=pair, bn=bno))
+            self._bn_fold(name + ".bnfold", bno, bn, M)
+            return bno is not None
         ws = self._scr("splitk", S * M * N, torch.float32).view(S, M, N)
         self._add(name, K.gemm(A, B, ws, splits=S, pair=pair))
-        self._add(name + ".reduce", K.splitk_reduce(ws, out))
+        return self._reduce(name + ".reduce", ws, out, bn, M) is not None
 
-    def _bn_fwd(self, bn, y, P, relu, res=None):
+    def _bn_fwd(self, bn, y, P, relu, res=None, fused=False):
         torch = self.torch
-        rb = _rb(P, bn.C)
-        nrb = (P + rb - 1) // rb
-        part = self._scr("part", 2 * nrb * bn.C, torch.float32)
+        if not fused:
+            rb = _rb(P, bn.C)
+            nrb = (P + rb - 1) // rb
+            part = self._scr("part", 2 * nrb * bn.C, torch.float32)
+            self._add(bn.name + ".stats", K.bn_stats(y, part, P, bn.C, rb, bn.mean, bn.invstd, bn.gamma, bn.beta,
+                                                     bn.scale_shift, BN_EPS))
         out = self._buf(P, bn.C)
-        self._add(bn.name + ".stats", K.bn_stats(y, part, P, bn.C, rb, bn.mean, bn.invstd, bn.gamma, bn.beta,
-                                                 bn.scale_shift, BN_EPS))
         self._add(bn.name + ".act", K.bn_act(y, out, bn.scale_shift[0], bn.scale_shift[1], P, bn.C, relu, res))
         return out
 
@@ -466,7 +505,8 @@ class ResNet50Train:
         for c in convs:
             s = c.spec
             P = self.B * s.oh * s.ow
-            part = max(part, 2 * ((P + _rb(P, s.cout, 4) - 1) // _rb(P, s.cout, 4)) * s.cout)
+            part = max(part, 2 * ((P + _rb(P, s.cout, 4) - 1) // _rb(P, s.cout, 4)) * s.cout,
+                       2 * K.BnStatsOut.gemm_rows(P, 32) * s.cout)
             if not s.direct:
                 dcol = max(dcol, P * s.kp)
             for (M, N, Kd) in ((P, s.cout, s.kp), (P, s.kp, s.cout)):     # forward, dgrad
@@ -480,6 +520,8 @@ class ResNet50Train:
                     splitk = max(splitk, S * M * N)
         self._reserve("splitk", max(splitk, 8), torch.float32)
         self._reserve("part", part, torch.float32)
+        self._reserve("bnfold", max(K.BnStatsOut.part_floats(K.BnStatsOut.gemm_rows(self.B * c.spec.oh * c.spec.ow, 32),
+                                                             c.spec.cout, 64) for c in convs), torch.float32)
         self._reserve("dcol", dcol, torch.bfloat16)
 
     # ---- the step ----------------------------------------------------------------
@@ -490,8 +532,8 @@ class ResNet50Train:
         # forward: stem
         st = self.stem.spec
         P1 = B * st.oh * st.ow
-        y0, A0 = self._conv_fwd(self.stem, self.x.view(B * self.image * self.image, IN_CH))
-        a0 = self._bn_fwd(self.stem_bn, y0, P1, relu=True)
+        y0, A0, f0 = self._conv_fwd(self.stem, self.x.view(B * self.image * self.image, IN_CH), self.stem_bn)
+        a0 = self._bn_fwd(self.stem_bn, y0, P1, relu=True, fused=f0)
         P2 = B * self.pool_h * self.pool_h
         a1 = self._buf(P2, 64)
         arg = torch.empty(P2 * 64, dtype=torch.uint8, device=self.device)
@@ -503,18 +545,18 @@ class ResNet50Train:
         for blk in self.blocks:
             hh, ho = blk["h"], blk["ho"]
             Pin, Pout = B * hh * hh, B * ho * ho
-            y1, A1 = self._conv_fwd(blk["c1"], x)
-            o1 = self._bn_fwd(blk["b1"], y1, Pin, relu=True)
-            y2, A2 = self._conv_fwd(blk["c2"], o1)
-            o2 = self._bn_fwd(blk["b2"], y2, Pout, relu=True)
-            y3, A3 = self._conv_fwd(blk["c3"], o2)
+            y1, A1, f1 = self._conv_fwd(blk["c1"], x, blk["b1"])
+            o1 = self._bn_fwd(blk["b1"], y1, Pin, relu=True, fused=f1)
+            y2, A2, f2 = self._conv_fwd(blk["c2"], o1, blk["b2"])
+            o2 = self._bn_fwd(blk["b2"], y2, Pout, relu=True, fused=f2)
+            y3, A3, f3 = self._conv_fwd(blk["c3"], o2, blk["b3"])
             if "cd" in blk:
-                yd, Ad = self._conv_fwd(blk["cd"], x)
-                sc = self._bn_fwd(blk["bd"], yd, Pout, relu=False)
+                yd, Ad, fd = self._conv_fwd(blk["cd"], x, blk["bd"])
+                sc = self._bn_fwd(blk["bd"], yd, Pout, relu=False, fused=fd)
             else:
                 yd = Ad = None
                 sc = x
-            out = self._bn_fwd(blk["b3"], y3, Pout, relu=True, res=sc)
+            out = self._bn_fwd(blk["b3"], y3, Pout, relu=True, res=sc, fused=f3)
             self.acts[blk["pre"]] = out
             saved.append(dict(x=x, y1=y1, A1=A1, o1=o1, y2=y2, A2=A2, o2=o2, y3=y3, A3=A3, yd=yd, Ad=Ad,
                               out=out))

@@ -50,6 +50,7 @@ def main():
     ap.add_argument("--reps", type=int, default=3)
     ap.add_argument("--out", default=None)
     ap.add_argument("--chosen", action="store_true", help="also time the tuner's chosen shape of every kernel")
+    ap.add_argument("--launches", default=None, help="also write per-launch untransformed times (jsonl)")
     ap.add_argument("--no-spin", action="store_true",
                     help="time launches on an idle stream (the events then include the host's launch latency)")
     args = ap.parse_args()
@@ -70,6 +71,7 @@ def main():
     orig = collections.defaultdict(float)
     ptb = collections.defaultdict(float)
     n = collections.Counter()
+    per = collections.defaultdict(float)
     alg_b = collections.defaultdict(float)
     alg_f = collections.defaultdict(float)
     for name, dk in tr.program:
@@ -88,6 +90,7 @@ def main():
             L = dk.original(s, timed=True)
             L.wait()
             orig[dk.kind] += L.elapsed_ns / 1e3 / args.reps
+            per[name] += L.elapsed_ns / 1e3 / args.reps
             w = min(dk.total_blocks * dk.info.cluster, 148 * max(1, dk.info.occupancy_ptb))
             ahead()
             L = dk.ptb(s, w, timed=True)
@@ -141,6 +144,12 @@ def main():
     if chosen:
         out["step_us_chosen"] = sum(chosen.values())
         out["chosen_vs_original_speed"] = tot_o / sum(chosen.values())
+    if args.launches:
+        with open(args.launches, "w") as f:
+            for name, dk in tr.program:
+                f.write(json.dumps({"name": name, "kind": dk.kind, "us": round(per[name], 2), "blocks": dk.total_blocks,
+                                    "alg_MB": round(dk.info.alg_bytes / 1e6, 2),
+                                    "alg_MFLOP": round(dk.info.alg_flops / 1e6, 1)}) + "\n")
     txt = json.dumps(out, indent=1)
     print(txt)
     if args.out:
