@@ -1884,6 +1884,16 @@ static int bind_gemm(const tally_kernel_args* a, Instance* inst, bool split) {
       // tile per cluster vs 196 us persistent) while leaving >= 2 blocks per pair
       const long long tiles_all = (long long)p.tiles_m * p.tiles_n * p.splits * p.batches;
       p.tpb = (int)std::max(1ll, std::min<long long>({4ll, (32 + p.kb_per_split - 1) / p.kb_per_split, tiles_all / 148}));
+      // short-K tiles (<= 4 k-blocks: epilogue-bound, ~2-3 us each): whole
+      // waves of the 74 pairs with <= 8 tiles per block -- tpb = ceil(tiles /
+      // (74 w)), w the fewest waves that allow it (ResNet-50 1x1 convolutions:
+      // 4 tiles per block left 1.3-2.6 waves; 38.9 -> 34.8, 28.7 -> 24.6,
+      // 28.7 -> 20.5 us Original, bnfuse_bench)
+      static const int old_pair = getenv("TALLY_PAIR_TPB_OLD") != nullptr;   // experiment knob
+      if (p.kb_per_split <= 4 && !old_pair) {
+        const long long waves = (tiles_all + 74 * 8 - 1) / (74 * 8);
+        p.tpb = (int)std::max(1ll, (tiles_all + 74 * waves - 1) / (74 * waves));
+      }
     }
   }
   p.total_tiles = (long long)p.tiles_m * p.tiles_n * p.splits * p.batches;
