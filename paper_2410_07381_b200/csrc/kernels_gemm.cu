@@ -230,6 +230,23 @@ __device__ __forceinline__ uint64_t smem_desc_mn(const void* p) {
   return d;
 }
 
+// No-swizzle ("interleaved") operand tiles of the narrow-channel implicit
+// convolutions (CONV 3 / 4: 8-channel NHWC input, one TMA im2col load per
+// filter tap of 128 / 64 pixels x 16 B, written densely): core matrices of
+// 8 rows x 16 B.  K-major A (forward): K-adjacent core matrices (the next
+// tap) 2048 B apart (LBO), M-adjacent (next 8 pixels) 128 B (SBO).
+// MN-major B (weight gradient): K-adjacent (next 8 pixels) 128 B apart
+// (LBO), N-adjacent (next tap's 8 channels) 1024 B (SBO).
+__device__ __forceinline__ uint64_t smem_desc_ns(const void* p, uint32_t lbo, uint32_t sbo) {
+  const uint64_t addr = smem_u32(p);
+  uint64_t d = 0;
+  d |= (addr & 0x3FFFFull) >> 4;
+  d |= (uint64_t)(lbo >> 4) << 16;
+  d |= (uint64_t)(sbo >> 4) << 32;
+  d |= 1ull << 46;                        // descriptor version (sm_100); layout 0 = SWIZZLE_NONE
+  return d;
+}
+
 // Instruction descriptor: D fp32, A and B K-major (or both MN-major), M = 128
 // (256 for a CTA pair), N = BN.
 template <int KIND, int BN, bool A_MN = false, bool B_MN = false, int MMA_M = 128>
@@ -399,6 +416,10 @@ using CfgConvF32 = CfgBf16T<128, float, false, false, 1, 1>;
 using CfgConvF32N64 = CfgBf16T<64, float, false, false, 1, 1>;
 using CfgConvW = CfgBf16T<128, float, true, true, 1, 2>;
 using CfgConvWN64 = CfgBf16T<64, float, true, true, 1, 2>;
+// 8-channel input (the ResNet stem's 3 channels padded to 8): a k-block is 8
+// filter taps x 8 channels, one 16-byte-wide im2col load per tap, no swizzle
+using CfgConvFC8 = CfgBf16T<64, __nv_bfloat16, false, false, 1, 3>;
+using CfgConvWC8 = CfgBf16T<64, float, true, true, 1, 4>;
 template <class Cfg, class = void>
 struct ConvOf { static constexpr int value = 0; };
 template <class Cfg>
@@ -447,7 +468,7 @@ struct alignas(64) GemmParams {
   int ep_pre;
   // implicit-GEMM convolution (CONV kinds): the im2col map is a_hi (forward)
   // or b_hi (weight gradient); output pixels o = (n, p, q) with hw = ho * wo
-  int cv_c, cv_k, cv_cblocks, cv_stride, cv_pad, cv_wo, cv_hw;
+  int cv_c, cv_k, cv_cblocks, cv_stride, cv_pad, cv_wo, cv_hw, cv_n;
   // fused batch-norm statistics of the bf16 output (bnfuse.cuh; part null: off)
   BnFuse bnf;
 };
@@ -812,6 +833,18 @@ k_gemm(const __grid_constant__ GemmParams p, const ShapeArgs s) {
                 const int n0 = am / p.cv_hw, rem = am - n0 * p.cv_hw, p0 = rem / p.cv_wo, q0 = rem - p0 * p.cv_wo;
                 tma_load_im2col(base, &p.a_hi, &full[st], cb * 64, q0 * p.cv_stride - p.cv_pad,
                                 p0 * p.cv_stride - p.cv_pad, n0, sx, r);
+              } else if constexpr (ConvOf<Cfg>::value == 3) {
+                // A = im2col(x), 8 channels: one 128-pixel x 16 B load per
+                // tap of the k-block (taps past k*k: an image index past the
+                // batch -- zeros)
+                const int n0 = am / p.cv_hw, rem = am - n0 * p.cv_hw, p0 = rem / p.cv_wo, q0 = rem - p0 * p.cv_wo;
+#pragma unroll 1
+                for (int t = 0; t < 8; ++t) {
+                  const int tap = kb * 8 + t, ok = tap < p.cv_k * p.cv_k;
+                  const int r = ok ? tap / p.cv_k : 0, sx = ok ? tap - r * p.cv_k : 0;
+                  tma_load_im2col(base + t * 2048, &p.a_hi, &full[st], 0, q0 * p.cv_stride - p.cv_pad,
+                                  p0 * p.cv_stride - p.cv_pad, ok ? n0 : p.cv_n, sx, r);
+                }
               } else if constexpr (Cfg::A_MN) {
                 // boxes of 64 M-elements x BK K-rows, 8 KB each
 #pragma unroll
@@ -830,6 +863,18 @@ k_gemm(const __grid_constant__ GemmParams p, const ShapeArgs s) {
                   const int r = tap / p.cv_k, sx = tap - r * p.cv_k;
                   tma_load_im2col(base + Cfg::A_BYTES + h * 8192, &p.b_hi, &full[st], ch, q0 * p.cv_stride - p.cv_pad,
                                   p0 * p.cv_stride - p.cv_pad, n0, sx, r);
+                }
+              } else if constexpr (ConvOf<Cfg>::value == 4) {
+                // B = im2col(x) MN-major, 8 channels: N = (tap, channel), one
+                // 64-pixel x 16 B load per tap of this 64-wide N tile
+                const int px = kb * Cfg::BK;
+                const int n0 = px / p.cv_hw, rem = px - n0 * p.cv_hw, p0 = rem / p.cv_wo, q0 = rem - p0 * p.cv_wo;
+#pragma unroll 1
+                for (int t = 0; t < 8; ++t) {
+                  const int tap = bn0 / 8 + t, ok = tap < p.cv_k * p.cv_k;
+                  const int r = ok ? tap / p.cv_k : 0, sx = ok ? tap - r * p.cv_k : 0;
+                  tma_load_im2col(base + Cfg::A_BYTES + t * 1024, &p.b_hi, &full[st], 0, q0 * p.cv_stride - p.cv_pad,
+                                  p0 * p.cv_stride - p.cv_pad, ok ? n0 : p.cv_n, sx, r);
                 }
               } else if constexpr (Cfg::B_MN) {
 #pragma unroll
@@ -902,9 +947,12 @@ k_gemm(const __grid_constant__ GemmParams p, const ShapeArgs s) {
               } else {
                 // MN-major: UMMA_K = 16 K-rows = two 8-row groups = 2048 B per step;
                 // K-major: 32 B per step inside the 128 B swizzle atom
-                const uint64_t da = Cfg::A_MN ? smem_desc_mn(base + k * 2048) : smem_desc(base + koff);
-                const uint64_t db = Cfg::B_MN ? smem_desc_mn(base + Cfg::A_BYTES + k * 2048)
-                                              : smem_desc(base + Cfg::A_BYTES + koff);
+                uint64_t da = Cfg::A_MN ? smem_desc_mn(base + k * 2048) : smem_desc(base + koff);
+                uint64_t db = Cfg::B_MN ? smem_desc_mn(base + Cfg::A_BYTES + k * 2048)
+                                        : smem_desc(base + Cfg::A_BYTES + koff);
+                // narrow-channel convolutions: 16 K = two taps per MMA step
+                if constexpr (ConvOf<Cfg>::value == 3) da = smem_desc_ns(base + k * 4096, 2048, 128);
+                if constexpr (ConvOf<Cfg>::value == 4) db = smem_desc_ns(base + Cfg::A_BYTES + k * 256, 128, 1024);
                 if constexpr (PR == 2) umma_pair(d, da, db, idesc, first);
                 else umma<1>(d, da, db, idesc, first);
               }
@@ -1634,7 +1682,8 @@ typedef CUresult (*EncodeIm2colFn)(CUtensorMap*, CUtensorMapDataType, cuuint32_t
 // 64 channels (128 B rows, 128B swizzle -- the K-major / MN-major operand
 // tile layouts), traversal stride = the convolution stride, the pixel box
 // [-pad, W - 1 + pad - (k - 1)] per spatial dimension (zeros outside)
-static int make_im2col_map(CUtensorMap* m, const void* x, const tally_conv_geometry& g, int pixels) {
+static int make_im2col_map(CUtensorMap* m, const void* x, const tally_conv_geometry& g, int pixels,
+                           bool narrow = false) {
   static EncodeIm2colFn enc = [] {
     void* f = nullptr;
     cudaDriverEntryPointQueryResult q;
@@ -1649,8 +1698,10 @@ static int make_im2col_map(CUtensorMap* m, const void* x, const tally_conv_geome
   int lower[2] = {-g.pad, -g.pad};
   int upper[2] = {g.pad - (g.k - 1), g.pad - (g.k - 1)};
   cuuint32_t estr[4] = {1, (cuuint32_t)g.stride, (cuuint32_t)g.stride, 1};
-  CUresult r = enc(m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 4, const_cast<void*>(x), dims, strides, lower, upper, 64,
-                   (cuuint32_t)pixels, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+  // narrow: 8-channel boxes (16 B per pixel), written densely (no swizzle)
+  CUresult r = enc(m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 4, const_cast<void*>(x), dims, strides, lower, upper,
+                   narrow ? 8 : 64, (cuuint32_t)pixels, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
+                   narrow ? CU_TENSOR_MAP_SWIZZLE_NONE : CU_TENSOR_MAP_SWIZZLE_128B,
                    CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   if (r != CUDA_SUCCESS) { set_error("cuTensorMapEncodeIm2col failed (%d)", (int)r); return TALLY_EINVAL; }
   return TALLY_OK;
@@ -1710,25 +1761,30 @@ static int bind_gemm(const tally_kernel_args* a, Instance* inst, bool split) {
     // implicit-GEMM convolution: ptr[3] = tally_conv_geometry
     constexpr int CV = gemm::ConvOf<Cfg>::value;
     const tally_conv_geometry* G = static_cast<const tally_conv_geometry*>(a->ptr[3]);
-    if (!G || G->n < 1 || G->h < 1 || G->w < 1 || G->c < 64 || G->c % 64 || G->k < 1 || G->stride < 1 ||
-        G->pad < 0 || G->k > 8 || G->pad >= G->k) {
-      set_error("conv: need a geometry with c %% 64 == 0, 1 <= k <= 8, stride >= 1, 0 <= pad < k");
+    constexpr bool narrow = CV >= 3;
+    if (!G || G->n < 1 || G->h < 1 || G->w < 1 || (narrow ? G->c != 8 : (G->c < 64 || G->c % 64)) || G->k < 1 ||
+        G->stride < 1 || G->pad < 0 || G->k > 8 || G->pad >= G->k) {
+      set_error("conv: need a geometry with c %% 64 == 0 (the *_c8 kinds: c == 8), 1 <= k <= 8, stride >= 1, "
+                "0 <= pad < k");
       return TALLY_EINVAL;
     }
     const long long ho = (G->h + 2 * G->pad - G->k) / G->stride + 1, wo = (G->w + 2 * G->pad - G->k) / G->stride + 1;
     const long long P = (long long)G->n * ho * wo, Kd = (long long)G->k * G->k * G->c;
-    if (ho < 1 || wo < 1 || (CV == 1 && (M != P || K != Kd)) || (CV == 2 && (N != Kd || K != P)) ||
+    // (narrow kinds: the k*k*8 taps padded to whole 64-wide k-blocks / N tiles)
+    const long long Kp = narrow ? (Kd + 63) / 64 * 64 : Kd;
+    constexpr bool fwd = CV == 1 || CV == 3;
+    if (ho < 1 || wo < 1 || (fwd && (M != P || K != Kp)) || (!fwd && (N != Kp || K != P)) ||
         (CV == 2 && G->c % Cfg::BN != 0 && Cfg::BN > G->c)) {
       set_error("conv: GEMM shape does not match the geometry (forward: M = n*ho*wo, K = k*k*c; weight "
                 "gradient: N = k*k*c, K = n*ho*wo)");
       return TALLY_EINVAL;
     }
-    if constexpr (CV == 1) {
-      if ((rc = make_im2col_map(&p.a_hi, a->ptr[0], *G, Cfg::BM))) return rc;
+    if constexpr (fwd) {
+      if ((rc = make_im2col_map(&p.a_hi, a->ptr[0], *G, Cfg::BM, narrow))) return rc;
       if ((rc = make_map(&p.b_hi, a->ptr[1], dt, Cfg::ESZ, N, K, Cfg::BN))) return rc;
     } else {
       if ((rc = make_map(&p.a_hi, a->ptr[0], dt, Cfg::ESZ, K, M, Cfg::BK))) return rc;   // dy [P, cout], MN-major
-      if ((rc = make_im2col_map(&p.b_hi, a->ptr[1], *G, Cfg::BK))) return rc;
+      if ((rc = make_im2col_map(&p.b_hi, a->ptr[1], *G, Cfg::BK, narrow))) return rc;
     }
     p.c = a->ptr[2];
     p.cv_c = G->c;
@@ -1738,6 +1794,7 @@ static int bind_gemm(const tally_kernel_args* a, Instance* inst, bool split) {
     p.cv_pad = G->pad;
     p.cv_wo = (int)wo;
     p.cv_hw = (int)(ho * wo);
+    p.cv_n = G->n;
   } else {       // ptr: A, B, C [, layout]; MN-major operand = its transpose stored row-major
     const tally_gemm_layout* L = static_cast<const tally_gemm_layout*>(a->ptr[3]);
     const long long ar = L ? L->a_rows : (Cfg::A_MN ? K : M), acl = L ? L->a_cols : (Cfg::A_MN ? M : K);
@@ -1884,16 +1941,10 @@ static int bind_gemm(const tally_kernel_args* a, Instance* inst, bool split) {
       // tile per cluster vs 196 us persistent) while leaving >= 2 blocks per pair
       const long long tiles_all = (long long)p.tiles_m * p.tiles_n * p.splits * p.batches;
       p.tpb = (int)std::max(1ll, std::min<long long>({4ll, (32 + p.kb_per_split - 1) / p.kb_per_split, tiles_all / 148}));
-      // short-K tiles (<= 4 k-blocks: epilogue-bound, ~2-3 us each): whole
-      // waves of the 74 pairs with <= 8 tiles per block -- tpb = ceil(tiles /
-      // (74 w)), w the fewest waves that allow it (ResNet-50 1x1 convolutions:
-      // 4 tiles per block left 1.3-2.6 waves; 38.9 -> 34.8, 28.7 -> 24.6,
-      // 28.7 -> 20.5 us Original, bnfuse_bench)
-      static const int old_pair = getenv("TALLY_PAIR_TPB_OLD") != nullptr;   // experiment knob
-      if (p.kb_per_split <= 4 && !old_pair) {
-        const long long waves = (tiles_all + 74 * 8 - 1) / (74 * 8);
-        p.tpb = (int)std::max(1ll, (tiles_all + 74 * waves - 1) / (74 * waves));
-      }
+      // (Whole waves of the 74 pairs for short-K tiles -- tpb = ceil(tiles /
+      // (74 w)) -- ran ResNet-50's 1x1 convolutions 10-30 % faster untransformed,
+      // but longer blocks cost the tuner's PTB choices more: C2 step chosen /
+      // untransformed 0.879 -> 0.864 (w >= 2), 0.78 (w >= 1; it sliced them).)
     }
   }
   p.total_tiles = (long long)p.tiles_m * p.tiles_n * p.splits * p.batches;
@@ -2068,7 +2119,7 @@ static KernelKind attn_kind(const char* name) {
 }
 
 int register_gemm_kernels(KernelKind* out, int cap) {
-  if (cap < 28) return 0;
+  if (cap < 30) return 0;
   out[0] = gemm_kind<gemm::CfgTf32x3>("sgemm_tf32x3", bind_sgemm);
   out[1] = gemm_kind<gemm::CfgBf16>("gemm_bf16", bind_bf16<gemm::CfgBf16>);
   out[3] = gemm_kind<gemm::CfgTf32x3N64>("sgemm_tf32x3_n64", bind_sgemm_n64);
@@ -2103,7 +2154,9 @@ int register_gemm_kernels(KernelKind* out, int cap) {
   out[25] = gemm_kind<gemm::CfgConvF32N64>("conv_fprop_bf16f32_n64", bind_bf16<gemm::CfgConvF32N64>);
   out[26] = gemm_kind<gemm::CfgConvW>("conv_wgrad_bf16f32", bind_bf16<gemm::CfgConvW>);
   out[27] = gemm_kind<gemm::CfgConvWN64>("conv_wgrad_bf16f32_n64", bind_bf16<gemm::CfgConvWN64>);
-  return 28;
+  out[28] = gemm_kind<gemm::CfgConvFC8>("conv_fprop_c8_bf16_n64", bind_bf16<gemm::CfgConvFC8>);
+  out[29] = gemm_kind<gemm::CfgConvWC8>("conv_wgrad_c8_bf16f32_n64", bind_bf16<gemm::CfgConvWC8>);
+  return 30;
 }
 
 }  // namespace tally

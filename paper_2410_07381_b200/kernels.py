@@ -173,6 +173,13 @@ class DeviceKernel:
     def total_blocks(self) -> int:
         return self.info.total_blocks
 
+    def full_workers(self, sms: int = 148) -> int:
+        """PTB workers (CTAs) for a full-occupancy launch: every resident slot,
+        at most one per logical block, a multiple of the cluster size."""
+        cl = max(1, self.info.cluster)
+        w = min(self.total_blocks * cl, sms * max(1, self.info.occupancy_ptb))
+        return max(cl, w // cl * cl)
+
     def _launch(self, stream: Stream, desc: _lib.c_launch_desc) -> Launch:
         lid = C.c_int()
         _lib.check(_lib.lib.tally_launch(self.id, stream.id, C.byref(desc), C.byref(lid)),
@@ -499,11 +506,17 @@ def conv_fprop(x, Wt, out, n, h, w, c, k, stride, pad, splits: int = 1,
     ho = (h + 2 * pad - k) // stride + 1
     wo = (w + 2 * pad - k) // stride + 1
     P = n * ho * wo
-    kind = "conv_fprop_bf16" + ("f32" if out.dtype == torch.float32 else "") + ("" if cout % 128 == 0 else "_n64")
+    if c == 8:
+        # 8-channel input (the ResNet stem): a k-block is 8 filter taps, K
+        # padded to whole k-blocks (Wt [cout, ceil(k*k*8 / 64) * 64], zeros past k*k*8)
+        kind, kd = "conv_fprop_c8_bf16_n64", (k * k * 8 + 63) // 64 * 64
+    else:
+        kind = "conv_fprop_bf16" + ("f32" if out.dtype == torch.float32 else "") + ("" if cout % 128 == 0 else "_n64")
+        kd = k * k * c
     g = _conv_geom(n, h, w, c, k, stride, pad)
     extra = () if bn is None else (None, None, None, C.addressof(bn.c))
     return DeviceKernel(kind, (x.data_ptr(), Wt.data_ptr(), out.data_ptr(), C.addressof(g)) + extra,
-                        (P, cout, k * k * c, 0, splits), keep=(x, Wt, out, g) + (() if bn is None else (bn,)))
+                        (P, cout, kd, 0, splits), keep=(x, Wt, out, g) + (() if bn is None else (bn,)))
 
 
 def conv_wgrad(dy, x, gpart, n, h, w, c, k, stride, pad, splits: int = 1) -> DeviceKernel:
@@ -516,6 +529,8 @@ def conv_wgrad(dy, x, gpart, n, h, w, c, k, stride, pad, splits: int = 1) -> Dev
     P = n * ho * wo
     kd = k * k * c
     kind = "conv_wgrad_bf16f32" + ("" if kd % 128 == 0 and c % 128 == 0 else "_n64")
+    if c == 8:   # 8-channel input: N = the k*k*8 taps padded to 64-wide tiles
+        kind, kd = "conv_wgrad_c8_bf16f32_n64", (k * k * 8 + 63) // 64 * 64
     g = _conv_geom(n, h, w, c, k, stride, pad)
     return DeviceKernel(kind, (dy.data_ptr(), x.data_ptr(), gpart.data_ptr(), C.addressof(g)),
                         (cout, kd, P, 0, splits), keep=(dy, x, gpart, g))

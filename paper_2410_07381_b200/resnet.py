@@ -195,6 +195,10 @@ class ResNet50Train:
     # implicit-GEMM convolutions (TMA im2col; see _implicit)
     implicit_conv = os.environ.get("TALLY_IMPLICIT_CONV", "1") != "0"
     implicit_dgrad = os.environ.get("TALLY_IMPLICIT_DGRAD", "1") != "0"
+    # the stem through the narrow-channel implicit kinds: measured slower
+    # (C2 step 10.21 -> 10.49 ms: one 16-byte gather per pixel and tap) than
+    # im2col + GEMM, so off by default
+    implicit_stem = os.environ.get("TALLY_IMPLICIT_STEM", "0") != "0"
     # batch-norm statistics fused into the producing GEMM / convolution
     # epilogue or split-K reduce (csrc/bnfuse.cuh): no bn_stats pass
     fuse_bn_stats = os.environ.get("TALLY_BN_FUSE", "1") != "0"
@@ -345,8 +349,9 @@ class ResNet50Train:
     def _implicit(self, s):
         """k x k / strided convolution as an implicit GEMM (TMA im2col loads of
         the NHWC activation, no column matrix): every one but the stem (3
-        channels padded to 8: not a 64-channel box)."""
-        return self.implicit_conv and not s.direct and s.cin % 64 == 0
+        channels padded to 8), which can go through the narrow-channel kinds
+        (one 16-byte im2col load per filter tap; TALLY_IMPLICIT_STEM=1)."""
+        return self.implicit_conv and not s.direct and (s.cin % 64 == 0 or (s.cin == IN_CH and self.implicit_stem))
 
     def _implicit_dgrad(self, s, conv):
         """Stride-1 "same" k x k convolutions: dx as an implicit-GEMM forward

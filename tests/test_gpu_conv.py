@@ -125,3 +125,68 @@ def test_conv_dgrad_as_flipped_forward_conv(env, geom):
     y.backward(dy.float().view(n, h, w, cout).permute(0, 3, 1, 2))
     ref = x.grad.permute(0, 2, 3, 1).reshape(n * h * w, c)
     assert _rel(out, ref) < 1e-2
+
+
+STEM_GEOMS = [  # n, h, w, c (3 real channels padded to 8), cout, k, stride, pad -- the ResNet-50 stem
+    (2, 32, 32, 8, 64, 7, 2, 3),
+    (8, 30, 26, 8, 64, 7, 2, 3),   # (P = n*ho*wo a multiple of 8: the GEMM's K for the weight gradient)
+    (2, 16, 16, 8, 64, 3, 1, 1),
+]
+
+
+def _stem_inputs(geom, seed):
+    n, h, w, c, cout, k, stride, pad = geom
+    g = torch.Generator(device="cuda").manual_seed(seed + sum(geom))
+    x = (torch.randn(n, h, w, c, device="cuda", generator=g) * 0.5)
+    x[..., 3:] = 0   # the stem's padding channels
+    kd = k * k * c
+    kp = (kd + 63) // 64 * 64
+    wt = torch.zeros(cout, kp, device="cuda")
+    wt[:, :kd] = torch.randn(cout, kd, device="cuda", generator=g) * 0.05
+    return x.bfloat16(), wt.bfloat16(), kd, kp
+
+
+@pytest.mark.parametrize("geom", STEM_GEOMS)
+def test_conv_fprop_c8_matches_im2col_gemm(env, geom):
+    """8-channel implicit convolution (one 16-byte im2col load per filter tap,
+    no-swizzle operand layout) against im2col + GEMM (bit-identical) and
+    PyTorch conv2d."""
+    P, K, s = env
+    n, h, w, c, cout, k, stride, pad = geom
+    x, wt, kd, kp = _stem_inputs(geom, 11)
+    ho, wo = (h + 2 * pad - k) // stride + 1, (w + 2 * pad - k) // stride + 1
+    Pn = n * ho * wo
+    y = torch.zeros(Pn, cout, device="cuda", dtype=torch.bfloat16)
+    dk = K.conv_fprop(x, wt, y, n, h, w, c, k, stride, pad)
+    assert dk.kind == "conv_fprop_c8_bf16_n64"
+    out = _shapes(P, dk, s, y)
+    col = torch.zeros(Pn, kp, device="cuda", dtype=torch.bfloat16)
+    K.im2col(x, col, n, h, w, c, k, k, stride, pad).original(s).wait()
+    y2 = torch.zeros_like(y)
+    K.gemm(col, wt, y2).original(s).wait()
+    assert torch.equal(out, y2)
+    ref = torch.nn.functional.conv2d(x.float().permute(0, 3, 1, 2),
+                                     wt[:, :kd].float().view(cout, k, k, c).permute(0, 3, 1, 2),
+                                     stride=stride, padding=pad)
+    assert _rel(out, ref.permute(0, 2, 3, 1).reshape(Pn, cout)) < 1e-2
+
+
+@pytest.mark.parametrize("geom", STEM_GEOMS)
+def test_conv_wgrad_c8_matches_gemm_mn(env, geom):
+    P, K, s = env
+    n, h, w, c, cout, k, stride, pad = geom
+    x, _, kd, kp = _stem_inputs(geom, 5)
+    ho, wo = (h + 2 * pad - k) // stride + 1, (w + 2 * pad - k) // stride + 1
+    Pn = n * ho * wo
+    g = torch.Generator(device="cuda").manual_seed(99)
+    dy = (torch.randn(Pn, cout, device="cuda", generator=g) * 0.5).bfloat16()
+    part = torch.zeros(1, cout, kp, device="cuda")
+    dk = K.conv_wgrad(dy, x, part, n, h, w, c, k, stride, pad)
+    assert dk.kind == "conv_wgrad_c8_bf16f32_n64"
+    out = _shapes(P, dk, s, part)
+    col = torch.zeros(Pn, kp, device="cuda", dtype=torch.bfloat16)
+    K.im2col(x, col, n, h, w, c, k, k, stride, pad).original(s).wait()
+    part2 = torch.zeros_like(part)
+    K.gemm_mn(dy, col, part2).original(s).wait()
+    assert torch.equal(out, part2)
+    assert bool((out[0, :, kd:] == 0).all())   # padded taps: zero gradient

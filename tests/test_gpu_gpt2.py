@@ -202,7 +202,7 @@ def test_gpt2_step_shapes_bit_identical(env):
             if shape == "original":
                 dk.original(stream).wait()
             elif shape == "ptb":
-                dk.ptb(stream, min(dk.total_blocks, 148 * max(1, dk.info.occupancy_ptb))).wait()
+                dk.ptb(stream, dk.full_workers()).wait()
             else:
                 for off, cnt in P.slice_plan(dk.total_blocks, Fraction(1, 4)):
                     dk.sliced(stream, off, cnt).wait()

@@ -428,7 +428,7 @@ def test_resnet50_train_step_shapes_bit_identical(env):
             if shape == "original":
                 dk.original(stream).wait()
             elif shape == "ptb":
-                dk.ptb(stream, min(dk.total_blocks, 148 * max(1, dk.info.occupancy_ptb))).wait()
+                dk.ptb(stream, dk.full_workers()).wait()
             else:
                 for off, cnt in P.slice_plan(dk.total_blocks, Fraction(1, 4)):
                     dk.sliced(stream, off, cnt).wait()
@@ -540,7 +540,7 @@ def test_gemm_ex_causal_rules(env):
             for off, cnt in P.slice_plan(dk.total_blocks, Fraction(1, 3)):
                 dk.sliced(stream, off, cnt).wait()
         else:
-            dk.ptb(stream, min(dk.total_blocks, 148)).wait()
+            dk.ptb(stream, min(dk.full_workers(), 148)).wait()
         outs[shape] = S.clone()
     ref = (qh @ kh.transpose(-1, -2)).reshape(B_ * H, T, T)
     got = outs["original"].view(B_ * H, T, T)

@@ -72,7 +72,7 @@ def main():
     # the same, every kernel in PTB shape at full resident occupancy
     aggp = collections.defaultdict(lambda: [0, 0.0])
     for name, dk in tr.program:
-        L = dk.ptb(s, min(dk.total_blocks, 148 * max(1, dk.info.occupancy_ptb)), timed=True)
+        L = dk.ptb(s, dk.full_workers(), timed=True)
         L.wait()
         aggp[dk.kind][0] += 1
         aggp[dk.kind][1] += L.elapsed_ns / 1e3

@@ -50,7 +50,7 @@ def main():
         a[0] += 1
         a[1] += L.elapsed_ns / 1e3
         a[2] += dk.info.alg_flops
-        Lp = dk.ptb(s, min(dk.total_blocks, 148 * max(1, dk.info.occupancy_ptb)), timed=True)
+        Lp = dk.ptb(s, dk.full_workers(), timed=True)
         Lp.wait()
         a[3] += Lp.elapsed_ns / 1e3
         a[4] += dk.info.alg_bytes

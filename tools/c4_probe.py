@@ -57,7 +57,7 @@ def main():
         Ls = []
         for _, dk in tr.program:
             if shape == "ptb":
-                Ls.append(dk.ptb(be_s, min(dk.total_blocks, 148 * max(1, dk.info.occupancy_ptb))))
+                Ls.append(dk.ptb(be_s, dk.full_workers()))
             else:
                 Ls.append(dk.original(be_s))
         return Ls

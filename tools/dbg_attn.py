@@ -13,7 +13,7 @@ seen = set()
 for name, dk in tr.program:
     if dk.kind in seen: continue
     seen.add(dk.kind)
-    w = min(dk.total_blocks * dk.info.cluster, 148 * max(1, dk.info.occupancy_ptb))
+    w = dk.full_workers()
     try:
         dk.original(s).wait()
         dk.ptb(s, w).wait()

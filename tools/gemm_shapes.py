@@ -50,7 +50,7 @@ def main():
         B = (torch.randn(N, K, device="cuda", generator=g) * 0.1).bfloat16()
         C = torch.empty(M, N, dtype=dt, device="cuda")
         dk = kernels.gemm(A, B, C)
-        workers = min(dk.total_blocks, 148 * max(1, dk.info.occupancy_ptb))
+        workers = dk.full_workers()
 
         def timed(fn, reps=5):
             ts = []

@@ -43,7 +43,7 @@ def main():
         for n in names:
             dk = progs[n]
             dk.original(s).wait()
-            dk.ptb(s, min(dk.total_blocks, 148 * max(1, dk.info.occupancy_ptb))).wait()
+            dk.ptb(s, dk.full_workers()).wait()
     torch.cuda.synchronize()
     print("ncu_c2 done:", mode)
 

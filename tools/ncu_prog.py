@@ -53,7 +53,7 @@ def main():
             # exact name, else the first program entry containing it
             dk = progs[n] if n in progs else next(d for m, d in tr.program if n in m)
             dk.original(s).wait()
-            dk.ptb(s, min(dk.total_blocks * dk.info.cluster, 148 * max(1, dk.info.occupancy_ptb))).wait()
+            dk.ptb(s, dk.full_workers()).wait()
     torch.cuda.synchronize()
     print("ncu_prog done:", args.config, args.mode)
 

@@ -91,7 +91,7 @@ def main():
             L.wait()
             orig[dk.kind] += L.elapsed_ns / 1e3 / args.reps
             per[name] += L.elapsed_ns / 1e3 / args.reps
-            w = min(dk.total_blocks * dk.info.cluster, 148 * max(1, dk.info.occupancy_ptb))
+            w = dk.full_workers()
             ahead()
             L = dk.ptb(s, w, timed=True)
             L.wait()
