@@ -39,7 +39,7 @@ struct alignas(64) LaunchRec {
   unsigned long long stops;         // workers that stopped because of the flag
   unsigned long long neg_first_start;  // ~min worker entry %globaltimer (0 = none yet)
   unsigned long long last_busy_exit;   // max exit %globaltimer of workers that ran a block
-  unsigned long long pad[1];
+  unsigned long long pops;             // return-ring pops started by this launch (<= ret_pending succeed)
 };
 
 // Worker retirement is two-level: workers fold into their group of 32
@@ -382,7 +382,7 @@ __device__ __forceinline__ void ptb_worker_exit(const PtbArgs& a, bool stopped,
 #ifdef TALLY_EXPERIMENT_NO_MIRROR   // timing experiment only (tools/ptb_publish_cost.py): no host writes
   r->claims = 0ull; r->exited = 0u; r->neg_first_stop = 0ull; r->executed = 0ull; r->stops = 0ull;
   r->neg_first_start = 0ull;
-  if (progress == ~0ull) r->pad[0] = nfs + nst + stops + now + pending;
+  if (progress == ~0ull) r->pops = nfs + nst + stops + now + pending;
   return;
 #endif
   volatile LaunchMirror* m = a.mirror;
@@ -410,6 +410,7 @@ __device__ __forceinline__ void ptb_worker_exit(const PtbArgs& a, bool stopped,
   r->stops = 0ull;
   r->neg_first_start = 0ull;
   r->last_busy_exit = 0ull;
+  r->pops = 0ull;
   st_release_sys(const_cast<unsigned*>(&m->serial), a.serial);
 }
 
@@ -461,19 +462,22 @@ __device__ __forceinline__ long long ptb_claim_gated(const PtbArgs& a) {
 // next batch), so the ring holds <= 2 entries per worker and one pop takes a
 // whole range.
 // A range an earlier launch of the chain handed back; -1 when none is left.
+// The entries a launch may pop are exactly the ret_pending ones its chain's
+// previous launch left (they are all written: that launch has exited); pushes
+// by this launch's own workers land behind them.  A per-launch ticket bounds
+// the pops, so each is two fetch-adds and no retries -- a CAS loop on the ring
+// head let a resumed launch's ~1200 workers contend for hundreds of
+// microseconds (C2 / C3 preemption drains up to ~300 us).
 __device__ __forceinline__ long long ptb_pop_range(const PtbArgs& a, int& count) {
   unsigned long long* ring = a.ret_ring;
-  for (;;) {
-    const unsigned long long h = atomicAdd(ring + 1, 0ull), t = atomicAdd(ring, 0ull);
-    if (h >= t) return -1;
-    if (atomicCAS(ring + 1, h, h + 1) != h) continue;
-    volatile unsigned long long* e = ring + 2 + (h % kRetCap);
-    unsigned long long v;
-    while ((v = *e) == 0ull) __nanosleep(32);
-    *e = 0ull;
-    count = (int)(v >> 48);
-    return (long long)(v & 0xFFFFFFFFFFFFull) - 1;
-  }
+  if (atomicAdd(&a.rec->pops, 1ull) >= a.ret_pending) return -1;
+  const unsigned long long h = atomicAdd(ring + 1, 1ull);
+  volatile unsigned long long* e = ring + 2 + (h % kRetCap);
+  unsigned long long v;
+  while ((v = *e) == 0ull) __nanosleep(32);
+  *e = 0ull;
+  count = (int)(v >> 48);
+  return (long long)(v & 0xFFFFFFFFFFFFull) - 1;
 }
 __device__ __forceinline__ void ptb_return_range(const PtbArgs& a, long long first, long long count) {
   if (count <= 0) return;
