@@ -270,11 +270,20 @@ struct Transpose {
 #ifndef TALLY_BN_BWD_ROWS
 #define TALLY_BN_BWD_ROWS 2
 #endif
+#ifndef TALLY_COLSTATS_ROWS
+#define TALLY_COLSTATS_ROWS 2
+#endif
+#ifndef TALLY_COLSTATS_MINBLOCKS
+#define TALLY_COLSTATS_MINBLOCKS 3
+#endif
 template <int MODE>
 struct BnStats {
   static constexpr int kThreads = 256;
-  static constexpr int kMinBlocks = MODE == 0 ? 4 : MODE >= 3 ? 3 : TALLY_BN_BWD_MINBLOCKS;   // register cap: bytes in flight per SM
-  static constexpr int kRows = MODE == 0 ? kIlp : MODE >= 3 ? 2 : TALLY_BN_BWD_ROWS;   // rows in flight per thread (1 or 4 streams each)
+  // (mode 2, column sums: four rows per thread in flight at two CTAs per SM
+  // measured slower -- BERT-large step 22.88 -> 23.13 ms; TALLY_COLSTATS_ROWS /
+  // _MINBLOCKS experiment knobs)
+  static constexpr int kMinBlocks = MODE == 0 ? 4 : MODE >= 3 ? 3 : MODE == 2 ? TALLY_COLSTATS_MINBLOCKS : TALLY_BN_BWD_MINBLOCKS;
+  static constexpr int kRows = MODE == 0 ? kIlp : MODE >= 3 ? 2 : MODE == 2 ? TALLY_COLSTATS_ROWS : TALLY_BN_BWD_ROWS;
   static constexpr int kGroup = 32;
   struct Params {
     const uint4* x;        // pre-BN activations [P, C]
