@@ -731,7 +731,7 @@ struct BnAct {
         }
       } else if (p.relu == 3) {
 #pragma unroll
-        for (int e = 0; e < 8; ++e) x[e] = 0.5f * x[e] * (1.f + erff(x[e] * 0.7071067811865476f));
+        for (int e = 0; e < 8; ++e) x[e] = gelu_erf(x[e]);
       }
       st16(p.y + v, pack8(x));
     }

@@ -16,6 +16,7 @@
 
 #include <cstdio>
 
+#include "epilogue.cuh"
 #include "registry.h"
 
 namespace tally {
@@ -192,7 +193,7 @@ __device__ __forceinline__ float gelu_grad(float x) {
   return 0.5f * (1.f + t) + 0.5f * x * (1.f - t * t) * k0 * (1.f + 3.f * k1 * x * x);
 }
 __device__ __forceinline__ float gelu_erf_grad(float x) {   // BERT "gelu": x * Phi(x)
-  return 0.5f * (1.f + erff(x * 0.7071067811865476f)) + x * 0.3989422804014327f * __expf(-0.5f * x * x);
+  return gelu_erf_grad_fast(x);   // (epilogue.cuh)
 }
 
 struct GeluBwd {
