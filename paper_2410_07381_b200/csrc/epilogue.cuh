@@ -50,6 +50,66 @@ __device__ __forceinline__ float gelu_erf_grad_fast(float x) {   // Phi(x) + x p
   return fmaf(x * 0.3989422804014327f, __expf(-z2), Phi);
 }
 
+// Two elements at a time: the polynomial and the multiplies as packed fp32
+// pairs (fma/mul.rn.f32x2), the reciprocal and exponentials per element --
+// these elementwise kernels are issue-bound (ncu: 82-84 % issue active).
+__device__ __forceinline__ unsigned long long f2_pack(float a, float b) {
+  unsigned long long r;
+  asm("mov.b64 %0, {%1, %2};" : "=l"(r) : "f"(a), "f"(b));
+  return r;
+}
+__device__ __forceinline__ void f2_unpack(unsigned long long v, float& a, float& b) {
+  asm("mov.b64 {%0, %1}, %2;" : "=f"(a), "=f"(b) : "l"(v));
+}
+__device__ __forceinline__ unsigned long long f2_fma(unsigned long long a, unsigned long long b, unsigned long long c) {
+  unsigned long long d;
+  asm("fma.rn.f32x2 %0, %1, %2, %3;" : "=l"(d) : "l"(a), "l"(b), "l"(c));
+  return d;
+}
+__device__ __forceinline__ unsigned long long f2_mul(unsigned long long a, unsigned long long b) {
+  unsigned long long d;
+  asm("mul.rn.f32x2 %0, %1, %2;" : "=l"(d) : "l"(a), "l"(b));
+  return d;
+}
+// erfc(a0), erfc(a1) (a >= 0, z2 = a * a) -- erfc_abs_p on a pair
+__device__ __forceinline__ void erfc_abs_p2(float a0, float a1, float z0, float z1, float& e0, float& e1) {
+  const float t0 = __fdividef(1.f, fmaf(0.5f, a0, 1.f)), t1 = __fdividef(1.f, fmaf(0.5f, a1, 1.f));
+  const unsigned long long t = f2_pack(t0, t1);
+  unsigned long long q = f2_pack(0.17087277f, 0.17087277f);
+  q = f2_fma(q, t, f2_pack(-0.82215223f, -0.82215223f));
+  q = f2_fma(q, t, f2_pack(1.48851587f, 1.48851587f));
+  q = f2_fma(q, t, f2_pack(-1.13520398f, -1.13520398f));
+  q = f2_fma(q, t, f2_pack(0.27886807f, 0.27886807f));
+  q = f2_fma(q, t, f2_pack(-0.18628806f, -0.18628806f));
+  q = f2_fma(q, t, f2_pack(0.09678418f, 0.09678418f));
+  q = f2_fma(q, t, f2_pack(0.37409196f, 0.37409196f));
+  q = f2_fma(q, t, f2_pack(1.00002368f, 1.00002368f));
+  q = f2_fma(q, t, f2_pack(-1.26551223f, -1.26551223f));
+  float q0, q1;
+  f2_unpack(q, q0, q1);
+  e0 = t0 * __expf(q0 - z0);
+  e1 = t1 * __expf(q1 - z1);
+}
+__device__ __forceinline__ void gelu_erf2(float& x0, float& x1) {
+  const float a0 = fabsf(x0) * 0.7071067811865476f, a1 = fabsf(x1) * 0.7071067811865476f;
+  float e0, e1;
+  erfc_abs_p2(a0, a1, a0 * a0, a1 * a1, e0, e1);
+  const float p0 = x0 >= 0.f ? fmaf(-0.5f, e0, 1.f) : 0.5f * e0;
+  const float p1 = x1 >= 0.f ? fmaf(-0.5f, e1, 1.f) : 0.5f * e1;
+  x0 *= p0;
+  x1 *= p1;
+}
+__device__ __forceinline__ void gelu_erf_grad2(float x0, float x1, float& d0, float& d1) {
+  const float a0 = fabsf(x0) * 0.7071067811865476f, a1 = fabsf(x1) * 0.7071067811865476f;
+  const float z0 = a0 * a0, z1 = a1 * a1;
+  float e0, e1;
+  erfc_abs_p2(a0, a1, z0, z1, e0, e1);
+  const float P0 = x0 >= 0.f ? fmaf(-0.5f, e0, 1.f) : 0.5f * e0;
+  const float P1 = x1 >= 0.f ? fmaf(-0.5f, e1, 1.f) : 0.5f * e1;
+  d0 = fmaf(x0 * 0.3989422804014327f, __expf(-z0), P0);
+  d1 = fmaf(x1 * 0.3989422804014327f, __expf(-z1), P1);
+}
+
 __device__ __forceinline__ float ep_act(float x, int act) {
   if (act == 1) return fmaxf(x, 0.f);
   if (act == 2) {

@@ -681,7 +681,10 @@ struct BnAct {
     long long nvec;
     int C, relu;          // activation: 0 none, 1 ReLU, 2 GELU (tanh approximation), 3 GELU (erf)
   };
-  static __device__ __forceinline__ void run(const Params& p, uint3 bidx, uint3, char*) {
+  // (the activation is chosen once per block -- chosen per element, the
+  // compiler if-converted every variant for every element)
+  template <int ACT>
+  static __device__ __forceinline__ void run_a(const Params& p, uint3 bidx) {
     const int cv = p.C >> 3;
     const long long v0 = (long long)bidx.x * kVecPerBlock + threadIdx.x;
     uint4 xv[kIlp], rv[kIlp];
@@ -697,7 +700,7 @@ struct BnAct {
     for (int u = 0; u < kIlp; ++u) {
       const long long v = v0 + u * kThreads;
       if (v >= p.nvec) continue;
-      const int c = (int)(v % cv) << 3;
+      const int c = (int)((unsigned)v % (unsigned)cv) << 3;   // (nvec < 2^31, checked at bind: 32-bit modulo)
       float x[8];
       unpack8(xv[u], x);
       const float4 h0 = __ldg(reinterpret_cast<const float4*>(p.shift + c));
@@ -720,20 +723,28 @@ struct BnAct {
         for (int e = 0; e < 8; ++e) x[e] += r[e];
       }
       if (p.pre) st16(p.pre + v, pack8(x));
-      if (p.relu == 1) {
+      if constexpr (ACT == 1) {
 #pragma unroll
         for (int e = 0; e < 8; ++e) x[e] = fmaxf(x[e], 0.f);
-      } else if (p.relu == 2) {
+      } else if constexpr (ACT == 2) {
 #pragma unroll
         for (int e = 0; e < 8; ++e) {
           const float u = 0.7978845608028654f * (x[e] + 0.044715f * x[e] * x[e] * x[e]);
           x[e] = 0.5f * x[e] * (1.f + tanhf(u));
         }
-      } else if (p.relu == 3) {
+      } else if constexpr (ACT == 3) {
 #pragma unroll
-        for (int e = 0; e < 8; ++e) x[e] = gelu_erf(x[e]);
+        for (int e = 0; e < 8; e += 2) gelu_erf2(x[e], x[e + 1]);
       }
       st16(p.y + v, pack8(x));
+    }
+  }
+  static __device__ __forceinline__ void run(const Params& p, uint3 bidx, uint3, char*) {
+    switch (p.relu) {
+      case 1: run_a<1>(p, bidx); break;
+      case 2: run_a<2>(p, bidx); break;
+      case 3: run_a<3>(p, bidx); break;
+      default: run_a<0>(p, bidx); break;
     }
   }
 };
@@ -779,7 +790,7 @@ struct BnBwd {
     for (int u = 0; u < kV; ++u) {
       const long long v = v0 + u * kThreads;
       if (v >= p.nvec) continue;
-      const int c = (int)(v % cv) << 3;
+      const int c = (int)((unsigned)v % (unsigned)cv) << 3;   // (nvec < 2^31, checked at bind: 32-bit modulo)
       float dz[8], x[8];
       unpack8(gv[u], dz);
       if (p.g2) {
@@ -1529,6 +1540,7 @@ static int bind_bn_act(const tally_kernel_args* a, Instance* inst) {
     return TALLY_EINVAL;
   }
   p.nvec = P * (p.C / 8);
+  if (p.nvec >= (1ll << 31)) { set_error("bn_act: fewer than 2^31 vectors"); return TALLY_EINVAL; }
   finish(inst, p, (p.nvec + nn::kVecPerBlock - 1) / nn::kVecPerBlock, nn::BnAct::kThreads, 0,
          16.0 * p.nvec * (p.res ? 3 : 2));
   return TALLY_OK;
@@ -1553,6 +1565,7 @@ static int bind_bn_bwd(const tally_kernel_args* a, Instance* inst) {
     return TALLY_EINVAL;
   }
   p.nvec = P * (p.C / 8);
+  if (p.nvec >= (1ll << 31)) { set_error("bn_bwd: fewer than 2^31 vectors"); return TALLY_EINVAL; }
   const int streams = 3 + (p.g2 ? 1 : 0) + (p.y ? 1 : 0) + (p.dz_out ? 1 : 0);
   finish(inst, p, (p.nvec + nn::BnBwd::kBlockVec - 1) / nn::BnBwd::kBlockVec, nn::BnBwd::kThreads, 0,
          16.0 * p.nvec * streams);
