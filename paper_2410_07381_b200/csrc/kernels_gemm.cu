@@ -1430,7 +1430,10 @@ struct SplitTf32 {
 //                      row by row from TMEM, P (bf16) TMA-stored -- the fp32 score
 //                      matrix never reaches HBM (it was a GEMM output + a softmax pass);
 //   backward (MODE 1): dP = dO V^T in TMEM, dS = P * (dP - rowsum(P * dP)) * scale,
-//                      dS (bf16) TMA-stored (P read back per row).
+//                      dS (bf16) TMA-stored; P is TMA-loaded as a tile into the
+//                      freed operand buffers (+ 48 KB) once the MMA is done --
+//                      per-lane row loads (32 rows per warp instruction) were
+//                      70 % of the stall samples, 65 us per BERT-large launch.
 // Q / K / V / dO are head-D (= 64) column slices of row-major activations (the
 // fused QKV buffer), read by TMA; the Body runs under k_original / k_sliced /
 // k_ptb like every transformable kind.  8 warps: thread 0 issues the TMA loads
@@ -1441,11 +1444,14 @@ struct AttnSoftmax {
   static constexpr int kThreads = 256;
   static constexpr int kD = 64;                  // head dim = one 128 B swizzle atom of bf16
   static constexpr int kTileBytes = 128 * kD * 2;   // 16 KB: 128 rows x 64 bf16
-  static constexpr int kSmem = 1024 + kTileBytes * 5 + 8 * 4096 + 2 * 2 * 128 * 4 + 64;
+  // operands (A + up to 4 B boxes) | 8 x 4 KB staging | row exchange, barriers,
+  // TMEM slot (4 KB) | MODE 1: P boxes 5..7 (boxes 0..4 reuse the operands)
+  static constexpr int kSmem = 1024 + kTileBytes * 5 + 8 * 4096 + 4096 + (MODE == 1 ? 3 * kTileBytes : 0);
   struct Params {
     CUtensorMap a_map;     // MODE 0: Q; MODE 1: dO   (box 64 cols x 128 rows)
     CUtensorMap b_map;     // MODE 0: K; MODE 1: V    (box 64 cols x 128 rows)
     CUtensorMap out_map;   // P / dS [z * T + i, T] bf16 (box 64 cols x 32 rows)
+    CUtensorMap p_map;     // MODE 1: P [z * T + i, T] bf16 (box 64 cols x 128 rows)
     const __nv_bfloat16* p_in;   // MODE 1: P [z * T + i, T]
     long long a_col0, a_col_h, b_col0, b_col_h;   // operand column origin: col0 + h * col_h
     int T, H;
@@ -1455,7 +1461,7 @@ struct AttnSoftmax {
   static __device__ __forceinline__ uint32_t* tmem_slot(char* smem_raw) {
     unsigned char* sm = reinterpret_cast<unsigned char*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
     float* red = reinterpret_cast<float*>(sm + 5 * kTileBytes + 8 * 4096);
-    return reinterpret_cast<uint32_t*>(reinterpret_cast<uint64_t*>(red + 2 * 2 * 128) + 2);
+    return reinterpret_cast<uint32_t*>(reinterpret_cast<uint64_t*>(red + 2 * 2 * 128) + 3);
   }
   // TMEM once per CTA (all 512 columns), taken before the CTA lets a
   // programmatic dependent launch begin: a successor GEMM CTA waiting for this
@@ -1485,14 +1491,15 @@ struct AttnSoftmax {
     unsigned char* sb = sm + kTileBytes;             // B: T / 128 boxes of 128 keys
     unsigned char* stg = sm + 5 * kTileBytes;        // 8 x 4 KB output staging
     float* red = reinterpret_cast<float*>(stg + 8 * 4096);   // [2 halves][2 values][128 rows]
-    uint64_t* bar = reinterpret_cast<uint64_t*>(red + 2 * 2 * 128);   // [0] operands, [1] MMA done
-    uint32_t* tslot = reinterpret_cast<uint32_t*>(bar + 2);
+    uint64_t* bar = reinterpret_cast<uint64_t*>(red + 2 * 2 * 128);   // [0] operands, [1] MMA done, [2] P tile
+    uint32_t* tslot = reinterpret_cast<uint32_t*>(bar + 3);
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int z = (int)bidx.y, b = z / p.H, h = z - b * p.H, r0 = (int)bidx.x * 128;
     const int nkb = p.T / 128;
     if (threadIdx.x == 0) {
       mbar_init(&bar[0], 1);
       mbar_init(&bar[1], 1);
+      mbar_init(&bar[2], 1);
       asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     }
     __syncthreads();
@@ -1584,22 +1591,43 @@ struct AttnSoftmax {
         __syncwarp();
       }
     } else {
-      // dS = P * (dP - delta) * scale, delta = sum_j P dP (P read back per row)
-      const __nv_bfloat16* prow = p.p_in + grow * p.T + half * kcols;
+      // dS = P * (dP - delta) * scale, delta = sum_j P dP.  P's tile (128 rows
+      // x T) by TMA into the operand buffers the finished MMA no longer reads
+      // (boxes 0..4) and 48 KB more (5..7); lane = row, 128B-swizzled rows.
+      unsigned char* pext = stg + 8 * 4096 + 4096;
+      auto pbox = [&](int bx) -> uint32_t { return smem_u32(bx < 5 ? sm + bx * kTileBytes : pext + (bx - 5) * kTileBytes); };
+      if (threadIdx.x == 0) {
+        mbar_expect_tx(&bar[2], (uint32_t)(kTileBytes * nkb * 2));
+        for (int bx = 0; bx < 2 * nkb; ++bx)
+          tma_load_2d(bx < 5 ? (void*)(sm + bx * kTileBytes) : (void*)(pext + (bx - 5) * kTileBytes), &p.p_map, &bar[2],
+                      bx * 64, z * p.T + r0);
+      }
+      mbar_wait(&bar[2], 0);
+      const int rr = q * 32 + lane;
+      auto ldp = [&](uint4 (&pv)[8], int c) {   // this lane's row, columns [half * kcols + c, + 64)
+        const uint32_t rowb = pbox((half * kcols + c) >> 6) + rr * 128;
+#pragma unroll
+        for (int v = 0; v < 8; ++v)
+          asm volatile("ld.shared.v4.b32 {%0, %1, %2, %3}, [%4];"
+                       : "=r"(pv[v].x), "=r"(pv[v].y), "=r"(pv[v].z), "=r"(pv[v].w)
+                       : "r"(rowb + ((v ^ (rr & 7)) << 4)));
+      };
       float dot = 0.f;
-      for (int c = 0; c < kcols; c += 32) {
-        uint32_t r[32];
-        uint4 pv[4];
+      for (int c = 0; c < kcols; c += 64) {
+        uint32_t r[2][32];
+        uint4 pv[8];
+        ldp(pv, c);
+        tmem_ld32_nw(lb + c, r[0]);
+        tmem_ld32_nw(lb + c + 32, r[1]);
+        tmem_wait_ld();
 #pragma unroll
-        for (int v = 0; v < 4; ++v) pv[v] = __ldg(reinterpret_cast<const uint4*>(prow + c) + v);
-        tmem_ld32(lb + c, r);
-#pragma unroll
-        for (int v = 0; v < 4; ++v) {
+        for (int v = 0; v < 8; ++v) {
           const __nv_bfloat162* h2 = reinterpret_cast<const __nv_bfloat162*>(&pv[v]);
 #pragma unroll
           for (int e = 0; e < 4; ++e) {
+            const int k = 8 * (v & 3) + 2 * e;
             const float2 f = __bfloat1622float2(h2[e]);
-            dot += f.x * __uint_as_float(r[8 * v + 2 * e]) + f.y * __uint_as_float(r[8 * v + 2 * e + 1]);
+            dot += f.x * __uint_as_float(r[v >> 2][k]) + f.y * __uint_as_float(r[v >> 2][k + 1]);
           }
         }
       }
@@ -1607,17 +1635,16 @@ struct AttnSoftmax {
       asm volatile("bar.sync %0, 64;" ::"r"(1 + q) : "memory");
       dot += other[0];
       unsigned char* wst = stg + (size_t)warp * 4096;
+      const uint32_t wsts = smem_u32(wst);
       for (int c = 0; c < kcols; c += 64) {
         uint32_t r[2][32];
         uint4 pv[8];
-#pragma unroll
-        for (int v = 0; v < 8; ++v) pv[v] = __ldg(reinterpret_cast<const uint4*>(prow + c) + v);
+        ldp(pv, c);
         tmem_ld32_nw(lb + c, r[0]);
         tmem_ld32_nw(lb + c + 32, r[1]);
         tmem_wait_ld();
         if (lane == 0) asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
         __syncwarp();
-        unsigned char* srow = wst + (size_t)lane * 128;
 #pragma unroll
         for (int v = 0; v < 8; ++v) {
           const __nv_bfloat162* h2 = reinterpret_cast<const __nv_bfloat162*>(&pv[v]);
@@ -1630,11 +1657,13 @@ struct AttnSoftmax {
                                                       f.y * (__uint_as_float(r[v >> 2][k + 1]) - dot) * p.scale);
             wv[e] = *reinterpret_cast<uint32_t*>(&bb);
           }
-          *reinterpret_cast<uint4*>(srow + ((v ^ (lane & 7)) << 4)) = make_uint4(wv[0], wv[1], wv[2], wv[3]);
+          asm volatile("st.shared.v4.b32 [%0], {%1, %2, %3, %4};" ::"r"(wsts + lane * 128 + ((v ^ (lane & 7)) << 4)),
+                       "r"(wv[0]), "r"(wv[1]), "r"(wv[2]), "r"(wv[3])
+                       : "memory");
         }
         asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
         __syncwarp();
-        if (lane == 0) tma_store_2d(&p.out_map, smem_u32(wst), half * kcols + c, (int)(grow - lane));
+        if (lane == 0) tma_store_2d(&p.out_map, wsts, half * kcols + c, (int)(grow - lane));
         __syncwarp();
       }
     }
@@ -2078,6 +2107,7 @@ static int bind_attn_softmax(const tally_kernel_args* a, Instance* inst) {
   if ((rc = make_map(&p.b_map, a->ptr[1], CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, B * T, ldb, 128, ldb))) return rc;
   if ((rc = make_map(&p.out_map, a->ptr[2], CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, B * H * T, T, 32, T))) return rc;
   p.p_in = static_cast<const __nv_bfloat16*>(a->ptr[3]);
+  if (MODE == 1 && (rc = make_map(&p.p_map, a->ptr[3], CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, B * H * T, T, 128, T))) return rc;
   static_assert(sizeof(p) <= kMaxParamBytes, "params too large");
   memcpy(inst->params, &p, sizeof(p));
   inst->grid = make_uint3((unsigned)(T / 128), (unsigned)(B * H), 1);
