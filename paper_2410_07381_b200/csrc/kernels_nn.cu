@@ -1164,7 +1164,27 @@ struct SplitKReduce {
       for (int u = 0; u < 2; ++u)
 #pragma unroll
         for (int e = 0; e < 8; ++e) acc[u][e] = 0.f;
-      for (int sp = 0; sp < p.S; ++sp) {
+      // two partials' loads in flight per step (one DRAM round trip per two
+      // splits), still summed in split order
+      int sp = 0;
+      for (; sp + 1 < p.S; sp += 2) {
+        float4 t[2][2][2];
+#pragma unroll
+        for (int h = 0; h < 2; ++h)
+#pragma unroll
+          for (int u = 0; u < 2; ++u) {
+            const long long v = v0 + u * kThreads;
+            if (v < p.n8) {
+              t[h][u][0] = __ldcs(p.in + (sp + h) * p.stride4 + 2 * v);
+              t[h][u][1] = __ldcs(p.in + (sp + h) * p.stride4 + 2 * v + 1);
+            }
+          }
+#pragma unroll
+        for (int h = 0; h < 2; ++h)
+#pragma unroll
+          for (int u = 0; u < 2; ++u) add8(acc[u], t[h][u][0], t[h][u][1]);
+      }
+      if (sp < p.S) {
         float4 t[2][2];
 #pragma unroll
         for (int u = 0; u < 2; ++u) {
