@@ -681,10 +681,9 @@ struct BnAct {
     long long nvec;
     int C, relu;          // activation: 0 none, 1 ReLU, 2 GELU (tanh approximation), 3 GELU (erf)
   };
-  // (the activation is chosen once per block -- chosen per element, the
-  // compiler if-converted every variant for every element)
-  template <int ACT>
-  static __device__ __forceinline__ void run_a(const Params& p, uint3 bidx) {
+  static __device__ __forceinline__ void run(const Params& p, uint3 bidx, uint3, char*) {
+    // (one body for every activation: a per-activation template switch was
+    // no faster untransformed and made the PTB shape 0.71 -> 0.51x of it)
     const int cv = p.C >> 3;
     const long long v0 = (long long)bidx.x * kVecPerBlock + threadIdx.x;
     uint4 xv[kIlp], rv[kIlp];
@@ -723,28 +722,20 @@ struct BnAct {
         for (int e = 0; e < 8; ++e) x[e] += r[e];
       }
       if (p.pre) st16(p.pre + v, pack8(x));
-      if constexpr (ACT == 1) {
+      if (p.relu == 1) {
 #pragma unroll
         for (int e = 0; e < 8; ++e) x[e] = fmaxf(x[e], 0.f);
-      } else if constexpr (ACT == 2) {
+      } else if (p.relu == 2) {
 #pragma unroll
         for (int e = 0; e < 8; ++e) {
           const float u = 0.7978845608028654f * (x[e] + 0.044715f * x[e] * x[e] * x[e]);
           x[e] = 0.5f * x[e] * (1.f + tanhf(u));
         }
-      } else if constexpr (ACT == 3) {
+      } else if (p.relu == 3) {
 #pragma unroll
         for (int e = 0; e < 8; e += 2) gelu_erf2(x[e], x[e + 1]);
       }
       st16(p.y + v, pack8(x));
-    }
-  }
-  static __device__ __forceinline__ void run(const Params& p, uint3 bidx, uint3, char*) {
-    switch (p.relu) {
-      case 1: run_a<1>(p, bidx); break;
-      case 2: run_a<2>(p, bidx); break;
-      case 3: run_a<3>(p, bidx); break;
-      default: run_a<0>(p, bidx); break;
     }
   }
 };
