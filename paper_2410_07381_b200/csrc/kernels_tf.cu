@@ -196,7 +196,8 @@ __device__ __forceinline__ float gelu_erf_grad(float x) {   // BERT "gelu": x * 
   return gelu_erf_grad_fast(x);   // (epilogue.cuh)
 }
 
-struct GeluBwd {
+template <int ERF_KIND>   // 0: "gelu_bwd" (tanh approximation), 1: "gelu_bwd_erf" (exact erf)
+struct GeluBwdT {
   static constexpr int kThreads = 256;
   static constexpr int kMinBlocks = 4;   // (PTB at 83 registers fitted 2 CTAs per SM: 0.7x of untransformed)
   static constexpr int kVec = 4;   // (8 measured slower untransformed: 33 -> 48 us per BERT-large launch)
@@ -241,11 +242,14 @@ struct GeluBwd {
       p.dx[v] = pack8(g);
     }
   }
+  // (one variant per kind: both in one kernel made its PTB shape 0.68 ->
+  // 0.53x of untransformed)
   static __device__ __forceinline__ void run(const Params& p, uint3 bidx, uint3, char*) {
-    if (p.erf) run_v<true>(p, bidx);
-    else run_v<false>(p, bidx);
+    run_v<ERF_KIND != 0>(p, bidx);
   }
 };
+using GeluBwd = GeluBwdT<0>;
+using GeluBwdErf = GeluBwdT<1>;
 
 // ---------------------------------------------------------------- causal softmax
 // One HBM pass per row: each lane holds its float4s of the row in registers
@@ -522,9 +526,12 @@ static int bind_ln_bwd(const tally_kernel_args* a, Instance* inst) {
   return TALLY_OK;
 }
 
-// ptr: g, pre, dx.  i: n (elements), erf
+// ptr: g, pre, dx.  i: n (elements), erf (must match the kind: gelu_bwd /
+// gelu_bwd_erf)
+template <int ERF>
 static int bind_gelu_bwd(const tally_kernel_args* a, Instance* inst) {
   tf::GeluBwd::Params p{};
+  if ((a->i[1] ? 1 : 0) != ERF) { set_error("gelu_bwd: the exact-erf variant is the gelu_bwd_erf kind"); return TALLY_EINVAL; }
   p.g = static_cast<const uint4*>(a->ptr[0]);
   p.pre = static_cast<const uint4*>(a->ptr[1]);
   p.dx = static_cast<uint4*>(a->ptr[2]);
@@ -620,11 +627,12 @@ static KernelKind tf_kind(const char* name, int (*bind)(const tally_kernel_args*
 }
 
 int register_tf_kernels(KernelKind* out, int cap) {
-  if (cap < 7) return 0;
+  if (cap < 8) return 0;
   int n = 0;
   out[n++] = tf_kind<tf::LayerNormFwd>("layernorm_fwd", bind_ln_fwd);
   out[n++] = tf_kind<tf::LayerNormBwd>("layernorm_bwd", bind_ln_bwd);
-  out[n++] = tf_kind<tf::GeluBwd>("gelu_bwd", bind_gelu_bwd);
+  out[n++] = tf_kind<tf::GeluBwd>("gelu_bwd", bind_gelu_bwd<0>);
+  out[n++] = tf_kind<tf::GeluBwdErf>("gelu_bwd_erf", bind_gelu_bwd<1>);
   out[n++] = tf_kind<tf::SoftmaxCausal>("softmax_causal", bind_softmax_causal);
   out[n++] = tf_kind<tf::SoftmaxCausalBwd>("softmax_causal_bwd", bind_softmax_causal_bwd);
   out[n++] = tf_kind<tf::EmbeddingFwd>("embedding_fwd", bind_embedding_fwd);

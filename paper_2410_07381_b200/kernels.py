@@ -675,7 +675,7 @@ def layernorm_bwd(dy, x, gamma, mean, rstd, dx, g2=None) -> DeviceKernel:
 
 def gelu_bwd(g, pre, dx, erf=False) -> DeviceKernel:
     """dx = g * GELU'(pre): tanh approximation (GPT-2) or exact erf (BERT)."""
-    return DeviceKernel("gelu_bwd", (g, pre, dx), (g.numel(), int(erf)))
+    return DeviceKernel("gelu_bwd_erf" if erf else "gelu_bwd", (g, pre, dx), (g.numel(), int(erf)))
 
 
 def softmax_causal(s, p, T, scale, causal=True) -> DeviceKernel:
