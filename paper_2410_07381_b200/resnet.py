@@ -57,6 +57,15 @@ def _rb(P, C, streams=1):
     return max(32, min(base, P * cblocks // 296 // 8 * 8))
 
 
+def _FOLD_RB(C):
+    """bn_fold rows per block: one load pass per block (the fold body covers
+    256 / (min(C, 256) / 8) rows x 2 per pass: 64 rows at C = 64, 16 from 256)."""
+    mode = os.environ.get("TALLY_BNFOLD_RB", "pass")   # experiment knob: "pass" or a fixed count
+    if mode != "pass":
+        return int(mode)
+    return max(16, 64 * 64 // min(C, 256))
+
+
 def _gemm_splits(M, N, Kdim):
     """Split-K factor for a GEMM: enough logical blocks of <= ~40 MFLOP each
     (~10-20 us on one SM, the preemption granularity) that the tuner finds a
@@ -401,8 +410,9 @@ class ResNet50Train:
         if bno is None:
             return
         R = K.BnStatsOut.gemm_rows(P, bno.c.rb)
-        fpart = self._scr("bnfold", K.BnStatsOut.part_floats(R, bn.C, 64), self.torch.float32)
-        fo = K.BnStatsOut(fpart, bn.gamma, bn.beta, bn.mean, bn.invstd, bn.scale_shift, BN_EPS, 64)
+        rb = _FOLD_RB(bn.C)
+        fpart = self._scr("bnfold", K.BnStatsOut.part_floats(R, bn.C, rb), self.torch.float32)
+        fo = K.BnStatsOut(fpart, bn.gamma, bn.beta, bn.mean, bn.invstd, bn.scale_shift, BN_EPS, rb)
         self._add(name, K.bn_fold(bno.tensors[0], R, bn.C, P, fo))
 
     def _reduce(self, name, ws, out, bn, P):
@@ -526,7 +536,8 @@ class ResNet50Train:
         self._reserve("splitk", max(splitk, 8), torch.float32)
         self._reserve("part", part, torch.float32)
         self._reserve("bnfold", max(K.BnStatsOut.part_floats(K.BnStatsOut.gemm_rows(self.B * c.spec.oh * c.spec.ow, 32),
-                                                             c.spec.cout, 64) for c in convs), torch.float32)
+                                                             c.spec.cout, min(16, _FOLD_RB(c.spec.cout)))
+                                    for c in convs), torch.float32)
         self._reserve("dcol", dcol, torch.bfloat16)
 
     # ---- the step ----------------------------------------------------------------
